@@ -1,0 +1,193 @@
+/*
+ * harmony_b200.h -- C ABI of libharmony_b200.so, the B200-native runtime of
+ * Harmony's swap-aware layer-pack training (arXiv 2202.01306).
+ *
+ * The reference (`wrapsched`, pure Python) has no FFI; its boundary is three
+ * Python calls.  Each entry point below names the reference interface it
+ * replaces (paths relative to /root/reference/pkg/src/wrapsched/):
+ *
+ *   hm_plan_*      <- simulator._build_items / simulator._run / simulate
+ *                     (simulator.py:150-336, 347-375, 378-434): the swap plan,
+ *                     the per-task swap-byte ledger and the event-driven
+ *                     estimate, built from the lowered task graph of
+ *                     taskgraph.generate_task_graph (taskgraph.py:211-236).
+ *   hm_runtime_*   <- no reference code: the runtime the paper describes in
+ *                     PAPER.md:572-586 and the reference only models.  Its
+ *                     ledger equals hm_plan's by construction (it executes it).
+ *   hm_k_*         <- no reference code: the sm_100a kernels of F/B/U tasks,
+ *                     exported individually so they are testable alone.
+ *
+ * Conventions: plain C types only, sizes in bytes (int64), times in ns.
+ * Every function returns an int status (HM_OK = 0, negative = error) unless
+ * documented otherwise; the message of the last error on the calling thread
+ * is available from hm_last_error().  Status codes map onto the reference's
+ * exception classes (errors.py:4-73) in paper_2202_01306_b200/errors.py.
+ */
+#ifndef HARMONY_B200_H
+#define HARMONY_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define HM_OK 0
+#define HM_ERR_VALIDATION (-1)      /* ValidationError                       */
+#define HM_ERR_CAPACITY (-2)        /* CapacityViolationError (alpha)        */
+#define HM_ERR_DEADLOCK (-3)        /* DeadlockError                         */
+#define HM_ERR_DEVICE (-4)          /* CUDA / NCCL failure (WrapschedError)  */
+#define HM_ERR_MISSING_PROFILE (-5) /* MissingProfileError                   */
+#define HM_ERR_INTERNAL (-6)        /* invariant violation                   */
+#define HM_ERR_PROFILE_RANGE (-7)   /* ProfileRangeError                     */
+
+/* ---- enums shared with the Python lowering (taskgraph.py:61-71, core.py:44-54) */
+enum hm_tensor { HM_X = 0, HM_Y = 1, HM_DX = 2, HM_DY = 3, HM_W = 4, HM_DW = 5, HM_K = 6, HM_SX = 7 };
+enum hm_channel { HM_CPU_GPU_SWAP = 0, HM_PEER2PEER = 1, HM_MESSAGE_PASSING = 2, HM_SHARED_MEMORY = 3 };
+enum hm_task_type { HM_TASK_F = 0, HM_TASK_B = 1, HM_TASK_U = 2 };
+enum hm_device_kind { HM_DEV_GPU = 0, HM_DEV_CPU = 1 };
+/* Resources of the estimator (simulator.py:3-10): id = kind * gpu_count + gpu,
+ * the two host root links use gpu = 0. */
+enum hm_resource_kind {
+  HM_RES_COMPUTE = 0, HM_RES_SWAP_IN = 1, HM_RES_SWAP_OUT = 2, HM_RES_P2P_IN = 3,
+  HM_RES_P2P_OUT = 4, HM_RES_UPDATE = 5, HM_RES_ROOT_OUT = 6, HM_RES_ROOT_IN = 7
+};
+
+/* ---- lowered task graph (one flat table; taskgraph.py:91-106) ------------ */
+typedef struct {
+  int32_t tensor;    /* hm_tensor                                          */
+  int32_t layer;     /* dict key of Task.inputs/outputs[tensor]            */
+  int32_t channel;   /* hm_channel                                         */
+  int32_t peer_task; /* Channel.src_task (inputs) / dst_task (outputs), -1  */
+  int32_t src_layer; /* Channel.src_layer (relay payload), -1 if none       */
+} hm_entry;
+
+typedef struct {
+  int32_t index, type, lo, hi, dev_kind, dev_id, recompute;
+  int32_t group_off, group_len; /* slice of the groups[] array            */
+  int32_t in_off, in_len;       /* slice of entries[], insertion order     */
+  int32_t out_off, out_len;
+} hm_task;
+
+typedef struct {
+  int32_t gpu_count;
+  int32_t cpu_offload_update;
+  int64_t pcie_bandwidth;      /* bytes/s per direction per GPU link     */
+  int64_t root_link_bandwidth; /* shared host uplink                     */
+  int64_t p2p_bandwidth;       /* 0 = pcie_bandwidth (reference model)   */
+  int64_t update_cpu_rate;
+  const int32_t *p2p_group_of; /* [gpu_count] switch-group id per GPU    */
+} hm_machine;
+
+/* Integer profile tables, row-major [layer][u] with u = 0..u_top (u = 0 is
+ * unused).  -1 = no model (MissingProfileError if touched), -2 = above the
+ * fitted u_max (ProfileRangeError if touched).  t_u is indexed [layer][1]. */
+typedef struct {
+  int32_t layers, u_top;
+  const int64_t *x, *y;      /* [layers*(u_top+1)] */
+  const int64_t *w, *dw, *k; /* [layers]           */
+  const int64_t *t_f, *t_b, *t_u; /* [layers*(u_top+1)] or NULL if no times */
+} hm_profile;
+
+/* One work item of the plan (simulator.py:86-108 `_Item`, extended with the
+ * addressing fields the runtime needs: layer, peer task, peer member). */
+typedef struct {
+  int32_t task, stage, member, seq; /* key (task, stage 0 in/1 compute/2 out, member, seq) */
+  int32_t is_compute;
+  int32_t tensor, channel;          /* -1 for compute items                 */
+  int32_t gpu;                      /* device index of the owning task      */
+  int32_t layer;                    /* stash/p2p layer key, -1 otherwise    */
+  int32_t peer_task, peer_member;   /* producer (inputs) or consumer (MP out) */
+  int32_t n_res, res[4];            /* resource ids (hm_resource_kind*N+gpu) */
+  int64_t nbytes;
+  int64_t duration_ns;
+  int64_t start_ns, end_ns;         /* filled by hm_plan_simulate           */
+} hm_item;
+
+typedef struct hm_plan hm_plan;
+
+/* Build the swap plan of a lowered graph (restates simulator._build_items). */
+hm_plan *hm_plan_build(const hm_task *tasks, int32_t n_tasks, const int32_t *groups,
+                       const hm_entry *entries, const hm_machine *machine,
+                       const hm_profile *profile, int32_t *status);
+/* Run the FIFO event loop (simulator._run); returns status, fills start/end. */
+int hm_plan_simulate(hm_plan *plan, int64_t *makespan_ns);
+int32_t hm_plan_item_count(const hm_plan *plan);
+int hm_plan_items(const hm_plan *plan, hm_item *out, int32_t cap);
+/* Dependency edges (dep item -> item; at_start = dep's start gates item). */
+int32_t hm_plan_edge_count(const hm_plan *plan);
+int hm_plan_edges(const hm_plan *plan, int32_t *dep, int32_t *item, int32_t *at_start, int32_t cap);
+void hm_plan_free(hm_plan *plan);
+
+const char *hm_last_error(void);
+const char *hm_version(void);
+
+/* ---- runtime -------------------------------------------
+ * One runtime per process and GPU (torchrun launches one process per GPU).
+ * It owns: pinned host arenas (W, K, stash), one device pool capped at alpha,
+ * the streams compute / swap_in / swap_out / p2p_in / p2p_out / update, and
+ * the sm_100a kernels.  hm_runtime_run_iteration executes every item of the
+ * loaded plan that belongs to this rank's GPU and records the ledger. */
+typedef struct {
+  int32_t n_layer;    /* R: chain layers (embedding fused into 0, head into R-1) */
+  int32_t d_model, n_head, seq_len, vocab, vocab_padded;
+  int32_t causal;     /* 1 = GPT, 0 = BERT-style full attention             */
+  int32_t math_mode;  /* 0 = bf16 operands / fp32 accumulate               */
+  float lr, beta1, beta2, eps;
+} hm_model;
+
+typedef struct hm_runtime hm_runtime;
+
+enum hm_arena { HM_ARENA_W = 0, HM_ARENA_K = 1, HM_ARENA_STASH = 2 };
+
+hm_runtime *hm_runtime_create(int32_t device, const hm_model *model, int64_t alpha_bytes,
+                              int32_t *status);
+/* Pinned host arena owned by the runtime; returns its host pointer. */
+void *hm_runtime_arena(hm_runtime *rt, int32_t kind, int64_t *bytes);
+/* Per-layer parameter offsets (in floats) of the W arena; K uses 2x. */
+int hm_runtime_layer_offsets(const hm_runtime *rt, int64_t *w_off, int32_t cap);
+int hm_runtime_load_plan(hm_runtime *rt, hm_plan *plan, int32_t rank, int32_t minibatch);
+/* tokens/labels: [minibatch, seq_len] int32, host (pinned or pageable) or
+ * device pointers (is_device = 1).  loss_out: mean token cross-entropy. */
+int hm_runtime_run_iteration(hm_runtime *rt, const int32_t *tokens, const int32_t *labels,
+                             int32_t is_device, double *loss_out);
+int32_t hm_runtime_ledger_count(const hm_runtime *rt);
+/* Executed transfer rows of the last iteration, in execution order; the
+ * start/end fields hold measured CUDA-event times relative to iteration start. */
+int hm_runtime_ledger(const hm_runtime *rt, hm_item *out, int32_t cap);
+/* Measured compute items (same hm_item layout) of the last iteration. */
+int32_t hm_runtime_trace_count(const hm_runtime *rt);
+int hm_runtime_trace(const hm_runtime *rt, hm_item *out, int32_t cap);
+/* Counters of the last iteration: [0] kernels launched, [1] iteration ns,
+ * [2] device bytes in use (peak), [3] H2D bytes, [4] D2H bytes, [5] P2P bytes. */
+int hm_runtime_counters(const hm_runtime *rt, int64_t *out, int32_t cap);
+void hm_runtime_free(hm_runtime *rt);
+
+/* ---- kernels, testable alone (raw device pointers, a cudaStream_t) -------- */
+/* Fused Adam over one pack: W, m, v updated in place from g; K holds (m, v)
+ * interleaved per parameter.  step >= 1.  Reads 16 B/param, writes 12 B/param. */
+int hm_k_adam(float *w, const float *g, float *k, int64_t n, float lr, float beta1,
+              float beta2, float eps, int32_t step, float grad_scale, void *stream);
+/* C[M,N] (+)= A . B^T with bf16 operands, fp32 accumulate (tcgen05 + TMEM + TMA).
+ * a_major/b_major: 0 = K-major (reduction dim contiguous), 1 = MN-major.
+ * epilogue: see hm_gemm_epilogue. */
+enum hm_gemm_epilogue {
+  HM_EPI_STORE_BF16 = 0,      /* D = acc (+bias) -> bf16                     */
+  HM_EPI_STORE_F32 = 1,       /* D = acc (+bias) -> fp32                     */
+  HM_EPI_ACC_F32 = 2,         /* D += acc (fp32 read-modify-write)           */
+  HM_EPI_RESID_F32 = 3,       /* D = R + acc + bias -> fp32 (R may alias D)  */
+  HM_EPI_GELU_BF16 = 4,       /* P = acc + bias (bf16), D = gelu(P) (bf16)   */
+  HM_EPI_DGELU_BF16 = 5       /* D = acc * gelu'(P) -> bf16                  */
+};
+int hm_k_gemm(const void *a, const void *b, void *d, int64_t m, int64_t n, int64_t k,
+              int64_t lda, int64_t ldb, int64_t ldd, int32_t a_major, int32_t b_major,
+              int32_t epilogue, const float *bias, const void *aux, int64_t ld_aux,
+              int32_t batch, int64_t stride_a, int64_t stride_b, int64_t stride_d,
+              void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HARMONY_B200_H */

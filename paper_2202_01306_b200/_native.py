@@ -1,0 +1,131 @@
+"""ctypes binding of libharmony_b200.so (declared in include/harmony_b200.h).
+
+The library is built in-tree by ``__graft_entry__.build()`` /
+``python -m paper_2202_01306_b200.build``.  There is no fallback: if the
+library is missing every entry point raises, so nothing silently runs on the
+CPU instead of the native runtime.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from .errors import WrapschedError, raise_for_status
+
+LIB_NAME = "libharmony_b200.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+
+class hm_entry(C.Structure):
+    _fields_ = [("tensor", C.c_int32), ("layer", C.c_int32), ("channel", C.c_int32),
+                ("peer_task", C.c_int32), ("src_layer", C.c_int32)]
+
+
+class hm_task(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in (
+        "index", "type", "lo", "hi", "dev_kind", "dev_id", "recompute",
+        "group_off", "group_len", "in_off", "in_len", "out_off", "out_len")]
+
+
+class hm_machine(C.Structure):
+    _fields_ = [("gpu_count", C.c_int32), ("cpu_offload_update", C.c_int32),
+                ("pcie_bandwidth", C.c_int64), ("root_link_bandwidth", C.c_int64),
+                ("p2p_bandwidth", C.c_int64), ("update_cpu_rate", C.c_int64),
+                ("p2p_group_of", C.POINTER(C.c_int32))]
+
+
+class hm_profile(C.Structure):
+    _fields_ = [("layers", C.c_int32), ("u_top", C.c_int32)] + [
+        (n, C.POINTER(C.c_int64)) for n in ("x", "y", "w", "dw", "k", "t_f", "t_b", "t_u")]
+
+
+ITEM_DTYPE = np.dtype([
+    ("task", np.int32), ("stage", np.int32), ("member", np.int32), ("seq", np.int32),
+    ("is_compute", np.int32), ("tensor", np.int32), ("channel", np.int32), ("gpu", np.int32),
+    ("layer", np.int32), ("peer_task", np.int32), ("peer_member", np.int32), ("n_res", np.int32),
+    ("res", np.int32, (4,)), ("nbytes", np.int64), ("duration_ns", np.int64),
+    ("start_ns", np.int64), ("end_ns", np.int64)])
+
+
+class hm_model(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in (
+        "n_layer", "d_model", "n_head", "seq_len", "vocab", "vocab_padded", "causal",
+        "math_mode")] + [(n, C.c_float) for n in ("lr", "beta1", "beta2", "eps")]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load the native library once; raise if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise WrapschedError(
+            f"{LIB_NAME} is not built (expected at {LIB_PATH}); run "
+            "`python -c 'import __graft_entry__ as g; g.build()'` -- there is no CPU fallback")
+    L = C.CDLL(LIB_PATH)
+    P = C.POINTER
+    sig = {
+        "hm_last_error": (C.c_char_p, []),
+        "hm_version": (C.c_char_p, []),
+        "hm_plan_build": (C.c_void_p, [P(hm_task), C.c_int32, P(C.c_int32), P(hm_entry),
+                                       P(hm_machine), P(hm_profile), P(C.c_int32)]),
+        "hm_plan_simulate": (C.c_int, [C.c_void_p, P(C.c_int64)]),
+        "hm_plan_item_count": (C.c_int32, [C.c_void_p]),
+        "hm_plan_items": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
+        "hm_plan_edge_count": (C.c_int32, [C.c_void_p]),
+        "hm_plan_edges": (C.c_int, [C.c_void_p, P(C.c_int32), P(C.c_int32), P(C.c_int32), C.c_int32]),
+        "hm_plan_free": (None, [C.c_void_p]),
+        "hm_runtime_create": (C.c_void_p, [C.c_int32, P(hm_model), C.c_int64, P(C.c_int32)]),
+        "hm_runtime_arena": (C.c_void_p, [C.c_void_p, C.c_int32, P(C.c_int64)]),
+        "hm_runtime_layer_offsets": (C.c_int, [C.c_void_p, P(C.c_int64), C.c_int32]),
+        "hm_runtime_load_plan": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32]),
+        "hm_runtime_run_iteration": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                                               P(C.c_double)]),
+        "hm_runtime_ledger_count": (C.c_int32, [C.c_void_p]),
+        "hm_runtime_ledger": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
+        "hm_runtime_trace_count": (C.c_int32, [C.c_void_p]),
+        "hm_runtime_trace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
+        "hm_runtime_counters": (C.c_int, [C.c_void_p, P(C.c_int64), C.c_int32]),
+        "hm_runtime_free": (None, [C.c_void_p]),
+        "hm_k_adam": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_float,
+                                C.c_float, C.c_float, C.c_float, C.c_int32, C.c_float, C.c_void_p]),
+        "hm_k_gemm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
+                                C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+                                C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int64, C.c_int64,
+                                C.c_int64, C.c_void_p]),
+    }
+    for name, (res, args) in sig.items():
+        try:
+            fn = getattr(L, name)
+        except AttributeError:
+            continue  # reported by tests/test_native_abi.py
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def exported_symbols() -> list[str]:
+    """Names the header declares (parsed from include/harmony_b200.h)."""
+    import re
+    here = os.path.dirname(os.path.abspath(__file__))
+    hdr = os.path.join(os.path.dirname(here), "include", "harmony_b200.h")
+    text = open(hdr).read()
+    return sorted(set(re.findall(r"\b(hm_[a-z0-9_]+)\s*\(", text)))
+
+
+def last_error() -> str:
+    msg = lib().hm_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(code: int) -> int:
+    if code < 0:
+        raise_for_status(code, last_error())
+    return code

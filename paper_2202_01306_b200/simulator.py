@@ -1,0 +1,166 @@
+"""``simulate``: the event-driven estimate of one iteration and its exact
+swap ledger, computed by the native planner (csrc/plan.cpp).
+
+Drop-in for `pkg/src/wrapsched/simulator.py:378-434`: same signature, same
+``SimReport`` fields and byte accounting.  The plan that prices the
+iteration here is the plan :func:`paper_2202_01306_b200.runtime.execute`
+runs on the GPU, so estimate and execution share one ledger.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+from .core import MachineModel, TensorKind
+from .errors import ValidationError
+from .lowering import CHANNEL_OF, TENSOR_OF, NativePlan, ledger_rows, resource_name
+from .profiler import ProfileSet
+from .taskgraph import ChannelKind, Task, TaskGraph, TaskType
+
+
+@dataclass(frozen=True)
+class TraceEvent:
+    resource: str
+    task: int
+    kind: str
+    label: str
+    start_ns: int
+    end_ns: int
+
+
+@dataclass
+class SimReport:
+    makespan_ns: int
+    gpu_busy_ns: dict[int, int]
+    gpu_idle_ns: dict[int, int]
+    channel_volumes: dict[str, int]
+    tensor_volumes: dict[str, dict[str, int]]
+    per_gpu_volumes: dict[int, dict[str, int]]
+    trace: list[TraceEvent]
+    caveats: tuple[str, ...] = ()
+    ledger: list[tuple] = field(default_factory=list)
+    measured: bool = False
+
+    @property
+    def per_gpu_swap_bytes(self) -> dict[int, int]:
+        sw = (ChannelKind.CPU_GPU_SWAP.value, ChannelKind.MESSAGE_PASSING.value)
+        return {g: sum(v.get(c, 0) for c in sw) for g, v in self.per_gpu_volumes.items()}
+
+    def tensor_total(self, tensor: TensorKind, channels: tuple[str, ...]) -> int:
+        per = self.tensor_volumes.get(tensor.value, {})
+        return sum(per.get(c, 0) for c in channels)
+
+    def swap_volume(self, tensor: TensorKind) -> int:
+        return self.tensor_total(tensor, (ChannelKind.CPU_GPU_SWAP.value,
+                                          ChannelKind.MESSAGE_PASSING.value))
+
+
+def _label(task: Task, it) -> tuple[str, str]:
+    if it["is_compute"]:
+        lo, hi = task.pack
+        return "compute", f"{task.type.value} L{lo}-{hi} mb{int(it['member'])}"
+    tensor = TENSOR_OF[int(it["tensor"])].value
+    ch = CHANNEL_OF[int(it["channel"])]
+    if ch is ChannelKind.PEER2PEER:
+        return tensor, f"{tensor} p2p"
+    return tensor, f"{tensor} {'in' if int(it['stage']) == 0 else 'out'}"
+
+
+def report_from_items(graph: TaskGraph, machine: MachineModel, items, makespan: int,
+                      measured: bool = False) -> SimReport:
+    """Aggregate plan (or measured) items into a SimReport
+    (`simulator.py:399-434`)."""
+    n = machine.gpu_count
+    busy = {g: 0 for g in range(n)}
+    channel_volumes = {k.value: 0 for k in ChannelKind}
+    tensor_volumes: dict[str, dict[str, int]] = {}
+    per_gpu: dict[int, dict[str, int]] = {g: {} for g in range(n)}
+    trace = []
+    for it in items:
+        task = graph.tasks[int(it["task"])]
+        kind, label = _label(task, it)
+        res0 = resource_name(int(it["res"][0]), n)
+        trace.append(TraceEvent(res0, int(it["task"]), kind, label, int(it["start_ns"]),
+                                int(it["end_ns"])))
+        if it["is_compute"]:
+            if res0.startswith("gpu"):
+                busy[int(it["gpu"])] += int(it["end_ns"] - it["start_ns"]) if measured else int(it["duration_ns"])
+            continue
+        ch = CHANNEL_OF[int(it["channel"])].value
+        tn = TENSOR_OF[int(it["tensor"])].value
+        nb = int(it["nbytes"])
+        channel_volumes[ch] += nb
+        tensor_volumes.setdefault(tn, {}).setdefault(ch, 0)
+        tensor_volumes[tn][ch] += nb
+        bucket = per_gpu[int(it["gpu"])]
+        bucket[ch] = bucket.get(ch, 0) + nb
+    trace.sort(key=lambda e: (e.start_ns, e.resource, e.task, e.end_ns))
+    caveats = []
+    if graph.mode.value == "dp":
+        if measured:
+            caveats.append("data-parallel gradient all-reduce runs on NCCL and is reported "
+                           "separately; the ledger counts only CPU-GPU and peer traffic")
+        else:
+            caveats.append("data-parallel gradient synchronization is modeled as a zero-cost "
+                           "CPU-side reduction; only CPU-GPU swap traffic is accounted")
+    return SimReport(makespan_ns=int(makespan), gpu_busy_ns=busy,
+                     gpu_idle_ns={g: int(makespan) - b for g, b in busy.items()},
+                     channel_volumes=channel_volumes, tensor_volumes=tensor_volumes,
+                     per_gpu_volumes=per_gpu, trace=trace, caveats=tuple(caveats),
+                     ledger=ledger_rows(items, n), measured=measured)
+
+
+def simulate(graph: TaskGraph, machine: MachineModel | None = None,
+             profiles: ProfileSet | None = None, *, check_memory: bool = False) -> SimReport:
+    """Estimate one training iteration (drop-in for `simulator.simulate`)."""
+    machine = machine or graph.machine
+    if profiles is None:
+        raise ValidationError("profiles are required")
+    if machine.gpu_count != graph.machine.gpu_count:
+        raise ValidationError("machine does not match the graph's GPU count")
+    graph.validate()
+    plan = NativePlan(graph, machine, profiles)
+    try:
+        if check_memory:
+            check_memory_fit(graph, machine, profiles)
+        makespan = plan.simulate()
+        items = plan.items()
+    finally:
+        plan.close()
+    return report_from_items(graph, machine, items, makespan)
+
+
+def estimate_makespan(graph: TaskGraph, machine: MachineModel, profiles: ProfileSet) -> int:
+    """Makespan only (the search's inner loop): no trace or report assembly."""
+    plan = NativePlan(graph, machine, profiles)
+    try:
+        return plan.simulate()
+    finally:
+        plan.close()
+
+
+def task_mem_bytes(task: Task, profiles: ProfileSet) -> int:
+    if task.type is TaskType.U:
+        return 0
+    u = max(task.group)
+    lo, hi = task.pack
+    mem = profiles.pack_mem_bytes(task.type.value, lo, hi, u)
+    if task.type is TaskType.F:
+        mem += profiles.x_bytes(lo, u)
+    return mem
+
+
+def check_memory_fit(graph: TaskGraph, machine: MachineModel, profiles: ProfileSet) -> None:
+    """Resident task plus one prefetched task must fit alpha
+    (`simulator.py:437-463`)."""
+    per_dev: dict[tuple[str, int], list[Task]] = {}
+    for t in graph.tasks:
+        if t.device[0] == "gpu":
+            per_dev.setdefault(t.device, []).append(t)
+    for dev, ts in per_dev.items():
+        for a, b in zip(ts, ts[1:]):
+            need = task_mem_bytes(a, profiles) + task_mem_bytes(b, profiles)
+            if need > machine.gpu_mem_capacity:
+                raise ValidationError(
+                    f"tasks {a.index} and {b.index} overflow gpu{dev[1]} memory "
+                    f"({need} > {machine.gpu_mem_capacity}) with prefetch")
