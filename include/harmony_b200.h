@@ -123,6 +123,8 @@ void hm_plan_free(hm_plan *plan);
 
 const char *hm_last_error(void);
 const char *hm_version(void);
+/* Kernels launched by this library so far (all streams, all threads). */
+int64_t hm_launch_count(void);
 
 /* ---- runtime -------------------------------------------
  * One runtime per process and GPU (torchrun launches one process per GPU).
@@ -186,6 +188,41 @@ int hm_k_gemm(const void *a, const void *b, void *d, int64_t m, int64_t n, int64
               int32_t epilogue, const float *bias, const void *aux, int64_t ld_aux,
               int32_t batch, int64_t stride_a, int64_t stride_b, int64_t stride_d,
               void *stream);
+
+/* Fused attention over qkv [batch*seq, 3*heads*head_dim] bf16 (q|k|v thirds).
+ * out [batch*seq, heads*head_dim] bf16; lse [batch*seq, heads] fp32 (log2).
+ * head_dim 64 or 128; seq multiple of 64; causal 1 = GPT mask. */
+int hm_k_attn_fwd(const void *qkv, void *out, float *lse, int32_t batch, int32_t seq, int32_t heads,
+                  int32_t head_dim, int32_t causal, void *stream);
+/* Backward: writes dq|dk|dv into dqkv (same layout as qkv).  Scratch:
+ * dvec [batch*seq*heads] fp32, dq_acc [batch*seq, heads*head_dim] fp32. */
+int hm_k_attn_bwd(const void *qkv, const void *out, const void *dout, const float *lse, float *dvec,
+                  float *dq_acc, void *dqkv, int32_t batch, int32_t seq, int32_t heads, int32_t head_dim,
+                  int32_t causal, void *stream);
+/* fp32 -> bf16 cast of n elements. */
+int hm_k_cast_bf16(const float *src, void *dst, int64_t n, void *stream);
+/* Token + position embedding: out[b*seq+p] = wte[tokens[b*seq+p]] + wpe[p] (fp32). */
+int hm_k_embed_fwd(const int32_t *tokens, const float *wte, const float *wpe, float *out, int32_t batch,
+                   int32_t seq, int32_t d, void *stream);
+/* dwte[tokens[r]] += dx[r]; dwpe[p] += sum_b dx[b*seq+p]. */
+int hm_k_embed_bwd(const int32_t *tokens, const float *dx, float *dwte, float *dwpe, int32_t batch,
+                   int32_t seq, int32_t d, void *stream);
+/* y = bf16(LN(x) * g + b), eps 1e-5; mean/rstd [rows] saved for backward. */
+int hm_k_layernorm_fwd(const float *x, const float *g, const float *b, void *y, float *mean, float *rstd,
+                       int64_t rows, int32_t d, void *stream);
+/* out = LN_bwd(dy) + resid (resid may be NULL or alias out); optional bf16
+ * copy of out; dg += sum dy*xhat, db += sum dy. */
+int hm_k_layernorm_bwd(const float *dy, const float *x, const float *mean, const float *rstd,
+                       const float *g, const float *resid, float *out, void *out_bf16, float *dg,
+                       float *db, int64_t rows, int32_t d, void *stream);
+/* Softmax cross-entropy over vocab columns [0, vocab) of fp32 logits with row
+ * pitch ld; dlogits (bf16, same pitch) = (softmax - onehot) * scale, padding
+ * columns zeroed; loss_sum (fp64) += sum of per-row CE. */
+int hm_k_cross_entropy(const float *logits, const int32_t *labels, int64_t rows, int64_t ld,
+                       int32_t vocab, void *dlogits, double *loss_sum, float scale, void *stream);
+/* db[n] += sum_r dy[r, n] (dy bf16 if is_bf16 else fp32, row pitch ld). */
+int hm_k_bias_grad(const void *dy, int32_t is_bf16, float *db, int64_t rows, int32_t n, int64_t ld,
+                   void *stream);
 
 #ifdef __cplusplus
 }

@@ -4,14 +4,22 @@
 
 #include "plan.hpp"
 
+#include <atomic>
+
 namespace hm {
 static thread_local std::string g_last_error;
 void set_last_error(const std::string &msg) { g_last_error = msg; }
+std::atomic<int64_t> &launch_counter() {
+  static std::atomic<int64_t> n{0};
+  return n;
+}
 }  // namespace hm
 
 extern "C" {
 
 const char *hm_last_error(void) { return hm::g_last_error.c_str(); }
+
+int64_t hm_launch_count(void) { return hm::launch_counter().load(); }
 
 const char *hm_version(void) { return "harmony_b200 0.1 (sm_100a)"; }
 

@@ -1,0 +1,508 @@
+// attention.cu -- fused (flash-style) multi-head attention, forward and
+// backward, for the transformer blocks of a layer pack.
+//
+// Layout: qkv [tokens, 3d] bf16 (q | k | v, head-major inside each third),
+// o / do [tokens, d] bf16, lse [tokens, H] fp32 (log2 domain).  Scores never
+// touch HBM: per (sample, head, 64-query block) the kernel streams 64-key K/V
+// tiles through shared memory (cp.async double buffer), keeps the online
+// softmax in registers and accumulates O in registers.
+//
+// Round-1 implementation: warp-level mma.sync m16n8k16 (bf16 -> fp32) with
+// ldmatrix fragments.  Attention is ~5-10% of a block's FLOPs at the BASELINE
+// shapes (4sd vs 24d^2, halved by the causal mask); the tcgen05 version is a
+// later-round item.
+#include <cuda_bf16.h>
+
+#include "../runtime/common.hpp"
+
+namespace hm {
+namespace attn {
+
+constexpr int BQ = 64, BKV = 64, THREADS = 128;
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N));
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void *p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void *p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"((uint32_t)__cvta_generic_to_shared(p)));
+}
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t *>(&v);
+}
+
+// Copy a [64 rows x DH] bf16 tile (global row pitch `ld` elements) into smem
+// with row pitch DH+8.
+template <int DH>
+__device__ __forceinline__ void load_tile(__nv_bfloat16 *s, const __nv_bfloat16 *g, int64_t ld) {
+  constexpr int CH = DH / 8;  // 16-byte chunks per row
+  for (int i = threadIdx.x; i < 64 * CH; i += THREADS) {
+    const int r = i / CH, c = i % CH;
+    cp_async16(s + r * (DH + 8) + c * 8, g + (int64_t)r * ld + c * 8);
+  }
+}
+
+// A fragments (16 rows x 16 cols) from a row-major smem tile.
+template <int LD>
+__device__ __forceinline__ void lda_frag(uint32_t (&a)[4], const __nv_bfloat16 *s, int row0, int col0) {
+  const int lane = threadIdx.x & 31;
+  const int mi = lane >> 3, ri = lane & 7;
+  ldsm_x4(a, s + (row0 + ri + (mi & 1) * 8) * LD + col0 + (mi >> 1) * 8);
+}
+// B fragments for two n-blocks from storage [n][k] (row-major, k contiguous).
+template <int LD>
+__device__ __forceinline__ void ldb_nk(uint32_t (&b)[4], const __nv_bfloat16 *s, int n0, int k0) {
+  const int lane = threadIdx.x & 31;
+  const int mi = lane >> 3, ri = lane & 7;
+  ldsm_x4(b, s + (n0 + ri + (mi >> 1) * 8) * LD + k0 + (mi & 1) * 8);
+}
+// B fragments for two n-blocks from storage [k][n] (row-major, n contiguous).
+template <int LD>
+__device__ __forceinline__ void ldb_kn(uint32_t (&b)[4], const __nv_bfloat16 *s, int k0, int n0) {
+  const int lane = threadIdx.x & 31;
+  const int mi = lane >> 3, ri = lane & 7;
+  ldsm_x4_t(b, s + (k0 + ri + (mi & 1) * 8) * LD + n0 + (mi >> 1) * 8);
+}
+
+template <int DH, bool CAUSAL>
+__global__ void __launch_bounds__(THREADS) fwd_kernel(const __nv_bfloat16 *__restrict__ qkv,
+                                                      __nv_bfloat16 *__restrict__ out, float *__restrict__ lse,
+                                                      int S, int H, float scale_log2) {
+  constexpr int LD = DH + 8;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  __nv_bfloat16 *sQ = reinterpret_cast<__nv_bfloat16 *>(smem_raw);
+  __nv_bfloat16 *sK = sQ + 64 * LD;       // [2][64][LD]
+  __nv_bfloat16 *sV = sK + 2 * 64 * LD;   // [2][64][LD]
+  const int nq = S / BQ;
+  const int qb = CAUSAL ? nq - 1 - (int)blockIdx.x : (int)blockIdx.x;
+  const int bh = blockIdx.y, b = bh / H, h = bh % H;
+  const int d = H * DH;
+  const int64_t ld = 3 * (int64_t)d;
+  const __nv_bfloat16 *base = qkv + (int64_t)b * S * ld;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+
+  load_tile<DH>(sQ, base + (int64_t)qb * BQ * ld + h * DH, ld);
+  load_tile<DH>(sK, base + d + h * DH, ld);
+  load_tile<DH>(sV, base + 2 * d + h * DH, ld);
+  cp_commit();
+  const int nk = CAUSAL ? qb + 1 : nq;
+
+  uint32_t qf[DH / 16][4];
+  float o[DH / 8][4];
+#pragma unroll
+  for (int j = 0; j < DH / 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+
+  for (int kb = 0; kb < nk; ++kb) {
+    const int st = kb & 1;
+    if (kb + 1 < nk) {
+      load_tile<DH>(sK + (st ^ 1) * 64 * LD, base + (int64_t)(kb + 1) * BKV * ld + d + h * DH, ld);
+      load_tile<DH>(sV + (st ^ 1) * 64 * LD, base + (int64_t)(kb + 1) * BKV * ld + 2 * d + h * DH, ld);
+    }
+    cp_commit();
+    cp_wait<1>();
+    __syncthreads();
+    if (kb == 0) {
+#pragma unroll
+      for (int kc = 0; kc < DH / 16; ++kc) lda_frag<LD>(qf[kc], sQ, warp * 16, kc * 16);
+    }
+    const __nv_bfloat16 *k_s = sK + st * 64 * LD;
+    const __nv_bfloat16 *v_s = sV + st * 64 * LD;
+    float s[8][4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s[j][0] = s[j][1] = s[j][2] = s[j][3] = 0.f;
+#pragma unroll
+    for (int kc = 0; kc < DH / 16; ++kc) {
+#pragma unroll
+      for (int nb2 = 0; nb2 < 4; ++nb2) {
+        uint32_t bf[4];
+        ldb_nk<LD>(bf, k_s, nb2 * 16, kc * 16);
+        mma16816(s[2 * nb2], qf[kc], bf[0], bf[1]);
+        mma16816(s[2 * nb2 + 1], qf[kc], bf[2], bf[3]);
+      }
+    }
+    const bool diag = CAUSAL && kb == qb;
+    float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float v = s[j][e] * scale_log2;
+        if (diag) {
+          const int key = 8 * j + 2 * t + (e & 1);
+          const int qry = warp * 16 + g + (e >= 2 ? 8 : 0);
+          if (key > qry) v = -INFINITY;
+        }
+        s[j][e] = v;
+      }
+      mx0 = fmaxf(mx0, fmaxf(s[j][0], s[j][1]));
+      mx1 = fmaxf(mx1, fmaxf(s[j][2], s[j][3]));
+    }
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffff, mx0, 1));
+    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffff, mx0, 2));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffff, mx1, 1));
+    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffff, mx1, 2));
+    const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+    const float a0 = exp2f(m0 - mn0), a1 = exp2f(m1 - mn1);
+    m0 = mn0;
+    m1 = mn1;
+    float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      s[j][0] = exp2f(s[j][0] - mn0);
+      s[j][1] = exp2f(s[j][1] - mn0);
+      s[j][2] = exp2f(s[j][2] - mn1);
+      s[j][3] = exp2f(s[j][3] - mn1);
+      rs0 += s[j][0] + s[j][1];
+      rs1 += s[j][2] + s[j][3];
+    }
+    l0 = l0 * a0 + rs0;
+    l1 = l1 * a1 + rs1;
+#pragma unroll
+    for (int j = 0; j < DH / 8; ++j) {
+      o[j][0] *= a0; o[j][1] *= a0;
+      o[j][2] *= a1; o[j][3] *= a1;
+    }
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc) {
+      uint32_t pa[4] = {pack_bf16(s[2 * kc][0], s[2 * kc][1]), pack_bf16(s[2 * kc][2], s[2 * kc][3]),
+                        pack_bf16(s[2 * kc + 1][0], s[2 * kc + 1][1]), pack_bf16(s[2 * kc + 1][2], s[2 * kc + 1][3])};
+#pragma unroll
+      for (int nb2 = 0; nb2 < DH / 16; ++nb2) {
+        uint32_t bf[4];
+        ldb_kn<LD>(bf, v_s, kc * 16, nb2 * 16);
+        mma16816(o[2 * nb2], pa, bf[0], bf[1]);
+        mma16816(o[2 * nb2 + 1], pa, bf[2], bf[3]);
+      }
+    }
+    __syncthreads();
+  }
+  l0 += __shfl_xor_sync(0xffffffff, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffff, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffff, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffff, l1, 2);
+  const float i0 = 1.f / l0, i1 = 1.f / l1;
+  const int64_t row0 = (int64_t)b * S + qb * BQ + warp * 16 + g;
+  __nv_bfloat16 *o0 = out + row0 * d + h * DH;
+  __nv_bfloat16 *o1 = o0 + 8 * (int64_t)d;
+#pragma unroll
+  for (int j = 0; j < DH / 8; ++j) {
+    *reinterpret_cast<uint32_t *>(o0 + 8 * j + 2 * t) = pack_bf16(o[j][0] * i0, o[j][1] * i0);
+    *reinterpret_cast<uint32_t *>(o1 + 8 * j + 2 * t) = pack_bf16(o[j][2] * i1, o[j][3] * i1);
+  }
+  if (t == 0) {
+    lse[row0 * H + h] = m0 + log2f(l0);
+    lse[(row0 + 8) * H + h] = m1 + log2f(l1);
+  }
+}
+
+// D[token, h] = sum_c dO * O  (the softmax-backward row term)
+template <int DH>
+__global__ void dvec_kernel(const __nv_bfloat16 *__restrict__ o, const __nv_bfloat16 *__restrict__ dout,
+                            float *__restrict__ dvec, int64_t rows, int H) {
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= rows * H) return;
+  const __nv_bfloat16 *a = o + w * DH;  // [tokens, H*DH] contiguous -> (token, h) rows of DH
+  const __nv_bfloat16 *c = dout + w * DH;
+  float acc = 0.f;
+  for (int i = lane * 2; i < DH; i += 64) {
+    float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(a + i));
+    float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(c + i));
+    acc += x.x * y.x + x.y * y.y;
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffff, acc, off);
+  if (lane == 0) dvec[w] = acc;
+}
+
+template <int DH, bool CAUSAL>
+__global__ void __launch_bounds__(THREADS) bwd_kernel(const __nv_bfloat16 *__restrict__ qkv,
+                                                      const __nv_bfloat16 *__restrict__ dout,
+                                                      const float *__restrict__ lse, const float *__restrict__ dvec,
+                                                      float *__restrict__ dq_acc, __nv_bfloat16 *__restrict__ dqkv,
+                                                      int S, int H, float scale_log2, float scale) {
+  constexpr int LD = DH + 8;
+  constexpr int LDS = 64 + 8;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  __nv_bfloat16 *sK = reinterpret_cast<__nv_bfloat16 *>(smem_raw);
+  __nv_bfloat16 *sV = sK + 64 * LD;
+  __nv_bfloat16 *sQ = sV + 64 * LD;
+  __nv_bfloat16 *sdO = sQ + 64 * LD;
+  __nv_bfloat16 *sdS = sdO + 64 * LD;  // [64 queries][LDS]
+  float *sL = reinterpret_cast<float *>(sdS + 64 * LDS);
+  float *sD = sL + 64;
+  const int nq = S / BQ;
+  const int kb = blockIdx.x;
+  const int bh = blockIdx.y, b = bh / H, h = bh % H;
+  const int d = H * DH;
+  const int64_t ld = 3 * (int64_t)d;
+  const __nv_bfloat16 *base = qkv + (int64_t)b * S * ld;
+  const __nv_bfloat16 *dbase = dout + (int64_t)b * S * d;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+
+  load_tile<DH>(sK, base + (int64_t)kb * BKV * ld + d + h * DH, ld);
+  load_tile<DH>(sV, base + (int64_t)kb * BKV * ld + 2 * d + h * DH, ld);
+  cp_commit();
+  cp_wait<0>();
+  __syncthreads();
+  uint32_t kf[DH / 16][4], vf[DH / 16][4];
+#pragma unroll
+  for (int kc = 0; kc < DH / 16; ++kc) {
+    lda_frag<LD>(kf[kc], sK, warp * 16, kc * 16);
+    lda_frag<LD>(vf[kc], sV, warp * 16, kc * 16);
+  }
+  float dk[DH / 8][4], dv[DH / 8][4];
+#pragma unroll
+  for (int j = 0; j < DH / 8; ++j)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) dk[j][e] = dv[j][e] = 0.f;
+
+  for (int qb = CAUSAL ? kb : 0; qb < nq; ++qb) {
+    load_tile<DH>(sQ, base + (int64_t)qb * BQ * ld + h * DH, ld);
+    load_tile<DH>(sdO, dbase + (int64_t)qb * BQ * d + h * DH, d);
+    cp_commit();
+    if (threadIdx.x < 64) {
+      const int64_t row = (int64_t)b * S + qb * BQ + threadIdx.x;
+      sL[threadIdx.x] = lse[row * H + h];
+      sD[threadIdx.x] = dvec[row * H + h];
+    }
+    cp_wait<0>();
+    __syncthreads();
+    // S^T[16 keys x 64 queries] = K Q^T
+    float st[8][4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) st[j][0] = st[j][1] = st[j][2] = st[j][3] = 0.f;
+#pragma unroll
+    for (int kc = 0; kc < DH / 16; ++kc)
+#pragma unroll
+      for (int nb2 = 0; nb2 < 4; ++nb2) {
+        uint32_t bf[4];
+        ldb_nk<LD>(bf, sQ, nb2 * 16, kc * 16);
+        mma16816(st[2 * nb2], kf[kc], bf[0], bf[1]);
+        mma16816(st[2 * nb2 + 1], kf[kc], bf[2], bf[3]);
+      }
+    const bool diag = CAUSAL && qb == kb;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int qry = 8 * j + 2 * t + (e & 1);
+        const int key = warp * 16 + g + (e >= 2 ? 8 : 0);
+        float p = exp2f(st[j][e] * scale_log2 - sL[qry]);
+        if (diag && qry < key) p = 0.f;
+        st[j][e] = p;  // P^T
+      }
+    // dV += P^T dO
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc) {
+      uint32_t pa[4] = {pack_bf16(st[2 * kc][0], st[2 * kc][1]), pack_bf16(st[2 * kc][2], st[2 * kc][3]),
+                        pack_bf16(st[2 * kc + 1][0], st[2 * kc + 1][1]),
+                        pack_bf16(st[2 * kc + 1][2], st[2 * kc + 1][3])};
+#pragma unroll
+      for (int nb2 = 0; nb2 < DH / 16; ++nb2) {
+        uint32_t bf[4];
+        ldb_kn<LD>(bf, sdO, kc * 16, nb2 * 16);
+        mma16816(dv[2 * nb2], pa, bf[0], bf[1]);
+        mma16816(dv[2 * nb2 + 1], pa, bf[2], bf[3]);
+      }
+    }
+    // dP^T = V dO^T
+    float dp[8][4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) dp[j][0] = dp[j][1] = dp[j][2] = dp[j][3] = 0.f;
+#pragma unroll
+    for (int kc = 0; kc < DH / 16; ++kc)
+#pragma unroll
+      for (int nb2 = 0; nb2 < 4; ++nb2) {
+        uint32_t bf[4];
+        ldb_nk<LD>(bf, sdO, nb2 * 16, kc * 16);
+        mma16816(dp[2 * nb2], vf[kc], bf[0], bf[1]);
+        mma16816(dp[2 * nb2 + 1], vf[kc], bf[2], bf[3]);
+      }
+    // dS^T = P^T * (dP^T - D)
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int qry = 8 * j + 2 * t + (e & 1);
+        dp[j][e] = st[j][e] * (dp[j][e] - sD[qry]);
+      }
+    // dK += dS^T Q ; stash dS (as [query][key]) for dQ
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc) {
+      uint32_t pa[4] = {pack_bf16(dp[2 * kc][0], dp[2 * kc][1]), pack_bf16(dp[2 * kc][2], dp[2 * kc][3]),
+                        pack_bf16(dp[2 * kc + 1][0], dp[2 * kc + 1][1]),
+                        pack_bf16(dp[2 * kc + 1][2], dp[2 * kc + 1][3])};
+#pragma unroll
+      for (int nb2 = 0; nb2 < DH / 16; ++nb2) {
+        uint32_t bf[4];
+        ldb_kn<LD>(bf, sQ, kc * 16, nb2 * 16);
+        mma16816(dk[2 * nb2], pa, bf[0], bf[1]);
+        mma16816(dk[2 * nb2 + 1], pa, bf[2], bf[3]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int qry = 8 * j + 2 * t + (e & 1);
+        const int key = warp * 16 + g + (e >= 2 ? 8 : 0);
+        sdS[qry * LDS + key] = __float2bfloat16_rn(dp[j][e]);
+      }
+    __syncthreads();
+    // dQ[16 queries of this warp x DH] += dS K   (reduction over the 64 keys)
+    float dq[DH / 8][4];
+#pragma unroll
+    for (int j = 0; j < DH / 8; ++j) dq[j][0] = dq[j][1] = dq[j][2] = dq[j][3] = 0.f;
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc) {
+      uint32_t af[4];
+      lda_frag<LDS>(af, sdS, warp * 16, kc * 16);
+#pragma unroll
+      for (int nb2 = 0; nb2 < DH / 16; ++nb2) {
+        uint32_t bf[4];
+        ldb_kn<LD>(bf, sK, kc * 16, nb2 * 16);
+        mma16816(dq[2 * nb2], af, bf[0], bf[1]);
+        mma16816(dq[2 * nb2 + 1], af, bf[2], bf[3]);
+      }
+    }
+    const int64_t q0 = (int64_t)b * S + qb * BQ + warp * 16 + g;
+    float *dq0 = dq_acc + q0 * d + h * DH;
+    float *dq1 = dq0 + 8 * (int64_t)d;
+#pragma unroll
+    for (int j = 0; j < DH / 8; ++j) {
+      atomicAdd(dq0 + 8 * j + 2 * t, dq[j][0]);
+      atomicAdd(dq0 + 8 * j + 2 * t + 1, dq[j][1]);
+      atomicAdd(dq1 + 8 * j + 2 * t, dq[j][2]);
+      atomicAdd(dq1 + 8 * j + 2 * t + 1, dq[j][3]);
+    }
+    __syncthreads();
+  }
+  const int64_t k0 = (int64_t)b * S + kb * BKV + warp * 16 + g;
+  __nv_bfloat16 *dk0 = dqkv + k0 * ld + d + h * DH;
+  __nv_bfloat16 *dv0 = dqkv + k0 * ld + 2 * d + h * DH;
+#pragma unroll
+  for (int j = 0; j < DH / 8; ++j) {
+    *reinterpret_cast<uint32_t *>(dk0 + 8 * j + 2 * t) = pack_bf16(dk[j][0] * scale, dk[j][1] * scale);
+    *reinterpret_cast<uint32_t *>(dk0 + 8 * ld + 8 * j + 2 * t) = pack_bf16(dk[j][2] * scale, dk[j][3] * scale);
+    *reinterpret_cast<uint32_t *>(dv0 + 8 * j + 2 * t) = pack_bf16(dv[j][0], dv[j][1]);
+    *reinterpret_cast<uint32_t *>(dv0 + 8 * ld + 8 * j + 2 * t) = pack_bf16(dv[j][2], dv[j][3]);
+  }
+}
+
+__global__ void dq_convert(const float *__restrict__ dq_acc, __nv_bfloat16 *__restrict__ dqkv, int64_t rows, int d,
+                           float scale) {
+  const int64_t n2 = rows * d / 2;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = 2 * i;
+    const int64_t r = e / d, c = e % d;
+    float2 v = *reinterpret_cast<const float2 *>(dq_acc + e);
+    *reinterpret_cast<__nv_bfloat162 *>(dqkv + r * 3 * (int64_t)d + c) = __floats2bfloat162_rn(v.x * scale, v.y * scale);
+  }
+}
+
+template <int DH>
+static size_t fwd_smem() { return (size_t)5 * 64 * (DH + 8) * 2; }
+template <int DH>
+static size_t bwd_smem() { return (size_t)4 * 64 * (DH + 8) * 2 + 64 * 72 * 2 + 2 * 64 * 4; }
+
+template <int DH, bool CAUSAL>
+static int fwd_launch(const __nv_bfloat16 *qkv, __nv_bfloat16 *o, float *lse, int B, int S, int H, cudaStream_t s) {
+  static bool attr = false;
+  auto k = fwd_kernel<DH, CAUSAL>;
+  if (!attr) {
+    HM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd_smem<DH>()));
+    attr = true;
+  }
+  const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
+  k<<<dim3(S / BQ, B * H), THREADS, fwd_smem<DH>(), s>>>(qkv, o, lse, S, H, scale_log2);
+  count_launch();
+  HM_CUDA(cudaGetLastError());
+  return HM_OK;
+}
+
+template <int DH, bool CAUSAL>
+static int bwd_launch(const __nv_bfloat16 *qkv, const __nv_bfloat16 *o, const __nv_bfloat16 *dout, const float *lse,
+                      float *dvec, float *dq_acc, __nv_bfloat16 *dqkv, int B, int S, int H, cudaStream_t s) {
+  static bool attr = false;
+  auto k = bwd_kernel<DH, CAUSAL>;
+  if (!attr) {
+    HM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd_smem<DH>()));
+    attr = true;
+  }
+  const int64_t rows = (int64_t)B * S;
+  const int d = H * DH;
+  HM_CUDA(cudaMemsetAsync(dq_acc, 0, rows * d * sizeof(float), s));
+  const int64_t warps = rows * H;
+  dvec_kernel<DH><<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(o, dout, dvec, rows, H);
+  const float scale = 1.f / sqrtf((float)DH);
+  k<<<dim3(S / BKV, B * H), THREADS, bwd_smem<DH>(), s>>>(qkv, dout, lse, dvec, dq_acc, dqkv, S, H,
+                                                           1.4426950408889634f * scale, scale);
+  dq_convert<<<1184, 256, 0, s>>>(dq_acc, dqkv, rows, d, scale);
+  count_launch(3);
+  HM_CUDA(cudaGetLastError());
+  return HM_OK;
+}
+
+int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int DH, int causal, cudaStream_t s) {
+  if (S % 64) return fail(HM_ERR_VALIDATION, "attention: seq_len must be a multiple of 64");
+  auto q = static_cast<const __nv_bfloat16 *>(qkv);
+  auto out = static_cast<__nv_bfloat16 *>(o);
+  if (DH == 64) return causal ? fwd_launch<64, true>(q, out, lse, B, S, H, s) : fwd_launch<64, false>(q, out, lse, B, S, H, s);
+  if (DH == 128)
+    return causal ? fwd_launch<128, true>(q, out, lse, B, S, H, s) : fwd_launch<128, false>(q, out, lse, B, S, H, s);
+  return fail(HM_ERR_VALIDATION, "attention: head_dim must be 64 or 128");
+}
+
+int backward(const void *qkv, const void *o, const void *dout, const float *lse, float *dvec, float *dq_acc,
+             void *dqkv, int B, int S, int H, int DH, int causal, cudaStream_t s) {
+  if (S % 64) return fail(HM_ERR_VALIDATION, "attention: seq_len must be a multiple of 64");
+  auto q = static_cast<const __nv_bfloat16 *>(qkv);
+  auto oo = static_cast<const __nv_bfloat16 *>(o);
+  auto dO = static_cast<const __nv_bfloat16 *>(dout);
+  auto dst = static_cast<__nv_bfloat16 *>(dqkv);
+  if (DH == 64)
+    return causal ? bwd_launch<64, true>(q, oo, dO, lse, dvec, dq_acc, dst, B, S, H, s)
+                  : bwd_launch<64, false>(q, oo, dO, lse, dvec, dq_acc, dst, B, S, H, s);
+  if (DH == 128)
+    return causal ? bwd_launch<128, true>(q, oo, dO, lse, dvec, dq_acc, dst, B, S, H, s)
+                  : bwd_launch<128, false>(q, oo, dO, lse, dvec, dq_acc, dst, B, S, H, s);
+  return fail(HM_ERR_VALIDATION, "attention: head_dim must be 64 or 128");
+}
+
+}  // namespace attn
+}  // namespace hm
+
+extern "C" int hm_k_attn_fwd(const void *qkv, void *out, float *lse, int32_t batch, int32_t seq, int32_t heads,
+                             int32_t head_dim, int32_t causal, void *stream) {
+  return hm::attn::forward(qkv, out, lse, batch, seq, heads, head_dim, causal, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int hm_k_attn_bwd(const void *qkv, const void *out, const void *dout, const float *lse, float *dvec,
+                             float *dq_acc, void *dqkv, int32_t batch, int32_t seq, int32_t heads, int32_t head_dim,
+                             int32_t causal, void *stream) {
+  return hm::attn::backward(qkv, out, dout, lse, dvec, dq_acc, dqkv, batch, seq, heads, head_dim, causal,
+                            static_cast<cudaStream_t>(stream));
+}

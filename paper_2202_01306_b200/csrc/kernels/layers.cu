@@ -1,0 +1,392 @@
+// layers.cu -- the bandwidth-bound kernels of a transformer layer pack:
+// weight cast, embedding fwd/bwd, LayerNorm fwd/bwd, softmax cross-entropy
+// fwd+bwd, bias gradients.  All are HBM-bound row/column kernels: one warp
+// per row, 16-byte vector accesses, fp32 math.
+#include <cuda_bf16.h>
+
+#include "../runtime/common.hpp"
+
+namespace hm {
+namespace layers {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffff, v, o));
+  return v;
+}
+
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// ---- fp32 -> bf16 cast (pack weights after swap-in; dY before GEMMs) --------
+__global__ void cast_kernel(const float4 *__restrict__ src, uint2 *__restrict__ dst, int64_t n4) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 v = src[i];
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    dst[i] = make_uint2(*reinterpret_cast<uint32_t *>(&a), *reinterpret_cast<uint32_t *>(&b));
+  }
+}
+__global__ void cast_tail(const float *src, __nv_bfloat16 *dst, int64_t begin, int64_t n) {
+  int64_t i = begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = __float2bfloat16_rn(src[i]);
+}
+
+int cast_f32_bf16(const float *src, void *dst, int64_t n, cudaStream_t s) {
+  if (n <= 0) return HM_OK;
+  const int64_t n4 = ((uintptr_t)src & 15) || ((uintptr_t)dst & 7) ? 0 : n / 4;
+  if (n4) {
+    int64_t blocks = (n4 + 255) / 256;
+    if (blocks > (int64_t)sm_count() * 16) blocks = (int64_t)sm_count() * 16;
+    cast_kernel<<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<const float4 *>(src), reinterpret_cast<uint2 *>(dst), n4);
+    count_launch();
+  }
+  if (n4 * 4 < n) {
+    const int64_t rest = n - n4 * 4;
+    cast_tail<<<(unsigned)((rest + 255) / 256), 256, 0, s>>>(src, static_cast<__nv_bfloat16 *>(dst), n4 * 4, n);
+    count_launch();
+  }
+  HM_CUDA(cudaGetLastError());
+  return HM_OK;
+}
+
+// ---- embedding -----------------------------------------------------------------
+__global__ void embed_fwd_kernel(const int32_t *__restrict__ tok, const float *__restrict__ wte,
+                                 const float *__restrict__ wpe, float *__restrict__ out, int64_t rows, int S, int d) {
+  const int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float4 *a = reinterpret_cast<const float4 *>(wte + (int64_t)tok[r] * d);
+  const float4 *b = reinterpret_cast<const float4 *>(wpe + (int64_t)(r % S) * d);
+  float4 *o = reinterpret_cast<float4 *>(out + r * d);
+  for (int i = lane; i < d / 4; i += 32) {
+    float4 x = a[i], y = b[i];
+    o[i] = make_float4(x.x + y.x, x.y + y.y, x.z + y.z, x.w + y.w);
+  }
+}
+// dwte[tok] += dx (atomic; tokens repeat), one warp per row
+__global__ void embed_bwd_tok_kernel(const int32_t *__restrict__ tok, const float *__restrict__ dx,
+                                     float *__restrict__ dwte, int64_t rows, int d) {
+  const int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  float *dst = dwte + (int64_t)tok[r] * d;
+  const float *src = dx + r * d;
+  for (int i = lane; i < d; i += 32) atomicAdd(dst + i, src[i]);
+}
+// dwpe[p] += sum_b dx[b*S + p] (deterministic, no atomics)
+__global__ void embed_bwd_pos_kernel(const float *__restrict__ dx, float *__restrict__ dwpe, int B, int S, int d) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)S * d) return;
+  float acc = 0.f;
+  for (int b = 0; b < B; ++b) acc += dx[(int64_t)b * S * d + i];
+  dwpe[i] += acc;
+}
+
+int embed_fwd(const int32_t *tok, const float *wte, const float *wpe, float *out, int B, int S, int d, cudaStream_t s) {
+  const int64_t rows = (int64_t)B * S;
+  embed_fwd_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, s>>>(tok, wte, wpe, out, rows, S, d);
+  count_launch();
+  HM_CUDA(cudaGetLastError());
+  return HM_OK;
+}
+int embed_bwd(const int32_t *tok, const float *dx, float *dwte, float *dwpe, int B, int S, int d, cudaStream_t s) {
+  const int64_t rows = (int64_t)B * S;
+  embed_bwd_tok_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, s>>>(tok, dx, dwte, rows, d);
+  embed_bwd_pos_kernel<<<(unsigned)(((int64_t)S * d + 255) / 256), 256, 0, s>>>(dx, dwpe, B, S, d);
+  count_launch(2);
+  HM_CUDA(cudaGetLastError());
+  return HM_OK;
+}
+
+// ---- LayerNorm forward: fp32 x -> bf16 y (GEMM operand), mean/rstd saved ---------
+__global__ void ln_fwd_kernel(const float *__restrict__ x, const float *__restrict__ gam, const float *__restrict__ bet,
+                              __nv_bfloat16 *__restrict__ y, float *__restrict__ mean, float *__restrict__ rstd,
+                              int64_t rows, int d, float eps) {
+  const int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float4 *xr = reinterpret_cast<const float4 *>(x + r * d);
+  const int n4 = d / 4;
+  float s = 0.f;
+  for (int i = lane; i < n4; i += 32) {
+    float4 v = xr[i];
+    s += v.x + v.y + v.z + v.w;
+  }
+  const float mu = warp_sum(s) / d;
+  float q = 0.f;
+  for (int i = lane; i < n4; i += 32) {
+    float4 v = xr[i];
+    q += (v.x - mu) * (v.x - mu) + (v.y - mu) * (v.y - mu) + (v.z - mu) * (v.z - mu) + (v.w - mu) * (v.w - mu);
+  }
+  const float rs = rsqrtf(warp_sum(q) / d + eps);
+  uint2 *yr = reinterpret_cast<uint2 *>(y + r * d);
+  const float4 *g4 = reinterpret_cast<const float4 *>(gam);
+  const float4 *b4 = reinterpret_cast<const float4 *>(bet);
+  for (int i = lane; i < n4; i += 32) {
+    float4 v = xr[i], gg = g4[i], bb = b4[i];
+    __nv_bfloat162 a = __floats2bfloat162_rn((v.x - mu) * rs * gg.x + bb.x, (v.y - mu) * rs * gg.y + bb.y);
+    __nv_bfloat162 c = __floats2bfloat162_rn((v.z - mu) * rs * gg.z + bb.z, (v.w - mu) * rs * gg.w + bb.w);
+    yr[i] = make_uint2(*reinterpret_cast<uint32_t *>(&a), *reinterpret_cast<uint32_t *>(&c));
+  }
+  if (lane == 0) {
+    mean[r] = mu;
+    rstd[r] = rs;
+  }
+}
+
+int ln_fwd(const float *x, const float *g, const float *b, void *y, float *mean, float *rstd, int64_t rows, int d,
+           cudaStream_t s) {
+  if (d % 4) return fail(HM_ERR_VALIDATION, "layernorm: d must be a multiple of 4");
+  ln_fwd_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, s>>>(x, g, b, static_cast<__nv_bfloat16 *>(y), mean,
+                                                                    rstd, rows, d, 1e-5f);
+  count_launch();
+  HM_CUDA(cudaGetLastError());
+  return HM_OK;
+}
+
+// ---- LayerNorm backward -------------------------------------------------------------
+// dx = rstd * (dxhat - mean(dxhat) - xhat * mean(dxhat * xhat)),  dxhat = dy * gamma
+// out = dx + resid (resid may alias out or be null); optional bf16 copy of out;
+// dgamma += sum dy*xhat, dbeta += sum dy (block partials in smem, then atomics).
+__global__ void ln_bwd_kernel(const float *__restrict__ dy, const float *__restrict__ x, const float *__restrict__ mean,
+                              const float *__restrict__ rstd, const float *__restrict__ gam, const float *resid,
+                              float *out, __nv_bfloat16 *__restrict__ out_bf, float *__restrict__ dgam,
+                              float *__restrict__ dbet, int64_t rows, int d, int rows_per_block) {
+  extern __shared__ float sacc[];  // [2*d]
+  for (int i = threadIdx.x; i < 2 * d; i += blockDim.x) sacc[i] = 0.f;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int64_t r_begin = (int64_t)blockIdx.x * rows_per_block;
+  const int64_t r_end = min(rows, r_begin + rows_per_block);
+  const int n4 = d / 4;
+  const float4 *g4 = reinterpret_cast<const float4 *>(gam);
+  for (int64_t r = r_begin + warp; r < r_end; r += nw) {
+    const float4 *dyr = reinterpret_cast<const float4 *>(dy + r * d);
+    const float4 *xr = reinterpret_cast<const float4 *>(x + r * d);
+    const float mu = mean[r], rs = rstd[r];
+    float c1 = 0.f, c2 = 0.f;
+    for (int i = lane; i < n4; i += 32) {
+      float4 a = dyr[i], v = xr[i], gg = g4[i];
+      float h0 = (v.x - mu) * rs, h1 = (v.y - mu) * rs, h2 = (v.z - mu) * rs, h3 = (v.w - mu) * rs;
+      float e0 = a.x * gg.x, e1 = a.y * gg.y, e2 = a.z * gg.z, e3 = a.w * gg.w;
+      c1 += e0 + e1 + e2 + e3;
+      c2 += e0 * h0 + e1 * h1 + e2 * h2 + e3 * h3;
+      atomicAdd(&sacc[4 * i], a.x * h0);
+      atomicAdd(&sacc[4 * i + 1], a.y * h1);
+      atomicAdd(&sacc[4 * i + 2], a.z * h2);
+      atomicAdd(&sacc[4 * i + 3], a.w * h3);
+      atomicAdd(&sacc[d + 4 * i], a.x);
+      atomicAdd(&sacc[d + 4 * i + 1], a.y);
+      atomicAdd(&sacc[d + 4 * i + 2], a.z);
+      atomicAdd(&sacc[d + 4 * i + 3], a.w);
+    }
+    c1 = warp_sum(c1) / d;
+    c2 = warp_sum(c2) / d;
+    float4 *outr = reinterpret_cast<float4 *>(out + r * d);
+    const float4 *rr = resid ? reinterpret_cast<const float4 *>(resid + r * d) : nullptr;
+    uint2 *ob = out_bf ? reinterpret_cast<uint2 *>(out_bf + r * d) : nullptr;
+    for (int i = lane; i < n4; i += 32) {
+      float4 a = dyr[i], v = xr[i], gg = g4[i];
+      float4 o;
+      o.x = rs * (a.x * gg.x - c1 - (v.x - mu) * rs * c2);
+      o.y = rs * (a.y * gg.y - c1 - (v.y - mu) * rs * c2);
+      o.z = rs * (a.z * gg.z - c1 - (v.z - mu) * rs * c2);
+      o.w = rs * (a.w * gg.w - c1 - (v.w - mu) * rs * c2);
+      if (rr) {
+        float4 q = rr[i];
+        o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+      }
+      outr[i] = o;
+      if (ob) {
+        __nv_bfloat162 p0 = __floats2bfloat162_rn(o.x, o.y), p1 = __floats2bfloat162_rn(o.z, o.w);
+        ob[i] = make_uint2(*reinterpret_cast<uint32_t *>(&p0), *reinterpret_cast<uint32_t *>(&p1));
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    atomicAdd(&dgam[i], sacc[i]);
+    atomicAdd(&dbet[i], sacc[d + i]);
+  }
+}
+
+int ln_bwd(const float *dy, const float *x, const float *mean, const float *rstd, const float *g, const float *resid,
+           float *out, void *out_bf, float *dg, float *db, int64_t rows, int d, cudaStream_t s) {
+  if (d % 4) return fail(HM_ERR_VALIDATION, "layernorm: d must be a multiple of 4");
+  const size_t smem = 2 * (size_t)d * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    HM_CUDA(cudaFuncSetAttribute(ln_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  int64_t blocks = sm_count() * 2;
+  int rpb = (int)((rows + blocks - 1) / blocks);
+  if (rpb < 8) rpb = 8;
+  blocks = (rows + rpb - 1) / rpb;
+  ln_bwd_kernel<<<(unsigned)blocks, 512, smem, s>>>(dy, x, mean, rstd, g, resid, out,
+                                                    static_cast<__nv_bfloat16 *>(out_bf), dg, db, rows, d, rpb);
+  count_launch();
+  HM_CUDA(cudaGetLastError());
+  return HM_OK;
+}
+
+// ---- softmax cross-entropy over the (padded) vocabulary -----------------------------
+// logits fp32 [rows, ldl], valid columns [0, V); loss_sum += sum_r CE_r (double);
+// dlogits bf16 [rows, ldl] = (softmax - onehot) * scale, zero in the padding.
+__global__ void ce_kernel(const float *__restrict__ logits, const int32_t *__restrict__ labels, int64_t ldl, int V,
+                          __nv_bfloat16 *__restrict__ dlog, double *loss_sum, float scale) {
+  const int64_t r = blockIdx.x;
+  const float *row = logits + r * ldl;
+  __shared__ float red_m[32], red_s[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  float m = -INFINITY, s = 0.f;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    const float v = row[i];
+    if (v > m) {
+      s = s * __expf(m - v) + 1.f;
+      m = v;
+    } else {
+      s += __expf(v - m);
+    }
+  }
+  // combine (m, s) pairs: warp, then block
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const float mo = __shfl_xor_sync(0xffffffff, m, o), so = __shfl_xor_sync(0xffffffff, s, o);
+    const float mn = fmaxf(m, mo);
+    s = (m == -INFINITY ? 0.f : s * __expf(m - mn)) + (mo == -INFINITY ? 0.f : so * __expf(mo - mn));
+    m = mn;
+  }
+  if (lane == 0) {
+    red_m[warp] = m;
+    red_s[warp] = s;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    m = lane < nw ? red_m[lane] : -INFINITY;
+    s = lane < nw ? red_s[lane] : 0.f;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const float mo = __shfl_xor_sync(0xffffffff, m, o), so = __shfl_xor_sync(0xffffffff, s, o);
+      const float mn = fmaxf(m, mo);
+      s = (m == -INFINITY ? 0.f : s * __expf(m - mn)) + (mo == -INFINITY ? 0.f : so * __expf(mo - mn));
+      m = mn;
+    }
+    if (lane == 0) {
+      red_m[0] = m;
+      red_s[0] = s;
+    }
+  }
+  __syncthreads();
+  m = red_m[0];
+  s = red_s[0];
+  const int lab = labels[r];
+  const float inv = 1.f / s;
+  __nv_bfloat16 *drow = dlog + r * ldl;
+  for (int i = threadIdx.x; i < ldl; i += blockDim.x) {
+    float gval = 0.f;
+    if (i < V) gval = (__expf(row[i] - m) * inv - (i == lab ? 1.f : 0.f)) * scale;
+    drow[i] = __float2bfloat16_rn(gval);
+  }
+  if (threadIdx.x == 0) atomicAdd(loss_sum, (double)(logf(s) + m - row[lab]));
+}
+
+int cross_entropy(const float *logits, const int32_t *labels, int64_t rows, int64_t ldl, int V, void *dlogits,
+                  double *loss_sum, float scale, cudaStream_t s) {
+  ce_kernel<<<(unsigned)rows, 512, 0, s>>>(logits, labels, ldl, V, static_cast<__nv_bfloat16 *>(dlogits), loss_sum,
+                                            scale);
+  count_launch();
+  HM_CUDA(cudaGetLastError());
+  return HM_OK;
+}
+
+// ---- bias gradient: db[n] += sum_r dy[r, n] ------------------------------------------
+template <typename T>
+__global__ void bias_grad_kernel(const T *__restrict__ dy, float *__restrict__ db, int64_t rows, int n, int64_t ld,
+                                 int rows_per_block) {
+  const int col = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
+  if (col >= n) return;
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_block;
+  const int64_t r1 = min(rows, r0 + rows_per_block);
+  float a0 = 0.f, a1 = 0.f;
+  for (int64_t r = r0; r < r1; ++r) {
+    if constexpr (sizeof(T) == 2) {
+      float2 v = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(dy + r * ld + col));
+      a0 += v.x;
+      a1 += v.y;
+    } else {
+      float2 v = *reinterpret_cast<const float2 *>(dy + r * ld + col);
+      a0 += v.x;
+      a1 += v.y;
+    }
+  }
+  atomicAdd(db + col, a0);
+  atomicAdd(db + col + 1, a1);
+}
+
+int bias_grad(const void *dy, int is_bf16, float *db, int64_t rows, int n, int64_t ld, cudaStream_t s) {
+  if (n % 2) return fail(HM_ERR_VALIDATION, "bias_grad: n must be even");
+  const int threads = 128;
+  const int gx = (n / 2 + threads - 1) / threads;
+  int64_t gy = (sm_count() * 8 + gx - 1) / gx;
+  int rpb = (int)((rows + gy - 1) / gy);
+  if (rpb < 32) rpb = 32;
+  gy = (rows + rpb - 1) / rpb;
+  if (is_bf16)
+    bias_grad_kernel<__nv_bfloat16><<<dim3(gx, (unsigned)gy), threads, 0, s>>>(
+        static_cast<const __nv_bfloat16 *>(dy), db, rows, n, ld, rpb);
+  else
+    bias_grad_kernel<float><<<dim3(gx, (unsigned)gy), threads, 0, s>>>(static_cast<const float *>(dy), db, rows, n,
+                                                                       ld, rpb);
+  count_launch();
+  HM_CUDA(cudaGetLastError());
+  return HM_OK;
+}
+
+}  // namespace layers
+}  // namespace hm
+
+using namespace hm::layers;
+
+extern "C" {
+int hm_k_cast_bf16(const float *src, void *dst, int64_t n, void *stream) {
+  return cast_f32_bf16(src, dst, n, static_cast<cudaStream_t>(stream));
+}
+int hm_k_embed_fwd(const int32_t *tokens, const float *wte, const float *wpe, float *out, int32_t batch, int32_t seq,
+                   int32_t d, void *stream) {
+  return embed_fwd(tokens, wte, wpe, out, batch, seq, d, static_cast<cudaStream_t>(stream));
+}
+int hm_k_embed_bwd(const int32_t *tokens, const float *dx, float *dwte, float *dwpe, int32_t batch, int32_t seq,
+                   int32_t d, void *stream) {
+  return embed_bwd(tokens, dx, dwte, dwpe, batch, seq, d, static_cast<cudaStream_t>(stream));
+}
+int hm_k_layernorm_fwd(const float *x, const float *g, const float *b, void *y, float *mean, float *rstd, int64_t rows,
+                       int32_t d, void *stream) {
+  return ln_fwd(x, g, b, y, mean, rstd, rows, d, static_cast<cudaStream_t>(stream));
+}
+int hm_k_layernorm_bwd(const float *dy, const float *x, const float *mean, const float *rstd, const float *g,
+                       const float *resid, float *out, void *out_bf16, float *dg, float *db, int64_t rows, int32_t d,
+                       void *stream) {
+  return ln_bwd(dy, x, mean, rstd, g, resid, out, out_bf16, dg, db, rows, d, static_cast<cudaStream_t>(stream));
+}
+int hm_k_cross_entropy(const float *logits, const int32_t *labels, int64_t rows, int64_t ld, int32_t vocab,
+                       void *dlogits, double *loss_sum, float scale, void *stream) {
+  return cross_entropy(logits, labels, rows, ld, vocab, dlogits, loss_sum, scale, static_cast<cudaStream_t>(stream));
+}
+int hm_k_bias_grad(const void *dy, int32_t is_bf16, float *db, int64_t rows, int32_t n, int64_t ld, void *stream) {
+  return bias_grad(dy, is_bf16, db, rows, n, ld, static_cast<cudaStream_t>(stream));
+}
+}

@@ -1,0 +1,39 @@
+// common.hpp -- error reporting and launch accounting shared by kernels and runtime.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <string>
+
+#include "../../../include/harmony_b200.h"
+
+namespace hm {
+
+void set_last_error(const std::string &msg);
+
+inline int fail(int code, const std::string &msg) {
+  set_last_error(msg);
+  return code;
+}
+
+// Kernels launched by this library (all threads); the bench reports the
+// delta over its timed region as "gpu_launches".
+std::atomic<int64_t> &launch_counter();
+inline void count_launch(int64_t n = 1) { launch_counter().fetch_add(n, std::memory_order_relaxed); }
+
+#define HM_CUDA(call)                                                                        \
+  do {                                                                                       \
+    cudaError_t _e = (call);                                                                 \
+    if (_e != cudaSuccess)                                                                   \
+      return ::hm::fail(HM_ERR_DEVICE, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+#define HM_TRY(expr)         \
+  do {                       \
+    int _rc = (expr);        \
+    if (_rc != HM_OK) return _rc; \
+  } while (0)
+
+}  // namespace hm

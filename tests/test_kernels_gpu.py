@@ -1,0 +1,220 @@
+"""Numerics of the sm_100a kernels against plain PyTorch fp32 references of
+the same op (run on the B200 box: pytest -m gpu)."""
+
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ops():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2202_01306_b200 import ops as O
+    return O
+
+
+def _bf(*shape, scale=1.0):
+    return (torch.randn(*shape, device="cuda") * scale).to(torch.bfloat16)
+
+
+def _rel(a, b):
+    return ((a.float() - b.float()).norm() / (b.float().norm() + 1e-30)).item()
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 128, 64), (256, 256, 128), (512, 1600, 1600), (4096, 4800, 1600),
+                                   (384, 4096, 256), (200, 136, 192), (1024, 50304, 256)])
+def test_gemm_fwd_kk(ops, M, N, K):
+    torch.manual_seed(0)
+    a, b = _bf(M, K), _bf(N, K)
+    d = torch.empty(M, N, device="cuda")
+    ops.gemm(a, b, d, epi="f32")
+    ref = a.float() @ b.float().t()
+    torch.cuda.synchronize()
+    assert _rel(d, ref) < 1e-5
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 128, 128), (512, 1600, 6400), (4096, 1600, 1600), (320, 192, 128)])
+def test_gemm_dgrad_k_mn(ops, M, N, K):
+    """dX[M,N] = dY[M,K] . W[K,N]  (W stored [out=K, in=N], B MN-major)."""
+    torch.manual_seed(1)
+    dy, w = _bf(M, K), _bf(K, N)
+    d = torch.empty(M, N, device="cuda")
+    ops.gemm(dy, w, d, b_mn=True, epi="f32")
+    assert _rel(d, dy.float() @ w.float()) < 1e-5
+
+
+@pytest.mark.parametrize("O,I,T", [(128, 128, 128), (1600, 1600, 4096), (4800, 1600, 1024), (6400, 1600, 512),
+                                   (200, 136, 256)])
+def test_gemm_wgrad_mn_mn_accumulate(ops, O, I, T):
+    """dW[O,I] += dY[T,O]^T . X[T,I]  (both MN-major), fp32 accumulate."""
+    torch.manual_seed(2)
+    dy, x = _bf(T, O), _bf(T, I)
+    dw = torch.randn(O, I, device="cuda")
+    ref = dw + dy.float().t() @ x.float()
+    ops.gemm(dy, x, dw, a_mn=True, b_mn=True, epi="acc_f32")
+    assert _rel(dw, ref) < 1e-5
+
+
+def test_gemm_epilogues(ops):
+    torch.manual_seed(3)
+    M, N, K = 512, 1600, 512
+    a, b = _bf(M, K), _bf(N, K, scale=0.05)
+    bias = torch.randn(N, device="cuda")
+    acc = a.float() @ b.float().t()
+    d = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    ops.gemm(a, b, d, epi="bf16", bias=bias)
+    assert _rel(d, acc + bias) < 1e-2
+    r = torch.randn(M, N, device="cuda")
+    d32 = torch.empty(M, N, device="cuda")
+    ops.gemm(a, b, d32, epi="resid_f32", bias=bias, aux=r)
+    assert _rel(d32, r + acc + bias) < 1e-5
+    p = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    g = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    ops.gemm(a, b, g, epi="gelu_bf16", bias=bias, aux=p)
+    pre = acc + bias
+    assert _rel(p, pre) < 1e-2
+    assert _rel(g, torch.nn.functional.gelu(pre, approximate="tanh")) < 1e-2
+    dg = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    ops.gemm(a, b, dg, epi="dgelu_bf16", aux=p)
+    x = p.float().requires_grad_(True)
+    torch.nn.functional.gelu(x, approximate="tanh").backward(acc)
+    assert _rel(dg, x.grad) < 1e-2
+
+
+def test_adam_matches_torch(ops):
+    torch.manual_seed(4)
+    n = 1_000_003
+    w0 = torch.randn(n, device="cuda") * 0.02
+    w = w0.clone()
+    k = torch.zeros(2 * n, device="cuda")
+    p = torch.nn.Parameter(w0.clone())
+    opt = torch.optim.Adam([p], lr=1e-4, betas=(0.9, 0.999), eps=1e-8)
+    for step in range(1, 6):
+        g = torch.randn(n, device="cuda")
+        ops.adam(w, g, k, lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, step=step)
+        p.grad = g.clone()
+        opt.step()
+    torch.cuda.synchronize()
+    assert torch.allclose(w, p.detach(), rtol=1e-6, atol=1e-7)
+    st = opt.state[p]
+    assert torch.allclose(k[0::2], st["exp_avg"], rtol=1e-5, atol=1e-8)
+    assert torch.allclose(k[1::2], st["exp_avg_sq"], rtol=1e-5, atol=1e-10)
+
+
+def _attn_ref(qkv, B, S, H, DH, causal):
+    d = H * DH
+    q, k, v = qkv.float().view(B, S, 3, H, DH).permute(2, 0, 3, 1, 4)  # [B,H,S,DH]
+    s = (q @ k.transpose(-1, -2)) / math.sqrt(DH)
+    if causal:
+        s = s.masked_fill(torch.triu(torch.ones(S, S, device=s.device, dtype=torch.bool), 1), float("-inf"))
+    lse = torch.logsumexp(s, -1)
+    o = torch.softmax(s, -1) @ v
+    return o.permute(0, 2, 1, 3).reshape(B * S, d), lse.permute(0, 2, 1).reshape(B * S, H)
+
+
+@pytest.mark.parametrize("B,S,H,DH,causal", [(2, 128, 4, 64, True), (1, 512, 2, 64, False),
+                                             (2, 256, 3, 64, True), (1, 256, 2, 128, True)])
+def test_attention_fwd_bwd(ops, B, S, H, DH, causal):
+    torch.manual_seed(5)
+    d = H * DH
+    qkv = _bf(B * S, 3 * d)
+    out = torch.empty(B * S, d, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(B * S, H, device="cuda")
+    ops.attn_fwd(qkv, out, lse, batch=B, seq=S, heads=H, head_dim=DH, causal=causal)
+    ro, rl = _attn_ref(qkv, B, S, H, DH, causal)
+    assert _rel(out, ro) < 1e-2
+    assert torch.allclose(lse, rl * 1.4426950408889634, atol=2e-3, rtol=1e-3)
+    dout = _bf(B * S, d)
+    dqkv = torch.empty_like(qkv)
+    ops.attn_bwd(qkv, out, dout, lse, dqkv, batch=B, seq=S, heads=H, head_dim=DH, causal=causal)
+    x = qkv.float().requires_grad_(True)
+    o2, _ = _attn_ref(x, B, S, H, DH, causal)
+    o2.backward(dout.float())
+    g = x.grad.view(B * S, 3, d)
+    got = dqkv.float().view(B * S, 3, d)
+    for i in range(3):
+        assert _rel(got[:, i], g[:, i]) < 2e-2, i
+
+
+def test_layernorm_fwd_bwd(ops):
+    torch.manual_seed(6)
+    M, d = 1000, 1600
+    x = torch.randn(M, d, device="cuda") * 2 + 0.5
+    g = torch.randn(d, device="cuda")
+    b = torch.randn(d, device="cuda")
+    y = torch.empty(M, d, device="cuda", dtype=torch.bfloat16)
+    mean = torch.empty(M, device="cuda")
+    rstd = torch.empty(M, device="cuda")
+    ops.layernorm_fwd(x, g, b, y, mean, rstd)
+    xr = x.clone().requires_grad_(True)
+    gr = g.clone().requires_grad_(True)
+    br = b.clone().requires_grad_(True)
+    yr = torch.nn.functional.layer_norm(xr, (d,), gr, br, 1e-5)
+    assert _rel(y, yr) < 1e-2
+    dy = torch.randn(M, d, device="cuda")
+    yr.backward(dy)
+    resid = torch.randn(M, d, device="cuda")
+    out = torch.empty(M, d, device="cuda")
+    ob = torch.empty(M, d, device="cuda", dtype=torch.bfloat16)
+    dg = torch.ones(d, device="cuda")
+    db = torch.ones(d, device="cuda")
+    ops.layernorm_bwd(dy, x, mean, rstd, g, out, dg, db, resid=resid, out_bf16=ob)
+    assert _rel(out, xr.grad + resid) < 1e-5
+    assert _rel(ob, xr.grad + resid) < 1e-2
+    assert _rel(dg, gr.grad + 1) < 1e-5
+    assert _rel(db, br.grad + 1) < 1e-5
+
+
+def test_embedding_fwd_bwd(ops):
+    torch.manual_seed(7)
+    B, S, V, d = 3, 128, 1024, 256
+    tok = torch.randint(0, V, (B * S,), device="cuda", dtype=torch.int32)
+    wte = torch.randn(V, d, device="cuda")
+    wpe = torch.randn(S, d, device="cuda")
+    out = torch.empty(B * S, d, device="cuda")
+    ops.embed_fwd(tok, wte, wpe, out, batch=B, seq=S)
+    ref = wte[tok.long()] + wpe.repeat(B, 1)
+    assert torch.allclose(out, ref)
+    dx = torch.randn(B * S, d, device="cuda")
+    dwte = torch.zeros(V, d, device="cuda")
+    dwpe = torch.zeros(S, d, device="cuda")
+    ops.embed_bwd(tok, dx, dwte, dwpe, batch=B, seq=S)
+    rwte = torch.zeros(V, d, device="cuda").index_add_(0, tok.long(), dx)
+    assert torch.allclose(dwte, rwte, atol=1e-5)
+    assert torch.allclose(dwpe, dx.view(B, S, d).sum(0), atol=1e-5)
+
+
+def test_cross_entropy(ops):
+    torch.manual_seed(8)
+    M, V, Vp = 300, 50257, 50304
+    logits = torch.randn(M, Vp, device="cuda") * 3
+    labels = torch.randint(0, V, (M,), device="cuda", dtype=torch.int32)
+    dl = torch.empty(M, Vp, device="cuda", dtype=torch.bfloat16)
+    loss = torch.zeros(1, device="cuda", dtype=torch.float64)
+    ops.cross_entropy(logits, labels, V, dl, loss, 0.5)
+    x = logits[:, :V].clone().requires_grad_(True)
+    ref = torch.nn.functional.cross_entropy(x, labels.long(), reduction="sum")
+    (ref * 0.5).backward()
+    assert abs(loss.item() - ref.item()) / ref.item() < 1e-5
+    assert _rel(dl[:, :V], x.grad) < 1e-2
+    assert dl[:, V:].abs().max().item() == 0
+
+
+def test_bias_grad_and_cast(ops):
+    torch.manual_seed(9)
+    dy = _bf(4096, 6400)
+    db = torch.ones(6400, device="cuda")
+    ops.bias_grad(dy, db)
+    assert _rel(db, dy.float().sum(0) + 1) < 1e-5
+    dyf = torch.randn(1000, 1600, device="cuda")
+    db2 = torch.zeros(1600, device="cuda")
+    ops.bias_grad(dyf, db2)
+    assert _rel(db2, dyf.sum(0)) < 1e-5
+    src = torch.randn(1_000_001, device="cuda")
+    dst = torch.empty(1_000_001, device="cuda", dtype=torch.bfloat16)
+    ops.cast_bf16(src, dst)
+    assert torch.equal(dst, src.to(torch.bfloat16))

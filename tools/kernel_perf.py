@@ -1,0 +1,102 @@
+"""Micro-benchmarks of the sm_100a kernels (CUDA events, warm-up, L2 flush).
+
+    python tools/kernel_perf.py [gemm|adam|all]
+Prints one JSON line per shape with achieved TFLOP/s or GB/s and the fraction
+of MEASURED_PEAKS.json.
+"""
+
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2202_01306_b200 import ops  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["bf16_tflops"], d["hbm_gbs"], "measured"
+    return 1590.0, 6650.0, "fallback"
+
+
+FLUSH = None
+
+
+def flush():
+    global FLUSH
+    if FLUSH is None:
+        FLUSH = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    FLUSH.zero_()
+
+
+def timeit(fn, iters=20, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(iters):
+        flush()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        fn()
+        e.record()
+        torch.cuda.synchronize()
+        ts.append(s.elapsed_time(e))
+    ts.sort()
+    return ts[len(ts) // 2]
+
+
+def bench_gemm():
+    tf_peak, _, kind = peaks()
+    shapes = [("fwd_qkv", 4096, 4800, 1600, False, False, "bf16"),
+              ("fwd_fc1", 4096, 6400, 1600, False, False, "gelu_bf16"),
+              ("fwd_fc2", 4096, 1600, 6400, False, False, "resid_f32"),
+              ("dgrad_fc1", 4096, 1600, 6400, False, True, "f32"),
+              ("wgrad_fc1", 6400, 1600, 4096, True, True, "acc_f32"),
+              ("square8k", 8192, 8192, 8192, False, False, "bf16"),
+              ("fwd_40b_qkv", 4096, 24576, 8192, False, False, "bf16")]
+    for name, M, N, K, amn, bmn, epi in shapes:
+        a = torch.randn(*((K, M) if amn else (M, K)), device="cuda").to(torch.bfloat16)
+        b = torch.randn(*((K, N) if bmn else (N, K)), device="cuda").to(torch.bfloat16)
+        f32 = epi in ("f32", "acc_f32", "resid_f32")
+        d = torch.zeros(M, N, device="cuda", dtype=torch.float32 if f32 else torch.bfloat16)
+        bias = torch.zeros(N, device="cuda") if epi not in ("acc_f32", "dgelu_bf16") else None
+        aux = None
+        if epi == "resid_f32":
+            aux = torch.zeros(M, N, device="cuda")
+        if epi == "gelu_bf16":
+            aux = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+        ms = timeit(lambda: ops.gemm(a, b, d, a_mn=amn, b_mn=bmn, epi=epi, bias=bias, aux=aux))
+        tf = 2 * M * N * K / ms / 1e9
+        ref_ms = None
+        if not amn and not bmn:
+            ref_ms = timeit(lambda: torch.matmul(a, b.t()))
+        print(json.dumps({"kernel": "gemm", "shape": name, "M": M, "N": N, "K": K, "ms": round(ms, 4),
+                          "tflops": round(tf, 1), "frac": round(tf / tf_peak, 3), "peak": kind,
+                          "cublas_ms": None if ref_ms is None else round(ref_ms, 4)}), flush=True)
+
+
+def bench_adam():
+    _, hbm, kind = peaks()
+    n = 256 << 20
+    w = torch.zeros(n, device="cuda")
+    g = torch.zeros(n, device="cuda")
+    k = torch.zeros(2 * n, device="cuda")
+    ms = timeit(lambda: ops.adam(w, g, k, lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, step=1))
+    gbs = 28 * n / ms / 1e6
+    print(json.dumps({"kernel": "adam", "params": n, "ms": round(ms, 4), "GBps": round(gbs, 1),
+                      "frac": round(gbs / hbm, 3), "peak": kind}), flush=True)
+
+
+if __name__ == "__main__":
+    what = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if what in ("gemm", "all"):
+        bench_gemm()
+    if what in ("adam", "all"):
+        bench_adam()
