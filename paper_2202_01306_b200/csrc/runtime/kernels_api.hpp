@@ -1,0 +1,32 @@
+// kernels_api.hpp -- internal C++ entry points of the kernels (csrc/kernels/*.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace hm {
+int adam_launch(float *w, const float *g, float *k, int64_t n, float lr, float b1, float b2, float eps, int step,
+                float gscale, cudaStream_t s);
+namespace gemm {
+int run(const void *A, const void *B, void *D, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldd,
+        int a_mn, int b_mn, int epi, const float *bias, void *aux, int64_t ld_aux, cudaStream_t stream, int force_bn);
+}
+namespace attn {
+int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int DH, int causal, cudaStream_t s);
+int backward(const void *qkv, const void *o, const void *dout, const float *lse, float *dvec, float *dq_acc,
+             void *dqkv, int B, int S, int H, int DH, int causal, cudaStream_t s);
+}
+namespace layers {
+int cast_f32_bf16(const float *src, void *dst, int64_t n, cudaStream_t s);
+int embed_fwd(const int32_t *tok, const float *wte, const float *wpe, float *out, int B, int S, int d, cudaStream_t s);
+int embed_bwd(const int32_t *tok, const float *dx, float *dwte, float *dwpe, int B, int S, int d, cudaStream_t s);
+int ln_fwd(const float *x, const float *g, const float *b, void *y, float *mean, float *rstd, int64_t rows, int d,
+           cudaStream_t s);
+int ln_bwd(const float *dy, const float *x, const float *mean, const float *rstd, const float *g, const float *resid,
+           float *out, void *out_bf, float *dg, float *db, int64_t rows, int d, cudaStream_t s);
+int cross_entropy(const float *logits, const int32_t *labels, int64_t rows, int64_t ldl, int V, void *dlogits,
+                  double *loss_sum, float scale, cudaStream_t s);
+int bias_grad(const void *dy, int is_bf16, float *db, int64_t rows, int n, int64_t ld, cudaStream_t s);
+}  // namespace layers
+}  // namespace hm

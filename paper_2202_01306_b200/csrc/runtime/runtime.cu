@@ -1,0 +1,949 @@
+// runtime.cu -- the Harmony runtime on one B200.
+//
+// Executes the swap plan built by plan.cpp (the same items the estimator
+// prices) for the tasks bound to this rank's GPU:
+//   * swap engine: pinned host arenas (W fp32, K = Adam (m,v), stash),
+//     H2D on the swap-in stream, D2H on the swap-out stream, every transfer
+//     gated by CUDA events on exactly the plan's dependencies, including the
+//     one-task-ahead prefetch window (an input may start once the previous
+//     task on the device has *started* computing -- simulator.py:262-269);
+//   * layer-pack compute on the compute stream (tcgen05 GEMMs, flash
+//     attention, LayerNorm, CE) with activation recompute for non-shared
+//     backward packs and group-wide gradient accumulation in the pack's
+//     GPU-resident dW buffer;
+//   * the jit UPD task: fused Adam on the update stream, overlapping the next
+//     backward task, followed by W and K swap-out.
+// Device memory is one pool allocated at load time and checked against
+// alpha; slots are reused round-robin and every reuse waits on the event
+// that ends the previous occupant's last use.
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "../plan.hpp"
+#include "common.hpp"
+#include "kernels_api.hpp"
+
+namespace hm {
+
+using bf16 = __nv_bfloat16;
+
+static inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+struct ParamLayout {  // float offsets inside one layer's parameter block; -1 = absent
+  int64_t wte = -1, wpe = -1, ln1_g, ln1_b, w_qkv, b_qkv, w_proj, b_proj, ln2_g, ln2_b, w_fc1, b_fc1, w_fc2, b_fc2;
+  int64_t lnf_g = -1, lnf_b = -1, w_head = -1, size = 0;
+};
+
+// Per-layer activation pointers for one member (u samples) inside a store.
+struct Acts {
+  float *x, *mean1, *rstd1, *lse, *h1, *mean2, *rstd2;
+  bf16 *ln1, *qkv, *o, *ln2, *hpre, *a;
+  float *yl, *meanf, *rstdf;  // head layer only
+  bf16 *lnf, *dlog;
+};
+
+struct Scratch {
+  bf16 *dy_bf, *dh, *dh1_bf, *dout, *dqkv;
+  float *dln, *dh1, *dvec, *dq, *dyh, *g[2], *h[2], *logits, *tmp;
+};
+
+struct Slots {
+  std::vector<float *> w;
+  std::vector<bf16 *> wsh;
+  std::vector<float *> dw;
+  std::vector<float *> k;
+  std::vector<uint8_t *> stash_in;
+};
+
+struct TaskRt {
+  int w_slot = -1, dw_slot = -1, k_slot = -1, stash_slot = -1;
+  int carry_in = -1, carry_out = -1;  // F: hidden carry; B: gradient carry
+  bool store_shared = false;          // F task keeping activations for the shared B
+  bool from_shared = false;           // B task reading the shared store
+  int64_t params = 0;                 // pack parameter count
+  int b_task = -1;                    // U: its B task
+  std::vector<int> members;           // member compute item ids
+  std::vector<int64_t> s0;            // member sample offsets
+  std::set<int> stash_heads;          // F: layers whose input is stashed
+};
+
+struct Action {
+  int item = -1;
+  int kind = 0;  // 0 = F/B member, 1 = U Adam, 2 = H2D, 3 = D2H, 4 = D2D
+  cudaStream_t stream = nullptr;
+  void *dst = nullptr;
+  const void *src = nullptr;
+  int64_t bytes = 0;
+  int task = -1, member = -1;
+  std::vector<std::pair<int, bool>> waits;  // (item, at_start)
+};
+
+}  // namespace hm
+
+struct hm_runtime {
+  int device = 0;
+  hm_model m{};
+  int64_t alpha = 0;
+  int D = 0, S = 0, H = 0, DH = 0, R = 0, V = 0, Vp = 0;
+  int64_t total_params = 0;
+  std::vector<hm::ParamLayout> lay;
+  std::vector<int64_t> w_off;  // floats, per layer, + total at [R]
+  cudaStream_t s_compute = nullptr, s_h2d = nullptr, s_d2h = nullptr, s_update = nullptr, s_p2p_in = nullptr,
+               s_p2p_out = nullptr;
+  float *w_host = nullptr, *k_host = nullptr;
+  uint8_t *stash_host = nullptr;
+  int64_t stash_host_bytes = 0;
+  // plan
+  hm::Plan *plan = nullptr;
+  int rank = 0;
+  int minibatch = 0;  // samples this rank processes
+  int64_t global_tokens = 0;
+  std::vector<hm::TaskRt> trt;
+  std::vector<hm::Action> actions;
+  std::vector<cudaEvent_t> ev_start, ev_end;
+  cudaEvent_t ev_iter0 = nullptr, ev_iter1 = nullptr;
+  // device pool
+  uint8_t *pool = nullptr;
+  int64_t pool_bytes = 0;
+  hm::Slots slots;
+  float *carry[2] = {nullptr, nullptr};
+  float *dcarry[2] = {nullptr, nullptr};
+  std::map<int, uint8_t *> stash_dev;      // head layer -> device buffer
+  std::map<int, int64_t> stash_host_off;   // head layer -> host arena offset
+  uint8_t *shared_store = nullptr;
+  int shared_lo = -1, shared_hi = -1;
+  uint8_t *work_store = nullptr;
+  hm::Scratch T{};
+  int32_t *tokens = nullptr, *labels = nullptr;
+  double *loss_dev = nullptr;
+  int step = 0;
+  // last iteration
+  std::vector<hm_item> ledger, trace;
+  int64_t counters[8] = {0};
+};
+
+namespace hm {
+
+// ---------------------------------------------------------------------------
+// model layout
+// ---------------------------------------------------------------------------
+static ParamLayout make_layout(const hm_runtime &rt, int L) {
+  const int64_t d = rt.m.d_model, v = rt.Vp, s = rt.S;
+  ParamLayout p;
+  int64_t o = 0;
+  if (L == 0) {
+    p.wte = o; o += v * d;
+    p.wpe = o; o += s * d;
+  }
+  p.ln1_g = o; o += d;
+  p.ln1_b = o; o += d;
+  p.w_qkv = o; o += 3 * d * d;
+  p.b_qkv = o; o += 3 * d;
+  p.w_proj = o; o += d * d;
+  p.b_proj = o; o += d;
+  p.ln2_g = o; o += d;
+  p.ln2_b = o; o += d;
+  p.w_fc1 = o; o += 4 * d * d;
+  p.b_fc1 = o; o += 4 * d;
+  p.w_fc2 = o; o += 4 * d * d;
+  p.b_fc2 = o; o += d;
+  if (L == rt.R - 1) {
+    p.lnf_g = o; o += d;
+    p.lnf_b = o; o += d;
+    p.w_head = o; o += v * d;
+  }
+  p.size = o;
+  return p;
+}
+
+// per-sample bytes of each stored tensor, in store order
+static std::vector<int64_t> act_sizes(const hm_runtime &rt, bool head) {
+  const int64_t S = rt.S, d = rt.m.d_model, H = rt.H;
+  std::vector<int64_t> v = {S * d * 4, S * 4, S * 4, S * H * 4, S * d * 4, S * 4, S * 4,        // x mean1 rstd1 lse h1 mean2 rstd2
+                            S * d * 2, S * 3 * d * 2, S * d * 2, S * d * 2, S * 4 * d * 2, S * 4 * d * 2};  // ln1 qkv o ln2 hpre a
+  if (head) {
+    v.push_back(S * d * 4);           // yl
+    v.push_back(S * 4);               // meanf
+    v.push_back(S * 4);               // rstdf
+    v.push_back(S * d * 2);           // lnf
+    v.push_back(S * (int64_t)rt.Vp * 2);  // dlog
+  }
+  return v;
+}
+
+static int64_t store_layer_bytes(const hm_runtime &rt, bool head, int64_t n) {
+  int64_t b = 0;
+  for (int64_t s : act_sizes(rt, head)) b += align_up(n * s, 256);
+  return b;
+}
+
+static Acts acts_at(const hm_runtime &rt, uint8_t *base, bool head, int64_t n, int64_t s0) {
+  auto sz = act_sizes(rt, head);
+  uint8_t *p = base;
+  uint8_t *r[18] = {nullptr};
+  for (size_t i = 0; i < sz.size(); ++i) {
+    r[i] = p + s0 * sz[i];
+    p += align_up(n * sz[i], 256);
+  }
+  Acts A{};
+  A.x = (float *)r[0]; A.mean1 = (float *)r[1]; A.rstd1 = (float *)r[2]; A.lse = (float *)r[3];
+  A.h1 = (float *)r[4]; A.mean2 = (float *)r[5]; A.rstd2 = (float *)r[6];
+  A.ln1 = (bf16 *)r[7]; A.qkv = (bf16 *)r[8]; A.o = (bf16 *)r[9]; A.ln2 = (bf16 *)r[10];
+  A.hpre = (bf16 *)r[11]; A.a = (bf16 *)r[12];
+  if (head) {
+    A.yl = (float *)r[13]; A.meanf = (float *)r[14]; A.rstdf = (float *)r[15];
+    A.lnf = (bf16 *)r[16]; A.dlog = (bf16 *)r[17];
+  }
+  return A;
+}
+
+static uint8_t *store_layer(const hm_runtime &rt, uint8_t *base, int lo, int L, int64_t n) {
+  uint8_t *p = base;
+  for (int j = lo; j < L; ++j) p += store_layer_bytes(rt, j == rt.R - 1, n);
+  return p;
+}
+
+// ---------------------------------------------------------------------------
+// layer compute
+// ---------------------------------------------------------------------------
+struct LayerW {
+  const float *w;   // fp32 master (for LN params, biases, embedding)
+  const bf16 *wsh;  // bf16 shadow (GEMM operands)
+  float *dw;        // gradient block (fp32)
+  const ParamLayout *p;
+};
+
+static LayerW layer_weights(hm_runtime &rt, const TaskRt &tr, int lo, int L, int w_slot, int dw_slot) {
+  LayerW lw;
+  const int64_t off = rt.w_off[L] - rt.w_off[lo];
+  lw.w = rt.slots.w[w_slot] + off;
+  lw.wsh = rt.slots.wsh[w_slot] + off;
+  lw.dw = dw_slot >= 0 ? rt.slots.dw[dw_slot] + off : nullptr;
+  lw.p = &rt.lay[L];
+  (void)tr;
+  return lw;
+}
+
+static int block_fwd(hm_runtime &rt, const Acts &A, const float *x, float *y, int u, const LayerW &W) {
+  const int64_t M = (int64_t)u * rt.S, d = rt.m.d_model;
+  cudaStream_t s = rt.s_compute;
+  const ParamLayout &P = *W.p;
+  HM_TRY(layers::ln_fwd(x, W.w + P.ln1_g, W.w + P.ln1_b, A.ln1, A.mean1, A.rstd1, M, (int)d, s));
+  HM_TRY(gemm::run(A.ln1, W.wsh + P.w_qkv, A.qkv, M, 3 * d, d, d, d, 3 * d, 0, 0, HM_EPI_STORE_BF16, W.w + P.b_qkv,
+                   nullptr, 0, s, 0));
+  HM_TRY(attn::forward(A.qkv, A.o, A.lse, u, rt.S, rt.H, rt.DH, rt.m.causal, s));
+  HM_TRY(gemm::run(A.o, W.wsh + P.w_proj, A.h1, M, d, d, d, d, d, 0, 0, HM_EPI_RESID_F32, W.w + P.b_proj,
+                   const_cast<float *>(x), d, s, 0));
+  HM_TRY(layers::ln_fwd(A.h1, W.w + P.ln2_g, W.w + P.ln2_b, A.ln2, A.mean2, A.rstd2, M, (int)d, s));
+  HM_TRY(gemm::run(A.ln2, W.wsh + P.w_fc1, A.a, M, 4 * d, d, d, d, 4 * d, 0, 0, HM_EPI_GELU_BF16, W.w + P.b_fc1,
+                   A.hpre, 4 * d, s, 0));
+  HM_TRY(gemm::run(A.a, W.wsh + P.w_fc2, y, M, d, 4 * d, 4 * d, 4 * d, d, 0, 0, HM_EPI_RESID_F32, W.w + P.b_fc2,
+                   A.h1, d, s, 0));
+  return HM_OK;
+}
+
+// LN_f + LM head + cross-entropy (dlogits stored for the backward pass).
+static int head_fwd(hm_runtime &rt, const Acts &A, int u, int64_t s0, const LayerW &W) {
+  const int64_t M = (int64_t)u * rt.S, d = rt.m.d_model;
+  cudaStream_t s = rt.s_compute;
+  const ParamLayout &P = *W.p;
+  HM_TRY(layers::ln_fwd(A.yl, W.w + P.lnf_g, W.w + P.lnf_b, A.lnf, A.meanf, A.rstdf, M, (int)d, s));
+  HM_TRY(gemm::run(A.lnf, W.wsh + P.w_head, rt.T.logits, M, rt.Vp, d, d, d, rt.Vp, 0, 0, HM_EPI_STORE_F32, nullptr,
+                   nullptr, 0, s, 0));
+  HM_TRY(layers::cross_entropy(rt.T.logits, rt.labels + s0 * rt.S, M, rt.Vp, rt.V, A.dlog, rt.loss_dev,
+                               (float)(1.0 / (double)rt.global_tokens), s));
+  return HM_OK;
+}
+
+static int head_bwd(hm_runtime &rt, const Acts &A, int u, const LayerW &W) {
+  const int64_t M = (int64_t)u * rt.S, d = rt.m.d_model, Vp = rt.Vp;
+  cudaStream_t s = rt.s_compute;
+  const ParamLayout &P = *W.p;
+  Scratch &T = rt.T;
+  HM_TRY(gemm::run(A.dlog, W.wsh + P.w_head, T.dln, M, d, Vp, Vp, d, d, 0, 1, HM_EPI_STORE_F32, nullptr, nullptr, 0,
+                   s, 0));
+  HM_TRY(gemm::run(A.dlog, A.lnf, W.dw + P.w_head, Vp, d, M, Vp, d, d, 1, 1, HM_EPI_ACC_F32, nullptr, nullptr, 0, s,
+                   0));
+  HM_TRY(layers::ln_bwd(T.dln, A.yl, A.meanf, A.rstdf, W.w + P.lnf_g, nullptr, T.dyh, nullptr, W.dw + P.lnf_g,
+                        W.dw + P.lnf_b, M, (int)d, s));
+  return HM_OK;
+}
+
+static int block_bwd(hm_runtime &rt, const Acts &A, const float *x, const float *dy, float *dx, int u,
+                     const LayerW &W) {
+  const int64_t M = (int64_t)u * rt.S, d = rt.m.d_model;
+  cudaStream_t s = rt.s_compute;
+  const ParamLayout &P = *W.p;
+  Scratch &T = rt.T;
+  HM_TRY(layers::cast_f32_bf16(dy, T.dy_bf, M * d, s));
+  HM_TRY(layers::bias_grad(dy, 0, W.dw + P.b_fc2, M, (int)d, d, s));
+  HM_TRY(gemm::run(T.dy_bf, A.a, W.dw + P.w_fc2, d, 4 * d, M, d, 4 * d, 4 * d, 1, 1, HM_EPI_ACC_F32, nullptr,
+                   nullptr, 0, s, 0));
+  HM_TRY(gemm::run(T.dy_bf, W.wsh + P.w_fc2, T.dh, M, 4 * d, d, d, 4 * d, 4 * d, 0, 1, HM_EPI_DGELU_BF16, nullptr,
+                   A.hpre, 4 * d, s, 0));
+  HM_TRY(layers::bias_grad(T.dh, 1, W.dw + P.b_fc1, M, (int)(4 * d), 4 * d, s));
+  HM_TRY(gemm::run(T.dh, A.ln2, W.dw + P.w_fc1, 4 * d, d, M, 4 * d, d, d, 1, 1, HM_EPI_ACC_F32, nullptr, nullptr, 0,
+                   s, 0));
+  HM_TRY(gemm::run(T.dh, W.wsh + P.w_fc1, T.dln, M, d, 4 * d, 4 * d, d, d, 0, 1, HM_EPI_STORE_F32, nullptr, nullptr,
+                   0, s, 0));
+  HM_TRY(layers::ln_bwd(T.dln, A.h1, A.mean2, A.rstd2, W.w + P.ln2_g, dy, T.dh1, T.dh1_bf, W.dw + P.ln2_g,
+                        W.dw + P.ln2_b, M, (int)d, s));
+  HM_TRY(layers::bias_grad(T.dh1, 0, W.dw + P.b_proj, M, (int)d, d, s));
+  HM_TRY(gemm::run(T.dh1_bf, A.o, W.dw + P.w_proj, d, d, M, d, d, d, 1, 1, HM_EPI_ACC_F32, nullptr, nullptr, 0, s, 0));
+  HM_TRY(gemm::run(T.dh1_bf, W.wsh + P.w_proj, T.dout, M, d, d, d, d, d, 0, 1, HM_EPI_STORE_BF16, nullptr, nullptr, 0,
+                   s, 0));
+  HM_TRY(attn::backward(A.qkv, A.o, T.dout, A.lse, T.dvec, T.dq, T.dqkv, u, rt.S, rt.H, rt.DH, rt.m.causal, s));
+  HM_TRY(layers::bias_grad(T.dqkv, 1, W.dw + P.b_qkv, M, (int)(3 * d), 3 * d, s));
+  HM_TRY(gemm::run(T.dqkv, A.ln1, W.dw + P.w_qkv, 3 * d, d, M, 3 * d, d, d, 1, 1, HM_EPI_ACC_F32, nullptr, nullptr, 0,
+                   s, 0));
+  HM_TRY(gemm::run(T.dqkv, W.wsh + P.w_qkv, T.dln, M, d, 3 * d, 3 * d, d, d, 0, 1, HM_EPI_STORE_F32, nullptr, nullptr,
+                   0, s, 0));
+  HM_TRY(layers::ln_bwd(T.dln, x, A.mean1, A.rstd1, W.w + P.ln1_g, T.dh1, dx, nullptr, W.dw + P.ln1_g,
+                        W.dw + P.ln1_b, M, (int)d, s));
+  return HM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// task members
+// ---------------------------------------------------------------------------
+static bool is_head(const hm_runtime &rt, int L) { return L == rt.R - 1; }
+
+// Forward of layers [lo, hi] for one member.  `store` != null keeps every
+// layer's activations (n samples, member at s0); otherwise one scratch layer
+// slot is reused and the hidden state ping-pongs between two buffers.
+static int forward_pack(hm_runtime &rt, TaskRt &tr, int lo, int hi, int u, int64_t s0, const float *x_in,
+                        const int32_t *tok_in, uint8_t *store, int64_t n, int64_t s_off, float *y_final) {
+  const int64_t M = (int64_t)u * rt.S, d = rt.m.d_model;
+  cudaStream_t s = rt.s_compute;
+  const float *x = x_in;
+  int hsel = 0;
+  for (int L = lo; L <= hi; ++L) {
+    const bool head = is_head(rt, L);
+    Acts A = store ? acts_at(rt, store_layer(rt, store, lo, L, n), head, n, s_off)
+                   : acts_at(rt, rt.work_store, head, u, 0);
+    LayerW W = layer_weights(rt, tr, lo, L, tr.w_slot, -1);
+    if (L == lo) {
+      float *dst = store ? A.x : rt.T.h[hsel];
+      if (L == 0) {
+        HM_TRY(layers::embed_fwd(tok_in, W.w + W.p->wte, W.w + W.p->wpe, dst, u, rt.S, (int)d, s));
+        x = dst;
+      } else if (store) {
+        HM_CUDA(cudaMemcpyAsync(dst, x_in, M * d * 4, cudaMemcpyDeviceToDevice, s));
+        x = dst;
+      }
+    }
+    if (tr.stash_heads.count(L)) {  // capture the input of a backward-pack head
+      uint8_t *dst = rt.stash_dev.at(L);
+      if (L == 0) {
+        HM_CUDA(cudaMemcpyAsync(dst + s0 * rt.S * 4, tok_in, M * 4, cudaMemcpyDeviceToDevice, s));
+      } else {
+        HM_CUDA(cudaMemcpyAsync(dst + s0 * rt.S * d * 4, x, M * d * 4, cudaMemcpyDeviceToDevice, s));
+      }
+    }
+    float *y;
+    if (head) {
+      y = store ? A.yl : rt.T.tmp;
+    } else if (L < hi) {
+      y = store ? acts_at(rt, store_layer(rt, store, lo, L + 1, n), is_head(rt, L + 1), n, s_off).x : rt.T.h[hsel ^ 1];
+    } else {
+      y = y_final ? y_final : rt.T.tmp;
+    }
+    HM_TRY(block_fwd(rt, A, x, y, u, W));
+    if (head) {
+      Acts Ah = A;
+      if (!store) Ah.yl = y;
+      HM_TRY(head_fwd(rt, Ah, u, s0, W));
+      if (y_final) HM_CUDA(cudaMemcpyAsync(y_final, y, M * d * 4, cudaMemcpyDeviceToDevice, s));
+    }
+    x = y;
+    hsel ^= 1;
+  }
+  return HM_OK;
+}
+
+static int backward_pack(hm_runtime &rt, TaskRt &tr, int lo, int hi, int u, int64_t s0, uint8_t *store, int64_t n,
+                         int64_t s_off, const float *dy_in, float *dx_out, const int32_t *tok_in) {
+  const float *dy = dy_in;
+  for (int L = hi; L >= lo; --L) {
+    const bool head = is_head(rt, L);
+    Acts A = acts_at(rt, store_layer(rt, store, lo, L, n), head, n, s_off);
+    LayerW W = layer_weights(rt, tr, lo, L, tr.w_slot, tr.dw_slot);
+    if (head) {
+      HM_TRY(head_bwd(rt, A, u, W));
+      dy = rt.T.dyh;
+    }
+    if (!dy) return fail(HM_ERR_INTERNAL, "backward without an incoming gradient");
+    float *dx = (L == lo && dx_out) ? dx_out : rt.T.g[(hi - L) & 1];
+    HM_TRY(block_bwd(rt, A, A.x, dy, dx, u, W));
+    dy = dx;
+    if (L == 0)
+      HM_TRY(layers::embed_bwd(tok_in, dy, W.dw + W.p->wte, W.dw + W.p->wpe, u, rt.S, (int)rt.m.d_model,
+                               rt.s_compute));
+  }
+  (void)s0;
+  return HM_OK;
+}
+
+static int run_member(hm_runtime &rt, int task, int g) {
+  TaskInfo &t = rt.plan->tasks[task];
+  TaskRt &tr = rt.trt[task];
+  const int u = t.group[g];
+  const int64_t s0 = tr.s0[g];
+  const int64_t d = rt.m.d_model;
+  const int64_t rowsd = (int64_t)rt.S * d;
+  cudaStream_t s = rt.s_compute;
+  if (g == 0) {
+    // bf16 operand copy of the pack's master weights, right after swap-in
+    HM_TRY(layers::cast_f32_bf16(rt.slots.w[tr.w_slot], rt.slots.wsh[tr.w_slot], tr.params, s));
+    if (t.type == HM_TASK_B) HM_CUDA(cudaMemsetAsync(rt.slots.dw[tr.dw_slot], 0, tr.params * 4, s));
+  }
+  if (t.type == HM_TASK_F) {
+    const float *x_in = t.lo == 0 ? nullptr : rt.carry[tr.carry_in] + s0 * rowsd;
+    const int32_t *tok = rt.tokens + s0 * rt.S;
+    if (tr.store_shared)
+      return forward_pack(rt, tr, t.lo, t.hi, u, s0, x_in, tok, rt.shared_store, rt.minibatch, s0, nullptr);
+    float *y = tr.carry_out >= 0 ? rt.carry[tr.carry_out] + s0 * rowsd : nullptr;
+    return forward_pack(rt, tr, t.lo, t.hi, u, s0, x_in, tok, nullptr, 0, 0, y);
+  }
+  // backward
+  float *dx = (t.lo == 0) ? nullptr : rt.dcarry[tr.carry_out] + s0 * rowsd;
+  if (tr.from_shared)
+    return backward_pack(rt, tr, t.lo, t.hi, u, s0, rt.shared_store, rt.minibatch, s0, nullptr, dx,
+                         rt.tokens + s0 * rt.S);
+  // recompute from the stash, keeping activations in the work store
+  uint8_t *st = rt.slots.stash_in[tr.stash_slot];
+  const float *x_in = t.lo == 0 ? nullptr : reinterpret_cast<const float *>(st) + s0 * rowsd;
+  const int32_t *tok = t.lo == 0 ? reinterpret_cast<const int32_t *>(st) + s0 * rt.S : rt.tokens + s0 * rt.S;
+  HM_TRY(forward_pack(rt, tr, t.lo, t.hi, u, s0, x_in, tok, rt.work_store, u, 0, nullptr));
+  const float *dy = rt.dcarry[tr.carry_in] + s0 * rowsd;
+  return backward_pack(rt, tr, t.lo, t.hi, u, s0, rt.work_store, u, 0, dy, dx, tok);
+}
+
+// ---------------------------------------------------------------------------
+// load: slots, buffers, actions
+// ---------------------------------------------------------------------------
+static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
+  rt.plan = plan;
+  rt.rank = rank;
+  rt.minibatch = minibatch;
+  const int n_tasks = (int)plan->tasks.size();
+  rt.trt.assign(n_tasks, TaskRt{});
+  const int64_t d = rt.m.d_model;
+  // ---- which tasks run here; structural checks ------------------------------
+  std::vector<int> mine;
+  for (auto &t : plan->tasks)
+    if (t.dev_id == rank) mine.push_back(t.index);
+  if (mine.empty()) return fail(HM_ERR_VALIDATION, "no task is bound to this rank");
+  for (auto &it : plan->items) {
+    if (it.rec.gpu != rank) continue;
+    if (!it.rec.is_compute && it.rec.channel == HM_PEER2PEER)
+      return fail(HM_ERR_VALIDATION, "peer-to-peer hand-offs (Harmony-PP with N>1) are not executed by this build yet");
+  }
+  int last_f = -1, shared_b = -1;
+  int64_t u_max = 1, pmax = 0;
+  std::vector<int> heads;  // stash head layers produced here
+  for (int ti : mine) {
+    TaskInfo &t = plan->tasks[ti];
+    TaskRt &tr = rt.trt[ti];
+    tr.params = rt.w_off[t.hi + 1] - rt.w_off[t.lo];
+    pmax = std::max(pmax, tr.params);
+    int64_t acc = 0;
+    for (int u : t.group) {
+      tr.s0.push_back(acc);
+      acc += u;
+      u_max = std::max<int64_t>(u_max, u);
+    }
+    if (t.type != HM_TASK_U && acc != minibatch)
+      return fail(HM_ERR_VALIDATION, "task group does not cover this rank's minibatch");
+    if (t.type == HM_TASK_F) last_f = ti;
+    if (t.type == HM_TASK_B && !t.recompute) shared_b = ti;
+    for (auto &e : t.outputs)
+      if (e.tensor == HM_SX && e.channel == HM_MESSAGE_PASSING) {
+        tr.stash_heads.insert(e.layer);
+        heads.push_back(e.layer);
+      }
+  }
+  if (last_f < 0 || shared_b < 0) return fail(HM_ERR_VALIDATION, "rank holds no complete F/B chain");
+  if (plan->tasks[last_f].lo != plan->tasks[shared_b].lo || plan->tasks[last_f].hi != plan->tasks[shared_b].hi)
+    return fail(HM_ERR_VALIDATION, "shared pack mismatch");
+  rt.trt[last_f].store_shared = true;
+  rt.trt[shared_b].from_shared = true;
+  rt.shared_lo = plan->tasks[last_f].lo;
+  rt.shared_hi = plan->tasks[last_f].hi;
+  for (auto &t : plan->tasks)
+    if (t.dev_id == rank && t.hi == rt.R - 1 && t.type != HM_TASK_U && !(t.index == last_f || t.index == shared_b))
+      return fail(HM_ERR_INTERNAL, "head layer outside the shared pack");
+
+  // ---- slot assignment (round robin in device order) -------------------------
+  const int NW = 3, NDW = 2, NK = 2, NST = 2;
+  int wn = 0, dwn = 0, kn = 0, stn = 0, fcur = -1, bcur = -1;
+  std::vector<int> w_owner(NW, -1), dw_owner(NDW, -1), k_owner(NK, -1), st_owner(NST, -1);
+  int64_t stash_in_max = 0;
+  std::map<int, int64_t> stash_bytes;  // head -> D * x bytes
+  for (int L : heads) stash_bytes[L] = (int64_t)minibatch * rt.S * (L == 0 ? 4 : d * 4);
+  for (int ti : mine) {
+    TaskInfo &t = plan->tasks[ti];
+    TaskRt &tr = rt.trt[ti];
+    if (t.type == HM_TASK_U) {
+      tr.b_task = ti - 1;
+      tr.k_slot = kn;
+      kn = (kn + 1) % NK;
+      continue;
+    }
+    tr.w_slot = wn;
+    wn = (wn + 1) % NW;
+    if (t.type == HM_TASK_F) {
+      tr.carry_in = fcur;
+      if (ti != last_f) {
+        tr.carry_out = (fcur + 1) & 1;
+        fcur = tr.carry_out;
+      }
+      if (t.lo > 0 && tr.carry_in < 0) return fail(HM_ERR_INTERNAL, "F task without an input carry");
+    } else {
+      tr.dw_slot = dwn;
+      dwn = (dwn + 1) % NDW;
+      tr.carry_in = bcur;
+      if (t.lo > 0) {
+        tr.carry_out = (bcur + 1) & 1;
+        bcur = tr.carry_out;
+      }
+      if (t.recompute) {
+        tr.stash_slot = stn;
+        stn = (stn + 1) % NST;
+        stash_in_max = std::max(stash_in_max, stash_bytes.count(t.lo) ? stash_bytes[t.lo] : 0);
+        if (tr.carry_in < 0) return fail(HM_ERR_INTERNAL, "recompute B task without a gradient carry");
+      }
+    }
+  }
+  // ---- device pool ------------------------------------------------------------
+  const int64_t rows_mb = (int64_t)minibatch * rt.S;
+  const int64_t rows_u = u_max * rt.S;
+  int64_t max_recompute_layers = 1;
+  for (int ti : mine) {
+    auto &t = plan->tasks[ti];
+    if (t.type == HM_TASK_B && t.recompute) max_recompute_layers = std::max<int64_t>(max_recompute_layers, t.hi - t.lo + 1);
+  }
+  int64_t work_bytes = 0;
+  for (int j = 0; j < max_recompute_layers; ++j) work_bytes += store_layer_bytes(rt, false, u_max);
+  work_bytes = std::max(work_bytes, store_layer_bytes(rt, true, u_max));
+  int64_t shared_bytes = 0;
+  for (int L = rt.shared_lo; L <= rt.shared_hi; ++L) shared_bytes += store_layer_bytes(rt, is_head(rt, L), minibatch);
+  struct Req { void **ptr; int64_t bytes; };
+  std::vector<Req> req;
+  rt.slots.w.assign(NW, nullptr);
+  rt.slots.wsh.assign(NW, nullptr);
+  rt.slots.dw.assign(NDW, nullptr);
+  rt.slots.k.assign(NK, nullptr);
+  rt.slots.stash_in.assign(NST, nullptr);
+  for (int i = 0; i < NW; ++i) {
+    req.push_back({(void **)&rt.slots.w[i], pmax * 4});
+    req.push_back({(void **)&rt.slots.wsh[i], pmax * 2});
+  }
+  for (int i = 0; i < NDW; ++i) req.push_back({(void **)&rt.slots.dw[i], pmax * 4});
+  for (int i = 0; i < NK; ++i) req.push_back({(void **)&rt.slots.k[i], pmax * 8});
+  for (int i = 0; i < NST; ++i) req.push_back({(void **)&rt.slots.stash_in[i], std::max<int64_t>(stash_in_max, 256)});
+  for (int i = 0; i < 2; ++i) {
+    req.push_back({(void **)&rt.carry[i], rows_mb * d * 4});
+    req.push_back({(void **)&rt.dcarry[i], rows_mb * d * 4});
+  }
+  std::vector<std::pair<int, uint8_t **>> stash_ptrs;
+  for (auto &kv : stash_bytes) {
+    rt.stash_dev[kv.first] = nullptr;
+  }
+  for (auto &kv : rt.stash_dev) req.push_back({(void **)&kv.second, stash_bytes[kv.first]});
+  req.push_back({(void **)&rt.shared_store, shared_bytes});
+  req.push_back({(void **)&rt.work_store, work_bytes});
+  Scratch &T = rt.T;
+  req.push_back({(void **)&T.dy_bf, rows_u * d * 2});
+  req.push_back({(void **)&T.dh, rows_u * 4 * d * 2});
+  req.push_back({(void **)&T.dh1_bf, rows_u * d * 2});
+  req.push_back({(void **)&T.dout, rows_u * d * 2});
+  req.push_back({(void **)&T.dqkv, rows_u * 3 * d * 2});
+  req.push_back({(void **)&T.dln, rows_u * d * 4});
+  req.push_back({(void **)&T.dh1, rows_u * d * 4});
+  req.push_back({(void **)&T.dvec, rows_u * rt.H * 4});
+  req.push_back({(void **)&T.dq, rows_u * d * 4});
+  req.push_back({(void **)&T.dyh, rows_u * d * 4});
+  req.push_back({(void **)&T.g[0], rows_u * d * 4});
+  req.push_back({(void **)&T.g[1], rows_u * d * 4});
+  req.push_back({(void **)&T.h[0], rows_u * d * 4});
+  req.push_back({(void **)&T.h[1], rows_u * d * 4});
+  req.push_back({(void **)&T.tmp, rows_u * d * 4});
+  req.push_back({(void **)&T.logits, rows_u * rt.Vp * 4});
+  req.push_back({(void **)&rt.tokens, rows_mb * 4});
+  req.push_back({(void **)&rt.labels, rows_mb * 4});
+  req.push_back({(void **)&rt.loss_dev, 256});
+  int64_t total = 0;
+  for (auto &r : req) total += align_up(r.bytes, 1024);
+  if (total > rt.alpha)
+    return fail(HM_ERR_CAPACITY, "runtime needs " + std::to_string(total) + " device bytes > alpha " +
+                                     std::to_string(rt.alpha));
+  if (rt.pool) {
+    cudaFree(rt.pool);
+    rt.pool = nullptr;
+  }
+  HM_CUDA(cudaMalloc(&rt.pool, total));
+  rt.pool_bytes = total;
+  int64_t off = 0;
+  for (auto &r : req) {
+    *r.ptr = rt.pool + off;
+    off += align_up(r.bytes, 1024);
+  }
+  HM_CUDA(cudaMemset(rt.pool, 0, total));
+  // host stash arena
+  int64_t sh = 0;
+  rt.stash_host_off.clear();
+  for (auto &kv : stash_bytes) {
+    rt.stash_host_off[kv.first] = sh;
+    sh += align_up(kv.second, 4096);
+  }
+  if (sh > rt.stash_host_bytes) {
+    if (rt.stash_host) cudaFreeHost(rt.stash_host);
+    rt.stash_host = nullptr;
+    HM_CUDA(cudaHostAlloc(&rt.stash_host, std::max<int64_t>(sh, 4096), cudaHostAllocDefault));
+    rt.stash_host_bytes = sh;
+  }
+
+  // ---- actions ----------------------------------------------------------------
+  rt.actions.clear();
+  for (auto &e : rt.ev_start) cudaEventDestroy(e);
+  for (auto &e : rt.ev_end) cudaEventDestroy(e);
+  rt.ev_start.assign(plan->items.size(), nullptr);
+  rt.ev_end.assign(plan->items.size(), nullptr);
+  for (size_t i = 0; i < plan->items.size(); ++i) {
+    if (plan->items[i].rec.gpu != rank) continue;
+    HM_CUDA(cudaEventCreate(&rt.ev_start[i]));
+    HM_CUDA(cudaEventCreate(&rt.ev_end[i]));
+  }
+  for (auto &t : plan->tasks)
+    if (t.dev_id == rank) rt.trt[t.index].members = plan->member_computes[t.index];
+  // last-use item of each slot occupant (for reuse gating)
+  auto w_release = [&](int ti) -> int {
+    TaskInfo &t = plan->tasks[ti];
+    if (t.type == HM_TASK_F) return rt.trt[ti].members.back();
+    // B task: its U task's W swap-out (or U compute)
+    int u = ti + 1;
+    int last = rt.trt[u].members.back();
+    for (size_t i = 0; i < plan->items.size(); ++i) {
+      auto &r = plan->items[i].rec;
+      if (r.task == u && !r.is_compute && r.stage == 2 && r.tensor == HM_W) last = (int)i;
+    }
+    return last;
+  };
+  auto k_release = [&](int ui) -> int {
+    int last = rt.trt[ui].members.back();
+    for (size_t i = 0; i < plan->items.size(); ++i) {
+      auto &r = plan->items[i].rec;
+      if (r.task == ui && !r.is_compute && r.stage == 2 && r.tensor == HM_K) last = (int)i;
+    }
+    return last;
+  };
+  std::vector<int> w_prev(NW, -1), dw_prev(NDW, -1), k_prev(NK, -1), st_prev(NST, -1);
+  std::map<int, int> w_wait, dw_wait, k_wait, st_wait;  // task -> item to wait (end) before reuse
+  // wrap-around: the first occupants wait on the last occupants of the previous iteration
+  std::vector<int> order;
+  for (int pass = 0; pass < 2; ++pass)
+    for (int ti : mine) {
+      TaskRt &tr = rt.trt[ti];
+      TaskInfo &t = plan->tasks[ti];
+      if (t.type != HM_TASK_U) {
+        if (w_prev[tr.w_slot] >= 0 && pass == 1) w_wait[ti] = w_release(w_prev[tr.w_slot]);
+        w_prev[tr.w_slot] = ti;
+        if (t.type == HM_TASK_B) {
+          if (dw_prev[tr.dw_slot] >= 0 && pass == 1) dw_wait[ti] = rt.trt[dw_prev[tr.dw_slot] + 1].members.back();
+          dw_prev[tr.dw_slot] = ti;
+          if (tr.stash_slot >= 0) {
+            if (st_prev[tr.stash_slot] >= 0 && pass == 1) st_wait[ti] = rt.trt[st_prev[tr.stash_slot]].members.back();
+            st_prev[tr.stash_slot] = ti;
+          }
+        }
+      } else {
+        if (k_prev[tr.k_slot] >= 0 && pass == 1) k_wait[ti] = k_release(k_prev[tr.k_slot]);
+        k_prev[tr.k_slot] = ti;
+      }
+    }
+  for (size_t i = 0; i < plan->items.size(); ++i) {
+    const hm_item &r = plan->items[i].rec;
+    if (r.gpu != rank) continue;
+    Action a;
+    a.item = (int)i;
+    a.task = r.task;
+    a.member = r.member;
+    for (auto &dp : plan->items[i].deps)
+      if (plan->items[dp.first].rec.gpu == rank) a.waits.push_back(dp);
+    TaskInfo &t = plan->tasks[r.task];
+    TaskRt &tr = rt.trt[r.task];
+    if (r.is_compute) {
+      if (t.type == HM_TASK_U) {
+        a.kind = 1;
+        a.stream = rt.s_update;
+      } else {
+        a.kind = 0;
+        a.stream = rt.s_compute;
+        if (r.member == 0 && dw_wait.count(r.task)) a.waits.push_back({dw_wait[r.task], false});
+      }
+    } else if (r.stage == 0) {
+      a.kind = 2;
+      a.stream = rt.s_h2d;
+      a.bytes = r.nbytes;
+      if (r.channel == HM_CPU_GPU_SWAP && r.tensor == HM_W) {
+        a.src = rt.w_host + rt.w_off[t.lo];
+        a.dst = rt.slots.w[tr.w_slot];
+        if (r.nbytes != tr.params * 4) return fail(HM_ERR_INTERNAL, "W swap-in size disagrees with the model layout");
+        if (w_wait.count(r.task)) a.waits.push_back({w_wait[r.task], false});
+      } else if (r.channel == HM_CPU_GPU_SWAP && r.tensor == HM_K) {
+        a.src = rt.k_host + 2 * rt.w_off[t.lo];
+        a.dst = rt.slots.k[tr.k_slot];
+        if (r.nbytes != tr.params * 8) return fail(HM_ERR_INTERNAL, "K swap-in size disagrees with the model layout");
+        if (k_wait.count(r.task)) a.waits.push_back({k_wait[r.task], false});
+      } else if (r.channel == HM_MESSAGE_PASSING && r.tensor == HM_SX) {
+        if (!rt.stash_host_off.count(r.layer)) return fail(HM_ERR_INTERNAL, "stash-in of an unknown head");
+        a.src = rt.stash_host + rt.stash_host_off[r.layer];
+        a.dst = rt.slots.stash_in[tr.stash_slot];
+        if (r.nbytes != stash_bytes[r.layer]) return fail(HM_ERR_INTERNAL, "stash-in size disagrees with x(L)");
+        if (st_wait.count(r.task)) a.waits.push_back({st_wait[r.task], false});
+      } else {
+        return fail(HM_ERR_VALIDATION, "unsupported input transfer in plan");
+      }
+    } else {
+      a.kind = 3;
+      a.stream = rt.s_d2h;
+      a.bytes = r.nbytes;
+      if (r.channel == HM_CPU_GPU_SWAP && r.tensor == HM_W) {
+        TaskRt &bt = rt.trt[tr.b_task];
+        a.src = rt.slots.w[bt.w_slot];
+        a.dst = rt.w_host + rt.w_off[t.lo];
+      } else if (r.channel == HM_CPU_GPU_SWAP && r.tensor == HM_K) {
+        a.src = rt.slots.k[tr.k_slot];
+        a.dst = rt.k_host + 2 * rt.w_off[t.lo];
+      } else if (r.channel == HM_MESSAGE_PASSING && r.tensor == HM_SX) {
+        const int64_t per = rt.S * (r.layer == 0 ? 4 : d * 4);
+        const int64_t boff = tr.s0[r.member] * per;
+        a.src = rt.stash_dev.at(r.layer) + boff;
+        a.dst = rt.stash_host + rt.stash_host_off[r.layer] + boff;
+        if (r.nbytes != (int64_t)t.group[r.member] * per) return fail(HM_ERR_INTERNAL, "stash-out size disagrees");
+      } else {
+        return fail(HM_ERR_VALIDATION, "unsupported output transfer in plan");
+      }
+    }
+    rt.actions.push_back(std::move(a));
+  }
+  return HM_OK;
+}
+
+static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *labels, int is_device, double *loss) {
+  if (!rt.plan) return fail(HM_ERR_VALIDATION, "no plan loaded");
+  HM_CUDA(cudaSetDevice(rt.device));
+  const int64_t launches0 = launch_counter().load();
+  rt.step += 1;
+  cudaStream_t sc = rt.s_compute;
+  const int64_t tb = (int64_t)rt.minibatch * rt.S * 4;
+  HM_CUDA(cudaEventRecord(rt.ev_iter0, sc));
+  HM_CUDA(cudaMemcpyAsync(rt.tokens, tokens, tb, is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, sc));
+  HM_CUDA(cudaMemcpyAsync(rt.labels, labels, tb, is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, sc));
+  HM_CUDA(cudaMemsetAsync(rt.loss_dev, 0, sizeof(double), sc));
+  cudaStream_t others[] = {rt.s_h2d, rt.s_d2h, rt.s_update};
+  for (cudaStream_t o : others) HM_CUDA(cudaStreamWaitEvent(o, rt.ev_iter0, 0));
+  int64_t h2d = 0, d2h = 0;
+  for (Action &a : rt.actions) {
+    for (auto &w : a.waits) HM_CUDA(cudaStreamWaitEvent(a.stream, w.second ? rt.ev_start[w.first] : rt.ev_end[w.first], 0));
+    HM_CUDA(cudaEventRecord(rt.ev_start[a.item], a.stream));
+    switch (a.kind) {
+      case 0:
+        HM_TRY(run_member(rt, a.task, a.member));
+        break;
+      case 1: {
+        TaskRt &tr = rt.trt[a.task];
+        TaskRt &bt = rt.trt[tr.b_task];
+        HM_TRY(adam_launch(rt.slots.w[bt.w_slot], rt.slots.dw[bt.dw_slot], rt.slots.k[tr.k_slot], tr.params, rt.m.lr,
+                           rt.m.beta1, rt.m.beta2, rt.m.eps, rt.step, 1.0f, a.stream));
+        break;
+      }
+      case 2:
+        HM_CUDA(cudaMemcpyAsync(a.dst, a.src, a.bytes, cudaMemcpyHostToDevice, a.stream));
+        h2d += a.bytes;
+        break;
+      case 3:
+        HM_CUDA(cudaMemcpyAsync(a.dst, a.src, a.bytes, cudaMemcpyDeviceToHost, a.stream));
+        d2h += a.bytes;
+        break;
+      default:
+        return fail(HM_ERR_INTERNAL, "bad action");
+    }
+    HM_CUDA(cudaEventRecord(rt.ev_end[a.item], a.stream));
+  }
+  // join every stream into the compute stream, read the loss
+  for (cudaStream_t o : others) {
+    cudaEvent_t e;
+    HM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    HM_CUDA(cudaEventRecord(e, o));
+    HM_CUDA(cudaStreamWaitEvent(sc, e, 0));
+    cudaEventDestroy(e);
+  }
+  double loss_sum = 0;
+  HM_CUDA(cudaMemcpyAsync(&loss_sum, rt.loss_dev, sizeof(double), cudaMemcpyDeviceToHost, sc));
+  HM_CUDA(cudaEventRecord(rt.ev_iter1, sc));
+  HM_CUDA(cudaEventSynchronize(rt.ev_iter1));
+  if (loss) *loss = loss_sum / (double)rt.global_tokens;
+  // measured ledger and trace
+  rt.ledger.clear();
+  rt.trace.clear();
+  for (Action &a : rt.actions) {
+    hm_item rec = rt.plan->items[a.item].rec;
+    float t0 = 0, t1 = 0;
+    HM_CUDA(cudaEventElapsedTime(&t0, rt.ev_iter0, rt.ev_start[a.item]));
+    HM_CUDA(cudaEventElapsedTime(&t1, rt.ev_iter0, rt.ev_end[a.item]));
+    rec.start_ns = (int64_t)((double)t0 * 1e6);
+    rec.end_ns = (int64_t)((double)t1 * 1e6);
+    rec.duration_ns = rec.end_ns - rec.start_ns;
+    (rec.is_compute ? rt.trace : rt.ledger).push_back(rec);
+  }
+  float it_ms = 0;
+  HM_CUDA(cudaEventElapsedTime(&it_ms, rt.ev_iter0, rt.ev_iter1));
+  rt.counters[0] = launch_counter().load() - launches0;
+  rt.counters[1] = (int64_t)((double)it_ms * 1e6);
+  rt.counters[2] = rt.pool_bytes;
+  rt.counters[3] = h2d;
+  rt.counters[4] = d2h;
+  rt.counters[5] = 0;
+  return HM_OK;
+}
+
+}  // namespace hm
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+hm_runtime *hm_runtime_create(int32_t device, const hm_model *model, int64_t alpha_bytes, int32_t *status) {
+  auto bad = [&](int code, const std::string &msg) -> hm_runtime * {
+    hm::set_last_error(msg);
+    if (status) *status = code;
+    return nullptr;
+  };
+  if (!model) return bad(HM_ERR_VALIDATION, "null model");
+  if (model->d_model % model->n_head) return bad(HM_ERR_VALIDATION, "d_model % n_head != 0");
+  const int dh = model->d_model / model->n_head;
+  if (dh != 64 && dh != 128) return bad(HM_ERR_VALIDATION, "head_dim must be 64 or 128");
+  if (model->seq_len % 64 || model->d_model % 64) return bad(HM_ERR_VALIDATION, "seq_len and d_model must be multiples of 64");
+  if (model->vocab_padded % 8 || model->vocab_padded < model->vocab) return bad(HM_ERR_VALIDATION, "bad padded vocab");
+  if (cudaSetDevice(device) != cudaSuccess) return bad(HM_ERR_DEVICE, "cudaSetDevice failed");
+  auto rt = std::make_unique<hm_runtime>();
+  rt->device = device;
+  rt->m = *model;
+  rt->alpha = alpha_bytes;
+  rt->R = model->n_layer;
+  rt->S = model->seq_len;
+  rt->H = model->n_head;
+  rt->DH = dh;
+  rt->V = model->vocab;
+  rt->Vp = model->vocab_padded;
+  rt->w_off.assign(rt->R + 1, 0);
+  for (int L = 0; L < rt->R; ++L) {
+    rt->lay.push_back(hm::make_layout(*rt, L));
+    rt->w_off[L + 1] = rt->w_off[L] + rt->lay.back().size;
+  }
+  rt->total_params = rt->w_off[rt->R];
+  cudaStream_t *ss[] = {&rt->s_compute, &rt->s_h2d, &rt->s_d2h, &rt->s_update, &rt->s_p2p_in, &rt->s_p2p_out};
+  for (auto p : ss)
+    if (cudaStreamCreateWithFlags(p, cudaStreamNonBlocking) != cudaSuccess) return bad(HM_ERR_DEVICE, "stream create");
+  cudaEventCreate(&rt->ev_iter0);
+  cudaEventCreate(&rt->ev_iter1);
+  if (cudaHostAlloc(&rt->w_host, rt->total_params * 4, cudaHostAllocDefault) != cudaSuccess ||
+      cudaHostAlloc(&rt->k_host, rt->total_params * 8, cudaHostAllocDefault) != cudaSuccess)
+    return bad(HM_ERR_DEVICE, "pinned host arena allocation failed (" + std::to_string(rt->total_params * 12) + " B)");
+  std::memset(rt->k_host, 0, rt->total_params * 8);
+  if (status) *status = HM_OK;
+  return rt.release();
+}
+
+void *hm_runtime_arena(hm_runtime *rt, int32_t kind, int64_t *bytes) {
+  if (!rt) return nullptr;
+  if (kind == HM_ARENA_W) {
+    if (bytes) *bytes = rt->total_params * 4;
+    return rt->w_host;
+  }
+  if (kind == HM_ARENA_K) {
+    if (bytes) *bytes = rt->total_params * 8;
+    return rt->k_host;
+  }
+  if (bytes) *bytes = rt->stash_host_bytes;
+  return rt->stash_host;
+}
+
+int hm_runtime_layer_offsets(const hm_runtime *rt, int64_t *w_off, int32_t cap) {
+  if (!rt || cap < rt->R + 1) return hm::fail(HM_ERR_VALIDATION, "layer offsets buffer too small");
+  for (int i = 0; i <= rt->R; ++i) w_off[i] = rt->w_off[i];
+  return rt->R + 1;
+}
+
+int hm_runtime_load_plan(hm_runtime *rt, hm_plan *plan, int32_t rank, int32_t minibatch) {
+  if (!rt || !plan) return hm::fail(HM_ERR_VALIDATION, "null argument");
+  if (cudaSetDevice(rt->device) != cudaSuccess) return hm::fail(HM_ERR_DEVICE, "cudaSetDevice");
+  int64_t global = 0;
+  for (auto &t : plan->p->tasks) (void)t;
+  // global tokens = minibatch of the whole job: sum over ranks' F groups of task 0 of each rank
+  std::map<int, int64_t> per_rank;
+  for (auto &t : plan->p->tasks)
+    if (t.type == HM_TASK_F && (t.lo == 0)) {
+      int64_t s = 0;
+      for (int u : t.group) s += u;
+      per_rank[t.dev_id] += s;
+    }
+  for (auto &kv : per_rank) global += kv.second;
+  rt->global_tokens = global * rt->S;
+  return hm::load_plan(*rt, plan->p, rank, minibatch);
+}
+
+int hm_runtime_run_iteration(hm_runtime *rt, const int32_t *tokens, const int32_t *labels, int32_t is_device,
+                             double *loss_out) {
+  if (!rt) return hm::fail(HM_ERR_VALIDATION, "null runtime");
+  return hm::run_iteration(*rt, tokens, labels, is_device, loss_out);
+}
+
+int32_t hm_runtime_ledger_count(const hm_runtime *rt) { return rt ? (int32_t)rt->ledger.size() : 0; }
+int hm_runtime_ledger(const hm_runtime *rt, hm_item *out, int32_t cap) {
+  if (!rt || cap < (int32_t)rt->ledger.size()) return hm::fail(HM_ERR_VALIDATION, "ledger buffer too small");
+  std::copy(rt->ledger.begin(), rt->ledger.end(), out);
+  return (int)rt->ledger.size();
+}
+int32_t hm_runtime_trace_count(const hm_runtime *rt) { return rt ? (int32_t)rt->trace.size() : 0; }
+int hm_runtime_trace(const hm_runtime *rt, hm_item *out, int32_t cap) {
+  if (!rt || cap < (int32_t)rt->trace.size()) return hm::fail(HM_ERR_VALIDATION, "trace buffer too small");
+  std::copy(rt->trace.begin(), rt->trace.end(), out);
+  return (int)rt->trace.size();
+}
+int hm_runtime_counters(const hm_runtime *rt, int64_t *out, int32_t cap) {
+  if (!rt) return hm::fail(HM_ERR_VALIDATION, "null runtime");
+  const int n = cap < 8 ? cap : 8;
+  for (int i = 0; i < n; ++i) out[i] = rt->counters[i];
+  return n;
+}
+
+void hm_runtime_free(hm_runtime *rt) {
+  if (!rt) return;
+  cudaSetDevice(rt->device);
+  cudaDeviceSynchronize();
+  for (auto &e : rt->ev_start) if (e) cudaEventDestroy(e);
+  for (auto &e : rt->ev_end) if (e) cudaEventDestroy(e);
+  if (rt->ev_iter0) cudaEventDestroy(rt->ev_iter0);
+  if (rt->ev_iter1) cudaEventDestroy(rt->ev_iter1);
+  if (rt->pool) cudaFree(rt->pool);
+  if (rt->w_host) cudaFreeHost(rt->w_host);
+  if (rt->k_host) cudaFreeHost(rt->k_host);
+  if (rt->stash_host) cudaFreeHost(rt->stash_host);
+  cudaStream_t ss[] = {rt->s_compute, rt->s_h2d, rt->s_d2h, rt->s_update, rt->s_p2p_in, rt->s_p2p_out};
+  for (auto s : ss) if (s) cudaStreamDestroy(s);
+  delete rt;
+}
+
+}  // extern "C"

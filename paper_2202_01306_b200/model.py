@@ -116,7 +116,7 @@ class GPTSpec:
                    + 2 * 4 * d)  # gelu out bf16
         b = s * per_tok
         if L == self.n_layer - 1:
-            b += s * (2 * d + 8 + 4 * self.vocab_padded)  # lnf out, stats, logits fp32
+            b += s * (4 * d + 2 * d + 8 + 2 * self.vocab_padded)  # block out, lnf out, stats, dlogits
         return b
 
 
@@ -169,3 +169,14 @@ def gpt_machine(gpu_count: int = 1, alpha_bytes: int = 160 << 30,
     return MachineModel(gpu_count=gpu_count, gpu_mem_capacity=int(alpha_bytes),
                         pcie_bandwidth=int(pcie_gbs), root_link_bandwidth=int(root_gbs),
                         p2p_bandwidth=int(nvlink_gbs))
+
+
+def synthetic_batch(spec: GPTSpec, samples: int, seed: int = 1234):
+    """Synthetic minibatch: tokens i.i.d. uniform in [0, V)
+    from torch.Generator().manual_seed(seed); labels = tokens shifted by one."""
+    import numpy as np
+    import torch
+    g = torch.Generator().manual_seed(seed)
+    seq = torch.randint(0, spec.vocab, (samples, spec.seq_len + 1), generator=g, dtype=torch.int64)
+    return (np.ascontiguousarray(seq[:, :-1].numpy().astype(np.int32)),
+            np.ascontiguousarray(seq[:, 1:].numpy().astype(np.int32)))

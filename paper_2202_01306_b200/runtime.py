@@ -1,0 +1,200 @@
+"""``execute``: run a task graph on the GPU through the native runtime.
+
+Drop-in sibling of :func:`paper_2202_01306_b200.simulator.simulate`
+(`pkg/src/wrapsched/simulator.py:378-434` is the reference's estimate of the
+same iteration).  The returned ``SimReport`` is built from CUDA events of the
+executed iteration; its ledger rows, byte volumes and per-GPU volumes equal
+``simulate``'s because the runtime executes the same native plan.
+
+One ``HarmonyRuntime`` per process and GPU.  Model state lives in the
+runtime's pinned host arenas (W fp32, K = Adam (m, v) interleaved): the GPU
+only ever holds the packs the schedule swaps in.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as NL
+from .core import MachineModel, gpu_shares
+from .errors import ValidationError
+from .lowering import NativePlan
+from .model import GPTSpec
+from .profiler import ProfileSet
+from .simulator import SimReport, report_from_items
+from .taskgraph import TaskGraph
+
+
+class HarmonyRuntime:
+    """Native runtime for one GPU: arenas, streams, kernels, plan executor."""
+
+    def __init__(self, spec: GPTSpec, *, alpha_bytes: int, device: int = 0, lr: float = 1e-4,
+                 betas: tuple[float, float] = (0.9, 0.999), eps: float = 1e-8) -> None:
+        self.spec = spec
+        self.lib = NL.lib()
+        m = NL.hm_model(spec.n_layer, spec.d_model, spec.n_head, spec.seq_len, spec.vocab,
+                        spec.vocab_padded, 1 if spec.causal else 0, 0, lr, betas[0], betas[1], eps)
+        self._model = m
+        st = C.c_int32(0)
+        h = self.lib.hm_runtime_create(device, C.byref(m), int(alpha_bytes), C.byref(st))
+        if not h:
+            NL.check(st.value or -4)
+        self.handle = h
+        self.alpha_bytes = int(alpha_bytes)
+        offs = (C.c_int64 * (spec.n_layer + 1))()
+        NL.check(self.lib.hm_runtime_layer_offsets(h, offs, spec.n_layer + 1))
+        self.w_off = np.array(offs[:], dtype=np.int64)
+        for L in range(spec.n_layer):
+            if self.w_off[L + 1] - self.w_off[L] != spec.layer_params(L):
+                raise ValidationError(f"native layout of layer {L} disagrees with GPTSpec")
+        self.w = self._arena(0, np.float32)
+        self.k = self._arena(1, np.float32)
+        self.plan: NativePlan | None = None
+        self.graph: TaskGraph | None = None
+        self.rank = 0
+        self.samples = 0
+
+    def _arena(self, kind: int, dtype) -> np.ndarray:
+        nbytes = C.c_int64(0)
+        ptr = self.lib.hm_runtime_arena(self.handle, kind, C.byref(nbytes))
+        n = nbytes.value // np.dtype(dtype).itemsize
+        return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_float)), shape=(n,))
+
+    # -- state ----------------------------------------------------------------
+    def layer_params(self, L: int) -> dict[str, np.ndarray]:
+        """Views of layer L's master weights in the W arena, by segment name."""
+        out, o = {}, int(self.w_off[L])
+        for name, n in self.spec.layer_segments(L):
+            out[name] = self.w[o:o + n]
+            o += n
+        return out
+
+    def init_weights(self, seed: int = 0) -> None:
+        """N(0, 0.02) matrices/embeddings, LayerNorm gamma=1 / beta=0, zero
+        biases, zero padded vocabulary rows; Adam state zero."""
+        import torch
+        gen = torch.Generator().manual_seed(seed)
+        V, d = self.spec.vocab, self.spec.d_model
+        for L in range(self.spec.n_layer):
+            for name, view in self.layer_params(L).items():
+                if name.endswith("_g"):
+                    view[:] = 1.0
+                elif name.startswith("b_") or name.endswith("_b"):
+                    view[:] = 0.0
+                else:
+                    t = torch.empty(view.size, dtype=torch.float32).normal_(0.0, 0.02, generator=gen)
+                    view[:] = t.numpy()
+                    if name in ("wte", "w_head"):
+                        view.reshape(-1, d)[V:] = 0.0
+        self.k[:] = 0.0
+
+    # -- plan -------------------------------------------------------------------
+    def load(self, graph: TaskGraph, machine: MachineModel, profiles: ProfileSet, rank: int = 0) -> None:
+        if graph.config is None:
+            raise ValidationError("execute needs a scheduler-generated graph")
+        if machine.gpu_count != graph.machine.gpu_count:
+            raise ValidationError("machine does not match the graph's GPU count")
+        plan = NativePlan(graph, machine, profiles)
+        if graph.mode.value == "dp":
+            samples = gpu_shares(graph.minibatch, machine.gpu_count)[rank]
+        else:
+            samples = graph.minibatch
+        NL.check(self.lib.hm_runtime_load_plan(self.handle, plan.handle, rank, samples))
+        self.plan, self.graph, self.rank, self.samples = plan, graph, rank, samples
+        self.machine = machine
+
+    def sample_range(self) -> tuple[int, int]:
+        """Global sample indices this rank processes."""
+        if self.graph is not None and self.graph.mode.value == "dp":
+            sh = gpu_shares(self.graph.minibatch, self.machine.gpu_count)
+            lo = sum(sh[:self.rank])
+            return lo, lo + sh[self.rank]
+        return 0, self.samples
+
+    def step(self, tokens, labels) -> float:
+        """One training iteration on this rank's samples.  ``tokens`` /
+        ``labels`` are [samples, seq] int32: numpy (host) or torch CUDA."""
+        if self.plan is None:
+            raise ValidationError("load() a plan first")
+        loss = C.c_double(0.0)
+        if hasattr(tokens, "is_cuda") and tokens.is_cuda:
+            rc = self.lib.hm_runtime_run_iteration(self.handle, C.c_void_p(tokens.data_ptr()),
+                                                   C.c_void_p(labels.data_ptr()), 1, C.byref(loss))
+        else:
+            t = np.ascontiguousarray(tokens, dtype=np.int32)
+            lb = np.ascontiguousarray(labels, dtype=np.int32)
+            if t.shape != (self.samples, self.spec.seq_len):
+                raise ValidationError(f"tokens must be [{self.samples}, {self.spec.seq_len}]")
+            rc = self.lib.hm_runtime_run_iteration(self.handle, t.ctypes.data, lb.ctypes.data, 0,
+                                                   C.byref(loss))
+        NL.check(rc)
+        return loss.value
+
+    def counters(self) -> dict:
+        out = (C.c_int64 * 8)()
+        NL.check(self.lib.hm_runtime_counters(self.handle, out, 8))
+        return {"kernels": out[0], "iteration_ns": out[1], "device_bytes": out[2],
+                "h2d_bytes": out[3], "d2h_bytes": out[4], "p2p_bytes": out[5]}
+
+    def measured_items(self) -> np.ndarray:
+        n1 = self.lib.hm_runtime_ledger_count(self.handle)
+        n2 = self.lib.hm_runtime_trace_count(self.handle)
+        a = np.zeros(n1, dtype=NL.ITEM_DTYPE)
+        b = np.zeros(n2, dtype=NL.ITEM_DTYPE)
+        if n1:
+            NL.check(self.lib.hm_runtime_ledger(self.handle, a.ctypes.data, n1))
+        if n2:
+            NL.check(self.lib.hm_runtime_trace(self.handle, b.ctypes.data, n2))
+        return np.concatenate([b, a])
+
+    def report(self) -> SimReport:
+        """SimReport of the last executed iteration (measured CUDA events)."""
+        items = self.measured_items()
+        c = self.counters()
+        return report_from_items(self.graph, self.machine, items, c["iteration_ns"], measured=True)
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            if self.plan is not None:
+                self.plan.close()
+            self.lib.hm_runtime_free(self.handle)
+            self.handle = None
+
+    def __del__(self) -> None:
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def execute(graph: TaskGraph, machine: MachineModel | None = None, profiles: ProfileSet | None = None, *,
+            model, batch, steps: int = 1, check_memory: bool = True, rank: int = 0) -> SimReport:
+    """Run ``steps`` training iterations of ``graph`` and report the last one.
+
+    ``model`` is a :class:`HarmonyRuntime` (state kept across calls) or a
+    :class:`GPTSpec` (a runtime with alpha = ``machine.gpu_mem_capacity`` and
+    seed-0 weights is created).  ``batch`` = (tokens, labels), each
+    [samples, seq] int32.  Capacity is enforced by the runtime's device pool
+    (CapacityViolationError if the plan's buffers exceed alpha)."""
+    machine = machine or graph.machine
+    if profiles is None:
+        raise ValidationError("profiles are required")
+    if check_memory:
+        from .simulator import check_memory_fit
+        check_memory_fit(graph, machine, profiles)
+    rt = model
+    if isinstance(model, GPTSpec):
+        rt = HarmonyRuntime(model, alpha_bytes=machine.gpu_mem_capacity)
+        rt.init_weights(0)
+    if rt.graph is not graph:
+        rt.load(graph, machine, profiles, rank)
+    tokens, labels = batch
+    losses = [rt.step(tokens, labels) for _ in range(steps)]
+    rep = rt.report()
+    rep.caveats = rep.caveats + (f"loss={losses[-1]:.6f}",)
+    return rep
+
+
+Runtime = HarmonyRuntime

@@ -1,0 +1,97 @@
+"""End-to-end runtime on the GPU: executed swap ledger == simulate's ledger
+(bit-exact) and loss / weights / Adam state vs the torch-CPU fp32 oracle.
+
+Tolerances (bf16 tensor-core operands, fp32 accumulate, fp32 master state):
+loss within 2e-3 relative per step; weights and Adam moments within 1e-3
+relative (L2 norm over the whole arena) after the steps."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2202_01306_b200 as H
+from paper_2202_01306_b200.model import GPT_PRESETS, GPTSpec, gpt_profiles, synthetic_batch
+
+pytestmark = pytest.mark.gpu
+
+LOSS_RTOL = 2e-3
+STATE_RTOL = 1e-3
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+def _run(spec, cfg, steps, n_gpus=1, alpha=16 << 30):
+    from oracle.gpt_cpu import GPTOracle
+    from paper_2202_01306_b200.runtime import HarmonyRuntime
+    prof = gpt_profiles(spec, u_max=64)
+    mach = H.MachineModel(gpu_count=n_gpus, gpu_mem_capacity=alpha, pcie_bandwidth=55_000_000_000)
+    g = H.generate_task_graph(cfg, mach, prof)
+    rt = HarmonyRuntime(spec, alpha_bytes=alpha)
+    rt.init_weights(0)
+    oracle = GPTOracle(spec, rt.w.copy(), rt.w_off)
+    rt.load(g, mach, prof)
+    tok, lab = synthetic_batch(spec, cfg.minibatch)
+    sim = H.simulate(g, mach, prof)
+    gb = g.tasks[-2].group  # groups of the last backward task
+    for i in range(steps):
+        loss = rt.step(tok, lab)
+        ref = oracle.step(tok, lab, list(g.tasks[0].group))
+        assert abs(loss - ref) / abs(ref) < LOSS_RTOL, (i, loss, ref)
+        rep = rt.report()
+        assert rep.ledger == sim.ledger
+        assert rep.channel_volumes == sim.channel_volumes
+        assert rep.tensor_volumes == sim.tensor_volumes
+    w_ref = oracle.w.numpy()
+    rel_w = np.linalg.norm(rt.w - w_ref) / np.linalg.norm(w_ref)
+    rel_m = np.linalg.norm(rt.k[0::2] - oracle.m.numpy()) / np.linalg.norm(oracle.m.numpy())
+    rel_v = np.linalg.norm(rt.k[1::2] - oracle.v.numpy()) / np.linalg.norm(oracle.v.numpy())
+    rt.close()
+    return rel_w, rel_m, rel_v, gb
+
+
+def test_tiny_c1_pp_matches_oracle():
+    spec = GPT_PRESETS["tiny"]
+    packs = ((0, 1), (2, 3))
+    cfg = H.Configuration(4, packs, 4, packs, 16, H.Mode.PP)
+    rel_w, rel_m, rel_v, _ = _run(spec, cfg, steps=10)
+    print("c1 rel", rel_w, rel_m, rel_v)
+    assert rel_w < STATE_RTOL
+    assert rel_m < 2e-2 and rel_v < 2e-2
+
+
+@pytest.mark.parametrize("pf,pb,uf,ub,d,mode", [
+    (((0, 0), (1, 1), (2, 3)), ((0, 1), (2, 3)), 4, 4, 8, "pp"),   # F pack holds a mid-pack stash head
+    (((0, 1), (2, 3)), ((0, 0), (1, 1), (2, 3)), 2, 4, 8, "pp"),   # u_f != u_b, three B packs
+    (((0, 3),), ((0, 3),), 3, 3, 8, "pp"),                         # single shared pack, remainder group
+    (((0, 1), (2, 3)), ((0, 1), (2, 3)), 4, 2, 8, "dp"),           # Harmony-DP at N=1
+])
+def test_tiny_schedules_match_oracle(pf, pb, uf, ub, d, mode):
+    spec = GPT_PRESETS["tiny"]
+    cfg = H.Configuration(uf, pf, ub, pb, d, H.Mode(mode))
+    rel_w, rel_m, rel_v, _ = _run(spec, cfg, steps=3)
+    assert rel_w < STATE_RTOL
+
+
+def test_bert_style_full_attention():
+    spec = GPTSpec(4, 256, 4, 128, 1024, causal=False, name="tiny-bert")
+    packs = ((0, 1), (2, 3))
+    cfg = H.Configuration(4, packs, 4, packs, 8, H.Mode.PP)
+    rel_w, _, _, _ = _run(spec, cfg, steps=3)
+    assert rel_w < STATE_RTOL
+
+
+def test_capacity_violation_raises():
+    from paper_2202_01306_b200.runtime import HarmonyRuntime
+    spec = GPT_PRESETS["tiny"]
+    prof = gpt_profiles(spec)
+    mach = H.MachineModel(gpu_count=1, gpu_mem_capacity=1 << 20, pcie_bandwidth=55_000_000_000)
+    packs = ((0, 1), (2, 3))
+    g = H.generate_task_graph(H.Configuration(4, packs, 4, packs, 16, H.Mode.PP), mach, prof)
+    rt = HarmonyRuntime(spec, alpha_bytes=1 << 20)
+    with pytest.raises(H.CapacityViolationError):
+        rt.load(g, mach, prof)
+    rt.close()
