@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""bench.py -- Harmony layer-pack training throughput on B200.
+
+Workload (BASELINE.json configs[2], the config the metric is quoted on at
+1/2/4/8 GPUs): GPT-2 XL (48 blocks, d=1600, 25 heads, seq 1024, V=50257,
+1.64 B params incl. untied head; W+dW+K = 26 GB) trained with Harmony-DP
+under a capped per-GPU memory budget alpha (default 32 GiB) so every pack's
+weights and Adam state are swapped through PCIe each iteration.  Weak
+scaling: 16 samples per GPU per iteration.  Synthetic data (tokens uniform
+in [0, V), seed 1234; weights N(0, 0.02), seed 0).
+
+One "step" = one full training iteration (all F/B/U tasks of the Harmony
+schedule: swap-in of every pack's W and K, F/B compute with recompute,
+fused Adam, swap-out of W and K).  Timing: the runtime's own CUDA events on
+its compute stream (all streams joined), max over ranks, after W warm-up
+steps.  Inputs are larger than L2 (model state streams from host memory every
+step).  ``value`` runs on device-resident tokens; ``e2e`` feeds tokens from
+pinned host memory and reads the loss back each step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (preset, samples_per_gpu, u, layers_per_pack, alpha_gib, mode)
+    "gpt2-xl-dp": ("gpt2-xl", 16, 4, 8, 32, "dp"),
+    "tiny": ("tiny", 16, 4, 2, 4, "pp"),
+}
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"bf16": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "bf16_burst": d["bf16_tflops"],
+                "hbm": d["hbm_gbs"], "kind": "measured"}
+    return {"bf16": 1400.0, "bf16_burst": 1590.0, "hbm": 6650.0, "kind": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def _max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _barrier(world: int) -> None:
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def _pcie_gbs():
+    """Measured pinned H2D / D2H GB/s of this GPU's link (1 GiB copies)."""
+    import torch
+    n = 1 << 30
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(n, dtype=torch.uint8, device="cuda")
+    out = {}
+    for name, fn in (("h2d", lambda: d.copy_(h, non_blocking=True)), ("d2h", lambda: h.copy_(d, non_blocking=True))):
+        fn()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(3):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        out[name] = 3 * n / (s.elapsed_time(e) / 1e3) / 1e9
+    del h, d
+    return out
+
+
+def step_flops(graph, spec) -> int:
+    """Algorithmic FLOPs of one iteration: F member
+    u*s*(24d^2+4sd) per block + 2*u*s*d*V for the head; B = 2F (+F recompute)."""
+    total = 0
+    for t in graph.tasks:
+        if t.type.value == "U":
+            continue
+        f = sum(spec.layer_fwd_flops(L, u) for L in range(t.pack[0], t.pack[1] + 1) for u in t.group)
+        total += f if t.type.value == "F" else (2 * f + (f if t.recompute else 0))
+    return total
+
+
+def cpu_port_sample(spec, threads: int, seconds_cap: float = 30.0) -> dict:
+    """Time the torch-CPU fp32 port (oracle/gpt_cpu.py) on a bounded sample:
+    one sample through a 2-layer model of the workload's shapes (embedding +
+    1 block + 1 block with LN_f/head), fwd + bwd + Adam, then scale by the
+    FLOP ratio to the full model's per-sample cost."""
+    import numpy as np
+    import torch
+    from oracle.gpt_cpu import GPTOracle
+    from paper_2202_01306_b200.model import GPTSpec, synthetic_batch
+    torch.set_num_threads(threads)
+    small = GPTSpec(2, spec.d_model, spec.n_head, spec.seq_len, spec.vocab, spec.causal, "cpu-sample")
+    n = small.total_params()
+    g = torch.Generator().manual_seed(0)
+    w = (torch.randn(n, generator=g) * 0.02).numpy()
+    off = np.cumsum([0] + [small.layer_params(L) for L in range(small.n_layer)])
+    o = GPTOracle(small, w, off)
+    tok, lab = synthetic_batch(small, 1)
+    o.step(tok, lab, [1])  # warm
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        o.step(tok, lab, [1])
+        reps += 1
+        if time.perf_counter() - t0 > min(seconds_cap, 10.0) or reps >= 5:
+            break
+    dt = (time.perf_counter() - t0) / reps
+    f_small = sum(small.layer_fwd_flops(L, 1) for L in range(2))
+    f_full = sum(spec.layer_fwd_flops(L, 1) for L in range(spec.n_layer))
+    per_sample = dt * f_full / f_small
+    return {"value": 1.0 / per_sample, "unit": "samples/s", "cores": threads, "kind": "port",
+            "sample": f"torch-CPU fp32 port (oracle/gpt_cpu.py), 1 sample x 2-layer {spec.name}-shaped model "
+                      f"(embedding, blocks, LN_f + head, Adam), {reps} reps of {dt:.2f} s, scaled by FLOPs "
+                      f"to {spec.n_layer} layers ({f_full / f_small:.1f}x)"}
+
+
+def run_reference(args) -> None:
+    world, rank, _ = _dist()
+    if rank != 0:
+        return
+    from paper_2202_01306_b200.model import GPT_PRESETS
+    preset, per_gpu, u, lpp, alpha_gib, mode = WORKLOADS[args.workload]
+    spec = GPT_PRESETS[preset]
+    threads = len(os.sched_getaffinity(0))
+    samples = []
+    for _ in range(max(1, args.steps)):
+        samples.append(cpu_port_sample(spec, threads, seconds_cap=20.0)["value"])
+    cb = cpu_port_sample(spec, threads, seconds_cap=20.0)
+    v = statistics.median(samples)
+    line = {"impl": "reference", "metric": "samples/s (Harmony layer-pack training, GPT-2 XL)", "value": v,
+            "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * per_gpu * args.gpus / v, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: {spec.name} Harmony-{mode.upper()} per-GPU minibatch {per_gpu}",
+                       "global_batch": per_gpu * args.gpus, "seq_len": spec.seq_len},
+            "cpu_baseline": dict(cb, value=v),
+            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_native(args) -> None:
+    import numpy as np
+    import torch
+
+    world, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2202_01306_b200 as H
+    from paper_2202_01306_b200 import ops
+    from paper_2202_01306_b200.model import GPT_PRESETS, gpt_machine, gpt_profiles, synthetic_batch
+    from paper_2202_01306_b200.runtime import HarmonyRuntime
+
+    preset, per_gpu, u, lpp, alpha_gib, mode = WORKLOADS[args.workload]
+    if args.alpha_gib:
+        alpha_gib = args.alpha_gib
+    spec = GPT_PRESETS[preset]
+    D = per_gpu * world
+    R = spec.n_layer
+    packs = tuple((i, min(i + lpp, R) - 1) for i in range(0, R, lpp))
+    cfg = H.Configuration(u, packs, u, packs, D, H.Mode(mode))
+    pcie = _pcie_gbs()
+    machine = gpt_machine(world, alpha_bytes=alpha_gib << 30, pcie_gbs=min(pcie["h2d"], pcie["d2h"]) * 1e9)
+    prof = gpt_profiles(spec)
+    graph = H.generate_task_graph(cfg, machine, prof)
+    sim = H.simulate(graph, machine, prof)
+    rt = HarmonyRuntime(spec, alpha_bytes=alpha_gib << 30, device=local)
+    rt.init_weights(0)
+    if world > 1:
+        import torch.distributed as dist
+        obj = [HarmonyRuntime.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        rt.init_comm(obj[0], world, rank)
+    rt.load(graph, machine, prof, rank=rank)
+    lo, hi = rt.sample_range()
+    tok_all, lab_all = synthetic_batch(spec, D)
+    tok, lab = tok_all[lo:hi], lab_all[lo:hi]
+    tok_d = torch.from_numpy(tok).cuda()
+    lab_d = torch.from_numpy(lab).cuda()
+    tok_p = torch.from_numpy(tok).pin_memory()
+    lab_p = torch.from_numpy(lab).pin_memory()
+
+    for i in range(args.warmup):
+        if i == args.warmup - 1:
+            rt.set_profiling(True)  # grow the profiler's event pool outside the timed region
+        rt.step(tok_d, lab_d)
+    _barrier(world)
+    torch.cuda.synchronize()
+    rt.set_profiling(True)  # reset stats, keep the event pool
+    launches0 = ops.launch_count()
+    its = []
+    losses = []
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            losses.append(rt.step(tok_d, lab_d))
+            its.append(rt.counters()["iteration_ns"])
+    torch.cuda.synchronize()
+    launches = ops.launch_count() - launches0
+    kstats = rt.kernel_stats()
+    rt.set_profiling(False)
+    cnt = rt.counters()
+    rep = rt.report()
+    # stream utilisation of the last timed iteration (measured CUDA events)
+    busy = {"h2d": 0, "d2h": 0, "compute": 0, "update": 0}
+    for e in rep.trace:
+        key = ("compute" if e.resource.endswith(".compute") else "update" if e.resource.endswith(".update")
+               else "h2d" if e.resource.endswith(".swap_in") else "d2h" if e.resource.endswith(".swap_out") else None)
+        if key:
+            busy[key] += e.end_ns - e.start_ns
+    util = {k: round(v / max(1, cnt["iteration_ns"]), 4) for k, v in busy.items()}
+    _barrier(world)
+    t_total = _max_over_ranks(sum(its) / 1e9, world)
+    # e2e: pinned host tokens -> device inside the iteration, loss read back
+    e2e_its = []
+    for _ in range(max(1, args.steps)):
+        rt.step(tok_p.numpy(), lab_p.numpy())
+        e2e_its.append(rt.counters()["iteration_ns"])
+    t_e2e = _max_over_ranks(sum(e2e_its) / 1e9, world)
+
+    samples_per_step = D
+    value = samples_per_step * args.steps / t_total
+    e2e_value = samples_per_step * len(e2e_its) / t_e2e
+    pk = _peaks()
+    # dominant kernel: the tcgen05 GEMM (tensor-bound)
+    g = kstats["gemm"]
+    gemm_tflops = g["flops"] / (g["ms"] / 1e3) / 1e12 if g["ms"] else 0.0
+    ad = kstats["adam"]
+    adam_gbs = ad["bytes"] / (ad["ms"] / 1e3) / 1e9 if ad["ms"] else 0.0
+    # iteration roofline: compute at tensor peak vs PCIe H2D / D2H at measured link bandwidth
+    flops = step_flops(graph, spec) / world
+    swap_in = sum(r[6] for r in sim.ledger if r[1] == 0 and r[4] in ("cpu_gpu_swap", "message_passing") and r[7] == rank)
+    swap_out = sum(r[6] for r in sim.ledger if r[1] == 2 and r[4] in ("cpu_gpu_swap", "message_passing") and r[7] == rank)
+    t_compute = flops / (pk["bf16"] * 1e12)
+    t_h2d = swap_in / (pcie["h2d"] * 1e9)
+    t_d2h = swap_out / (pcie["d2h"] * 1e9)
+    t_roof = max(t_compute, t_h2d, t_d2h)
+    ms_step = 1000.0 * t_total / args.steps
+    clk = clocks.summary()
+    share = {k: round(v["ms"] / (ms_step * args.steps), 4) for k, v in kstats.items()}
+    line = {
+        "metric": "samples/s (Harmony layer-pack training, GPT-2 XL)",
+        "value": round(value, 3),
+        "unit": "samples/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (tokens U[0,V) seed 1234; weights N(0,0.02) seed 0)",
+        "config": {"workload": f"{args.workload}: {spec.name} Harmony-{mode.upper()}, packs of {lpp} layers, "
+                               f"u_f=u_b={u}, alpha={alpha_gib} GiB/GPU",
+                   "global_batch": D, "seq_len": spec.seq_len, "parallelism": f"harmony-{mode}{world}",
+                   "l2": "inputs larger than L2 (W and K stream from host every step)"},
+        "swap_gb_per_iter": round((swap_in + swap_out) / 1e9, 3),
+        "swap_h2d_gb": round(swap_in / 1e9, 3), "swap_d2h_gb": round(swap_out / 1e9, 3),
+        "step_roofline": {"bound": "pcie" if t_roof > t_compute else "tensor", "t_roof_ms": round(1000 * t_roof, 2),
+                          "t_compute_ms": round(1000 * t_compute, 2), "t_h2d_ms": round(1000 * t_h2d, 2),
+                          "t_d2h_ms": round(1000 * t_d2h, 2), "frac": round(1000 * t_roof / ms_step, 4),
+                          "pcie_gbs": {k: round(v, 2) for k, v in pcie.items()},
+                          "tensor_peak_tflops": pk["bf16"], "peak": pk["kind"]},
+        "roofline": {"bound": "tensor", "achieved": round(gemm_tflops, 1), "peak": pk["bf16"],
+                     "unit": "TFLOP/s", "frac": round(gemm_tflops / pk["bf16"], 4), "traffic": None,
+                     "kernel": "hm::gemm::gemm_kernel (tcgen05)", "launches": g["launches"],
+                     "share_of_step": share.get("gemm")},
+        "kernel_shares": share,
+        "stream_busy_frac": util,
+        "iter_ms_each": [round(x / 1e6, 2) for x in its],
+        "adam_hbm": {"achieved_gbs": round(adam_gbs, 1), "peak": pk["hbm"], "frac": round(adam_gbs / pk["hbm"], 4)},
+        "e2e": {"value": round(e2e_value, 3), "unit": "samples/s", "h2d_bytes_per_step": int(tok.nbytes + lab.nbytes),
+                "d2h_bytes_per_step": 8},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "loss": [round(x, 5) for x in losses[-3:]],
+        "ledger_rows": len(rep.ledger), "ledger_equals_plan": rep.ledger == sim.ledger,
+        "device_bytes": cnt["device_bytes"],
+        "nccl_allreduce_gb_per_iter": round(cnt["nccl_bytes"] / 1e9, 3),
+    }
+    if not args.no_cpu_baseline and rank == 0 and world == 1:
+        line["cpu_baseline"] = cpu_port_sample(spec, len(os.sched_getaffinity(0)), seconds_cap=20.0)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    rt.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=("native", "reference"))
+    ap.add_argument("--workload", default="gpt2-xl-dp", choices=sorted(WORKLOADS))
+    ap.add_argument("--alpha-gib", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "native":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_native(args)
+
+
+if __name__ == "__main__":
+    main()

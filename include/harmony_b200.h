@@ -163,8 +163,23 @@ int hm_runtime_ledger(const hm_runtime *rt, hm_item *out, int32_t cap);
 int32_t hm_runtime_trace_count(const hm_runtime *rt);
 int hm_runtime_trace(const hm_runtime *rt, hm_item *out, int32_t cap);
 /* Counters of the last iteration: [0] kernels launched, [1] iteration ns,
- * [2] device bytes in use (peak), [3] H2D bytes, [4] D2H bytes, [5] P2P bytes. */
+ * [2] device bytes in use (peak), [3] H2D bytes, [4] D2H bytes, [5] P2P bytes,
+ * [6] NCCL all-reduce bytes per GPU (ring volume 2(N-1)/N x |dW|). */
 int hm_runtime_counters(const hm_runtime *rt, int64_t *out, int32_t cap);
+/* Harmony-DP: NCCL (dlopen'ed from nccl_path, NULL = default search) unique
+ * id on one rank (128 bytes), then every rank joins the communicator.  With
+ * nranks > 1, hm_runtime_load_plan inserts one all-reduce (sum) of each
+ * pack's gradient buffer between its B task and its U task, on a comm stream
+ * that overlaps the next B task. */
+int hm_nccl_unique_id(const char *nccl_path, uint8_t *out);
+int hm_runtime_init_comm(hm_runtime *rt, const char *nccl_path, const uint8_t *id, int32_t nranks,
+                         int32_t rank);
+/* Per-launch CUDA-event timing of the runtime's kernels (resets the stats). */
+int hm_runtime_set_profiling(hm_runtime *rt, int32_t enable);
+/* Accumulated stats since profiling was enabled, 7 classes x {ms, flops,
+ * bytes, launches}: 0 GEMM, 1 attention fwd, 2 attention bwd, 3 LayerNorm,
+ * 4 cross-entropy, 5 Adam, 6 other (cast, embedding, bias grad). */
+int hm_runtime_kernel_stats(const hm_runtime *rt, double *out, int32_t cap);
 void hm_runtime_free(hm_runtime *rt);
 
 /* ---- kernels, testable alone (raw device pointers, a cudaStream_t) -------- */

@@ -3,12 +3,17 @@
 #include <string>
 
 #include "plan.hpp"
+#include "runtime/common.hpp"
 
 #include <atomic>
 
 namespace hm {
 static thread_local std::string g_last_error;
 void set_last_error(const std::string &msg) { g_last_error = msg; }
+KernelProfiler *&profiler() {
+  static thread_local KernelProfiler *p = nullptr;
+  return p;
+}
 std::atomic<int64_t> &launch_counter() {
   static std::atomic<int64_t> n{0};
   return n;

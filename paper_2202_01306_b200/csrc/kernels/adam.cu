@@ -58,6 +58,7 @@ int adam_launch(float *w, const float *g, float *k, int64_t n, float lr, float b
   const float lr_t = (float)(lr / bc1);
   const float isb = (float)(1.0 / std::sqrt(bc2));
   const int64_t n4 = n / 4;
+  ProfScope ps(KC_ADAM, s, 0, 28.0 * n);
   if (n4) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);

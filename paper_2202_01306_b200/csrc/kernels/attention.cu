@@ -437,6 +437,8 @@ static int fwd_launch(const __nv_bfloat16 *qkv, __nv_bfloat16 *o, float *lse, in
     attr = true;
   }
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
+  const double fl = 4.0 * B * (double)S * S * H * DH * (CAUSAL ? 0.5 : 1.0);
+  ProfScope ps(KC_ATTN_FWD, s, fl, (double)B * S * H * DH * 2 * 4);
   k<<<dim3(S / BQ, B * H), THREADS, fwd_smem<DH>(), s>>>(qkv, o, lse, S, H, scale_log2);
   count_launch();
   HM_CUDA(cudaGetLastError());
@@ -454,6 +456,7 @@ static int bwd_launch(const __nv_bfloat16 *qkv, const __nv_bfloat16 *o, const __
   }
   const int64_t rows = (int64_t)B * S;
   const int d = H * DH;
+  ProfScope ps(KC_ATTN_BWD, s, 10.0 * B * (double)S * S * H * DH * (CAUSAL ? 0.5 : 1.0), (double)rows * d * 2 * 8);
   HM_CUDA(cudaMemsetAsync(dq_acc, 0, rows * d * sizeof(float), s));
   const int64_t warps = rows * H;
   dvec_kernel<DH><<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(o, dout, dvec, rows, H);

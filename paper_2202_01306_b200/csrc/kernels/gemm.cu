@@ -387,6 +387,9 @@ static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const Args &a, c
   }
   const int ntiles = a.num_m * a.num_n;
   const int grid = ntiles < num_sms() ? ntiles : num_sms();
+  const bool f32 = a.epi == HM_EPI_STORE_F32 || a.epi == HM_EPI_ACC_F32 || a.epi == HM_EPI_RESID_F32;
+  const double io = (double)a.M * a.N * (f32 ? 4 : 2) * (a.epi == HM_EPI_ACC_F32 || a.epi >= HM_EPI_RESID_F32 ? 2 : 1);
+  ProfScope ps(KC_GEMM, s, 2.0 * a.M * a.N * a.K, 2.0 * ((double)a.M * a.K + (double)a.N * a.K) + io);
   kern<<<grid, 256, C::kSmem, s>>>(ta, tb, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(HM_ERR_DEVICE, std::string("gemm launch: ") + cudaGetErrorString(e));

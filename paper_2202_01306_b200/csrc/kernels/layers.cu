@@ -46,6 +46,7 @@ __global__ void cast_tail(const float *src, __nv_bfloat16 *dst, int64_t begin, i
 
 int cast_f32_bf16(const float *src, void *dst, int64_t n, cudaStream_t s) {
   if (n <= 0) return HM_OK;
+  ProfScope ps(KC_MISC, s, 0, 6.0 * n);
   const int64_t n4 = ((uintptr_t)src & 15) || ((uintptr_t)dst & 7) ? 0 : n / 4;
   if (n4) {
     int64_t blocks = (n4 + 255) / 256;
@@ -97,6 +98,7 @@ __global__ void embed_bwd_pos_kernel(const float *__restrict__ dx, float *__rest
 
 int embed_fwd(const int32_t *tok, const float *wte, const float *wpe, float *out, int B, int S, int d, cudaStream_t s) {
   const int64_t rows = (int64_t)B * S;
+  ProfScope ps(KC_MISC, s, 0, 12.0 * rows * d);
   embed_fwd_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, s>>>(tok, wte, wpe, out, rows, S, d);
   count_launch();
   HM_CUDA(cudaGetLastError());
@@ -104,6 +106,7 @@ int embed_fwd(const int32_t *tok, const float *wte, const float *wpe, float *out
 }
 int embed_bwd(const int32_t *tok, const float *dx, float *dwte, float *dwpe, int B, int S, int d, cudaStream_t s) {
   const int64_t rows = (int64_t)B * S;
+  ProfScope ps(KC_MISC, s, 0, 16.0 * rows * d);
   embed_bwd_tok_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, s>>>(tok, dx, dwte, rows, d);
   embed_bwd_pos_kernel<<<(unsigned)(((int64_t)S * d + 255) / 256), 256, 0, s>>>(dx, dwpe, B, S, d);
   count_launch(2);
@@ -150,6 +153,7 @@ __global__ void ln_fwd_kernel(const float *__restrict__ x, const float *__restri
 int ln_fwd(const float *x, const float *g, const float *b, void *y, float *mean, float *rstd, int64_t rows, int d,
            cudaStream_t s) {
   if (d % 4) return fail(HM_ERR_VALIDATION, "layernorm: d must be a multiple of 4");
+  ProfScope ps(KC_LAYERNORM, s, 0, 6.0 * rows * d);
   ln_fwd_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, s>>>(x, g, b, static_cast<__nv_bfloat16 *>(y), mean,
                                                                     rstd, rows, d, 1e-5f);
   count_launch();
@@ -232,6 +236,7 @@ int ln_bwd(const float *dy, const float *x, const float *mean, const float *rstd
     HM_CUDA(cudaFuncSetAttribute(ln_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
+  ProfScope ps(KC_LAYERNORM, s, 0, (resid ? 16.0 : 12.0) * rows * d + (out_bf ? 2.0 * rows * d : 0));
   int64_t blocks = sm_count() * 2;
   int rpb = (int)((rows + blocks - 1) / blocks);
   if (rpb < 8) rpb = 8;
@@ -306,6 +311,7 @@ __global__ void ce_kernel(const float *__restrict__ logits, const int32_t *__res
 
 int cross_entropy(const float *logits, const int32_t *labels, int64_t rows, int64_t ldl, int V, void *dlogits,
                   double *loss_sum, float scale, cudaStream_t s) {
+  ProfScope ps(KC_XENT, s, 0, 6.0 * rows * ldl);
   ce_kernel<<<(unsigned)rows, 512, 0, s>>>(logits, labels, ldl, V, static_cast<__nv_bfloat16 *>(dlogits), loss_sum,
                                             scale);
   count_launch();
@@ -339,6 +345,7 @@ __global__ void bias_grad_kernel(const T *__restrict__ dy, float *__restrict__ d
 
 int bias_grad(const void *dy, int is_bf16, float *db, int64_t rows, int n, int64_t ld, cudaStream_t s) {
   if (n % 2) return fail(HM_ERR_VALIDATION, "bias_grad: n must be even");
+  ProfScope ps(KC_MISC, s, 0, (is_bf16 ? 2.0 : 4.0) * rows * n);
   const int threads = 128;
   const int gx = (n / 2 + threads - 1) / threads;
   int64_t gy = (sm_count() * 8 + gx - 1) / gx;

@@ -23,6 +23,26 @@ inline int fail(int code, const std::string &msg) {
 std::atomic<int64_t> &launch_counter();
 inline void count_launch(int64_t n = 1) { launch_counter().fetch_add(n, std::memory_order_relaxed); }
 
+// Optional per-launch timing hook (set by the runtime while profiling).
+enum KernelClass { KC_GEMM = 0, KC_ATTN_FWD, KC_ATTN_BWD, KC_LAYERNORM, KC_XENT, KC_ADAM, KC_MISC, KC_COUNT };
+struct KernelProfiler {
+  virtual void begin(int cls, cudaStream_t s) = 0;
+  virtual void end(int cls, cudaStream_t s, double flops, double bytes) = 0;
+  virtual ~KernelProfiler() = default;
+};
+KernelProfiler *&profiler();
+struct ProfScope {
+  int cls;
+  cudaStream_t s;
+  double flops, bytes;
+  ProfScope(int c, cudaStream_t st, double f, double b) : cls(c), s(st), flops(f), bytes(b) {
+    if (profiler()) profiler()->begin(cls, s);
+  }
+  ~ProfScope() {
+    if (profiler()) profiler()->end(cls, s, flops, bytes);
+  }
+};
+
 #define HM_CUDA(call)                                                                        \
   do {                                                                                       \
     cudaError_t _e = (call);                                                                 \

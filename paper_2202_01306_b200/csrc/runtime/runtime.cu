@@ -30,6 +30,7 @@
 #include "../plan.hpp"
 #include "common.hpp"
 #include "kernels_api.hpp"
+#include "nccl_loader.hpp"
 
 namespace hm {
 
@@ -84,11 +85,55 @@ struct Action {
   int64_t bytes = 0;
   int task = -1, member = -1;
   std::vector<std::pair<int, bool>> waits;  // (item, at_start)
+  std::vector<cudaEvent_t> wait_events;     // non-plan dependencies (all-reduce)
+  cudaEvent_t done = nullptr;               // kind 5: all-reduce completion
+  int64_t count = 0;                        // kind 5: floats reduced
+};
+
+// Per-launch CUDA-event timing of the runtime's kernels (enabled on demand).
+struct RtProfiler : KernelProfiler {
+  struct Rec { int cls; cudaEvent_t e0, e1; double flops, bytes; };
+  std::vector<cudaEvent_t> pool;
+  std::vector<Rec> recs;
+  size_t used = 0;
+  cudaEvent_t get() {
+    if (used == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[used++];
+  }
+  void begin(int cls, cudaStream_t s) override {
+    Rec r{cls, get(), nullptr, 0, 0};
+    cudaEventRecord(r.e0, s);
+    recs.push_back(r);
+  }
+  void end(int cls, cudaStream_t s, double flops, double bytes) override {
+    for (auto it = recs.rbegin(); it != recs.rend(); ++it)
+      if (it->cls == cls && it->e1 == nullptr) {
+        it->e1 = get();
+        cudaEventRecord(it->e1, s);
+        it->flops = flops;
+        it->bytes = bytes;
+        return;
+      }
+  }
+  void reset() {
+    recs.clear();
+    used = 0;
+  }
+  ~RtProfiler() override {
+    for (auto e : pool) cudaEventDestroy(e);
+  }
 };
 
 }  // namespace hm
 
 struct hm_runtime {
+  bool profiling = false;
+  hm::RtProfiler prof;
+  double kstats[hm::KC_COUNT][4] = {{0}};  // ms, flops, bytes, launches (accumulated)
   int device = 0;
   hm_model m{};
   int64_t alpha = 0;
@@ -125,6 +170,11 @@ struct hm_runtime {
   int32_t *tokens = nullptr, *labels = nullptr;
   double *loss_dev = nullptr;
   int step = 0;
+  // Harmony-DP gradient all-reduce (NCCL), one comm per job
+  ncclComm_t comm = nullptr;
+  int nranks = 1;
+  cudaStream_t s_comm = nullptr;
+  std::vector<cudaEvent_t> ar_events;
   // last iteration
   std::vector<hm_item> ledger, trace;
   int64_t counters[8] = {0};
@@ -614,6 +664,8 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
 
   // ---- actions ----------------------------------------------------------------
   rt.actions.clear();
+  for (auto &e : rt.ar_events) cudaEventDestroy(e);
+  rt.ar_events.clear();
   for (auto &e : rt.ev_start) cudaEventDestroy(e);
   for (auto &e : rt.ev_end) cudaEventDestroy(e);
   rt.ev_start.assign(plan->items.size(), nullptr);
@@ -683,6 +735,24 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
     TaskRt &tr = rt.trt[r.task];
     if (r.is_compute) {
       if (t.type == HM_TASK_U) {
+        if (rt.comm && rt.nranks > 1) {
+          // sum the pack's gradient over the data-parallel ranks on the comm
+          // stream; overlaps the next backward task on the compute stream
+          Action ar;
+          ar.kind = 5;
+          ar.stream = rt.s_comm;
+          ar.task = r.task;
+          TaskRt &bt = rt.trt[tr.b_task];
+          ar.waits.push_back({bt.members.back(), false});
+          ar.dst = rt.slots.dw[bt.dw_slot];
+          ar.count = tr.params;
+          cudaEvent_t e;
+          HM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+          rt.ar_events.push_back(e);
+          ar.done = e;
+          a.wait_events.push_back(e);
+          rt.actions.push_back(std::move(ar));
+        }
         a.kind = 1;
         a.stream = rt.s_update;
       } else {
@@ -743,6 +813,11 @@ static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *l
   if (!rt.plan) return fail(HM_ERR_VALIDATION, "no plan loaded");
   HM_CUDA(cudaSetDevice(rt.device));
   const int64_t launches0 = launch_counter().load();
+  rt.prof.reset();
+  profiler() = rt.profiling ? &rt.prof : nullptr;
+  struct Reset {
+    ~Reset() { profiler() = nullptr; }
+  } reset_guard;
   rt.step += 1;
   cudaStream_t sc = rt.s_compute;
   const int64_t tb = (int64_t)rt.minibatch * rt.S * 4;
@@ -750,11 +825,19 @@ static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *l
   HM_CUDA(cudaMemcpyAsync(rt.tokens, tokens, tb, is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, sc));
   HM_CUDA(cudaMemcpyAsync(rt.labels, labels, tb, is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, sc));
   HM_CUDA(cudaMemsetAsync(rt.loss_dev, 0, sizeof(double), sc));
-  cudaStream_t others[] = {rt.s_h2d, rt.s_d2h, rt.s_update};
+  cudaStream_t others[] = {rt.s_h2d, rt.s_d2h, rt.s_update, rt.s_comm};
   for (cudaStream_t o : others) HM_CUDA(cudaStreamWaitEvent(o, rt.ev_iter0, 0));
-  int64_t h2d = 0, d2h = 0;
+  int64_t h2d = 0, d2h = 0, coll = 0;
   for (Action &a : rt.actions) {
     for (auto &w : a.waits) HM_CUDA(cudaStreamWaitEvent(a.stream, w.second ? rt.ev_start[w.first] : rt.ev_end[w.first], 0));
+    for (cudaEvent_t e : a.wait_events) HM_CUDA(cudaStreamWaitEvent(a.stream, e, 0));
+    if (a.kind == 5) {
+      ncclResult_t nr = nccl().all_reduce(a.dst, a.dst, (size_t)a.count, ncclFloat32, ncclSum, rt.comm, a.stream);
+      if (nr != ncclSuccess) return fail(HM_ERR_DEVICE, std::string("ncclAllReduce: ") + nccl().error_string(nr));
+      HM_CUDA(cudaEventRecord(a.done, a.stream));
+      coll += 2 * (rt.nranks - 1) * a.count * 4 / rt.nranks;
+      continue;
+    }
     HM_CUDA(cudaEventRecord(rt.ev_start[a.item], a.stream));
     switch (a.kind) {
       case 0:
@@ -797,6 +880,7 @@ static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *l
   rt.ledger.clear();
   rt.trace.clear();
   for (Action &a : rt.actions) {
+    if (a.item < 0) continue;
     hm_item rec = rt.plan->items[a.item].rec;
     float t0 = 0, t1 = 0;
     HM_CUDA(cudaEventElapsedTime(&t0, rt.ev_iter0, rt.ev_start[a.item]));
@@ -808,12 +892,24 @@ static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *l
   }
   float it_ms = 0;
   HM_CUDA(cudaEventElapsedTime(&it_ms, rt.ev_iter0, rt.ev_iter1));
+  if (rt.profiling) {
+    for (auto &p : rt.prof.recs) {
+      if (!p.e1) continue;
+      float ms = 0;
+      HM_CUDA(cudaEventElapsedTime(&ms, p.e0, p.e1));
+      rt.kstats[p.cls][0] += ms;
+      rt.kstats[p.cls][1] += p.flops;
+      rt.kstats[p.cls][2] += p.bytes;
+      rt.kstats[p.cls][3] += 1;
+    }
+  }
   rt.counters[0] = launch_counter().load() - launches0;
   rt.counters[1] = (int64_t)((double)it_ms * 1e6);
   rt.counters[2] = rt.pool_bytes;
   rt.counters[3] = h2d;
   rt.counters[4] = d2h;
   rt.counters[5] = 0;
+  rt.counters[6] = coll;
   return HM_OK;
 }
 
@@ -853,7 +949,8 @@ hm_runtime *hm_runtime_create(int32_t device, const hm_model *model, int64_t alp
     rt->w_off[L + 1] = rt->w_off[L] + rt->lay.back().size;
   }
   rt->total_params = rt->w_off[rt->R];
-  cudaStream_t *ss[] = {&rt->s_compute, &rt->s_h2d, &rt->s_d2h, &rt->s_update, &rt->s_p2p_in, &rt->s_p2p_out};
+  cudaStream_t *ss[] = {&rt->s_compute, &rt->s_h2d,     &rt->s_d2h,    &rt->s_update,
+                        &rt->s_p2p_in,  &rt->s_p2p_out, &rt->s_comm};
   for (auto p : ss)
     if (cudaStreamCreateWithFlags(p, cudaStreamNonBlocking) != cudaSuccess) return bad(HM_ERR_DEVICE, "stream create");
   cudaEventCreate(&rt->ev_iter0);
@@ -929,6 +1026,44 @@ int hm_runtime_counters(const hm_runtime *rt, int64_t *out, int32_t cap) {
   return n;
 }
 
+int hm_nccl_unique_id(const char *nccl_path, uint8_t *out) {
+  std::string err;
+  if (!hm::nccl().load(nccl_path, err)) return hm::fail(HM_ERR_DEVICE, err);
+  ncclUniqueId id;
+  ncclResult_t r = hm::nccl().get_unique_id(&id);
+  if (r != ncclSuccess) return hm::fail(HM_ERR_DEVICE, std::string("ncclGetUniqueId: ") + hm::nccl().error_string(r));
+  std::memcpy(out, id.internal, NCCL_UNIQUE_ID_BYTES);
+  return HM_OK;
+}
+
+int hm_runtime_init_comm(hm_runtime *rt, const char *nccl_path, const uint8_t *id, int32_t nranks, int32_t rank) {
+  if (!rt) return hm::fail(HM_ERR_VALIDATION, "null runtime");
+  std::string err;
+  if (!hm::nccl().load(nccl_path, err)) return hm::fail(HM_ERR_DEVICE, err);
+  if (cudaSetDevice(rt->device) != cudaSuccess) return hm::fail(HM_ERR_DEVICE, "cudaSetDevice");
+  ncclUniqueId uid;
+  std::memcpy(uid.internal, id, NCCL_UNIQUE_ID_BYTES);
+  ncclResult_t r = hm::nccl().comm_init_rank(&rt->comm, nranks, uid, rank);
+  if (r != ncclSuccess) return hm::fail(HM_ERR_DEVICE, std::string("ncclCommInitRank: ") + hm::nccl().error_string(r));
+  rt->nranks = nranks;
+  return HM_OK;
+}
+
+int hm_runtime_set_profiling(hm_runtime *rt, int32_t enable) {
+  if (!rt) return hm::fail(HM_ERR_VALIDATION, "null runtime");
+  rt->profiling = enable != 0;
+  for (auto &row : rt->kstats)
+    for (double &v : row) v = 0;
+  return HM_OK;
+}
+
+int hm_runtime_kernel_stats(const hm_runtime *rt, double *out, int32_t cap) {
+  if (!rt || cap < hm::KC_COUNT * 4) return hm::fail(HM_ERR_VALIDATION, "kernel stats buffer too small");
+  for (int c = 0; c < hm::KC_COUNT; ++c)
+    for (int j = 0; j < 4; ++j) out[c * 4 + j] = rt->kstats[c][j];
+  return hm::KC_COUNT;
+}
+
 void hm_runtime_free(hm_runtime *rt) {
   if (!rt) return;
   cudaSetDevice(rt->device);
@@ -937,11 +1072,13 @@ void hm_runtime_free(hm_runtime *rt) {
   for (auto &e : rt->ev_end) if (e) cudaEventDestroy(e);
   if (rt->ev_iter0) cudaEventDestroy(rt->ev_iter0);
   if (rt->ev_iter1) cudaEventDestroy(rt->ev_iter1);
+  for (auto &e : rt->ar_events) cudaEventDestroy(e);
+  if (rt->comm) hm::nccl().comm_destroy(rt->comm);
   if (rt->pool) cudaFree(rt->pool);
   if (rt->w_host) cudaFreeHost(rt->w_host);
   if (rt->k_host) cudaFreeHost(rt->k_host);
   if (rt->stash_host) cudaFreeHost(rt->stash_host);
-  cudaStream_t ss[] = {rt->s_compute, rt->s_h2d, rt->s_d2h, rt->s_update, rt->s_p2p_in, rt->s_p2p_out};
+  cudaStream_t ss[] = {rt->s_compute, rt->s_h2d, rt->s_d2h, rt->s_update, rt->s_p2p_in, rt->s_p2p_out, rt->s_comm};
   for (auto s : ss) if (s) cudaStreamDestroy(s);
   delete rt;
 }

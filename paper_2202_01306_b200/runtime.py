@@ -90,6 +90,32 @@ class HarmonyRuntime:
                         view.reshape(-1, d)[V:] = 0.0
         self.k[:] = 0.0
 
+    # -- Harmony-DP communicator -------------------------------------------------
+    @staticmethod
+    def nccl_path() -> bytes:
+        """libnccl.so.2 shipped with torch (the one torch.distributed uses)."""
+        import os
+        try:
+            import nvidia.nccl as nn
+            base = list(nn.__path__)[0]
+            p = os.path.join(base, "lib", "libnccl.so.2")
+            if os.path.exists(p):
+                return p.encode()
+        except ImportError:
+            pass
+        return b""
+
+    @classmethod
+    def nccl_unique_id(cls) -> bytes:
+        buf = (C.c_uint8 * 128)()
+        NL.check(NL.lib().hm_nccl_unique_id(cls.nccl_path(), buf))
+        return bytes(buf)
+
+    def init_comm(self, unique_id: bytes, nranks: int, rank: int) -> None:
+        """Join the job's NCCL communicator (call before load())."""
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        NL.check(self.lib.hm_runtime_init_comm(self.handle, self.nccl_path(), buf, nranks, rank))
+
     # -- plan -------------------------------------------------------------------
     def load(self, graph: TaskGraph, machine: MachineModel, profiles: ProfileSet, rank: int = 0) -> None:
         if graph.config is None:
@@ -136,7 +162,19 @@ class HarmonyRuntime:
         out = (C.c_int64 * 8)()
         NL.check(self.lib.hm_runtime_counters(self.handle, out, 8))
         return {"kernels": out[0], "iteration_ns": out[1], "device_bytes": out[2],
-                "h2d_bytes": out[3], "d2h_bytes": out[4], "p2p_bytes": out[5]}
+                "h2d_bytes": out[3], "d2h_bytes": out[4], "p2p_bytes": out[5], "nccl_bytes": out[6]}
+
+    KERNEL_CLASSES = ("gemm", "attn_fwd", "attn_bwd", "layernorm", "xent", "adam", "other")
+
+    def set_profiling(self, enable: bool) -> None:
+        NL.check(self.lib.hm_runtime_set_profiling(self.handle, 1 if enable else 0))
+
+    def kernel_stats(self) -> dict:
+        """{class: {ms, flops, bytes, launches}} accumulated while profiling."""
+        buf = (C.c_double * 28)()
+        NL.check(self.lib.hm_runtime_kernel_stats(self.handle, buf, 28))
+        return {c: {"ms": buf[4 * i], "flops": buf[4 * i + 1], "bytes": buf[4 * i + 2],
+                    "launches": int(buf[4 * i + 3])} for i, c in enumerate(self.KERNEL_CLASSES)}
 
     def measured_items(self) -> np.ndarray:
         n1 = self.lib.hm_runtime_ledger_count(self.handle)
