@@ -174,6 +174,9 @@ int hm_runtime_counters(const hm_runtime *rt, int64_t *out, int32_t cap);
 int hm_nccl_unique_id(const char *nccl_path, uint8_t *out);
 int hm_runtime_init_comm(hm_runtime *rt, const char *nccl_path, const uint8_t *id, int32_t nranks,
                          int32_t rank);
+/* Record each iteration into a CUDA graph after the first (default on) and
+ * replay it: one launch per iteration instead of thousands. */
+int hm_runtime_set_graph(hm_runtime *rt, int32_t enable);
 /* Per-launch CUDA-event timing of the runtime's kernels (resets the stats). */
 int hm_runtime_set_profiling(hm_runtime *rt, int32_t enable);
 /* Accumulated stats since profiling was enabled, 7 classes x {ms, flops,

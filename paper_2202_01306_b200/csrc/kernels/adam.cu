@@ -14,7 +14,12 @@ namespace hm {
 
 __global__ void __launch_bounds__(256) adam_kernel(float4 *__restrict__ w, const float4 *__restrict__ g,
                                                    float4 *__restrict__ k, int64_t n4, float lr_t, float b1,
-                                                   float b2, float inv_sqrt_bc2, float eps, float gscale) {
+                                                   float b2, float inv_sqrt_bc2, float eps, float gscale,
+                                                   const float *__restrict__ sc) {
+  if (sc) {  // step-dependent scalars from device memory (graph replay)
+    lr_t = sc[0];
+    inv_sqrt_bc2 = sc[1];
+  }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     float4 wi = w[i];
     const float4 gi = g[i];
@@ -37,7 +42,11 @@ __global__ void __launch_bounds__(256) adam_kernel(float4 *__restrict__ w, const
 }
 
 __global__ void adam_tail(float *w, const float *g, float *k, int64_t begin, int64_t n, float lr_t, float b1,
-                          float b2, float inv_sqrt_bc2, float eps, float gscale) {
+                          float b2, float inv_sqrt_bc2, float eps, float gscale, const float *sc) {
+  if (sc) {
+    lr_t = sc[0];
+    inv_sqrt_bc2 = sc[1];
+  }
   int64_t i = begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   float gi = g[i] * gscale;
@@ -48,15 +57,10 @@ __global__ void adam_tail(float *w, const float *g, float *k, int64_t begin, int
   k[2 * i + 1] = v;
 }
 
-int adam_launch(float *w, const float *g, float *k, int64_t n, float lr, float b1, float b2, float eps, int step,
-                float gscale, cudaStream_t s) {
+static int adam_impl(float *w, const float *g, float *k, int64_t n, float lr_t, float b1, float b2, float eps,
+                     float isb, const float *sc, float gscale, cudaStream_t s) {
   if (n <= 0) return HM_OK;
-  if (step < 1) return fail(HM_ERR_VALIDATION, "adam: step must be >= 1");
   if (((uintptr_t)w | (uintptr_t)g | (uintptr_t)k) & 15) return fail(HM_ERR_VALIDATION, "adam: 16B alignment");
-  const double bc1 = 1.0 - std::pow((double)b1, step);
-  const double bc2 = 1.0 - std::pow((double)b2, step);
-  const float lr_t = (float)(lr / bc1);
-  const float isb = (float)(1.0 / std::sqrt(bc2));
   const int64_t n4 = n / 4;
   ProfScope ps(KC_ADAM, s, 0, 28.0 * n);
   if (n4) {
@@ -66,15 +70,29 @@ int adam_launch(float *w, const float *g, float *k, int64_t n, float lr, float b
     int64_t blocks = (n4 + 255) / 256;
     if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
     adam_kernel<<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<float4 *>(w), reinterpret_cast<const float4 *>(g),
-                                                 reinterpret_cast<float4 *>(k), n4, lr_t, b1, b2, isb, eps, gscale);
+                                                 reinterpret_cast<float4 *>(k), n4, lr_t, b1, b2, isb, eps, gscale, sc);
     count_launch();
   }
   if (n4 * 4 < n) {
-    adam_tail<<<1, 32, 0, s>>>(w, g, k, n4 * 4, n, lr_t, b1, b2, isb, eps, gscale);
+    adam_tail<<<1, 32, 0, s>>>(w, g, k, n4 * 4, n, lr_t, b1, b2, isb, eps, gscale, sc);
     count_launch();
   }
   HM_CUDA(cudaGetLastError());
   return HM_OK;
+}
+
+int adam_launch(float *w, const float *g, float *k, int64_t n, float lr, float b1, float b2, float eps, int step,
+                float gscale, cudaStream_t s) {
+  if (step < 1) return fail(HM_ERR_VALIDATION, "adam: step must be >= 1");
+  const double bc1 = 1.0 - std::pow((double)b1, step);
+  const double bc2 = 1.0 - std::pow((double)b2, step);
+  return adam_impl(w, g, k, n, (float)(lr / bc1), b1, b2, eps, (float)(1.0 / std::sqrt(bc2)), nullptr, gscale, s);
+}
+
+// Same update with {lr/(1-b1^t), 1/sqrt(1-b2^t)} read from device memory.
+int adam_launch_dev(float *w, const float *g, float *k, int64_t n, float b1, float b2, float eps, const float *scalars,
+                    float gscale, cudaStream_t s) {
+  return adam_impl(w, g, k, n, 0.f, b1, b2, eps, 0.f, scalars, gscale, s);
 }
 
 }  // namespace hm

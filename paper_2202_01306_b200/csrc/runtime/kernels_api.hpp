@@ -6,6 +6,8 @@
 #include <cstdint>
 
 namespace hm {
+int adam_launch_dev(float *w, const float *g, float *k, int64_t n, float b1, float b2, float eps,
+                    const float *scalars, float gscale, cudaStream_t s);
 int adam_launch(float *w, const float *g, float *k, int64_t n, float lr, float b1, float b2, float eps, int step,
                 float gscale, cudaStream_t s);
 namespace gemm {

@@ -96,6 +96,10 @@ struct RtProfiler : KernelProfiler {
   std::vector<cudaEvent_t> pool;
   std::vector<Rec> recs;
   size_t used = 0;
+  bool capture = false;
+  cudaError_t rec(cudaEvent_t e, cudaStream_t s) {
+    return capture ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s);
+  }
   cudaEvent_t get() {
     if (used == pool.size()) {
       cudaEvent_t e;
@@ -106,14 +110,14 @@ struct RtProfiler : KernelProfiler {
   }
   void begin(int cls, cudaStream_t s) override {
     Rec r{cls, get(), nullptr, 0, 0};
-    cudaEventRecord(r.e0, s);
+    rec(r.e0, s);
     recs.push_back(r);
   }
   void end(int cls, cudaStream_t s, double flops, double bytes) override {
     for (auto it = recs.rbegin(); it != recs.rend(); ++it)
       if (it->cls == cls && it->e1 == nullptr) {
         it->e1 = get();
-        cudaEventRecord(it->e1, s);
+        rec(it->e1, s);
         it->flops = flops;
         it->bytes = bytes;
         return;
@@ -153,8 +157,17 @@ struct hm_runtime {
   int64_t global_tokens = 0;
   std::vector<hm::TaskRt> trt;
   std::vector<hm::Action> actions;
-  std::vector<cudaEvent_t> ev_start, ev_end;
-  cudaEvent_t ev_iter0 = nullptr, ev_iter1 = nullptr;
+  std::vector<cudaEvent_t> ev_start, ev_end;     // dependencies
+  std::vector<cudaEvent_t> ev_tstart, ev_tend;   // timing (external records inside graphs)
+  cudaEvent_t ev_iter0 = nullptr, ev_iter1 = nullptr, ev_fork = nullptr, ev_join[4] = {nullptr};
+  // CUDA graph of one iteration ([0] plain, [1] with per-kernel timing events)
+  bool use_graph = true;
+  int64_t iterations = 0;
+  cudaGraphExec_t graph_exec[2] = {nullptr, nullptr};
+  int64_t graph_launches[2] = {0, 0};
+  int64_t graph_bytes[2][3] = {{0}};
+  float *adam_host = nullptr;  // pinned {lr_t, 1/sqrt(bc2)}
+  float *adam_dev = nullptr;
   // device pool
   uint8_t *pool = nullptr;
   int64_t pool_bytes = 0;
@@ -631,6 +644,7 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
   req.push_back({(void **)&rt.tokens, rows_mb * 4});
   req.push_back({(void **)&rt.labels, rows_mb * 4});
   req.push_back({(void **)&rt.loss_dev, 256});
+  req.push_back({(void **)&rt.adam_dev, 256});
   int64_t total = 0;
   for (auto &r : req) total += align_up(r.bytes, 1024);
   if (total > rt.alpha)
@@ -668,12 +682,24 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
   rt.ar_events.clear();
   for (auto &e : rt.ev_start) cudaEventDestroy(e);
   for (auto &e : rt.ev_end) cudaEventDestroy(e);
+  for (auto &e : rt.ev_tstart) if (e) cudaEventDestroy(e);
+  for (auto &e : rt.ev_tend) if (e) cudaEventDestroy(e);
+  for (auto &g : rt.graph_exec)
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+  rt.iterations = 0;
   rt.ev_start.assign(plan->items.size(), nullptr);
   rt.ev_end.assign(plan->items.size(), nullptr);
+  rt.ev_tstart.assign(plan->items.size(), nullptr);
+  rt.ev_tend.assign(plan->items.size(), nullptr);
   for (size_t i = 0; i < plan->items.size(); ++i) {
     if (plan->items[i].rec.gpu != rank) continue;
     HM_CUDA(cudaEventCreate(&rt.ev_start[i]));
     HM_CUDA(cudaEventCreate(&rt.ev_end[i]));
+    HM_CUDA(cudaEventCreate(&rt.ev_tstart[i]));
+    HM_CUDA(cudaEventCreate(&rt.ev_tend[i]));
   }
   for (auto &t : plan->tasks)
     if (t.dev_id == rank) rt.trt[t.index].members = plan->member_computes[t.index];
@@ -809,27 +835,25 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
   return HM_OK;
 }
 
-static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *labels, int is_device, double *loss) {
-  if (!rt.plan) return fail(HM_ERR_VALIDATION, "no plan loaded");
-  HM_CUDA(cudaSetDevice(rt.device));
-  const int64_t launches0 = launch_counter().load();
-  rt.prof.reset();
-  profiler() = rt.profiling ? &rt.prof : nullptr;
-  struct Reset {
-    ~Reset() { profiler() = nullptr; }
-  } reset_guard;
-  rt.step += 1;
+// Enqueue one iteration's body on the runtime's streams.  With `capture`,
+// the enqueue is being recorded into a CUDA graph: dependency events stay
+// capture-internal, timing events become external event-record nodes, and
+// waits on the previous iteration's events are dropped (an iteration only
+// starts after the previous one completed).
+static int enqueue_body(hm_runtime &rt, bool capture, int64_t &h2d, int64_t &d2h, int64_t &coll) {
   cudaStream_t sc = rt.s_compute;
-  const int64_t tb = (int64_t)rt.minibatch * rt.S * 4;
-  HM_CUDA(cudaEventRecord(rt.ev_iter0, sc));
-  HM_CUDA(cudaMemcpyAsync(rt.tokens, tokens, tb, is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, sc));
-  HM_CUDA(cudaMemcpyAsync(rt.labels, labels, tb, is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, sc));
+  auto rec_time = [&](cudaEvent_t e, cudaStream_t s) -> cudaError_t {
+    return capture ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s);
+  };
   HM_CUDA(cudaMemsetAsync(rt.loss_dev, 0, sizeof(double), sc));
+  HM_CUDA(cudaEventRecord(rt.ev_fork, sc));
   cudaStream_t others[] = {rt.s_h2d, rt.s_d2h, rt.s_update, rt.s_comm};
-  for (cudaStream_t o : others) HM_CUDA(cudaStreamWaitEvent(o, rt.ev_iter0, 0));
-  int64_t h2d = 0, d2h = 0, coll = 0;
+  for (cudaStream_t o : others) HM_CUDA(cudaStreamWaitEvent(o, rt.ev_fork, 0));
   for (Action &a : rt.actions) {
-    for (auto &w : a.waits) HM_CUDA(cudaStreamWaitEvent(a.stream, w.second ? rt.ev_start[w.first] : rt.ev_end[w.first], 0));
+    for (auto &w : a.waits) {
+      if (capture && a.item >= 0 && w.first > a.item) continue;  // previous iteration: already complete
+      HM_CUDA(cudaStreamWaitEvent(a.stream, w.second ? rt.ev_start[w.first] : rt.ev_end[w.first], 0));
+    }
     for (cudaEvent_t e : a.wait_events) HM_CUDA(cudaStreamWaitEvent(a.stream, e, 0));
     if (a.kind == 5) {
       ncclResult_t nr = nccl().all_reduce(a.dst, a.dst, (size_t)a.count, ncclFloat32, ncclSum, rt.comm, a.stream);
@@ -839,6 +863,7 @@ static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *l
       continue;
     }
     HM_CUDA(cudaEventRecord(rt.ev_start[a.item], a.stream));
+    if (capture) HM_CUDA(rec_time(rt.ev_tstart[a.item], a.stream));
     switch (a.kind) {
       case 0:
         HM_TRY(run_member(rt, a.task, a.member));
@@ -846,8 +871,8 @@ static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *l
       case 1: {
         TaskRt &tr = rt.trt[a.task];
         TaskRt &bt = rt.trt[tr.b_task];
-        HM_TRY(adam_launch(rt.slots.w[bt.w_slot], rt.slots.dw[bt.dw_slot], rt.slots.k[tr.k_slot], tr.params, rt.m.lr,
-                           rt.m.beta1, rt.m.beta2, rt.m.eps, rt.step, 1.0f, a.stream));
+        HM_TRY(adam_launch_dev(rt.slots.w[bt.w_slot], rt.slots.dw[bt.dw_slot], rt.slots.k[tr.k_slot], tr.params,
+                               rt.m.beta1, rt.m.beta2, rt.m.eps, rt.adam_dev, 1.0f, a.stream));
         break;
       }
       case 2:
@@ -862,19 +887,78 @@ static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *l
         return fail(HM_ERR_INTERNAL, "bad action");
     }
     HM_CUDA(cudaEventRecord(rt.ev_end[a.item], a.stream));
+    if (capture) HM_CUDA(rec_time(rt.ev_tend[a.item], a.stream));
   }
-  // join every stream into the compute stream, read the loss
-  for (cudaStream_t o : others) {
-    cudaEvent_t e;
-    HM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    HM_CUDA(cudaEventRecord(e, o));
-    HM_CUDA(cudaStreamWaitEvent(sc, e, 0));
-    cudaEventDestroy(e);
+  for (size_t i = 0; i < 4; ++i) {
+    HM_CUDA(cudaEventRecord(rt.ev_join[i], others[i]));
+    HM_CUDA(cudaStreamWaitEvent(sc, rt.ev_join[i], 0));
+  }
+  return HM_OK;
+}
+
+static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *labels, int is_device, double *loss) {
+  if (!rt.plan) return fail(HM_ERR_VALIDATION, "no plan loaded");
+  HM_CUDA(cudaSetDevice(rt.device));
+  const int64_t launches0 = launch_counter().load();
+  rt.step += 1;
+  cudaStream_t sc = rt.s_compute;
+  const int64_t tb = (int64_t)rt.minibatch * rt.S * 4;
+  // Adam bias corrections for this step live in device memory so a captured
+  // graph replays correctly: {lr / (1 - b1^t), 1 / sqrt(1 - b2^t)}
+  rt.adam_host[0] = (float)(rt.m.lr / (1.0 - std::pow((double)rt.m.beta1, rt.step)));
+  rt.adam_host[1] = (float)(1.0 / std::sqrt(1.0 - std::pow((double)rt.m.beta2, rt.step)));
+  HM_CUDA(cudaEventRecord(rt.ev_iter0, sc));
+  HM_CUDA(cudaMemcpyAsync(rt.adam_dev, rt.adam_host, 2 * sizeof(float), cudaMemcpyHostToDevice, sc));
+  HM_CUDA(cudaMemcpyAsync(rt.tokens, tokens, tb, is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, sc));
+  HM_CUDA(cudaMemcpyAsync(rt.labels, labels, tb, is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, sc));
+  int64_t h2d = 0, d2h = 0, coll = 0;
+  const int gi = rt.profiling ? 1 : 0;
+  const bool use_graph = rt.use_graph && rt.iterations >= 1;
+  if (use_graph) {
+    if (!rt.graph_exec[gi]) {
+      // record the iteration once (with or without per-kernel timing events)
+      if (gi == 1) {  // the timing events recorded here are replayed by graph [1] only
+        rt.prof.reset();
+        rt.prof.capture = true;
+      }
+      profiler() = rt.profiling ? &rt.prof : nullptr;
+      const int64_t l0 = launch_counter().load();
+      HM_CUDA(cudaStreamBeginCapture(sc, cudaStreamCaptureModeRelaxed));
+      int rc = enqueue_body(rt, true, h2d, d2h, coll);
+      cudaGraph_t g = nullptr;
+      cudaError_t ce = cudaStreamEndCapture(sc, &g);
+      profiler() = nullptr;
+      rt.prof.capture = false;
+      if (rc != HM_OK) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+      }
+      if (ce != cudaSuccess) return fail(HM_ERR_DEVICE, std::string("graph capture: ") + cudaGetErrorString(ce));
+      HM_CUDA(cudaGraphInstantiate(&rt.graph_exec[gi], g, 0));
+      cudaGraphDestroy(g);
+      rt.graph_launches[gi] = launch_counter().load() - l0;
+      rt.graph_bytes[gi][0] = h2d;
+      rt.graph_bytes[gi][1] = d2h;
+      rt.graph_bytes[gi][2] = coll;
+      launch_counter().fetch_sub(rt.graph_launches[gi]);  // counted when replayed
+    }
+    HM_CUDA(cudaGraphLaunch(rt.graph_exec[gi], sc));
+    count_launch(rt.graph_launches[gi]);
+    h2d = rt.graph_bytes[gi][0];
+    d2h = rt.graph_bytes[gi][1];
+    coll = rt.graph_bytes[gi][2];
+  } else {
+    rt.prof.reset();
+    profiler() = rt.profiling ? &rt.prof : nullptr;
+    int rc = enqueue_body(rt, false, h2d, d2h, coll);
+    profiler() = nullptr;
+    HM_TRY(rc);
   }
   double loss_sum = 0;
   HM_CUDA(cudaMemcpyAsync(&loss_sum, rt.loss_dev, sizeof(double), cudaMemcpyDeviceToHost, sc));
   HM_CUDA(cudaEventRecord(rt.ev_iter1, sc));
   HM_CUDA(cudaEventSynchronize(rt.ev_iter1));
+  rt.iterations += 1;
   if (loss) *loss = loss_sum / (double)rt.global_tokens;
   // measured ledger and trace
   rt.ledger.clear();
@@ -883,8 +967,10 @@ static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *l
     if (a.item < 0) continue;
     hm_item rec = rt.plan->items[a.item].rec;
     float t0 = 0, t1 = 0;
-    HM_CUDA(cudaEventElapsedTime(&t0, rt.ev_iter0, rt.ev_start[a.item]));
-    HM_CUDA(cudaEventElapsedTime(&t1, rt.ev_iter0, rt.ev_end[a.item]));
+    cudaEvent_t es = use_graph ? rt.ev_tstart[a.item] : rt.ev_start[a.item];
+    cudaEvent_t ee = use_graph ? rt.ev_tend[a.item] : rt.ev_end[a.item];
+    HM_CUDA(cudaEventElapsedTime(&t0, rt.ev_iter0, es));
+    HM_CUDA(cudaEventElapsedTime(&t1, rt.ev_iter0, ee));
     rec.start_ns = (int64_t)((double)t0 * 1e6);
     rec.end_ns = (int64_t)((double)t1 * 1e6);
     rec.duration_ns = rec.end_ns - rec.start_ns;
@@ -955,6 +1041,9 @@ hm_runtime *hm_runtime_create(int32_t device, const hm_model *model, int64_t alp
     if (cudaStreamCreateWithFlags(p, cudaStreamNonBlocking) != cudaSuccess) return bad(HM_ERR_DEVICE, "stream create");
   cudaEventCreate(&rt->ev_iter0);
   cudaEventCreate(&rt->ev_iter1);
+  cudaEventCreateWithFlags(&rt->ev_fork, cudaEventDisableTiming);
+  for (auto &e : rt->ev_join) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  if (cudaHostAlloc(&rt->adam_host, 64, cudaHostAllocDefault) != cudaSuccess) return bad(HM_ERR_DEVICE, "pinned alloc");
   if (cudaHostAlloc(&rt->w_host, rt->total_params * 4, cudaHostAllocDefault) != cudaSuccess ||
       cudaHostAlloc(&rt->k_host, rt->total_params * 8, cudaHostAllocDefault) != cudaSuccess)
     return bad(HM_ERR_DEVICE, "pinned host arena allocation failed (" + std::to_string(rt->total_params * 12) + " B)");
@@ -1049,6 +1138,12 @@ int hm_runtime_init_comm(hm_runtime *rt, const char *nccl_path, const uint8_t *i
   return HM_OK;
 }
 
+int hm_runtime_set_graph(hm_runtime *rt, int32_t enable) {
+  if (!rt) return hm::fail(HM_ERR_VALIDATION, "null runtime");
+  rt->use_graph = enable != 0;
+  return HM_OK;
+}
+
 int hm_runtime_set_profiling(hm_runtime *rt, int32_t enable) {
   if (!rt) return hm::fail(HM_ERR_VALIDATION, "null runtime");
   rt->profiling = enable != 0;
@@ -1070,6 +1165,12 @@ void hm_runtime_free(hm_runtime *rt) {
   cudaDeviceSynchronize();
   for (auto &e : rt->ev_start) if (e) cudaEventDestroy(e);
   for (auto &e : rt->ev_end) if (e) cudaEventDestroy(e);
+  for (auto &e : rt->ev_tstart) if (e) cudaEventDestroy(e);
+  for (auto &e : rt->ev_tend) if (e) cudaEventDestroy(e);
+  for (auto &g : rt->graph_exec) if (g) cudaGraphExecDestroy(g);
+  if (rt->ev_fork) cudaEventDestroy(rt->ev_fork);
+  for (auto &e : rt->ev_join) if (e) cudaEventDestroy(e);
+  if (rt->adam_host) cudaFreeHost(rt->adam_host);
   if (rt->ev_iter0) cudaEventDestroy(rt->ev_iter0);
   if (rt->ev_iter1) cudaEventDestroy(rt->ev_iter1);
   for (auto &e : rt->ar_events) cudaEventDestroy(e);
