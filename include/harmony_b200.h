@@ -137,7 +137,7 @@ typedef struct {
   int32_t d_model, n_head, seq_len, vocab, vocab_padded;
   int32_t causal;     /* 1 = GPT, 0 = BERT-style full attention             */
   int32_t math_mode;  /* 0 = bf16 operands / fp32 accumulate               */
-  float lr, beta1, beta2, eps;
+  double lr, beta1, beta2, eps; /* double: 1-beta computed exactly as torch does */
 } hm_model;
 
 typedef struct hm_runtime hm_runtime;
@@ -155,6 +155,12 @@ int hm_runtime_load_plan(hm_runtime *rt, hm_plan *plan, int32_t rank, int32_t mi
  * device pointers (is_device = 1).  loss_out: mean token cross-entropy. */
 int hm_runtime_run_iteration(hm_runtime *rt, const int32_t *tokens, const int32_t *labels,
                              int32_t is_device, double *loss_out);
+/* n (1..64) back-to-back iterations on the same batch with cross-iteration
+ * overlap (iteration i+1's swap-ins start while iteration i's last swap-outs
+ * drain; every buffer hand-off across the boundary is event-ordered).
+ * losses[n] per iteration; total_ns = device time of all n iterations. */
+int hm_runtime_run_steps(hm_runtime *rt, int32_t n, const int32_t *tokens, const int32_t *labels,
+                         int32_t is_device, double *losses, int64_t *total_ns);
 int32_t hm_runtime_ledger_count(const hm_runtime *rt);
 /* Executed transfer rows of the last iteration, in execution order; the
  * start/end fields hold measured CUDA-event times relative to iteration start. */
@@ -188,8 +194,8 @@ void hm_runtime_free(hm_runtime *rt);
 /* ---- kernels, testable alone (raw device pointers, a cudaStream_t) -------- */
 /* Fused Adam over one pack: W, m, v updated in place from g; K holds (m, v)
  * interleaved per parameter.  step >= 1.  Reads 16 B/param, writes 12 B/param. */
-int hm_k_adam(float *w, const float *g, float *k, int64_t n, float lr, float beta1,
-              float beta2, float eps, int32_t step, float grad_scale, void *stream);
+int hm_k_adam(float *w, const float *g, float *k, int64_t n, double lr, double beta1,
+              double beta2, double eps, int32_t step, float grad_scale, void *stream);
 /* C[M,N] (+)= A . B^T with bf16 operands, fp32 accumulate (tcgen05 + TMEM + TMA).
  * a_major/b_major: 0 = K-major (reduction dim contiguous), 1 = MN-major.
  * epilogue: see hm_gemm_epilogue. */

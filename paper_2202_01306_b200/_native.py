@@ -53,7 +53,7 @@ ITEM_DTYPE = np.dtype([
 class hm_model(C.Structure):
     _fields_ = [(n, C.c_int32) for n in (
         "n_layer", "d_model", "n_head", "seq_len", "vocab", "vocab_padded", "causal",
-        "math_mode")] + [(n, C.c_float) for n in ("lr", "beta1", "beta2", "eps")]
+        "math_mode")] + [(n, C.c_double) for n in ("lr", "beta1", "beta2", "eps")]
 
 
 _lib = None
@@ -88,6 +88,8 @@ def lib() -> C.CDLL:
         "hm_runtime_run_iteration": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
                                                P(C.c_double)]),
         "hm_runtime_ledger_count": (C.c_int32, [C.c_void_p]),
+        "hm_runtime_run_steps": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32,
+                                           P(C.c_double), P(C.c_int64)]),
         "hm_runtime_ledger": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
         "hm_runtime_trace_count": (C.c_int32, [C.c_void_p]),
         "hm_runtime_trace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
@@ -98,8 +100,8 @@ def lib() -> C.CDLL:
         "hm_runtime_set_graph": (C.c_int, [C.c_void_p, C.c_int32]),
         "hm_runtime_set_profiling": (C.c_int, [C.c_void_p, C.c_int32]),
         "hm_runtime_kernel_stats": (C.c_int, [C.c_void_p, P(C.c_double), C.c_int32]),
-        "hm_k_adam": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_float,
-                                C.c_float, C.c_float, C.c_float, C.c_int32, C.c_float, C.c_void_p]),
+        "hm_k_adam": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_double,
+                                C.c_double, C.c_double, C.c_double, C.c_int32, C.c_float, C.c_void_p]),
         "hm_k_gemm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
                                 C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
                                 C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int64, C.c_int64,

@@ -13,8 +13,8 @@
 namespace hm {
 
 __global__ void __launch_bounds__(256) adam_kernel(float4 *__restrict__ w, const float4 *__restrict__ g,
-                                                   float4 *__restrict__ k, int64_t n4, float lr_t, float b1,
-                                                   float b2, float inv_sqrt_bc2, float eps, float gscale,
+                                                   float4 *__restrict__ k, int64_t n4, float lr_t, float omb1,
+                                                   float b2, float omb2, float inv_sqrt_bc2, float eps, float gscale,
                                                    const float *__restrict__ sc) {
   if (sc) {  // step-dependent scalars from device memory (graph replay)
     lr_t = sc[0];
@@ -30,8 +30,8 @@ __global__ void __launch_bounds__(256) adam_kernel(float4 *__restrict__ w, const
     float ww[4] = {wi.x, wi.y, wi.z, wi.w};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      m[j] = m[j] + (1.f - b1) * (gg[j] - m[j]);  // torch lerp form
-      v[j] = b2 * v[j] + (1.f - b2) * gg[j] * gg[j];
+      m[j] = m[j] + omb1 * (gg[j] - m[j]);  // torch lerp form
+      v[j] = b2 * v[j] + omb2 * gg[j] * gg[j];
       const float denom = sqrtf(v[j]) * inv_sqrt_bc2 + eps;
       ww[j] -= lr_t * (m[j] / denom);
     }
@@ -41,8 +41,8 @@ __global__ void __launch_bounds__(256) adam_kernel(float4 *__restrict__ w, const
   }
 }
 
-__global__ void adam_tail(float *w, const float *g, float *k, int64_t begin, int64_t n, float lr_t, float b1,
-                          float b2, float inv_sqrt_bc2, float eps, float gscale, const float *sc) {
+__global__ void adam_tail(float *w, const float *g, float *k, int64_t begin, int64_t n, float lr_t, float omb1,
+                          float b2, float omb2, float inv_sqrt_bc2, float eps, float gscale, const float *sc) {
   if (sc) {
     lr_t = sc[0];
     inv_sqrt_bc2 = sc[1];
@@ -50,18 +50,20 @@ __global__ void adam_tail(float *w, const float *g, float *k, int64_t begin, int
   int64_t i = begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   float gi = g[i] * gscale;
-  float m = k[2 * i] + (1.f - b1) * (gi - k[2 * i]);
-  float v = b2 * k[2 * i + 1] + (1.f - b2) * gi * gi;
+  float m = k[2 * i] + omb1 * (gi - k[2 * i]);
+  float v = b2 * k[2 * i + 1] + omb2 * gi * gi;
   w[i] -= lr_t * (m / (sqrtf(v) * inv_sqrt_bc2 + eps));
   k[2 * i] = m;
   k[2 * i + 1] = v;
 }
 
-static int adam_impl(float *w, const float *g, float *k, int64_t n, float lr_t, float b1, float b2, float eps,
+static int adam_impl(float *w, const float *g, float *k, int64_t n, float lr_t, double b1, double b2, double eps,
                      float isb, const float *sc, float gscale, cudaStream_t s) {
   if (n <= 0) return HM_OK;
   if (((uintptr_t)w | (uintptr_t)g | (uintptr_t)k) & 15) return fail(HM_ERR_VALIDATION, "adam: 16B alignment");
   const int64_t n4 = n / 4;
+  // 1 - beta in double, as torch.optim.Adam does (1 - 0.999f in float is off by 1.3e-5)
+  const float omb1 = (float)(1.0 - b1), omb2 = (float)(1.0 - b2);
   ProfScope ps(KC_ADAM, s, 0, 28.0 * n);
   if (n4) {
     int dev = 0, sms = 148;
@@ -70,34 +72,34 @@ static int adam_impl(float *w, const float *g, float *k, int64_t n, float lr_t, 
     int64_t blocks = (n4 + 255) / 256;
     if (blocks > (int64_t)sms * 8) blocks = (int64_t)sms * 8;
     adam_kernel<<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<float4 *>(w), reinterpret_cast<const float4 *>(g),
-                                                 reinterpret_cast<float4 *>(k), n4, lr_t, b1, b2, isb, eps, gscale, sc);
+                                                 reinterpret_cast<float4 *>(k), n4, lr_t, omb1, (float)b2, omb2, isb, (float)eps, gscale, sc);
     count_launch();
   }
   if (n4 * 4 < n) {
-    adam_tail<<<1, 32, 0, s>>>(w, g, k, n4 * 4, n, lr_t, b1, b2, isb, eps, gscale, sc);
+    adam_tail<<<1, 32, 0, s>>>(w, g, k, n4 * 4, n, lr_t, omb1, (float)b2, omb2, isb, (float)eps, gscale, sc);
     count_launch();
   }
   HM_CUDA(cudaGetLastError());
   return HM_OK;
 }
 
-int adam_launch(float *w, const float *g, float *k, int64_t n, float lr, float b1, float b2, float eps, int step,
+int adam_launch(float *w, const float *g, float *k, int64_t n, double lr, double b1, double b2, double eps, int step,
                 float gscale, cudaStream_t s) {
   if (step < 1) return fail(HM_ERR_VALIDATION, "adam: step must be >= 1");
-  const double bc1 = 1.0 - std::pow((double)b1, step);
-  const double bc2 = 1.0 - std::pow((double)b2, step);
+  const double bc1 = 1.0 - std::pow(b1, step);
+  const double bc2 = 1.0 - std::pow(b2, step);
   return adam_impl(w, g, k, n, (float)(lr / bc1), b1, b2, eps, (float)(1.0 / std::sqrt(bc2)), nullptr, gscale, s);
 }
 
 // Same update with {lr/(1-b1^t), 1/sqrt(1-b2^t)} read from device memory.
-int adam_launch_dev(float *w, const float *g, float *k, int64_t n, float b1, float b2, float eps, const float *scalars,
+int adam_launch_dev(float *w, const float *g, float *k, int64_t n, double b1, double b2, double eps, const float *scalars,
                     float gscale, cudaStream_t s) {
   return adam_impl(w, g, k, n, 0.f, b1, b2, eps, 0.f, scalars, gscale, s);
 }
 
 }  // namespace hm
 
-extern "C" int hm_k_adam(float *w, const float *g, float *k, int64_t n, float lr, float beta1, float beta2, float eps,
-                         int32_t step, float grad_scale, void *stream) {
+extern "C" int hm_k_adam(float *w, const float *g, float *k, int64_t n, double lr, double beta1, double beta2,
+                         double eps, int32_t step, float grad_scale, void *stream) {
   return hm::adam_launch(w, g, k, n, lr, beta1, beta2, eps, step, grad_scale, static_cast<cudaStream_t>(stream));
 }

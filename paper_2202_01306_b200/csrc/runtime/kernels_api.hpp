@@ -6,9 +6,9 @@
 #include <cstdint>
 
 namespace hm {
-int adam_launch_dev(float *w, const float *g, float *k, int64_t n, float b1, float b2, float eps,
+int adam_launch_dev(float *w, const float *g, float *k, int64_t n, double b1, double b2, double eps,
                     const float *scalars, float gscale, cudaStream_t s);
-int adam_launch(float *w, const float *g, float *k, int64_t n, float lr, float b1, float b2, float eps, int step,
+int adam_launch(float *w, const float *g, float *k, int64_t n, double lr, double b1, double b2, double eps, int step,
                 float gscale, cudaStream_t s);
 namespace gemm {
 int run(const void *A, const void *B, void *D, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldd,

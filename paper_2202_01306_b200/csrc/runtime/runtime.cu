@@ -86,6 +86,7 @@ struct Action {
   int task = -1, member = -1;
   std::vector<std::pair<int, bool>> waits;  // (item, at_start)
   std::vector<cudaEvent_t> wait_events;     // non-plan dependencies (all-reduce)
+  std::vector<int> xwaits;                  // previous-iteration items (end) this one must follow
   cudaEvent_t done = nullptr;               // kind 5: all-reduce completion
   int64_t count = 0;                        // kind 5: floats reduced
 };
@@ -159,6 +160,7 @@ struct hm_runtime {
   std::vector<hm::Action> actions;
   std::vector<cudaEvent_t> ev_start, ev_end;     // dependencies
   std::vector<cudaEvent_t> ev_tstart, ev_tend;   // timing (external records inside graphs)
+  std::vector<char> ev_live;  // dependency event last recorded eagerly (waitable outside a capture)
   cudaEvent_t ev_iter0 = nullptr, ev_iter1 = nullptr, ev_fork = nullptr, ev_join[4] = {nullptr};
   // CUDA graph of one iteration ([0] plain, [1] with per-kernel timing events)
   bool use_graph = true;
@@ -167,6 +169,8 @@ struct hm_runtime {
   int64_t graph_launches[2] = {0, 0};
   int64_t graph_bytes[2][3] = {{0}};
   float *adam_host = nullptr;  // pinned {lr_t, 1/sqrt(bc2)}
+  double *loss_host = nullptr;  // pinned [64]
+  cudaEvent_t ev_first = nullptr;
   float *adam_dev = nullptr;
   // device pool
   uint8_t *pool = nullptr;
@@ -181,7 +185,8 @@ struct hm_runtime {
   uint8_t *work_store = nullptr;
   hm::Scratch T{};
   int32_t *tokens = nullptr, *labels = nullptr;
-  double *loss_dev = nullptr;
+  double *loss_dev = nullptr;  // [64] per-step loss slots
+  double *loss_cur = nullptr;
   int step = 0;
   // Harmony-DP gradient all-reduce (NCCL), one comm per job
   ncclComm_t comm = nullptr;
@@ -321,7 +326,7 @@ static int head_fwd(hm_runtime &rt, const Acts &A, int u, int64_t s0, const Laye
   HM_TRY(layers::ln_fwd(A.yl, W.w + P.lnf_g, W.w + P.lnf_b, A.lnf, A.meanf, A.rstdf, M, (int)d, s));
   HM_TRY(gemm::run(A.lnf, W.wsh + P.w_head, rt.T.logits, M, rt.Vp, d, d, d, rt.Vp, 0, 0, HM_EPI_STORE_F32, nullptr,
                    nullptr, 0, s, 0));
-  HM_TRY(layers::cross_entropy(rt.T.logits, rt.labels + s0 * rt.S, M, rt.Vp, rt.V, A.dlog, rt.loss_dev,
+  HM_TRY(layers::cross_entropy(rt.T.logits, rt.labels + s0 * rt.S, M, rt.Vp, rt.V, A.dlog, rt.loss_cur,
                                (float)(1.0 / (double)rt.global_tokens), s));
   return HM_OK;
 }
@@ -643,7 +648,7 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
   req.push_back({(void **)&T.logits, rows_u * rt.Vp * 4});
   req.push_back({(void **)&rt.tokens, rows_mb * 4});
   req.push_back({(void **)&rt.labels, rows_mb * 4});
-  req.push_back({(void **)&rt.loss_dev, 256});
+  req.push_back({(void **)&rt.loss_dev, 64 * sizeof(double)});
   req.push_back({(void **)&rt.adam_dev, 256});
   int64_t total = 0;
   for (auto &r : req) total += align_up(r.bytes, 1024);
@@ -694,6 +699,7 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
   rt.ev_end.assign(plan->items.size(), nullptr);
   rt.ev_tstart.assign(plan->items.size(), nullptr);
   rt.ev_tend.assign(plan->items.size(), nullptr);
+  rt.ev_live.assign(plan->items.size(), 0);
   for (size_t i = 0; i < plan->items.size(); ++i) {
     if (plan->items[i].rec.gpu != rank) continue;
     HM_CUDA(cudaEventCreate(&rt.ev_start[i]));
@@ -832,6 +838,58 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
     }
     rt.actions.push_back(std::move(a));
   }
+  // ---- cross-iteration dependencies (pipelined steps) --------------------------
+  // Iteration i+1 may start while iteration i's last swap-outs drain; these
+  // waits keep every host / device buffer hand-off across the boundary exact.
+  auto overlaps = [&](int t1, int t2) {
+    auto &a = plan->tasks[t1];
+    auto &b = plan->tasks[t2];
+    return a.lo <= b.hi && b.lo <= a.hi;
+  };
+  std::vector<int> w_out, k_out, sx_in;
+  std::map<std::pair<int, int>, int> sx_out;  // (layer, member) -> item
+  for (auto &a : rt.actions) {
+    if (a.item < 0 || a.kind < 2) continue;
+    const hm_item &r = plan->items[a.item].rec;
+    if (r.stage == 2 && r.tensor == HM_W) w_out.push_back(a.item);
+    if (r.stage == 2 && r.tensor == HM_K) k_out.push_back(a.item);
+    if (r.stage == 0 && r.tensor == HM_SX) sx_in.push_back(a.item);
+    if (r.stage == 2 && r.tensor == HM_SX) sx_out[{r.layer, r.member}] = a.item;
+  }
+  for (auto &a : rt.actions) {
+    if (a.item < 0) continue;
+    const hm_item &r = plan->items[a.item].rec;
+    if (a.kind == 2 && r.tensor == HM_W)
+      for (int o : w_out)
+        if (overlaps(plan->items[o].rec.task, r.task)) a.xwaits.push_back(o);
+    if (a.kind == 2 && r.tensor == HM_K)
+      for (int o : k_out)
+        if (overlaps(plan->items[o].rec.task, r.task)) a.xwaits.push_back(o);
+    if (a.kind == 3 && r.tensor == HM_SX)
+      for (int o : sx_in)
+        if (plan->items[o].rec.layer == r.layer) a.xwaits.push_back(o);
+    if (a.kind == 0 && plan->tasks[r.task].type == HM_TASK_F)
+      for (int L : rt.trt[r.task].stash_heads) {
+        auto it = sx_out.find({L, r.member});
+        if (it != sx_out.end()) a.xwaits.push_back(it->second);
+      }
+  }
+  // W leaves before K: the next iteration's forward needs W first
+  for (size_t i = 0; i + 1 < rt.actions.size(); ++i) {
+    Action &x = rt.actions[i], &y = rt.actions[i + 1];
+    if (x.kind == 3 && y.kind == 3 && x.task == y.task && x.item >= 0 && y.item >= 0 &&
+        plan->items[x.item].rec.tensor == HM_K && plan->items[y.item].rec.tensor == HM_W)
+      std::swap(x, y);
+  }
+  return HM_OK;
+}
+
+static int join_streams(hm_runtime &rt) {
+  cudaStream_t others[] = {rt.s_h2d, rt.s_d2h, rt.s_update, rt.s_comm};
+  for (size_t i = 0; i < 4; ++i) {
+    HM_CUDA(cudaEventRecord(rt.ev_join[i], others[i]));
+    HM_CUDA(cudaStreamWaitEvent(rt.s_compute, rt.ev_join[i], 0));
+  }
   return HM_OK;
 }
 
@@ -840,18 +898,27 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
 // capture-internal, timing events become external event-record nodes, and
 // waits on the previous iteration's events are dropped (an iteration only
 // starts after the previous one completed).
-static int enqueue_body(hm_runtime &rt, bool capture, int64_t &h2d, int64_t &d2h, int64_t &coll) {
+static int enqueue_body(hm_runtime &rt, bool capture, bool pipelined, int64_t &h2d, int64_t &d2h, int64_t &coll) {
   cudaStream_t sc = rt.s_compute;
   auto rec_time = [&](cudaEvent_t e, cudaStream_t s) -> cudaError_t {
     return capture ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s);
   };
-  HM_CUDA(cudaMemsetAsync(rt.loss_dev, 0, sizeof(double), sc));
-  HM_CUDA(cudaEventRecord(rt.ev_fork, sc));
+  HM_CUDA(cudaMemsetAsync(rt.loss_cur, 0, sizeof(double), sc));
   cudaStream_t others[] = {rt.s_h2d, rt.s_d2h, rt.s_update, rt.s_comm};
-  for (cudaStream_t o : others) HM_CUDA(cudaStreamWaitEvent(o, rt.ev_fork, 0));
+  if (!pipelined) {
+    HM_CUDA(cudaEventRecord(rt.ev_fork, sc));
+    for (cudaStream_t o : others) HM_CUDA(cudaStreamWaitEvent(o, rt.ev_fork, 0));
+  }
   for (Action &a : rt.actions) {
+    // waits on the previous iteration: dropped inside a capture (iterations are
+    // serialised around graph launches) and when that event's last record
+    // happened inside a graph capture (the previous iteration has completed)
+    if (!capture)
+      for (int x : a.xwaits)
+        if (rt.ev_live[x]) HM_CUDA(cudaStreamWaitEvent(a.stream, rt.ev_end[x], 0));
     for (auto &w : a.waits) {
-      if (capture && a.item >= 0 && w.first > a.item) continue;  // previous iteration: already complete
+      const bool prev_iter = a.item >= 0 && w.first > a.item;
+      if (prev_iter && (capture || !rt.ev_live[w.first])) continue;
       HM_CUDA(cudaStreamWaitEvent(a.stream, w.second ? rt.ev_start[w.first] : rt.ev_end[w.first], 0));
     }
     for (cudaEvent_t e : a.wait_events) HM_CUDA(cudaStreamWaitEvent(a.stream, e, 0));
@@ -871,8 +938,12 @@ static int enqueue_body(hm_runtime &rt, bool capture, int64_t &h2d, int64_t &d2h
       case 1: {
         TaskRt &tr = rt.trt[a.task];
         TaskRt &bt = rt.trt[tr.b_task];
-        HM_TRY(adam_launch_dev(rt.slots.w[bt.w_slot], rt.slots.dw[bt.dw_slot], rt.slots.k[tr.k_slot], tr.params,
-                               rt.m.beta1, rt.m.beta2, rt.m.eps, rt.adam_dev, 1.0f, a.stream));
+        if (capture)  // step-dependent scalars read from device memory at replay
+          HM_TRY(adam_launch_dev(rt.slots.w[bt.w_slot], rt.slots.dw[bt.dw_slot], rt.slots.k[tr.k_slot], tr.params,
+                                 rt.m.beta1, rt.m.beta2, rt.m.eps, rt.adam_dev, 1.0f, a.stream));
+        else
+          HM_TRY(adam_launch(rt.slots.w[bt.w_slot], rt.slots.dw[bt.dw_slot], rt.slots.k[tr.k_slot], tr.params,
+                             rt.m.lr, rt.m.beta1, rt.m.beta2, rt.m.eps, rt.step, 1.0f, a.stream));
         break;
       }
       case 2:
@@ -888,11 +959,9 @@ static int enqueue_body(hm_runtime &rt, bool capture, int64_t &h2d, int64_t &d2h
     }
     HM_CUDA(cudaEventRecord(rt.ev_end[a.item], a.stream));
     if (capture) HM_CUDA(rec_time(rt.ev_tend[a.item], a.stream));
+    rt.ev_live[a.item] = capture ? 0 : 1;
   }
-  for (size_t i = 0; i < 4; ++i) {
-    HM_CUDA(cudaEventRecord(rt.ev_join[i], others[i]));
-    HM_CUDA(cudaStreamWaitEvent(sc, rt.ev_join[i], 0));
-  }
+  if (!pipelined) HM_TRY(join_streams(rt));
   return HM_OK;
 }
 
@@ -903,6 +972,7 @@ static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *l
   rt.step += 1;
   cudaStream_t sc = rt.s_compute;
   const int64_t tb = (int64_t)rt.minibatch * rt.S * 4;
+  rt.loss_cur = rt.loss_dev;
   // Adam bias corrections for this step live in device memory so a captured
   // graph replays correctly: {lr / (1 - b1^t), 1 / sqrt(1 - b2^t)}
   rt.adam_host[0] = (float)(rt.m.lr / (1.0 - std::pow((double)rt.m.beta1, rt.step)));
@@ -924,7 +994,7 @@ static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *l
       profiler() = rt.profiling ? &rt.prof : nullptr;
       const int64_t l0 = launch_counter().load();
       HM_CUDA(cudaStreamBeginCapture(sc, cudaStreamCaptureModeRelaxed));
-      int rc = enqueue_body(rt, true, h2d, d2h, coll);
+      int rc = enqueue_body(rt, true, false, h2d, d2h, coll);
       cudaGraph_t g = nullptr;
       cudaError_t ce = cudaStreamEndCapture(sc, &g);
       profiler() = nullptr;
@@ -950,7 +1020,7 @@ static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *l
   } else {
     rt.prof.reset();
     profiler() = rt.profiling ? &rt.prof : nullptr;
-    int rc = enqueue_body(rt, false, h2d, d2h, coll);
+    int rc = enqueue_body(rt, false, false, h2d, d2h, coll);
     profiler() = nullptr;
     HM_TRY(rc);
   }
@@ -989,6 +1059,65 @@ static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *l
       rt.kstats[p.cls][3] += 1;
     }
   }
+  rt.counters[0] = launch_counter().load() - launches0;
+  rt.counters[1] = (int64_t)((double)it_ms * 1e6);
+  rt.counters[2] = rt.pool_bytes;
+  rt.counters[3] = h2d;
+  rt.counters[4] = d2h;
+  rt.counters[5] = 0;
+  rt.counters[6] = coll;
+  return HM_OK;
+}
+
+// `n` back-to-back iterations with cross-iteration overlap: iteration i+1's
+// swap-ins start as soon as the buffers they need are free (e.g. while
+// iteration i's last K swap-out drains).  Eager enqueue; one sync at the end.
+static int run_steps(hm_runtime &rt, int n, const int32_t *tokens, const int32_t *labels, int is_device,
+                     double *losses, int64_t *total_ns) {
+  if (!rt.plan) return fail(HM_ERR_VALIDATION, "no plan loaded");
+  if (n < 1 || n > 64) return fail(HM_ERR_VALIDATION, "run_steps: 1 <= n <= 64");
+  HM_CUDA(cudaSetDevice(rt.device));
+  const int64_t launches0 = launch_counter().load();
+  cudaStream_t sc = rt.s_compute;
+  const int64_t tb = (int64_t)rt.minibatch * rt.S * 4;
+  int64_t h2d = 0, d2h = 0, coll = 0;
+  HM_CUDA(cudaEventRecord(rt.ev_first, sc));
+  cudaStream_t others[] = {rt.s_h2d, rt.s_d2h, rt.s_update, rt.s_comm};
+  for (cudaStream_t o : others) HM_CUDA(cudaStreamWaitEvent(o, rt.ev_first, 0));
+  for (int i = 0; i < n; ++i) {
+    rt.step += 1;
+    rt.loss_cur = rt.loss_dev + i;
+    if (i == n - 1) HM_CUDA(cudaEventRecord(rt.ev_iter0, sc));
+    HM_CUDA(cudaMemcpyAsync(rt.tokens, tokens, tb, is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, sc));
+    HM_CUDA(cudaMemcpyAsync(rt.labels, labels, tb, is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, sc));
+    HM_TRY(enqueue_body(rt, false, true, h2d, d2h, coll));
+  }
+  HM_TRY(join_streams(rt));
+  HM_CUDA(cudaMemcpyAsync(rt.loss_host, rt.loss_dev, n * sizeof(double), cudaMemcpyDeviceToHost, sc));
+  HM_CUDA(cudaEventRecord(rt.ev_iter1, sc));
+  HM_CUDA(cudaEventSynchronize(rt.ev_iter1));
+  rt.iterations += n;
+  for (int i = 0; i < n; ++i)
+    if (losses) losses[i] = rt.loss_host[i] / (double)rt.global_tokens;
+  float ms = 0;
+  HM_CUDA(cudaEventElapsedTime(&ms, rt.ev_first, rt.ev_iter1));
+  if (total_ns) *total_ns = (int64_t)((double)ms * 1e6);
+  // measured ledger / trace of the last iteration (relative to its start)
+  rt.ledger.clear();
+  rt.trace.clear();
+  for (Action &a : rt.actions) {
+    if (a.item < 0) continue;
+    hm_item rec = rt.plan->items[a.item].rec;
+    float t0 = 0, t1 = 0;
+    HM_CUDA(cudaEventElapsedTime(&t0, rt.ev_iter0, rt.ev_start[a.item]));
+    HM_CUDA(cudaEventElapsedTime(&t1, rt.ev_iter0, rt.ev_end[a.item]));
+    rec.start_ns = (int64_t)((double)t0 * 1e6);
+    rec.end_ns = (int64_t)((double)t1 * 1e6);
+    rec.duration_ns = rec.end_ns - rec.start_ns;
+    (rec.is_compute ? rt.trace : rt.ledger).push_back(rec);
+  }
+  float it_ms = 0;
+  HM_CUDA(cudaEventElapsedTime(&it_ms, rt.ev_iter0, rt.ev_iter1));
   rt.counters[0] = launch_counter().load() - launches0;
   rt.counters[1] = (int64_t)((double)it_ms * 1e6);
   rt.counters[2] = rt.pool_bytes;
@@ -1043,7 +1172,10 @@ hm_runtime *hm_runtime_create(int32_t device, const hm_model *model, int64_t alp
   cudaEventCreate(&rt->ev_iter1);
   cudaEventCreateWithFlags(&rt->ev_fork, cudaEventDisableTiming);
   for (auto &e : rt->ev_join) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-  if (cudaHostAlloc(&rt->adam_host, 64, cudaHostAllocDefault) != cudaSuccess) return bad(HM_ERR_DEVICE, "pinned alloc");
+  if (cudaHostAlloc(&rt->adam_host, 64, cudaHostAllocDefault) != cudaSuccess ||
+      cudaHostAlloc(&rt->loss_host, 64 * sizeof(double), cudaHostAllocDefault) != cudaSuccess)
+    return bad(HM_ERR_DEVICE, "pinned alloc");
+  cudaEventCreate(&rt->ev_first);
   if (cudaHostAlloc(&rt->w_host, rt->total_params * 4, cudaHostAllocDefault) != cudaSuccess ||
       cudaHostAlloc(&rt->k_host, rt->total_params * 8, cudaHostAllocDefault) != cudaSuccess)
     return bad(HM_ERR_DEVICE, "pinned host arena allocation failed (" + std::to_string(rt->total_params * 12) + " B)");
@@ -1094,6 +1226,12 @@ int hm_runtime_run_iteration(hm_runtime *rt, const int32_t *tokens, const int32_
                              double *loss_out) {
   if (!rt) return hm::fail(HM_ERR_VALIDATION, "null runtime");
   return hm::run_iteration(*rt, tokens, labels, is_device, loss_out);
+}
+
+int hm_runtime_run_steps(hm_runtime *rt, int32_t n, const int32_t *tokens, const int32_t *labels, int32_t is_device,
+                         double *losses, int64_t *total_ns) {
+  if (!rt) return hm::fail(HM_ERR_VALIDATION, "null runtime");
+  return hm::run_steps(*rt, n, tokens, labels, is_device, losses, total_ns);
 }
 
 int32_t hm_runtime_ledger_count(const hm_runtime *rt) { return rt ? (int32_t)rt->ledger.size() : 0; }
@@ -1171,6 +1309,8 @@ void hm_runtime_free(hm_runtime *rt) {
   if (rt->ev_fork) cudaEventDestroy(rt->ev_fork);
   for (auto &e : rt->ev_join) if (e) cudaEventDestroy(e);
   if (rt->adam_host) cudaFreeHost(rt->adam_host);
+  if (rt->loss_host) cudaFreeHost(rt->loss_host);
+  if (rt->ev_first) cudaEventDestroy(rt->ev_first);
   if (rt->ev_iter0) cudaEventDestroy(rt->ev_iter0);
   if (rt->ev_iter1) cudaEventDestroy(rt->ev_iter1);
   for (auto &e : rt->ar_events) cudaEventDestroy(e);

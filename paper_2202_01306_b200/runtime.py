@@ -158,6 +158,24 @@ class HarmonyRuntime:
         NL.check(rc)
         return loss.value
 
+    def run_steps(self, n: int, tokens, labels) -> tuple[list[float], float]:
+        """``n`` pipelined iterations (cross-iteration overlap); returns the
+        per-iteration losses and the device seconds of all n iterations."""
+        if self.plan is None:
+            raise ValidationError("load() a plan first")
+        losses = (C.c_double * n)()
+        total = C.c_int64(0)
+        if hasattr(tokens, "is_cuda") and tokens.is_cuda:
+            rc = self.lib.hm_runtime_run_steps(self.handle, n, C.c_void_p(tokens.data_ptr()),
+                                               C.c_void_p(labels.data_ptr()), 1, losses, C.byref(total))
+        else:
+            t = np.ascontiguousarray(tokens, dtype=np.int32)
+            lb = np.ascontiguousarray(labels, dtype=np.int32)
+            rc = self.lib.hm_runtime_run_steps(self.handle, n, t.ctypes.data, lb.ctypes.data, 0, losses,
+                                               C.byref(total))
+        NL.check(rc)
+        return list(losses), total.value / 1e9
+
     def counters(self) -> dict:
         out = (C.c_int64 * 8)()
         NL.check(self.lib.hm_runtime_counters(self.handle, out, 8))

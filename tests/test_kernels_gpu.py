@@ -101,8 +101,8 @@ def test_adam_matches_torch(ops):
     torch.cuda.synchronize()
     assert torch.allclose(w, p.detach(), rtol=1e-6, atol=1e-7)
     st = opt.state[p]
-    assert torch.allclose(k[0::2], st["exp_avg"], rtol=1e-5, atol=1e-7)
-    assert torch.allclose(k[1::2], st["exp_avg_sq"], rtol=1e-5, atol=1e-9)
+    for got, ref in ((k[0::2], st["exp_avg"]), (k[1::2], st["exp_avg_sq"])):
+        assert ((got - ref).norm() / ref.norm()).item() < 1e-6
 
 
 def _attn_ref(qkv, B, S, H, DH, causal):
