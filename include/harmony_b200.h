@@ -180,6 +180,17 @@ int hm_runtime_counters(const hm_runtime *rt, int64_t *out, int32_t cap);
 int hm_nccl_unique_id(const char *nccl_path, uint8_t *out);
 int hm_runtime_init_comm(hm_runtime *rt, const char *nccl_path, const uint8_t *id, int32_t nranks,
                          int32_t rank);
+/* Harmony-PP across processes (one per GPU): W, K and stash arenas live in
+ * one POSIX shared-memory segment registered as pinned memory in every rank
+ * (rank 0 creates it, then the others attach).  Call before load_plan. */
+int hm_runtime_share_arenas(hm_runtime *rt, const char *shm_name, int32_t create, int64_t stash_bytes);
+/* After load_plan: export this rank's device pool (CUDA IPC handle), the
+ * offsets of its peer-visible source buffers and of its per-item completion
+ * counters; every rank imports every peer's blob.  Cross-GPU hand-offs are
+ * then pulled with cudaMemcpyAsync over NVLink and ordered by device-side
+ * waits on the producer's counters (cuStreamWaitValue32). */
+int hm_runtime_ipc_export(hm_runtime *rt, uint8_t *buf, int32_t cap);
+int hm_runtime_ipc_import(hm_runtime *rt, const uint8_t *buf, int32_t len);
 /* Record each iteration into a CUDA graph after the first (default on) and
  * replay it: one launch per iteration instead of thousands. */
 int hm_runtime_set_graph(hm_runtime *rt, int32_t enable);

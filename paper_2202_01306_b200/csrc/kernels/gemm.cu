@@ -18,6 +18,7 @@
 #include <cuda.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <tuple>
 #include <map>
@@ -364,6 +365,18 @@ static int make_map(CUtensorMap *out, const void *ptr, uint64_t d0, uint64_t d1,
   return HM_OK;
 }
 
+static int num_sms();
+
+// Tile width: minimise (waves x tile width) over BN in {128, 256}, with a 5%
+// preference for the wider tile (half the A re-reads per FLOP).
+static int pick_bn(int64_t M, int64_t N) {
+  const int64_t sms = num_sms();
+  const int64_t mb = (M + BM - 1) / BM;
+  const int64_t w128 = (mb * ((N + 127) / 128) + sms - 1) / sms;
+  const int64_t w256 = (mb * ((N + 255) / 256) + sms - 1) / sms;
+  return (double)(w128 * 128) < 0.95 * (double)(w256 * 256) ? 128 : 256;
+}
+
 static int num_sms() {
   static int n = 0;
   if (!n) {
@@ -410,7 +423,11 @@ int run(const void *A, const void *B, void *D, int64_t M, int64_t N, int64_t K, 
     return fail(HM_ERR_VALIDATION, "gemm: epilogue needs an aux tensor");
   if (aux && ((ld_aux * (epi == HM_EPI_RESID_F32 ? 4 : 2)) % 16 || ((uintptr_t)aux & 15)))
     return fail(HM_ERR_VALIDATION, "gemm: aux must be 16B aligned with 16B pitch");
-  int bn = force_bn ? force_bn : (N >= 3072 ? 256 : 128);
+  static const int env_bn = [] {
+    const char *e = getenv("HM_GEMM_BN");
+    return e ? atoi(e) : 0;
+  }();
+  int bn = force_bn ? force_bn : env_bn ? env_bn : pick_bn(M, N);
   Args a{};
   a.M = (int)M; a.N = (int)N; a.K = (int)K;
   a.num_m = (int)((M + BM - 1) / BM);

@@ -16,7 +16,11 @@
 // Device memory is one pool allocated at load time and checked against
 // alpha; slots are reused round-robin and every reuse waits on the event
 // that ends the previous occupant's last use.
+#include <cuda.h>
 #include <cuda_bf16.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cmath>
@@ -74,19 +78,27 @@ struct TaskRt {
   std::vector<int> members;           // member compute item ids
   std::vector<int64_t> s0;            // member sample offsets
   std::set<int> stash_heads;          // F: layers whose input is stashed
+  // Harmony-PP across GPUs (peer-to-peer hand-offs)
+  float *in_buf = nullptr;            // receive buffer: X (F), dY or the Y seam (B)
+  float *out_buf = nullptr;           // source buffer read by the peer: Y (F), dX (B)
+  bool ship_input = false;            // last F with a remote shared B: ship the shared pack's input
+  bool remote_shared = false;         // shared B whose forward ran on another GPU: recompute
 };
 
 struct Action {
   int item = -1;
-  int kind = 0;  // 0 = F/B member, 1 = U Adam, 2 = H2D, 3 = D2H, 4 = D2D
+  int kind = 0;  // 0 = F/B member, 1 = U Adam, 2 = H2D, 3 = D2H, 5 = all-reduce, 6 = peer copy
   cudaStream_t stream = nullptr;
   void *dst = nullptr;
   const void *src = nullptr;
   int64_t bytes = 0;
   int task = -1, member = -1;
+  int peer_rank = -1, peer_task = -1;       // kind 6: producer of the peer copy
+  int64_t peer_off = 0;                     // kind 6: byte offset inside the producer's source buffer
   std::vector<std::pair<int, bool>> waits;  // (item, at_start)
   std::vector<cudaEvent_t> wait_events;     // non-plan dependencies (all-reduce)
   std::vector<int> xwaits;                  // previous-iteration items (end) this one must follow
+  std::vector<std::pair<int, int>> rwaits;  // (item on another rank, iteration lag 0/1): signal waits
   cudaEvent_t done = nullptr;               // kind 5: all-reduce completion
   int64_t count = 0;                        // kind 5: floats reduced
 };
@@ -187,18 +199,60 @@ struct hm_runtime {
   int32_t *tokens = nullptr, *labels = nullptr;
   double *loss_dev = nullptr;  // [64] per-step loss slots
   double *loss_cur = nullptr;
+  bool count_loss = true;
   int step = 0;
   // Harmony-DP gradient all-reduce (NCCL), one comm per job
   ncclComm_t comm = nullptr;
   int nranks = 1;
   cudaStream_t s_comm = nullptr;
   std::vector<cudaEvent_t> ar_events;
+  // Harmony-PP across processes
+  bool p2p_mode = false;
+  bool shared_arena = false, shared_owner = false;
+  std::string shm_name;
+  void *shm_ptr = nullptr;
+  int64_t shm_bytes = 0;
+  uint32_t *sig = nullptr;  // [n_items] per-item completion counters (iteration number)
+  int64_t sig_off = 0;
+  std::map<int, int64_t> out_off;  // my task -> offset of its P2P source buffer in my pool
+  std::vector<uint8_t *> peer_pool;
+  std::vector<std::map<int, int64_t>> peer_out_off;
+  std::vector<int64_t> peer_sig_off;
+  double *loss_sink = nullptr;  // CE of recompute passes (not part of the loss)
+  int64_t p2p_bytes = 0;
   // last iteration
   std::vector<hm_item> ledger, trace;
   int64_t counters[8] = {0};
 };
 
 namespace hm {
+
+// ---------------------------------------------------------------------------
+// stream memory operations (driver API, resolved at run time): device-side
+// counters that order work across processes / GPUs without host round trips
+// ---------------------------------------------------------------------------
+using MemopWaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using MemopWriteFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+struct Memops {
+  MemopWaitFn wait = nullptr;
+  MemopWriteFn write = nullptr;
+};
+static Memops &memops() {
+  static Memops m;
+  static bool init = false;
+  if (!init) {
+    init = true;
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      m.wait = reinterpret_cast<MemopWaitFn>(p);
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      m.write = reinterpret_cast<MemopWriteFn>(p);
+  }
+  return m;
+}
 
 // ---------------------------------------------------------------------------
 // model layout
@@ -326,7 +380,8 @@ static int head_fwd(hm_runtime &rt, const Acts &A, int u, int64_t s0, const Laye
   HM_TRY(layers::ln_fwd(A.yl, W.w + P.lnf_g, W.w + P.lnf_b, A.lnf, A.meanf, A.rstdf, M, (int)d, s));
   HM_TRY(gemm::run(A.lnf, W.wsh + P.w_head, rt.T.logits, M, rt.Vp, d, d, d, rt.Vp, 0, 0, HM_EPI_STORE_F32, nullptr,
                    nullptr, 0, s, 0));
-  HM_TRY(layers::cross_entropy(rt.T.logits, rt.labels + s0 * rt.S, M, rt.Vp, rt.V, A.dlog, rt.loss_cur,
+  HM_TRY(layers::cross_entropy(rt.T.logits, rt.labels + s0 * rt.S, M, rt.Vp, rt.V, A.dlog,
+                               rt.count_loss ? rt.loss_cur : rt.loss_sink,
                                (float)(1.0 / (double)rt.global_tokens), s));
   return HM_OK;
 }
@@ -388,7 +443,8 @@ static bool is_head(const hm_runtime &rt, int L) { return L == rt.R - 1; }
 // layer's activations (n samples, member at s0); otherwise one scratch layer
 // slot is reused and the hidden state ping-pongs between two buffers.
 static int forward_pack(hm_runtime &rt, TaskRt &tr, int lo, int hi, int u, int64_t s0, const float *x_in,
-                        const int32_t *tok_in, uint8_t *store, int64_t n, int64_t s_off, float *y_final) {
+                        const int32_t *tok_in, uint8_t *store, int64_t n, int64_t s_off, float *y_final,
+                        float *ship = nullptr) {
   const int64_t M = (int64_t)u * rt.S, d = rt.m.d_model;
   cudaStream_t s = rt.s_compute;
   const float *x = x_in;
@@ -408,6 +464,8 @@ static int forward_pack(hm_runtime &rt, TaskRt &tr, int lo, int hi, int u, int64
         x = dst;
       }
     }
+    if (L == lo && ship)  // Harmony-PP seam: the shared pack's input goes to the peer
+      HM_CUDA(cudaMemcpyAsync(ship, x, M * d * 4, cudaMemcpyDeviceToDevice, s));
     if (tr.stash_heads.count(L)) {  // capture the input of a backward-pack head
       uint8_t *dst = rt.stash_dev.at(L);
       if (L == 0) {
@@ -474,24 +532,39 @@ static int run_member(hm_runtime &rt, int task, int g) {
     if (t.type == HM_TASK_B) HM_CUDA(cudaMemsetAsync(rt.slots.dw[tr.dw_slot], 0, tr.params * 4, s));
   }
   if (t.type == HM_TASK_F) {
-    const float *x_in = t.lo == 0 ? nullptr : rt.carry[tr.carry_in] + s0 * rowsd;
+    const float *x_in = t.lo == 0 ? nullptr
+                        : tr.in_buf ? tr.in_buf + s0 * rowsd
+                                    : rt.carry[tr.carry_in] + s0 * rowsd;
     const int32_t *tok = rt.tokens + s0 * rt.S;
     if (tr.store_shared)
       return forward_pack(rt, tr, t.lo, t.hi, u, s0, x_in, tok, rt.shared_store, rt.minibatch, s0, nullptr);
-    float *y = tr.carry_out >= 0 ? rt.carry[tr.carry_out] + s0 * rowsd : nullptr;
+    if (tr.ship_input)
+      return forward_pack(rt, tr, t.lo, t.hi, u, s0, x_in, tok, nullptr, 0, 0, nullptr, tr.out_buf + s0 * rowsd);
+    float *y = tr.out_buf ? tr.out_buf + s0 * rowsd : tr.carry_out >= 0 ? rt.carry[tr.carry_out] + s0 * rowsd : nullptr;
     return forward_pack(rt, tr, t.lo, t.hi, u, s0, x_in, tok, nullptr, 0, 0, y);
   }
   // backward
-  float *dx = (t.lo == 0) ? nullptr : rt.dcarry[tr.carry_out] + s0 * rowsd;
+  float *dx = (t.lo == 0) ? nullptr : tr.out_buf ? tr.out_buf + s0 * rowsd : rt.dcarry[tr.carry_out] + s0 * rowsd;
   if (tr.from_shared)
     return backward_pack(rt, tr, t.lo, t.hi, u, s0, rt.shared_store, rt.minibatch, s0, nullptr, dx,
                          rt.tokens + s0 * rt.S);
+  if (tr.remote_shared) {
+    // the shared pack's forward ran on the peer: recompute it from the shipped
+    // input (its cross-entropy is not counted again), then backward from the head
+    const float *x_in = t.lo == 0 ? nullptr : tr.in_buf + s0 * rowsd;
+    const int32_t *tok = rt.tokens + s0 * rt.S;
+    rt.count_loss = false;
+    int rc = forward_pack(rt, tr, t.lo, t.hi, u, s0, x_in, tok, rt.work_store, u, 0, nullptr);
+    rt.count_loss = true;
+    HM_TRY(rc);
+    return backward_pack(rt, tr, t.lo, t.hi, u, s0, rt.work_store, u, 0, nullptr, dx, tok);
+  }
   // recompute from the stash, keeping activations in the work store
   uint8_t *st = rt.slots.stash_in[tr.stash_slot];
   const float *x_in = t.lo == 0 ? nullptr : reinterpret_cast<const float *>(st) + s0 * rowsd;
   const int32_t *tok = t.lo == 0 ? reinterpret_cast<const int32_t *>(st) + s0 * rt.S : rt.tokens + s0 * rt.S;
   HM_TRY(forward_pack(rt, tr, t.lo, t.hi, u, s0, x_in, tok, rt.work_store, u, 0, nullptr));
-  const float *dy = rt.dcarry[tr.carry_in] + s0 * rowsd;
+  const float *dy = tr.in_buf ? tr.in_buf + s0 * rowsd : rt.dcarry[tr.carry_in] + s0 * rowsd;
   return backward_pack(rt, tr, t.lo, t.hi, u, s0, rt.work_store, u, 0, dy, dx, tok);
 }
 
@@ -510,11 +583,12 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
   for (auto &t : plan->tasks)
     if (t.dev_id == rank) mine.push_back(t.index);
   if (mine.empty()) return fail(HM_ERR_VALIDATION, "no task is bound to this rank");
-  for (auto &it : plan->items) {
-    if (it.rec.gpu != rank) continue;
-    if (!it.rec.is_compute && it.rec.channel == HM_PEER2PEER)
-      return fail(HM_ERR_VALIDATION, "peer-to-peer hand-offs (Harmony-PP with N>1) are not executed by this build yet");
-  }
+  rt.p2p_mode = false;
+  for (auto &it : plan->items)
+    if (!it.rec.is_compute && it.rec.channel == HM_PEER2PEER) rt.p2p_mode = true;
+  if (rt.p2p_mode && !rt.shared_arena)
+    return fail(HM_ERR_VALIDATION,
+                "peer-to-peer hand-offs (Harmony-PP, N>1) need shared host arenas: call hm_runtime_share_arenas");
   int last_f = -1, shared_b = -1;
   int64_t u_max = 1, pmax = 0;
   std::vector<int> heads;  // stash head layers produced here
@@ -539,24 +613,53 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
         heads.push_back(e.layer);
       }
   }
-  if (last_f < 0 || shared_b < 0) return fail(HM_ERR_VALIDATION, "rank holds no complete F/B chain");
-  if (plan->tasks[last_f].lo != plan->tasks[shared_b].lo || plan->tasks[last_f].hi != plan->tasks[shared_b].hi)
-    return fail(HM_ERR_VALIDATION, "shared pack mismatch");
-  rt.trt[last_f].store_shared = true;
-  rt.trt[shared_b].from_shared = true;
-  rt.shared_lo = plan->tasks[last_f].lo;
-  rt.shared_hi = plan->tasks[last_f].hi;
+  // the last F task of the graph (its Y feeds the shared B task)
+  int graph_last_f = -1;
   for (auto &t : plan->tasks)
-    if (t.dev_id == rank && t.hi == rt.R - 1 && t.type != HM_TASK_U && !(t.index == last_f || t.index == shared_b))
+    if (t.type == HM_TASK_F && (t.dev_id == rank || rt.p2p_mode)) graph_last_f = std::max(graph_last_f, t.index);
+  const bool local_seam = last_f >= 0 && shared_b >= 0 && last_f == graph_last_f;
+  if (!rt.p2p_mode && !local_seam) return fail(HM_ERR_VALIDATION, "rank holds no complete F/B chain");
+  if (local_seam) {
+    if (plan->tasks[last_f].lo != plan->tasks[shared_b].lo || plan->tasks[last_f].hi != plan->tasks[shared_b].hi)
+      return fail(HM_ERR_VALIDATION, "shared pack mismatch");
+    rt.trt[last_f].store_shared = true;
+    rt.trt[shared_b].from_shared = true;
+    rt.shared_lo = plan->tasks[last_f].lo;
+    rt.shared_hi = plan->tasks[last_f].hi;
+  } else {
+    rt.shared_lo = rt.shared_hi = -1;
+  }
+  // peer-to-peer roles of my tasks
+  for (int ti : mine) {
+    TaskInfo &t = plan->tasks[ti];
+    TaskRt &tr = rt.trt[ti];
+    for (auto &e : t.inputs)
+      if (e.channel == HM_PEER2PEER) {
+        if (t.type == HM_TASK_B && e.tensor == HM_Y) tr.remote_shared = true;
+        tr.in_buf = reinterpret_cast<float *>(1);  // allocated below
+      }
+    for (auto &e : t.outputs)
+      if (e.channel == HM_PEER2PEER) {
+        tr.out_buf = reinterpret_cast<float *>(1);
+        if (t.type == HM_TASK_F && e.tensor == HM_Y && ti == graph_last_f) tr.ship_input = true;
+      }
+    if (t.type != HM_TASK_U && t.hi == rt.R - 1 && !(tr.store_shared || tr.from_shared || tr.ship_input ||
+                                                     tr.remote_shared))
       return fail(HM_ERR_INTERNAL, "head layer outside the shared pack");
+  }
+  // stash regions of every head in the graph (the host arena may be shared)
+  std::map<int, int64_t> all_heads;  // head -> D * x bytes
+  for (auto &t : plan->tasks)
+    for (auto &e : t.outputs)
+      if (e.tensor == HM_SX && e.channel == HM_MESSAGE_PASSING)
+        all_heads[e.layer] = (int64_t)minibatch * rt.S * (e.layer == 0 ? 4 : d * 4);
 
   // ---- slot assignment (round robin in device order) -------------------------
   const int NW = 3, NDW = 2, NK = 2, NST = 2;
   int wn = 0, dwn = 0, kn = 0, stn = 0, fcur = -1, bcur = -1;
   std::vector<int> w_owner(NW, -1), dw_owner(NDW, -1), k_owner(NK, -1), st_owner(NST, -1);
   int64_t stash_in_max = 0;
-  std::map<int, int64_t> stash_bytes;  // head -> D * x bytes
-  for (int L : heads) stash_bytes[L] = (int64_t)minibatch * rt.S * (L == 0 ? 4 : d * 4);
+  std::map<int, int64_t> stash_bytes = all_heads;
   for (int ti : mine) {
     TaskInfo &t = plan->tasks[ti];
     TaskRt &tr = rt.trt[ti];
@@ -569,6 +672,7 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
     tr.w_slot = wn;
     wn = (wn + 1) % NW;
     if (t.type == HM_TASK_F) {
+      if (rt.p2p_mode) continue;
       tr.carry_in = fcur;
       if (ti != last_f) {
         tr.carry_out = (fcur + 1) & 1;
@@ -578,16 +682,18 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
     } else {
       tr.dw_slot = dwn;
       dwn = (dwn + 1) % NDW;
-      tr.carry_in = bcur;
-      if (t.lo > 0) {
-        tr.carry_out = (bcur + 1) & 1;
-        bcur = tr.carry_out;
+      if (!rt.p2p_mode) {
+        tr.carry_in = bcur;
+        if (t.lo > 0) {
+          tr.carry_out = (bcur + 1) & 1;
+          bcur = tr.carry_out;
+        }
       }
       if (t.recompute) {
         tr.stash_slot = stn;
         stn = (stn + 1) % NST;
         stash_in_max = std::max(stash_in_max, stash_bytes.count(t.lo) ? stash_bytes[t.lo] : 0);
-        if (tr.carry_in < 0) return fail(HM_ERR_INTERNAL, "recompute B task without a gradient carry");
+        if (tr.carry_in < 0 && !tr.in_buf) return fail(HM_ERR_INTERNAL, "recompute B task without a gradient input");
       }
     }
   }
@@ -597,13 +703,15 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
   int64_t max_recompute_layers = 1;
   for (int ti : mine) {
     auto &t = plan->tasks[ti];
-    if (t.type == HM_TASK_B && t.recompute) max_recompute_layers = std::max<int64_t>(max_recompute_layers, t.hi - t.lo + 1);
+    if (t.type == HM_TASK_B && (t.recompute || rt.trt[ti].remote_shared))
+      max_recompute_layers = std::max<int64_t>(max_recompute_layers, t.hi - t.lo + 1);
   }
   int64_t work_bytes = 0;
-  for (int j = 0; j < max_recompute_layers; ++j) work_bytes += store_layer_bytes(rt, false, u_max);
+  for (int j = 0; j < max_recompute_layers; ++j) work_bytes += store_layer_bytes(rt, j == max_recompute_layers - 1, u_max);
   work_bytes = std::max(work_bytes, store_layer_bytes(rt, true, u_max));
   int64_t shared_bytes = 0;
-  for (int L = rt.shared_lo; L <= rt.shared_hi; ++L) shared_bytes += store_layer_bytes(rt, is_head(rt, L), minibatch);
+  if (rt.shared_lo >= 0)
+    for (int L = rt.shared_lo; L <= rt.shared_hi; ++L) shared_bytes += store_layer_bytes(rt, is_head(rt, L), minibatch);
   struct Req { void **ptr; int64_t bytes; };
   std::vector<Req> req;
   rt.slots.w.assign(NW, nullptr);
@@ -623,10 +731,22 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
     req.push_back({(void **)&rt.dcarry[i], rows_mb * d * 4});
   }
   std::vector<std::pair<int, uint8_t **>> stash_ptrs;
-  for (auto &kv : stash_bytes) {
-    rt.stash_dev[kv.first] = nullptr;
-  }
+  rt.stash_dev.clear();
+  for (int L : heads) rt.stash_dev[L] = nullptr;
   for (auto &kv : rt.stash_dev) req.push_back({(void **)&kv.second, stash_bytes[kv.first]});
+  // peer-to-peer buffers: one receive and one source buffer per task (no reuse
+  // inside an iteration; reuse across iterations is signal-ordered)
+  std::vector<std::pair<int, float **>> out_bufs;
+  for (int ti : mine) {
+    TaskRt &tr = rt.trt[ti];
+    if (tr.in_buf) req.push_back({(void **)&tr.in_buf, rows_mb * d * 4});
+    if (tr.out_buf) {
+      req.push_back({(void **)&tr.out_buf, rows_mb * d * 4});
+      out_bufs.push_back({ti, &tr.out_buf});
+    }
+  }
+  req.push_back({(void **)&rt.sig, (int64_t)plan->items.size() * 4 + 64});
+  req.push_back({(void **)&rt.loss_sink, 256});
   req.push_back({(void **)&rt.shared_store, shared_bytes});
   req.push_back({(void **)&rt.work_store, work_bytes});
   Scratch &T = rt.T;
@@ -667,6 +787,9 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
     off += align_up(r.bytes, 1024);
   }
   HM_CUDA(cudaMemset(rt.pool, 0, total));
+  rt.out_off.clear();
+  for (auto &ob : out_bufs) rt.out_off[ob.first] = reinterpret_cast<uint8_t *>(*ob.second) - rt.pool;
+  rt.sig_off = reinterpret_cast<uint8_t *>(rt.sig) - rt.pool;
   // host stash arena
   int64_t sh = 0;
   rt.stash_host_off.clear();
@@ -675,6 +798,7 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
     sh += align_up(kv.second, 4096);
   }
   if (sh > rt.stash_host_bytes) {
+    if (rt.shared_arena) return fail(HM_ERR_VALIDATION, "shared stash arena too small: need " + std::to_string(sh));
     if (rt.stash_host) cudaFreeHost(rt.stash_host);
     rt.stash_host = nullptr;
     HM_CUDA(cudaHostAlloc(&rt.stash_host, std::max<int64_t>(sh, 4096), cudaHostAllocDefault));
@@ -761,8 +885,10 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
     a.item = (int)i;
     a.task = r.task;
     a.member = r.member;
-    for (auto &dp : plan->items[i].deps)
+    for (auto &dp : plan->items[i].deps) {
       if (plan->items[dp.first].rec.gpu == rank) a.waits.push_back(dp);
+      else a.rwaits.push_back({dp.first, 0});  // produced on another GPU this iteration
+    }
     TaskInfo &t = plan->tasks[r.task];
     TaskRt &tr = rt.trt[r.task];
     if (r.is_compute) {
@@ -806,6 +932,19 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
         a.dst = rt.slots.k[tr.k_slot];
         if (r.nbytes != tr.params * 8) return fail(HM_ERR_INTERNAL, "K swap-in size disagrees with the model layout");
         if (k_wait.count(r.task)) a.waits.push_back({k_wait[r.task], false});
+      } else if (r.channel == HM_PEER2PEER) {
+        // pull the producer's output over NVLink into this task's receive buffer
+        a.kind = 6;
+        a.stream = rt.s_p2p_in;
+        const int64_t per = (int64_t)rt.S * d * 4;
+        const int64_t off = r.peer_member >= 0 ? tr.s0[r.member] * per : 0;
+        const int64_t expect = r.peer_member >= 0 ? (int64_t)t.group[r.member] * per : (int64_t)minibatch * per;
+        if (r.nbytes != expect) return fail(HM_ERR_INTERNAL, "peer hand-off size disagrees with the activation layout");
+        if (!tr.in_buf) return fail(HM_ERR_INTERNAL, "peer hand-off without a receive buffer");
+        a.dst = reinterpret_cast<uint8_t *>(tr.in_buf) + off;
+        a.peer_rank = plan->tasks[r.peer_task].dev_id;
+        a.peer_task = r.peer_task;
+        a.peer_off = off;
       } else if (r.channel == HM_MESSAGE_PASSING && r.tensor == HM_SX) {
         if (!rt.stash_host_off.count(r.layer)) return fail(HM_ERR_INTERNAL, "stash-in of an unknown head");
         a.src = rt.stash_host + rt.stash_host_off[r.layer];
@@ -846,33 +985,43 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
     auto &b = plan->tasks[t2];
     return a.lo <= b.hi && b.lo <= a.hi;
   };
-  std::vector<int> w_out, k_out, sx_in;
-  std::map<std::pair<int, int>, int> sx_out;  // (layer, member) -> item
-  for (auto &a : rt.actions) {
-    if (a.item < 0 || a.kind < 2) continue;
-    const hm_item &r = plan->items[a.item].rec;
-    if (r.stage == 2 && r.tensor == HM_W) w_out.push_back(a.item);
-    if (r.stage == 2 && r.tensor == HM_K) k_out.push_back(a.item);
-    if (r.stage == 0 && r.tensor == HM_SX) sx_in.push_back(a.item);
-    if (r.stage == 2 && r.tensor == HM_SX) sx_out[{r.layer, r.member}] = a.item;
+  std::vector<int> w_out, k_out, sx_in, p2p_in;
+  std::map<std::pair<int, int>, int> sx_out;  // (layer, member) -> item (the F task's rank)
+  for (size_t i = 0; i < plan->items.size(); ++i) {
+    const hm_item &r = plan->items[i].rec;
+    if (r.is_compute) continue;
+    if (r.stage == 2 && r.tensor == HM_W) w_out.push_back((int)i);
+    if (r.stage == 2 && r.tensor == HM_K) k_out.push_back((int)i);
+    if (r.stage == 0 && r.tensor == HM_SX) sx_in.push_back((int)i);
+    if (r.stage == 2 && r.tensor == HM_SX && r.gpu == rank) sx_out[{r.layer, r.member}] = (int)i;
+    if (r.channel == HM_PEER2PEER) p2p_in.push_back((int)i);
   }
+  auto xdep = [&](Action &a, int item) {
+    if (plan->items[item].rec.gpu == rank) a.xwaits.push_back(item);
+    else a.rwaits.push_back({item, 1});
+  };
   for (auto &a : rt.actions) {
     if (a.item < 0) continue;
     const hm_item &r = plan->items[a.item].rec;
-    if (a.kind == 2 && r.tensor == HM_W)
+    if (a.kind == 2 && r.tensor == HM_W)  // host W region rewritten by last iteration's swap-out
       for (int o : w_out)
-        if (overlaps(plan->items[o].rec.task, r.task)) a.xwaits.push_back(o);
+        if (overlaps(plan->items[o].rec.task, r.task)) xdep(a, o);
     if (a.kind == 2 && r.tensor == HM_K)
       for (int o : k_out)
-        if (overlaps(plan->items[o].rec.task, r.task)) a.xwaits.push_back(o);
-    if (a.kind == 3 && r.tensor == HM_SX)
+        if (overlaps(plan->items[o].rec.task, r.task)) xdep(a, o);
+    if (a.kind == 3 && r.tensor == HM_SX)  // host stash region still read by last iteration's stash-in
       for (int o : sx_in)
-        if (plan->items[o].rec.layer == r.layer) a.xwaits.push_back(o);
+        if (plan->items[o].rec.layer == r.layer) xdep(a, o);
     if (a.kind == 0 && plan->tasks[r.task].type == HM_TASK_F)
       for (int L : rt.trt[r.task].stash_heads) {
         auto it = sx_out.find({L, r.member});
-        if (it != sx_out.end()) a.xwaits.push_back(it->second);
+        if (it != sx_out.end()) xdep(a, it->second);
       }
+    if (a.kind == 0 && rt.trt[r.task].out_buf)  // peers still copying last iteration's output
+      for (int o : p2p_in)
+        if (plan->items[o].rec.peer_task == r.task) xdep(a, o);
+    if (a.kind == 6)  // my receive buffer is read by last iteration's compute of this task
+      xdep(a, rt.trt[r.task].members.back());
   }
   // W leaves before K: the next iteration's forward needs W first
   for (size_t i = 0; i + 1 < rt.actions.size(); ++i) {
@@ -922,6 +1071,18 @@ static int enqueue_body(hm_runtime &rt, bool capture, bool pipelined, int64_t &h
       HM_CUDA(cudaStreamWaitEvent(a.stream, w.second ? rt.ev_start[w.first] : rt.ev_end[w.first], 0));
     }
     for (cudaEvent_t e : a.wait_events) HM_CUDA(cudaStreamWaitEvent(a.stream, e, 0));
+    for (auto &rw : a.rwaits) {  // produced on another GPU: wait for its device-side counter
+      const int64_t want = rt.step - rw.second;
+      if (want < 1) continue;
+      const int peer = rt.plan->items[rw.first].rec.gpu;
+      if (peer >= (int)rt.peer_pool.size() || !rt.peer_pool[peer])
+        return fail(HM_ERR_VALIDATION, "peer " + std::to_string(peer) + " not imported (hm_runtime_ipc_import)");
+      const CUdeviceptr flag =
+          reinterpret_cast<CUdeviceptr>(rt.peer_pool[peer] + rt.peer_sig_off[peer]) + 4 * (CUdeviceptr)rw.first;
+      if (!memops().wait) return fail(HM_ERR_DEVICE, "cuStreamWaitValue32 unavailable");
+      if (memops().wait(a.stream, flag, (cuuint32_t)want, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+        return fail(HM_ERR_DEVICE, "cuStreamWaitValue32 failed");
+    }
     if (a.kind == 5) {
       ncclResult_t nr = nccl().all_reduce(a.dst, a.dst, (size_t)a.count, ncclFloat32, ncclSum, rt.comm, a.stream);
       if (nr != ncclSuccess) return fail(HM_ERR_DEVICE, std::string("ncclAllReduce: ") + nccl().error_string(nr));
@@ -954,10 +1115,26 @@ static int enqueue_body(hm_runtime &rt, bool capture, bool pipelined, int64_t &h
         HM_CUDA(cudaMemcpyAsync(a.dst, a.src, a.bytes, cudaMemcpyDeviceToHost, a.stream));
         d2h += a.bytes;
         break;
+      case 6: {
+        if (a.peer_rank >= (int)rt.peer_pool.size() || !rt.peer_pool[a.peer_rank])
+          return fail(HM_ERR_VALIDATION, "peer buffer not imported");
+        auto it = rt.peer_out_off[a.peer_rank].find(a.peer_task);
+        if (it == rt.peer_out_off[a.peer_rank].end()) return fail(HM_ERR_INTERNAL, "peer has no source buffer");
+        const uint8_t *src = rt.peer_pool[a.peer_rank] + it->second + a.peer_off;
+        HM_CUDA(cudaMemcpyAsync(a.dst, src, a.bytes, cudaMemcpyDeviceToDevice, a.stream));
+        rt.p2p_bytes += a.bytes;
+        break;
+      }
       default:
         return fail(HM_ERR_INTERNAL, "bad action");
     }
     HM_CUDA(cudaEventRecord(rt.ev_end[a.item], a.stream));
+    if (rt.p2p_mode) {  // publish completion of this item for the peers (value = iteration)
+      if (!memops().write) return fail(HM_ERR_DEVICE, "cuStreamWriteValue32 unavailable");
+      if (memops().write(a.stream, reinterpret_cast<CUdeviceptr>(rt.sig) + 4 * (CUdeviceptr)a.item,
+                         (cuuint32_t)rt.step, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+        return fail(HM_ERR_DEVICE, "cuStreamWriteValue32 failed");
+    }
     if (capture) HM_CUDA(rec_time(rt.ev_tend[a.item], a.stream));
     rt.ev_live[a.item] = capture ? 0 : 1;
   }
@@ -983,7 +1160,7 @@ static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *l
   HM_CUDA(cudaMemcpyAsync(rt.labels, labels, tb, is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, sc));
   int64_t h2d = 0, d2h = 0, coll = 0;
   const int gi = rt.profiling ? 1 : 0;
-  const bool use_graph = rt.use_graph && rt.iterations >= 1;
+  const bool use_graph = rt.use_graph && !rt.p2p_mode && rt.iterations >= 1;
   if (use_graph) {
     if (!rt.graph_exec[gi]) {
       // record the iteration once (with or without per-kernel timing events)
@@ -1064,8 +1241,9 @@ static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *l
   rt.counters[2] = rt.pool_bytes;
   rt.counters[3] = h2d;
   rt.counters[4] = d2h;
-  rt.counters[5] = 0;
+  rt.counters[5] = rt.p2p_bytes;
   rt.counters[6] = coll;
+  rt.p2p_bytes = 0;
   return HM_OK;
 }
 
@@ -1123,8 +1301,9 @@ static int run_steps(hm_runtime &rt, int n, const int32_t *tokens, const int32_t
   rt.counters[2] = rt.pool_bytes;
   rt.counters[3] = h2d;
   rt.counters[4] = d2h;
-  rt.counters[5] = 0;
+  rt.counters[5] = rt.p2p_bytes / n;
   rt.counters[6] = coll;
+  rt.p2p_bytes = 0;
   return HM_OK;
 }
 
@@ -1276,6 +1455,113 @@ int hm_runtime_init_comm(hm_runtime *rt, const char *nccl_path, const uint8_t *i
   return HM_OK;
 }
 
+int hm_runtime_share_arenas(hm_runtime *rt, const char *shm_name, int32_t create, int64_t stash_bytes) {
+  if (!rt || !shm_name || !*shm_name) return hm::fail(HM_ERR_VALIDATION, "shared arena needs a name");
+  if (rt->shared_arena) return hm::fail(HM_ERR_VALIDATION, "arenas already shared");
+  const int64_t wb = hm::align_up(rt->total_params * 4, 1 << 21), kb = hm::align_up(rt->total_params * 8, 1 << 21);
+  const int64_t sb = hm::align_up(std::max<int64_t>(stash_bytes, 4096), 1 << 21);
+  const int64_t total = wb + kb + sb;
+  std::string name = shm_name[0] == '/' ? shm_name : std::string("/") + shm_name;
+  int fd = shm_open(name.c_str(), O_RDWR | (create ? O_CREAT | O_EXCL : 0), 0600);
+  if (fd < 0) return hm::fail(HM_ERR_DEVICE, "shm_open(" + name + ") failed");
+  if (create && ftruncate(fd, total) != 0) {
+    close(fd);
+    shm_unlink(name.c_str());
+    return hm::fail(HM_ERR_DEVICE, "ftruncate of the shared arena failed");
+  }
+  void *p = mmap(nullptr, total, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  if (p == MAP_FAILED) return hm::fail(HM_ERR_DEVICE, "mmap of the shared arena failed");
+  if (cudaHostRegister(p, total, cudaHostRegisterPortable) != cudaSuccess) {
+    munmap(p, total);
+    return hm::fail(HM_ERR_DEVICE, "cudaHostRegister of the shared arena failed");
+  }
+  if (rt->w_host) cudaFreeHost(rt->w_host);
+  if (rt->k_host) cudaFreeHost(rt->k_host);
+  if (rt->stash_host) cudaFreeHost(rt->stash_host);
+  uint8_t *base = static_cast<uint8_t *>(p);
+  rt->w_host = reinterpret_cast<float *>(base);
+  rt->k_host = reinterpret_cast<float *>(base + wb);
+  rt->stash_host = base + wb + kb;
+  rt->stash_host_bytes = sb;
+  rt->shared_arena = true;
+  rt->shared_owner = create != 0;
+  rt->shm_name = name;
+  rt->shm_ptr = p;
+  rt->shm_bytes = total;
+  return HM_OK;
+}
+
+int hm_runtime_ipc_export(hm_runtime *rt, uint8_t *buf, int32_t cap) {
+  if (!rt || !rt->pool) return hm::fail(HM_ERR_VALIDATION, "load a plan before exporting");
+  std::vector<uint8_t> out;
+  auto put = [&](const void *p, size_t n) {
+    const uint8_t *b = static_cast<const uint8_t *>(p);
+    out.insert(out.end(), b, b + n);
+  };
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, rt->pool) != cudaSuccess) return hm::fail(HM_ERR_DEVICE, "cudaIpcGetMemHandle failed");
+  const uint32_t magic = 0x484d3250;  // "HM2P"
+  const int32_t rank = rt->rank, n = (int32_t)rt->out_off.size();
+  put(&magic, 4);
+  put(&rank, 4);
+  put(&h, sizeof(h));
+  put(&rt->sig_off, 8);
+  put(&n, 4);
+  for (auto &kv : rt->out_off) {
+    const int32_t task = kv.first;
+    put(&task, 4);
+    put(&kv.second, 8);
+  }
+  if ((int32_t)out.size() > cap) return hm::fail(HM_ERR_VALIDATION, "ipc buffer too small");
+  std::memcpy(buf, out.data(), out.size());
+  return (int)out.size();
+}
+
+int hm_runtime_ipc_import(hm_runtime *rt, const uint8_t *buf, int32_t len) {
+  if (!rt || !buf || len < 8) return hm::fail(HM_ERR_VALIDATION, "bad ipc blob");
+  size_t o = 0;
+  auto get = [&](void *p, size_t n) {
+    std::memcpy(p, buf + o, n);
+    o += n;
+  };
+  uint32_t magic;
+  int32_t peer, n;
+  cudaIpcMemHandle_t h;
+  int64_t sig_off;
+  get(&magic, 4);
+  if (magic != 0x484d3250) return hm::fail(HM_ERR_VALIDATION, "bad ipc blob magic");
+  get(&peer, 4);
+  get(&h, sizeof(h));
+  get(&sig_off, 8);
+  get(&n, 4);
+  if (peer < 0 || peer > 4096) return hm::fail(HM_ERR_VALIDATION, "bad peer rank");
+  if ((int)rt->peer_pool.size() <= peer) {
+    rt->peer_pool.resize(peer + 1, nullptr);
+    rt->peer_out_off.resize(peer + 1);
+    rt->peer_sig_off.resize(peer + 1, 0);
+  }
+  rt->peer_out_off[peer].clear();
+  for (int i = 0; i < n; ++i) {
+    int32_t task;
+    int64_t off;
+    get(&task, 4);
+    get(&off, 8);
+    rt->peer_out_off[peer][task] = off;
+  }
+  rt->peer_sig_off[peer] = sig_off;
+  if (peer == rt->rank) {
+    rt->peer_pool[peer] = rt->pool;
+    return HM_OK;
+  }
+  if (cudaSetDevice(rt->device) != cudaSuccess) return hm::fail(HM_ERR_DEVICE, "cudaSetDevice");
+  void *p = nullptr;
+  if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+    return hm::fail(HM_ERR_DEVICE, "cudaIpcOpenMemHandle failed for rank " + std::to_string(peer));
+  rt->peer_pool[peer] = static_cast<uint8_t *>(p);
+  return HM_OK;
+}
+
 int hm_runtime_set_graph(hm_runtime *rt, int32_t enable) {
   if (!rt) return hm::fail(HM_ERR_VALIDATION, "null runtime");
   rt->use_graph = enable != 0;
@@ -1316,9 +1602,17 @@ void hm_runtime_free(hm_runtime *rt) {
   for (auto &e : rt->ar_events) cudaEventDestroy(e);
   if (rt->comm) hm::nccl().comm_destroy(rt->comm);
   if (rt->pool) cudaFree(rt->pool);
-  if (rt->w_host) cudaFreeHost(rt->w_host);
-  if (rt->k_host) cudaFreeHost(rt->k_host);
-  if (rt->stash_host) cudaFreeHost(rt->stash_host);
+  for (size_t i = 0; i < rt->peer_pool.size(); ++i)
+    if (rt->peer_pool[i] && (int)i != rt->rank) cudaIpcCloseMemHandle(rt->peer_pool[i]);
+  if (rt->shared_arena) {
+    cudaHostUnregister(rt->shm_ptr);
+    munmap(rt->shm_ptr, rt->shm_bytes);
+    if (rt->shared_owner) shm_unlink(rt->shm_name.c_str());
+  } else {
+    if (rt->w_host) cudaFreeHost(rt->w_host);
+    if (rt->k_host) cudaFreeHost(rt->k_host);
+    if (rt->stash_host) cudaFreeHost(rt->stash_host);
+  }
   cudaStream_t ss[] = {rt->s_compute, rt->s_h2d, rt->s_d2h, rt->s_update, rt->s_p2p_in, rt->s_p2p_out, rt->s_comm};
   for (auto s : ss) if (s) cudaStreamDestroy(s);
   delete rt;

@@ -90,6 +90,31 @@ class HarmonyRuntime:
                         view.reshape(-1, d)[V:] = 0.0
         self.k[:] = 0.0
 
+    # -- Harmony-PP across processes ----------------------------------------------
+    @staticmethod
+    def stash_bytes_for(graph: TaskGraph, profiles: ProfileSet) -> int:
+        """Host stash arena size the native layout needs (one region per
+        backward-pack head, D samples, 4 KiB aligned)."""
+        heads = sorted({L for t in graph.tasks for k, e in t.outputs.items() if k.value == "sX" for L in e})
+        return sum(-(-profiles.x_bytes(L, graph.minibatch) // 4096) * 4096 for L in heads)
+
+    def share_arenas(self, name: str, create: bool, stash_bytes: int) -> None:
+        """Move W / K / stash into one shared-memory segment (every PP rank
+        maps the same pinned host state).  Rank 0 creates, the others attach."""
+        NL.check(self.lib.hm_runtime_share_arenas(self.handle, name.encode(), 1 if create else 0,
+                                                  int(stash_bytes)))
+        self.w = self._arena(0, np.float32)
+        self.k = self._arena(1, np.float32)
+
+    def ipc_export(self) -> bytes:
+        buf = (C.c_uint8 * 65536)()
+        n = NL.check(self.lib.hm_runtime_ipc_export(self.handle, buf, 65536))
+        return bytes(buf[:n])
+
+    def ipc_import(self, blob: bytes) -> None:
+        b = (C.c_uint8 * len(blob)).from_buffer_copy(blob)
+        NL.check(self.lib.hm_runtime_ipc_import(self.handle, b, len(blob)))
+
     # -- Harmony-DP communicator -------------------------------------------------
     @staticmethod
     def nccl_path() -> bytes:

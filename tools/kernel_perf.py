@@ -55,6 +55,12 @@ def timeit(fn, iters=20, warm=3):
 def bench_gemm():
     tf_peak, _, kind = peaks()
     shapes = [("fwd_qkv", 4096, 4800, 1600, False, False, "bf16"),
+              ("fwd_proj", 4096, 1600, 1600, False, False, "resid_f32"),
+              ("fwd_head", 4096, 50304, 1600, False, False, "f32"),
+              ("dgrad_qkv", 4096, 1600, 4800, False, True, "f32"),
+              ("dgrad_fc2", 4096, 6400, 1600, False, True, "dgelu_bf16"),
+              ("wgrad_qkv", 4800, 1600, 4096, True, True, "acc_f32"),
+              ("wgrad_head", 50304, 1600, 4096, True, True, "acc_f32"),
               ("fwd_fc1", 4096, 6400, 1600, False, False, "gelu_bf16"),
               ("fwd_fc2", 4096, 1600, 6400, False, False, "resid_f32"),
               ("dgrad_fc1", 4096, 1600, 6400, False, True, "f32"),
@@ -70,7 +76,7 @@ def bench_gemm():
         aux = None
         if epi == "resid_f32":
             aux = torch.zeros(M, N, device="cuda")
-        if epi == "gelu_bf16":
+        if epi in ("gelu_bf16", "dgelu_bf16"):
             aux = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
         ms = timeit(lambda: ops.gemm(a, b, d, a_mn=amn, b_mn=bmn, epi=epi, bias=bias, aux=aux))
         tf = 2 * M * N * K / ms / 1e9
@@ -94,7 +100,23 @@ def bench_adam():
                       "frac": round(gbs / hbm, 3), "peak": kind}), flush=True)
 
 
+def bench_gemm_bn():
+    """Same shapes with the tile width forced (HM_GEMM_BN is read once per
+    process, so each width runs in a subprocess)."""
+    import subprocess
+    for bn in ("128", "256"):
+        env = dict(os.environ, HM_GEMM_BN=bn)
+        out = subprocess.run([sys.executable, __file__, "gemm"], env=env, capture_output=True, text=True).stdout
+        for line in out.splitlines():
+            d = json.loads(line)
+            d["bn"] = int(bn)
+            print(json.dumps(d), flush=True)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "gemm_bn":
+        bench_gemm_bn()
+        sys.exit(0)
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
     if what in ("gemm", "all"):
         bench_gemm()
