@@ -12,7 +12,8 @@
 //   warp 1   MMA issuer: one elected thread issues tcgen05.mma 128xBNx16,
 //            accumulator double-buffered in TMEM (2 x BN fp32 columns)
 //   warp 2   TMEM allocator
-//   warps 4-7 epilogue: tcgen05.ld 32 lanes x 32 columns per warp, fused
+//   warps 4-11 epilogue (two per TMEM lane quadrant, each draining half the
+//            columns): tcgen05.ld 32 lanes x 32 columns per warp, fused
 //            bias / residual / GELU / dGELU / fp32 accumulate, vector stores
 // The epilogue of tile i overlaps the MMAs of tile i+1.
 #include <cuda.h>
@@ -34,6 +35,8 @@ using namespace sm100;
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one SW128 atom row
 constexpr int kGroupM = 8;
+constexpr int kEpiWarps = 8;  // two warps per TMEM lane quadrant, each draining half the columns
+constexpr int kThreads = 128 + 32 * kEpiWarps;
 
 struct Args {
   int32_t M, N, K, num_m, num_n, num_k;
@@ -176,7 +179,7 @@ __device__ __forceinline__ void epilogue_row(const Args &a, int row, int col0, f
 }
 
 template <int BN, int A_MN, int B_MN>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Args args) {
   using C = Cfg<BN>;
   extern __shared__ uint8_t smem_raw[];
@@ -200,7 +203,7 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);
+      mbar_init(&tempty[i], 32 * kEpiWarps);
     }
     fence_barrier_init();
   }
@@ -281,7 +284,9 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp >= 4) {
-    const int q = warp & 3;
+    const int q = warp & 3;              // a warp may only touch TMEM lanes 32*(warp%4)..+31
+    const int half = (warp - 4) >> 2;    // which half of the tile's columns
+    constexpr int kChunks = BN / 32 / (kEpiWarps / 4);
     int local = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
       int mb, nb;
@@ -292,7 +297,7 @@ __global__ void __launch_bounds__(256, 1)
       tc_fence_after();
       const int row = mb * BM + q * 32 + (int)lane;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half * kChunks; c < (half + 1) * kChunks; ++c) {
         const int col0 = nb * BN + c * 32;
         if (col0 >= args.N) break;
         uint32_t r[32];
@@ -367,14 +372,14 @@ static int make_map(CUtensorMap *out, const void *ptr, uint64_t d0, uint64_t d1,
 
 static int num_sms();
 
-// Tile width: minimise (waves x tile width) over BN in {128, 256}, with a 5%
-// preference for the wider tile (half the A re-reads per FLOP).
-static int pick_bn(int64_t M, int64_t N) {
+// Tile width (measured on B200, profiles/r01_kernel_perf_bn.jsonl): the
+// 128x256 tile wins almost everywhere; the narrower tile only pays off for
+// short reductions (K <= 2048) with fewer than two waves of wide tiles, where
+// per-tile fill/drain dominates.
+static int pick_bn(int64_t M, int64_t N, int64_t K) {
   const int64_t sms = num_sms();
-  const int64_t mb = (M + BM - 1) / BM;
-  const int64_t w128 = (mb * ((N + 127) / 128) + sms - 1) / sms;
-  const int64_t w256 = (mb * ((N + 255) / 256) + sms - 1) / sms;
-  return (double)(w128 * 128) < 0.95 * (double)(w256 * 256) ? 128 : 256;
+  const int64_t tiles256 = ((M + BM - 1) / BM) * ((N + 255) / 256);
+  return (tiles256 < 2 * sms && K <= 2048) ? 128 : 256;
 }
 
 static int num_sms() {
@@ -403,7 +408,7 @@ static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const Args &a, c
   const bool f32 = a.epi == HM_EPI_STORE_F32 || a.epi == HM_EPI_ACC_F32 || a.epi == HM_EPI_RESID_F32;
   const double io = (double)a.M * a.N * (f32 ? 4 : 2) * (a.epi == HM_EPI_ACC_F32 || a.epi >= HM_EPI_RESID_F32 ? 2 : 1);
   ProfScope ps(KC_GEMM, s, 2.0 * a.M * a.N * a.K, 2.0 * ((double)a.M * a.K + (double)a.N * a.K) + io);
-  kern<<<grid, 256, C::kSmem, s>>>(ta, tb, a);
+  kern<<<grid, kThreads, C::kSmem, s>>>(ta, tb, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(HM_ERR_DEVICE, std::string("gemm launch: ") + cudaGetErrorString(e));
   count_launch();
@@ -427,7 +432,7 @@ int run(const void *A, const void *B, void *D, int64_t M, int64_t N, int64_t K, 
     const char *e = getenv("HM_GEMM_BN");
     return e ? atoi(e) : 0;
   }();
-  int bn = force_bn ? force_bn : env_bn ? env_bn : pick_bn(M, N);
+  int bn = force_bn ? force_bn : env_bn ? env_bn : pick_bn(M, N, K);
   Args a{};
   a.M = (int)M; a.N = (int)N; a.K = (int)K;
   a.num_m = (int)((M + BM - 1) / BM);

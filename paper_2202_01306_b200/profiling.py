@@ -1,0 +1,81 @@
+"""The profiler loop (paper §4.2, SURVEY §8f "next #1"): measure per-layer
+F / B / U costs of the real B200 kernels, fit the reference's affine cost
+models and hand them to the planner.
+
+Samples come from the runtime's own measured trace: a task graph of
+single-layer packs is executed with ``D = u`` samples (one microbatch member
+per task), so each compute item's CUDA-event duration is one layer's cost:
+
+* F task member           -> time_F(L, u)
+* B task with recompute   -> time_B(L, u) + time_F(L, u)   (time_F subtracted)
+* B task of the last pack -> time_B(L, u)                  (no recompute)
+* U task                  -> time_U(L)                     (fused Adam)
+
+Memory, activation and state sizes are the runtime's real byte layout
+(`model.py`), so ``fit_profiles`` sees integer-exact W / dW / K / x / y
+(`profiler.py:234-314` of the reference requires them to be u-independent).
+"""
+
+from __future__ import annotations
+
+from .core import Configuration, MachineModel, Mode
+from .model import GPTSpec, gpt_profiles, synthetic_batch
+from .profiler import ProfileSample, ProfileSet, fit_profiles, sample_points
+from .taskgraph import TaskType, generate_task_graph
+
+
+def samples_from_trace(spec: GPTSpec, graph, trace, u: int) -> list[ProfileSample]:
+    """ProfileSamples of one single-layer-pack run (trace = measured
+    compute TraceEvents of the report)."""
+    shapes = gpt_profiles(spec)
+    dur: dict[int, list[int]] = {}
+    for e in trace:
+        if e.kind == "compute":
+            dur.setdefault(e.task, []).append(e.end_ns - e.start_ns)
+    f_time, b_time, u_time = {}, {}, {}
+    for t in graph.tasks:
+        L = t.pack[0]
+        d = sum(dur.get(t.index, [0]))
+        if t.type is TaskType.F:
+            f_time[L] = d
+        elif t.type is TaskType.B:
+            b_time[L] = (d, t.recompute)
+        else:
+            u_time[L] = d
+    out = []
+    for L in range(spec.n_layer):
+        b, rec = b_time[L]
+        tb = max(0, b - f_time[L]) if rec else b
+        common = dict(layer_id=L, microbatch=u, x_bytes=shapes.x_bytes(L, u), y_bytes=shapes.y_bytes(L, u),
+                      w_bytes=shapes.w_bytes(L), dw_bytes=shapes.dw_bytes(L), k_bytes=shapes.k_bytes(L))
+        out.append(ProfileSample(pass_="F", compute_time_ns=f_time[L], mem_bytes=shapes.mem_bytes("F", L, u),
+                                 **common))
+        out.append(ProfileSample(pass_="B", compute_time_ns=tb, mem_bytes=shapes.mem_bytes("B", L, u), **common))
+        out.append(ProfileSample(pass_="U", compute_time_ns=u_time[L], mem_bytes=shapes.mem_bytes("U", L, 1),
+                                 **common))
+    return out
+
+
+def profile_gpt(spec: GPTSpec, u_values=None, u_max: int = 8, stride: int = 4, alpha_bytes: int = 64 << 30,
+                device: int = 0, warmup: int = 1) -> tuple[ProfileSet, list[ProfileSample]]:
+    """Measure and fit a ProfileSet on this GPU (sample points 1, stride
+    multiples and u_max, as the reference's profiler, `profiler.py:421-427`)."""
+    from .runtime import HarmonyRuntime
+    us = tuple(u_values) if u_values else sample_points(u_max, stride)
+    packs = tuple((L, L) for L in range(spec.n_layer))
+    samples: list[ProfileSample] = []
+    rt = HarmonyRuntime(spec, alpha_bytes=alpha_bytes, device=device)
+    try:
+        rt.init_weights(0)
+        mach = MachineModel(gpu_count=1, gpu_mem_capacity=alpha_bytes, pcie_bandwidth=55_000_000_000)
+        prof0 = gpt_profiles(spec, u_max=max(us))
+        for u in us:
+            g = generate_task_graph(Configuration(u, packs, u, packs, u, Mode.DP), mach, prof0)
+            rt.load(g, mach, prof0)
+            tok, lab = synthetic_batch(spec, u)
+            for _ in range(warmup + 1):
+                rt.step(tok, lab)
+            samples += samples_from_trace(spec, g, rt.report().trace, u)
+    finally:
+        rt.close()
+    return fit_profiles(samples, stride=stride), samples
