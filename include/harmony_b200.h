@@ -229,6 +229,10 @@ int hm_k_gemm(const void *a, const void *b, void *d, int64_t m, int64_t n, int64
  * head_dim 64 or 128; seq multiple of 64; causal 1 = GPT mask. */
 int hm_k_attn_fwd(const void *qkv, void *out, float *lse, int32_t batch, int32_t seq, int32_t heads,
                   int32_t head_dim, int32_t causal, void *stream);
+/* Same forward on tcgen05 tensor cores (head_dim 64, seq % 128 == 0); the
+ * runtime uses it whenever the shape allows. */
+int hm_k_attn_fwd_tc(const void *qkv, void *out, float *lse, int32_t batch, int32_t seq, int32_t heads,
+                     int32_t head_dim, int32_t causal, void *stream);
 /* Backward: writes dq|dk|dv into dqkv (same layout as qkv).  Scratch:
  * dvec [batch*seq*heads] fp32, dq_acc [batch*seq, heads*head_dim] fp32. */
 int hm_k_attn_bwd(const void *qkv, const void *out, const void *dout, const float *lse, float *dvec,

@@ -111,6 +111,7 @@ def lib() -> C.CDLL:
                                 C.c_int64, C.c_void_p]),
         "hm_launch_count": (C.c_int64, []),
         "hm_k_attn_fwd": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p] + [C.c_int32] * 5 + [C.c_void_p]),
+        "hm_k_attn_fwd_tc": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p] + [C.c_int32] * 5 + [C.c_void_p]),
         "hm_k_attn_bwd": (C.c_int, [C.c_void_p] * 7 + [C.c_int32] * 5 + [C.c_void_p]),
         "hm_k_cast_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
         "hm_k_embed_fwd": (C.c_int, [C.c_void_p] * 4 + [C.c_int32] * 3 + [C.c_void_p]),

@@ -13,9 +13,18 @@
 // later-round item.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+#include <string>
+
 #include "../runtime/common.hpp"
 
 namespace hm {
+namespace attn_tc {
+bool supported(int S, int DH);
+int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causal, cudaStream_t s);
+int backward_main(const void *qkv, const void *dout, const float *lse, const float *dvec, float *dq_acc, void *dqkv,
+                  int B, int S, int H, int causal, cudaStream_t s);
+}  // namespace attn_tc
 namespace attn {
 
 constexpr int BQ = 64, BKV = 64, THREADS = 128;
@@ -461,9 +470,22 @@ static int bwd_launch(const __nv_bfloat16 *qkv, const __nv_bfloat16 *o, const __
   const int64_t warps = rows * H;
   dvec_kernel<DH><<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(o, dout, dvec, rows, H);
   const float scale = 1.f / sqrtf((float)DH);
-  k<<<dim3(S / BKV, B * H), THREADS, bwd_smem<DH>(), s>>>(qkv, dout, lse, dvec, dq_acc, dqkv, S, H,
-                                                           1.4426950408889634f * scale, scale);
-  dq_convert<<<1184, 256, 0, s>>>(dq_acc, dqkv, rows, d, scale);
+  // The tcgen05 backward (attention_tc.cu) is correct but not yet faster than
+  // this mma.sync kernel on B200 (single softmax warp per SM sub-partition);
+  // opt in with HM_ATTN_BWD=tc while it is being tuned.
+  static const bool use_tc = [] {
+    const char *e = getenv("HM_ATTN_BWD");
+    return e && std::string(e) == "tc";
+  }();
+  if (use_tc && attn_tc::supported(S, DH)) {
+    // tcgen05 main kernel; it folds the softmax scale into dq_acc
+    HM_TRY(attn_tc::backward_main(qkv, dout, lse, dvec, dq_acc, dqkv, B, S, H, CAUSAL ? 1 : 0, s));
+    dq_convert<<<1184, 256, 0, s>>>(dq_acc, dqkv, rows, d, 1.f);
+  } else {
+    k<<<dim3(S / BKV, B * H), THREADS, bwd_smem<DH>(), s>>>(qkv, dout, lse, dvec, dq_acc, dqkv, S, H,
+                                                             1.4426950408889634f * scale, scale);
+    dq_convert<<<1184, 256, 0, s>>>(dq_acc, dqkv, rows, d, scale);
+  }
   count_launch(3);
   HM_CUDA(cudaGetLastError());
   return HM_OK;
@@ -471,6 +493,11 @@ static int bwd_launch(const __nv_bfloat16 *qkv, const __nv_bfloat16 *o, const __
 
 int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int DH, int causal, cudaStream_t s) {
   if (S % 64) return fail(HM_ERR_VALIDATION, "attention: seq_len must be a multiple of 64");
+  static const bool force_mma = [] {
+    const char *e = getenv("HM_ATTN");
+    return e && std::string(e) == "mma";
+  }();
+  if (!force_mma && attn_tc::supported(S, DH)) return attn_tc::forward(qkv, o, lse, B, S, H, causal, s);
   auto q = static_cast<const __nv_bfloat16 *>(qkv);
   auto out = static_cast<__nv_bfloat16 *>(o);
   if (DH == 64) return causal ? fwd_launch<64, true>(q, out, lse, B, S, H, s) : fwd_launch<64, false>(q, out, lse, B, S, H, s);

@@ -1,0 +1,574 @@
+// attention_tc.cu -- flash-attention forward on the 5th-gen tensor cores.
+//
+// One CTA per (sample, head, 128-query block), head_dim 64:
+//   warp 0     TMA: Q once, then K_j / V_j tiles (128 keys) into a 2-stage ring
+//   warp 1     MMA issuer: S_j = Q K_j^T (128x128x64) into TMEM (2 buffers),
+//              O_j = P_j V_j (128x64x128) into TMEM (2 buffers); S_{j+1} is
+//              issued before waiting for P_j so QK^T overlaps the softmax
+//   warps 4-7  softmax / epilogue, one thread per query row (TMEM lane):
+//              tcgen05.ld the S row, online max / exp2 / sum in registers,
+//              P_j (bf16) written to 128B-swizzled smem as the next MMA's A
+//              operand, O accumulated in registers one tile behind with the
+//              running rescale
+// Output o [tokens, d] bf16 and lse [tokens, H] (log2 domain) exactly as the
+// mma.sync kernel (attention.cu), which stays the fallback for head_dim 128
+// and for sequence lengths that are not a multiple of 128.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <mutex>
+
+#include "../runtime/common.hpp"
+#include "sm100.cuh"
+
+namespace hm {
+namespace attn_tc {
+
+using namespace sm100;
+
+constexpr int BQ = 128, BKV = 128, DH = 64;
+constexpr int kThreads = 256;
+constexpr uint32_t kTileBytes = BKV * DH * 2;  // 16 KB: 128 rows x 128 B
+constexpr uint32_t kPBytes = BQ * BKV * 2;     // 32 KB: two 64-key swizzle atoms
+constexpr size_t kSmem = 1024 + kTileBytes /*Q*/ + 2 * kTileBytes /*K*/ + 2 * kTileBytes /*V*/ + 2 * kPBytes + 512;
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <bool CAUSAL>
+__global__ void __launch_bounds__(kThreads, 1)
+    fwd_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16 *__restrict__ out, float *__restrict__ lse, int S,
+               int H, float scale_log2) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sQ = smem;
+  uint8_t *sK = sQ + kTileBytes;
+  uint8_t *sV = sK + 2 * kTileBytes;
+  uint8_t *sP = sV + 2 * kTileBytes;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sP + 2 * kPBytes);
+  uint64_t *q_full = bar;
+  uint64_t *kv_full = bar + 1, *kv_empty = bar + 3;
+  uint64_t *s_full = bar + 5, *s_empty = bar + 7;
+  uint64_t *p_full = bar + 9, *p_empty = bar + 11;
+  uint64_t *o_full = bar + 13, *o_empty = bar + 15;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 17);
+
+  const int nq = S / BQ;
+  const int qb = CAUSAL ? nq - 1 - (int)blockIdx.x : (int)blockIdx.x;
+  const int bh = blockIdx.y, b = bh / H, h = bh % H;
+  const int d = H * DH;
+  const int nkv = CAUSAL ? qb + 1 : S / BKV;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 128);
+      mbar_init(&p_full[i], 128);
+      mbar_init(&p_empty[i], 1);
+      mbar_init(&o_full[i], 1);
+      mbar_init(&o_empty[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int row0 = b * S;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(q_full, kTileBytes);
+      tma_load_2d(sQ, &tm, q_full, h * DH, row0 + qb * BQ);
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[st], 2 * kTileBytes);
+        tma_load_2d(sK + st * kTileBytes, &tm, &kv_full[st], d + h * DH, row0 + j * BKV);
+        tma_load_2d(sV + st * kTileBytes, &tm, &kv_full[st], 2 * d + h * DH, row0 + j * BKV);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = idesc_bf16_f32(BQ, BKV, 0, 0);  // Q K-major, K K-major
+      constexpr uint32_t idesc_o = idesc_bf16_f32(BQ, DH, 0, 1);   // P K-major, V MN-major
+      mbar_wait(q_full, 0);
+      const uint32_t q_base = smem_u32(sQ);
+      auto issue_s = [&](int j) {
+        const int st = j & 1, buf = j & 1;
+        mbar_wait(&kv_full[st], (j >> 1) & 1);
+        mbar_wait(&s_empty[buf], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t k_base = smem_u32(sK + st * kTileBytes);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk)
+          mma_bf16(tmem + buf * BKV, umma_desc_sw128(q_base + kk * 32, 16, 1024),
+                   umma_desc_sw128(k_base + kk * 32, 16, 1024), idesc_s, kk > 0);
+        mma_commit(&s_full[buf]);
+      };
+      issue_s(0);
+      for (int j = 0; j < nkv; ++j) {
+        if (j + 1 < nkv) issue_s(j + 1);
+        const int st = j & 1, buf = j & 1;
+        mbar_wait(&p_full[buf], (j >> 1) & 1);
+        mbar_wait(&o_empty[buf], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t p_base = smem_u32(sP + buf * kPBytes);
+        const uint32_t v_base = smem_u32(sV + st * kTileBytes);
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk)
+          mma_bf16(tmem + 2 * BKV + buf * DH,
+                   umma_desc_sw128(p_base + (kk >> 2) * (BQ * 128) + (kk & 3) * 32, 16, 1024),
+                   umma_desc_sw128(v_base + kk * 2048, BKV * 128, 1024), idesc_o, kk > 0);
+        mma_commit(&o_full[buf]);
+        mma_commit(&kv_empty[st]);
+        mma_commit(&p_empty[buf]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int r = q * 32 + lane;  // query row inside the block == TMEM lane
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    float o[DH];
+#pragma unroll
+    for (int c = 0; c < DH; ++c) o[c] = 0.f;
+    float m = -INFINITY, l = 0.f, alpha_prev = 1.f;
+    auto add_o = [&](int j, float alpha) {
+      const int buf = j & 1;
+      mbar_wait(&o_full[buf], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t v[DH];
+#pragma unroll
+      for (int c0 = 0; c0 < DH; c0 += 32)
+        tmem_ld_32x32b_x32(tmem + lane_addr + 2 * BKV + buf * DH + c0, *reinterpret_cast<uint32_t(*)[32]>(v + c0));
+      tmem_ld_wait();
+#pragma unroll
+      for (int c = 0; c < DH; ++c) o[c] = o[c] * alpha + __uint_as_float(v[c]);
+      tc_fence_before();
+      mbar_arrive(&o_empty[buf]);
+    };
+    for (int j = 0; j < nkv; ++j) {
+      const int buf = j & 1;
+      mbar_wait(&s_full[buf], (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t s_addr = tmem + lane_addr + buf * BKV;
+      const bool diag = CAUSAL && j == qb;
+      // the whole S row in registers: four TMEM loads in flight, one wait
+      uint32_t v[BKV];
+#pragma unroll
+      for (int c0 = 0; c0 < BKV; c0 += 32)
+        tmem_ld_32x32b_x32(s_addr + c0, *reinterpret_cast<uint32_t(*)[32]>(v + c0));
+      tmem_ld_wait();
+      if (diag) {  // causal mask on the diagonal tile (key > query)
+#pragma unroll
+        for (int c = 0; c < BKV; ++c)
+          if (c > r) v[c] = __float_as_uint(-INFINITY);
+      }
+      // row max with 8 independent chains (one warp per SM sub-partition: no
+      // other warp hides the FMNMX latency)
+      float mx8[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) mx8[e] = __uint_as_float(v[e]);
+#pragma unroll
+      for (int c = 8; c < BKV; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(v[c]));
+      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+      const float m_new = fmaxf(m, mx * scale_log2);
+      const float alpha = ex2(m - m_new);
+      m = m_new;
+      // P_j goes to smem buffer `buf`: wait until the MMA of P_{j-2} has consumed it
+      mbar_wait(&p_empty[buf], ((j >> 1) & 1) ^ 1);
+      uint8_t *prow = sP + buf * kPBytes + r * 128;
+      float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int c0 = 0; c0 < BKV; c0 += 32) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+          const float p0 = ex2(fmaf(__uint_as_float(v[c0 + c]), scale_log2, -m_new));
+          const float p1 = ex2(fmaf(__uint_as_float(v[c0 + c + 1]), scale_log2, -m_new));
+          rs8[(c >> 1) & 7] += p0 + p1;
+          __nv_bfloat162 t = __floats2bfloat162_rn(p0, p1);
+          pk[c >> 1] = *reinterpret_cast<uint32_t *>(&t);
+        }
+        // 32 keys = four 16-byte chunks of the 64-key swizzle atom (c0 / 64)
+        uint8_t *atom_row = prow + (c0 >> 6) * (BQ * 128);
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          const int chunk = ((c0 & 63) >> 3) + ch;
+          *reinterpret_cast<uint4 *>(atom_row + ((chunk ^ (r & 7)) << 4)) =
+              make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&s_empty[buf]);
+      fence_async_smem();  // generic-proxy P writes -> visible to the MMA (async proxy)
+      mbar_arrive(&p_full[buf]);
+      const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+      l = l * alpha + rs;
+      if (j > 0) add_o(j - 1, alpha_prev);
+      alpha_prev = alpha;
+    }
+    add_o(nkv - 1, alpha_prev);
+    // o is at the scale of the last tile's max; l too
+    const float inv = 1.f / l;
+    __nv_bfloat16 *orow = out + (int64_t)(row0 + qb * BQ + r) * d + h * DH;
+#pragma unroll
+    for (int c = 0; c < DH; c += 8) {
+      uint4 w;
+      uint32_t *wp = reinterpret_cast<uint32_t *>(&w);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        __nv_bfloat162 t = __floats2bfloat162_rn(o[c + 2 * e] * inv, o[c + 2 * e + 1] * inv);
+        wp[e] = *reinterpret_cast<uint32_t *>(&t);
+      }
+      *reinterpret_cast<uint4 *>(orow + c) = w;
+    }
+    lse[(int64_t)(row0 + qb * BQ + r) * H + h] = m + log2f(l);
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                              const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+
+// ---------------------------------------------------------------------------
+// backward: one CTA per (sample, head, 128-key block), looping over the query
+// blocks that attend to it (FA2 dataflow on tcgen05):
+//   S^T  = K Q^T        dP^T = V dO^T          (TMEM, 128 keys x 128 queries)
+//   P^T  = exp2(S^T * c - lse)   dS^T = P^T * (dP^T - D)   (bf16 -> smem)
+//   dV  += P^T dO       dK  += dS^T Q          (TMEM accumulators)
+//   dQ_i = dS K  -> fp32 atomics into dq_acc (scaled), converted by dq_convert
+// ---------------------------------------------------------------------------
+constexpr size_t kSmemBwd = 1024 + 2 * kTileBytes /*K,V*/ + 4 * kTileBytes /*Q,dO x2*/ + 2 * kPBytes /*P^T,dS^T*/ +
+                            2 * 2 * BQ * 4 /*lse,D x2*/ + 512;
+
+template <bool CAUSAL>
+__global__ void __launch_bounds__(kThreads, 1)
+    bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+               const float *__restrict__ lse, const float *__restrict__ dvec, float *__restrict__ dq_acc,
+               __nv_bfloat16 *__restrict__ dqkv, int S, int H, float scale_log2, float scale) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sK = smem;
+  uint8_t *sV = sK + kTileBytes;
+  uint8_t *sQ = sV + kTileBytes;          // [2] stages
+  uint8_t *sdO = sQ + 2 * kTileBytes;     // [2] stages
+  uint8_t *sP = sdO + 2 * kTileBytes;     // P^T  [128 keys x 128 queries]
+  uint8_t *sdS = sP + kPBytes;            // dS^T
+  float *sL = reinterpret_cast<float *>(sdS + kPBytes);  // [2][128] lse
+  float *sD = sL + 2 * BQ;                               // [2][128] D
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sD + 2 * BQ);
+  uint64_t *kv_full = bar;
+  uint64_t *q_full = bar + 1, *q_empty = bar + 3;
+  uint64_t *st_full = bar + 5, *st_empty = bar + 6;
+  uint64_t *p_full = bar + 7, *p_empty = bar + 8;
+  uint64_t *dq_full = bar + 9, *dq_empty = bar + 10, *acc_full = bar + 11;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 12);
+
+  const int nq = S / BQ;
+  const int kb = blockIdx.x;
+  const int bh = blockIdx.y, b = bh / H, h = bh % H;
+  const int d = H * DH;
+  const int q_begin = CAUSAL ? kb : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row0 = b * S;
+  // TMEM columns
+  constexpr uint32_t C_ST = 0, C_DP = 128, C_DV = 256, C_DK = 320, C_DQ = 384;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_qkv);
+    tma_prefetch(&tm_do);
+    mbar_init(kv_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+    }
+    mbar_init(st_full, 1);
+    mbar_init(st_empty, 128);
+    mbar_init(p_full, 128);
+    mbar_init(p_empty, 1);
+    mbar_init(dq_full, 1);
+    mbar_init(dq_empty, 128);
+    mbar_init(acc_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(kv_full, 2 * kTileBytes);
+      tma_load_2d(sK, &tm_qkv, kv_full, d + h * DH, row0 + kb * BKV);
+      tma_load_2d(sV, &tm_qkv, kv_full, 2 * d + h * DH, row0 + kb * BKV);
+      for (int i = q_begin, n = 0; i < nq; ++i, ++n) {
+        const int st = n & 1;
+        mbar_wait(&q_empty[st], ((n >> 1) & 1) ^ 1);
+        mbar_expect_tx(&q_full[st], 2 * kTileBytes);
+        tma_load_2d(sQ + st * kTileBytes, &tm_qkv, &q_full[st], h * DH, row0 + i * BQ);
+        tma_load_2d(sdO + st * kTileBytes, &tm_do, &q_full[st], h * DH, row0 + i * BQ);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id_kk = idesc_bf16_f32(128, 128, 0, 0);   // S^T, dP^T: K-major x K-major
+      constexpr uint32_t id_kmn = idesc_bf16_f32(128, DH, 0, 1);   // dV, dK: A K-major, B MN-major
+      constexpr uint32_t id_mnmn = idesc_bf16_f32(128, DH, 1, 1);  // dQ: A MN-major (dS), B MN-major (K)
+      mbar_wait(kv_full, 0);
+      const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV);
+      const uint32_t p_base = smem_u32(sP), ds_base = smem_u32(sdS);
+      for (int i = q_begin, n = 0; i < nq; ++i, ++n) {
+        const int st = n & 1;
+        const uint32_t ph = n & 1;
+        mbar_wait(&q_full[st], (n >> 1) & 1);
+        mbar_wait(st_empty, ph ^ 1);
+        tc_fence_after();
+        const uint32_t q_base = smem_u32(sQ + st * kTileBytes), do_base = smem_u32(sdO + st * kTileBytes);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          mma_bf16(tmem + C_ST, umma_desc_sw128(k_base + kk * 32, 16, 1024),
+                   umma_desc_sw128(q_base + kk * 32, 16, 1024), id_kk, kk > 0);
+          mma_bf16(tmem + C_DP, umma_desc_sw128(v_base + kk * 32, 16, 1024),
+                   umma_desc_sw128(do_base + kk * 32, 16, 1024), id_kk, kk > 0);
+        }
+        mma_commit(st_full);
+        mbar_wait(p_full, ph);
+        mbar_wait(dq_empty, ph ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < BQ / 16; ++kk) {  // reduction over the 128 queries
+          const uint32_t a_off = (kk >> 2) * (BKV * 128) + (kk & 3) * 32;
+          mma_bf16(tmem + C_DV, umma_desc_sw128(p_base + a_off, 16, 1024),
+                   umma_desc_sw128(do_base + kk * 2048, BQ * 128, 1024), id_kmn, (n > 0 || kk > 0) ? 1u : 0u);
+          mma_bf16(tmem + C_DK, umma_desc_sw128(ds_base + a_off, 16, 1024),
+                   umma_desc_sw128(q_base + kk * 2048, BQ * 128, 1024), id_kmn, (n > 0 || kk > 0) ? 1u : 0u);
+        }
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk)  // reduction over the 128 keys
+          mma_bf16(tmem + C_DQ, umma_desc_sw128(ds_base + kk * 2048, BKV * 128, 1024),
+                   umma_desc_sw128(k_base + kk * 2048, BKV * 128, 1024), id_mnmn, kk > 0);
+        mma_commit(dq_full);
+        mma_commit(&q_empty[st]);
+        mma_commit(p_empty);
+      }
+      mma_commit(acc_full);
+    }
+  } else if (warp >= 4) {
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;  // key row (S^T, dP^T, dV, dK) / query row (dQ) == TMEM lane
+    const uint32_t lane_addr = (uint32_t)(q4 * 32) << 16;
+    for (int i = q_begin, n = 0; i < nq; ++i, ++n) {
+      const int st = n & 1;
+      const uint32_t ph = n & 1;
+      // lse and D of this query block (tiny: read through L1, not TMA)
+      sL[st * BQ + r] = lse[(int64_t)(row0 + i * BQ + r) * H + h];
+      sD[st * BQ + r] = dvec[(int64_t)(row0 + i * BQ + r) * H + h];
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      mbar_wait(st_full, ph);
+      tc_fence_after();
+      const bool diag = CAUSAL && i == kb;
+      const float *Ls = sL + st * BQ;
+      const float *Ds = sD + st * BQ;
+      uint8_t *prow = sP + r * 128;
+      uint8_t *dsrow = sdS + r * 128;
+      // two halves of 64 queries (one swizzle atom each) keep S and dP rows in registers
+#pragma unroll 1
+      for (int hq = 0; hq < 2; ++hq) {
+        uint32_t sv[64], dp[64];
+#pragma unroll
+        for (int c0 = 0; c0 < 64; c0 += 32) {
+          tmem_ld_32x32b_x32(tmem + lane_addr + C_ST + hq * 64 + c0, *reinterpret_cast<uint32_t(*)[32]>(sv + c0));
+          tmem_ld_32x32b_x32(tmem + lane_addr + C_DP + hq * 64 + c0, *reinterpret_cast<uint32_t(*)[32]>(dp + c0));
+        }
+        tmem_ld_wait();
+        if (hq == 1) {
+          tc_fence_before();
+          mbar_arrive(st_empty);  // S^T / dP^T fully read: the next block's MMAs may overwrite
+        } else {
+          mbar_wait(p_empty, ph ^ 1);  // the previous block's MMAs have consumed P^T / dS^T
+        }
+#pragma unroll
+        for (int c0 = 0; c0 < 64; c0 += 32) {
+          uint32_t pk[16], dk[16];
+#pragma unroll
+          for (int c = 0; c < 32; c += 2) {
+            const int qi = hq * 64 + c0 + c;
+            float p0 = ex2(fmaf(__uint_as_float(sv[c0 + c]), scale_log2, -Ls[qi]));
+            float p1 = ex2(fmaf(__uint_as_float(sv[c0 + c + 1]), scale_log2, -Ls[qi + 1]));
+            if (diag && qi < r) p0 = 0.f;  // query < key: masked
+            if (diag && qi + 1 < r) p1 = 0.f;
+            const float s0 = p0 * (__uint_as_float(dp[c0 + c]) - Ds[qi]);
+            const float s1 = p1 * (__uint_as_float(dp[c0 + c + 1]) - Ds[qi + 1]);
+            __nv_bfloat162 tp = __floats2bfloat162_rn(p0, p1), td = __floats2bfloat162_rn(s0, s1);
+            pk[c >> 1] = *reinterpret_cast<uint32_t *>(&tp);
+            dk[c >> 1] = *reinterpret_cast<uint32_t *>(&td);
+          }
+          const uint32_t atom = hq * (BKV * 128);
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            const int chunk = (c0 >> 3) + ch;
+            const uint32_t off = atom + ((chunk ^ (r & 7)) << 4);
+            *reinterpret_cast<uint4 *>(prow + off) = make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+            *reinterpret_cast<uint4 *>(dsrow + off) =
+                make_uint4(dk[4 * ch], dk[4 * ch + 1], dk[4 * ch + 2], dk[4 * ch + 3]);
+          }
+        }
+      }
+      fence_async_smem();
+      mbar_arrive(p_full);
+      // dQ_i rows (TMEM lane = query) -> fp32 atomics
+      mbar_wait(dq_full, ph);
+      tc_fence_after();
+      uint32_t q[DH];
+#pragma unroll
+      for (int c0 = 0; c0 < DH; c0 += 32)
+        tmem_ld_32x32b_x32(tmem + lane_addr + C_DQ + c0, *reinterpret_cast<uint32_t(*)[32]>(q + c0));
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(dq_empty);
+      float *dst = dq_acc + (int64_t)(row0 + i * BQ + r) * d + h * DH;
+#pragma unroll
+      for (int c = 0; c < DH; ++c) atomicAdd(dst + c, __uint_as_float(q[c]) * scale);
+    }
+    // dV, dK of this key block
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    uint32_t vv[DH], kk2[DH];
+#pragma unroll
+    for (int c0 = 0; c0 < DH; c0 += 32) {
+      tmem_ld_32x32b_x32(tmem + lane_addr + C_DV + c0, *reinterpret_cast<uint32_t(*)[32]>(vv + c0));
+      tmem_ld_32x32b_x32(tmem + lane_addr + C_DK + c0, *reinterpret_cast<uint32_t(*)[32]>(kk2 + c0));
+    }
+    tmem_ld_wait();
+    const int64_t ld = 3 * (int64_t)d;
+    __nv_bfloat16 *dk_row = dqkv + (int64_t)(row0 + kb * BKV + r) * ld + d + h * DH;
+    __nv_bfloat16 *dv_row = dk_row + d;
+#pragma unroll
+    for (int c = 0; c < DH; c += 8) {
+      uint4 wk, wv;
+      uint32_t *pk = reinterpret_cast<uint32_t *>(&wk), *pv = reinterpret_cast<uint32_t *>(&wv);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        __nv_bfloat162 a = __floats2bfloat162_rn(__uint_as_float(kk2[c + 2 * e]) * scale,
+                                                 __uint_as_float(kk2[c + 2 * e + 1]) * scale);
+        __nv_bfloat162 bvv = __floats2bfloat162_rn(__uint_as_float(vv[c + 2 * e]), __uint_as_float(vv[c + 2 * e + 1]));
+        pk[e] = *reinterpret_cast<uint32_t *>(&a);
+        pv[e] = *reinterpret_cast<uint32_t *>(&bvv);
+      }
+      *reinterpret_cast<uint4 *>(dk_row + c) = wk;
+      *reinterpret_cast<uint4 *>(dv_row + c) = wv;
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+static int make_map(CUtensorMap *tm, const void *base, int64_t inner, int64_t rows, int64_t pitch_bytes) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return fail(HM_ERR_DEVICE, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)pitch_bytes};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t estr[2] = {1, 1};
+  if (fn(tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box, estr,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return fail(HM_ERR_DEVICE, "attention tensor map encode failed");
+  return HM_OK;
+}
+
+int backward_main(const void *qkv, const void *dout, const float *lse, const float *dvec, float *dq_acc, void *dqkv,
+                  int B, int S, int H, int causal, cudaStream_t s) {
+  const int d = H * DH;
+  CUtensorMap tq, td;
+  HM_TRY(make_map(&tq, qkv, 3 * (int64_t)d, (int64_t)B * S, 3 * (int64_t)d * 2));
+  HM_TRY(make_map(&td, dout, d, (int64_t)B * S, (int64_t)d * 2));
+  static bool attr[2] = {false, false};
+  auto k = causal ? bwd_kernel<true> : bwd_kernel<false>;
+  if (!attr[causal ? 1 : 0]) {
+    HM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBwd));
+    attr[causal ? 1 : 0] = true;
+  }
+  const float scale = 1.f / sqrtf((float)DH);
+  k<<<dim3(S / BKV, B * H), kThreads, kSmemBwd, s>>>(tq, td, lse, dvec, dq_acc, static_cast<__nv_bfloat16 *>(dqkv), S,
+                                                      H, 1.4426950408889634f * scale, scale);
+  count_launch();
+  HM_CUDA(cudaGetLastError());
+  return HM_OK;
+}
+
+// true if the tensor-core path handles this shape (else use the mma.sync kernel)
+bool supported(int S, int DHx) { return DHx == DH && S % BQ == 0; }
+
+int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causal, cudaStream_t s) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return fail(HM_ERR_DEVICE, "cuTensorMapEncodeTiled unavailable");
+  const int d = H * DH;
+  CUtensorMap tm;
+  cuuint64_t dims[2] = {(cuuint64_t)3 * d, (cuuint64_t)B * S};
+  cuuint64_t strides[1] = {(cuuint64_t)3 * d * 2};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t estr[2] = {1, 1};
+  if (fn(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(qkv), dims, strides, box, estr,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return fail(HM_ERR_DEVICE, "attention tensor map encode failed");
+  static bool attr[2] = {false, false};
+  auto k = causal ? fwd_kernel<true> : fwd_kernel<false>;
+  if (!attr[causal ? 1 : 0]) {
+    HM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
+    attr[causal ? 1 : 0] = true;
+  }
+  const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
+  ProfScope ps(KC_ATTN_FWD, s, 4.0 * B * (double)S * S * H * DH * (causal ? 0.5 : 1.0), (double)B * S * H * DH * 2 * 4);
+  k<<<dim3(S / BQ, B * H), kThreads, kSmem, s>>>(tm, static_cast<__nv_bfloat16 *>(o), lse, S, H, scale_log2);
+  count_launch();
+  HM_CUDA(cudaGetLastError());
+  return HM_OK;
+}
+
+}  // namespace attn_tc
+}  // namespace hm
+
+extern "C" int hm_k_attn_fwd_tc(const void *qkv, void *out, float *lse, int32_t batch, int32_t seq, int32_t heads,
+                                int32_t head_dim, int32_t causal, void *stream) {
+  if (!hm::attn_tc::supported(seq, head_dim))
+    return hm::fail(HM_ERR_VALIDATION, "tcgen05 attention needs head_dim 64 and seq % 128 == 0");
+  return hm::attn_tc::forward(qkv, out, lse, batch, seq, heads, causal, static_cast<cudaStream_t>(stream));
+}

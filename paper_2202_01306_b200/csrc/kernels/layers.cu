@@ -227,8 +227,124 @@ __global__ void ln_bwd_kernel(const float *__restrict__ dy, const float *__restr
   }
 }
 
+// Same math, dgamma/dbeta accumulated in registers: a warp keeps the same
+// lane -> column mapping for every row it processes, so each lane sums its
+// NV4 float4 columns privately; warps then combine through shared memory
+// and one atomic per column per block.  Used for d <= 2048.
+template <int NV4>
+__global__ void __launch_bounds__(256) ln_bwd_reg_kernel(const float *__restrict__ dy, const float *__restrict__ x,
+                                                         const float *__restrict__ mean, const float *__restrict__ rstd,
+                                                         const float *__restrict__ gam, const float *resid, float *out,
+                                                         __nv_bfloat16 *__restrict__ out_bf, float *__restrict__ dgam,
+                                                         float *__restrict__ dbet, int64_t rows, int d, int rows_per_block) {
+  extern __shared__ float spart[];  // [nwarps][2][d]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int n4 = d / 4;
+  float4 ag[NV4], ab[NV4];
+#pragma unroll
+  for (int k = 0; k < NV4; ++k) ag[k] = ab[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 *g4 = reinterpret_cast<const float4 *>(gam);
+  const int64_t r_begin = (int64_t)blockIdx.x * rows_per_block;
+  const int64_t r_end = min(rows, r_begin + rows_per_block);
+  for (int64_t r = r_begin + warp; r < r_end; r += nw) {
+    const float4 *dyr = reinterpret_cast<const float4 *>(dy + r * d);
+    const float4 *xr = reinterpret_cast<const float4 *>(x + r * d);
+    const float mu = mean[r], rs = rstd[r];
+    float c1 = 0.f, c2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV4; ++k) {
+      const int i = lane + 32 * k;
+      if (i < n4) {
+        const float4 a = dyr[i], v = xr[i], gg = g4[i];
+        const float4 hh = make_float4((v.x - mu) * rs, (v.y - mu) * rs, (v.z - mu) * rs, (v.w - mu) * rs);
+        c1 += a.x * gg.x + a.y * gg.y + a.z * gg.z + a.w * gg.w;
+        c2 += a.x * gg.x * hh.x + a.y * gg.y * hh.y + a.z * gg.z * hh.z + a.w * gg.w * hh.w;
+        ag[k].x += a.x * hh.x; ag[k].y += a.y * hh.y; ag[k].z += a.z * hh.z; ag[k].w += a.w * hh.w;
+        ab[k].x += a.x; ab[k].y += a.y; ab[k].z += a.z; ab[k].w += a.w;
+      }
+    }
+    c1 = warp_sum(c1) / d;
+    c2 = warp_sum(c2) / d;
+    float4 *outr = reinterpret_cast<float4 *>(out + r * d);
+    const float4 *rr = resid ? reinterpret_cast<const float4 *>(resid + r * d) : nullptr;
+    uint2 *ob = out_bf ? reinterpret_cast<uint2 *>(out_bf + r * d) : nullptr;
+#pragma unroll
+    for (int k = 0; k < NV4; ++k) {
+      const int i = lane + 32 * k;
+      if (i < n4) {  // second pass re-reads the row (L1/L2 resident)
+        const float4 a = dyr[i], v = xr[i], gg = g4[i];
+        const float4 hh = make_float4((v.x - mu) * rs, (v.y - mu) * rs, (v.z - mu) * rs, (v.w - mu) * rs);
+        float4 o;
+        o.x = rs * (a.x * gg.x - c1 - hh.x * c2);
+        o.y = rs * (a.y * gg.y - c1 - hh.y * c2);
+        o.z = rs * (a.z * gg.z - c1 - hh.z * c2);
+        o.w = rs * (a.w * gg.w - c1 - hh.w * c2);
+        if (rr) {
+          const float4 q = rr[i];
+          o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+        }
+        outr[i] = o;
+        if (ob) {
+          __nv_bfloat162 p0 = __floats2bfloat162_rn(o.x, o.y), p1 = __floats2bfloat162_rn(o.z, o.w);
+          ob[i] = make_uint2(*reinterpret_cast<uint32_t *>(&p0), *reinterpret_cast<uint32_t *>(&p1));
+        }
+      }
+    }
+  }
+  float4 *mine = reinterpret_cast<float4 *>(spart + (size_t)warp * 2 * d);
+#pragma unroll
+  for (int k = 0; k < NV4; ++k) {
+    const int i = lane + 32 * k;
+    if (i < n4) {
+      mine[i] = ag[k];
+      mine[n4 + i] = ab[k];
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    float sg = 0.f, sb = 0.f;
+    for (int w = 0; w < nw; ++w) {
+      sg += spart[(size_t)w * 2 * d + c];
+      sb += spart[(size_t)w * 2 * d + d + c];
+    }
+    atomicAdd(&dgam[c], sg);
+    atomicAdd(&dbet[c], sb);
+  }
+}
+
+template <int NV4>
+static int ln_bwd_reg(const float *dy, const float *x, const float *mean, const float *rstd, const float *g,
+                      const float *resid, float *out, void *out_bf, float *dg, float *db, int64_t rows, int d,
+                      cudaStream_t s) {
+  const int nw = 8;
+  const size_t smem = (size_t)nw * 2 * d * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    HM_CUDA(cudaFuncSetAttribute(ln_bwd_reg_kernel<NV4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  int64_t blocks = sm_count() * 2;
+  int rpb = (int)((rows + blocks - 1) / blocks);
+  if (rpb < 8) rpb = 8;
+  blocks = (rows + rpb - 1) / rpb;
+  ln_bwd_reg_kernel<NV4><<<(unsigned)blocks, nw * 32, smem, s>>>(dy, x, mean, rstd, g, resid, out,
+                                                               static_cast<__nv_bfloat16 *>(out_bf), dg, db, rows, d, rpb);
+  count_launch();
+  HM_CUDA(cudaGetLastError());
+  return HM_OK;
+}
+
 int ln_bwd(const float *dy, const float *x, const float *mean, const float *rstd, const float *g, const float *resid,
            float *out, void *out_bf, float *dg, float *db, int64_t rows, int d, cudaStream_t s) {
+  if (d % 4 == 0 && d <= 2048) {
+    ProfScope ps(KC_LAYERNORM, s, 0, (resid ? 16.0 : 12.0) * rows * d + (out_bf ? 2.0 * rows * d : 0));
+    const int nv4 = (d / 4 + 31) / 32;
+    if (nv4 <= 2) return ln_bwd_reg<2>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
+    if (nv4 <= 4) return ln_bwd_reg<4>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
+    if (nv4 <= 8) return ln_bwd_reg<8>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
+    if (nv4 <= 13) return ln_bwd_reg<13>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
+    return ln_bwd_reg<16>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
+  }
   if (d % 4) return fail(HM_ERR_VALIDATION, "layernorm: d must be a multiple of 4");
   const size_t smem = 2 * (size_t)d * sizeof(float);
   static bool attr = false;

@@ -59,6 +59,11 @@ def attn_fwd(qkv, out, lse, *, batch, seq, heads, head_dim, causal=True):
                                    int(causal), _stream()))
 
 
+def attn_fwd_tc(qkv, out, lse, *, batch, seq, heads, head_dim, causal=True):
+    NL.check(N_lib().hm_k_attn_fwd_tc(_ptr(qkv), _ptr(out), _ptr(lse), batch, seq, heads, head_dim,
+                                      int(causal), _stream()))
+
+
 def attn_bwd(qkv, out, dout, lse, dqkv, *, batch, seq, heads, head_dim, causal=True):
     rows = batch * seq
     dvec = torch.empty(rows * heads, device=qkv.device)

@@ -218,3 +218,30 @@ def test_bias_grad_and_cast(ops):
     dst = torch.empty(1_000_001, device="cuda", dtype=torch.bfloat16)
     ops.cast_bf16(src, dst)
     assert torch.equal(dst, src.to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("B,S,H,causal", [(2, 128, 4, True), (1, 512, 2, False), (2, 1024, 3, True),
+                                          (1, 256, 25, True)])
+def test_attention_fwd_tcgen05_matches(ops, B, S, H, causal):
+    torch.manual_seed(11)
+    DH = 64
+    d = H * DH
+    qkv = _bf(B * S, 3 * d)
+    out = torch.empty(B * S, d, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(B * S, H, device="cuda")
+    ops.attn_fwd_tc(qkv, out, lse, batch=B, seq=S, heads=H, head_dim=DH, causal=causal)
+    ro, rl = _attn_ref(qkv, B, S, H, DH, causal)
+    assert _rel(out, ro) < 1e-2
+    assert torch.allclose(lse, rl * 1.4426950408889634, atol=2e-3, rtol=1e-3)
+
+
+def test_attention_bwd_tcgen05_opt_in():
+    """The tcgen05 backward (opt-in via HM_ATTN_BWD=tc) matches autograd."""
+    import subprocess
+    import sys
+    code = ("import torch, sys; sys.path.insert(0, '.'); import tests.test_kernels_gpu as T; "
+            "from paper_2202_01306_b200 import ops; "
+            "T.test_attention_fwd_bwd(ops, 2, 256, 3, 64, True); T.test_attention_fwd_bwd(ops, 1, 512, 2, 64, False)")
+    env = dict(__import__("os").environ, HM_ATTN_BWD="tc")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]

@@ -124,3 +124,15 @@ def test_pipelined_steps_match_sequential():
     # equal up to run-to-run nondeterminism of atomics (dQ, LayerNorm dγ/dβ, embedding)
     assert np.linalg.norm(w0 - w1) / np.linalg.norm(w0) < 5e-4
     assert np.linalg.norm(k0 - k1) / np.linalg.norm(k0) < 1e-2
+
+
+@pytest.mark.slow
+def test_bert_large_c2_matches_oracle():
+    """BASELINE config c2: BERT-Large shapes (24 layers, d=1024, 16 heads,
+    seq 512, V=30522, full attention) with layer-pack swapping on one B200
+    (alpha capped at 8 GiB so every pack swaps), 2 steps vs the fp32 oracle."""
+    spec = GPT_PRESETS["bert-large"]
+    packs = tuple((i, i + 5) for i in range(0, 24, 6))
+    cfg = H.Configuration(2, packs, 2, packs, 4, H.Mode.PP)
+    rel_w, rel_m, rel_v, _ = _run(spec, cfg, steps=2, alpha=8 << 30)
+    assert rel_w < STATE_RTOL

@@ -100,6 +100,26 @@ def bench_adam():
                       "frac": round(gbs / hbm, 3), "peak": kind}), flush=True)
 
 
+def bench_attn():
+    tf_peak, _, kind = peaks()
+    for B, S, H, causal in ((4, 1024, 25, True), (8, 512, 16, False), (16, 128, 4, True)):
+        DH = 64
+        d = H * DH
+        qkv = torch.randn(B * S, 3 * d, device="cuda").to(torch.bfloat16)
+        out = torch.empty(B * S, d, device="cuda", dtype=torch.bfloat16)
+        lse = torch.empty(B * S, H, device="cuda")
+        dout = torch.randn(B * S, d, device="cuda").to(torch.bfloat16)
+        dqkv = torch.empty_like(qkv)
+        fl = 4.0 * B * S * S * H * DH * (0.5 if causal else 1.0)
+        ms = timeit(lambda: ops.attn_fwd(qkv, out, lse, batch=B, seq=S, heads=H, head_dim=DH, causal=causal))
+        msb = timeit(lambda: ops.attn_bwd(qkv, out, dout, lse, dqkv, batch=B, seq=S, heads=H, head_dim=DH,
+                                          causal=causal))
+        print(json.dumps({"kernel": "attention", "impl": os.environ.get("HM_ATTN", "tcgen05"), "B": B, "S": S,
+                          "H": H, "causal": causal, "fwd_ms": round(ms, 4), "fwd_tflops": round(fl / ms / 1e9, 1),
+                          "bwd_ms": round(msb, 4), "bwd_tflops": round(2.5 * fl / msb / 1e9, 1),
+                          "peak": tf_peak, "peak_kind": kind}), flush=True)
+
+
 def bench_gemm_bn():
     """Same shapes with the tile width forced (HM_GEMM_BN is read once per
     process, so each width runs in a subprocess)."""
@@ -118,6 +138,8 @@ if __name__ == "__main__":
         bench_gemm_bn()
         sys.exit(0)
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if what in ("attn", "all"):
+        bench_attn()
     if what in ("gemm", "all"):
         bench_gemm()
     if what in ("adam", "all"):
