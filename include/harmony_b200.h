@@ -191,6 +191,10 @@ int hm_runtime_share_arenas(hm_runtime *rt, const char *shm_name, int32_t create
  * waits on the producer's counters (cuStreamWaitValue32). */
 int hm_runtime_ipc_export(hm_runtime *rt, uint8_t *buf, int32_t cap);
 int hm_runtime_ipc_import(hm_runtime *rt, const uint8_t *buf, int32_t len);
+/* Optimizer step counter (Adam bias correction); checkpoint / resume of the
+ * host arenas restores it together with W and K. */
+int hm_runtime_get_step(const hm_runtime *rt);
+int hm_runtime_set_step(hm_runtime *rt, int32_t step);
 /* Record each iteration into a CUDA graph after the first (default on) and
  * replay it: one launch per iteration instead of thousands. */
 int hm_runtime_set_graph(hm_runtime *rt, int32_t enable);

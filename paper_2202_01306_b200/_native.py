@@ -98,6 +98,8 @@ def lib() -> C.CDLL:
         "hm_nccl_unique_id": (C.c_int, [C.c_char_p, C.c_void_p]),
         "hm_runtime_init_comm": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_int32, C.c_int32]),
         "hm_runtime_set_graph": (C.c_int, [C.c_void_p, C.c_int32]),
+        "hm_runtime_get_step": (C.c_int, [C.c_void_p]),
+        "hm_runtime_set_step": (C.c_int, [C.c_void_p, C.c_int32]),
         "hm_runtime_share_arenas": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int32, C.c_int64]),
         "hm_runtime_ipc_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
         "hm_runtime_ipc_import": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),

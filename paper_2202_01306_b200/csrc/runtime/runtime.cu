@@ -1562,6 +1562,14 @@ int hm_runtime_ipc_import(hm_runtime *rt, const uint8_t *buf, int32_t len) {
   return HM_OK;
 }
 
+int hm_runtime_get_step(const hm_runtime *rt) { return rt ? rt->step : -1; }
+
+int hm_runtime_set_step(hm_runtime *rt, int32_t step) {
+  if (!rt || step < 0) return hm::fail(HM_ERR_VALIDATION, "bad step");
+  rt->step = step;
+  return HM_OK;
+}
+
 int hm_runtime_set_graph(hm_runtime *rt, int32_t enable) {
   if (!rt) return hm::fail(HM_ERR_VALIDATION, "null runtime");
   rt->use_graph = enable != 0;

@@ -90,6 +90,25 @@ class HarmonyRuntime:
                         view.reshape(-1, d)[V:] = 0.0
         self.k[:] = 0.0
 
+    # -- checkpoint / resume (the host arenas are the model state) ------
+    def save_checkpoint(self, path: str) -> None:
+        """W and K arenas + optimizer step, as one .npz (no device state: the
+        GPU only holds transient packs between iterations)."""
+        np.savez(path, w=self.w, k=self.k, step=np.int64(self.lib.hm_runtime_get_step(self.handle)),
+                 spec=np.array([self.spec.n_layer, self.spec.d_model, self.spec.n_head, self.spec.seq_len,
+                                self.spec.vocab], dtype=np.int64))
+        return None
+
+    def load_checkpoint(self, path: str) -> None:
+        z = np.load(path)
+        want = np.array([self.spec.n_layer, self.spec.d_model, self.spec.n_head, self.spec.seq_len,
+                         self.spec.vocab], dtype=np.int64)
+        if not np.array_equal(z["spec"], want) or z["w"].shape != self.w.shape:
+            raise ValidationError("checkpoint was written for a different model")
+        self.w[:] = z["w"]
+        self.k[:] = z["k"]
+        NL.check(self.lib.hm_runtime_set_step(self.handle, int(z["step"])))
+
     # -- Harmony-PP across processes ----------------------------------------------
     @staticmethod
     def stash_bytes_for(graph: TaskGraph, profiles: ProfileSet) -> int:

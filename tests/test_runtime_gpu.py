@@ -136,3 +136,30 @@ def test_bert_large_c2_matches_oracle():
     cfg = H.Configuration(2, packs, 2, packs, 4, H.Mode.PP)
     rel_w, rel_m, rel_v, _ = _run(spec, cfg, steps=2, alpha=8 << 30)
     assert rel_w < STATE_RTOL
+
+
+def test_checkpoint_resume_is_exact(tmp_path):
+    """Training 4 steps == 2 steps, checkpoint, fresh runtime, resume, 2 steps."""
+    from paper_2202_01306_b200.runtime import HarmonyRuntime
+    spec = GPT_PRESETS["tiny"]
+    prof = gpt_profiles(spec)
+    mach = H.MachineModel(gpu_count=1, gpu_mem_capacity=4 << 30, pcie_bandwidth=55_000_000_000)
+    packs = ((0, 1), (2, 3))
+    g = H.generate_task_graph(H.Configuration(4, packs, 4, packs, 8, H.Mode.PP), mach, prof)
+    tok, lab = synthetic_batch(spec, 8)
+    a = HarmonyRuntime(spec, alpha_bytes=4 << 30)
+    a.init_weights(0)
+    a.load(g, mach, prof)
+    for _ in range(2):
+        a.step(tok, lab)
+    a.save_checkpoint(str(tmp_path / "ck.npz"))
+    ref = [a.step(tok, lab) for _ in range(2)]
+    w_ref = a.w.copy()
+    a.close()
+    b = HarmonyRuntime(spec, alpha_bytes=4 << 30)
+    b.load_checkpoint(str(tmp_path / "ck.npz"))
+    b.load(g, mach, prof)
+    got = [b.step(tok, lab) for _ in range(2)]
+    assert np.allclose(got, ref, rtol=1e-5)
+    assert np.linalg.norm(b.w - w_ref) / np.linalg.norm(w_ref) < 5e-4
+    b.close()
