@@ -77,8 +77,30 @@ __device__ __forceinline__ float dgelu_f(float x) {
   return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x * x);
 }
 
+// Operands the epilogue reads from global memory for one 32-column chunk,
+// fetched before the TMEM load so the two latencies overlap.
+struct EpiPre {
+  float4 f[8];  // residual / accumulate source (fp32)
+  uint4 b[4];   // pre-activation (bf16) for dGELU
+};
+
+__device__ __forceinline__ void epilogue_prefetch(const Args &a, int row, int col0, EpiPre &p) {
+  if (a.epi == HM_EPI_ACC_F32 || a.epi == HM_EPI_RESID_F32) {
+    const float *src = a.epi == HM_EPI_ACC_F32
+                           ? reinterpret_cast<const float *>(a.d) + (int64_t)row * a.ldd + col0
+                           : reinterpret_cast<const float *>(a.aux) + (int64_t)row * a.ld_aux + col0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) p.f[j] = reinterpret_cast<const float4 *>(src)[j];
+  } else if (a.epi == HM_EPI_DGELU_BF16) {
+    const __nv_bfloat16 *aux = reinterpret_cast<const __nv_bfloat16 *>(a.aux) + (int64_t)row * a.ld_aux + col0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) p.b[j] = reinterpret_cast<const uint4 *>(aux)[j];
+  }
+}
+
 // Apply the epilogue to 32 consecutive columns [col0, col0+32) of one row.
-__device__ __forceinline__ void epilogue_row(const Args &a, int row, int col0, float (&v)[32]) {
+// `pre` holds the chunk's global operands when the chunk is full.
+__device__ __forceinline__ void epilogue_row(const Args &a, int row, int col0, float (&v)[32], const EpiPre &pre) {
   const int N = a.N;
   const bool full = col0 + 32 <= N;
   if (a.bias && a.epi != HM_EPI_ACC_F32 && a.epi != HM_EPI_DGELU_BF16) {
@@ -107,7 +129,7 @@ __device__ __forceinline__ void epilogue_row(const Args &a, int row, int col0, f
         for (int j = 0; j < 8; ++j) {
           float4 o = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           if (src) {
-            float4 s = reinterpret_cast<const float4 *>(src)[j];
+            const float4 s = pre.f[j];
             o.x += s.x; o.y += s.y; o.z += s.z; o.w += s.w;
           }
           reinterpret_cast<float4 *>(dst)[j] = o;
@@ -127,7 +149,7 @@ __device__ __forceinline__ void epilogue_row(const Args &a, int row, int col0, f
         if (full) {
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            uint4 p = reinterpret_cast<const uint4 *>(aux)[j];
+            const uint4 p = pre.b[j];
             const __nv_bfloat162 *p2 = reinterpret_cast<const __nv_bfloat162 *>(&p);
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -300,13 +322,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c = half * kChunks; c < (half + 1) * kChunks; ++c) {
         const int col0 = nb * BN + c * 32;
         if (col0 >= args.N) break;
+        EpiPre pre;
+        if (row < args.M && col0 + 32 <= args.N) epilogue_prefetch(args, row, col0, pre);
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
         tmem_ld_wait();
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        if (row < args.M) epilogue_row(args, row, col0, v);
+        if (row < args.M) epilogue_row(args, row, col0, v, pre);
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);

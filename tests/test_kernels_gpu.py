@@ -239,7 +239,9 @@ def test_attention_bwd_tcgen05_opt_in():
     """The tcgen05 backward (opt-in via HM_ATTN_BWD=tc) matches autograd."""
     import subprocess
     import sys
-    code = ("import torch, sys; sys.path.insert(0, '.'); import tests.test_kernels_gpu as T; "
+    here = __import__("os").path.dirname(__import__("os").path.abspath(__file__))
+    code = (f"import torch, sys; sys.path.insert(0, {here!r}); sys.path.insert(0, {here + '/..'!r}); "
+            "import test_kernels_gpu as T; "
             "from paper_2202_01306_b200 import ops; "
             "T.test_attention_fwd_bwd(ops, 2, 256, 3, 64, True); T.test_attention_fwd_bwd(ops, 1, 512, 2, 64, False)")
     env = dict(__import__("os").environ, HM_ATTN_BWD="tc")
