@@ -148,6 +148,22 @@ def _pcie_gbs():
     return out
 
 
+def _gemm_groups(launches, top=8):
+    """GEMM launches of the profiled iteration grouped by FLOPs per launch
+    (one group per (M, N, K) product): where the GEMM time goes."""
+    groups = {}
+    for cls, fl, _by, ms in launches:
+        if int(cls) != 0:
+            continue
+        g = groups.setdefault(round(fl / 1e9, 3), [0, 0.0])
+        g[0] += 1
+        g[1] += ms
+    rows = [{"gflop": k, "launches": n, "ms_total": round(t, 3), "us_avg": round(1e3 * t / n, 2),
+             "tflops": round(k * n / t, 1) if t else 0.0} for k, (n, t) in groups.items()]
+    rows.sort(key=lambda r: -r["ms_total"])
+    return rows[:top]
+
+
 def step_flops(graph, spec) -> int:
     """Algorithmic FLOPs of one iteration: F member
     u*s*(24d^2+4sd) per block + 2*u*s*d*V for the head; B = 2F (+F recompute)."""
@@ -290,6 +306,7 @@ def run_native(args) -> None:
     rt.set_profiling(True)  # reset stats
     rt.step(tok_d, lab_d)
     kstats = rt.kernel_stats()
+    gemm_groups = _gemm_groups(rt.kernel_launches())
     prof_iter_ns = rt.counters()["iteration_ns"]
     rt.set_profiling(False)
     t_total = _max_over_ranks(t_dev, world)
@@ -349,6 +366,7 @@ def run_native(args) -> None:
                      "how": "per-launch CUDA events (graph event nodes) in one profiled iteration after the timed steps; "
                             "algorithmic 2MNK per launch"},
         "kernel_shares": share,
+        "gemm_by_gflop": gemm_groups,
         "stream_busy_frac": util,
         "last_iter_ms_unpipelined_view": round(cnt["iteration_ns"] / 1e6, 2),
         "adam_hbm": {"achieved_gbs": round(adam_gbs, 1), "peak": pk["hbm"], "frac": round(adam_gbs / pk["hbm"], 4)},

@@ -105,6 +105,7 @@ def lib() -> C.CDLL:
         "hm_runtime_ipc_import": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
         "hm_runtime_set_profiling": (C.c_int, [C.c_void_p, C.c_int32]),
         "hm_runtime_kernel_stats": (C.c_int, [C.c_void_p, P(C.c_double), C.c_int32]),
+        "hm_runtime_kernel_launches": (C.c_int, [C.c_void_p, P(C.c_double), C.c_int32]),
         "hm_k_adam": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_double,
                                 C.c_double, C.c_double, C.c_double, C.c_int32, C.c_float, C.c_void_p]),
         "hm_k_gemm": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,

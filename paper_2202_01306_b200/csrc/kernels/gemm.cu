@@ -238,6 +238,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
+      // programmatic dependent launch: everything above (barrier init, TMEM
+      // alloc, descriptor prefetch) overlapped the previous kernel's tail;
+      // global operands are read only after it has fully completed
+      griddep_wait();
       int stage = 0;
       uint32_t phase = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -304,11 +308,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mma_commit(&tfull[acc]);
       }
+      griddep_launch_dependents();  // only epilogues remain: let the next kernel set up
     }
   } else if (warp >= 4) {
     const int q = warp & 3;              // a warp may only touch TMEM lanes 32*(warp%4)..+31
     const int half = (warp - 4) >> 2;    // which half of the tile's columns
     constexpr int kChunks = BN / 32 / (kEpiWarps / 4);
+    griddep_wait();  // epilogue reads / writes global memory of the previous kernel's outputs
     int local = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
       int mb, nb;
@@ -432,7 +438,18 @@ static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const Args &a, c
   const bool f32 = a.epi == HM_EPI_STORE_F32 || a.epi == HM_EPI_ACC_F32 || a.epi == HM_EPI_RESID_F32;
   const double io = (double)a.M * a.N * (f32 ? 4 : 2) * (a.epi == HM_EPI_ACC_F32 || a.epi >= HM_EPI_RESID_F32 ? 2 : 1);
   ProfScope ps(KC_GEMM, s, 2.0 * a.M * a.N * a.K, 2.0 * ((double)a.M * a.K + (double)a.N * a.K) + io);
-  kern<<<grid, kThreads, C::kSmem, s>>>(ta, tb, a);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr_pdl[1];
+  attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr_pdl;
+  cfg.numAttrs = 1;
+  cudaError_t le = cudaLaunchKernelEx(&cfg, kern, ta, tb, a);
+  if (le != cudaSuccess) return fail(HM_ERR_DEVICE, std::string("gemm launch: ") + cudaGetErrorString(le));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(HM_ERR_DEVICE, std::string("gemm launch: ") + cudaGetErrorString(e));
   count_launch();

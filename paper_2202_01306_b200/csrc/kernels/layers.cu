@@ -4,6 +4,8 @@
 // per row, 16-byte vector accesses, fp32 math.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "../runtime/common.hpp"
 
 namespace hm {
@@ -336,7 +338,14 @@ static int ln_bwd_reg(const float *dy, const float *x, const float *mean, const 
 
 int ln_bwd(const float *dy, const float *x, const float *mean, const float *rstd, const float *g, const float *resid,
            float *out, void *out_bf, float *dg, float *db, int64_t rows, int d, cudaStream_t s) {
-  if (d % 4 == 0 && d <= 2048) {
+  // The register-accumulated variant (ln_bwd_reg_kernel) measured slower on
+  // B200 (70 us vs 38 us at 4096 x 1600: one 8-warp block per SM is too little
+  // memory parallelism); it stays behind HM_LN_BWD=reg for tuning.
+  static const bool use_reg = [] {
+    const char *e = getenv("HM_LN_BWD");
+    return e && e[0] == 'r';
+  }();
+  if (use_reg && d % 4 == 0 && d <= 2048) {
     ProfScope ps(KC_LAYERNORM, s, 0, (resid ? 16.0 : 12.0) * rows * d + (out_bf ? 2.0 * rows * d : 0));
     const int nv4 = (d / 4 + 31) / 32;
     if (nv4 <= 2) return ln_bwd_reg<2>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);

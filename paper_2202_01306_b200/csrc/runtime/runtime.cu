@@ -151,6 +151,7 @@ struct hm_runtime {
   bool profiling = false;
   hm::RtProfiler prof;
   double kstats[hm::KC_COUNT][4] = {{0}};  // ms, flops, bytes, launches (accumulated)
+  std::vector<double> klaunch;              // last profiled iteration: (class, flops, bytes, ms) per launch
   int device = 0;
   hm_model m{};
   int64_t alpha = 0;
@@ -1226,10 +1227,12 @@ static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *l
   float it_ms = 0;
   HM_CUDA(cudaEventElapsedTime(&it_ms, rt.ev_iter0, rt.ev_iter1));
   if (rt.profiling) {
+    rt.klaunch.clear();
     for (auto &p : rt.prof.recs) {
       if (!p.e1) continue;
       float ms = 0;
       HM_CUDA(cudaEventElapsedTime(&ms, p.e0, p.e1));
+      rt.klaunch.insert(rt.klaunch.end(), {(double)p.cls, p.flops, p.bytes, (double)ms});
       rt.kstats[p.cls][0] += ms;
       rt.kstats[p.cls][1] += p.flops;
       rt.kstats[p.cls][2] += p.bytes;
@@ -1589,6 +1592,14 @@ int hm_runtime_kernel_stats(const hm_runtime *rt, double *out, int32_t cap) {
   for (int c = 0; c < hm::KC_COUNT; ++c)
     for (int j = 0; j < 4; ++j) out[c * 4 + j] = rt->kstats[c][j];
   return hm::KC_COUNT;
+}
+
+int hm_runtime_kernel_launches(const hm_runtime *rt, double *out, int32_t cap) {
+  int n = (int)(rt->klaunch.size() / 4);
+  if (out)
+    for (int i = 0; i < n && i < cap; ++i)
+      for (int j = 0; j < 4; ++j) out[4 * i + j] = rt->klaunch[4 * i + j];
+  return n;
 }
 
 void hm_runtime_free(hm_runtime *rt) {

@@ -238,6 +238,14 @@ class HarmonyRuntime:
         return {c: {"ms": buf[4 * i], "flops": buf[4 * i + 1], "bytes": buf[4 * i + 2],
                     "launches": int(buf[4 * i + 3])} for i, c in enumerate(self.KERNEL_CLASSES)}
 
+    def kernel_launches(self) -> np.ndarray:
+        """[n, 4] (class, flops, bytes, ms) per launch of the last profiled iteration."""
+        n = self.lib.hm_runtime_kernel_launches(self.handle, None, 0)
+        out = np.zeros((max(n, 0), 4), dtype=np.float64)
+        if n > 0:
+            self.lib.hm_runtime_kernel_launches(self.handle, out.ctypes.data_as(C.POINTER(C.c_double)), n)
+        return out
+
     def measured_items(self) -> np.ndarray:
         n1 = self.lib.hm_runtime_ledger_count(self.handle)
         n2 = self.lib.hm_runtime_trace_count(self.handle)

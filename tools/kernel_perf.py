@@ -26,6 +26,7 @@ def peaks():
 
 
 FLUSH = None
+GRAPH = False
 
 
 def flush():
@@ -33,6 +34,28 @@ def flush():
     if FLUSH is None:
         FLUSH = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     FLUSH.zero_()
+
+
+def time_graph(fn, reps=50):
+    """Steady-state per-launch time: `reps` back-to-back launches captured in
+    one CUDA graph (no flush, no host gaps; consecutive launches overlap
+    through programmatic dependent launch where the kernel supports it)."""
+    fn()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(reps):
+                fn()
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
 
 
 def timeit(fn, iters=20, warm=3):
@@ -65,6 +88,9 @@ def bench_gemm():
               ("fwd_fc2", 4096, 1600, 6400, False, False, "resid_f32"),
               ("dgrad_fc1", 4096, 1600, 6400, False, True, "f32"),
               ("wgrad_fc1", 6400, 1600, 4096, True, True, "acc_f32"),
+              ("fc1_plain_epi", 4096, 6400, 1600, False, False, "bf16"),
+              ("fc1_long_k", 4096, 6400, 6400, False, False, "bf16"),
+              ("fc1_big_m", 16384, 6400, 1600, False, False, "bf16"),
               ("square8k", 8192, 8192, 8192, False, False, "bf16"),
               ("fwd_40b_qkv", 4096, 24576, 8192, False, False, "bf16")]
     for name, M, N, K, amn, bmn, epi in shapes:
@@ -78,12 +104,14 @@ def bench_gemm():
             aux = torch.zeros(M, N, device="cuda")
         if epi in ("gelu_bf16", "dgelu_bf16"):
             aux = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
-        ms = timeit(lambda: ops.gemm(a, b, d, a_mn=amn, b_mn=bmn, epi=epi, bias=bias, aux=aux))
+        fn = lambda: ops.gemm(a, b, d, a_mn=amn, b_mn=bmn, epi=epi, bias=bias, aux=aux)  # noqa: E731
+        ms = time_graph(fn) if GRAPH else timeit(fn)
         tf = 2 * M * N * K / ms / 1e9
         ref_ms = None
         if not amn and not bmn:
-            ref_ms = timeit(lambda: torch.matmul(a, b.t()))
-        print(json.dumps({"kernel": "gemm", "shape": name, "M": M, "N": N, "K": K, "ms": round(ms, 4),
+            rf = lambda: torch.matmul(a, b.t())  # noqa: E731
+            ref_ms = time_graph(rf) if GRAPH else timeit(rf)
+        print(json.dumps({"kernel": "gemm", "timing": "graph50" if GRAPH else "single+flush", "shape": name, "M": M, "N": N, "K": K, "ms": round(ms, 4),
                           "tflops": round(tf, 1), "frac": round(tf / tf_peak, 3), "peak": kind,
                           "cublas_ms": None if ref_ms is None else round(ref_ms, 4)}), flush=True)
 
@@ -138,6 +166,9 @@ if __name__ == "__main__":
         bench_gemm_bn()
         sys.exit(0)
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if what == "gemm_graph":
+        GRAPH = True
+        what = "gemm"
     if what in ("attn", "all"):
         bench_attn()
     if what in ("gemm", "all"):
