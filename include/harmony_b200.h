@@ -220,7 +220,7 @@ int hm_k_adam(float *w, const float *g, float *k, int64_t n, double lr, double b
 enum hm_gemm_epilogue {
   HM_EPI_STORE_BF16 = 0,      /* D = acc (+bias) -> bf16                     */
   HM_EPI_STORE_F32 = 1,       /* D = acc (+bias) -> fp32                     */
-  HM_EPI_ACC_F32 = 2,         /* D += acc (fp32 read-modify-write)           */
+  HM_EPI_ACC_F32 = 2,         /* D += acc (fp32, TMA reduce-add; split-K ok)  */
   HM_EPI_RESID_F32 = 3,       /* D = R + acc + bias -> fp32 (R may alias D)  */
   HM_EPI_GELU_BF16 = 4,       /* P = acc + bias (bf16), D = gelu(P) (bf16)   */
   HM_EPI_DGELU_BF16 = 5       /* D = acc * gelu'(P) -> bf16                  */
@@ -230,6 +230,16 @@ int hm_k_gemm(const void *a, const void *b, void *d, int64_t m, int64_t n, int64
               int32_t epilogue, const float *bias, const void *aux, int64_t ld_aux,
               int32_t batch, int64_t stride_a, int64_t stride_b, int64_t stride_d,
               void *stream);
+
+/* Tile configuration the GEMM picks for an (m, n, k, epilogue) problem:
+ * bn = output tile width (128 | 256), cta_pair = 1 (128-row tile on one SM) or
+ * 2 (256-row tile on a CTA pair, tcgen05.mma.cta_group::2), splits = split-K
+ * factor (ACC_F32 only; partial sums meet in a TMA reduce-add). */
+int hm_k_gemm_tile(int64_t m, int64_t n, int64_t k, int32_t epilogue, int32_t *bn,
+                   int32_t *cta_pair, int32_t *splits);
+/* Force a tile configuration for every later GEMM of the process (0 = auto);
+ * for tests and tuning (same as HM_GEMM_BN / HM_GEMM_CG / HM_GEMM_SPLITK). */
+int hm_k_gemm_set_tile(int32_t bn, int32_t cta_pair, int32_t splits);
 
 /* Fused attention over qkv [batch*seq, 3*heads*head_dim] bf16 (q|k|v thirds).
  * out [batch*seq, heads*head_dim] bf16; lse [batch*seq, heads] fp32 (log2).

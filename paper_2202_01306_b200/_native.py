@@ -112,6 +112,9 @@ def lib() -> C.CDLL:
                                 C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
                                 C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int64, C.c_int64,
                                 C.c_int64, C.c_void_p]),
+        "hm_k_gemm_tile": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int32, P(C.c_int32), P(C.c_int32),
+                                     P(C.c_int32)]),
+        "hm_k_gemm_set_tile": (C.c_int, [C.c_int32, C.c_int32, C.c_int32]),
         "hm_launch_count": (C.c_int64, []),
         "hm_k_attn_fwd": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p] + [C.c_int32] * 5 + [C.c_void_p]),
         "hm_k_attn_fwd_tc": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p] + [C.c_int32] * 5 + [C.c_void_p]),

@@ -18,6 +18,7 @@
 // The epilogue of tile i overlaps the MMAs of tile i+1.
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -40,6 +41,7 @@ constexpr int kThreads = 128 + 32 * kEpiWarps;
 
 struct Args {
   int32_t M, N, K, num_m, num_n, num_k;
+  int32_t splits;  // split-K factor (ACC_F32 only: partial sums meet in the TMA reduce-add)
   void *d;
   int64_t ldd;
   const float *bias;
@@ -48,15 +50,27 @@ struct Args {
   int32_t epi;
 };
 
-template <int BN>
+// CG = CTAs per tile: 1 (128 x BN tile, one SM) or 2 (a CTA pair on one TPC
+// computes a 256 x BN tile with tcgen05.mma.cta_group::2: each CTA stages its
+// own 128 rows of A and HALF of B's BN rows, so per-SM operand traffic per
+// FLOP drops by a third at BN = 256).
+template <int BN, int CG>
 struct Cfg {
-  static constexpr int kStages = BN == 256 ? 4 : 6;
+  static constexpr int kBRows = BN / CG;  // B rows staged per CTA
   static constexpr uint32_t kABytes = BM * BK * 2;
-  static constexpr uint32_t kBBytes = BN * BK * 2;
+  static constexpr uint32_t kBBytes = kBRows * BK * 2;
+  static constexpr int kStages = (int)((196608u) / (kABytes + kBBytes)) > 8 ? 8 : (int)(196608u / (kABytes + kBBytes));
   static constexpr uint32_t kTmemCols = 2 * BN >= 512 ? 512 : (2 * BN >= 256 ? 256 : 128);
-  static constexpr size_t kSmem = 1024 + (size_t)kStages * (kABytes + kBBytes) + 256;
+  static constexpr size_t kSmem = 1024 + (size_t)kStages * (kABytes + kBBytes) + kEpiWarps * 4096 + 256;
 };
 
+// k-block range of split `sp` of `n` over num_k k-blocks
+__device__ __forceinline__ void split_range(int sp, int n, int num_k, int &lo, int &hi) {
+  lo = (int)((int64_t)sp * num_k / n);
+  hi = (int)((int64_t)(sp + 1) * num_k / n);
+}
+
+// grouped raster: kGroupM row-tiles sweep the column tiles together (L2 reuse of B)
 __device__ __forceinline__ void tile_coord(int t, int num_m, int num_n, int &mb, int &nb) {
   const int per_group = kGroupM * num_n;
   const int g = t / per_group;
@@ -69,42 +83,35 @@ __device__ __forceinline__ void tile_coord(int t, int num_m, int num_n, int &mb,
 
 __device__ __forceinline__ float gelu_f(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  return 0.5f * x * (1.f + tanhf(k0 * (x + k1 * x * x * x)));
+  return 0.5f * x * (1.f + tanh_approx(k0 * (x + k1 * x * x * x)));
 }
 __device__ __forceinline__ float dgelu_f(float x) {
   const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  const float t = tanhf(k0 * (x + k1 * x * x * x));
+  const float t = tanh_approx(k0 * (x + k1 * x * x * x));
   return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * k0 * (1.f + 3.f * k1 * x * x);
 }
 
-// Operands the epilogue reads from global memory for one 32-column chunk,
-// fetched before the TMEM load so the two latencies overlap.
-struct EpiPre {
-  float4 f[8];  // residual / accumulate source (fp32)
-  uint4 b[4];   // pre-activation (bf16) for dGELU
-};
+// Epilogue staging: each epilogue warp owns a 4 KB shared-memory buffer that
+// holds one 32-row x 32-column chunk of the tile.  fp32 chunks are 128 B rows
+// in the TMA SWIZZLE_128B layout, bf16 chunks 64 B rows in SWIZZLE_64B, so the
+// thread-per-row writes out of tcgen05.ld are bank-conflict free and the chunk
+// leaves (and source operands arrive) as one coalesced TMA bulk tensor copy.
+constexpr int kEpiBuf = 4096;
 
-__device__ __forceinline__ void epilogue_prefetch(const Args &a, int row, int col0, EpiPre &p) {
-  if (a.epi == HM_EPI_ACC_F32 || a.epi == HM_EPI_RESID_F32) {
-    const float *src = a.epi == HM_EPI_ACC_F32
-                           ? reinterpret_cast<const float *>(a.d) + (int64_t)row * a.ldd + col0
-                           : reinterpret_cast<const float *>(a.aux) + (int64_t)row * a.ld_aux + col0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) p.f[j] = reinterpret_cast<const float4 *>(src)[j];
-  } else if (a.epi == HM_EPI_DGELU_BF16) {
-    const __nv_bfloat16 *aux = reinterpret_cast<const __nv_bfloat16 *>(a.aux) + (int64_t)row * a.ld_aux + col0;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) p.b[j] = reinterpret_cast<const uint4 *>(aux)[j];
-  }
-}
+__device__ __forceinline__ uint32_t sw128_off(int r, int j) { return r * 128 + ((j ^ (r & 7)) << 4); }
+__device__ __forceinline__ uint32_t sw64_off(int r, int j) { return r * 64 + ((j ^ ((r >> 1) & 3)) << 4); }
 
-// Apply the epilogue to 32 consecutive columns [col0, col0+32) of one row.
-// `pre` holds the chunk's global operands when the chunk is full.
-__device__ __forceinline__ void epilogue_row(const Args &a, int row, int col0, float (&v)[32], const EpiPre &pre) {
+// Sources read back through TMA before the epilogue math: the residual
+// (RESID_F32) and the pre-activation (DGELU_BF16).  ACC_F32 reads nothing: its
+// chunk leaves as a TMA reduce-add, which also makes split-K free of fix-ups.
+__device__ __forceinline__ bool epi_src_f32(int epi) { return epi == HM_EPI_RESID_F32; }
+
+// Apply the epilogue to one row's 32 columns [col0, col0+32) held in v and
+// write the result(s) into the warp's staging buffer (row r = lane).
+__device__ __forceinline__ void epilogue_chunk(const Args &a, int col0, float (&v)[32], uint8_t *buf, int r) {
   const int N = a.N;
-  const bool full = col0 + 32 <= N;
   if (a.bias && a.epi != HM_EPI_ACC_F32 && a.epi != HM_EPI_DGELU_BF16) {
-    if (full) {
+    if (col0 + 32 <= N) {
       const float4 *b4 = reinterpret_cast<const float4 *>(a.bias + col0);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -112,86 +119,65 @@ __device__ __forceinline__ void epilogue_row(const Args &a, int row, int col0, f
         v[4 * j] += b.x; v[4 * j + 1] += b.y; v[4 * j + 2] += b.z; v[4 * j + 3] += b.w;
       }
     } else {
+#pragma unroll
       for (int j = 0; j < 32; ++j)
-        if (col0 + j < N) v[j] += a.bias[col0 + j];
+        if (col0 + j < N) v[j] += __ldg(a.bias + col0 + j);
     }
   }
   switch (a.epi) {
     case HM_EPI_STORE_F32:
     case HM_EPI_ACC_F32:
     case HM_EPI_RESID_F32: {
-      float *dst = reinterpret_cast<float *>(a.d) + (int64_t)row * a.ldd + col0;
-      const float *src = nullptr;
-      if (a.epi == HM_EPI_ACC_F32) src = dst;
-      if (a.epi == HM_EPI_RESID_F32) src = reinterpret_cast<const float *>(a.aux) + (int64_t)row * a.ld_aux + col0;
-      if (full) {
+      const bool src = a.epi == HM_EPI_RESID_F32;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          float4 o = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-          if (src) {
-            const float4 s = pre.f[j];
-            o.x += s.x; o.y += s.y; o.z += s.z; o.w += s.w;
-          }
-          reinterpret_cast<float4 *>(dst)[j] = o;
+      for (int j = 0; j < 8; ++j) {
+        float4 *p = reinterpret_cast<float4 *>(buf + sw128_off(r, j));
+        float4 o = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+        if (src) {
+          const float4 s = *p;
+          o.x += s.x; o.y += s.y; o.z += s.z; o.w += s.w;
         }
-      } else {
-        for (int j = 0; j < 32; ++j)
-          if (col0 + j < N) dst[j] = v[j] + (src ? src[j] : 0.f);
+        *p = o;
       }
       break;
     }
     case HM_EPI_STORE_BF16:
     case HM_EPI_GELU_BF16:
     case HM_EPI_DGELU_BF16: {
-      __nv_bfloat16 *dst = reinterpret_cast<__nv_bfloat16 *>(a.d) + (int64_t)row * a.ldd + col0;
-      __nv_bfloat16 *aux = a.aux ? reinterpret_cast<__nv_bfloat16 *>(a.aux) + (int64_t)row * a.ld_aux + col0 : nullptr;
+      uint8_t *out = buf;
       if (a.epi == HM_EPI_DGELU_BF16) {
-        if (full) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint4 p = pre.b[j];
-            const __nv_bfloat162 *p2 = reinterpret_cast<const __nv_bfloat162 *>(&p);
+        for (int j = 0; j < 4; ++j) {
+          const uint4 p = *reinterpret_cast<const uint4 *>(buf + sw64_off(r, j));
+          const __nv_bfloat162 *p2 = reinterpret_cast<const __nv_bfloat162 *>(&p);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              float2 f = __bfloat1622float2(p2[e]);
-              v[8 * j + 2 * e] *= dgelu_f(f.x);
-              v[8 * j + 2 * e + 1] *= dgelu_f(f.y);
-            }
+          for (int e = 0; e < 4; ++e) {
+            float2 f = __bfloat1622float2(p2[e]);
+            v[8 * j + 2 * e] *= dgelu_f(f.x);
+            v[8 * j + 2 * e + 1] *= dgelu_f(f.y);
           }
-        } else {
-          for (int j = 0; j < 32; ++j)
-            if (col0 + j < N) v[j] *= dgelu_f(__bfloat162float(aux[j]));
         }
       } else if (a.epi == HM_EPI_GELU_BF16) {
-        // store the pre-activation, then activate
-        if (full) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            uint4 p;
-            __nv_bfloat162 *p2 = reinterpret_cast<__nv_bfloat162 *>(&p);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) p2[e] = __floats2bfloat162_rn(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]);
-            reinterpret_cast<uint4 *>(aux)[j] = p;
-          }
-        } else {
-          for (int j = 0; j < 32; ++j)
-            if (col0 + j < N) aux[j] = __float2bfloat16_rn(v[j]);
-        }
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
-      }
-      if (full) {
+        // pre-activation -> first half of the buffer, activation -> second half
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           uint4 p;
           __nv_bfloat162 *p2 = reinterpret_cast<__nv_bfloat162 *>(&p);
 #pragma unroll
           for (int e = 0; e < 4; ++e) p2[e] = __floats2bfloat162_rn(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]);
-          reinterpret_cast<uint4 *>(dst)[j] = p;
+          *reinterpret_cast<uint4 *>(buf + sw64_off(r, j)) = p;
         }
-      } else {
-        for (int j = 0; j < 32; ++j)
-          if (col0 + j < N) dst[j] = __float2bfloat16_rn(v[j]);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
+        out = buf + kEpiBuf / 2;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint4 p;
+        __nv_bfloat162 *p2 = reinterpret_cast<__nv_bfloat162 *>(&p);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) p2[e] = __floats2bfloat162_rn(v[8 * j + 2 * e], v[8 * j + 2 * e + 1]);
+        *reinterpret_cast<uint4 *>(out + sw64_off(r, j)) = p;
       }
       break;
     }
@@ -200,41 +186,60 @@ __device__ __forceinline__ void epilogue_row(const Args &a, int row, int col0, f
   }
 }
 
-template <int BN, int A_MN, int B_MN>
+template <int BN, int A_MN, int B_MN, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Args args) {
-  using C = Cfg<BN>;
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX, Args args) {
+  using C = Cfg<BN, CG>;
+  constexpr int kTileM = BM * CG;
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sA = smem;
   uint8_t *sB = smem + C::kStages * C::kABytes;
-  uint64_t *full = reinterpret_cast<uint64_t *>(sB + C::kStages * C::kBBytes);
+  uint8_t *sEpi = sB + C::kStages * C::kBBytes;
+  uint64_t *full = reinterpret_cast<uint64_t *>(sEpi + kEpiWarps * kEpiBuf);
   uint64_t *empty = full + C::kStages;
   uint64_t *tfull = empty + C::kStages;
   uint64_t *tempty = tfull + 2;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+  uint64_t *ebar = tempty + 2;  // one per epilogue warp: source chunk landed
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(ebar + kEpiWarps);
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;  // 0 = pair leader (issues the MMAs)
+  const bool leader = rank == 0;
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    tma_prefetch(&tmD);
+    tma_prefetch(&tmX);
     for (int i = 0; i < C::kStages; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 32 * kEpiWarps);
+      mbar_init(&tempty[i], CG * kEpiWarps);  // one arrival per epilogue warp of every CTA of the tile
     }
+    for (int i = 0; i < kEpiWarps; ++i) mbar_init(&ebar[i], 1);
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc<C::kTmemCols>(tmem_slot);
+  if (warp == 2) {
+    if (CG == 2)
+      tmem_alloc_pair<C::kTmemCols>(tmem_slot);
+    else
+      tmem_alloc<C::kTmemCols>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 2)
+    cluster_sync();  // peer barriers initialised before any remote arrive / complete_tx
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int ntiles = args.num_m * args.num_n;
+  const int nsplit = args.splits;
+  const int ntiles = args.num_m * args.num_n * nsplit;  // work units: (tile, k-split)
+  const int unit0 = blockIdx.x / CG, unit_step = gridDim.x / CG;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -244,27 +249,36 @@ __global__ void __launch_bounds__(kThreads, 1)
       griddep_wait();
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        int mb, nb;
-        tile_coord(t, args.num_m, args.num_n, mb, nb);
-        for (int kb = 0; kb < args.num_k; ++kb) {
+      for (int t = unit0; t < ntiles; t += unit_step) {
+        int mb, nb, kb0, kb1;
+        tile_coord(t / nsplit, args.num_m, args.num_n, mb, nb);
+        split_range(t % nsplit, nsplit, args.num_k, kb0, kb1);
+        const int m0 = mb * kTileM + (int)rank * BM;           // this CTA's A rows
+        const int n0 = nb * BN + (int)rank * C::kBRows;        // this CTA's B rows
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], C::kABytes + C::kBBytes);
+          uint32_t bar_addr = smem_u32(&full[stage]);
+          if (leader) mbar_expect_tx(&full[stage], CG * (C::kABytes + C::kBBytes));
+          if (CG == 2) bar_addr = mapa_shared(bar_addr, 0);
           uint8_t *a_dst = sA + stage * C::kABytes;
           uint8_t *b_dst = sB + stage * C::kBBytes;
+          auto load = [&](uint8_t *dst, const CUtensorMap *m, int c0, int c1) {
+            if (CG == 2)
+              tma_load_2d_pair(dst, m, bar_addr, c0, c1);
+            else
+              tma_load_2d(dst, m, &full[stage], c0, c1);
+          };
           if (!A_MN) {
-            tma_load_2d(a_dst, &tmA, &full[stage], kb * BK, mb * BM);
+            load(a_dst, &tmA, kb * BK, m0);
           } else {
 #pragma unroll
-            for (int c = 0; c < BM / 64; ++c)
-              tma_load_2d(a_dst + c * (BK * 128), &tmA, &full[stage], mb * BM + c * 64, kb * BK);
+            for (int c = 0; c < BM / 64; ++c) load(a_dst + c * (BK * 128), &tmA, m0 + c * 64, kb * BK);
           }
           if (!B_MN) {
-            tma_load_2d(b_dst, &tmB, &full[stage], kb * BK, nb * BN);
+            load(b_dst, &tmB, kb * BK, n0);
           } else {
 #pragma unroll
-            for (int c = 0; c < BN / 64; ++c)
-              tma_load_2d(b_dst + c * (BK * 128), &tmB, &full[stage], nb * BN + c * 64, kb * BK);
+            for (int c = 0; c < C::kBRows / 64; ++c) load(b_dst + c * (BK * 128), &tmB, n0 + c * 64, kb * BK);
           }
           if (++stage == C::kStages) {
             stage = 0;
@@ -274,18 +288,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, A_MN, B_MN);
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = idesc_bf16_f32(kTileM, BN, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+      for (int t = unit0; t < ntiles; t += unit_step, ++local) {
         const int acc = local & 1;
         const uint32_t use = (uint32_t)(local >> 1);
         mbar_wait(&tempty[acc], (use & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < args.num_k; ++kb) {
+        int kb0, kb1;
+        split_range(t % nsplit, nsplit, args.num_k, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_base = smem_u32(sA + stage * C::kABytes);
@@ -298,15 +314,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                                      : umma_desc_sw128(a_base + k * 32, 16, 1024);
             const uint64_t db = B_MN ? umma_desc_sw128(b_base + k * 2048, BK * 128, 1024)
                                      : umma_desc_sw128(b_base + k * 32, 16, 1024);
-            mma_bf16(d_tmem, da, db, idesc, (kb | k) != 0 ? 1u : 0u);
+            const uint32_t accum = (kb != kb0 || k != 0) ? 1u : 0u;
+            if (CG == 2)
+              mma_bf16_pair(d_tmem, da, db, idesc, accum);
+            else
+              mma_bf16(d_tmem, da, db, idesc, accum);
           }
-          mma_commit(&empty[stage]);
+          if (CG == 2)
+            mma_commit_pair(&empty[stage], 0x3);
+          else
+            mma_commit(&empty[stage]);
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit(&tfull[acc]);
+        if (CG == 2)
+          mma_commit_pair(&tfull[acc], 0x3);
+        else
+          mma_commit(&tfull[acc]);
       }
       griddep_launch_dependents();  // only epilogues remain: let the next kernel set up
     }
@@ -314,38 +340,89 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = warp & 3;              // a warp may only touch TMEM lanes 32*(warp%4)..+31
     const int half = (warp - 4) >> 2;    // which half of the tile's columns
     constexpr int kChunks = BN / 32 / (kEpiWarps / 4);
+    uint8_t *buf = sEpi + (warp - 4) * kEpiBuf;
+    uint64_t *bar = &ebar[warp - 4];
+    uint32_t bphase = 0;
+    const int epi = args.epi;
+    const bool src_f32 = epi_src_f32(epi);
+    const bool has_src = src_f32 || epi == HM_EPI_DGELU_BF16;
+    const CUtensorMap *tsrc = &tmX;
     griddep_wait();  // epilogue reads / writes global memory of the previous kernel's outputs
     int local = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++local) {
+    for (int t = unit0; t < ntiles; t += unit_step, ++local) {
       int mb, nb;
-      tile_coord(t, args.num_m, args.num_n, mb, nb);
+      tile_coord(t / nsplit, args.num_m, args.num_n, mb, nb);
       const int acc = local & 1;
       const uint32_t use = (uint32_t)(local >> 1);
+      const int row0 = mb * kTileM + (int)rank * BM + q * 32;
+      const int c_first = half * kChunks;
+      // free the staging buffer and start the chunk's source-operand load
+      auto prep = [&](int c) {
+        if (lane == 0) {
+          bulk_wait_read0();
+          if (has_src) {
+            mbar_expect_tx(bar, src_f32 ? 4096u : 2048u);
+            tma_load_2d(buf, tsrc, bar, nb * BN + c * 32, row0);
+          }
+        }
+        __syncwarp();
+      };
+      if (nb * BN + c_first * 32 < args.N) prep(c_first);  // overlaps the wait for the accumulator
       mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
-      const int row = mb * BM + q * 32 + (int)lane;
 #pragma unroll 1
-      for (int c = half * kChunks; c < (half + 1) * kChunks; ++c) {
+      for (int c = c_first; c < c_first + kChunks; ++c) {
         const int col0 = nb * BN + c * 32;
         if (col0 >= args.N) break;
-        EpiPre pre;
-        if (row < args.M && col0 + 32 <= args.N) epilogue_prefetch(args, row, col0, pre);
+        if (c != c_first) prep(c);
         uint32_t r[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c * 32, r);
         tmem_ld_wait();
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-        if (row < args.M) epilogue_row(args, row, col0, v, pre);
+        if (has_src) {
+          mbar_wait(bar, bphase);
+          bphase ^= 1;
+        }
+        epilogue_chunk(args, col0, v, buf, (int)lane);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (epi == HM_EPI_GELU_BF16) {
+            tma_store_2d(&tmX, buf, col0, row0);
+            tma_store_2d(&tmD, buf + kEpiBuf / 2, col0, row0);
+          } else if (epi == HM_EPI_ACC_F32) {
+            tma_reduce_add_2d(&tmD, buf, col0, row0);
+          } else {
+            tma_store_2d(&tmD, buf, col0, row0);
+          }
+          bulk_commit();
+        }
       }
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      __syncwarp();
+      if (lane == 0) {
+        if (CG == 2)
+          mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+        else
+          mbar_arrive(&tempty[acc]);
+      }
     }
+    if (lane == 0) bulk_wait0();  // stores complete before the CTA (and its smem) retires
   }
-  __syncthreads();
+  if (CG == 2) {
+    tc_fence_before();
+    cluster_sync();  // no remote arrive may target a CTA that has left; TMEM freed by both
+  } else {
+    __syncthreads();
+  }
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<C::kTmemCols>(tmem_base);
+    if (CG == 2)
+      tmem_dealloc_pair<C::kTmemCols>(tmem_base);
+    else
+      tmem_dealloc<C::kTmemCols>(tmem_base);
   }
 }
 
@@ -369,13 +446,15 @@ static EncodeFn encode_fn() {
   return fn;
 }
 
-// 2D bf16 map: inner dim d0 (contiguous), outer d1, row pitch in bytes, box {64, box1}, SW128.
+// 2D map: inner dim d0 (contiguous), outer d1, row pitch in bytes, box {box0, box1}.
+// Operand maps are bf16 {64, rows} SW128 (one 128-B swizzle atom per row);
+// epilogue maps are {32, 32} chunks: fp32 SW128 (128-B rows), bf16 SW64 (64-B rows).
 static int make_map(CUtensorMap *out, const void *ptr, uint64_t d0, uint64_t d1, uint64_t pitch_bytes,
-                    uint32_t box1) {
-  using Key = std::tuple<const void *, uint64_t, uint64_t, uint64_t, uint32_t>;
+                    uint32_t box1, bool f32 = false, uint32_t box0 = 64) {
+  using Key = std::tuple<const void *, uint64_t, uint64_t, uint64_t, uint32_t, uint32_t, bool>;
   static std::mutex mu;
   static std::map<Key, CUtensorMap> cache;
-  Key key{ptr, d0, d1, pitch_bytes, box1};
+  Key key{ptr, d0, d1, pitch_bytes, box1, box0, f32};
   {
     std::lock_guard<std::mutex> g(mu);
     auto it = cache.find(key);
@@ -388,11 +467,13 @@ static int make_map(CUtensorMap *out, const void *ptr, uint64_t d0, uint64_t d1,
   if (!fn) return fail(HM_ERR_DEVICE, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {d0, d1};
   cuuint64_t strides[1] = {pitch_bytes};
-  cuuint32_t box[2] = {64, box1};
+  cuuint32_t box[2] = {box0, box1};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const uint32_t row_bytes = box0 * (f32 ? 4 : 2);
+  const CUtensorMapSwizzle sw = row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  CUresult r = fn(out, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                  const_cast<void *>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(HM_ERR_DEVICE, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   std::lock_guard<std::mutex> g(mu);
   if (cache.size() > 4096) cache.clear();
@@ -402,14 +483,56 @@ static int make_map(CUtensorMap *out, const void *ptr, uint64_t d0, uint64_t d1,
 
 static int num_sms();
 
-// Tile width (measured on B200, profiles/r01_kernel_perf_bn.jsonl): the
-// 128x256 tile wins almost everywhere; the narrower tile only pays off for
-// short reductions (K <= 2048) with fewer than two waves of wide tiles, where
-// per-tile fill/drain dominates.
-static int pick_bn(int64_t M, int64_t N, int64_t K) {
+struct TileCfg {
+  int bn, cg, splits;
+};
+
+static int env_int(const char *name) {
+  const char *e = getenv(name);
+  return e ? atoi(e) : 0;
+}
+
+// Tile shape, CTA pairing and split-K from a wave-quantisation cost model:
+//   time = waves x (k-blocks per unit + ~4 k-blocks of fill / epilogue tail) x t_kb
+// where a unit is a (128*cg) x bn output tile (or one of its k-splits), waves =
+// ceil(units / (SMs / cg)), and t_kb is the time of one 64-deep k-block of a
+// unit relative to the MMA bound: bn / 256 / eff(cg, bn).  eff is the
+// fraction of tensor peak each shape sustains on long-K problems, measured on
+// B200 (profiles/r01_gemm_tile_sweep.jsonl: 8192^3 runs at 1550 TFLOP/s on
+// 256x256 pair tiles, 1382 on 128x256, < 1000 on 128-wide tiles; operand
+// traffic per SM per MMA cycle 64 / 96 / 96-128 B).  Split-K only for ACC_F32
+// (partials meet in the TMA reduce-add).  HM_GEMM_BN / HM_GEMM_CG /
+// HM_GEMM_SPLITK force a choice.
+static int g_force_bn = env_int("HM_GEMM_BN"), g_force_cg = env_int("HM_GEMM_CG"),
+           g_force_s = env_int("HM_GEMM_SPLITK");
+
+static TileCfg pick_tile(int64_t M, int64_t N, int64_t K, int epi) {
+  const int env_bn = g_force_bn, env_cg = g_force_cg, env_s = g_force_s;
   const int64_t sms = num_sms();
-  const int64_t tiles256 = ((M + BM - 1) / BM) * ((N + 255) / 256);
-  return (tiles256 < 2 * sms && K <= 2048) ? 128 : 256;
+  const int64_t num_k = (K + BK - 1) / BK;
+  TileCfg best{256, 1, 1};
+  double best_t = 1e300;
+  for (int cg = 1; cg <= 2; ++cg) {
+    if (env_cg && cg != env_cg) continue;
+    for (int bn = 128; bn <= 256; bn += 128) {
+      if (env_bn && bn != env_bn) continue;
+      const double eff = bn == 128 ? 0.55 : (cg == 1 ? 0.80 : 0.93);
+      const double t_kb = bn / 256.0 / eff;
+      const int64_t tiles = ((M + BM * cg - 1) / (BM * cg)) * ((N + bn - 1) / bn);
+      const int64_t slots = sms / cg;
+      for (int s = 1; s <= (epi == HM_EPI_ACC_F32 ? 8 : 1); ++s) {
+        if (env_s && s != env_s) continue;
+        if (s > 1 && num_k / s < 8) break;
+        const double waves = (double)((tiles * s + slots - 1) / slots);
+        const double t = waves * ((double)num_k / s + 4.0) * t_kb * (s > 1 ? 1.03 : 1.0);
+        if (t < best_t) {
+          best_t = t;
+          best = TileCfg{bn, cg, s};
+        }
+      }
+    }
+  }
+  return best;
 }
 
 static int num_sms() {
@@ -423,18 +546,19 @@ static int num_sms() {
   return n;
 }
 
-template <int BN, int A_MN, int B_MN>
-static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const Args &a, cudaStream_t s) {
-  using C = Cfg<BN>;
+template <int BN, int A_MN, int B_MN, int CG>
+static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &td, const CUtensorMap &tx,
+                  const Args &a, cudaStream_t s) {
+  using C = Cfg<BN, CG>;
   static bool attr = false;
-  auto kern = gemm_kernel<BN, A_MN, B_MN>;
+  auto kern = gemm_kernel<BN, A_MN, B_MN, CG>;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
     if (e != cudaSuccess) return fail(HM_ERR_DEVICE, std::string("gemm smem attr: ") + cudaGetErrorString(e));
     attr = true;
   }
-  const int ntiles = a.num_m * a.num_n;
-  const int grid = ntiles < num_sms() ? ntiles : num_sms();
+  const int units = a.num_m * a.num_n * a.splits;
+  const int grid = CG * std::min(units, num_sms() / CG);
   const bool f32 = a.epi == HM_EPI_STORE_F32 || a.epi == HM_EPI_ACC_F32 || a.epi == HM_EPI_RESID_F32;
   const double io = (double)a.M * a.N * (f32 ? 4 : 2) * (a.epi == HM_EPI_ACC_F32 || a.epi >= HM_EPI_RESID_F32 ? 2 : 1);
   ProfScope ps(KC_GEMM, s, 2.0 * a.M * a.N * a.K, 2.0 * ((double)a.M * a.K + (double)a.N * a.K) + io);
@@ -443,12 +567,16 @@ static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const Args &a, c
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = s;
-  cudaLaunchAttribute attr_pdl[1];
-  attr_pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr_pdl[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr_pdl;
-  cfg.numAttrs = 1;
-  cudaError_t le = cudaLaunchKernelEx(&cfg, kern, ta, tb, a);
+  cudaLaunchAttribute attrs[2];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  attrs[1].id = cudaLaunchAttributeClusterDimension;
+  attrs[1].val.clusterDim.x = CG;
+  attrs[1].val.clusterDim.y = 1;
+  attrs[1].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = CG > 1 ? 2 : 1;
+  cudaError_t le = cudaLaunchKernelEx(&cfg, kern, ta, tb, td, tx, a);
   if (le != cudaSuccess) return fail(HM_ERR_DEVICE, std::string("gemm launch: ") + cudaGetErrorString(le));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(HM_ERR_DEVICE, std::string("gemm launch: ") + cudaGetErrorString(e));
@@ -469,37 +597,71 @@ int run(const void *A, const void *B, void *D, int64_t M, int64_t N, int64_t K, 
     return fail(HM_ERR_VALIDATION, "gemm: epilogue needs an aux tensor");
   if (aux && ((ld_aux * (epi == HM_EPI_RESID_F32 ? 4 : 2)) % 16 || ((uintptr_t)aux & 15)))
     return fail(HM_ERR_VALIDATION, "gemm: aux must be 16B aligned with 16B pitch");
-  static const int env_bn = [] {
-    const char *e = getenv("HM_GEMM_BN");
-    return e ? atoi(e) : 0;
-  }();
-  int bn = force_bn ? force_bn : env_bn ? env_bn : pick_bn(M, N, K);
+  TileCfg tc = pick_tile(M, N, K, epi);
+  if (force_bn) tc.bn = force_bn;
+  const int bn = tc.bn;
   Args a{};
   a.M = (int)M; a.N = (int)N; a.K = (int)K;
-  a.num_m = (int)((M + BM - 1) / BM);
+  a.num_m = (int)((M + BM * tc.cg - 1) / (BM * tc.cg));
   a.num_n = (int)((N + bn - 1) / bn);
   a.num_k = (int)((K + BK - 1) / BK);
+  a.splits = tc.splits;
   a.d = D; a.ldd = ldd; a.bias = bias; a.aux = aux; a.ld_aux = ld_aux; a.epi = epi;
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, td, tx;
   int rc = a_mn ? make_map(&ta, A, M, K, lda * 2, 64) : make_map(&ta, A, K, M, lda * 2, BM);
   if (rc) return rc;
-  rc = b_mn ? make_map(&tb, B, N, K, ldb * 2, 64) : make_map(&tb, B, K, N, ldb * 2, bn);
+  rc = b_mn ? make_map(&tb, B, N, K, ldb * 2, 64) : make_map(&tb, B, K, N, ldb * 2, bn / tc.cg);
   if (rc) return rc;
-  const int key = (bn == 256 ? 4 : 0) | (a_mn ? 2 : 0) | (b_mn ? 1 : 0);
+  rc = make_map(&td, D, N, M, ldd * (f32out ? 4 : 2), 32, f32out, 32);
+  if (rc) return rc;
+  if (aux) {
+    const bool aux_f32 = epi == HM_EPI_RESID_F32;
+    rc = make_map(&tx, aux, N, M, ld_aux * (aux_f32 ? 4 : 2), 32, aux_f32, 32);
+    if (rc) return rc;
+  } else {
+    tx = td;
+  }
+  const int key = (tc.cg == 2 ? 8 : 0) | (bn == 256 ? 4 : 0) | (a_mn ? 2 : 0) | (b_mn ? 1 : 0);
   switch (key) {
-    case 0: return launch<128, 0, 0>(ta, tb, a, stream);
-    case 1: return launch<128, 0, 1>(ta, tb, a, stream);
-    case 2: return launch<128, 1, 0>(ta, tb, a, stream);
-    case 3: return launch<128, 1, 1>(ta, tb, a, stream);
-    case 4: return launch<256, 0, 0>(ta, tb, a, stream);
-    case 5: return launch<256, 0, 1>(ta, tb, a, stream);
-    case 6: return launch<256, 1, 0>(ta, tb, a, stream);
-    default: return launch<256, 1, 1>(ta, tb, a, stream);
+    case 0: return launch<128, 0, 0, 1>(ta, tb, td, tx, a, stream);
+    case 1: return launch<128, 0, 1, 1>(ta, tb, td, tx, a, stream);
+    case 2: return launch<128, 1, 0, 1>(ta, tb, td, tx, a, stream);
+    case 3: return launch<128, 1, 1, 1>(ta, tb, td, tx, a, stream);
+    case 4: return launch<256, 0, 0, 1>(ta, tb, td, tx, a, stream);
+    case 5: return launch<256, 0, 1, 1>(ta, tb, td, tx, a, stream);
+    case 6: return launch<256, 1, 0, 1>(ta, tb, td, tx, a, stream);
+    case 7: return launch<256, 1, 1, 1>(ta, tb, td, tx, a, stream);
+    case 8: return launch<128, 0, 0, 2>(ta, tb, td, tx, a, stream);
+    case 9: return launch<128, 0, 1, 2>(ta, tb, td, tx, a, stream);
+    case 10: return launch<128, 1, 0, 2>(ta, tb, td, tx, a, stream);
+    case 11: return launch<128, 1, 1, 2>(ta, tb, td, tx, a, stream);
+    case 12: return launch<256, 0, 0, 2>(ta, tb, td, tx, a, stream);
+    case 13: return launch<256, 0, 1, 2>(ta, tb, td, tx, a, stream);
+    case 14: return launch<256, 1, 0, 2>(ta, tb, td, tx, a, stream);
+    default: return launch<256, 1, 1, 2>(ta, tb, td, tx, a, stream);
   }
 }
 
 }  // namespace gemm
 }  // namespace hm
+
+extern "C" int hm_k_gemm_set_tile(int32_t bn, int32_t cta_pair, int32_t splits) {
+  if ((bn && bn != 128 && bn != 256) || (cta_pair && cta_pair != 1 && cta_pair != 2) || splits < 0 || splits > 8)
+    return hm::fail(HM_ERR_VALIDATION, "gemm tile override: bn in {0,128,256}, cta_pair in {0,1,2}, splits in [0,8]");
+  hm::gemm::g_force_bn = bn;
+  hm::gemm::g_force_cg = cta_pair;
+  hm::gemm::g_force_s = splits;
+  return HM_OK;
+}
+
+extern "C" int hm_k_gemm_tile(int64_t m, int64_t n, int64_t k, int32_t epilogue, int32_t *bn, int32_t *cta_pair,
+                              int32_t *splits) {
+  const hm::gemm::TileCfg t = hm::gemm::pick_tile(m, n, k, epilogue);
+  *bn = t.bn;
+  *cta_pair = t.cg;
+  *splits = t.splits;
+  return HM_OK;
+}
 
 extern "C" int hm_k_gemm(const void *a, const void *b, void *d, int64_t m, int64_t n, int64_t k, int64_t lda,
                          int64_t ldb, int64_t ldd, int32_t a_major, int32_t b_major, int32_t epilogue,

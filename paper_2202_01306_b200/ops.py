@@ -44,6 +44,18 @@ def gemm(a, b, d, *, a_mn=False, b_mn=False, epi="f32", bias=None, aux=None):
     return d
 
 
+def gemm_tile(M, N, K, epi="f32"):
+    """(bn, cta_pair, splits) the GEMM picks for this problem."""
+    bn, cg, sp = C.c_int32(), C.c_int32(), C.c_int32()
+    NL.check(N_lib().hm_k_gemm_tile(M, N, K, EPI[epi], C.byref(bn), C.byref(cg), C.byref(sp)))
+    return bn.value, cg.value, sp.value
+
+
+def gemm_set_tile(bn=0, cta_pair=0, splits=0):
+    """Force the GEMM tile configuration process-wide (0 = automatic)."""
+    NL.check(N_lib().hm_k_gemm_set_tile(bn, cta_pair, splits))
+
+
 def adam(w, g, k, *, lr, beta1, beta2, eps, step, grad_scale=1.0):
     rc = N_lib().hm_k_adam(_ptr(w), _ptr(g), _ptr(k), w.numel(), lr, beta1, beta2, eps, step,
                            grad_scale, _stream())

@@ -48,9 +48,11 @@ def test_gemm_dgrad_k_mn(ops, M, N, K):
 
 
 @pytest.mark.parametrize("O,I,T", [(128, 128, 128), (1600, 1600, 4096), (4800, 1600, 1024), (6400, 1600, 512),
-                                   (200, 136, 256)])
+                                   (200, 136, 256), (1000, 392, 8192)])
 def test_gemm_wgrad_mn_mn_accumulate(ops, O, I, T):
-    """dW[O,I] += dY[T,O]^T . X[T,I]  (both MN-major), fp32 accumulate."""
+    """dW[O,I] += dY[T,O]^T . X[T,I]  (both MN-major), fp32 accumulate.
+    (1600, 1600, 4096) and (1000, 392, 8192) run split-K (3- and 8-way, the
+    second with M/N tails): partial sums meet in the TMA reduce-add."""
     torch.manual_seed(2)
     dy, x = _bf(T, O), _bf(T, I)
     dw = torch.randn(O, I, device="cuda")
@@ -83,6 +85,57 @@ def test_gemm_epilogues(ops):
     x = p.float().requires_grad_(True)
     torch.nn.functional.gelu(x, approximate="tanh").backward(acc)
     assert _rel(dg, x.grad) < 1e-2
+
+
+@pytest.mark.parametrize("bn,cg", [(128, 1), (256, 1), (128, 2), (256, 2)])
+def test_gemm_every_tile_config(ops, bn, cg):
+    """Each forced tile configuration (128/256-wide tiles, single CTA or CTA
+    pair with cta_group::2 MMAs) on every operand layout and epilogue, with M,
+    N and K tails, against fp32 torch."""
+    torch.manual_seed(7)
+    try:
+        for split in (0, 3):
+            ops.gemm_set_tile(bn, cg, split)
+            for M, N, K in ((200, 136, 192), (640, 1600, 320), (1280, 512, 1024)):
+                a, b = _bf(M, K), _bf(N, K)
+                d = torch.empty(M, N, device="cuda")
+                ops.gemm(a, b, d, epi="f32")
+                assert _rel(d, a.float() @ b.float().t()) < 1e-5, (M, N, K)
+                bt = b.t().contiguous()           # B MN-major [K, N]
+                ops.gemm(a, bt, d, b_mn=True, epi="f32")
+                assert _rel(d, a.float() @ b.float().t()) < 1e-5, (M, N, K)
+                at = a.t().contiguous()           # A MN-major [K, M]
+                acc = torch.randn(M, N, device="cuda")
+                ref = acc + a.float() @ b.float().t()
+                ops.gemm(at, bt, acc, a_mn=True, b_mn=True, epi="acc_f32")
+                assert _rel(acc, ref) < 1e-5, (M, N, K)
+            M, N, K = 384, 1600, 512
+            a, b = _bf(M, K), _bf(N, K, scale=0.05)
+            bias = torch.randn(N, device="cuda")
+            pre = a.float() @ b.float().t() + bias
+            r = torch.randn(M, N, device="cuda")
+            d32 = torch.empty(M, N, device="cuda")
+            ops.gemm(a, b, d32, epi="resid_f32", bias=bias, aux=r)
+            assert _rel(d32, r + pre) < 1e-5
+            p = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+            g = torch.empty_like(p)
+            ops.gemm(a, b, g, epi="gelu_bf16", bias=bias, aux=p)
+            assert _rel(p, pre) < 1e-2
+            assert _rel(g, torch.nn.functional.gelu(pre, approximate="tanh")) < 1e-2
+            dg = torch.empty_like(p)
+            ops.gemm(a, b, dg, epi="dgelu_bf16", aux=p)
+            x = p.float().requires_grad_(True)
+            torch.nn.functional.gelu(x, approximate="tanh").backward(pre - bias)
+            assert _rel(dg, x.grad) < 1e-2
+    finally:
+        ops.gemm_set_tile(0, 0, 0)
+
+
+def test_gemm_tile_choice():
+    from paper_2202_01306_b200 import ops as O
+    bn, cg, sp = O.gemm_tile(1600, 1600, 4096, "acc_f32")
+    assert sp > 1  # 13 x 7 wide tiles cannot fill 148 SMs: the weight gradient splits K
+    assert O.gemm_tile(4096, 50304, 1600, "f32")[1] == 2  # big problems run on CTA pairs
 
 
 def test_adam_matches_torch(ops):

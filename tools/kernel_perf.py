@@ -27,6 +27,7 @@ def peaks():
 
 FLUSH = None
 GRAPH = False
+SWEEP = None  # list of (bn, cta_pair, splits) to force, None = automatic choice
 
 
 def flush():
@@ -105,15 +106,21 @@ def bench_gemm():
         if epi in ("gelu_bf16", "dgelu_bf16"):
             aux = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
         fn = lambda: ops.gemm(a, b, d, a_mn=amn, b_mn=bmn, epi=epi, bias=bias, aux=aux)  # noqa: E731
-        ms = time_graph(fn) if GRAPH else timeit(fn)
-        tf = 2 * M * N * K / ms / 1e9
         ref_ms = None
         if not amn and not bmn:
             rf = lambda: torch.matmul(a, b.t())  # noqa: E731
             ref_ms = time_graph(rf) if GRAPH else timeit(rf)
-        print(json.dumps({"kernel": "gemm", "timing": "graph50" if GRAPH else "single+flush", "shape": name, "M": M, "N": N, "K": K, "ms": round(ms, 4),
-                          "tflops": round(tf, 1), "frac": round(tf / tf_peak, 3), "peak": kind,
-                          "cublas_ms": None if ref_ms is None else round(ref_ms, 4)}), flush=True)
+        for cfg in (SWEEP or [None]):
+            if cfg:
+                ops.gemm_set_tile(*cfg)
+            ms = time_graph(fn) if GRAPH else timeit(fn)
+            tf = 2 * M * N * K / ms / 1e9
+            tile = ops.gemm_tile(M, N, K, epi)
+            ops.gemm_set_tile(0, 0, 0)
+            print(json.dumps({"kernel": "gemm", "timing": "graph50" if GRAPH else "single+flush", "shape": name,
+                              "M": M, "N": N, "K": K, "tile": {"bn": tile[0], "cta_pair": tile[1], "splits": tile[2]},
+                              "ms": round(ms, 4), "tflops": round(tf, 1), "frac": round(tf / tf_peak, 3),
+                              "peak": kind, "cublas_ms": None if ref_ms is None else round(ref_ms, 4)}), flush=True)
 
 
 def bench_adam():
@@ -168,6 +175,9 @@ if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
     if what == "gemm_graph":
         GRAPH = True
+        what = "gemm"
+    if what == "gemm_sweep":
+        SWEEP = [(bn, cg, 0) for cg in (1, 2) for bn in (128, 256)]
         what = "gemm"
     if what in ("attn", "all"):
         bench_attn()
