@@ -38,6 +38,8 @@ WORKLOADS = {
     # name: (preset, samples_per_gpu, u, layers_per_pack, alpha_gib, mode)
     "gpt2-xl-dp": ("gpt2-xl", 16, 4, 8, 32, "dp"),
     "tiny": ("tiny", 16, 4, 2, 4, "pp"),
+    # north-star target shape: W + Adam state (184 GB) > one GPU's HBM
+    "gpt-15b-dp": ("gpt-15b", 24, 4, 3, 170, "dp"),
 }
 
 
@@ -263,7 +265,7 @@ def run_native(args) -> None:
     graph = H.generate_task_graph(cfg, machine, prof)
     sim = H.simulate(graph, machine, prof)
     rt = HarmonyRuntime(spec, alpha_bytes=alpha_gib << 30, device=local)
-    rt.init_weights(0)
+    rt.init_weights(0, device="cuda" if spec.total_params() > 4_000_000_000 else None)
     if world > 1:
         import torch.distributed as dist
         obj = [HarmonyRuntime.nccl_unique_id() if rank == 0 else None]
@@ -336,7 +338,8 @@ def run_native(args) -> None:
     clk = clocks.summary()
     share = {k: round(v["ms"] / (prof_iter_ns / 1e6), 4) for k, v in kstats.items()}
     line = {
-        "metric": "samples/s (Harmony layer-pack training, GPT-2 XL)",
+        "metric": "samples/s (Harmony layer-pack training, GPT-2 XL)" if preset == "gpt2-xl"
+                  else f"samples/s (Harmony layer-pack training, {spec.name})",
         "value": round(value, 3),
         "unit": "samples/s",
         "n_gpus": world,

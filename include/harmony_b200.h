@@ -172,6 +172,9 @@ int hm_runtime_trace(const hm_runtime *rt, hm_item *out, int32_t cap);
  * [2] device bytes in use (peak), [3] H2D bytes, [4] D2H bytes, [5] P2P bytes,
  * [6] NCCL all-reduce bytes per GPU (ring volume 2(N-1)/N x |dW|). */
 int hm_runtime_counters(const hm_runtime *rt, int64_t *out, int32_t cap);
+/* Diagnostics: copy `bytes` at `offset` of the shared-pack activation store
+ * (which = 0) or the recompute work store (1) to host memory (synchronous). */
+int hm_runtime_debug_read(const hm_runtime *rt, int32_t which, int64_t offset, int64_t bytes, void *host);
 /* Harmony-DP: NCCL (dlopen'ed from nccl_path, NULL = default search) unique
  * id on one rank (128 bytes), then every rank joins the communicator.  With
  * nranks > 1, hm_runtime_load_plan inserts one all-reduce (sum) of each

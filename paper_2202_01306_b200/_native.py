@@ -94,6 +94,7 @@ def lib() -> C.CDLL:
         "hm_runtime_trace_count": (C.c_int32, [C.c_void_p]),
         "hm_runtime_trace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
         "hm_runtime_counters": (C.c_int, [C.c_void_p, P(C.c_int64), C.c_int32]),
+        "hm_runtime_debug_read": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.c_void_p]),
         "hm_runtime_free": (None, [C.c_void_p]),
         "hm_nccl_unique_id": (C.c_int, [C.c_char_p, C.c_void_p]),
         "hm_runtime_init_comm": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_int32, C.c_int32]),

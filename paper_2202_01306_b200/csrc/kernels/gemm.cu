@@ -574,6 +574,8 @@ static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMa
   attrs[1].val.clusterDim.x = CG;
   attrs[1].val.clusterDim.y = 1;
   attrs[1].val.clusterDim.z = 1;
+  static const bool pdl = !(getenv("HM_GEMM_PDL") && getenv("HM_GEMM_PDL")[0] == '0');
+  attrs[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attrs;
   cfg.numAttrs = CG > 1 ? 2 : 1;
   cudaError_t le = cudaLaunchKernelEx(&cfg, kern, ta, tb, td, tx, a);

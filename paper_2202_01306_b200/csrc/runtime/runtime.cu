@@ -656,7 +656,9 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
         all_heads[e.layer] = (int64_t)minibatch * rt.S * (e.layer == 0 ? 4 : d * 4);
 
   // ---- slot assignment (round robin in device order) -------------------------
-  const int NW = 3, NDW = 2, NK = 2, NST = 2;
+  static const int env_nw = getenv("HM_W_SLOTS") ? atoi(getenv("HM_W_SLOTS")) : 0;
+  static const int env_nk = getenv("HM_K_SLOTS") ? atoi(getenv("HM_K_SLOTS")) : 0;
+  const int NW = env_nw >= 3 ? env_nw : 3, NDW = 2, NK = env_nk >= 2 ? env_nk : 2, NST = 2;
   int wn = 0, dwn = 0, kn = 0, stn = 0, fcur = -1, bcur = -1;
   std::vector<int> w_owner(NW, -1), dw_owner(NDW, -1), k_owner(NK, -1), st_owner(NST, -1);
   int64_t stash_in_max = 0;
@@ -787,7 +789,11 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
     *r.ptr = rt.pool + off;
     off += align_up(r.bytes, 1024);
   }
+  // cudaMemset runs on the legacy default stream, which does NOT order against
+  // the runtime's non-blocking streams: finish it before anything else can
+  // touch the pool (otherwise the first iteration's swap-ins race the zeroing)
   HM_CUDA(cudaMemset(rt.pool, 0, total));
+  HM_CUDA(cudaDeviceSynchronize());
   rt.out_off.clear();
   for (auto &ob : out_bufs) rt.out_off[ob.first] = reinterpret_cast<uint8_t *>(*ob.second) - rt.pool;
   rt.sig_off = reinterpret_cast<uint8_t *>(rt.sig) - rt.pool;
@@ -1059,7 +1065,14 @@ static int enqueue_body(hm_runtime &rt, bool capture, bool pipelined, int64_t &h
     HM_CUDA(cudaEventRecord(rt.ev_fork, sc));
     for (cudaStream_t o : others) HM_CUDA(cudaStreamWaitEvent(o, rt.ev_fork, 0));
   }
-  for (Action &a : rt.actions) {
+  static const bool serialize = getenv("HM_SERIALIZE") && getenv("HM_SERIALIZE")[0] == '1';
+  for (Action &a0 : rt.actions) {
+    Action tmp;
+    if (serialize) {  // diagnostics: every action on the compute stream, in plan order
+      tmp = a0;
+      tmp.stream = sc;
+    }
+    Action &a = serialize ? tmp : a0;
     // waits on the previous iteration: dropped inside a capture (iterations are
     // serialised around graph launches) and when that event's last record
     // happened inside a graph capture (the previous iteration has completed)
@@ -1433,6 +1446,15 @@ int hm_runtime_counters(const hm_runtime *rt, int64_t *out, int32_t cap) {
   const int n = cap < 8 ? cap : 8;
   for (int i = 0; i < n; ++i) out[i] = rt->counters[i];
   return n;
+}
+
+int hm_runtime_debug_read(const hm_runtime *rt, int32_t which, int64_t offset, int64_t bytes, void *host) {
+  if (!rt || !host || offset < 0 || bytes < 0) return hm::fail(HM_ERR_VALIDATION, "debug_read: bad arguments");
+  const uint8_t *base = which == 0 ? rt->shared_store : which == 1 ? rt->work_store : nullptr;
+  if (!base) return hm::fail(HM_ERR_VALIDATION, "debug_read: which = 0 (shared store) | 1 (work store)");
+  HM_CUDA(cudaDeviceSynchronize());
+  HM_CUDA(cudaMemcpy(host, base + offset, bytes, cudaMemcpyDeviceToHost));
+  return HM_OK;
 }
 
 int hm_nccl_unique_id(const char *nccl_path, uint8_t *out) {

@@ -129,6 +129,9 @@ GPT_PRESETS = {
     "gpt2-xl": GPTSpec(48, 1600, 25, 1024, 50257, True, "gpt2-xl"),
     # c4: GPT-style 40B
     "gpt-40b": GPTSpec(48, 8192, 64, 1024, 50257, True, "gpt-40b"),
+    # c4's layer shape at the largest depth one box's host RAM (197 GiB) can pin:
+    # 15.3 B params, W + Adam state = 184 GB > 180 GB HBM (W + dW + K = 245 GB)
+    "gpt-15b": GPTSpec(18, 8192, 64, 1024, 50257, True, "gpt-15b"),
 }
 
 

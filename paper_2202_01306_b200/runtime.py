@@ -71,10 +71,30 @@ class HarmonyRuntime:
             o += n
         return out
 
-    def init_weights(self, seed: int = 0) -> None:
+    def init_weights(self, seed: int = 0, device: str | None = None) -> None:
         """N(0, 0.02) matrices/embeddings, LayerNorm gamma=1 / beta=0, zero
-        biases, zero padded vocabulary rows; Adam state zero."""
+        biases, zero padded vocabulary rows; Adam state zero.
+        ``device="cuda"`` draws the normals on the GPU and copies them into the
+        pinned arena (seconds instead of minutes for a 15 B-parameter model;
+        a different random stream than the CPU generator)."""
         import torch
+        if device is not None:
+            gen = torch.Generator(device=device).manual_seed(seed)
+            V, d = self.spec.vocab, self.spec.d_model
+            for L in range(self.spec.n_layer):
+                for name, view in self.layer_params(L).items():
+                    if name.endswith("_g"):
+                        view[:] = 1.0
+                    elif name.startswith("b_") or name.endswith("_b"):
+                        view[:] = 0.0
+                    else:
+                        t = torch.empty(view.size, dtype=torch.float32, device=device).normal_(0.0, 0.02,
+                                                                                             generator=gen)
+                        if name in ("wte", "w_head"):
+                            t.view(-1, d)[V:] = 0.0
+                        torch.from_numpy(view).copy_(t)
+                        del t
+            return  # K is zeroed by hm_runtime_create
         gen = torch.Generator().manual_seed(seed)
         V, d = self.spec.vocab, self.spec.d_model
         for L in range(self.spec.n_layer):
@@ -190,6 +210,10 @@ class HarmonyRuntime:
             raise ValidationError("load() a plan first")
         loss = C.c_double(0.0)
         if hasattr(tokens, "is_cuda") and tokens.is_cuda:
+            # the runtime's streams are non-blocking: torch's pending work on
+            # the token buffers must be finished before they are read
+            import torch
+            torch.cuda.current_stream(tokens.device).synchronize()
             rc = self.lib.hm_runtime_run_iteration(self.handle, C.c_void_p(tokens.data_ptr()),
                                                    C.c_void_p(labels.data_ptr()), 1, C.byref(loss))
         else:
@@ -210,6 +234,8 @@ class HarmonyRuntime:
         losses = (C.c_double * n)()
         total = C.c_int64(0)
         if hasattr(tokens, "is_cuda") and tokens.is_cuda:
+            import torch
+            torch.cuda.current_stream(tokens.device).synchronize()
             rc = self.lib.hm_runtime_run_steps(self.handle, n, C.c_void_p(tokens.data_ptr()),
                                                C.c_void_p(labels.data_ptr()), 1, losses, C.byref(total))
         else:
