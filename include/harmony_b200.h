@@ -226,13 +226,32 @@ enum hm_gemm_epilogue {
   HM_EPI_ACC_F32 = 2,         /* D += acc (fp32, TMA reduce-add; split-K ok)  */
   HM_EPI_RESID_F32 = 3,       /* D = R + acc + bias -> fp32 (R may alias D)  */
   HM_EPI_GELU_BF16 = 4,       /* P = acc + bias (bf16), D = gelu(P) (bf16)   */
-  HM_EPI_DGELU_BF16 = 5       /* D = acc * gelu'(P) -> bf16                  */
+  HM_EPI_DGELU_BF16 = 5,      /* D = acc * gelu'(P) -> bf16                  */
+  HM_EPI_RELU_BF16 = 6,       /* D = relu(acc + bias) -> bf16                */
+  HM_EPI_RESID_RELU_BF16 = 7, /* D = relu(acc + bias + R), R bf16 -> bf16    */
+  HM_EPI_DRELU_BF16 = 8,      /* D = acc * (P > 0), P bf16 -> bf16           */
+  HM_EPI_ADD_BF16 = 9         /* D = acc + R, R bf16 -> bf16                 */
 };
 int hm_k_gemm(const void *a, const void *b, void *d, int64_t m, int64_t n, int64_t k,
               int64_t lda, int64_t ldb, int64_t ldd, int32_t a_major, int32_t b_major,
               int32_t epilogue, const float *bias, const void *aux, int64_t ld_aux,
               int32_t batch, int64_t stride_a, int64_t stride_b, int64_t stride_d,
               void *stream);
+
+/* 3x3 convolution, stride 1, zero padding 1, NHWC bf16 activations, weights
+ * W[Cout][3][3][Cin] bf16 (= [Cout, 9*Cin], K-major), as implicit GEMM on
+ * tcgen05: the activation operand is gathered by TMA im2col loads (one
+ * 64-channel slice of one filter tap per k-block), never materialised.
+ * Cin and Cout must be multiples of 64.
+ *   fwd:   y[N*H*W, Cout]  = im2col(x) . W^T            (epilogue: any bf16 one)
+ *   dgrad: dx[N*H*W, Cin]  = im2col(dy) . flip(W)       (epilogue: STORE/DRELU/ADD bf16)
+ *   wgrad: dw[Cout, 9*Cin] += dy^T . im2col(x)          (fp32 TMA reduce-add, split-K) */
+int hm_k_conv_fwd(const void *x, const void *w, void *y, int32_t n, int32_t h, int32_t wd, int32_t cin,
+                  int32_t cout, int32_t epilogue, const float *bias, const void *aux, void *stream);
+int hm_k_conv_dgrad(const void *dy, const void *w, void *dx, int32_t n, int32_t h, int32_t wd, int32_t cin,
+                    int32_t cout, int32_t epilogue, const void *aux, void *stream);
+int hm_k_conv_wgrad(const void *dy, const void *x, float *dw, int32_t n, int32_t h, int32_t wd, int32_t cin,
+                    int32_t cout, void *stream);
 
 /* Tile configuration the GEMM picks for an (m, n, k, epilogue) problem:
  * bn = output tile width (128 | 256), cta_pair = 1 (128-row tile on one SM) or

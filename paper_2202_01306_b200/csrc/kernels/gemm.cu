@@ -42,6 +42,9 @@ constexpr int kThreads = 128 + 32 * kEpiWarps;
 struct Args {
   int32_t M, N, K, num_m, num_n, num_k;
   int32_t splits;  // split-K factor (ACC_F32 only: partial sums meet in the TMA reduce-add)
+  // implicit-GEMM 3x3 convolution (MODE 1-3): image H x W of the im2col
+  // operand, its 64-channel blocks, and (dgrad) the output-channel blocks
+  int32_t cv_h, cv_w, cv_cb, cv_cbo;
   void *d;
   int64_t ldd;
   const float *bias;
@@ -105,12 +108,19 @@ __device__ __forceinline__ uint32_t sw64_off(int r, int j) { return r * 64 + ((j
 // (RESID_F32) and the pre-activation (DGELU_BF16).  ACC_F32 reads nothing: its
 // chunk leaves as a TMA reduce-add, which also makes split-K free of fix-ups.
 __device__ __forceinline__ bool epi_src_f32(int epi) { return epi == HM_EPI_RESID_F32; }
+__host__ __device__ __forceinline__ bool epi_src_bf16(int epi) {
+  return epi == HM_EPI_DGELU_BF16 || epi == HM_EPI_RESID_RELU_BF16 || epi == HM_EPI_DRELU_BF16 ||
+         epi == HM_EPI_ADD_BF16;
+}
+__host__ __device__ __forceinline__ bool epi_takes_bias(int epi) {
+  return epi != HM_EPI_ACC_F32 && epi != HM_EPI_DGELU_BF16 && epi != HM_EPI_DRELU_BF16 && epi != HM_EPI_ADD_BF16;
+}
 
 // Apply the epilogue to one row's 32 columns [col0, col0+32) held in v and
 // write the result(s) into the warp's staging buffer (row r = lane).
 __device__ __forceinline__ void epilogue_chunk(const Args &a, int col0, float (&v)[32], uint8_t *buf, int r) {
   const int N = a.N;
-  if (a.bias && a.epi != HM_EPI_ACC_F32 && a.epi != HM_EPI_DGELU_BF16) {
+  if (a.bias && epi_takes_bias(a.epi)) {
     if (col0 + 32 <= N) {
       const float4 *b4 = reinterpret_cast<const float4 *>(a.bias + col0);
 #pragma unroll
@@ -143,8 +153,36 @@ __device__ __forceinline__ void epilogue_chunk(const Args &a, int col0, float (&
     }
     case HM_EPI_STORE_BF16:
     case HM_EPI_GELU_BF16:
-    case HM_EPI_DGELU_BF16: {
+    case HM_EPI_DGELU_BF16:
+    case HM_EPI_RELU_BF16:
+    case HM_EPI_RESID_RELU_BF16:
+    case HM_EPI_DRELU_BF16:
+    case HM_EPI_ADD_BF16: {
       uint8_t *out = buf;
+      if (a.epi == HM_EPI_RESID_RELU_BF16 || a.epi == HM_EPI_DRELU_BF16 || a.epi == HM_EPI_ADD_BF16) {
+        // bf16 source chunk (residual or post-activation) landed in buf
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint4 p = *reinterpret_cast<const uint4 *>(buf + sw64_off(r, j));
+          const __nv_bfloat162 *p2 = reinterpret_cast<const __nv_bfloat162 *>(&p);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(p2[e]);
+            float &v0 = v[8 * j + 2 * e], &v1 = v[8 * j + 2 * e + 1];
+            if (a.epi == HM_EPI_DRELU_BF16) {
+              v0 = f.x > 0.f ? v0 : 0.f;
+              v1 = f.y > 0.f ? v1 : 0.f;
+            } else {
+              v0 += f.x;
+              v1 += f.y;
+            }
+          }
+        }
+      }
+      if (a.epi == HM_EPI_RELU_BF16 || a.epi == HM_EPI_RESID_RELU_BF16) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = fmaxf(v[j], 0.f);
+      }
       if (a.epi == HM_EPI_DGELU_BF16) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -186,7 +224,12 @@ __device__ __forceinline__ void epilogue_chunk(const Args &a, int col0, float (&
   }
 }
 
-template <int BN, int A_MN, int B_MN, int CG>
+// MODE: 0 plain GEMM (2-D tensor maps)
+//       1 conv fwd   A = im2col(x): one k-block = 64 channels of one filter tap
+//       2 conv dgrad A = im2col(dy), B = W[Cout][9][Cin] through a 3-D map with
+//                    the tap flipped (dx = correlation of dy with the rotated W)
+//       3 conv wgrad B = im2col(x) in 64-pixel x 64-channel MN-major chunks
+template <int BN, int A_MN, int B_MN, int CG, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX, Args args) {
@@ -268,13 +311,44 @@ __global__ void __launch_bounds__(kThreads, 1)
             else
               tma_load_2d(dst, m, &full[stage], c0, c1);
           };
-          if (!A_MN) {
+          // im2col gather of 64 channels [c0, c0+64) of filter tap `tap` for the
+          // pixels starting at flat NHW index p (base pixel = p - (1, 1))
+          auto load_im2col = [&](uint8_t *dst, const CUtensorMap *m, int c0, int tap, int p) {
+            const int hw = args.cv_h * args.cv_w;
+            const int n = p / hw, rem = p - n * hw, h = rem / args.cv_w, w = rem - h * args.cv_w;
+            const uint16_t r = (uint16_t)(tap / 3), s = (uint16_t)(tap - 3 * (tap / 3));
+            if (CG == 2)
+              tma_load_im2col_pair(dst, m, bar_addr, c0, w - 1, h - 1, n, s, r);
+            else
+              tma_load_im2col(dst, m, &full[stage], c0, w - 1, h - 1, n, s, r);
+          };
+          if (MODE == 1 || MODE == 2) {
+            const int tap = kb / args.cv_cb;
+            load_im2col(a_dst, &tmA, (kb - tap * args.cv_cb) * 64, tap, m0);
+          } else if (!A_MN) {
             load(a_dst, &tmA, kb * BK, m0);
           } else {
 #pragma unroll
             for (int c = 0; c < BM / 64; ++c) load(a_dst + c * (BK * 128), &tmA, m0 + c * 64, kb * BK);
           }
-          if (!B_MN) {
+          if (MODE == 2) {
+            // K = (tap', co): 64 output channels of tap' against the flipped tap
+            const int tap = kb / args.cv_cbo, co0 = (kb - tap * args.cv_cbo) * 64;
+#pragma unroll
+            for (int c = 0; c < C::kBRows / 64; ++c) {
+              if (CG == 2)
+                tma_load_3d_pair(b_dst + c * (BK * 128), &tmB, bar_addr, n0 + c * 64, 8 - tap, co0);
+              else
+                tma_load_3d(b_dst + c * (BK * 128), &tmB, &full[stage], n0 + c * 64, 8 - tap, co0);
+            }
+          } else if (MODE == 3) {
+            // N = (tap, ci): each 64-column chunk is one tap's 64-channel block
+#pragma unroll
+            for (int c = 0; c < C::kBRows / 64; ++c) {
+              const int nbk = (n0 >> 6) + c, tap = nbk / args.cv_cb;
+              load_im2col(b_dst + c * (BK * 128), &tmB, (nbk - tap * args.cv_cb) * 64, tap, kb * BK);
+            }
+          } else if (!B_MN) {
             load(b_dst, &tmB, kb * BK, n0);
           } else {
 #pragma unroll
@@ -345,7 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t bphase = 0;
     const int epi = args.epi;
     const bool src_f32 = epi_src_f32(epi);
-    const bool has_src = src_f32 || epi == HM_EPI_DGELU_BF16;
+    const bool has_src = src_f32 || epi_src_bf16(epi);
     const CUtensorMap *tsrc = &tmX;
     griddep_wait();  // epilogue reads / writes global memory of the previous kernel's outputs
     int local = 0;
@@ -546,12 +620,12 @@ static int num_sms() {
   return n;
 }
 
-template <int BN, int A_MN, int B_MN, int CG>
+template <int BN, int A_MN, int B_MN, int CG, int MODE = 0>
 static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &td, const CUtensorMap &tx,
                   const Args &a, cudaStream_t s) {
   using C = Cfg<BN, CG>;
   static bool attr = false;
-  auto kern = gemm_kernel<BN, A_MN, B_MN, CG>;
+  auto kern = gemm_kernel<BN, A_MN, B_MN, CG, MODE>;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
     if (e != cudaSuccess) return fail(HM_ERR_DEVICE, std::string("gemm smem attr: ") + cudaGetErrorString(e));
@@ -590,12 +664,13 @@ int run(const void *A, const void *B, void *D, int64_t M, int64_t N, int64_t K, 
         int64_t ldd, int a_mn, int b_mn, int epi, const float *bias, void *aux, int64_t ld_aux,
         cudaStream_t stream, int force_bn) {
   if (M <= 0 || N <= 0 || K <= 0) return fail(HM_ERR_VALIDATION, "gemm: empty problem");
+  if (epi < HM_EPI_STORE_BF16 || epi > HM_EPI_ADD_BF16) return fail(HM_ERR_VALIDATION, "gemm: unknown epilogue");
   if ((lda * 2) % 16 || (ldb * 2) % 16) return fail(HM_ERR_VALIDATION, "gemm: operand pitch must be 16B aligned");
   if (((uintptr_t)A | (uintptr_t)B) & 15) return fail(HM_ERR_VALIDATION, "gemm: operands must be 16B aligned");
   const bool f32out = epi == HM_EPI_STORE_F32 || epi == HM_EPI_ACC_F32 || epi == HM_EPI_RESID_F32;
   if ((ldd * (f32out ? 4 : 2)) % 16 || ((uintptr_t)D & 15))
     return fail(HM_ERR_VALIDATION, "gemm: output must be 16B aligned with 16B pitch");
-  if ((epi == HM_EPI_RESID_F32 || epi == HM_EPI_GELU_BF16 || epi == HM_EPI_DGELU_BF16) && !aux)
+  if ((epi == HM_EPI_RESID_F32 || epi == HM_EPI_GELU_BF16 || epi_src_bf16(epi)) && !aux)
     return fail(HM_ERR_VALIDATION, "gemm: epilogue needs an aux tensor");
   if (aux && ((ld_aux * (epi == HM_EPI_RESID_F32 ? 4 : 2)) % 16 || ((uintptr_t)aux & 15)))
     return fail(HM_ERR_VALIDATION, "gemm: aux must be 16B aligned with 16B pitch");
@@ -644,8 +719,147 @@ int run(const void *A, const void *B, void *D, int64_t M, int64_t N, int64_t K, 
   }
 }
 
+// ---- implicit-GEMM 3x3 convolution -------------------------------------------------
+// im2col map over an NHWC bf16 activation [n, h, w, c]: base pixels range over
+// [-1, dim-1) in W and H (zero padding 1, output size = input size), one
+// 64-channel slice per request, `pixels` (128 or 64) pixels per request.
+static int make_im2col_map(CUtensorMap *out, const void *ptr, int n, int h, int w, int c, uint32_t pixels) {
+  using Key = std::tuple<const void *, int, int, int, int, uint32_t>;
+  static std::mutex mu;
+  static std::map<Key, CUtensorMap> cache;
+  Key key{ptr, n, h, w, c, pixels};
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *out = it->second;
+      return HM_OK;
+    }
+  }
+  using Im2colFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                const cuuint64_t *, const int *, const int *, cuuint32_t, cuuint32_t,
+                                const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Im2colFn fn = [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      return reinterpret_cast<Im2colFn>(p);
+    return (Im2colFn) nullptr;
+  }();
+  if (!fn) return fail(HM_ERR_DEVICE, "cuTensorMapEncodeIm2col unavailable");
+  cuuint64_t dims[4] = {(cuuint64_t)c, (cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+  cuuint64_t strides[3] = {(cuuint64_t)c * 2, (cuuint64_t)w * c * 2, (cuuint64_t)h * w * c * 2};
+  int lower[2] = {-1, -1}, upper[2] = {-1, -1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(ptr), dims, strides, lower, upper, 64,
+                  pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(HM_ERR_DEVICE, "cuTensorMapEncodeIm2col failed (" + std::to_string((int)r) + ")");
+  std::lock_guard<std::mutex> g(mu);
+  if (cache.size() > 1024) cache.clear();
+  cache[key] = *out;
+  return HM_OK;
+}
+
+// W[cout][9][cin] bf16 as a 3-D map {cin, 9, cout}, box {64, 1, 64}: one tap's
+// 64 x 64 (cout x cin) block, cin contiguous (an MN-major B chunk for dgrad).
+static int make_filter_map(CUtensorMap *out, const void *ptr, int cin, int cout) {
+  EncodeFn fn = encode_fn();
+  if (!fn) return fail(HM_ERR_DEVICE, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)cin, 9, (cuuint64_t)cout};
+  cuuint64_t strides[2] = {(cuuint64_t)cin * 2, (cuuint64_t)cin * 9 * 2};
+  cuuint32_t box[3] = {64, 1, 64};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(ptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(HM_ERR_DEVICE, "filter tensor map failed (" + std::to_string((int)r) + ")");
+  return HM_OK;
+}
+
+template <int MODE, int A_MN, int B_MN>
+static int launch_conv(const TileCfg &tc, const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &td,
+                       const CUtensorMap &tx, const Args &a, cudaStream_t s) {
+  const int key = (tc.cg == 2 ? 2 : 0) | (tc.bn == 256 ? 1 : 0);
+  switch (key) {
+    case 0: return launch<128, A_MN, B_MN, 1, MODE>(ta, tb, td, tx, a, s);
+    case 1: return launch<256, A_MN, B_MN, 1, MODE>(ta, tb, td, tx, a, s);
+    case 2: return launch<128, A_MN, B_MN, 2, MODE>(ta, tb, td, tx, a, s);
+    default: return launch<256, A_MN, B_MN, 2, MODE>(ta, tb, td, tx, a, s);
+  }
+}
+
+// mode 1 fwd, 2 dgrad, 3 wgrad (see the kernel's MODE comment)
+int run_conv(int mode, const void *act, const void *wt, void *out, int n, int h, int w, int cin, int cout, int epi,
+             const float *bias, const void *aux, cudaStream_t stream) {
+  if (n <= 0 || h <= 0 || w <= 0 || cin <= 0 || cout <= 0) return fail(HM_ERR_VALIDATION, "conv: empty problem");
+  if (cin % 64 || cout % 64) return fail(HM_ERR_VALIDATION, "conv: channels must be multiples of 64");
+  if (((uintptr_t)act | (uintptr_t)wt | (uintptr_t)out | (uintptr_t)aux) & 15)
+    return fail(HM_ERR_VALIDATION, "conv: tensors must be 16B aligned");
+  const int64_t P = (int64_t)n * h * w;
+  if (P >= (int64_t)1 << 31) return fail(HM_ERR_VALIDATION, "conv: too many pixels");
+  int64_t M, N, K;
+  if (mode == 1) { M = P; N = cout; K = 9LL * cin; }
+  else if (mode == 2) { M = P; N = cin; K = 9LL * cout; }
+  else { M = cout; N = 9LL * cin; K = P; epi = HM_EPI_ACC_F32; }
+  if (mode != 3 && (epi == HM_EPI_STORE_F32 || epi == HM_EPI_ACC_F32 || epi == HM_EPI_RESID_F32 ||
+                    epi == HM_EPI_GELU_BF16))
+    return fail(HM_ERR_VALIDATION, "conv: fwd/dgrad epilogues are the bf16 ones");
+  if (epi_src_bf16(epi) && !aux) return fail(HM_ERR_VALIDATION, "conv: epilogue needs an aux tensor");
+  TileCfg tc = pick_tile(M, N, K, epi);
+  Args a{};
+  a.M = (int)M; a.N = (int)N; a.K = (int)K;
+  a.num_m = (int)((M + BM * tc.cg - 1) / (BM * tc.cg));
+  a.num_n = (int)((N + tc.bn - 1) / tc.bn);
+  a.num_k = (int)((K + BK - 1) / BK);
+  a.splits = tc.splits;
+  a.d = out; a.ldd = N; a.bias = bias; a.aux = const_cast<void *>(aux); a.ld_aux = N; a.epi = epi;
+  a.cv_h = h; a.cv_w = w; a.cv_cb = (mode == 2 ? cout : cin) / 64; a.cv_cbo = cout / 64;
+  const bool f32out = mode == 3;
+  CUtensorMap ta, tb, td, tx;
+  int rc;
+  if (mode == 1 || mode == 2) {
+    rc = make_im2col_map(&ta, act, n, h, w, mode == 1 ? cin : cout, BM);
+    if (rc) return rc;
+    rc = mode == 1 ? make_map(&tb, wt, 9ULL * cin, cout, 9ULL * cin * 2, tc.bn / tc.cg) : make_filter_map(&tb, wt, cin, cout);
+  } else {
+    rc = make_map(&ta, act, cout, P, (uint64_t)cout * 2, 64);  // dy [P, cout] read MN-major
+    if (rc) return rc;
+    rc = make_im2col_map(&tb, wt, n, h, w, cin, BK);  // here `wt` is the activation x
+  }
+  if (rc) return rc;
+  rc = make_map(&td, out, N, M, N * (f32out ? 4 : 2), 32, f32out, 32);
+  if (rc) return rc;
+  if (aux) {
+    rc = make_map(&tx, aux, N, M, N * 2, 32, false, 32);
+    if (rc) return rc;
+  } else {
+    tx = td;
+  }
+  if (mode == 1) return launch_conv<1, 0, 0>(tc, ta, tb, td, tx, a, stream);
+  if (mode == 2) return launch_conv<2, 0, 1>(tc, ta, tb, td, tx, a, stream);
+  return launch_conv<3, 1, 1>(tc, ta, tb, td, tx, a, stream);
+}
+
 }  // namespace gemm
 }  // namespace hm
+
+extern "C" int hm_k_conv_fwd(const void *x, const void *w, void *y, int32_t n, int32_t h, int32_t wd, int32_t cin,
+                             int32_t cout, int32_t epilogue, const float *bias, const void *aux, void *stream) {
+  return hm::gemm::run_conv(1, x, w, y, n, h, wd, cin, cout, epilogue, bias, aux, static_cast<cudaStream_t>(stream));
+}
+extern "C" int hm_k_conv_dgrad(const void *dy, const void *w, void *dx, int32_t n, int32_t h, int32_t wd, int32_t cin,
+                               int32_t cout, int32_t epilogue, const void *aux, void *stream) {
+  return hm::gemm::run_conv(2, dy, w, dx, n, h, wd, cin, cout, epilogue, nullptr, aux,
+                            static_cast<cudaStream_t>(stream));
+}
+extern "C" int hm_k_conv_wgrad(const void *dy, const void *x, float *dw, int32_t n, int32_t h, int32_t wd, int32_t cin,
+                               int32_t cout, void *stream) {
+  return hm::gemm::run_conv(3, dy, x, dw, n, h, wd, cin, cout, HM_EPI_ACC_F32, nullptr, nullptr,
+                            static_cast<cudaStream_t>(stream));
+}
 
 extern "C" int hm_k_gemm_set_tile(int32_t bn, int32_t cta_pair, int32_t splits) {
   if ((bn && bn != 128 && bn != 256) || (cta_pair && cta_pair != 1 && cta_pair != 2) || splits < 0 || splits > 8)

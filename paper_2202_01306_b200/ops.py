@@ -12,7 +12,8 @@ import torch
 
 from . import _native as NL
 
-EPI = {"bf16": 0, "f32": 1, "acc_f32": 2, "resid_f32": 3, "gelu_bf16": 4, "dgelu_bf16": 5}
+EPI = {"bf16": 0, "f32": 1, "acc_f32": 2, "resid_f32": 3, "gelu_bf16": 4, "dgelu_bf16": 5,
+       "relu_bf16": 6, "resid_relu_bf16": 7, "drelu_bf16": 8, "add_bf16": 9}
 
 
 def _ptr(t):
@@ -42,6 +43,32 @@ def gemm(a, b, d, *, a_mn=False, b_mn=False, epi="f32", bias=None, aux=None):
                        aux.stride(0) if aux is not None else 0, 1, 0, 0, 0, _stream())
     NL.check(rc)
     return d
+
+
+def conv_fwd(x, w, y, *, epi="bf16", bias=None, aux=None):
+    """y[n,h,w,cout] = conv3x3(x[n,h,w,cin], w[cout,3,3,cin]) (+epilogue), NHWC bf16."""
+    n, h, wd, cin = x.shape
+    cout = w.shape[0]
+    NL.check(N_lib().hm_k_conv_fwd(_ptr(x), _ptr(w), _ptr(y), n, h, wd, cin, cout, EPI[epi], _ptr(bias), _ptr(aux),
+                                   _stream()))
+    return y
+
+
+def conv_dgrad(dy, w, dx, *, epi="bf16", aux=None):
+    """dx[n,h,w,cin] = grad of conv3x3 w.r.t. its input, from dy[n,h,w,cout]."""
+    n, h, wd, cout = dy.shape
+    cin = w.shape[-1]
+    NL.check(N_lib().hm_k_conv_dgrad(_ptr(dy), _ptr(w), _ptr(dx), n, h, wd, cin, cout, EPI[epi], _ptr(aux),
+                                     _stream()))
+    return dx
+
+
+def conv_wgrad(dy, x, dw):
+    """dw[cout,3,3,cin] (fp32) += grad of conv3x3 w.r.t. its weights."""
+    n, h, wd, cin = x.shape
+    cout = dy.shape[-1]
+    NL.check(N_lib().hm_k_conv_wgrad(_ptr(dy), _ptr(x), _ptr(dw), n, h, wd, cin, cout, _stream()))
+    return dw
 
 
 def gemm_tile(M, N, K, epi="f32"):

@@ -300,3 +300,51 @@ def test_attention_bwd_tcgen05_opt_in():
     env = dict(__import__("os").environ, HM_ATTN_BWD="tc")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
+
+
+def _conv_ref(x, w):
+    import torch.nn.functional as F
+    return F.conv2d(x.float().permute(0, 3, 1, 2), w.float().permute(0, 3, 1, 2), padding=1).permute(0, 2, 3, 1)
+
+
+@pytest.mark.parametrize("n,h,wd,cin,cout", [(2, 8, 8, 64, 64), (3, 14, 10, 128, 64), (1, 32, 32, 64, 256),
+                                            (2, 7, 9, 192, 128)])
+@pytest.mark.parametrize("cfg", [(0, 0), (128, 1), (256, 2)])
+def test_conv3x3_implicit_gemm(ops, n, h, wd, cin, cout, cfg):
+    """Implicit-GEMM 3x3 conv (TMA im2col operands) fwd / dgrad / wgrad and the
+    ReLU / residual epilogues vs torch fp32, on odd image sizes (pixel tiles
+    straddle rows and images) and every tile configuration."""
+    import torch.nn.functional as F
+    torch.manual_seed(11)
+    x = _bf(n, h, wd, cin)
+    w = _bf(cout, 3, 3, cin, scale=0.05)
+    bias = torch.randn(cout, device="cuda") * 0.1
+    try:
+        ops.gemm_set_tile(cfg[0], cfg[1], 0)
+        ref = _conv_ref(x, w)
+        y = torch.empty(n, h, wd, cout, device="cuda", dtype=torch.bfloat16)
+        ops.conv_fwd(x, w, y)
+        assert _rel(y, ref) < 1e-2
+        ops.conv_fwd(x, w, y, epi="relu_bf16", bias=bias)
+        assert _rel(y, torch.relu(ref + bias)) < 1e-2
+        r = _bf(n, h, wd, cout)
+        ops.conv_fwd(x, w, y, epi="resid_relu_bf16", bias=bias, aux=r)
+        assert _rel(y, torch.relu(ref + bias + r.float())) < 1e-2
+        dy = _bf(n, h, wd, cout)
+        xr = x.float().permute(0, 3, 1, 2).requires_grad_(True)
+        wr = w.float().permute(0, 3, 1, 2).requires_grad_(True)
+        F.conv2d(xr, wr, padding=1).backward(dy.float().permute(0, 3, 1, 2))
+        dx_ref = xr.grad.permute(0, 2, 3, 1)
+        dx = torch.empty_like(x)
+        ops.conv_dgrad(dy, w, dx)
+        assert _rel(dx, dx_ref) < 1e-2
+        ops.conv_dgrad(dy, w, dx, epi="drelu_bf16", aux=x)
+        assert _rel(dx, dx_ref * (x.float() > 0)) < 1e-2
+        ops.conv_dgrad(dy, w, dx, epi="add_bf16", aux=x)
+        assert _rel(dx, dx_ref + x.float()) < 1e-2
+        dw = torch.randn(cout, 3, 3, cin, device="cuda")
+        dw_ref = dw + wr.grad.permute(0, 2, 3, 1)
+        ops.conv_wgrad(dy, x, dw)
+        assert _rel(dw, dw_ref) < 1e-4
+    finally:
+        ops.gemm_set_tile(0, 0, 0)
