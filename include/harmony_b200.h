@@ -142,11 +142,31 @@ typedef struct {
 
 typedef struct hm_runtime hm_runtime;
 
+/* Deep-CNN layer chain (BASELINE config c5, VGG / ResNet-style packs).  Each
+ * chain layer is one of: 0 conv (3x3 conv + bias + ReLU), 1 down (conv + ReLU,
+ * then 2x2 average pool), 2 res (basic residual block relu(x + conv(relu(conv
+ * x)))), 3 head (global average pool + fully connected + cross-entropy).
+ * h, w, cin = the layer's input; activations NHWC bf16; channels % 64 == 0
+ * (the image enters layer 0 zero-padded to 64 channels); one label per sample. */
+enum { HM_FAMILY_GPT = 0, HM_FAMILY_CNN = 1 };
+enum { HM_CNN_CONV = 0, HM_CNN_DOWN = 1, HM_CNN_RES = 2, HM_CNN_HEAD = 3 };
+typedef struct {
+  int32_t type, cin, cout, h, w;
+} hm_cnn_layer;
+typedef struct {
+  int32_t n_layer;
+  const hm_cnn_layer *layers;
+  int32_t classes, classes_padded;
+  double lr, beta1, beta2, eps;
+} hm_cnn_model;
+
 enum hm_arena { HM_ARENA_W = 0, HM_ARENA_K = 1, HM_ARENA_STASH = 2 };
 
 hm_runtime *hm_runtime_create(int32_t device, const hm_model *model, int64_t alpha_bytes,
                               int32_t *status);
 /* Pinned host arena owned by the runtime; returns its host pointer. */
+hm_runtime *hm_runtime_create_cnn(int32_t device, const hm_cnn_model *model, int64_t alpha_bytes,
+                                  int32_t *status);
 void *hm_runtime_arena(hm_runtime *rt, int32_t kind, int64_t *bytes);
 /* Per-layer parameter offsets (in floats) of the W arena; K uses 2x. */
 int hm_runtime_layer_offsets(const hm_runtime *rt, int64_t *w_off, int32_t cap);
@@ -252,6 +272,16 @@ int hm_k_conv_dgrad(const void *dy, const void *w, void *dx, int32_t n, int32_t 
                     int32_t cout, int32_t epilogue, const void *aux, void *stream);
 int hm_k_conv_wgrad(const void *dy, const void *x, float *dw, int32_t n, int32_t h, int32_t wd, int32_t cin,
                     int32_t cout, void *stream);
+
+/* Deep-CNN layer pieces (NHWC bf16): dz = dy * (y > 0); 2x2 average pool
+ * and its backward fused with the producing conv's ReLU mask; global average
+ * pool [nb, P, c] -> [nb, c] and its backward (fp32 gradient in). */
+int hm_k_relu_bwd(const void *dy, const void *y, void *dz, int64_t n, void *stream);
+int hm_k_pool2_fwd(const void *a, void *y, int32_t n, int32_t h, int32_t w, int32_t c, void *stream);
+int hm_k_pool2_relu_bwd(const void *dy, const void *a, void *dz, int32_t n, int32_t h, int32_t w, int32_t c,
+                        void *stream);
+int hm_k_gap_fwd(const void *x, void *pooled, int32_t nb, int32_t P, int32_t c, void *stream);
+int hm_k_gap_bwd(const float *dp, void *dx, int32_t nb, int32_t P, int32_t c, void *stream);
 
 /* Tile configuration the GEMM picks for an (m, n, k, epilogue) problem:
  * bn = output tile width (128 | 256), cta_pair = 1 (128-row tile on one SM) or

@@ -56,6 +56,15 @@ class hm_model(C.Structure):
         "math_mode")] + [(n, C.c_double) for n in ("lr", "beta1", "beta2", "eps")]
 
 
+class hm_cnn_layer(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("type", "cin", "cout", "h", "w")]
+
+
+class hm_cnn_model(C.Structure):
+    _fields_ = [("n_layer", C.c_int32), ("layers", C.POINTER(hm_cnn_layer)), ("classes", C.c_int32),
+                ("classes_padded", C.c_int32)] + [(n, C.c_double) for n in ("lr", "beta1", "beta2", "eps")]
+
+
 _lib = None
 
 
@@ -94,6 +103,12 @@ def lib() -> C.CDLL:
         "hm_runtime_trace_count": (C.c_int32, [C.c_void_p]),
         "hm_runtime_trace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
         "hm_runtime_counters": (C.c_int, [C.c_void_p, P(C.c_int64), C.c_int32]),
+        "hm_runtime_create_cnn": (C.c_void_p, [C.c_int32, P(hm_cnn_model), C.c_int64, P(C.c_int32)]),
+        "hm_k_relu_bwd": (C.c_int, [C.c_void_p] * 3 + [C.c_int64, C.c_void_p]),
+        "hm_k_pool2_fwd": (C.c_int, [C.c_void_p] * 2 + [C.c_int32] * 4 + [C.c_void_p]),
+        "hm_k_pool2_relu_bwd": (C.c_int, [C.c_void_p] * 3 + [C.c_int32] * 4 + [C.c_void_p]),
+        "hm_k_gap_fwd": (C.c_int, [C.c_void_p] * 2 + [C.c_int32] * 3 + [C.c_void_p]),
+        "hm_k_gap_bwd": (C.c_int, [C.c_void_p] * 2 + [C.c_int32] * 3 + [C.c_void_p]),
         "hm_runtime_debug_read": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.c_void_p]),
         "hm_runtime_free": (None, [C.c_void_p]),
         "hm_nccl_unique_id": (C.c_int, [C.c_char_p, C.c_void_p]),

@@ -31,4 +31,15 @@ int cross_entropy(const float *logits, const int32_t *labels, int64_t rows, int6
                   double *loss_sum, float scale, cudaStream_t s);
 int bias_grad(const void *dy, int is_bf16, float *db, int64_t rows, int n, int64_t ld, cudaStream_t s);
 }  // namespace layers
+namespace gemm {
+int run_conv(int mode, const void *act, const void *wt, void *out, int n, int h, int w, int cin, int cout, int epi,
+             const float *bias, const void *aux, cudaStream_t stream);
+}
+namespace cnn {
+int relu_bwd(const void *dy, const void *y, void *dz, int64_t n, cudaStream_t s);
+int pool2_fwd(const void *a, void *y, int n, int h, int w, int c, cudaStream_t s);
+int pool2_relu_bwd(const void *dy, const void *a, void *dz, int n, int h, int w, int c, cudaStream_t s);
+int gap_fwd(const void *x, void *pooled, int nb, int P, int c, cudaStream_t s);
+int gap_bwd(const float *dp, void *dx, int nb, int P, int c, cudaStream_t s);
+}  // namespace cnn
 }  // namespace hm

@@ -60,6 +60,17 @@ struct Scratch {
   float *dln, *dh1, *dvec, *dq, *dyh, *g[2], *h[2], *logits, *tmp;
 };
 
+// Deep-CNN layer (BASELINE config c5): parameter offsets (floats) in the layer block
+struct CnnParam {
+  int64_t w1 = -1, b1 = -1, w2 = -1, b2 = -1, size = 0;
+};
+
+struct CnnScratch {
+  bf16 *g[2] = {nullptr, nullptr};  // gradient ping-pong between layers of a pack
+  bf16 *dz = nullptr, *dz2 = nullptr;
+  float *logits = nullptr, *dpool = nullptr;
+};
+
 struct Slots {
   std::vector<float *> w;
   std::vector<bf16 *> wsh;
@@ -154,6 +165,11 @@ struct hm_runtime {
   std::vector<double> klaunch;              // last profiled iteration: (class, flops, bytes, ms) per launch
   int device = 0;
   hm_model m{};
+  int family = HM_FAMILY_GPT;          // GPT / BERT transformer chain or deep CNN
+  std::vector<hm_cnn_layer> cnn;       // CNN: per-layer shapes
+  std::vector<hm::CnnParam> cnn_lay;   // CNN: per-layer parameter offsets
+  int classes = 0, classes_p = 0;      // CNN: classifier width (padded to 64)
+  hm::CnnScratch CT{};
   int64_t alpha = 0;
   int D = 0, S = 0, H = 0, DH = 0, R = 0, V = 0, Vp = 0;
   int64_t total_params = 0;
@@ -332,6 +348,226 @@ static uint8_t *store_layer(const hm_runtime &rt, uint8_t *base, int lo, int L, 
   uint8_t *p = base;
   for (int j = lo; j < L; ++j) p += store_layer_bytes(rt, j == rt.R - 1, n);
   return p;
+}
+
+// ---------------------------------------------------------------------------
+// boundary tensors: the per-sample bytes entering chain layer L (the byte model
+// x(L, 1) of the ProfileSet; L == R is the chain's output)
+// ---------------------------------------------------------------------------
+static int64_t bnd(const hm_runtime &rt, int L) {
+  if (rt.family == HM_FAMILY_CNN) {
+    if (L >= rt.R) return 0;
+    const hm_cnn_layer &c = rt.cnn[L];
+    return (int64_t)c.h * c.w * c.cin * 2;
+  }
+  return L == 0 ? (int64_t)rt.S * 4 : (int64_t)rt.S * rt.m.d_model * 4;
+}
+static int64_t max_bnd(const hm_runtime &rt) {
+  int64_t m = 0;
+  for (int L = 1; L <= rt.R; ++L) m = std::max(m, bnd(rt, L));
+  return m;
+}
+static int64_t labels_per_sample(const hm_runtime &rt) { return rt.family == HM_FAMILY_CNN ? 1 : rt.S; }
+
+// ---------------------------------------------------------------------------
+// deep-CNN layer packs: store layout, forward, backward
+// ---------------------------------------------------------------------------
+static CnnParam cnn_layout(const hm_runtime &rt, int L) {
+  const hm_cnn_layer &c = rt.cnn[L];
+  CnnParam p;
+  int64_t o = 0;
+  if (c.type == HM_CNN_HEAD) {
+    p.w1 = o; o += (int64_t)rt.classes_p * c.cin;
+    p.b1 = o; o += rt.classes_p;
+  } else {
+    p.w1 = o; o += (int64_t)c.cout * 9 * c.cin;
+    p.b1 = o; o += c.cout;
+    if (c.type == HM_CNN_RES) {
+      p.w2 = o; o += (int64_t)c.cout * 9 * c.cout;
+      p.b2 = o; o += c.cout;
+    }
+  }
+  p.size = o;
+  return p;
+}
+
+// per-sample bytes of the tensors layer L keeps, in store order
+static std::vector<int64_t> cnn_act_sizes(const hm_runtime &rt, int L) {
+  const hm_cnn_layer &c = rt.cnn[L];
+  const int64_t P = (int64_t)c.h * c.w;
+  switch (c.type) {
+    case HM_CNN_CONV: return {P * c.cout * 2};                         // y
+    case HM_CNN_DOWN: return {P * c.cout * 2, P / 4 * c.cout * 2};     // a, y = pool(a)
+    case HM_CNN_RES: return {P * c.cout * 2, P * c.cout * 2};          // h, y
+    default: return {(int64_t)c.cin * 2, (int64_t)rt.classes_p * 2};  // pooled, dlogits
+  }
+}
+static int64_t cnn_pack_bytes(const hm_runtime &rt, int lo, int hi, int64_t n) {
+  int64_t b = align_up(n * bnd(rt, lo), 256);
+  for (int L = lo; L <= hi; ++L)
+    for (int64_t sz : cnn_act_sizes(rt, L)) b += align_up(n * sz, 256);
+  return b;
+}
+struct CnnActs {
+  bf16 *x = nullptr;                  // layer input (the pack input or the previous layer's output)
+  bf16 *a = nullptr, *h = nullptr;    // down: post-ReLU pre-pool; res: inner activation
+  bf16 *y = nullptr;                  // layer output
+  bf16 *pooled = nullptr, *dlog = nullptr;  // head
+};
+// activations of layer L (member at sample s0) inside a pack store of n samples
+static CnnActs cnn_acts(const hm_runtime &rt, uint8_t *store, int lo, int L, int64_t n, int64_t s0) {
+  uint8_t *p = store;
+  bf16 *prev_out = reinterpret_cast<bf16 *>(p + s0 * bnd(rt, lo));
+  p += align_up(n * bnd(rt, lo), 256);
+  CnnActs A;
+  for (int j = lo; j <= L; ++j) {
+    auto sz = cnn_act_sizes(rt, j);
+    std::vector<bf16 *> r;
+    for (int64_t b : sz) {
+      r.push_back(reinterpret_cast<bf16 *>(p + s0 * b));
+      p += align_up(n * b, 256);
+    }
+    if (j == L) {
+      A.x = prev_out;
+      switch (rt.cnn[j].type) {
+        case HM_CNN_CONV: A.y = r[0]; break;
+        case HM_CNN_DOWN: A.a = r[0]; A.y = r[1]; break;
+        case HM_CNN_RES: A.h = r[0]; A.y = r[1]; break;
+        default: A.pooled = r[0]; A.dlog = r[1]; break;
+      }
+    }
+    if (rt.cnn[j].type != HM_CNN_HEAD) prev_out = r.back();  // y: the next layer's input
+  }
+  return A;
+}
+
+// Forward of layers [lo, hi] for one member of u samples.  Activations go to
+// `store` (n samples, member at s_off) or, with store == nullptr, to the work
+// store (u samples).  x_in is the pack input (for lo == 0 the image).
+static int cnn_forward_pack(hm_runtime &rt, TaskRt &tr, int lo, int hi, int u, int64_t s0, const uint8_t *x_in,
+                            uint8_t *store, int64_t n, int64_t s_off, uint8_t *y_final) {
+  cudaStream_t s = rt.s_compute;
+  if (!store) {
+    store = rt.work_store;
+    n = u;
+    s_off = 0;
+  }
+  {
+    CnnActs A0 = cnn_acts(rt, store, lo, lo, n, s_off);
+    HM_CUDA(cudaMemcpyAsync(A0.x, x_in, (int64_t)u * bnd(rt, lo), cudaMemcpyDeviceToDevice, s));
+  }
+  for (int L = lo; L <= hi; ++L) {
+    const hm_cnn_layer &c = rt.cnn[L];
+    const CnnParam &P = rt.cnn_lay[L];
+    const int64_t off = rt.w_off[L] - rt.w_off[lo];
+    const float *w = rt.slots.w[tr.w_slot] + off;
+    const bf16 *wsh = rt.slots.wsh[tr.w_slot] + off;
+    CnnActs A = cnn_acts(rt, store, lo, L, n, s_off);
+    if (tr.stash_heads.count(L))  // capture the input of a backward-pack head
+      HM_CUDA(cudaMemcpyAsync(rt.stash_dev.at(L) + s0 * bnd(rt, L), A.x, (int64_t)u * bnd(rt, L),
+                              cudaMemcpyDeviceToDevice, s));
+    switch (c.type) {
+      case HM_CNN_CONV:
+        HM_TRY(gemm::run_conv(1, A.x, wsh + P.w1, A.y, u, c.h, c.w, c.cin, c.cout, HM_EPI_RELU_BF16, w + P.b1,
+                              nullptr, s));
+        break;
+      case HM_CNN_DOWN:
+        HM_TRY(gemm::run_conv(1, A.x, wsh + P.w1, A.a, u, c.h, c.w, c.cin, c.cout, HM_EPI_RELU_BF16, w + P.b1,
+                              nullptr, s));
+        HM_TRY(cnn::pool2_fwd(A.a, A.y, u, c.h, c.w, c.cout, s));
+        break;
+      case HM_CNN_RES:
+        HM_TRY(gemm::run_conv(1, A.x, wsh + P.w1, A.h, u, c.h, c.w, c.cin, c.cout, HM_EPI_RELU_BF16, w + P.b1,
+                              nullptr, s));
+        HM_TRY(gemm::run_conv(1, A.h, wsh + P.w2, A.y, u, c.h, c.w, c.cout, c.cout, HM_EPI_RESID_RELU_BF16,
+                              w + P.b2, A.x, s));
+        break;
+      default: {  // head: global average pool, classifier, cross-entropy
+        HM_TRY(cnn::gap_fwd(A.x, A.pooled, u, c.h * c.w, c.cin, s));
+        HM_TRY(gemm::run(A.pooled, wsh + P.w1, rt.CT.logits, u, rt.classes_p, c.cin, c.cin, c.cin, rt.classes_p, 0, 0,
+                         HM_EPI_STORE_F32, w + P.b1, nullptr, 0, s, 0));
+        HM_TRY(layers::cross_entropy(rt.CT.logits, rt.labels + s0, u, rt.classes_p, rt.classes, A.dlog,
+                                     rt.count_loss ? rt.loss_cur : rt.loss_sink,
+                                     (float)(1.0 / (double)rt.global_tokens), s));
+        break;
+      }
+    }
+    if (L == hi && y_final && c.type != HM_CNN_HEAD)
+      HM_CUDA(cudaMemcpyAsync(y_final, A.y, (int64_t)u * bnd(rt, L + 1), cudaMemcpyDeviceToDevice, s));
+  }
+  return HM_OK;
+}
+
+// Backward of layers [hi .. lo] for one member: dy_in is the gradient of the
+// pack output (null when the pack ends in the head), dx_out receives the
+// gradient of the pack input (null for the pack holding layer 0).
+static int cnn_backward_pack(hm_runtime &rt, TaskRt &tr, int lo, int hi, int u, uint8_t *store, int64_t n,
+                             int64_t s_off, const uint8_t *dy_in, uint8_t *dx_out) {
+  cudaStream_t s = rt.s_compute;
+  if (!store) {
+    store = rt.work_store;
+    n = u;
+    s_off = 0;
+  }
+  CnnScratch &T = rt.CT;
+  const bf16 *dy = reinterpret_cast<const bf16 *>(dy_in);
+  for (int L = hi; L >= lo; --L) {
+    const hm_cnn_layer &c = rt.cnn[L];
+    const CnnParam &P = rt.cnn_lay[L];
+    const int64_t off = rt.w_off[L] - rt.w_off[lo];
+    const bf16 *wsh = rt.slots.wsh[tr.w_slot] + off;
+    float *dw = rt.slots.dw[tr.dw_slot] + off;
+    CnnActs A = cnn_acts(rt, store, lo, L, n, s_off);
+    const int64_t M = (int64_t)u * c.h * c.w;
+    const bool need_dx = L > 0;
+    bf16 *dx = (L == lo && dx_out) ? reinterpret_cast<bf16 *>(dx_out) : T.g[(hi - L) & 1];
+    switch (c.type) {
+      case HM_CNN_HEAD: {
+        // dW_fc += dlog^T . pooled; db_fc += sum dlog; dpooled = dlog . W_fc; dx = dpooled / P
+        HM_TRY(gemm::run(A.dlog, A.pooled, dw + P.w1, rt.classes_p, c.cin, u, rt.classes_p, c.cin, c.cin, 1, 1,
+                         HM_EPI_ACC_F32, nullptr, nullptr, 0, s, 0));
+        HM_TRY(layers::bias_grad(A.dlog, 1, dw + P.b1, u, rt.classes_p, rt.classes_p, s));
+        HM_TRY(gemm::run(A.dlog, wsh + P.w1, T.dpool, u, c.cin, rt.classes_p, rt.classes_p, c.cin, c.cin, 0, 1,
+                         HM_EPI_STORE_F32, nullptr, nullptr, 0, s, 0));
+        HM_TRY(cnn::gap_bwd(T.dpool, dx, u, c.h * c.w, c.cin, s));
+        break;
+      }
+      case HM_CNN_CONV:
+      case HM_CNN_DOWN: {
+        if (!dy) return fail(HM_ERR_INTERNAL, "cnn backward without an incoming gradient");
+        if (c.type == HM_CNN_CONV)
+          HM_TRY(cnn::relu_bwd(dy, A.y, T.dz, M * c.cout, s));
+        else
+          HM_TRY(cnn::pool2_relu_bwd(dy, A.a, T.dz, u, c.h, c.w, c.cout, s));
+        HM_TRY(layers::bias_grad(T.dz, 1, dw + P.b1, M, c.cout, c.cout, s));
+        HM_TRY(gemm::run_conv(3, T.dz, A.x, dw + P.w1, u, c.h, c.w, c.cin, c.cout, HM_EPI_ACC_F32, nullptr, nullptr, s));
+        if (need_dx)
+          HM_TRY(gemm::run_conv(2, T.dz, wsh + P.w1, dx, u, c.h, c.w, c.cin, c.cout, HM_EPI_STORE_BF16, nullptr,
+                                nullptr, s));
+        break;
+      }
+      default: {  // residual block
+        if (!dy) return fail(HM_ERR_INTERNAL, "cnn backward without an incoming gradient");
+        HM_TRY(cnn::relu_bwd(dy, A.y, T.dz2, M * c.cout, s));  // dz2 = dy * (y > 0)
+        HM_TRY(layers::bias_grad(T.dz2, 1, dw + P.b2, M, c.cout, c.cout, s));
+        HM_TRY(gemm::run_conv(3, T.dz2, A.h, dw + P.w2, u, c.h, c.w, c.cout, c.cout, HM_EPI_ACC_F32, nullptr, nullptr,
+                              s));
+        // dz1 = dgrad(dz2) * (h > 0)
+        HM_TRY(gemm::run_conv(2, T.dz2, wsh + P.w2, T.dz, u, c.h, c.w, c.cout, c.cout, HM_EPI_DRELU_BF16, nullptr,
+                              A.h, s));
+        HM_TRY(layers::bias_grad(T.dz, 1, dw + P.b1, M, c.cout, c.cout, s));
+        HM_TRY(gemm::run_conv(3, T.dz, A.x, dw + P.w1, u, c.h, c.w, c.cin, c.cout, HM_EPI_ACC_F32, nullptr, nullptr,
+                              s));
+        // dx = dgrad(dz1) + dz2 (the identity path)
+        if (need_dx)
+          HM_TRY(gemm::run_conv(2, T.dz, wsh + P.w1, dx, u, c.h, c.w, c.cin, c.cout, HM_EPI_ADD_BF16, nullptr, T.dz2,
+                                s));
+        break;
+      }
+    }
+    dy = dx;
+  }
+  return HM_OK;
 }
 
 // ---------------------------------------------------------------------------
@@ -532,6 +768,27 @@ static int run_member(hm_runtime &rt, int task, int g) {
     HM_TRY(layers::cast_f32_bf16(rt.slots.w[tr.w_slot], rt.slots.wsh[tr.w_slot], tr.params, s));
     if (t.type == HM_TASK_B) HM_CUDA(cudaMemsetAsync(rt.slots.dw[tr.dw_slot], 0, tr.params * 4, s));
   }
+  if (rt.family == HM_FAMILY_CNN) {
+    // byte offsets of this member inside the boundary buffers (x(L) per sample)
+    auto at = [&](const void *base, int L) -> uint8_t * {
+      return base ? const_cast<uint8_t *>(static_cast<const uint8_t *>(base)) + s0 * bnd(rt, L) : nullptr;
+    };
+    if (t.type == HM_TASK_F) {
+      const uint8_t *x_in = t.lo == 0 ? at(rt.tokens, 0) : at(tr.in_buf ? tr.in_buf : rt.carry[tr.carry_in], t.lo);
+      if (tr.store_shared)
+        return cnn_forward_pack(rt, tr, t.lo, t.hi, u, s0, x_in, rt.shared_store, rt.minibatch, s0, nullptr);
+      uint8_t *y = tr.out_buf ? at(tr.out_buf, t.hi + 1) : tr.carry_out >= 0 ? at(rt.carry[tr.carry_out], t.hi + 1) : nullptr;
+      return cnn_forward_pack(rt, tr, t.lo, t.hi, u, s0, x_in, nullptr, 0, 0, y);
+    }
+    uint8_t *dx = t.lo == 0 ? nullptr : at(tr.out_buf ? tr.out_buf : rt.dcarry[tr.carry_out], t.lo);
+    if (tr.from_shared)
+      return cnn_backward_pack(rt, tr, t.lo, t.hi, u, rt.shared_store, rt.minibatch, s0, nullptr, dx);
+    // recompute the pack from its stashed input, then backward
+    const uint8_t *x_in = at(rt.slots.stash_in[tr.stash_slot], t.lo);
+    HM_TRY(cnn_forward_pack(rt, tr, t.lo, t.hi, u, s0, x_in, nullptr, 0, 0, nullptr));
+    const uint8_t *dy = at(tr.in_buf ? tr.in_buf : rt.dcarry[tr.carry_in], t.hi + 1);
+    return cnn_backward_pack(rt, tr, t.lo, t.hi, u, nullptr, 0, 0, dy, dx);
+  }
   if (t.type == HM_TASK_F) {
     const float *x_in = t.lo == 0 ? nullptr
                         : tr.in_buf ? tr.in_buf + s0 * rowsd
@@ -653,7 +910,7 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
   for (auto &t : plan->tasks)
     for (auto &e : t.outputs)
       if (e.tensor == HM_SX && e.channel == HM_MESSAGE_PASSING)
-        all_heads[e.layer] = (int64_t)minibatch * rt.S * (e.layer == 0 ? 4 : d * 4);
+        all_heads[e.layer] = (int64_t)minibatch * bnd(rt, e.layer);
 
   // ---- slot assignment (round robin in device order) -------------------------
   static const int env_nw = getenv("HM_W_SLOTS") ? atoi(getenv("HM_W_SLOTS")) : 0;
@@ -703,18 +960,37 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
   // ---- device pool ------------------------------------------------------------
   const int64_t rows_mb = (int64_t)minibatch * rt.S;
   const int64_t rows_u = u_max * rt.S;
+  const int64_t carry_bytes = (int64_t)minibatch * max_bnd(rt);  // one boundary tensor of the whole minibatch
+  if (rt.family == HM_FAMILY_CNN) {
+    for (int ti : mine)
+      if (rt.trt[ti].remote_shared || rt.trt[ti].ship_input)
+        return fail(HM_ERR_VALIDATION, "CNN chains: the shared pack's F and B must run on one GPU");
+    for (auto &t : plan->tasks)
+      for (auto &e : t.inputs)
+        if (e.src_layer >= 0) return fail(HM_ERR_VALIDATION, "CNN chains: relay entries are not executable yet");
+  }
   int64_t max_recompute_layers = 1;
   for (int ti : mine) {
     auto &t = plan->tasks[ti];
     if (t.type == HM_TASK_B && (t.recompute || rt.trt[ti].remote_shared))
       max_recompute_layers = std::max<int64_t>(max_recompute_layers, t.hi - t.lo + 1);
   }
-  int64_t work_bytes = 0;
-  for (int j = 0; j < max_recompute_layers; ++j) work_bytes += store_layer_bytes(rt, j == max_recompute_layers - 1, u_max);
-  work_bytes = std::max(work_bytes, store_layer_bytes(rt, true, u_max));
-  int64_t shared_bytes = 0;
-  if (rt.shared_lo >= 0)
-    for (int L = rt.shared_lo; L <= rt.shared_hi; ++L) shared_bytes += store_layer_bytes(rt, is_head(rt, L), minibatch);
+  int64_t work_bytes = 0, shared_bytes = 0;
+  if (rt.family == HM_FAMILY_CNN) {
+    // the work store holds a whole pack for one member (F without a store, B recompute)
+    for (int ti : mine) {
+      auto &t = plan->tasks[ti];
+      if (t.type != HM_TASK_U) work_bytes = std::max(work_bytes, cnn_pack_bytes(rt, t.lo, t.hi, u_max));
+    }
+    if (rt.shared_lo >= 0) shared_bytes = cnn_pack_bytes(rt, rt.shared_lo, rt.shared_hi, minibatch);
+  } else {
+    for (int j = 0; j < max_recompute_layers; ++j)
+      work_bytes += store_layer_bytes(rt, j == max_recompute_layers - 1, u_max);
+    work_bytes = std::max(work_bytes, store_layer_bytes(rt, true, u_max));
+    if (rt.shared_lo >= 0)
+      for (int L = rt.shared_lo; L <= rt.shared_hi; ++L)
+        shared_bytes += store_layer_bytes(rt, is_head(rt, L), minibatch);
+  }
   struct Req { void **ptr; int64_t bytes; };
   std::vector<Req> req;
   rt.slots.w.assign(NW, nullptr);
@@ -730,8 +1006,8 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
   for (int i = 0; i < NK; ++i) req.push_back({(void **)&rt.slots.k[i], pmax * 8});
   for (int i = 0; i < NST; ++i) req.push_back({(void **)&rt.slots.stash_in[i], std::max<int64_t>(stash_in_max, 256)});
   for (int i = 0; i < 2; ++i) {
-    req.push_back({(void **)&rt.carry[i], rows_mb * d * 4});
-    req.push_back({(void **)&rt.dcarry[i], rows_mb * d * 4});
+    req.push_back({(void **)&rt.carry[i], carry_bytes});
+    req.push_back({(void **)&rt.dcarry[i], carry_bytes});
   }
   std::vector<std::pair<int, uint8_t **>> stash_ptrs;
   rt.stash_dev.clear();
@@ -742,9 +1018,9 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
   std::vector<std::pair<int, float **>> out_bufs;
   for (int ti : mine) {
     TaskRt &tr = rt.trt[ti];
-    if (tr.in_buf) req.push_back({(void **)&tr.in_buf, rows_mb * d * 4});
+    if (tr.in_buf) req.push_back({(void **)&tr.in_buf, carry_bytes});
     if (tr.out_buf) {
-      req.push_back({(void **)&tr.out_buf, rows_mb * d * 4});
+      req.push_back({(void **)&tr.out_buf, carry_bytes});
       out_bufs.push_back({ti, &tr.out_buf});
     }
   }
@@ -753,6 +1029,19 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
   req.push_back({(void **)&rt.shared_store, shared_bytes});
   req.push_back({(void **)&rt.work_store, work_bytes});
   Scratch &T = rt.T;
+  if (rt.family == HM_FAMILY_CNN) {
+    int64_t act = 0, cmax = 0;  // largest per-sample activation of any layer, widest channel count
+    for (auto &c : rt.cnn) {
+      act = std::max(act, (int64_t)c.h * c.w * std::max(c.cin, c.cout) * 2);
+      cmax = std::max<int64_t>(cmax, std::max(c.cin, c.cout));
+    }
+    req.push_back({(void **)&rt.CT.g[0], u_max * act});
+    req.push_back({(void **)&rt.CT.g[1], u_max * act});
+    req.push_back({(void **)&rt.CT.dz, u_max * act});
+    req.push_back({(void **)&rt.CT.dz2, u_max * act});
+    req.push_back({(void **)&rt.CT.logits, u_max * rt.classes_p * 4});
+    req.push_back({(void **)&rt.CT.dpool, u_max * cmax * 4});
+  } else {
   req.push_back({(void **)&T.dy_bf, rows_u * d * 2});
   req.push_back({(void **)&T.dh, rows_u * 4 * d * 2});
   req.push_back({(void **)&T.dh1_bf, rows_u * d * 2});
@@ -769,8 +1058,10 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
   req.push_back({(void **)&T.h[1], rows_u * d * 4});
   req.push_back({(void **)&T.tmp, rows_u * d * 4});
   req.push_back({(void **)&T.logits, rows_u * rt.Vp * 4});
-  req.push_back({(void **)&rt.tokens, rows_mb * 4});
-  req.push_back({(void **)&rt.labels, rows_mb * 4});
+  }
+  (void)rows_mb;
+  req.push_back({(void **)&rt.tokens, (int64_t)minibatch * bnd(rt, 0)});
+  req.push_back({(void **)&rt.labels, (int64_t)minibatch * labels_per_sample(rt) * 4});
   req.push_back({(void **)&rt.loss_dev, 64 * sizeof(double)});
   req.push_back({(void **)&rt.adam_dev, 256});
   int64_t total = 0;
@@ -943,7 +1234,7 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
         // pull the producer's output over NVLink into this task's receive buffer
         a.kind = 6;
         a.stream = rt.s_p2p_in;
-        const int64_t per = (int64_t)rt.S * d * 4;
+        const int64_t per = bnd(rt, r.tensor == HM_X ? r.layer : r.layer + 1);
         const int64_t off = r.peer_member >= 0 ? tr.s0[r.member] * per : 0;
         const int64_t expect = r.peer_member >= 0 ? (int64_t)t.group[r.member] * per : (int64_t)minibatch * per;
         if (r.nbytes != expect) return fail(HM_ERR_INTERNAL, "peer hand-off size disagrees with the activation layout");
@@ -973,7 +1264,7 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
         a.src = rt.slots.k[tr.k_slot];
         a.dst = rt.k_host + 2 * rt.w_off[t.lo];
       } else if (r.channel == HM_MESSAGE_PASSING && r.tensor == HM_SX) {
-        const int64_t per = rt.S * (r.layer == 0 ? 4 : d * 4);
+        const int64_t per = bnd(rt, r.layer);
         const int64_t boff = tr.s0[r.member] * per;
         a.src = rt.stash_dev.at(r.layer) + boff;
         a.dst = rt.stash_host + rt.stash_host_off[r.layer] + boff;
@@ -1162,7 +1453,8 @@ static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *l
   const int64_t launches0 = launch_counter().load();
   rt.step += 1;
   cudaStream_t sc = rt.s_compute;
-  const int64_t tb = (int64_t)rt.minibatch * rt.S * 4;
+  const int64_t tb = (int64_t)rt.minibatch * bnd(rt, 0);                    // tokens / images
+  const int64_t lb = (int64_t)rt.minibatch * labels_per_sample(rt) * 4;  // labels
   rt.loss_cur = rt.loss_dev;
   // Adam bias corrections for this step live in device memory so a captured
   // graph replays correctly: {lr / (1 - b1^t), 1 / sqrt(1 - b2^t)}
@@ -1171,7 +1463,7 @@ static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *l
   HM_CUDA(cudaEventRecord(rt.ev_iter0, sc));
   HM_CUDA(cudaMemcpyAsync(rt.adam_dev, rt.adam_host, 2 * sizeof(float), cudaMemcpyHostToDevice, sc));
   HM_CUDA(cudaMemcpyAsync(rt.tokens, tokens, tb, is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, sc));
-  HM_CUDA(cudaMemcpyAsync(rt.labels, labels, tb, is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, sc));
+  HM_CUDA(cudaMemcpyAsync(rt.labels, labels, lb, is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, sc));
   int64_t h2d = 0, d2h = 0, coll = 0;
   const int gi = rt.profiling ? 1 : 0;
   const bool use_graph = rt.use_graph && !rt.p2p_mode && rt.iterations >= 1;
@@ -1273,7 +1565,8 @@ static int run_steps(hm_runtime &rt, int n, const int32_t *tokens, const int32_t
   HM_CUDA(cudaSetDevice(rt.device));
   const int64_t launches0 = launch_counter().load();
   cudaStream_t sc = rt.s_compute;
-  const int64_t tb = (int64_t)rt.minibatch * rt.S * 4;
+  const int64_t tb = (int64_t)rt.minibatch * bnd(rt, 0);
+  const int64_t lb = (int64_t)rt.minibatch * labels_per_sample(rt) * 4;
   int64_t h2d = 0, d2h = 0, coll = 0;
   HM_CUDA(cudaEventRecord(rt.ev_first, sc));
   cudaStream_t others[] = {rt.s_h2d, rt.s_d2h, rt.s_update, rt.s_comm};
@@ -1283,7 +1576,7 @@ static int run_steps(hm_runtime &rt, int n, const int32_t *tokens, const int32_t
     rt.loss_cur = rt.loss_dev + i;
     if (i == n - 1) HM_CUDA(cudaEventRecord(rt.ev_iter0, sc));
     HM_CUDA(cudaMemcpyAsync(rt.tokens, tokens, tb, is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, sc));
-    HM_CUDA(cudaMemcpyAsync(rt.labels, labels, tb, is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, sc));
+    HM_CUDA(cudaMemcpyAsync(rt.labels, labels, lb, is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, sc));
     HM_TRY(enqueue_body(rt, false, true, h2d, d2h, coll));
   }
   HM_TRY(join_streams(rt));
@@ -1325,6 +1618,35 @@ static int run_steps(hm_runtime &rt, int n, const int32_t *tokens, const int32_t
 
 }  // namespace hm
 
+namespace hm {
+// streams, events and the pinned W / K arenas (shared by both model families)
+static hm_runtime *finish_create(std::unique_ptr<hm_runtime> rt, int32_t *status) {
+  auto bad = [&](int code, const std::string &msg) -> hm_runtime * {
+    hm::set_last_error(msg);
+    if (status) *status = code;
+    return nullptr;
+  };
+  cudaStream_t *ss[] = {&rt->s_compute, &rt->s_h2d,     &rt->s_d2h,    &rt->s_update,
+                        &rt->s_p2p_in,  &rt->s_p2p_out, &rt->s_comm};
+  for (auto p : ss)
+    if (cudaStreamCreateWithFlags(p, cudaStreamNonBlocking) != cudaSuccess) return bad(HM_ERR_DEVICE, "stream create");
+  cudaEventCreate(&rt->ev_iter0);
+  cudaEventCreate(&rt->ev_iter1);
+  cudaEventCreateWithFlags(&rt->ev_fork, cudaEventDisableTiming);
+  for (auto &e : rt->ev_join) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  if (cudaHostAlloc(&rt->adam_host, 64, cudaHostAllocDefault) != cudaSuccess ||
+      cudaHostAlloc(&rt->loss_host, 64 * sizeof(double), cudaHostAllocDefault) != cudaSuccess)
+    return bad(HM_ERR_DEVICE, "pinned alloc");
+  cudaEventCreate(&rt->ev_first);
+  if (cudaHostAlloc(&rt->w_host, rt->total_params * 4, cudaHostAllocDefault) != cudaSuccess ||
+      cudaHostAlloc(&rt->k_host, rt->total_params * 8, cudaHostAllocDefault) != cudaSuccess)
+    return bad(HM_ERR_DEVICE, "pinned host arena allocation failed (" + std::to_string(rt->total_params * 12) + " B)");
+  std::memset(rt->k_host, 0, rt->total_params * 8);
+  if (status) *status = HM_OK;
+  return rt.release();
+}
+}  // namespace hm
+
 // ---------------------------------------------------------------------------
 // C ABI
 // ---------------------------------------------------------------------------
@@ -1359,25 +1681,60 @@ hm_runtime *hm_runtime_create(int32_t device, const hm_model *model, int64_t alp
     rt->w_off[L + 1] = rt->w_off[L] + rt->lay.back().size;
   }
   rt->total_params = rt->w_off[rt->R];
-  cudaStream_t *ss[] = {&rt->s_compute, &rt->s_h2d,     &rt->s_d2h,    &rt->s_update,
-                        &rt->s_p2p_in,  &rt->s_p2p_out, &rt->s_comm};
-  for (auto p : ss)
-    if (cudaStreamCreateWithFlags(p, cudaStreamNonBlocking) != cudaSuccess) return bad(HM_ERR_DEVICE, "stream create");
-  cudaEventCreate(&rt->ev_iter0);
-  cudaEventCreate(&rt->ev_iter1);
-  cudaEventCreateWithFlags(&rt->ev_fork, cudaEventDisableTiming);
-  for (auto &e : rt->ev_join) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-  if (cudaHostAlloc(&rt->adam_host, 64, cudaHostAllocDefault) != cudaSuccess ||
-      cudaHostAlloc(&rt->loss_host, 64 * sizeof(double), cudaHostAllocDefault) != cudaSuccess)
-    return bad(HM_ERR_DEVICE, "pinned alloc");
-  cudaEventCreate(&rt->ev_first);
-  if (cudaHostAlloc(&rt->w_host, rt->total_params * 4, cudaHostAllocDefault) != cudaSuccess ||
-      cudaHostAlloc(&rt->k_host, rt->total_params * 8, cudaHostAllocDefault) != cudaSuccess)
-    return bad(HM_ERR_DEVICE, "pinned host arena allocation failed (" + std::to_string(rt->total_params * 12) + " B)");
-  std::memset(rt->k_host, 0, rt->total_params * 8);
-  if (status) *status = HM_OK;
-  return rt.release();
+  return hm::finish_create(std::move(rt), status);
 }
+
+hm_runtime *hm_runtime_create_cnn(int32_t device, const hm_cnn_model *model, int64_t alpha_bytes, int32_t *status) {
+  auto bad = [&](int code, const std::string &msg) -> hm_runtime * {
+    hm::set_last_error(msg);
+    if (status) *status = code;
+    return nullptr;
+  };
+  if (!model || !model->layers || model->n_layer < 1) return bad(HM_ERR_VALIDATION, "null or empty CNN model");
+  const int R = model->n_layer;
+  if (model->classes < 1 || model->classes_padded % 64 || model->classes_padded < model->classes)
+    return bad(HM_ERR_VALIDATION, "classes_padded must be a multiple of 64 and >= classes");
+  for (int L = 0; L < R; ++L) {
+    const hm_cnn_layer &c = model->layers[L];
+    const std::string at = "CNN layer " + std::to_string(L) + ": ";
+    if ((c.type == HM_CNN_HEAD) != (L == R - 1)) return bad(HM_ERR_VALIDATION, at + "the head must be the last layer");
+    if (c.type < HM_CNN_CONV || c.type > HM_CNN_HEAD) return bad(HM_ERR_VALIDATION, at + "unknown type");
+    if (c.h < 1 || c.w < 1 || c.cin % 64 || c.cin < 64 || (c.type != HM_CNN_HEAD && (c.cout % 64 || c.cout < 64)))
+      return bad(HM_ERR_VALIDATION, at + "channels must be positive multiples of 64");
+    if (c.type == HM_CNN_DOWN && (c.h % 2 || c.w % 2)) return bad(HM_ERR_VALIDATION, at + "pooling needs even h, w");
+    if (c.type == HM_CNN_RES && c.cin != c.cout) return bad(HM_ERR_VALIDATION, at + "residual blocks keep the width");
+    if (L + 1 < R) {
+      const hm_cnn_layer &n = model->layers[L + 1];
+      const int oh = c.type == HM_CNN_DOWN ? c.h / 2 : c.h, ow = c.type == HM_CNN_DOWN ? c.w / 2 : c.w;
+      if (n.cin != c.cout || n.h != oh || n.w != ow)
+        return bad(HM_ERR_VALIDATION, at + "output shape does not match the next layer's input");
+    }
+  }
+  if (cudaSetDevice(device) != cudaSuccess) return bad(HM_ERR_DEVICE, "cudaSetDevice failed");
+  auto rt = std::make_unique<hm_runtime>();
+  rt->device = device;
+  rt->family = HM_FAMILY_CNN;
+  rt->m.n_layer = R;
+  rt->m.lr = model->lr;
+  rt->m.beta1 = model->beta1;
+  rt->m.beta2 = model->beta2;
+  rt->m.eps = model->eps;
+  rt->alpha = alpha_bytes;
+  rt->R = R;
+  rt->S = 1;
+  rt->classes = model->classes;
+  rt->classes_p = model->classes_padded;
+  rt->cnn.assign(model->layers, model->layers + R);
+  rt->w_off.assign(R + 1, 0);
+  for (int L = 0; L < R; ++L) {
+    rt->cnn_lay.push_back(hm::cnn_layout(*rt, L));
+    rt->w_off[L + 1] = rt->w_off[L] + rt->cnn_lay.back().size;
+  }
+  rt->total_params = rt->w_off[R];
+  return hm::finish_create(std::move(rt), status);
+}
+
+
 
 void *hm_runtime_arena(hm_runtime *rt, int32_t kind, int64_t *bytes) {
   if (!rt) return nullptr;
@@ -1413,7 +1770,7 @@ int hm_runtime_load_plan(hm_runtime *rt, hm_plan *plan, int32_t rank, int32_t mi
       per_rank[t.dev_id] += s;
     }
   for (auto &kv : per_rank) global += kv.second;
-  rt->global_tokens = global * rt->S;
+  rt->global_tokens = global * hm::labels_per_sample(*rt);
   return hm::load_plan(*rt, plan->p, rank, minibatch);
 }
 

@@ -21,6 +21,7 @@ from . import _native as NL
 from .core import MachineModel, gpu_shares
 from .errors import ValidationError
 from .lowering import NativePlan
+from .cnn import CNNSpec
 from .model import GPTSpec
 from .profiler import ProfileSet
 from .simulator import SimReport, report_from_items
@@ -30,15 +31,22 @@ from .taskgraph import TaskGraph
 class HarmonyRuntime:
     """Native runtime for one GPU: arenas, streams, kernels, plan executor."""
 
-    def __init__(self, spec: GPTSpec, *, alpha_bytes: int, device: int = 0, lr: float = 1e-4,
+    def __init__(self, spec: GPTSpec | CNNSpec, *, alpha_bytes: int, device: int = 0, lr: float = 1e-4,
                  betas: tuple[float, float] = (0.9, 0.999), eps: float = 1e-8) -> None:
         self.spec = spec
         self.lib = NL.lib()
-        m = NL.hm_model(spec.n_layer, spec.d_model, spec.n_head, spec.seq_len, spec.vocab,
-                        spec.vocab_padded, 1 if spec.causal else 0, 0, lr, betas[0], betas[1], eps)
-        self._model = m
+        self.is_cnn = isinstance(spec, CNNSpec)
         st = C.c_int32(0)
-        h = self.lib.hm_runtime_create(device, C.byref(m), int(alpha_bytes), C.byref(st))
+        if self.is_cnn:
+            arr = (NL.hm_cnn_layer * spec.n_layer)(*[NL.hm_cnn_layer(*lay) for lay in spec.layers])
+            m = NL.hm_cnn_model(spec.n_layer, arr, spec.classes, spec.classes_padded, lr, betas[0], betas[1], eps)
+            self._model = (m, arr)
+            h = self.lib.hm_runtime_create_cnn(device, C.byref(m), int(alpha_bytes), C.byref(st))
+        else:
+            m = NL.hm_model(spec.n_layer, spec.d_model, spec.n_head, spec.seq_len, spec.vocab,
+                            spec.vocab_padded, 1 if spec.causal else 0, 0, lr, betas[0], betas[1], eps)
+            self._model = m
+            h = self.lib.hm_runtime_create(device, C.byref(m), int(alpha_bytes), C.byref(st))
         if not h:
             NL.check(st.value or -4)
         self.handle = h
@@ -64,12 +72,42 @@ class HarmonyRuntime:
 
     # -- state ----------------------------------------------------------------
     def layer_params(self, L: int) -> dict[str, np.ndarray]:
-        """Views of layer L's master weights in the W arena, by segment name."""
+        """Views of layer L's master weights in the W arena, by segment name
+        (CNN segments come shaped: weights [cout, 3, 3, cin])."""
         out, o = {}, int(self.w_off[L])
-        for name, n in self.spec.layer_segments(L):
-            out[name] = self.w[o:o + n]
+        for name, shp in self.spec.layer_segments(L):
+            n = int(np.prod(shp)) if isinstance(shp, tuple) else int(shp)
+            out[name] = self.w[o:o + n].reshape(shp) if isinstance(shp, tuple) else self.w[o:o + n]
             o += n
         return out
+
+    def _init_cnn(self, seed: int) -> None:
+        """He-normal convolutions (fan-in 9 x the real input channels), the
+        second convolution of a residual block scaled by 0.1 (SkipInit-style:
+        no BatchNorm), classifier N(0, 0.01) with zero padding rows, zero
+        biases; Adam state zero."""
+        import torch
+        from .cnn import HEAD, RES
+        gen = torch.Generator().manual_seed(seed)
+        for L, (t, cin, cout, _, _) in enumerate(self.spec.layers):
+            p = self.layer_params(L)
+            for name, view in p.items():
+                if name.startswith("b"):
+                    view[...] = 0.0
+                    continue
+                shape = tuple(view.shape)
+                if t == HEAD:
+                    v = torch.empty(shape).normal_(0.0, 0.01, generator=gen)
+                    v[self.spec.classes:] = 0.0
+                else:
+                    fan_in = 9 * (3 if L == 0 else shape[-1])
+                    v = torch.empty(shape).normal_(0.0, (2.0 / fan_in) ** 0.5, generator=gen)
+                    if L == 0:
+                        v[..., 3:] = 0.0  # padded image channels
+                    if t == RES and name == "w2":
+                        v *= 0.1
+                view[...] = v.numpy()
+        self.k[:] = 0.0
 
     def init_weights(self, seed: int = 0, device: str | None = None) -> None:
         """N(0, 0.02) matrices/embeddings, LayerNorm gamma=1 / beta=0, zero
@@ -78,6 +116,8 @@ class HarmonyRuntime:
         pinned arena (seconds instead of minutes for a 15 B-parameter model;
         a different random stream than the CPU generator)."""
         import torch
+        if self.is_cnn:
+            return self._init_cnn(seed)
         if device is not None:
             gen = torch.Generator(device=device).manual_seed(seed)
             V, d = self.spec.vocab, self.spec.d_model
@@ -209,6 +249,11 @@ class HarmonyRuntime:
         if self.plan is None:
             raise ValidationError("load() a plan first")
         loss = C.c_double(0.0)
+        if self.is_cnn:
+            img, lab = self._cnn_inputs(tokens, labels)
+            NL.check(self.lib.hm_runtime_run_iteration(self.handle, C.c_void_p(img.data_ptr()),
+                                                       C.c_void_p(lab.data_ptr()), int(img.is_cuda), C.byref(loss)))
+            return loss.value
         if hasattr(tokens, "is_cuda") and tokens.is_cuda:
             # the runtime's streams are non-blocking: torch's pending work on
             # the token buffers must be finished before they are read
@@ -226,6 +271,22 @@ class HarmonyRuntime:
         NL.check(rc)
         return loss.value
 
+    def _cnn_inputs(self, images, labels):
+        """CNN inputs as torch tensors: images [samples, h, w, 64] bf16 (NHWC,
+        zero-padded channels), labels [samples] int32; both on one device."""
+        import torch
+        h, w, c = self.spec.image
+        if not isinstance(images, torch.Tensor) or images.dtype != torch.bfloat16 or \
+                tuple(images.shape) != (self.samples, h, w, c):
+            raise ValidationError(f"images must be a bf16 tensor [{self.samples}, {h}, {w}, {c}]")
+        labels = torch.as_tensor(labels, dtype=torch.int32, device=images.device)
+        if tuple(labels.shape) != (self.samples,):
+            raise ValidationError(f"labels must be [{self.samples}]")
+        images, labels = images.contiguous(), labels.contiguous()
+        if images.is_cuda:
+            torch.cuda.current_stream(images.device).synchronize()
+        return images, labels
+
     def run_steps(self, n: int, tokens, labels) -> tuple[list[float], float]:
         """``n`` pipelined iterations (cross-iteration overlap); returns the
         per-iteration losses and the device seconds of all n iterations."""
@@ -233,6 +294,12 @@ class HarmonyRuntime:
             raise ValidationError("load() a plan first")
         losses = (C.c_double * n)()
         total = C.c_int64(0)
+        if self.is_cnn:
+            img, lab = self._cnn_inputs(tokens, labels)
+            NL.check(self.lib.hm_runtime_run_steps(self.handle, n, C.c_void_p(img.data_ptr()),
+                                                   C.c_void_p(lab.data_ptr()), int(img.is_cuda), losses,
+                                                   C.byref(total)))
+            return list(losses), total.value / 1e9
         if hasattr(tokens, "is_cuda") and tokens.is_cuda:
             import torch
             torch.cuda.current_stream(tokens.device).synchronize()

@@ -178,3 +178,58 @@ def test_checkpoint_resume_is_exact(tmp_path):
     assert np.allclose(got, ref, rtol=1e-5)
     assert np.linalg.norm(b.w - w_ref) / np.linalg.norm(w_ref) < 5e-4
     b.close()
+
+
+def _run_cnn(spec, cfg, steps, alpha=8 << 30, lr=1e-4):
+    """CNN chain through the runtime vs the fp32 oracle; the executed ledger
+    must equal simulate's row for row."""
+    from oracle.cnn_cpu import CNNOracle
+    from paper_2202_01306_b200.cnn import cnn_profiles, synthetic_images
+    from paper_2202_01306_b200.runtime import HarmonyRuntime
+    prof = cnn_profiles(spec, u_max=64)
+    mach = H.MachineModel(gpu_count=1, gpu_mem_capacity=alpha, pcie_bandwidth=55_000_000_000)
+    g = H.generate_task_graph(cfg, mach, prof)
+    rt = HarmonyRuntime(spec, alpha_bytes=alpha, lr=lr)
+    rt.init_weights(0)
+    oracle = CNNOracle(spec, rt.w.copy(), rt.w_off, lr=lr)
+    rt.load(g, mach, prof)
+    img, lab = synthetic_images(spec, cfg.minibatch)
+    sim = H.simulate(g, mach, prof)
+    losses = []
+    for i in range(steps):
+        loss = rt.step(img, lab)
+        ref = oracle.step(img, lab, list(g.tasks[0].group))
+        losses.append((loss, ref))
+        assert abs(loss - ref) / abs(ref) < CNN_LOSS_RTOL, (i, loss, ref)
+        rep = rt.report()
+        assert rep.ledger == sim.ledger
+        assert rep.tensor_volumes == sim.tensor_volumes
+    w_ref = oracle.w.numpy()
+    rel_w = np.linalg.norm(rt.w - w_ref) / np.linalg.norm(w_ref)
+    rt.close()
+    return rel_w, losses
+
+
+# bf16 NHWC activations between every layer (the CNN byte model); measured
+# 5e-5 (loss) and 4-5e-4 (weights) after 3 steps at lr 1e-4
+CNN_LOSS_RTOL = 2e-3
+CNN_STATE_RTOL = 1e-3
+
+
+@pytest.mark.parametrize("name", ["resnet-tiny", "vgg-tiny"])
+@pytest.mark.parametrize("pf,pb,uf,ub,mode", [
+    (((0, 2), (3, 6)), ((0, 2), (3, 6)), 2, 2, "pp"),          # two packs, recompute from the stash
+    (((0, 1), (2, 3), (4, 6)), ((0, 2), (3, 3), (4, 6)), 2, 4, "pp"),  # u_f != u_b, a mid-pack stash head
+    (((0, 6),), ((0, 6),), 3, 3, "pp"),                        # one shared pack, remainder group
+    (((0, 2), (3, 6)), ((0, 2), (3, 6)), 2, 2, "dp"),          # Harmony-DP at N=1
+])
+def test_cnn_chain_matches_oracle(name, pf, pb, uf, ub, mode):
+    """BASELINE config c5 at test size: ResNet- and VGG-style chains (implicit-
+    GEMM conv packs) through the swap schedule; ledger bit-exact, loss and
+    weights vs the fp32 oracle after 3 steps."""
+    from paper_2202_01306_b200.cnn import CNN_PRESETS
+    spec = CNN_PRESETS[name]
+    cfg = H.Configuration(uf, pf, ub, pb, 8, H.Mode(mode))
+    rel_w, losses = _run_cnn(spec, cfg, steps=3)
+    print(name, "cnn rel_w", rel_w, losses)
+    assert rel_w < CNN_STATE_RTOL
