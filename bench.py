@@ -40,6 +40,8 @@ WORKLOADS = {
     "tiny": ("tiny", 16, 4, 2, 4, "pp"),
     # north-star target shape: W + Adam state (184 GB) > one GPU's HBM
     "gpt-15b-dp": ("gpt-15b", 24, 4, 3, 170, "dp"),
+    # config c5: deep-CNN packs (128 residual blocks at 56x56 / 28x28, implicit-GEMM convs)
+    "resnet-dp": ("resnet-bench", 64, 16, 16, 8, "dp"),
 }
 
 
@@ -178,6 +180,34 @@ def step_flops(graph, spec) -> int:
     return total
 
 
+def cnn_port_sample(spec, threads: int, seconds_cap: float = 30.0) -> dict:
+    """Time the torch-CPU fp32 port (oracle/cnn_cpu.py) on one sample through
+    the whole chain (fwd + bwd + Adam): the per-sample cost of the workload."""
+    import numpy as np
+    import torch
+    from oracle.cnn_cpu import CNNOracle
+    from paper_2202_01306_b200.cnn import synthetic_images
+    torch.set_num_threads(threads)
+    n = spec.total_params()
+    g = torch.Generator().manual_seed(0)
+    w = (torch.randn(n, generator=g) * 0.02).numpy()
+    off = np.cumsum([0] + [spec.layer_params(L) for L in range(spec.n_layer)])
+    o = CNNOracle(spec, w, off)
+    img, lab = synthetic_images(spec, 1)
+    o.step(img, lab, [1])  # warm
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        o.step(img, lab, [1])
+        reps += 1
+        if time.perf_counter() - t0 > min(seconds_cap, 10.0) or reps >= 5:
+            break
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": 1.0 / dt, "unit": "samples/s", "cores": threads, "kind": "port",
+            "sample": f"torch-CPU fp32 port (oracle/cnn_cpu.py), 1 sample through the full {spec.name} chain "
+                      f"(fwd + bwd + Adam), {reps} reps of {dt:.2f} s"}
+
+
 def cpu_port_sample(spec, threads: int, seconds_cap: float = 30.0) -> dict:
     """Time the torch-CPU fp32 port (oracle/gpt_cpu.py) on a bounded sample:
     one sample through a 2-layer model of the workload's shapes (embedding +
@@ -248,24 +278,26 @@ def run_native(args) -> None:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2202_01306_b200 as H
     from paper_2202_01306_b200 import ops
+    from paper_2202_01306_b200.cnn import CNN_PRESETS, cnn_profiles, synthetic_images
     from paper_2202_01306_b200.model import GPT_PRESETS, gpt_machine, gpt_profiles, synthetic_batch
     from paper_2202_01306_b200.runtime import HarmonyRuntime
 
     preset, per_gpu, u, lpp, alpha_gib, mode = WORKLOADS[args.workload]
     if args.alpha_gib:
         alpha_gib = args.alpha_gib
-    spec = GPT_PRESETS[preset]
+    is_cnn = preset in CNN_PRESETS
+    spec = CNN_PRESETS[preset] if is_cnn else GPT_PRESETS[preset]
     D = per_gpu * world
     R = spec.n_layer
     packs = tuple((i, min(i + lpp, R) - 1) for i in range(0, R, lpp))
     cfg = H.Configuration(u, packs, u, packs, D, H.Mode(mode))
     pcie = _pcie_gbs()
     machine = gpt_machine(world, alpha_bytes=alpha_gib << 30, pcie_gbs=min(pcie["h2d"], pcie["d2h"]) * 1e9)
-    prof = gpt_profiles(spec)
+    prof = cnn_profiles(spec) if is_cnn else gpt_profiles(spec)
     graph = H.generate_task_graph(cfg, machine, prof)
     sim = H.simulate(graph, machine, prof)
     rt = HarmonyRuntime(spec, alpha_bytes=alpha_gib << 30, device=local)
-    rt.init_weights(0, device="cuda" if spec.total_params() > 4_000_000_000 else None)
+    rt.init_weights(0, device="cuda" if spec.total_params() > 4_000_000_000 and not is_cnn else None)
     if world > 1:
         import torch.distributed as dist
         obj = [HarmonyRuntime.nccl_unique_id() if rank == 0 else None]
@@ -273,12 +305,17 @@ def run_native(args) -> None:
         rt.init_comm(obj[0], world, rank)
     rt.load(graph, machine, prof, rank=rank)
     lo, hi = rt.sample_range()
-    tok_all, lab_all = synthetic_batch(spec, D)
-    tok, lab = tok_all[lo:hi], lab_all[lo:hi]
-    tok_d = torch.from_numpy(tok).cuda()
-    lab_d = torch.from_numpy(lab).cuda()
-    tok_p = torch.from_numpy(tok).pin_memory()
-    lab_p = torch.from_numpy(lab).pin_memory()
+    if is_cnn:
+        img_all, labc_all = synthetic_images(spec, D)
+        tok_c, lab_c = img_all[lo:hi].contiguous(), labc_all[lo:hi].contiguous()
+    else:
+        tok_all, lab_all = synthetic_batch(spec, D)
+        tok_c, lab_c = torch.from_numpy(tok_all[lo:hi]), torch.from_numpy(lab_all[lo:hi])
+    in_bytes = tok_c.numel() * tok_c.element_size() + lab_c.numel() * lab_c.element_size()
+    tok_d = tok_c.cuda()
+    lab_d = lab_c.cuda()
+    tok_p = tok_c.pin_memory()
+    lab_p = lab_c.pin_memory()
 
     for _ in range(args.warmup):
         rt.step(tok_d, lab_d)
@@ -314,7 +351,8 @@ def run_native(args) -> None:
     t_total = _max_over_ranks(t_dev, world)
     # e2e: tokens from pinned host memory every step, per-step losses read back
     _barrier(world)
-    _, t_e2e = rt.run_steps(args.steps, tok_p.numpy(), lab_p.numpy())
+    _, t_e2e = rt.run_steps(args.steps, tok_p, lab_p) if is_cnn else rt.run_steps(args.steps, tok_p.numpy(),
+                                                                                   lab_p.numpy())
     t_e2e = _max_over_ranks(t_e2e, world)
 
     samples_per_step = D
@@ -353,7 +391,7 @@ def run_native(args) -> None:
         "data": "synthetic (tokens U[0,V) seed 1234; weights N(0,0.02) seed 0)",
         "config": {"workload": f"{args.workload}: {spec.name} Harmony-{mode.upper()}, packs of {lpp} layers, "
                                f"u_f=u_b={u}, alpha={alpha_gib} GiB/GPU",
-                   "global_batch": D, "seq_len": spec.seq_len, "parallelism": f"harmony-{mode}{world}",
+                   "global_batch": D, "seq_len": getattr(spec, "seq_len", None), "parallelism": f"harmony-{mode}{world}",
                    "l2": "inputs larger than L2 (W and K stream from host every step)"},
         "swap_gb_per_iter": round((swap_in + swap_out) / 1e9, 3),
         "swap_h2d_gb": round(swap_in / 1e9, 3), "swap_d2h_gb": round(swap_out / 1e9, 3),
@@ -373,7 +411,7 @@ def run_native(args) -> None:
         "stream_busy_frac": util,
         "last_iter_ms_unpipelined_view": round(cnt["iteration_ns"] / 1e6, 2),
         "adam_hbm": {"achieved_gbs": round(adam_gbs, 1), "peak": pk["hbm"], "frac": round(adam_gbs / pk["hbm"], 4)},
-        "e2e": {"value": round(e2e_value, 3), "unit": "samples/s", "h2d_bytes_per_step": int(tok.nbytes + lab.nbytes),
+        "e2e": {"value": round(e2e_value, 3), "unit": "samples/s", "h2d_bytes_per_step": int(in_bytes),
                 "d2h_bytes_per_step": 8},
         "gpu_launches": int(launches),
         "clocks": clk,
@@ -383,7 +421,8 @@ def run_native(args) -> None:
         "nccl_allreduce_gb_per_iter": round(cnt["nccl_bytes"] / 1e9, 3),
     }
     if not args.no_cpu_baseline and rank == 0 and world == 1:
-        line["cpu_baseline"] = cpu_port_sample(spec, len(os.sched_getaffinity(0)), seconds_cap=20.0)
+        line["cpu_baseline"] = (cnn_port_sample if is_cnn else cpu_port_sample)(
+            spec, len(os.sched_getaffinity(0)), seconds_cap=20.0)
     if rank == 0:
         print(json.dumps(line), flush=True)
     rt.close()
