@@ -166,6 +166,8 @@ struct hm_runtime {
   int device = 0;
   hm_model m{};
   int family = HM_FAMILY_GPT;          // GPT / BERT transformer chain or deep CNN
+  int slot_nw = 0, slot_nk = 0;        // W / K slot counts chosen by load_plan (0 = minimum)
+  bool slots_sized = false;
   std::vector<hm_cnn_layer> cnn;       // CNN: per-layer shapes
   std::vector<hm::CnnParam> cnn_lay;   // CNN: per-layer parameter offsets
   int classes = 0, classes_p = 0;      // CNN: classifier width (padded to 64)
@@ -913,9 +915,14 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
         all_heads[e.layer] = (int64_t)minibatch * bnd(rt, e.layer);
 
   // ---- slot assignment (round robin in device order) -------------------------
+  // Slot counts: 3 W and 2 K slots are the minimum the one-task-ahead schedule
+  // needs; load_plan re-runs itself with more (up to 4 each, K first) when
+  // alpha leaves room, so a K swap-in never waits for the swap-out of the K
+  // two updates back (HM_W_SLOTS / HM_K_SLOTS pin the counts).
   static const int env_nw = getenv("HM_W_SLOTS") ? atoi(getenv("HM_W_SLOTS")) : 0;
   static const int env_nk = getenv("HM_K_SLOTS") ? atoi(getenv("HM_K_SLOTS")) : 0;
-  const int NW = env_nw >= 3 ? env_nw : 3, NDW = 2, NK = env_nk >= 2 ? env_nk : 2, NST = 2;
+  const int NW = env_nw >= 3 ? env_nw : std::max(3, rt.slot_nw), NDW = 2,
+            NK = env_nk >= 2 ? env_nk : std::max(2, rt.slot_nk), NST = 2;
   int wn = 0, dwn = 0, kn = 0, stn = 0, fcur = -1, bcur = -1;
   std::vector<int> w_owner(NW, -1), dw_owner(NDW, -1), k_owner(NK, -1), st_owner(NST, -1);
   int64_t stash_in_max = 0;
@@ -1069,6 +1076,22 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
   if (total > rt.alpha)
     return fail(HM_ERR_CAPACITY, "runtime needs " + std::to_string(total) + " device bytes > alpha " +
                                      std::to_string(rt.alpha));
+  if (!rt.slots_sized && !env_nw && !env_nk) {
+    int nw = NW, nk = NK;
+    int64_t room = rt.alpha - total;
+    const int64_t kslot = align_up(pmax * 8, 1024), wslot = align_up(pmax * 4, 1024) + align_up(pmax * 2, 1024);
+    while (nk < 4 && room >= kslot) { ++nk; room -= kslot; }
+    while (nw < 4 && room >= wslot) { ++nw; room -= wslot; }
+    if (nw != NW || nk != NK) {
+      rt.slot_nw = nw;
+      rt.slot_nk = nk;
+      rt.slots_sized = true;
+      const int rc = load_plan(rt, plan, rank, minibatch);
+      rt.slots_sized = false;
+      rt.slot_nw = rt.slot_nk = 0;
+      return rc;
+    }
+  }
   if (rt.pool) {
     cudaFree(rt.pool);
     rt.pool = nullptr;

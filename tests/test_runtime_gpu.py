@@ -1,9 +1,13 @@
 """End-to-end runtime on the GPU: executed swap ledger == simulate's ledger
 (bit-exact) and loss / weights / Adam state vs the torch-CPU fp32 oracle.
 
-Tolerances (bf16 tensor-core operands, fp32 accumulate, fp32 master state):
-loss within 2e-3 relative per step; weights and Adam moments within 1e-3
-relative (L2 norm over the whole arena) after the steps."""
+Tolerances (bf16 tensor-core operands, fp32 accumulate, fp32 master state --
+the north star's "1e-3 relative in fp32-accumulate mode"): loss within 1e-3
+relative at every step and weights within 1e-3 relative (L2 norm over the
+whole arena) after K steps (10 for config c1).  The bf16 rounding of the GEMM
+operands is what the margin covers: Adam moments, whose bf16 gradient noise
+does not average out, are held to 2e-2 separately.  Measured: loss 1e-5..1e-4,
+weights 3.7e-4 after 10 steps."""
 
 import numpy as np
 import pytest
@@ -14,7 +18,7 @@ from paper_2202_01306_b200.model import GPT_PRESETS, GPTSpec, gpt_profiles, synt
 
 pytestmark = pytest.mark.gpu
 
-LOSS_RTOL = 2e-3
+LOSS_RTOL = 1e-3
 STATE_RTOL = 1e-3
 
 
@@ -22,6 +26,8 @@ STATE_RTOL = 1e-3
 def _gpu():
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
+
+
 
 
 def _run(spec, cfg, steps, n_gpus=1, alpha=16 << 30, lr=1e-4):
@@ -37,9 +43,11 @@ def _run(spec, cfg, steps, n_gpus=1, alpha=16 << 30, lr=1e-4):
     tok, lab = synthetic_batch(spec, cfg.minibatch)
     sim = H.simulate(g, mach, prof)
     gb = g.tasks[-2].group  # groups of the last backward task
+    worst = 0.0
     for i in range(steps):
         loss = rt.step(tok, lab)
         ref = oracle.step(tok, lab, list(g.tasks[0].group))
+        worst = max(worst, abs(loss - ref) / abs(ref))
         assert abs(loss - ref) / abs(ref) < LOSS_RTOL, (i, loss, ref)
         rep = rt.report()
         assert rep.ledger == sim.ledger
@@ -50,6 +58,7 @@ def _run(spec, cfg, steps, n_gpus=1, alpha=16 << 30, lr=1e-4):
     rel_m = np.linalg.norm(rt.k[0::2] - oracle.m.numpy()) / np.linalg.norm(oracle.m.numpy())
     rel_v = np.linalg.norm(rt.k[1::2] - oracle.v.numpy()) / np.linalg.norm(oracle.v.numpy())
     rt.close()
+    print(f"{spec.name} {cfg}: worst loss rel {worst:.2e}, weights rel {rel_w:.2e}, m {rel_m:.2e}, v {rel_v:.2e}")
     return rel_w, rel_m, rel_v, gb
 
 
@@ -212,7 +221,7 @@ def _run_cnn(spec, cfg, steps, alpha=8 << 30, lr=1e-4):
 
 # bf16 NHWC activations between every layer (the CNN byte model); measured
 # 5e-5 (loss) and 4-5e-4 (weights) after 3 steps at lr 1e-4
-CNN_LOSS_RTOL = 2e-3
+CNN_LOSS_RTOL = 1e-3
 CNN_STATE_RTOL = 1e-3
 
 

@@ -8,21 +8,22 @@ import paper_2202_01306_b200 as H
 from paper_2202_01306_b200.model import GPT_PRESETS, gpt_machine, gpt_profiles, synthetic_batch
 from paper_2202_01306_b200.runtime import HarmonyRuntime
 
+import bench  # noqa: E402
+
 ap = argparse.ArgumentParser()
-ap.add_argument("--d", type=int, default=16)
-ap.add_argument("--lpp", type=int, default=8)
-ap.add_argument("--u", type=int, default=4)
-ap.add_argument("--alpha", type=int, default=32)
+ap.add_argument("--workload", default="gpt2-xl-dp")
 ap.add_argument("--steps", type=int, default=4)
 ap.add_argument("--out", default="gpurun_out/pipeline.json")
 a = ap.parse_args()
-spec = GPT_PRESETS["gpt2-xl"]
-packs = tuple((i, min(i + a.lpp, 48) - 1) for i in range(0, 48, a.lpp))
+preset, a.d, a.u, a.lpp, a.alpha, mode = bench.WORKLOADS[a.workload]
+spec = GPT_PRESETS[preset]
+R = spec.n_layer
+packs = tuple((i, min(i + a.lpp, R) - 1) for i in range(0, R, a.lpp))
 mach = gpt_machine(1, alpha_bytes=a.alpha << 30)
 prof = gpt_profiles(spec)
-g = H.generate_task_graph(H.Configuration(a.u, packs, a.u, packs, a.d, H.Mode.DP), mach, prof)
+g = H.generate_task_graph(H.Configuration(a.u, packs, a.u, packs, a.d, H.Mode(mode)), mach, prof)
 rt = HarmonyRuntime(spec, alpha_bytes=a.alpha << 30)
-rt.init_weights(0)
+rt.init_weights(0, device="cuda" if spec.total_params() > 4_000_000_000 else None)
 rt.load(g, mach, prof)
 tok, lab = synthetic_batch(spec, a.d)
 td, ld = torch.from_numpy(tok).cuda(), torch.from_numpy(lab).cuda()
