@@ -156,7 +156,7 @@ def _gemm_groups(launches, top=8):
     """GEMM launches of the profiled iteration grouped by FLOPs per launch
     (one group per (M, N, K) product): where the GEMM time goes."""
     groups = {}
-    for cls, fl, _by, ms in launches:
+    for cls, fl, _by, ms, _span in launches:
         if int(cls) != 0:
             continue
         g = groups.setdefault(round(fl / 1e9, 3), [0, 0.0])
@@ -166,6 +166,18 @@ def _gemm_groups(launches, top=8):
              "tflops": round(k * n / t, 1) if t else 0.0} for k, (n, t) in groups.items()]
     rows.sort(key=lambda r: -r["ms_total"])
     return rows[:top]
+
+
+def _ncu_traffic() -> dict:
+    """DRAM traffic of the dominant kernel from the committed `ncu --set full`
+    capture (profiles/r01_gemm_ncu_summary.json, made by tools/ncu_summary.py)."""
+    p = os.path.join(ROOT, "profiles", "r01_gemm_ncu_summary.json")
+    if not os.path.exists(p):
+        return {}
+    d = json.load(open(p))
+    return {"traffic": d["dram_bytes_per_launch_mean"],
+            "traffic_how": f"dram__bytes_read.sum + dram__bytes_write.sum per launch, mean of {d['launches']} "
+                           f"in-step GEMM launches of one ncu --set full capture ({d['source']})"}
 
 
 def step_flops(graph, spec) -> int:
@@ -345,7 +357,10 @@ def run_native(args) -> None:
     rt.set_profiling(True)  # reset stats
     rt.step(tok_d, lab_d)
     kstats = rt.kernel_stats()
-    gemm_groups = _gemm_groups(rt.kernel_launches())
+    kl = rt.kernel_launches()
+    gemm_groups = _gemm_groups(kl)
+    gk = kl[(kl[:, 0] == 0) & (kl[:, 4] > 0)]
+    gemm_span_tflops = float(gk[:, 1].sum() / (gk[:, 4].sum() / 1e3) / 1e12) if len(gk) else 0.0
     prof_iter_ns = rt.counters()["iteration_ns"]
     rt.set_profiling(False)
     t_total = _max_over_ranks(t_dev, world)
@@ -405,7 +420,13 @@ def run_native(args) -> None:
                      "kernel": "hm::gemm::gemm_kernel (tcgen05)", "launches_per_step": g["launches"],
                      "share_of_step": share.get("gemm"),
                      "how": "per-launch CUDA events (graph event nodes) in one profiled iteration after the timed steps; "
-                            "algorithmic 2MNK per launch"},
+                            "algorithmic 2MNK per launch",
+                     "achieved_device_clock": round(gemm_span_tflops, 1),
+                     "frac_device_clock": round(gemm_span_tflops / pk["bf16"], 4),
+                     "device_clock_how": "same launches timed by the kernel itself: first CTA start (after "
+                                         "griddepcontrol.wait) to last CTA end on %globaltimer; the event pair "
+                                         "around each launch also times the graph's event nodes and loses PDL overlap",
+                     **(_ncu_traffic() if args.workload == "gpt2-xl-dp" else {})},
         "kernel_shares": share,
         "gemm_by_gflop": gemm_groups,
         "stream_busy_frac": util,

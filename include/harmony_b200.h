@@ -227,8 +227,10 @@ int hm_runtime_set_profiling(hm_runtime *rt, int32_t enable);
  * bytes, launches}: 0 GEMM, 1 attention fwd, 2 attention bwd, 3 LayerNorm,
  * 4 cross-entropy, 5 Adam, 6 other (cast, embedding, bias grad). */
 int hm_runtime_kernel_stats(const hm_runtime *rt, double *out, int32_t cap);
-/* Per-launch records of the last profiled iteration, {class, flops, bytes, ms}
- * each; returns the number of launches (copies at most cap). */
+/* Per-launch records of the last profiled iteration, {class, flops, bytes,
+ * event ms, device-clock ms} each (the device-clock span -- first CTA start
+ * to last CTA end on %globaltimer -- is recorded by GEMM launches only);
+ * returns the number of launches (copies at most cap). */
 int hm_runtime_kernel_launches(const hm_runtime *rt, double *out, int32_t cap);
 void hm_runtime_free(hm_runtime *rt);
 

@@ -45,6 +45,7 @@ struct Args {
   // implicit-GEMM 3x3 convolution (MODE 1-3): image H x W of the im2col
   // operand, its 64-channel blocks, and (dgrad) the output-channel blocks
   int32_t cv_h, cv_w, cv_cb, cv_cbo;
+  unsigned long long *span;  // profiling: {~first start, last end} globaltimer (null = off)
   void *d;
   int64_t ldd;
   const float *bias;
@@ -290,6 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // alloc, descriptor prefetch) overlapped the previous kernel's tail;
       // global operands are read only after it has fully completed
       griddep_wait();
+      if (args.span) atomicMax(&args.span[0], ~globaltimer());
       int stage = 0;
       uint32_t phase = 0;
       for (int t = unit0; t < ntiles; t += unit_step) {
@@ -498,6 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     else
       tmem_dealloc<C::kTmemCols>(tmem_base);
   }
+  if (args.span && threadIdx.x == 0) atomicMax(&args.span[1], globaltimer());
 }
 
 // ---------------------------------------------------------------------------
@@ -636,6 +639,8 @@ static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMa
   const bool f32 = a.epi == HM_EPI_STORE_F32 || a.epi == HM_EPI_ACC_F32 || a.epi == HM_EPI_RESID_F32;
   const double io = (double)a.M * a.N * (f32 ? 4 : 2) * (a.epi == HM_EPI_ACC_F32 || a.epi >= HM_EPI_RESID_F32 ? 2 : 1);
   ProfScope ps(KC_GEMM, s, 2.0 * a.M * a.N * a.K, 2.0 * ((double)a.M * a.K + (double)a.N * a.K) + io);
+  Args args = a;
+  args.span = profiler() ? profiler()->span_slot() : nullptr;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
@@ -652,7 +657,7 @@ static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMa
   attrs[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cfg.attrs = attrs;
   cfg.numAttrs = CG > 1 ? 2 : 1;
-  cudaError_t le = cudaLaunchKernelEx(&cfg, kern, ta, tb, td, tx, a);
+  cudaError_t le = cudaLaunchKernelEx(&cfg, kern, ta, tb, td, tx, args);
   if (le != cudaSuccess) return fail(HM_ERR_DEVICE, std::string("gemm launch: ") + cudaGetErrorString(le));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(HM_ERR_DEVICE, std::string("gemm launch: ") + cudaGetErrorString(e));

@@ -28,6 +28,9 @@ enum KernelClass { KC_GEMM = 0, KC_ATTN_FWD, KC_ATTN_BWD, KC_LAYERNORM, KC_XENT,
 struct KernelProfiler {
   virtual void begin(int cls, cudaStream_t s) = 0;
   virtual void end(int cls, cudaStream_t s, double flops, double bytes) = 0;
+  // device {~first CTA start, last CTA end} globaltimer pair for the launch just
+  // begun (atomicMax targets, zeroed before the profiled iteration), or null
+  virtual unsigned long long *span_slot() { return nullptr; }
   virtual ~KernelProfiler() = default;
 };
 KernelProfiler *&profiler();

@@ -147,12 +147,24 @@ struct RtProfiler : KernelProfiler {
         return;
       }
   }
+  // device globaltimer spans, one {~start, end} pair per record
+  static constexpr size_t kSpanCap = 1 << 15;
+  unsigned long long *spans = nullptr;
+  unsigned long long *span_slot() override {
+    if (!spans && cudaMalloc(&spans, kSpanCap * 2 * sizeof(unsigned long long)) != cudaSuccess) spans = nullptr;
+    if (!spans || recs.empty() || recs.size() > kSpanCap) return nullptr;
+    return spans + 2 * (recs.size() - 1);
+  }
+  cudaError_t clear_spans(cudaStream_t s) {
+    return spans ? cudaMemsetAsync(spans, 0, kSpanCap * 2 * sizeof(unsigned long long), s) : cudaSuccess;
+  }
   void reset() {
     recs.clear();
     used = 0;
   }
   ~RtProfiler() override {
     for (auto e : pool) cudaEventDestroy(e);
+    if (spans) cudaFree(spans);
   }
 };
 
@@ -162,7 +174,7 @@ struct hm_runtime {
   bool profiling = false;
   hm::RtProfiler prof;
   double kstats[hm::KC_COUNT][4] = {{0}};  // ms, flops, bytes, launches (accumulated)
-  std::vector<double> klaunch;              // last profiled iteration: (class, flops, bytes, ms) per launch
+  std::vector<double> klaunch;  // last profiled iteration: (class, flops, bytes, event ms, device-clock ms) per launch
   int device = 0;
   hm_model m{};
   int family = HM_FAMILY_GPT;          // GPT / BERT transformer chain or deep CNN
@@ -1518,6 +1530,7 @@ static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *l
       rt.graph_bytes[gi][2] = coll;
       launch_counter().fetch_sub(rt.graph_launches[gi]);  // counted when replayed
     }
+    if (gi == 1) HM_CUDA(rt.prof.clear_spans(sc));
     HM_CUDA(cudaGraphLaunch(rt.graph_exec[gi], sc));
     count_launch(rt.graph_launches[gi]);
     h2d = rt.graph_bytes[gi][0];
@@ -1525,6 +1538,7 @@ static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *l
     coll = rt.graph_bytes[gi][2];
   } else {
     rt.prof.reset();
+    if (rt.profiling) HM_CUDA(rt.prof.clear_spans(sc));
     profiler() = rt.profiling ? &rt.prof : nullptr;
     int rc = enqueue_body(rt, false, false, h2d, d2h, coll);
     profiler() = nullptr;
@@ -1556,11 +1570,21 @@ static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *l
   HM_CUDA(cudaEventElapsedTime(&it_ms, rt.ev_iter0, rt.ev_iter1));
   if (rt.profiling) {
     rt.klaunch.clear();
-    for (auto &p : rt.prof.recs) {
+    std::vector<unsigned long long> spans;
+    if (rt.prof.spans) {
+      spans.resize(std::min(rt.prof.recs.size(), RtProfiler::kSpanCap) * 2);
+      HM_CUDA(cudaMemcpy(spans.data(), rt.prof.spans, spans.size() * sizeof(unsigned long long),
+                         cudaMemcpyDeviceToHost));
+    }
+    for (size_t i = 0; i < rt.prof.recs.size(); ++i) {
+      auto &p = rt.prof.recs[i];
       if (!p.e1) continue;
       float ms = 0;
       HM_CUDA(cudaEventElapsedTime(&ms, p.e0, p.e1));
-      rt.klaunch.insert(rt.klaunch.end(), {(double)p.cls, p.flops, p.bytes, (double)ms});
+      double span_ms = 0;  // kernel-only device time (GEMM launches record it)
+      if (2 * i + 1 < spans.size() && spans[2 * i] && spans[2 * i + 1])
+        span_ms = (double)(spans[2 * i + 1] - ~spans[2 * i]) * 1e-6;
+      rt.klaunch.insert(rt.klaunch.end(), {(double)p.cls, p.flops, p.bytes, (double)ms, span_ms});
       rt.kstats[p.cls][0] += ms;
       rt.kstats[p.cls][1] += p.flops;
       rt.kstats[p.cls][2] += p.bytes;
@@ -1997,10 +2021,10 @@ int hm_runtime_kernel_stats(const hm_runtime *rt, double *out, int32_t cap) {
 }
 
 int hm_runtime_kernel_launches(const hm_runtime *rt, double *out, int32_t cap) {
-  int n = (int)(rt->klaunch.size() / 4);
+  int n = (int)(rt->klaunch.size() / 5);
   if (out)
     for (int i = 0; i < n && i < cap; ++i)
-      for (int j = 0; j < 4; ++j) out[4 * i + j] = rt->klaunch[4 * i + j];
+      for (int j = 0; j < 5; ++j) out[5 * i + j] = rt->klaunch[5 * i + j];
   return n;
 }
 

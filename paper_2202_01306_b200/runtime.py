@@ -332,9 +332,11 @@ class HarmonyRuntime:
                     "launches": int(buf[4 * i + 3])} for i, c in enumerate(self.KERNEL_CLASSES)}
 
     def kernel_launches(self) -> np.ndarray:
-        """[n, 4] (class, flops, bytes, ms) per launch of the last profiled iteration."""
+        """[n, 5] (class, flops, bytes, event ms, device-clock ms) per launch of
+        the last profiled iteration; the device-clock span (first CTA start to
+        last CTA end, %globaltimer) is recorded by the GEMM launches, 0 elsewhere."""
         n = self.lib.hm_runtime_kernel_launches(self.handle, None, 0)
-        out = np.zeros((max(n, 0), 4), dtype=np.float64)
+        out = np.zeros((max(n, 0), 5), dtype=np.float64)
         if n > 0:
             self.lib.hm_runtime_kernel_launches(self.handle, out.ctypes.data_as(C.POINTER(C.c_double)), n)
         return out
