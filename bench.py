@@ -41,7 +41,7 @@ WORKLOADS = {
     # north-star target shape: W + Adam state (184 GB) > one GPU's HBM
     "gpt-15b-dp": ("gpt-15b", 24, 4, 3, 170, "dp"),
     # config c5: deep-CNN packs (128 residual blocks at 56x56 / 28x28, implicit-GEMM convs)
-    "resnet-dp": ("resnet-bench", 64, 16, 16, 8, "dp"),
+    "resnet-dp": ("resnet-bench", 64, 32, 16, 12, "dp"),
 }
 
 

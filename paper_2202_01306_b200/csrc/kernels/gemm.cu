@@ -597,7 +597,7 @@ static TileCfg pick_tile(int64_t M, int64_t N, int64_t K, int epi) {
       const double t_kb = bn / 256.0 / eff;
       const int64_t tiles = ((M + BM * cg - 1) / (BM * cg)) * ((N + bn - 1) / bn);
       const int64_t slots = sms / cg;
-      for (int s = 1; s <= (epi == HM_EPI_ACC_F32 ? 8 : 1); ++s) {
+      for (int s = 1; s <= (epi == HM_EPI_ACC_F32 ? 32 : 1); ++s) {
         if (env_s && s != env_s) continue;
         if (s > 1 && num_k / s < 8) break;
         const double waves = (double)((tiles * s + slots - 1) / slots);
@@ -867,8 +867,8 @@ extern "C" int hm_k_conv_wgrad(const void *dy, const void *x, float *dw, int32_t
 }
 
 extern "C" int hm_k_gemm_set_tile(int32_t bn, int32_t cta_pair, int32_t splits) {
-  if ((bn && bn != 128 && bn != 256) || (cta_pair && cta_pair != 1 && cta_pair != 2) || splits < 0 || splits > 8)
-    return hm::fail(HM_ERR_VALIDATION, "gemm tile override: bn in {0,128,256}, cta_pair in {0,1,2}, splits in [0,8]");
+  if ((bn && bn != 128 && bn != 256) || (cta_pair && cta_pair != 1 && cta_pair != 2) || splits < 0 || splits > 32)
+    return hm::fail(HM_ERR_VALIDATION, "gemm tile override: bn in {0,128,256}, cta_pair in {0,1,2}, splits in [0,32]");
   hm::gemm::g_force_bn = bn;
   hm::gemm::g_force_cg = cta_pair;
   hm::gemm::g_force_s = splits;
