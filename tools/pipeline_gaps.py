@@ -16,17 +16,23 @@ ap.add_argument("--steps", type=int, default=4)
 ap.add_argument("--out", default="gpurun_out/pipeline.json")
 a = ap.parse_args()
 preset, a.d, a.u, a.lpp, a.alpha, mode = bench.WORKLOADS[a.workload]
-spec = GPT_PRESETS[preset]
+from paper_2202_01306_b200.cnn import CNN_PRESETS, cnn_profiles, synthetic_images  # noqa: E402
+is_cnn = preset in CNN_PRESETS
+spec = CNN_PRESETS[preset] if is_cnn else GPT_PRESETS[preset]
 R = spec.n_layer
 packs = tuple((i, min(i + a.lpp, R) - 1) for i in range(0, R, a.lpp))
 mach = gpt_machine(1, alpha_bytes=a.alpha << 30)
-prof = gpt_profiles(spec)
+prof = cnn_profiles(spec) if is_cnn else gpt_profiles(spec)
 g = H.generate_task_graph(H.Configuration(a.u, packs, a.u, packs, a.d, H.Mode(mode)), mach, prof)
 rt = HarmonyRuntime(spec, alpha_bytes=a.alpha << 30)
-rt.init_weights(0, device="cuda" if spec.total_params() > 4_000_000_000 else None)
+rt.init_weights(0, device="cuda" if spec.total_params() > 4_000_000_000 and not is_cnn else None)
 rt.load(g, mach, prof)
-tok, lab = synthetic_batch(spec, a.d)
-td, ld = torch.from_numpy(tok).cuda(), torch.from_numpy(lab).cuda()
+if is_cnn:
+    img, lab = synthetic_images(spec, a.d)
+    td, ld = img.cuda(), lab.cuda()
+else:
+    tok, lab = synthetic_batch(spec, a.d)
+    td, ld = torch.from_numpy(tok).cuda(), torch.from_numpy(lab).cuda()
 rt.run_steps(2, td, ld)
 _, secs = rt.run_steps(a.steps, td, ld)
 c = rt.counters()
