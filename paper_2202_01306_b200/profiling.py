@@ -18,16 +18,27 @@ Memory, activation and state sizes are the runtime's real byte layout
 
 from __future__ import annotations
 
+from .cnn import CNNSpec, cnn_profiles, synthetic_images
 from .core import Configuration, MachineModel, Mode
 from .model import GPTSpec, gpt_profiles, synthetic_batch
 from .profiler import ProfileSample, ProfileSet, fit_profiles, sample_points
 from .taskgraph import TaskType, generate_task_graph
 
 
-def samples_from_trace(spec: GPTSpec, graph, trace, u: int) -> list[ProfileSample]:
+def shape_profiles(spec: GPTSpec | CNNSpec, u_max: int = 64) -> ProfileSet:
+    """Byte-exact ProfileSet of either model family (times FLOP-derived)."""
+    return cnn_profiles(spec, u_max=u_max) if isinstance(spec, CNNSpec) else gpt_profiles(spec, u_max=u_max)
+
+
+def synthetic_inputs(spec: GPTSpec | CNNSpec, samples: int):
+    """Synthetic minibatch of either family (tokens / images, labels)."""
+    return synthetic_images(spec, samples) if isinstance(spec, CNNSpec) else synthetic_batch(spec, samples)
+
+
+def samples_from_trace(spec: GPTSpec | CNNSpec, graph, trace, u: int) -> list[ProfileSample]:
     """ProfileSamples of one single-layer-pack run (trace = measured
     compute TraceEvents of the report)."""
-    shapes = gpt_profiles(spec)
+    shapes = shape_profiles(spec)
     dur: dict[int, list[int]] = {}
     for e in trace:
         if e.kind == "compute":
@@ -56,7 +67,7 @@ def samples_from_trace(spec: GPTSpec, graph, trace, u: int) -> list[ProfileSampl
     return out
 
 
-def profile_gpt(spec: GPTSpec, u_values=None, u_max: int = 8, stride: int = 4, alpha_bytes: int = 64 << 30,
+def profile_gpt(spec: GPTSpec | CNNSpec, u_values=None, u_max: int = 8, stride: int = 4, alpha_bytes: int = 64 << 30,
                 device: int = 0, warmup: int = 1) -> tuple[ProfileSet, list[ProfileSample]]:
     """Measure and fit a ProfileSet on this GPU (sample points 1, stride
     multiples and u_max, as the reference's profiler, `profiler.py:421-427`)."""
@@ -68,14 +79,17 @@ def profile_gpt(spec: GPTSpec, u_values=None, u_max: int = 8, stride: int = 4, a
     try:
         rt.init_weights(0)
         mach = MachineModel(gpu_count=1, gpu_mem_capacity=alpha_bytes, pcie_bandwidth=55_000_000_000)
-        prof0 = gpt_profiles(spec, u_max=max(us))
+        prof0 = shape_profiles(spec, u_max=max(us))
         for u in us:
             g = generate_task_graph(Configuration(u, packs, u, packs, u, Mode.DP), mach, prof0)
             rt.load(g, mach, prof0)
-            tok, lab = synthetic_batch(spec, u)
+            tok, lab = synthetic_inputs(spec, u)
             for _ in range(warmup + 1):
                 rt.step(tok, lab)
             samples += samples_from_trace(spec, g, rt.report().trace, u)
     finally:
         rt.close()
     return fit_profiles(samples, stride=stride), samples
+
+
+profile_model = profile_gpt  # either family (GPTSpec or CNNSpec)
