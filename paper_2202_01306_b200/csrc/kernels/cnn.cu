@@ -6,6 +6,7 @@
 #include <cuda_bf16.h>
 
 #include "../runtime/common.hpp"
+#include "pdl.cuh"
 
 namespace hm {
 namespace cnn {
@@ -49,6 +50,7 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
 // dz = dy * (y > 0)
 __global__ void relu_bwd_kernel(const uint4 *__restrict__ dy, const uint4 *__restrict__ y, uint4 *__restrict__ dz,
                                 int64_t n8) {
+  pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
     float g[8], v[8];
     unpack8(dy[i], g);
@@ -61,6 +63,7 @@ __global__ void relu_bwd_kernel(const uint4 *__restrict__ dy, const uint4 *__res
 
 // y[n, h/2, w/2, c] = mean of the 2x2 window of a[n, h, w, c]; one thread per 8 channels of one output pixel
 __global__ void pool2_fwd_kernel(const bf16 *__restrict__ a, bf16 *__restrict__ y, int n, int h, int w, int c) {
+  pdl_wait();
   const int ho = h / 2, wo = w / 2, c8 = c / 8;
   const int64_t total = (int64_t)n * ho * wo * c8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -91,6 +94,7 @@ __global__ void pool2_fwd_kernel(const bf16 *__restrict__ a, bf16 *__restrict__ 
 // the ReLU mask of the convolution that produced a
 __global__ void pool2_relu_bwd_kernel(const bf16 *__restrict__ dy, const bf16 *__restrict__ a, bf16 *__restrict__ dz,
                                       int n, int h, int w, int c) {
+  pdl_wait();
   const int ho = h / 2, wo = w / 2, c8 = c / 8;
   const int64_t total = (int64_t)n * h * w * c8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -111,6 +115,7 @@ __global__ void pool2_relu_bwd_kernel(const bf16 *__restrict__ dy, const bf16 *_
 
 // pooled[b, c] = mean over p of x[b, p, c]; block per (sample, 8*256-channel slab), fp32 sums
 __global__ void gap_fwd_kernel(const bf16 *__restrict__ x, bf16 *__restrict__ pooled, int P, int c) {
+  pdl_wait();
   const int b = blockIdx.y;
   const int c8 = blockIdx.x * blockDim.x + threadIdx.x;
   if (c8 * 8 >= c) return;
@@ -130,6 +135,7 @@ __global__ void gap_fwd_kernel(const bf16 *__restrict__ x, bf16 *__restrict__ po
 
 // dx[b, p, c] = dpooled[b, c] / P
 __global__ void gap_bwd_kernel(const float *__restrict__ dp, bf16 *__restrict__ dx, int nb, int P, int c) {
+  pdl_wait();
   const int c8n = c / 8;
   const int64_t total = (int64_t)nb * P * c8n;
   const float inv = 1.f / (float)P;
@@ -146,8 +152,8 @@ __global__ void gap_bwd_kernel(const float *__restrict__ dp, bf16 *__restrict__ 
 int relu_bwd(const void *dy, const void *y, void *dz, int64_t n, cudaStream_t s) {
   if (n % 8) return fail(HM_ERR_VALIDATION, "relu_bwd: n must be a multiple of 8");
   ProfScope ps(KC_MISC, s, 0, 6.0 * n);
-  relu_bwd_kernel<<<grid_for(n / 8), 256, 0, s>>>(static_cast<const uint4 *>(dy), static_cast<const uint4 *>(y),
-                                                 static_cast<uint4 *>(dz), n / 8);
+  HM_CUDA(launch_pdl(relu_bwd_kernel, dim3(grid_for(n / 8)), dim3(256), 0, s, static_cast<const uint4 *>(dy), static_cast<const uint4 *>(y),
+                                                 static_cast<uint4 *>(dz), n / 8));
   count_launch();
   HM_CUDA(cudaGetLastError());
   return HM_OK;
@@ -156,8 +162,8 @@ int relu_bwd(const void *dy, const void *y, void *dz, int64_t n, cudaStream_t s)
 int pool2_fwd(const void *a, void *y, int n, int h, int w, int c, cudaStream_t s) {
   if (h % 2 || w % 2 || c % 8) return fail(HM_ERR_VALIDATION, "pool2: even h, w and c % 8 == 0");
   ProfScope ps(KC_MISC, s, 0, 2.5 * n * h * w * (double)c);
-  pool2_fwd_kernel<<<grid_for((int64_t)n * h * w * c / 32), 256, 0, s>>>(static_cast<const bf16 *>(a),
-                                                                         static_cast<bf16 *>(y), n, h, w, c);
+  HM_CUDA(launch_pdl(pool2_fwd_kernel, dim3(grid_for((int64_t)n * h * w * c / 32)), dim3(256), 0, s, static_cast<const bf16 *>(a),
+                                                                         static_cast<bf16 *>(y), n, h, w, c));
   count_launch();
   HM_CUDA(cudaGetLastError());
   return HM_OK;
@@ -166,8 +172,8 @@ int pool2_fwd(const void *a, void *y, int n, int h, int w, int c, cudaStream_t s
 int pool2_relu_bwd(const void *dy, const void *a, void *dz, int n, int h, int w, int c, cudaStream_t s) {
   if (h % 2 || w % 2 || c % 8) return fail(HM_ERR_VALIDATION, "pool2: even h, w and c % 8 == 0");
   ProfScope ps(KC_MISC, s, 0, 4.5 * n * h * w * (double)c);
-  pool2_relu_bwd_kernel<<<grid_for((int64_t)n * h * w * c / 8), 256, 0, s>>>(
-      static_cast<const bf16 *>(dy), static_cast<const bf16 *>(a), static_cast<bf16 *>(dz), n, h, w, c);
+  HM_CUDA(launch_pdl(pool2_relu_bwd_kernel, dim3(grid_for((int64_t)n * h * w * c / 8)), dim3(256), 0, s, 
+      static_cast<const bf16 *>(dy), static_cast<const bf16 *>(a), static_cast<bf16 *>(dz), n, h, w, c));
   count_launch();
   HM_CUDA(cudaGetLastError());
   return HM_OK;
@@ -177,8 +183,8 @@ int gap_fwd(const void *x, void *pooled, int nb, int P, int c, cudaStream_t s) {
   if (c % 8) return fail(HM_ERR_VALIDATION, "gap: c % 8 == 0");
   ProfScope ps(KC_MISC, s, 0, 2.0 * nb * (double)P * c);
   const int c8 = c / 8, threads = c8 < 128 ? c8 : 128;
-  gap_fwd_kernel<<<dim3((c8 + threads - 1) / threads, nb), threads, 0, s>>>(static_cast<const bf16 *>(x),
-                                                                          static_cast<bf16 *>(pooled), P, c);
+  HM_CUDA(launch_pdl(gap_fwd_kernel, dim3(dim3((c8 + threads - 1) / threads, nb)), dim3(threads), 0, s, static_cast<const bf16 *>(x),
+                                                                          static_cast<bf16 *>(pooled), P, c));
   count_launch();
   HM_CUDA(cudaGetLastError());
   return HM_OK;
@@ -187,7 +193,7 @@ int gap_fwd(const void *x, void *pooled, int nb, int P, int c, cudaStream_t s) {
 int gap_bwd(const float *dp, void *dx, int nb, int P, int c, cudaStream_t s) {
   if (c % 8) return fail(HM_ERR_VALIDATION, "gap: c % 8 == 0");
   ProfScope ps(KC_MISC, s, 0, 2.0 * nb * (double)P * c);
-  gap_bwd_kernel<<<grid_for((int64_t)nb * P * c / 8), 256, 0, s>>>(dp, static_cast<bf16 *>(dx), nb, P, c);
+  HM_CUDA(launch_pdl(gap_bwd_kernel, dim3(grid_for((int64_t)nb * P * c / 8)), dim3(256), 0, s, dp, static_cast<bf16 *>(dx), nb, P, c));
   count_launch();
   HM_CUDA(cudaGetLastError());
   return HM_OK;

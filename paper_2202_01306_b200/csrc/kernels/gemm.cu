@@ -362,6 +362,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      // every CTA must trigger (or exit) before the dependent grid may launch:
+      // the pair follower has no MMA thread, so its producer signals here
+      if (CG == 2 && !leader) griddep_launch_dependents();
     }
   } else if (warp == 1) {
     if (lane == 0 && leader) {

@@ -7,6 +7,7 @@
 #include <cstdlib>
 
 #include "../runtime/common.hpp"
+#include "pdl.cuh"
 
 namespace hm {
 namespace layers {
@@ -35,6 +36,7 @@ static int sm_count() {
 
 // ---- fp32 -> bf16 cast (pack weights after swap-in; dY before GEMMs) --------
 __global__ void cast_kernel(const float4 *__restrict__ src, uint2 *__restrict__ dst, int64_t n4) {
+  pdl_wait();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     float4 v = src[i];
     __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
@@ -42,6 +44,7 @@ __global__ void cast_kernel(const float4 *__restrict__ src, uint2 *__restrict__ 
   }
 }
 __global__ void cast_tail(const float *src, __nv_bfloat16 *dst, int64_t begin, int64_t n) {
+  pdl_wait();
   int64_t i = begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) dst[i] = __float2bfloat16_rn(src[i]);
 }
@@ -53,12 +56,12 @@ int cast_f32_bf16(const float *src, void *dst, int64_t n, cudaStream_t s) {
   if (n4) {
     int64_t blocks = (n4 + 255) / 256;
     if (blocks > (int64_t)sm_count() * 16) blocks = (int64_t)sm_count() * 16;
-    cast_kernel<<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<const float4 *>(src), reinterpret_cast<uint2 *>(dst), n4);
+    HM_CUDA(launch_pdl(cast_kernel, dim3((unsigned)blocks), dim3(256), 0, s, reinterpret_cast<const float4 *>(src), reinterpret_cast<uint2 *>(dst), n4));
     count_launch();
   }
   if (n4 * 4 < n) {
     const int64_t rest = n - n4 * 4;
-    cast_tail<<<(unsigned)((rest + 255) / 256), 256, 0, s>>>(src, static_cast<__nv_bfloat16 *>(dst), n4 * 4, n);
+    HM_CUDA(launch_pdl(cast_tail, dim3((unsigned)((rest + 255) / 256)), dim3(256), 0, s, src, static_cast<__nv_bfloat16 *>(dst), n4 * 4, n));
     count_launch();
   }
   HM_CUDA(cudaGetLastError());
@@ -68,6 +71,7 @@ int cast_f32_bf16(const float *src, void *dst, int64_t n, cudaStream_t s) {
 // ---- embedding -----------------------------------------------------------------
 __global__ void embed_fwd_kernel(const int32_t *__restrict__ tok, const float *__restrict__ wte,
                                  const float *__restrict__ wpe, float *__restrict__ out, int64_t rows, int S, int d) {
+  pdl_wait();
   const int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
@@ -82,6 +86,7 @@ __global__ void embed_fwd_kernel(const int32_t *__restrict__ tok, const float *_
 // dwte[tok] += dx (atomic; tokens repeat), one warp per row
 __global__ void embed_bwd_tok_kernel(const int32_t *__restrict__ tok, const float *__restrict__ dx,
                                      float *__restrict__ dwte, int64_t rows, int d) {
+  pdl_wait();
   const int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
@@ -91,6 +96,7 @@ __global__ void embed_bwd_tok_kernel(const int32_t *__restrict__ tok, const floa
 }
 // dwpe[p] += sum_b dx[b*S + p] (deterministic, no atomics)
 __global__ void embed_bwd_pos_kernel(const float *__restrict__ dx, float *__restrict__ dwpe, int B, int S, int d) {
+  pdl_wait();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= (int64_t)S * d) return;
   float acc = 0.f;
@@ -101,7 +107,7 @@ __global__ void embed_bwd_pos_kernel(const float *__restrict__ dx, float *__rest
 int embed_fwd(const int32_t *tok, const float *wte, const float *wpe, float *out, int B, int S, int d, cudaStream_t s) {
   const int64_t rows = (int64_t)B * S;
   ProfScope ps(KC_MISC, s, 0, 12.0 * rows * d);
-  embed_fwd_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, s>>>(tok, wte, wpe, out, rows, S, d);
+  HM_CUDA(launch_pdl(embed_fwd_kernel, dim3((unsigned)((rows * 32 + 255) / 256)), dim3(256), 0, s, tok, wte, wpe, out, rows, S, d));
   count_launch();
   HM_CUDA(cudaGetLastError());
   return HM_OK;
@@ -109,7 +115,7 @@ int embed_fwd(const int32_t *tok, const float *wte, const float *wpe, float *out
 int embed_bwd(const int32_t *tok, const float *dx, float *dwte, float *dwpe, int B, int S, int d, cudaStream_t s) {
   const int64_t rows = (int64_t)B * S;
   ProfScope ps(KC_MISC, s, 0, 16.0 * rows * d);
-  embed_bwd_tok_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, s>>>(tok, dx, dwte, rows, d);
+  HM_CUDA(launch_pdl(embed_bwd_tok_kernel, dim3((unsigned)((rows * 32 + 255) / 256)), dim3(256), 0, s, tok, dx, dwte, rows, d));
   embed_bwd_pos_kernel<<<(unsigned)(((int64_t)S * d + 255) / 256), 256, 0, s>>>(dx, dwpe, B, S, d);
   count_launch(2);
   HM_CUDA(cudaGetLastError());
@@ -120,6 +126,7 @@ int embed_bwd(const int32_t *tok, const float *dx, float *dwte, float *dwpe, int
 __global__ void ln_fwd_kernel(const float *__restrict__ x, const float *__restrict__ gam, const float *__restrict__ bet,
                               __nv_bfloat16 *__restrict__ y, float *__restrict__ mean, float *__restrict__ rstd,
                               int64_t rows, int d, float eps) {
+  pdl_wait();
   const int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
@@ -156,8 +163,8 @@ int ln_fwd(const float *x, const float *g, const float *b, void *y, float *mean,
            cudaStream_t s) {
   if (d % 4) return fail(HM_ERR_VALIDATION, "layernorm: d must be a multiple of 4");
   ProfScope ps(KC_LAYERNORM, s, 0, 6.0 * rows * d);
-  ln_fwd_kernel<<<(unsigned)((rows * 32 + 255) / 256), 256, 0, s>>>(x, g, b, static_cast<__nv_bfloat16 *>(y), mean,
-                                                                    rstd, rows, d, 1e-5f);
+  HM_CUDA(launch_pdl(ln_fwd_kernel, dim3((unsigned)((rows * 32 + 255) / 256)), dim3(256), 0, s, x, g, b, static_cast<__nv_bfloat16 *>(y), mean,
+                                                                    rstd, rows, d, 1e-5f));
   count_launch();
   HM_CUDA(cudaGetLastError());
   return HM_OK;
@@ -171,6 +178,7 @@ __global__ void ln_bwd_kernel(const float *__restrict__ dy, const float *__restr
                               const float *__restrict__ rstd, const float *__restrict__ gam, const float *resid,
                               float *out, __nv_bfloat16 *__restrict__ out_bf, float *__restrict__ dgam,
                               float *__restrict__ dbet, int64_t rows, int d, int rows_per_block) {
+  pdl_wait();
   extern __shared__ float sacc[];  // [2*d]
   for (int i = threadIdx.x; i < 2 * d; i += blockDim.x) sacc[i] = 0.f;
   __syncthreads();
@@ -366,8 +374,8 @@ int ln_bwd(const float *dy, const float *x, const float *mean, const float *rstd
   int rpb = (int)((rows + blocks - 1) / blocks);
   if (rpb < 8) rpb = 8;
   blocks = (rows + rpb - 1) / rpb;
-  ln_bwd_kernel<<<(unsigned)blocks, 512, smem, s>>>(dy, x, mean, rstd, g, resid, out,
-                                                    static_cast<__nv_bfloat16 *>(out_bf), dg, db, rows, d, rpb);
+  HM_CUDA(launch_pdl(ln_bwd_kernel, dim3((unsigned)blocks), dim3(512), smem, s, dy, x, mean, rstd, g, resid, out,
+                                                    static_cast<__nv_bfloat16 *>(out_bf), dg, db, rows, d, rpb));
   count_launch();
   HM_CUDA(cudaGetLastError());
   return HM_OK;
@@ -378,6 +386,7 @@ int ln_bwd(const float *dy, const float *x, const float *mean, const float *rstd
 // dlogits bf16 [rows, ldl] = (softmax - onehot) * scale, zero in the padding.
 __global__ void ce_kernel(const float *__restrict__ logits, const int32_t *__restrict__ labels, int64_t ldl, int V,
                           __nv_bfloat16 *__restrict__ dlog, double *loss_sum, float scale) {
+  pdl_wait();
   const int64_t r = blockIdx.x;
   const float *row = logits + r * ldl;
   __shared__ float red_m[32], red_s[32];
@@ -437,8 +446,8 @@ __global__ void ce_kernel(const float *__restrict__ logits, const int32_t *__res
 int cross_entropy(const float *logits, const int32_t *labels, int64_t rows, int64_t ldl, int V, void *dlogits,
                   double *loss_sum, float scale, cudaStream_t s) {
   ProfScope ps(KC_XENT, s, 0, 6.0 * rows * ldl);
-  ce_kernel<<<(unsigned)rows, 512, 0, s>>>(logits, labels, ldl, V, static_cast<__nv_bfloat16 *>(dlogits), loss_sum,
-                                            scale);
+  HM_CUDA(launch_pdl(ce_kernel, dim3((unsigned)rows), dim3(512), 0, s, logits, labels, ldl, V, static_cast<__nv_bfloat16 *>(dlogits), loss_sum,
+                                            scale));
   count_launch();
   HM_CUDA(cudaGetLastError());
   return HM_OK;
@@ -448,6 +457,7 @@ int cross_entropy(const float *logits, const int32_t *labels, int64_t rows, int6
 template <typename T>
 __global__ void bias_grad_kernel(const T *__restrict__ dy, float *__restrict__ db, int64_t rows, int n, int64_t ld,
                                  int rows_per_block) {
+  pdl_wait();
   const int col = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
   if (col >= n) return;
   const int64_t r0 = (int64_t)blockIdx.y * rows_per_block;
@@ -478,11 +488,11 @@ int bias_grad(const void *dy, int is_bf16, float *db, int64_t rows, int n, int64
   if (rpb < 32) rpb = 32;
   gy = (rows + rpb - 1) / rpb;
   if (is_bf16)
-    bias_grad_kernel<__nv_bfloat16><<<dim3(gx, (unsigned)gy), threads, 0, s>>>(
-        static_cast<const __nv_bfloat16 *>(dy), db, rows, n, ld, rpb);
+    HM_CUDA(launch_pdl(bias_grad_kernel<__nv_bfloat16>, dim3(dim3(gx, (unsigned)gy)), dim3(threads), 0, s, 
+        static_cast<const __nv_bfloat16 *>(dy), db, rows, n, ld, rpb));
   else
-    bias_grad_kernel<float><<<dim3(gx, (unsigned)gy), threads, 0, s>>>(static_cast<const float *>(dy), db, rows, n,
-                                                                       ld, rpb);
+    HM_CUDA(launch_pdl(bias_grad_kernel<float>, dim3(dim3(gx, (unsigned)gy)), dim3(threads), 0, s, static_cast<const float *>(dy), db, rows, n,
+                                                                       ld, rpb));
   count_launch();
   HM_CUDA(cudaGetLastError());
   return HM_OK;
