@@ -149,9 +149,13 @@ typedef struct hm_runtime hm_runtime;
  * h, w, cin = the layer's input; activations NHWC bf16; channels % 64 == 0
  * (the image enters layer 0 zero-padded to 64 channels); one label per sample. */
 enum { HM_FAMILY_GPT = 0, HM_FAMILY_CNN = 1 };
-enum { HM_CNN_CONV = 0, HM_CNN_DOWN = 1, HM_CNN_RES = 2, HM_CNN_HEAD = 3 };
+enum { HM_CNN_CONV = 0, HM_CNN_DOWN = 1, HM_CNN_RES = 2, HM_CNN_HEAD = 3, HM_CNN_RES2 = 4 };
+/* type 4 res2: relu(conv(x) + bias + skip) with skip = the output of layer
+ * `skip` (a residual block at convolution granularity; the skip edge may cross
+ * pack boundaries and travels through device-resident relay stores). */
 typedef struct {
   int32_t type, cin, cout, h, w;
+  int32_t skip; /* res2: source layer of the skip input; -1 otherwise */
 } hm_cnn_layer;
 typedef struct {
   int32_t n_layer;
@@ -284,6 +288,8 @@ int hm_k_pool2_relu_bwd(const void *dy, const void *a, void *dz, int32_t n, int3
                         void *stream);
 int hm_k_gap_fwd(const void *x, void *pooled, int32_t nb, int32_t P, int32_t c, void *stream);
 int hm_k_gap_bwd(const float *dp, void *dx, int32_t nb, int32_t P, int32_t c, void *stream);
+/* out = a + b (bf16, n % 8 == 0): the skip gradient joining the trunk gradient */
+int hm_k_add_bf16(const void *a, const void *b, void *out, int64_t n, void *stream);
 
 /* Tile configuration the GEMM picks for an (m, n, k, epilogue) problem:
  * bn = output tile width (128 | 256), cta_pair = 1 (128-row tile on one SM) or

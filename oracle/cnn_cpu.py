@@ -18,7 +18,7 @@ import numpy as np
 import torch
 import torch.nn.functional as F
 
-CONV, DOWN, RES, HEAD = 0, 1, 2, 3
+CONV, DOWN, RES, HEAD, RES2 = 0, 1, 2, 3, 4
 
 
 class CNNOracle:
@@ -43,8 +43,13 @@ class CNNOracle:
     def loss_sum(self, flat, images, labels):
         """Summed cross-entropy of one member: images [u, h, w, c] fp32 NHWC."""
         x = images.permute(0, 3, 1, 2)
+        outs = []  # every layer's output (res2 adds an earlier one back)
         for L, (t, cin, cout, h, w) in enumerate(self.spec.layers):
             p = self._views(flat, L)
+            if t == RES2:
+                x = F.relu(F.conv2d(x, p["w1"], p["b1"], padding=1) + outs[self.spec.skips[L]])
+                outs.append(x)
+                continue
             if t == HEAD:
                 pooled = x.mean(dim=(2, 3))
                 logits = pooled @ p["w1"][: self.spec.classes].t() + p["b1"][: self.spec.classes]
@@ -56,6 +61,7 @@ class CNNOracle:
                 x = F.relu(F.conv2d(x, p["w1"], p["b1"], padding=1))
                 if t == DOWN:
                     x = F.avg_pool2d(x, 2)
+            outs.append(x)
         raise AssertionError("chain without a head")
 
     def step(self, images, labels, groups) -> float:

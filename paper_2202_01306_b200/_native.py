@@ -57,7 +57,7 @@ class hm_model(C.Structure):
 
 
 class hm_cnn_layer(C.Structure):
-    _fields_ = [(n, C.c_int32) for n in ("type", "cin", "cout", "h", "w")]
+    _fields_ = [(n, C.c_int32) for n in ("type", "cin", "cout", "h", "w", "skip")]
 
 
 class hm_cnn_model(C.Structure):
@@ -109,6 +109,7 @@ def lib() -> C.CDLL:
         "hm_k_pool2_relu_bwd": (C.c_int, [C.c_void_p] * 3 + [C.c_int32] * 4 + [C.c_void_p]),
         "hm_k_gap_fwd": (C.c_int, [C.c_void_p] * 2 + [C.c_int32] * 3 + [C.c_void_p]),
         "hm_k_gap_bwd": (C.c_int, [C.c_void_p] * 2 + [C.c_int32] * 3 + [C.c_void_p]),
+        "hm_k_add_bf16": (C.c_int, [C.c_void_p] * 3 + [C.c_int64, C.c_void_p]),
         "hm_runtime_debug_read": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_int64, C.c_void_p]),
         "hm_runtime_free": (None, [C.c_void_p]),
         "hm_nccl_unique_id": (C.c_int, [C.c_char_p, C.c_void_p]),

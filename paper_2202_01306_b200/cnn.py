@@ -7,11 +7,18 @@ A chain layer is one of (``include/harmony_b200.h`` hm_cnn_layer):
 * ``conv``: 3x3 convolution (stride 1, zero padding 1) + bias + ReLU;
 * ``down``: the same, then a 2x2 average pool (stage transition);
 * ``res``:  basic residual block ``relu(x + conv2(relu(conv1(x))))``;
-* ``head``: global average pool + fully connected classifier + cross-entropy.
+* ``head``: global average pool + fully connected classifier + cross-entropy;
+* ``res2``: the second half of a residual block at convolution granularity,
+  ``relu(conv(x) + skip)``, where skip is the output of an earlier layer.
 
-Every layer is one node of a linear chain, so pack boundaries carry one
-tensor each and the schedule needs no relays (``core.py:181-265``). A residual
-block's skip edge stays inside its own layer.
+With whole-block ``res`` layers the chain is linear: pack boundaries carry one
+tensor each and the schedule needs no relays (``core.py:181-265``). With
+``res2`` layers (``cnn_chain(kind="fine")``, one chain node per convolution,
+as the paper decomposes ResNet-1026) the skip edge can cross pack boundaries.
+``CNNSpec.chain()`` serializes the layer DAG with the reference's relays
+(``serialize_graph``). The runtime keeps skip tensors and their gradients in
+device-resident relay stores; they are SHARED_MEMORY hand-offs, so the ledger
+bills no bytes for them.
 
 Deviations from torchvision VGG / ResNet, kept in the CPU oracle too:
 
@@ -42,8 +49,8 @@ from dataclasses import dataclass
 
 from .profiler import AffineModel, ProfileSet
 
-CONV, DOWN, RES, HEAD = 0, 1, 2, 3
-_TYPES = {"conv": CONV, "down": DOWN, "res": RES, "head": HEAD}
+CONV, DOWN, RES, HEAD, RES2 = 0, 1, 2, 3, 4
+_TYPES = {"conv": CONV, "down": DOWN, "res": RES, "head": HEAD, "res2": RES2}
 
 
 def _pad64(v: int) -> int:
@@ -56,9 +63,25 @@ class CNNSpec:
     layers: tuple[tuple[int, int, int, int, int], ...]
     classes: int
     name: str = "cnn"
+    skips: tuple[int, ...] = ()  # per layer: source layer of a res2's skip input, -1 otherwise
 
     def __post_init__(self) -> None:
         R = len(self.layers)
+        if not self.skips:
+            object.__setattr__(self, "skips", (-1,) * R)
+        if len(self.skips) != R:
+            raise ValueError("one skip entry per layer")
+        for L, src in enumerate(self.skips):
+            t, cin, cout, h, w = self.layers[L]
+            if (t == RES2) != (src >= 0):
+                raise ValueError(f"layer {L}: exactly the res2 layers have a skip source")
+            if t == RES2:
+                if not 0 <= src < L - 1 or cin != cout:
+                    raise ValueError(f"layer {L}: res2 needs an earlier skip source and equal widths")
+                st, _, scout, sh, sw = self.layers[src]
+                oh, ow = (sh // 2, sw // 2) if st == DOWN else (sh, sw)
+                if (scout, oh, ow) != (cout, h, w):
+                    raise ValueError(f"layer {L}: skip source {src} has a different shape")
         if R < 1 or self.layers[-1][0] != HEAD or any(t == HEAD for t, *_ in self.layers[:-1]):
             raise ValueError("a CNN chain ends with exactly one head layer")
         for L, (t, cin, cout, h, w) in enumerate(self.layers):
@@ -93,7 +116,7 @@ class CNNSpec:
         if t == HEAD:
             return [("w1", (self.classes_padded, cin)), ("b1", (self.classes_padded,))]
         seg = [("w1", (cout, 3, 3, cin)), ("b1", (cout,))]
-        if t == RES:
+        if t == RES:  # (res2 is one convolution: w1, b1)
             seg += [("w2", (cout, 3, 3, cout)), ("b2", (cout,))]
         return seg
 
@@ -122,14 +145,25 @@ class CNNSpec:
         if t == HEAD:
             return 2 * u * cin * self.classes
         f = 2 * u * h * w * 9 * cin * cout
-        return 2 * f if t == RES else f
+        return 2 * f if t == RES else f  # res2: one convolution
 
     def act_bytes_per_sample(self, L: int) -> int:
         t, cin, cout, h, w = self.layers[L]
         if t == HEAD:
             return 2 * cin + 2 * self.classes_padded
         y = h * w * cout * 2
-        return {CONV: y, DOWN: y + y // 4, RES: 2 * y}[t] + h * w * cin * 2
+        return {CONV: y, DOWN: y + y // 4, RES: 2 * y, RES2: y}[t] + h * w * cin * 2
+
+    def chain(self):
+        """The planner's LayerChain: the layer DAG (skip edges included)
+        serialized with the reference's relay annotations (``core.py:181-265``)."""
+        from .core import LayerChain, LayerNode, serialize_graph
+        if all(s < 0 for s in self.skips):
+            return LayerChain.linear(self.n_layer)
+        nodes = [LayerNode(L, predecessors=tuple(p for p in ((L - 1,) if L else ()) + ((self.skips[L],)
+                                                                                        if self.skips[L] >= 0 else ())))
+                 for L in range(self.n_layer)]
+        return serialize_graph(nodes)
 
 
 def cnn_chain(name: str, image: int, widths: list[int], blocks: list[int], classes: int, kind: str = "res",
@@ -137,30 +171,45 @@ def cnn_chain(name: str, image: int, widths: list[int], blocks: list[int], class
     """Stem conv (+ ``stem_downs`` down layers of the first width), then per
     stage ``blocks[s]`` res blocks (kind "res") or conv layers (kind "vgg") of
     width ``widths[s]``, a ``down`` layer between stages, and the head."""
-    layers = []
+    layers, skips = [], []
     h = image
     cin = 64  # the image, zero-padded to 64 channels
     layers.append((CONV, cin, widths[0], h, h))
+    skips.append(-1)
     cin = widths[0]
     for _ in range(stem_downs):
         layers.append((DOWN, cin, widths[0], h, h))
+        skips.append(-1)
         h //= 2
     for s, (wd, nb) in enumerate(zip(widths, blocks)):
         for _ in range(nb):
-            layers.append((RES if kind == "res" else CONV, cin, wd, h, h))
+            if kind == "fine":  # one chain node per convolution; the skip spans the pair
+                if cin != wd:
+                    raise ValueError("fine residual stages keep the width (use a down layer between stages)")
+                src = len(layers) - 1
+                layers.append((CONV, cin, wd, h, h))
+                layers.append((RES2, wd, wd, h, h))
+                skips += [-1, src]
+            else:
+                layers.append((RES if kind == "res" else CONV, cin, wd, h, h))
+                skips.append(-1)
             cin = wd
         if s + 1 < len(widths):
             layers.append((DOWN, cin, widths[s + 1], h, h))
+            skips.append(-1)
             cin = widths[s + 1]
             h //= 2
     layers.append((HEAD, cin, 0, h, h))
-    return CNNSpec(tuple(layers), classes, name)
+    skips.append(-1)
+    return CNNSpec(tuple(layers), classes, name, tuple(skips))
 
 
 CNN_PRESETS = {
     # small chains for parity tests (16x16 images, 10 classes)
     "resnet-tiny": cnn_chain("resnet-tiny", 16, [64, 128], [2, 2], 10, "res"),
     "vgg-tiny": cnn_chain("vgg-tiny", 16, [64, 128], [2, 2], 10, "vgg"),
+    # convolution-granularity residual chain: skip edges cross pack boundaries (relays)
+    "resnet-fine-tiny": cnn_chain("resnet-fine-tiny", 16, [64, 128], [2, 2], 10, "fine"),
     # BASELINE config c5 shapes at 224^2 / 1000 classes (stem, two stem downs to
     # 56^2, stages at 56/28/14/7): ResNet-1026 = 1 + 2 + 2 x 510 + 3 = 1026
     # convolutions + classifier; VGG-416 = 1 + 2 + 409 + 4 = 416 convolutions

@@ -61,6 +61,20 @@ __global__ void relu_bwd_kernel(const uint4 *__restrict__ dy, const uint4 *__res
   }
 }
 
+// out = a + b
+__global__ void add_kernel(const uint4 *__restrict__ a, const uint4 *__restrict__ b, uint4 *__restrict__ out,
+                           int64_t n8) {
+  pdl_wait();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    float x[8], y[8];
+    unpack8(a[i], x);
+    unpack8(b[i], y);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] += y[j];
+    out[i] = pack8(x);
+  }
+}
+
 // y[n, h/2, w/2, c] = mean of the 2x2 window of a[n, h, w, c]; one thread per 8 channels of one output pixel
 __global__ void pool2_fwd_kernel(const bf16 *__restrict__ a, bf16 *__restrict__ y, int n, int h, int w, int c) {
   pdl_wait();
@@ -159,6 +173,15 @@ int relu_bwd(const void *dy, const void *y, void *dz, int64_t n, cudaStream_t s)
   return HM_OK;
 }
 
+int add_bf16(const void *a, const void *b, void *out, int64_t n, cudaStream_t s) {
+  if (n % 8) return fail(HM_ERR_VALIDATION, "add_bf16: n must be a multiple of 8");
+  ProfScope ps(KC_MISC, s, 0, 6.0 * n);
+  HM_CUDA(launch_pdl(add_kernel, dim3(grid_for(n / 8)), dim3(256), 0, s, static_cast<const uint4 *>(a),
+                     static_cast<const uint4 *>(b), static_cast<uint4 *>(out), n / 8));
+  count_launch();
+  return HM_OK;
+}
+
 int pool2_fwd(const void *a, void *y, int n, int h, int w, int c, cudaStream_t s) {
   if (h % 2 || w % 2 || c % 8) return fail(HM_ERR_VALIDATION, "pool2: even h, w and c % 8 == 0");
   ProfScope ps(KC_MISC, s, 0, 2.5 * n * h * w * (double)c);
@@ -215,6 +238,9 @@ int hm_k_pool2_relu_bwd(const void *dy, const void *a, void *dz, int32_t n, int3
 }
 int hm_k_gap_fwd(const void *x, void *pooled, int32_t nb, int32_t P, int32_t c, void *stream) {
   return hm::cnn::gap_fwd(x, pooled, nb, P, c, static_cast<cudaStream_t>(stream));
+}
+int hm_k_add_bf16(const void *a, const void *b, void *out, int64_t n, void *stream) {
+  return hm::cnn::add_bf16(a, b, out, n, static_cast<cudaStream_t>(stream));
 }
 int hm_k_gap_bwd(const float *dp, void *dx, int32_t nb, int32_t P, int32_t c, void *stream) {
   return hm::cnn::gap_bwd(dp, dx, nb, P, c, static_cast<cudaStream_t>(stream));

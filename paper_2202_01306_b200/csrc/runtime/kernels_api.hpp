@@ -41,5 +41,6 @@ int pool2_fwd(const void *a, void *y, int n, int h, int w, int c, cudaStream_t s
 int pool2_relu_bwd(const void *dy, const void *a, void *dz, int n, int h, int w, int c, cudaStream_t s);
 int gap_fwd(const void *x, void *pooled, int nb, int P, int c, cudaStream_t s);
 int gap_bwd(const float *dp, void *dx, int nb, int P, int c, cudaStream_t s);
+int add_bf16(const void *a, const void *b, void *out, int64_t n, cudaStream_t s);
 }  // namespace cnn
 }  // namespace hm

@@ -68,6 +68,7 @@ struct CnnParam {
 struct CnnScratch {
   bf16 *g[2] = {nullptr, nullptr};  // gradient ping-pong between layers of a pack
   bf16 *dz = nullptr, *dz2 = nullptr;
+  bf16 *gsum = nullptr;              // trunk + skip gradient of a relay source
   float *logits = nullptr, *dpool = nullptr;
 };
 
@@ -184,6 +185,9 @@ struct hm_runtime {
   std::vector<hm::CnnParam> cnn_lay;   // CNN: per-layer parameter offsets
   int classes = 0, classes_p = 0;      // CNN: classifier width (padded to 64)
   hm::CnnScratch CT{};
+  // res2 skip edges: source layer -> its output (forward) and the skip path's
+  // gradient (backward) for the whole minibatch, device-resident between tasks
+  std::map<int, uint8_t *> relay_y, relay_g;
   int64_t alpha = 0;
   int D = 0, S = 0, H = 0, DH = 0, R = 0, V = 0, Vp = 0;
   int64_t total_params = 0;
@@ -394,7 +398,7 @@ static CnnParam cnn_layout(const hm_runtime &rt, int L) {
     p.w1 = o; o += (int64_t)rt.classes_p * c.cin;
     p.b1 = o; o += rt.classes_p;
   } else {
-    p.w1 = o; o += (int64_t)c.cout * 9 * c.cin;
+    p.w1 = o; o += (int64_t)c.cout * 9 * c.cin;  // conv, down, res (first conv), res2
     p.b1 = o; o += c.cout;
     if (c.type == HM_CNN_RES) {
       p.w2 = o; o += (int64_t)c.cout * 9 * c.cout;
@@ -413,6 +417,7 @@ static std::vector<int64_t> cnn_act_sizes(const hm_runtime &rt, int L) {
     case HM_CNN_CONV: return {P * c.cout * 2};                         // y
     case HM_CNN_DOWN: return {P * c.cout * 2, P / 4 * c.cout * 2};     // a, y = pool(a)
     case HM_CNN_RES: return {P * c.cout * 2, P * c.cout * 2};          // h, y
+    case HM_CNN_RES2: return {P * c.cout * 2};                         // y
     default: return {(int64_t)c.cin * 2, (int64_t)rt.classes_p * 2};  // pooled, dlogits
   }
 }
@@ -447,6 +452,7 @@ static CnnActs cnn_acts(const hm_runtime &rt, uint8_t *store, int lo, int L, int
         case HM_CNN_CONV: A.y = r[0]; break;
         case HM_CNN_DOWN: A.a = r[0]; A.y = r[1]; break;
         case HM_CNN_RES: A.h = r[0]; A.y = r[1]; break;
+        case HM_CNN_RES2: A.y = r[0]; break;
         default: A.pooled = r[0]; A.dlog = r[1]; break;
       }
     }
@@ -496,6 +502,12 @@ static int cnn_forward_pack(hm_runtime &rt, TaskRt &tr, int lo, int hi, int u, i
         HM_TRY(gemm::run_conv(1, A.h, wsh + P.w2, A.y, u, c.h, c.w, c.cout, c.cout, HM_EPI_RESID_RELU_BF16,
                               w + P.b2, A.x, s));
         break;
+      case HM_CNN_RES2: {  // relu(conv(x) + b + skip), skip from the relay store
+        const uint8_t *skip = rt.relay_y.at(c.skip) + s0 * bnd(rt, c.skip + 1);
+        HM_TRY(gemm::run_conv(1, A.x, wsh + P.w1, A.y, u, c.h, c.w, c.cin, c.cout, HM_EPI_RESID_RELU_BF16, w + P.b1,
+                              skip, s));
+        break;
+      }
       default: {  // head: global average pool, classifier, cross-entropy
         HM_TRY(cnn::gap_fwd(A.x, A.pooled, u, c.h * c.w, c.cin, s));
         HM_TRY(gemm::run(A.pooled, wsh + P.w1, rt.CT.logits, u, rt.classes_p, c.cin, c.cin, c.cin, rt.classes_p, 0, 0,
@@ -506,6 +518,9 @@ static int cnn_forward_pack(hm_runtime &rt, TaskRt &tr, int lo, int hi, int u, i
         break;
       }
     }
+    if (rt.relay_y.count(L))  // this layer's output feeds a later res2's skip input
+      HM_CUDA(cudaMemcpyAsync(rt.relay_y.at(L) + s0 * bnd(rt, L + 1), A.y, (int64_t)u * bnd(rt, L + 1),
+                              cudaMemcpyDeviceToDevice, s));
     if (L == hi && y_final && c.type != HM_CNN_HEAD)
       HM_CUDA(cudaMemcpyAsync(y_final, A.y, (int64_t)u * bnd(rt, L + 1), cudaMemcpyDeviceToDevice, s));
   }
@@ -515,7 +530,7 @@ static int cnn_forward_pack(hm_runtime &rt, TaskRt &tr, int lo, int hi, int u, i
 // Backward of layers [hi .. lo] for one member: dy_in is the gradient of the
 // pack output (null when the pack ends in the head), dx_out receives the
 // gradient of the pack input (null for the pack holding layer 0).
-static int cnn_backward_pack(hm_runtime &rt, TaskRt &tr, int lo, int hi, int u, uint8_t *store, int64_t n,
+static int cnn_backward_pack(hm_runtime &rt, TaskRt &tr, int lo, int hi, int u, int64_t s0, uint8_t *store, int64_t n,
                              int64_t s_off, const uint8_t *dy_in, uint8_t *dx_out) {
   cudaStream_t s = rt.s_compute;
   if (!store) {
@@ -535,7 +550,24 @@ static int cnn_backward_pack(hm_runtime &rt, TaskRt &tr, int lo, int hi, int u, 
     const int64_t M = (int64_t)u * c.h * c.w;
     const bool need_dx = L > 0;
     bf16 *dx = (L == lo && dx_out) ? reinterpret_cast<bf16 *>(dx_out) : T.g[(hi - L) & 1];
+    if (rt.relay_g.count(L)) {  // the skip path's gradient joins the trunk gradient of this layer's output
+      if (!dy) return fail(HM_ERR_INTERNAL, "relay source without a trunk gradient");
+      HM_TRY(cnn::add_bf16(dy, rt.relay_g.at(L) + s0 * bnd(rt, L + 1), T.gsum, (int64_t)u * bnd(rt, L + 1) / 2, s));
+      dy = T.gsum;
+    }
     switch (c.type) {
+      case HM_CNN_RES2: {  // dz = dy * (y > 0): the conv's gradient and, unchanged, the skip's
+        if (!dy) return fail(HM_ERR_INTERNAL, "cnn backward without an incoming gradient");
+        HM_TRY(cnn::relu_bwd(dy, A.y, T.dz, M * c.cout, s));
+        HM_TRY(layers::bias_grad(T.dz, 1, dw + P.b1, M, c.cout, c.cout, s));
+        HM_TRY(gemm::run_conv(3, T.dz, A.x, dw + P.w1, u, c.h, c.w, c.cin, c.cout, HM_EPI_ACC_F32, nullptr, nullptr, s));
+        HM_CUDA(cudaMemcpyAsync(rt.relay_g.at(c.skip) + s0 * bnd(rt, c.skip + 1), T.dz, M * c.cout * 2,
+                                cudaMemcpyDeviceToDevice, s));
+        if (need_dx)
+          HM_TRY(gemm::run_conv(2, T.dz, wsh + P.w1, dx, u, c.h, c.w, c.cin, c.cout, HM_EPI_STORE_BF16, nullptr,
+                                nullptr, s));
+        break;
+      }
       case HM_CNN_HEAD: {
         // dW_fc += dlog^T . pooled; db_fc += sum dlog; dpooled = dlog . W_fc; dx = dpooled / P
         HM_TRY(gemm::run(A.dlog, A.pooled, dw + P.w1, rt.classes_p, c.cin, u, rt.classes_p, c.cin, c.cin, 1, 1,
@@ -796,12 +828,12 @@ static int run_member(hm_runtime &rt, int task, int g) {
     }
     uint8_t *dx = t.lo == 0 ? nullptr : at(tr.out_buf ? tr.out_buf : rt.dcarry[tr.carry_out], t.lo);
     if (tr.from_shared)
-      return cnn_backward_pack(rt, tr, t.lo, t.hi, u, rt.shared_store, rt.minibatch, s0, nullptr, dx);
+      return cnn_backward_pack(rt, tr, t.lo, t.hi, u, s0, rt.shared_store, rt.minibatch, s0, nullptr, dx);
     // recompute the pack from its stashed input, then backward
     const uint8_t *x_in = at(rt.slots.stash_in[tr.stash_slot], t.lo);
     HM_TRY(cnn_forward_pack(rt, tr, t.lo, t.hi, u, s0, x_in, nullptr, 0, 0, nullptr));
     const uint8_t *dy = at(tr.in_buf ? tr.in_buf : rt.dcarry[tr.carry_in], t.hi + 1);
-    return cnn_backward_pack(rt, tr, t.lo, t.hi, u, nullptr, 0, 0, dy, dx);
+    return cnn_backward_pack(rt, tr, t.lo, t.hi, u, s0, nullptr, 0, 0, dy, dx);
   }
   if (t.type == HM_TASK_F) {
     const float *x_in = t.lo == 0 ? nullptr
@@ -986,7 +1018,8 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
         return fail(HM_ERR_VALIDATION, "CNN chains: the shared pack's F and B must run on one GPU");
     for (auto &t : plan->tasks)
       for (auto &e : t.inputs)
-        if (e.src_layer >= 0) return fail(HM_ERR_VALIDATION, "CNN chains: relay entries are not executable yet");
+        if (e.src_layer >= 0 && e.channel != HM_SHARED_MEMORY)
+          return fail(HM_ERR_VALIDATION, "CNN chains: relays between GPUs are not executable (keep the chain on one GPU)");
   }
   int64_t max_recompute_layers = 1;
   for (int ti : mine) {
@@ -1059,6 +1092,16 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
     req.push_back({(void **)&rt.CT.dz, u_max * act});
     req.push_back({(void **)&rt.CT.dz2, u_max * act});
     req.push_back({(void **)&rt.CT.logits, u_max * rt.classes_p * 4});
+    req.push_back({(void **)&rt.CT.gsum, u_max * act});
+    rt.relay_y.clear();
+    rt.relay_g.clear();
+    for (auto &c : rt.cnn)
+      if (c.type == HM_CNN_RES2) {
+        rt.relay_y[c.skip] = nullptr;
+        rt.relay_g[c.skip] = nullptr;
+      }
+    for (auto &kv : rt.relay_y) req.push_back({(void **)&kv.second, (int64_t)minibatch * bnd(rt, kv.first + 1)});
+    for (auto &kv : rt.relay_g) req.push_back({(void **)&kv.second, (int64_t)minibatch * bnd(rt, kv.first + 1)});
     req.push_back({(void **)&rt.CT.dpool, u_max * cmax * 4});
   } else {
   req.push_back({(void **)&T.dy_bf, rows_u * d * 2});
@@ -1745,11 +1788,20 @@ hm_runtime *hm_runtime_create_cnn(int32_t device, const hm_cnn_model *model, int
     const hm_cnn_layer &c = model->layers[L];
     const std::string at = "CNN layer " + std::to_string(L) + ": ";
     if ((c.type == HM_CNN_HEAD) != (L == R - 1)) return bad(HM_ERR_VALIDATION, at + "the head must be the last layer");
-    if (c.type < HM_CNN_CONV || c.type > HM_CNN_HEAD) return bad(HM_ERR_VALIDATION, at + "unknown type");
+    if (c.type < HM_CNN_CONV || c.type > HM_CNN_RES2) return bad(HM_ERR_VALIDATION, at + "unknown type");
     if (c.h < 1 || c.w < 1 || c.cin % 64 || c.cin < 64 || (c.type != HM_CNN_HEAD && (c.cout % 64 || c.cout < 64)))
       return bad(HM_ERR_VALIDATION, at + "channels must be positive multiples of 64");
     if (c.type == HM_CNN_DOWN && (c.h % 2 || c.w % 2)) return bad(HM_ERR_VALIDATION, at + "pooling needs even h, w");
-    if (c.type == HM_CNN_RES && c.cin != c.cout) return bad(HM_ERR_VALIDATION, at + "residual blocks keep the width");
+    if ((c.type == HM_CNN_RES || c.type == HM_CNN_RES2) && c.cin != c.cout)
+      return bad(HM_ERR_VALIDATION, at + "residual blocks keep the width");
+    if ((c.type == HM_CNN_RES2) != (c.skip >= 0)) return bad(HM_ERR_VALIDATION, at + "only res2 layers have a skip");
+    if (c.type == HM_CNN_RES2) {
+      if (c.skip >= L - 1) return bad(HM_ERR_VALIDATION, at + "the skip source must precede the block");
+      const hm_cnn_layer &sc = model->layers[c.skip];
+      const int sh = sc.type == HM_CNN_DOWN ? sc.h / 2 : sc.h, sw = sc.type == HM_CNN_DOWN ? sc.w / 2 : sc.w;
+      if (sc.type == HM_CNN_HEAD || sc.cout != c.cout || sh != c.h || sw != c.w)
+        return bad(HM_ERR_VALIDATION, at + "skip source shape differs from the block output");
+    }
     if (L + 1 < R) {
       const hm_cnn_layer &n = model->layers[L + 1];
       const int oh = c.type == HM_CNN_DOWN ? c.h / 2 : c.h, ow = c.type == HM_CNN_DOWN ? c.w / 2 : c.w;

@@ -38,7 +38,8 @@ class HarmonyRuntime:
         self.is_cnn = isinstance(spec, CNNSpec)
         st = C.c_int32(0)
         if self.is_cnn:
-            arr = (NL.hm_cnn_layer * spec.n_layer)(*[NL.hm_cnn_layer(*lay) for lay in spec.layers])
+            arr = (NL.hm_cnn_layer * spec.n_layer)(*[NL.hm_cnn_layer(*lay, sk)
+                                                      for lay, sk in zip(spec.layers, spec.skips)])
             m = NL.hm_cnn_model(spec.n_layer, arr, spec.classes, spec.classes_padded, lr, betas[0], betas[1], eps)
             self._model = (m, arr)
             h = self.lib.hm_runtime_create_cnn(device, C.byref(m), int(alpha_bytes), C.byref(st))

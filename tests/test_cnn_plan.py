@@ -43,3 +43,27 @@ def test_ledger_closed_forms_full_size(name):
     assert vol["K"]["cpu_gpu_swap"] == 2 * 2 * W
     heads = [lo for lo, _ in packs[:-1]]
     assert vol["sX"]["message_passing"] == 2 * 32 * sum(spec.x_bytes(L) for L in heads)
+
+
+def test_fine_resnet_relays_in_plan():
+    """Convolution-granularity ResNet: each block's skip edge becomes a relay
+    annotation (serialize_graph); relays crossing a pack boundary appear as X /
+    dY entries with src_layer -- zero-byte SHARED_MEMORY on one GPU, billed
+    y(src) on the P2P channel when the packs sit on different GPUs
+    (taskgraph.py:195-208)."""
+    spec = CNN_PRESETS["resnet-fine-tiny"]
+    chain = spec.chain()
+    assert [(a.source, a.destination) for a in chain.relay_annotations] == [(0, 2), (2, 4), (5, 7), (7, 9)]
+    prof = cnn_profiles(spec)
+    pf, pb = ((0, 1), (2, 5), (6, 10)), ((0, 3), (4, 5), (6, 10))
+    cfg = H.Configuration(2, pf, 2, pb, 8, H.Mode.PP)
+    one = H.MachineModel(gpu_count=1, gpu_mem_capacity=8 << 30, pcie_bandwidth=55_000_000_000)
+    g1 = H.generate_task_graph(cfg, one, prof, chain)
+    relays = [(t.index, L, ch.src_layer, ch.kind.value) for t in g1.tasks for ents in t.inputs.values()
+              for L, ch in ents.items() if ch.src_layer is not None]
+    assert relays == [(1, 0, 0, "shared_memory"), (7, 2, 2, "shared_memory")]
+    assert "peer2peer" not in {r[4] for r in H.simulate(g1, one, prof).ledger}
+    two = H.MachineModel(gpu_count=2, gpu_mem_capacity=8 << 30, pcie_bandwidth=55_000_000_000)
+    g2 = H.generate_task_graph(cfg, two, prof, chain)
+    p2p = H.simulate(g2, two, prof).channel_volumes.get("peer2peer", {})
+    assert p2p  # trunk and relay hand-offs between the two GPUs are billed

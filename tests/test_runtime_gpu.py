@@ -197,7 +197,7 @@ def _run_cnn(spec, cfg, steps, alpha=8 << 30, lr=1e-4):
     from paper_2202_01306_b200.runtime import HarmonyRuntime
     prof = cnn_profiles(spec, u_max=64)
     mach = H.MachineModel(gpu_count=1, gpu_mem_capacity=alpha, pcie_bandwidth=55_000_000_000)
-    g = H.generate_task_graph(cfg, mach, prof)
+    g = H.generate_task_graph(cfg, mach, prof, spec.chain())
     rt = HarmonyRuntime(spec, alpha_bytes=alpha, lr=lr)
     rt.init_weights(0)
     oracle = CNNOracle(spec, rt.w.copy(), rt.w_off, lr=lr)
@@ -241,4 +241,29 @@ def test_cnn_chain_matches_oracle(name, pf, pb, uf, ub, mode):
     cfg = H.Configuration(uf, pf, ub, pb, 8, H.Mode(mode))
     rel_w, losses = _run_cnn(spec, cfg, steps=3)
     print(name, "cnn rel_w", rel_w, losses)
+    assert rel_w < CNN_STATE_RTOL
+
+
+@pytest.mark.parametrize("pf,pb,uf,ub,mode", [
+    (((0, 1), (2, 5), (6, 10)), ((0, 3), (4, 5), (6, 10)), 2, 2, "pp"),  # skip edges cross F and B pack boundaries
+    (((0, 4), (5, 10)), ((0, 1), (2, 4), (5, 10)), 4, 2, "pp"),          # u_f != u_b, relay into a recomputed pack
+    (((0, 1), (2, 5), (6, 10)), ((0, 1), (2, 5), (6, 10)), 2, 2, "dp"),  # Harmony-DP (relays implicit)
+])
+def test_cnn_relays_match_oracle(pf, pb, uf, ub, mode):
+    """Convolution-granularity residual chain (res2 layers): the skip edges
+    are the reference's relays (serialize_graph, taskgraph.py:195-208);
+    skip tensors and their gradients cross pack boundaries through the
+    device relay stores; ledger bit-exact, loss / weights vs the oracle."""
+    from paper_2202_01306_b200.cnn import CNN_PRESETS
+    spec = CNN_PRESETS["resnet-fine-tiny"]
+    cfg = H.Configuration(uf, pf, ub, pb, 8, H.Mode(mode))
+    if mode == "pp":
+        g = H.generate_task_graph(cfg, H.MachineModel(gpu_count=1, gpu_mem_capacity=8 << 30,
+                                                      pcie_bandwidth=55_000_000_000),
+                                  __import__("paper_2202_01306_b200.cnn", fromlist=["cnn_profiles"]).cnn_profiles(spec),
+                                  spec.chain())
+        assert any(ch.src_layer is not None for t in g.tasks for ents in t.inputs.values()
+                   for ch in ents.values()), "the packs were meant to cut skip edges"
+    rel_w, losses = _run_cnn(spec, cfg, steps=3)
+    print("resnet-fine cnn rel_w", rel_w, losses)
     assert rel_w < CNN_STATE_RTOL
