@@ -1269,7 +1269,7 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
     TaskRt &tr = rt.trt[r.task];
     if (r.is_compute) {
       if (t.type == HM_TASK_U) {
-        if (rt.comm && rt.nranks > 1) {
+        if (rt.comm) {  // (a 1-rank communicator still runs the collective: the N=1 test of this path)
           // sum the pack's gradient over the data-parallel ranks on the comm
           // stream; overlaps the next backward task on the compute stream
           Action ar;
