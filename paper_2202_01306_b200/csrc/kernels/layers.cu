@@ -4,6 +4,7 @@
 // per row, 16-byte vector accesses, fp32 math.
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "../runtime/common.hpp"
@@ -159,10 +160,77 @@ __global__ void ln_fwd_kernel(const float *__restrict__ x, const float *__restri
   }
 }
 
+// Row-in-registers variant (d <= 128 * NV4): x is read from HBM exactly once
+// (all NV4 float4 loads of a lane issued together), mean and variance come
+// from the registers, and gamma / beta are L2-resident.
+template <int NV4>
+__global__ void __launch_bounds__(256) ln_fwd_reg_kernel(const float *__restrict__ x, const float *__restrict__ gam,
+                                                         const float *__restrict__ bet, __nv_bfloat16 *__restrict__ y,
+                                                         float *__restrict__ mean, float *__restrict__ rstd,
+                                                         int64_t rows, int d, float eps) {
+  pdl_wait();
+  const int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float4 *xr = reinterpret_cast<const float4 *>(x + r * d);
+  const int n4 = d / 4;
+  float4 v[NV4];
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV4; ++k) {
+    const int i = lane + 32 * k;
+    v[k] = i < n4 ? xr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+#pragma unroll
+  for (int k = 0; k < NV4; ++k) s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+  const float mu = warp_sum(s) / d;
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV4; ++k)
+    if (lane + 32 * k < n4) {
+      const float a = v[k].x - mu, b = v[k].y - mu, c = v[k].z - mu, e = v[k].w - mu;
+      q += (a * a + b * b) + (c * c + e * e);
+    }
+  const float rs = rsqrtf(warp_sum(q) / d + eps);
+  uint2 *yr = reinterpret_cast<uint2 *>(y + r * d);
+  const float4 *g4 = reinterpret_cast<const float4 *>(gam);
+  const float4 *b4 = reinterpret_cast<const float4 *>(bet);
+#pragma unroll
+  for (int k = 0; k < NV4; ++k) {
+    const int i = lane + 32 * k;
+    if (i < n4) {
+      const float4 gg = __ldg(g4 + i), bb = __ldg(b4 + i);
+      __nv_bfloat162 a = __floats2bfloat162_rn((v[k].x - mu) * rs * gg.x + bb.x, (v[k].y - mu) * rs * gg.y + bb.y);
+      __nv_bfloat162 c = __floats2bfloat162_rn((v[k].z - mu) * rs * gg.z + bb.z, (v[k].w - mu) * rs * gg.w + bb.w);
+      yr[i] = make_uint2(*reinterpret_cast<uint32_t *>(&a), *reinterpret_cast<uint32_t *>(&c));
+    }
+  }
+  if (lane == 0) {
+    mean[r] = mu;
+    rstd[r] = rs;
+  }
+}
+
 int ln_fwd(const float *x, const float *g, const float *b, void *y, float *mean, float *rstd, int64_t rows, int d,
            cudaStream_t s) {
   if (d % 4) return fail(HM_ERR_VALIDATION, "layernorm: d must be a multiple of 4");
   ProfScope ps(KC_LAYERNORM, s, 0, 6.0 * rows * d);
+  static const int impl = getenv("HM_LN_FWD") ? atoi(getenv("HM_LN_FWD")) : 1;  // 0 = three-pass kernel
+  if (impl) {
+    const dim3 grid((unsigned)((rows * 32 + 255) / 256)), block(256);
+    auto yy = static_cast<__nv_bfloat16 *>(y);
+    const int nv4 = (d / 4 + 31) / 32;
+    cudaError_t e = cudaErrorInvalidValue;
+    if (nv4 <= 4) e = launch_pdl(ln_fwd_reg_kernel<4>, grid, block, 0, s, x, g, b, yy, mean, rstd, rows, d, 1e-5f);
+    else if (nv4 <= 8) e = launch_pdl(ln_fwd_reg_kernel<8>, grid, block, 0, s, x, g, b, yy, mean, rstd, rows, d, 1e-5f);
+    else if (nv4 <= 13) e = launch_pdl(ln_fwd_reg_kernel<13>, grid, block, 0, s, x, g, b, yy, mean, rstd, rows, d, 1e-5f);
+    else if (nv4 <= 16) e = launch_pdl(ln_fwd_reg_kernel<16>, grid, block, 0, s, x, g, b, yy, mean, rstd, rows, d, 1e-5f);
+    if (nv4 <= 16) {
+      HM_CUDA(e);
+      count_launch();
+      return HM_OK;
+    }
+  }
   HM_CUDA(launch_pdl(ln_fwd_kernel, dim3((unsigned)((rows * 32 + 255) / 256)), dim3(256), 0, s, x, g, b, static_cast<__nv_bfloat16 *>(y), mean,
                                                                     rstd, rows, d, 1e-5f));
   count_launch();

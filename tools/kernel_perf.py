@@ -155,6 +155,28 @@ def bench_attn():
                           "peak": tf_peak, "peak_kind": kind}), flush=True)
 
 
+def bench_ln():
+    _, hbm, kind = peaks()
+    for rows, d in ((4096, 1600), (4096, 1024), (4096, 8192)):
+        x = torch.randn(rows, d, device="cuda")
+        g = torch.randn(d, device="cuda")
+        b = torch.randn(d, device="cuda")
+        y = torch.empty(rows, d, device="cuda", dtype=torch.bfloat16)
+        mu = torch.empty(rows, device="cuda")
+        rs = torch.empty(rows, device="cuda")
+        ms = timeit(lambda: ops.layernorm_fwd(x, g, b, y, mu, rs))
+        dy = torch.randn(rows, d, device="cuda")
+        out = torch.empty(rows, d, device="cuda")
+        ob = torch.empty(rows, d, device="cuda", dtype=torch.bfloat16)
+        dg = torch.zeros(d, device="cuda")
+        db = torch.zeros(d, device="cuda")
+        msb = timeit(lambda: ops.layernorm_bwd(dy, x, mu, rs, g, out, dg, db, resid=x, out_bf16=ob))
+        print(json.dumps({"kernel": "layernorm", "rows": rows, "d": d, "fwd_ms": round(ms, 4),
+                          "fwd_GBps": round(6 * rows * d / ms / 1e6, 1), "bwd_ms": round(msb, 4),
+                          "bwd_GBps": round(18 * rows * d / msb / 1e6, 1), "peak": hbm,
+                          "env": {k: os.environ.get(k) for k in ("HM_LN_FWD",)}}), flush=True)
+
+
 def bench_gemm_bn():
     """Same shapes with the tile width forced (HM_GEMM_BN is read once per
     process, so each width runs in a subprocess)."""
@@ -185,3 +207,5 @@ if __name__ == "__main__":
         bench_gemm()
     if what in ("adam", "all"):
         bench_adam()
+    if what in ("ln", "all"):
+        bench_ln()
