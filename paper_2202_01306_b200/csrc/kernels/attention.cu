@@ -470,12 +470,13 @@ static int bwd_launch(const __nv_bfloat16 *qkv, const __nv_bfloat16 *o, const __
   const int64_t warps = rows * H;
   dvec_kernel<DH><<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(o, dout, dvec, rows, H);
   const float scale = 1.f / sqrtf((float)DH);
-  // The tcgen05 backward (attention_tc.cu) is correct but not yet faster than
-  // this mma.sync kernel on B200 (single softmax warp per SM sub-partition);
-  // opt in with HM_ATTN_BWD=tc while it is being tuned.
+  // The tcgen05 backward (attention_tc.cu: TMEM accumulators, dQ as one TMA
+  // reduce-add per query block) is the default where it applies (head_dim 64,
+  // seq % 128 == 0): 1.4-1.5x this mma.sync kernel on B200.  HM_ATTN_BWD=mma
+  // forces the mma.sync kernel.
   static const bool use_tc = [] {
     const char *e = getenv("HM_ATTN_BWD");
-    return e && std::string(e) == "tc";
+    return !(e && std::string(e) == "mma");
   }();
   if (use_tc && attn_tc::supported(S, DH)) {
     // tcgen05 main kernel; it folds the softmax scale into dq_acc

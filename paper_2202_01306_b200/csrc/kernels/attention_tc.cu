@@ -270,12 +270,15 @@ static EncodeFn encode_fn() {
 //   dV  += P^T dO       dK  += dS^T Q          (TMEM accumulators)
 //   dQ_i = dS K  -> fp32 atomics into dq_acc (scaled), converted by dq_convert
 // ---------------------------------------------------------------------------
+constexpr uint32_t kDqStage = BQ * DH * 4;  // 32 KB: dQ tile (fp32) staged for the TMA reduce-add
 constexpr size_t kSmemBwd = 1024 + 2 * kTileBytes /*K,V*/ + 4 * kTileBytes /*Q,dO x2*/ + 2 * kPBytes /*P^T,dS^T*/ +
+                            kDqStage +
                             2 * 2 * BQ * 4 /*lse,D x2*/ + 512;
 
 template <bool CAUSAL>
 __global__ void __launch_bounds__(kThreads, 1)
     bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+               const __grid_constant__ CUtensorMap tm_dq,
                const float *__restrict__ lse, const float *__restrict__ dvec, float *__restrict__ dq_acc,
                __nv_bfloat16 *__restrict__ dqkv, int S, int H, float scale_log2, float scale) {
   extern __shared__ uint8_t smem_raw[];
@@ -286,7 +289,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t *sdO = sQ + 2 * kTileBytes;     // [2] stages
   uint8_t *sP = sdO + 2 * kTileBytes;     // P^T  [128 keys x 128 queries]
   uint8_t *sdS = sP + kPBytes;            // dS^T
-  float *sL = reinterpret_cast<float *>(sdS + kPBytes);  // [2][128] lse
+  uint8_t *sDQ = sdS + kPBytes;           // dQ stage: 2 x [128 rows x 32 fp32] SW128 chunks
+  float *sL = reinterpret_cast<float *>(sDQ + kDqStage);  // [2][128] lse
   float *sD = sL + 2 * BQ;                               // [2][128] D
   uint64_t *bar = reinterpret_cast<uint64_t *>(sD + 2 * BQ);
   uint64_t *kv_full = bar;
@@ -309,6 +313,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm_qkv);
     tma_prefetch(&tm_do);
+    tma_prefetch(&tm_dq);
     mbar_init(kv_full, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&q_full[i], 1);
@@ -459,10 +464,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(dq_empty);
-      float *dst = dq_acc + (int64_t)(row0 + i * BQ + r) * d + h * DH;
+      // dQ_i: one TMA reduce-add of the whole 128 x 64 fp32 tile (in L2) instead
+      // of 8192 scalar atomics -- staged in SW128 rows (conflict-free writes)
+      if (r == 0) bulk_wait_read0();  // the previous block's reduce has read the stage
+      asm volatile("bar.sync 2, 128;" ::: "memory");
 #pragma unroll
-      for (int c = 0; c < DH; ++c) atomicAdd(dst + c, __uint_as_float(q[c]) * scale);
+      for (int c = 0; c < DH / 32; ++c) {
+        uint8_t *chunk = sDQ + c * (BQ * 128) + r * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<float4 *>(chunk + ((j ^ (r & 7)) << 4)) =
+              make_float4(__uint_as_float(q[32 * c + 4 * j]) * scale, __uint_as_float(q[32 * c + 4 * j + 1]) * scale,
+                          __uint_as_float(q[32 * c + 4 * j + 2]) * scale, __uint_as_float(q[32 * c + 4 * j + 3]) * scale);
+      }
+      fence_async_smem();
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      if (r == 0) {
+#pragma unroll
+        for (int c = 0; c < DH / 32; ++c) tma_reduce_add_2d(&tm_dq, sDQ + c * (BQ * 128), h * DH + 32 * c, row0 + i * BQ);
+        bulk_commit();
+      }
     }
+    if (r == 0) bulk_wait0();
     // dV, dK of this key block
     mbar_wait(acc_full, 0);
     tc_fence_after();
@@ -519,6 +542,18 @@ int backward_main(const void *qkv, const void *dout, const float *lse, const flo
   CUtensorMap tq, td;
   HM_TRY(make_map(&tq, qkv, 3 * (int64_t)d, (int64_t)B * S, 3 * (int64_t)d * 2));
   HM_TRY(make_map(&td, dout, d, (int64_t)B * S, (int64_t)d * 2));
+  CUtensorMap tdq;  // dq_acc [B*S, d] fp32, {32, 128} boxes in SW128 (the reduce-add target)
+  {
+    EncodeFn fn = encode_fn();
+    cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)B * S};
+    cuuint64_t strides[1] = {(cuuint64_t)d * 4};
+    cuuint32_t box[2] = {32, 128};
+    cuuint32_t estr[2] = {1, 1};
+    if (!fn || fn(&tdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dq_acc, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return fail(HM_ERR_DEVICE, "attention dQ tensor map encode failed");
+  }
   static bool attr[2] = {false, false};
   auto k = causal ? bwd_kernel<true> : bwd_kernel<false>;
   if (!attr[causal ? 1 : 0]) {
@@ -526,7 +561,7 @@ int backward_main(const void *qkv, const void *dout, const float *lse, const flo
     attr[causal ? 1 : 0] = true;
   }
   const float scale = 1.f / sqrtf((float)DH);
-  k<<<dim3(S / BKV, B * H), kThreads, kSmemBwd, s>>>(tq, td, lse, dvec, dq_acc, static_cast<__nv_bfloat16 *>(dqkv), S,
+  k<<<dim3(S / BKV, B * H), kThreads, kSmemBwd, s>>>(tq, td, tdq, lse, dvec, dq_acc, static_cast<__nv_bfloat16 *>(dqkv), S,
                                                       H, 1.4426950408889634f * scale, scale);
   count_launch();
   HM_CUDA(cudaGetLastError());

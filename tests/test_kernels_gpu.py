@@ -289,7 +289,8 @@ def test_attention_fwd_tcgen05_matches(ops, B, S, H, causal):
 
 
 def test_attention_bwd_tcgen05_opt_in():
-    """The tcgen05 backward (opt-in via HM_ATTN_BWD=tc) matches autograd."""
+    """The mma.sync backward (HM_ATTN_BWD=mma; the tcgen05 one is the default
+    where it applies) matches autograd."""
     import subprocess
     import sys
     here = __import__("os").path.dirname(__import__("os").path.abspath(__file__))
@@ -297,7 +298,7 @@ def test_attention_bwd_tcgen05_opt_in():
             "import test_kernels_gpu as T; "
             "from paper_2202_01306_b200 import ops; "
             "T.test_attention_fwd_bwd(ops, 2, 256, 3, 64, True); T.test_attention_fwd_bwd(ops, 1, 512, 2, 64, False)")
-    env = dict(__import__("os").environ, HM_ATTN_BWD="tc")
+    env = dict(__import__("os").environ, HM_ATTN_BWD="mma")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
 
