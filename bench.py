@@ -39,7 +39,7 @@ WORKLOADS = {
     "gpt2-xl-dp": ("gpt2-xl", 16, 4, 8, 32, "dp"),
     "tiny": ("tiny", 16, 4, 2, 4, "pp"),
     # config c2: BERT-Large (24 x d1024, seq 512, full attention), D = 64, every pack swapped
-    "bert-large-pp": ("bert-large", 64, 8, 6, 24, "pp"),
+    "bert-large-pp": ("bert-large", 64, 16, 6, 32, "pp"),
     # north-star target shape: W + Adam state (184 GB) > one GPU's HBM
     "gpt-15b-dp": ("gpt-15b", 24, 4, 3, 170, "dp"),
     # config c5: deep-CNN packs (128 residual blocks at 56x56 / 28x28, implicit-GEMM convs)
