@@ -291,11 +291,11 @@ int hm_k_gap_bwd(const float *dp, void *dx, int32_t nb, int32_t P, int32_t c, vo
 /* out = a + b (bf16, n % 8 == 0): the skip gradient joining the trunk gradient */
 int hm_k_add_bf16(const void *a, const void *b, void *out, int64_t n, void *stream);
 
-/* Tile configuration the GEMM picks for an (m, n, k, epilogue) problem:
- * bn = output tile width (128 | 256), cta_pair = 1 (128-row tile on one SM) or
+/* Tile configuration the GEMM picks for an (m, n, k, epilogue, B major) problem:
+ * bn = output tile width (128 | 192 | 256; 192 single-CTA only), cta_pair = 1 (128-row tile on one SM) or
  * 2 (256-row tile on a CTA pair, tcgen05.mma.cta_group::2), splits = split-K
  * factor (ACC_F32 only; partial sums meet in a TMA reduce-add). */
-int hm_k_gemm_tile(int64_t m, int64_t n, int64_t k, int32_t epilogue, int32_t *bn,
+int hm_k_gemm_tile(int64_t m, int64_t n, int64_t k, int32_t epilogue, int32_t b_major, int32_t *bn,
                    int32_t *cta_pair, int32_t *splits);
 /* Force a tile configuration for every later GEMM of the process (0 = auto);
  * for tests and tuning (same as HM_GEMM_BN / HM_GEMM_CG / HM_GEMM_SPLITK). */

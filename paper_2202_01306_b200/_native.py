@@ -129,8 +129,8 @@ def lib() -> C.CDLL:
                                 C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
                                 C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_int64, C.c_int64,
                                 C.c_int64, C.c_void_p]),
-        "hm_k_gemm_tile": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int32, P(C.c_int32), P(C.c_int32),
-                                     P(C.c_int32)]),
+        "hm_k_gemm_tile": (C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_int32, C.c_int32, P(C.c_int32),
+                                     P(C.c_int32), P(C.c_int32)]),
         "hm_k_gemm_set_tile": (C.c_int, [C.c_int32, C.c_int32, C.c_int32]),
         "hm_k_conv_fwd": (C.c_int, [C.c_void_p] * 3 + [C.c_int32] * 6 + [C.c_void_p] * 3),
         "hm_k_conv_dgrad": (C.c_int, [C.c_void_p] * 3 + [C.c_int32] * 6 + [C.c_void_p] * 2),

@@ -64,7 +64,7 @@ struct Cfg {
   static constexpr uint32_t kABytes = BM * BK * 2;
   static constexpr uint32_t kBBytes = kBRows * BK * 2;
   static constexpr int kStages = (int)((196608u) / (kABytes + kBBytes)) > 8 ? 8 : (int)(196608u / (kABytes + kBBytes));
-  static constexpr uint32_t kTmemCols = 2 * BN >= 512 ? 512 : (2 * BN >= 256 ? 256 : 128);
+  static constexpr uint32_t kTmemCols = 2 * BN > 256 ? 512 : (2 * BN > 128 ? 256 : 128);  // pow2 >= 2 BN
   static constexpr size_t kSmem = 1024 + (size_t)kStages * (kABytes + kBBytes) + kEpiWarps * 4096 + 256;
 };
 
@@ -585,8 +585,11 @@ static int env_int(const char *name) {
 // HM_GEMM_SPLITK force a choice.
 static int g_force_bn = env_int("HM_GEMM_BN"), g_force_cg = env_int("HM_GEMM_CG"),
            g_force_s = env_int("HM_GEMM_SPLITK");
+// 128 x 192 single-CTA tiles (fit 1600-wide outputs in 9 column tiles)
+static const bool g_tile192 = getenv("HM_GEMM_192") ? atoi(getenv("HM_GEMM_192")) != 0 : true;
+static const double g_eff192 = getenv("HM_GEMM_EFF192") ? atof(getenv("HM_GEMM_EFF192")) : 0.70;
 
-static TileCfg pick_tile(int64_t M, int64_t N, int64_t K, int epi) {
+static TileCfg pick_tile(int64_t M, int64_t N, int64_t K, int epi, bool allow192 = true, bool b_mn = false) {
   const int env_bn = g_force_bn, env_cg = g_force_cg, env_s = g_force_s;
   const int64_t sms = num_sms();
   const int64_t num_k = (K + BK - 1) / BK;
@@ -594,9 +597,11 @@ static TileCfg pick_tile(int64_t M, int64_t N, int64_t K, int epi) {
   double best_t = 1e300;
   for (int cg = 1; cg <= 2; ++cg) {
     if (env_cg && cg != env_cg) continue;
-    for (int bn = 128; bn <= 256; bn += 128) {
+    for (int bn : {128, 192, 256}) {
       if (env_bn && bn != env_bn) continue;
-      const double eff = bn == 128 ? 0.55 : (cg == 1 ? 0.80 : 0.93);
+      if (bn == 192 && (cg == 2 || !g_tile192 || !allow192)) continue;
+      // pair tiles lose more when B is MN-major (dgrad / wgrad: 64-wide B chunks per k-block)
+      const double eff = bn == 128 ? 0.55 : bn == 192 ? g_eff192 : (cg == 1 ? 0.80 : (b_mn ? 0.86 : 0.93));
       const double t_kb = bn / 256.0 / eff;
       const int64_t tiles = ((M + BM * cg - 1) / (BM * cg)) * ((N + bn - 1) / bn);
       const int64_t slots = sms / cg;
@@ -682,7 +687,7 @@ int run(const void *A, const void *B, void *D, int64_t M, int64_t N, int64_t K, 
     return fail(HM_ERR_VALIDATION, "gemm: epilogue needs an aux tensor");
   if (aux && ((ld_aux * (epi == HM_EPI_RESID_F32 ? 4 : 2)) % 16 || ((uintptr_t)aux & 15)))
     return fail(HM_ERR_VALIDATION, "gemm: aux must be 16B aligned with 16B pitch");
-  TileCfg tc = pick_tile(M, N, K, epi);
+  TileCfg tc = pick_tile(M, N, K, epi, true, b_mn != 0);
   if (force_bn) tc.bn = force_bn;
   const int bn = tc.bn;
   Args a{};
@@ -705,6 +710,14 @@ int run(const void *A, const void *B, void *D, int64_t M, int64_t N, int64_t K, 
     if (rc) return rc;
   } else {
     tx = td;
+  }
+  if (bn == 192) {  // single-CTA only (a pair would stage 96-row B halves)
+    switch ((a_mn ? 2 : 0) | (b_mn ? 1 : 0)) {
+      case 0: return launch<192, 0, 0, 1>(ta, tb, td, tx, a, stream);
+      case 1: return launch<192, 0, 1, 1>(ta, tb, td, tx, a, stream);
+      case 2: return launch<192, 1, 0, 1>(ta, tb, td, tx, a, stream);
+      default: return launch<192, 1, 1, 1>(ta, tb, td, tx, a, stream);
+    }
   }
   const int key = (tc.cg == 2 ? 8 : 0) | (bn == 256 ? 4 : 0) | (a_mn ? 2 : 0) | (b_mn ? 1 : 0);
   switch (key) {
@@ -816,7 +829,7 @@ int run_conv(int mode, const void *act, const void *wt, void *out, int n, int h,
                     epi == HM_EPI_GELU_BF16))
     return fail(HM_ERR_VALIDATION, "conv: fwd/dgrad epilogues are the bf16 ones");
   if (epi_src_bf16(epi) && !aux) return fail(HM_ERR_VALIDATION, "conv: epilogue needs an aux tensor");
-  TileCfg tc = pick_tile(M, N, K, epi);
+  TileCfg tc = pick_tile(M, N, K, epi, /*allow192=*/false, mode != 1);  // conv kernels come in 128 / 256 widths
   Args a{};
   a.M = (int)M; a.N = (int)N; a.K = (int)K;
   a.num_m = (int)((M + BM * tc.cg - 1) / (BM * tc.cg));
@@ -870,17 +883,19 @@ extern "C" int hm_k_conv_wgrad(const void *dy, const void *x, float *dw, int32_t
 }
 
 extern "C" int hm_k_gemm_set_tile(int32_t bn, int32_t cta_pair, int32_t splits) {
-  if ((bn && bn != 128 && bn != 256) || (cta_pair && cta_pair != 1 && cta_pair != 2) || splits < 0 || splits > 32)
-    return hm::fail(HM_ERR_VALIDATION, "gemm tile override: bn in {0,128,256}, cta_pair in {0,1,2}, splits in [0,32]");
+  if ((bn && bn != 128 && bn != 192 && bn != 256) || (cta_pair && cta_pair != 1 && cta_pair != 2) || splits < 0 ||
+      splits > 32 || (bn == 192 && cta_pair == 2))
+    return hm::fail(HM_ERR_VALIDATION,
+                    "gemm tile override: bn in {0,128,192,256} (192 single-CTA), cta_pair in {0,1,2}, splits in [0,32]");
   hm::gemm::g_force_bn = bn;
   hm::gemm::g_force_cg = cta_pair;
   hm::gemm::g_force_s = splits;
   return HM_OK;
 }
 
-extern "C" int hm_k_gemm_tile(int64_t m, int64_t n, int64_t k, int32_t epilogue, int32_t *bn, int32_t *cta_pair,
-                              int32_t *splits) {
-  const hm::gemm::TileCfg t = hm::gemm::pick_tile(m, n, k, epilogue);
+extern "C" int hm_k_gemm_tile(int64_t m, int64_t n, int64_t k, int32_t epilogue, int32_t b_major, int32_t *bn,
+                              int32_t *cta_pair, int32_t *splits) {
+  const hm::gemm::TileCfg t = hm::gemm::pick_tile(m, n, k, epilogue, true, b_major != 0);
   *bn = t.bn;
   *cta_pair = t.cg;
   *splits = t.splits;

@@ -71,10 +71,10 @@ def conv_wgrad(dy, x, dw):
     return dw
 
 
-def gemm_tile(M, N, K, epi="f32"):
+def gemm_tile(M, N, K, epi="f32", b_mn=False):
     """(bn, cta_pair, splits) the GEMM picks for this problem."""
     bn, cg, sp = C.c_int32(), C.c_int32(), C.c_int32()
-    NL.check(N_lib().hm_k_gemm_tile(M, N, K, EPI[epi], C.byref(bn), C.byref(cg), C.byref(sp)))
+    NL.check(N_lib().hm_k_gemm_tile(M, N, K, EPI[epi], int(b_mn), C.byref(bn), C.byref(cg), C.byref(sp)))
     return bn.value, cg.value, sp.value
 
 

@@ -115,7 +115,7 @@ def bench_gemm():
                 ops.gemm_set_tile(*cfg)
             ms = time_graph(fn) if GRAPH else timeit(fn)
             tf = 2 * M * N * K / ms / 1e9
-            tile = ops.gemm_tile(M, N, K, epi)
+            tile = ops.gemm_tile(M, N, K, epi, bmn)
             ops.gemm_set_tile(0, 0, 0)
             print(json.dumps({"kernel": "gemm", "timing": "graph50" if GRAPH else "single+flush", "shape": name,
                               "M": M, "N": N, "K": K, "tile": {"bn": tile[0], "cta_pair": tile[1], "splits": tile[2]},
@@ -199,7 +199,7 @@ if __name__ == "__main__":
         GRAPH = True
         what = "gemm"
     if what == "gemm_sweep":
-        SWEEP = [(bn, cg, 0) for cg in (1, 2) for bn in (128, 256)]
+        SWEEP = [(bn, cg, 0) for cg in (1, 2) for bn in (128, 192, 256) if not (bn == 192 and cg == 2)]
         what = "gemm"
     if what in ("attn", "all"):
         bench_attn()
