@@ -244,6 +244,241 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// forward, two query tiles per CTA (256 queries): two softmax warpgroups (A =
+// warps 4-7, B = warps 8-11; causal: query blocks p and nq-1-p, so every CTA
+// does the same work; full attention: 2p and 2p+1) share every K/V tile,
+// and the MMA thread interleaves them -- S_A(j+1) is issued while softmax B
+// works on S_B(j) and vice versa -- so the exp / pack work of one tile hides
+// the MMA and TMEM latencies of the other.  The S row is read from TMEM twice
+// (max pass, exp pass) in 32-column chunks to keep the thread under 168
+// registers (12 warps per CTA).
+// ---------------------------------------------------------------------------
+constexpr int kThreads2 = 384;
+constexpr size_t kSmem2 = 1024 + 2 * kTileBytes /*Q_A, Q_B*/ + 4 * kTileBytes /*K, V x2*/ + 2 * kPBytes /*P_A, P_B*/ + 512;
+
+template <bool CAUSAL>
+__global__ void __launch_bounds__(kThreads2, 1)
+    fwd2_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16 *__restrict__ out, float *__restrict__ lse,
+                int S, int H, float scale_log2) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sQ = smem;                   // [2] query tiles
+  uint8_t *sK = sQ + 2 * kTileBytes;    // [2] stages
+  uint8_t *sV = sK + 2 * kTileBytes;    // [2] stages
+  uint8_t *sP = sV + 2 * kTileBytes;    // [2] tiles
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sP + 2 * kPBytes);
+  uint64_t *q_full = bar;
+  uint64_t *kv_full = bar + 1, *kv_empty = bar + 3;
+  uint64_t *s_full = bar + 5, *s_empty = bar + 7;   // [tile]
+  uint64_t *p_full = bar + 9, *p_empty = bar + 11;  // [tile]
+  uint64_t *o_full = bar + 13, *o_empty = bar + 15; // [tile]
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 17);
+
+  const int nq = S / BQ;
+  const int pr = (int)blockIdx.x;
+  // causal: pair query block p with nq-1-p, so every CTA walks nq+1 KV tiles
+  // (balanced); full attention: consecutive blocks
+  const int qb_a = CAUSAL ? pr : 2 * pr, qb_b = CAUSAL ? nq - 1 - pr : 2 * pr + 1;
+  const int bh = blockIdx.y, b = bh / H, h = bh % H;
+  const int d = H * DH;
+  // KV tiles each query tile needs (nkv_b >= nkv_a)
+  const int nkv_a = CAUSAL ? qb_a + 1 : S / BKV, nkv_b = CAUSAL ? qb_b + 1 : S / BKV;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr uint32_t C_S = 0, C_O = 2 * BKV;  // TMEM: S_A, S_B | O_A, O_B
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 128);
+      mbar_init(&p_full[i], 128);
+      mbar_init(&p_empty[i], 1);
+      mbar_init(&o_full[i], 1);
+      mbar_init(&o_empty[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int row0 = b * S;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(q_full, 2 * kTileBytes);
+      tma_load_2d(sQ, &tm, q_full, h * DH, row0 + qb_a * BQ);
+      tma_load_2d(sQ + kTileBytes, &tm, q_full, h * DH, row0 + qb_b * BQ);
+      for (int j = 0; j < nkv_b; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[st], 2 * kTileBytes);
+        tma_load_2d(sK + st * kTileBytes, &tm, &kv_full[st], d + h * DH, row0 + j * BKV);
+        tma_load_2d(sV + st * kTileBytes, &tm, &kv_full[st], 2 * d + h * DH, row0 + j * BKV);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = idesc_bf16_f32(BQ, BKV, 0, 0);
+      constexpr uint32_t idesc_o = idesc_bf16_f32(BQ, DH, 0, 1);
+      mbar_wait(q_full, 0);
+      auto issue_s = [&](int t, int j) {  // S_t(j) = Q_t K_j^T
+        const int st = j & 1;
+        if (t == 0) mbar_wait(&kv_full[st], (j >> 1) & 1);
+        mbar_wait(&s_empty[t], (j & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t q_base = smem_u32(sQ + t * kTileBytes), k_base = smem_u32(sK + st * kTileBytes);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk)
+          mma_bf16(tmem + C_S + t * BKV, umma_desc_sw128(q_base + kk * 32, 16, 1024),
+                   umma_desc_sw128(k_base + kk * 32, 16, 1024), idesc_s, kk > 0);
+        mma_commit(&s_full[t]);
+      };
+      auto issue_pv = [&](int t, int j) {  // O_t(j) = P_t(j) V_j
+        const int st = j & 1;
+        mbar_wait(&p_full[t], j & 1);
+        mbar_wait(&o_empty[t], (j & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t p_base = smem_u32(sP + t * kPBytes), v_base = smem_u32(sV + st * kTileBytes);
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk)
+          mma_bf16(tmem + C_O + t * DH, umma_desc_sw128(p_base + (kk >> 2) * (BQ * 128) + (kk & 3) * 32, 16, 1024),
+                   umma_desc_sw128(v_base + kk * 2048, BKV * 128, 1024), idesc_o, kk > 0);
+        mma_commit(&o_full[t]);
+        mma_commit(&p_empty[t]);
+      };
+      if (nkv_a > 0) issue_s(0, 0);
+      else mbar_wait(&kv_full[0], 0);
+      issue_s(1, 0);
+      for (int j = 0; j < nkv_b; ++j) {
+        if (j < nkv_a) {
+          issue_pv(0, j);
+          if (j + 1 < nkv_a) issue_s(0, j + 1);
+        }
+        issue_pv(1, j);
+        mma_commit(&kv_empty[j & 1]);  // both tiles are done with K_j / V_j once these MMAs retire
+        if (j + 1 < nkv_b) {
+          if (!(j + 1 < nkv_a)) mbar_wait(&kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+          issue_s(1, j + 1);
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int t = (warp - 4) >> 2;  // query tile: 0 = A, 1 = B
+    const int qb = t == 0 ? qb_a : qb_b;
+    const int nkv = t == 0 ? nkv_a : nkv_b;
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    const uint32_t s_addr = tmem + lane_addr + C_S + t * BKV;
+    float o[DH];
+#pragma unroll
+    for (int c = 0; c < DH; ++c) o[c] = 0.f;
+    float m = -INFINITY, l = 0.f, alpha_prev = 1.f;
+    auto add_o = [&](int j, float alpha) {
+      mbar_wait(&o_full[t], j & 1);
+      tc_fence_after();
+      uint32_t v[DH];
+#pragma unroll
+      for (int c0 = 0; c0 < DH; c0 += 32)
+        tmem_ld_32x32b_x32(tmem + lane_addr + C_O + t * DH + c0, *reinterpret_cast<uint32_t(*)[32]>(v + c0));
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&o_empty[t]);
+#pragma unroll
+      for (int c = 0; c < DH; ++c) o[c] = o[c] * alpha + __uint_as_float(v[c]);
+    };
+    for (int j = 0; j < nkv; ++j) {
+      mbar_wait(&s_full[t], j & 1);
+      tc_fence_after();
+      const bool diag = CAUSAL && j == qb;
+      // pass 1: row max over four 32-column chunks
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c0 = 0; c0 < BKV; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(s_addr + c0, v);
+        tmem_ld_wait();
+        float m8[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) m8[e] = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const float x = (diag && c0 + c > r) ? -INFINITY : __uint_as_float(v[c]);
+          m8[c & 7] = fmaxf(m8[c & 7], x);
+        }
+        mx = fmaxf(mx, fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                              fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))));
+      }
+      const float m_new = fmaxf(m, mx * scale_log2);
+      const float alpha = ex2(m - m_new);
+      m = m_new;
+      // P_t(j) goes to smem: wait until PV_t(j-1) has consumed the previous P
+      mbar_wait(&p_empty[t], (j & 1) ^ 1);
+      uint8_t *prow = sP + t * kPBytes + r * 128;
+      float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      // pass 2: exp, row sum, bf16 pack into the 128B-swizzled A operand
+#pragma unroll
+      for (int c0 = 0; c0 < BKV; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(s_addr + c0, v);
+        tmem_ld_wait();
+        uint32_t pk[16];
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+          float p0 = ex2(fmaf(__uint_as_float(v[c]), scale_log2, -m_new));
+          float p1 = ex2(fmaf(__uint_as_float(v[c + 1]), scale_log2, -m_new));
+          if (diag && c0 + c > r) p0 = 0.f;
+          if (diag && c0 + c + 1 > r) p1 = 0.f;
+          rs8[(c >> 1) & 7] += p0 + p1;
+          __nv_bfloat162 tb = __floats2bfloat162_rn(p0, p1);
+          pk[c >> 1] = *reinterpret_cast<uint32_t *>(&tb);
+        }
+        uint8_t *atom_row = prow + (c0 >> 6) * (BQ * 128);
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          const int chunk = ((c0 & 63) >> 3) + ch;
+          *reinterpret_cast<uint4 *>(atom_row + ((chunk ^ (r & 7)) << 4)) =
+              make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&s_empty[t]);
+      fence_async_smem();
+      mbar_arrive(&p_full[t]);
+      const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+      l = l * alpha + rs;
+      if (j > 0) add_o(j - 1, alpha_prev);
+      alpha_prev = alpha;
+    }
+    add_o(nkv - 1, alpha_prev);
+    const float inv = 1.f / l;
+    __nv_bfloat16 *orow = out + (int64_t)(row0 + qb * BQ + r) * d + h * DH;
+#pragma unroll
+    for (int c = 0; c < DH; c += 8) {
+      uint4 w;
+      uint32_t *wp = reinterpret_cast<uint32_t *>(&w);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        __nv_bfloat162 tb = __floats2bfloat162_rn(o[c + 2 * e] * inv, o[c + 2 * e + 1] * inv);
+        wp[e] = *reinterpret_cast<uint32_t *>(&tb);
+      }
+      *reinterpret_cast<uint4 *>(orow + c) = w;
+    }
+    lse[(int64_t)(row0 + qb * BQ + r) * H + h] = m + log2f(l);
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                               const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -584,14 +819,32 @@ int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causa
          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return fail(HM_ERR_DEVICE, "attention tensor map encode failed");
+  const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
+  ProfScope ps(KC_ATTN_FWD, s, 4.0 * B * (double)S * S * H * DH * (causal ? 0.5 : 1.0), (double)B * S * H * DH * 2 * 4);
+  static const bool two_tiles = !(getenv("HM_ATTN_FWD") && getenv("HM_ATTN_FWD")[0] == '1');
+  // two query tiles per CTA (ping-pong softmax warpgroups) for full attention:
+  // 1.31x at 8 x 512 x 16 heads.  Causal attention stays on one tile per CTA:
+  // pairing blocks either unbalances the CTAs (2p, 2p+1) or leaves the longer
+  // tile running alone for most of its K/V sweep (p, nq-1-p) -- both measured
+  // slower than the single-tile kernel's finer-grained 128-query CTAs.
+  if (two_tiles && !causal && S % (2 * BQ) == 0) {
+    static bool attr2[2] = {false, false};
+    auto k2 = causal ? fwd2_kernel<true> : fwd2_kernel<false>;
+    if (!attr2[causal ? 1 : 0]) {
+      HM_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem2));
+      attr2[causal ? 1 : 0] = true;
+    }
+    k2<<<dim3(S / (2 * BQ), B * H), kThreads2, kSmem2, s>>>(tm, static_cast<__nv_bfloat16 *>(o), lse, S, H, scale_log2);
+    count_launch();
+    HM_CUDA(cudaGetLastError());
+    return HM_OK;
+  }
   static bool attr[2] = {false, false};
   auto k = causal ? fwd_kernel<true> : fwd_kernel<false>;
   if (!attr[causal ? 1 : 0]) {
     HM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
     attr[causal ? 1 : 0] = true;
   }
-  const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
-  ProfScope ps(KC_ATTN_FWD, s, 4.0 * B * (double)S * S * H * DH * (causal ? 0.5 : 1.0), (double)B * S * H * DH * 2 * 4);
   k<<<dim3(S / BQ, B * H), kThreads, kSmem, s>>>(tm, static_cast<__nv_bfloat16 *>(o), lse, S, H, scale_log2);
   count_launch();
   HM_CUDA(cudaGetLastError());

@@ -129,7 +129,9 @@ def test_pipelined_steps_match_sequential():
         out.append((losses, rt.w.copy(), rt.k.copy()))
         rt.close()
     (l0, w0, k0), (l1, w1, k1) = out
-    assert np.allclose(l0, l1, rtol=1e-5)
+    # equal up to the run-to-run order of fp32 atomics / TMA reduce-adds
+    # (dQ, LayerNorm dgamma/dbeta, embedding, split-K weight gradients)
+    assert np.allclose(l0, l1, rtol=1e-4)
     # equal up to run-to-run nondeterminism of atomics (dQ, LayerNorm dγ/dβ, embedding)
     assert np.linalg.norm(w0 - w1) / np.linalg.norm(w0) < 5e-4
     assert np.linalg.norm(k0 - k1) / np.linalg.norm(k0) < 1e-2
