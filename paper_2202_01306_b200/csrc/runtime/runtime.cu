@@ -467,12 +467,16 @@ static CnnActs cnn_acts(const hm_runtime &rt, uint8_t *store, int lo, int L, int
 static int cnn_forward_pack(hm_runtime &rt, TaskRt &tr, int lo, int hi, int u, int64_t s0, const uint8_t *x_in,
                             uint8_t *store, int64_t n, int64_t s_off, uint8_t *y_final) {
   cudaStream_t s = rt.s_compute;
+  // A forward task without a store hands its output on and keeps nothing: it
+  // reads its input in place and writes the last layer straight into y_final
+  // (no staging copies).  Stored / recomputed passes keep the input for backward.
+  const bool pass_through = !store && y_final;
   if (!store) {
     store = rt.work_store;
     n = u;
     s_off = 0;
   }
-  {
+  if (!pass_through) {
     CnnActs A0 = cnn_acts(rt, store, lo, lo, n, s_off);
     HM_CUDA(cudaMemcpyAsync(A0.x, x_in, (int64_t)u * bnd(rt, lo), cudaMemcpyDeviceToDevice, s));
   }
@@ -483,6 +487,8 @@ static int cnn_forward_pack(hm_runtime &rt, TaskRt &tr, int lo, int hi, int u, i
     const float *w = rt.slots.w[tr.w_slot] + off;
     const bf16 *wsh = rt.slots.wsh[tr.w_slot] + off;
     CnnActs A = cnn_acts(rt, store, lo, L, n, s_off);
+    if (pass_through && L == lo) A.x = reinterpret_cast<bf16 *>(const_cast<uint8_t *>(x_in));
+    if (pass_through && L == hi && c.type != HM_CNN_HEAD) A.y = reinterpret_cast<bf16 *>(y_final);
     if (tr.stash_heads.count(L))  // capture the input of a backward-pack head
       HM_CUDA(cudaMemcpyAsync(rt.stash_dev.at(L) + s0 * bnd(rt, L), A.x, (int64_t)u * bnd(rt, L),
                               cudaMemcpyDeviceToDevice, s));
@@ -521,7 +527,7 @@ static int cnn_forward_pack(hm_runtime &rt, TaskRt &tr, int lo, int hi, int u, i
     if (rt.relay_y.count(L))  // this layer's output feeds a later res2's skip input
       HM_CUDA(cudaMemcpyAsync(rt.relay_y.at(L) + s0 * bnd(rt, L + 1), A.y, (int64_t)u * bnd(rt, L + 1),
                               cudaMemcpyDeviceToDevice, s));
-    if (L == hi && y_final && c.type != HM_CNN_HEAD)
+    if (L == hi && y_final && !pass_through && c.type != HM_CNN_HEAD)
       HM_CUDA(cudaMemcpyAsync(y_final, A.y, (int64_t)u * bnd(rt, L + 1), cudaMemcpyDeviceToDevice, s));
   }
   return HM_OK;

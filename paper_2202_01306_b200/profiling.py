@@ -36,8 +36,11 @@ def synthetic_inputs(spec: GPTSpec | CNNSpec, samples: int):
 
 
 def samples_from_trace(spec: GPTSpec | CNNSpec, graph, trace, u: int) -> list[ProfileSample]:
-    """ProfileSamples of one single-layer-pack run (trace = measured
-    compute TraceEvents of the report)."""
+    """ProfileSamples of one profiling run (trace = measured compute
+    TraceEvents of the report).  Packs of several layers are apportioned to
+    their layers by FLOPs (F, B) and parameters (U): the layers then carry the
+    kernel efficiency they have inside real packs, where consecutive kernels
+    overlap their launches, instead of the isolated single-layer cost."""
     shapes = shape_profiles(spec)
     dur: dict[int, list[int]] = {}
     for e in trace:
@@ -45,14 +48,19 @@ def samples_from_trace(spec: GPTSpec | CNNSpec, graph, trace, u: int) -> list[Pr
             dur.setdefault(e.task, []).append(e.end_ns - e.start_ns)
     f_time, b_time, u_time = {}, {}, {}
     for t in graph.tasks:
-        L = t.pack[0]
+        lo, hi = t.pack
         d = sum(dur.get(t.index, [0]))
-        if t.type is TaskType.F:
-            f_time[L] = d
-        elif t.type is TaskType.B:
-            b_time[L] = (d, t.recompute)
-        else:
-            u_time[L] = d
+        layers = range(lo, hi + 1)
+        wts = [spec.layer_params(L) if t.type is TaskType.U else max(1, spec.layer_fwd_flops(L, 1)) for L in layers]
+        tot = float(sum(wts))
+        for L, w in zip(layers, wts):
+            share = int(round(d * w / tot))
+            if t.type is TaskType.F:
+                f_time[L] = share
+            elif t.type is TaskType.B:
+                b_time[L] = (share, t.recompute)
+            else:
+                u_time[L] = share
     out = []
     for L in range(spec.n_layer):
         b, rec = b_time[L]
@@ -68,12 +76,13 @@ def samples_from_trace(spec: GPTSpec | CNNSpec, graph, trace, u: int) -> list[Pr
 
 
 def profile_gpt(spec: GPTSpec | CNNSpec, u_values=None, u_max: int = 8, stride: int = 4, alpha_bytes: int = 64 << 30,
-                device: int = 0, warmup: int = 1) -> tuple[ProfileSet, list[ProfileSample]]:
+                device: int = 0, warmup: int = 1, pack_layers: int = 1) -> tuple[ProfileSet, list[ProfileSample]]:
     """Measure and fit a ProfileSet on this GPU (sample points 1, stride
     multiples and u_max, as the reference's profiler, `profiler.py:421-427`)."""
     from .runtime import HarmonyRuntime
     us = tuple(u_values) if u_values else sample_points(u_max, stride)
-    packs = tuple((L, L) for L in range(spec.n_layer))
+    R = spec.n_layer
+    packs = tuple((L, min(L + pack_layers, R) - 1) for L in range(0, R, pack_layers))
     samples: list[ProfileSample] = []
     rt = HarmonyRuntime(spec, alpha_bytes=alpha_bytes, device=device)
     try:

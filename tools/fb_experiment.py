@@ -23,6 +23,7 @@ ap.add_argument("--alpha-gib", type=float, default=2.0)
 ap.add_argument("--d", type=int, default=32)
 ap.add_argument("--umax", type=int, default=16)
 ap.add_argument("--iters", type=int, default=4)
+ap.add_argument("--pack-layers", type=int, default=1, help="layers per profiling pack (apportioned by FLOPs)")
 a = ap.parse_args()
 presets = dict(CNN_PRESETS, **GPT_PRESETS)
 # an irregular chain: wide, high-resolution stages early (big activations, few
@@ -31,7 +32,8 @@ presets["resnet-fb"] = cnn_chain("resnet-fb", 64, [64, 128, 256, 512], [6, 6, 6,
 spec = presets[a.model]
 alpha = int(a.alpha_gib * (1 << 30))
 t0 = time.time()
-prof, samples = profile_model(spec, u_values=(1, 2, 4, 8, 16), u_max=16, stride=4, alpha_bytes=48 << 30)
+prof, samples = profile_model(spec, u_values=(1, 2, 4, 8, 16), u_max=16, stride=4, alpha_bytes=48 << 30,
+                              pack_layers=a.pack_layers)
 print(json.dumps({"model": spec.name, "layers": spec.n_layer, "params_M": round(spec.total_params() / 1e6, 1),
                   "profiled_s": round(time.time() - t0, 1), "samples": len(samples)}), flush=True)
 mach = H.MachineModel(gpu_count=1, gpu_mem_capacity=alpha, pcie_bandwidth=int(50e9))
