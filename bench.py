@@ -38,6 +38,9 @@ WORKLOADS = {
     # name: (preset, samples_per_gpu, u, layers_per_pack, alpha_gib, mode)
     "gpt2-xl-dp": ("gpt2-xl", 16, 4, 8, 32, "dp"),
     "tiny": ("tiny", 16, 4, 2, 4, "pp"),
+    # the same model at a 4x larger minibatch: Harmony's grouping amortises the fixed
+    # per-iteration swap bytes (W, K) over more samples ("no grouping")
+    "gpt2-xl-dp-d64": ("gpt2-xl", 64, 8, 4, 64, "dp"),
     # config c2: BERT-Large (24 x d1024, seq 512, full attention), D = 64, every pack swapped
     "bert-large-pp": ("bert-large", 64, 16, 6, 32, "pp"),
     # north-star target shape: W + Adam state (184 GB) > one GPU's HBM
