@@ -376,6 +376,13 @@ def run_native(args) -> None:
         if key:
             busy[key] += e.end_ns - e.start_ns
     util = {k: round(v / max(1, cnt["iteration_ns"]), 4) for k, v in busy.items()}
+    # achieved link rate of the swap streams while they move data (bytes / busy time
+    # of the last timed iteration's transfers, measured CUDA events)
+    moved = {"h2d": 0, "d2h": 0}
+    for r in rep.ledger:
+        if r[4] in ("cpu_gpu_swap", "message_passing") and r[7] == rank:
+            moved["h2d" if r[1] == 0 else "d2h"] += r[6]
+    swap_gbs = {k: round(moved[k] / busy[k], 2) if busy[k] else None for k in moved}
     _barrier(world)
     # per-kernel CUDA-event timings: one extra iteration with an event pair
     # around every kernel launch (kept out of the timed steps above, whose
@@ -460,6 +467,7 @@ def run_native(args) -> None:
         "kernel_shares": share,
         "gemm_by_gflop": gemm_groups,
         "stream_busy_frac": util,
+        "swap_achieved_gbs": swap_gbs,
         "last_iter_ms_unpipelined_view": round(cnt["iteration_ns"] / 1e6, 2),
         "adam_hbm": {"achieved_gbs": round(adam_gbs, 1), "peak": pk["hbm"], "frac": round(adam_gbs / pk["hbm"], 4)},
         "e2e": {"value": round(e2e_value, 3), "unit": "samples/s", "h2d_bytes_per_step": int(in_bytes),
