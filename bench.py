@@ -441,7 +441,9 @@ def run_native(args) -> None:
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "bf16",
-        "data": "synthetic (tokens U[0,V) seed 1234; weights N(0,0.02) from a CUDA generator seeded 0)",
+        "data": ("synthetic (images N(0,1), 3 channels zero-padded to 64, labels U[0,classes) seed 1234; "
+                 "He-normal weights seed 0)") if is_cnn else
+                "synthetic (tokens U[0,V) seed 1234; weights N(0,0.02) from a CUDA generator seeded 0)",
         "config": {"workload": f"{args.workload}: {spec.name} Harmony-{mode.upper()}, packs of {lpp} layers, "
                                f"u_f=u_b={u}, alpha={alpha_gib} GiB/GPU",
                    "global_batch": D, "seq_len": getattr(spec, "seq_len", None), "parallelism": f"harmony-{mode}{world}",
