@@ -479,6 +479,196 @@ __global__ void __launch_bounds__(kThreads2, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// forward, lean variant: two CTAs per SM hide each other's latencies.  P goes
+// to TMEM (bf16 pairs packed into S's own columns, FA4-style) and is read by
+// the PV MMA as its A operand, O accumulates in TMEM (rescaled in place by the
+// softmax threads when the row max moves), so a CTA needs 80 KB of shared
+// memory, 256 TMEM columns and <= 128 registers per thread.
+// ---------------------------------------------------------------------------
+constexpr size_t kSmem3 = 1024 + kTileBytes /*Q*/ + 4 * kTileBytes /*K, V x2*/ + 256;
+
+template <bool CAUSAL>
+__global__ void __launch_bounds__(kThreads, 2)
+    fwd3_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16 *__restrict__ out, float *__restrict__ lse,
+                int S, int H, float scale_log2) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sQ = smem;
+  uint8_t *sK = sQ + kTileBytes;
+  uint8_t *sV = sK + 2 * kTileBytes;
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sV + 2 * kTileBytes);
+  uint64_t *q_full = bar;
+  uint64_t *kv_full = bar + 1, *kv_empty = bar + 3;
+  uint64_t *s_full = bar + 5, *p_full = bar + 6, *o_full = bar + 7;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 8);
+
+  const int nq = S / BQ;
+  const int qb = CAUSAL ? nq - 1 - (int)blockIdx.x : (int)blockIdx.x;
+  const int bh = blockIdx.y, b = bh / H, h = bh % H;
+  const int d = H * DH;
+  const int nkv = CAUSAL ? qb + 1 : S / BKV;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr uint32_t C_S = 0, C_O = BKV;  // S (fp32, 128 cols; P bf16 pairs in its first 64) | O (64 cols)
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 128);
+    mbar_init(o_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<256>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int row0 = b * S;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(q_full, kTileBytes);
+      tma_load_2d(sQ, &tm, q_full, h * DH, row0 + qb * BQ);
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[st], 2 * kTileBytes);
+        tma_load_2d(sK + st * kTileBytes, &tm, &kv_full[st], d + h * DH, row0 + j * BKV);
+        tma_load_2d(sV + st * kTileBytes, &tm, &kv_full[st], 2 * d + h * DH, row0 + j * BKV);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = idesc_bf16_f32(BQ, BKV, 0, 0);
+      constexpr uint32_t idesc_o = idesc_bf16_f32(BQ, DH, 0, 1);
+      mbar_wait(q_full, 0);
+      const uint32_t q_base = smem_u32(sQ);
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        mbar_wait(&kv_full[st], (j >> 1) & 1);
+        if (j > 0) mbar_wait(p_full, (j - 1) & 1);  // PV_{j-1} is issued before S_j overwrites its P
+        tc_fence_after();
+        const uint32_t k_base = smem_u32(sK + st * kTileBytes);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk)
+          mma_bf16(tmem + C_S, umma_desc_sw128(q_base + kk * 32, 16, 1024),
+                   umma_desc_sw128(k_base + kk * 32, 16, 1024), idesc_s, kk > 0);
+        mma_commit(s_full);
+        // O += P_j V_j once the softmax has packed P_j and rescaled O
+        mbar_wait(p_full, j & 1);
+        tc_fence_after();
+        const uint32_t v_base = smem_u32(sV + st * kTileBytes);
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk)
+          mma_bf16_ts(tmem + C_O, tmem + C_S + kk * 8, umma_desc_sw128(v_base + kk * 2048, BKV * 128, 1024), idesc_o,
+                      (j > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(o_full);
+        mma_commit(&kv_empty[st]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    const uint32_t s_addr = tmem + lane_addr + C_S, o_addr = tmem + lane_addr + C_O;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < nkv; ++j) {
+      mbar_wait(s_full, j & 1);
+      tc_fence_after();
+      const bool diag = CAUSAL && j == qb;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c0 = 0; c0 < BKV; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(s_addr + c0, v);
+        tmem_ld_wait();
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const float x = (diag && c0 + c > r) ? -INFINITY : __uint_as_float(v[c]);
+          m4[c & 3] = fmaxf(m4[c & 3], x);
+        }
+        mx = fmaxf(mx, fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])));
+      }
+      const float m_new = fmaxf(m, mx * scale_log2);
+      const float alpha = ex2(m - m_new);
+      m = m_new;
+      if (j > 0) {  // O_{j-1} complete: rescale it in place before PV_j accumulates
+        mbar_wait(o_full, (j - 1) & 1);
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, alpha != 1.f)) {  // warp-uniform: tcgen05.ld / st are .sync.aligned
+#pragma unroll
+          for (int c0 = 0; c0 < DH; c0 += 32) {
+            uint32_t ov[32];
+            tmem_ld_32x32b_x32(o_addr + c0, ov);
+            tmem_ld_wait();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * alpha);
+            tmem_st_32x32b_x32(o_addr + c0, ov);
+          }
+        }
+      }
+      float rs4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int c0 = 0; c0 < BKV; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(s_addr + c0, v);
+        tmem_ld_wait();
+        uint32_t pk[16];
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+          float p0 = ex2(fmaf(__uint_as_float(v[c]), scale_log2, -m_new));
+          float p1 = ex2(fmaf(__uint_as_float(v[c + 1]), scale_log2, -m_new));
+          if (diag && c0 + c > r) p0 = 0.f;
+          if (diag && c0 + c + 1 > r) p1 = 0.f;
+          rs4[(c >> 1) & 3] += p0 + p1;
+          __nv_bfloat162 tb = __floats2bfloat162_rn(p0, p1);
+          pk[c >> 1] = *reinterpret_cast<uint32_t *>(&tb);
+        }
+        // keys c0..c0+31 -> P columns c0/2..c0/2+15 (S columns already read)
+        tmem_st_32x32b_x16(s_addr + (c0 >> 1), pk);
+      }
+      tmem_st_wait();
+      l = l * alpha + ((rs4[0] + rs4[1]) + (rs4[2] + rs4[3]));
+      tc_fence_before();
+      mbar_arrive(p_full);
+    }
+    mbar_wait(o_full, (nkv - 1) & 1);
+    tc_fence_after();
+    const float inv = 1.f / l;
+    __nv_bfloat16 *orow = out + (int64_t)(row0 + qb * BQ + r) * d + h * DH;
+#pragma unroll
+    for (int c0 = 0; c0 < DH; c0 += 32) {
+      uint32_t ov[32];
+      tmem_ld_32x32b_x32(o_addr + c0, ov);
+      tmem_ld_wait();
+#pragma unroll
+      for (int c = 0; c < 32; c += 8) {
+        uint4 w;
+        uint32_t *wp = reinterpret_cast<uint32_t *>(&w);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          __nv_bfloat162 tb = __floats2bfloat162_rn(__uint_as_float(ov[c + 2 * e]) * inv,
+                                                    __uint_as_float(ov[c + 2 * e + 1]) * inv);
+          wp[e] = *reinterpret_cast<uint32_t *>(&tb);
+        }
+        *reinterpret_cast<uint4 *>(orow + c0 + c) = w;
+      }
+    }
+    lse[(int64_t)(row0 + qb * BQ + r) * H + h] = m + log2f(l);
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<256>(tmem);
+  }
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                               const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -821,7 +1011,8 @@ int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causa
     return fail(HM_ERR_DEVICE, "attention tensor map encode failed");
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
   ProfScope ps(KC_ATTN_FWD, s, 4.0 * B * (double)S * S * H * DH * (causal ? 0.5 : 1.0), (double)B * S * H * DH * 2 * 4);
-  static const bool two_tiles = !(getenv("HM_ATTN_FWD") && getenv("HM_ATTN_FWD")[0] == '1');
+  static const bool two_tiles = !(getenv("HM_ATTN_FWD") && (getenv("HM_ATTN_FWD")[0] == '1' ||
+                                                             getenv("HM_ATTN_FWD")[0] == '3'));
   // two query tiles per CTA (ping-pong softmax warpgroups) for full attention:
   // 1.31x at 8 x 512 x 16 heads.  Causal attention stays on one tile per CTA:
   // pairing blocks either unbalances the CTAs (2p, 2p+1) or leaves the longer
@@ -835,6 +1026,19 @@ int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causa
       attr2[causal ? 1 : 0] = true;
     }
     k2<<<dim3(S / (2 * BQ), B * H), kThreads2, kSmem2, s>>>(tm, static_cast<__nv_bfloat16 *>(o), lse, S, H, scale_log2);
+    count_launch();
+    HM_CUDA(cudaGetLastError());
+    return HM_OK;
+  }
+  static const bool lean = getenv("HM_ATTN_FWD") && getenv("HM_ATTN_FWD")[0] == '3';
+  if (lean) {  // P / O in TMEM, two CTAs per SM (experimental)
+    static bool attr3[2] = {false, false};
+    auto k3 = causal ? fwd3_kernel<true> : fwd3_kernel<false>;
+    if (!attr3[causal ? 1 : 0]) {
+      HM_CUDA(cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem3));
+      attr3[causal ? 1 : 0] = true;
+    }
+    k3<<<dim3(S / BQ, B * H), kThreads, kSmem3, s>>>(tm, static_cast<__nv_bfloat16 *>(o), lse, S, H, scale_log2);
     count_launch();
     HM_CUDA(cudaGetLastError());
     return HM_OK;
