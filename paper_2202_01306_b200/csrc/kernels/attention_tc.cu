@@ -17,6 +17,7 @@
 #include <cuda_bf16.h>
 
 #include <mutex>
+#include <type_traits>
 
 #include "../runtime/common.hpp"
 #include "sm100.cuh"
@@ -39,6 +40,7 @@ __device__ __forceinline__ float ex2(float x) {
 }
 
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 
 template <bool CAUSAL>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -236,6 +238,264 @@ __global__ void __launch_bounds__(kThreads, 1)
       *reinterpret_cast<uint4 *>(orow + c) = w;
     }
     lse[(int64_t)(row0 + qb * BQ + r) * H + h] = m + log2f(l);
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// forward, persistent: one CTA per SM walks a list of (sample-head, query
+// block) work items, heaviest first for causal attention.  Same warp roles
+// and per-tile dataflow as fwd_kernel, but the TMEM allocation, barrier set-up
+// and pipeline fill are paid once per SM instead of once per 128 queries: the
+// TMA warp loads the next item's Q (double-buffered) and first K/V tiles, and
+// the MMA warp issues its first Q K^T, while the softmax warps are still on
+// the previous item's last tile and epilogue.  All ring / buffer parities
+// follow one running tile counter across items.
+// ---------------------------------------------------------------------------
+constexpr size_t kSmemP = 1024 + 2 * kTileBytes /*Q x2*/ + 2 * kTileBytes /*K*/ + 2 * kTileBytes /*V*/ + 2 * kPBytes + 512;
+
+struct FwdItems {
+  int nq, bh_count, n_items;
+  __device__ __forceinline__ void item(int i, bool causal, int &bh, int &qb) const {
+    if (causal) {  // heaviest (longest K/V sweep) first
+      qb = nq - 1 - i / bh_count;
+      bh = i % bh_count;
+    } else {
+      qb = i % nq;
+      bh = i / nq;
+    }
+  }
+};
+
+template <bool CAUSAL>
+__global__ void __launch_bounds__(kThreads, 1)
+    fwdp_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16 *__restrict__ out, float *__restrict__ lse,
+                int S, int H, int BH, float scale_log2) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sQ = smem;                  // [2] items
+  uint8_t *sK = sQ + 2 * kTileBytes;   // [2] stages
+  uint8_t *sV = sK + 2 * kTileBytes;   // [2] stages
+  uint8_t *sP = sV + 2 * kTileBytes;   // [2] tiles
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sP + 2 * kPBytes);
+  uint64_t *q_full = bar, *q_empty = bar + 2;
+  uint64_t *kv_full = bar + 4, *kv_empty = bar + 6;
+  uint64_t *s_full = bar + 8, *s_empty = bar + 10;
+  uint64_t *p_full = bar + 12, *p_empty = bar + 14;
+  uint64_t *o_full = bar + 16, *o_empty = bar + 18;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 20);
+
+  const FwdItems W{S / BQ, BH, (S / BQ) * BH};
+  const int d = H * DH;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto nkv_of = [&](int qb) { return CAUSAL ? qb + 1 : S / BKV; };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 128);
+      mbar_init(&p_full[i], 128);
+      mbar_init(&p_empty[i], 1);
+      mbar_init(&o_full[i], 1);
+      mbar_init(&o_empty[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int g = 0, it = 0;
+      for (int i = blockIdx.x; i < W.n_items; i += gridDim.x, ++it) {
+        int bh, qb;
+        W.item(i, CAUSAL, bh, qb);
+        const int b = bh / H, h = bh % H, row0 = b * S;
+        const int qs = it & 1;
+        mbar_wait(&q_empty[qs], ((it >> 1) & 1) ^ 1);
+        mbar_expect_tx(&q_full[qs], kTileBytes);
+        tma_load_2d(sQ + qs * kTileBytes, &tm, &q_full[qs], h * DH, row0 + qb * BQ);
+        const int nkv = nkv_of(qb);
+        for (int j = 0; j < nkv; ++j, ++g) {
+          const int st = g & 1;
+          mbar_wait(&kv_empty[st], ((g >> 1) & 1) ^ 1);
+          mbar_expect_tx(&kv_full[st], 2 * kTileBytes);
+          tma_load_2d(sK + st * kTileBytes, &tm, &kv_full[st], d + h * DH, row0 + j * BKV);
+          tma_load_2d(sV + st * kTileBytes, &tm, &kv_full[st], 2 * d + h * DH, row0 + j * BKV);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = idesc_bf16_f32(BQ, BKV, 0, 0);  // Q K-major, K K-major
+      constexpr uint32_t idesc_o = idesc_bf16_f32(BQ, DH, 0, 1);   // P K-major, V MN-major
+      // flattened (item, tile) sequence; S of tile g+1 is issued before PV of tile g
+      int it_s = 0, j_s = 0, i_s = blockIdx.x, nkv_s = 0;  // cursor of the next S to issue
+      if (i_s < W.n_items) {
+        int bh, qb;
+        W.item(i_s, CAUSAL, bh, qb);
+        nkv_s = nkv_of(qb);
+      }
+      int g_s = 0;
+      auto issue_next_s = [&]() -> bool {
+        if (i_s >= W.n_items) return false;
+        const int qs = it_s & 1;
+        if (j_s == 0) mbar_wait(&q_full[qs], (it_s >> 1) & 1);
+        const int st = g_s & 1, buf = g_s & 1;
+        mbar_wait(&kv_full[st], (g_s >> 1) & 1);
+        mbar_wait(&s_empty[buf], ((g_s >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t q_base = smem_u32(sQ + qs * kTileBytes), k_base = smem_u32(sK + st * kTileBytes);
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk)
+          mma_bf16(tmem + buf * BKV, umma_desc_sw128(q_base + kk * 32, 16, 1024),
+                   umma_desc_sw128(k_base + kk * 32, 16, 1024), idesc_s, kk > 0);
+        mma_commit(&s_full[buf]);
+        ++g_s;
+        if (++j_s == nkv_s) {  // last Q K^T of this item: Q buffer free once it retires
+          mma_commit(&q_empty[qs]);
+          j_s = 0;
+          ++it_s;
+          i_s += gridDim.x;
+          if (i_s < W.n_items) {
+            int bh, qb;
+            W.item(i_s, CAUSAL, bh, qb);
+            nkv_s = nkv_of(qb);
+          }
+        }
+        return true;
+      };
+      issue_next_s();
+      for (int g = 0; g < g_s; ++g) {
+        issue_next_s();
+        const int st = g & 1, buf = g & 1;
+        mbar_wait(&p_full[buf], (g >> 1) & 1);
+        mbar_wait(&o_empty[buf], ((g >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t p_base = smem_u32(sP + buf * kPBytes);
+        const uint32_t v_base = smem_u32(sV + st * kTileBytes);
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk)
+          mma_bf16(tmem + 2 * BKV + buf * DH,
+                   umma_desc_sw128(p_base + (kk >> 2) * (BQ * 128) + (kk & 3) * 32, 16, 1024),
+                   umma_desc_sw128(v_base + kk * 2048, BKV * 128, 1024), idesc_o, kk > 0);
+        mma_commit(&o_full[buf]);
+        mma_commit(&kv_empty[st]);
+        mma_commit(&p_empty[buf]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int r = q * 32 + lane;  // query row inside the block == TMEM lane
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    int g = 0;
+    for (int i = blockIdx.x; i < W.n_items; i += gridDim.x) {
+      int bh, qb;
+      W.item(i, CAUSAL, bh, qb);
+      const int b = bh / H, h = bh % H, row0 = b * S;
+      const int nkv = nkv_of(qb);
+      float o[DH];
+#pragma unroll
+      for (int c = 0; c < DH; ++c) o[c] = 0.f;
+      float m = -INFINITY, l = 0.f, alpha_prev = 1.f;
+      auto add_o = [&](int gg, float alpha) {
+        const int buf = gg & 1;
+        mbar_wait(&o_full[buf], (gg >> 1) & 1);
+        tc_fence_after();
+        uint32_t v[DH];
+#pragma unroll
+        for (int c0 = 0; c0 < DH; c0 += 32)
+          tmem_ld_32x32b_x32(tmem + lane_addr + 2 * BKV + buf * DH + c0, *reinterpret_cast<uint32_t(*)[32]>(v + c0));
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&o_empty[buf]);
+#pragma unroll
+        for (int c = 0; c < DH; ++c) o[c] = o[c] * alpha + __uint_as_float(v[c]);
+      };
+      for (int j = 0; j < nkv; ++j, ++g) {
+        const int buf = g & 1;
+        mbar_wait(&s_full[buf], (g >> 1) & 1);
+        tc_fence_after();
+        const uint32_t s_addr = tmem + lane_addr + buf * BKV;
+        uint32_t v[BKV];
+#pragma unroll
+        for (int c0 = 0; c0 < BKV; c0 += 32)
+          tmem_ld_32x32b_x32(s_addr + c0, *reinterpret_cast<uint32_t(*)[32]>(v + c0));
+        tmem_ld_wait();
+        if (CAUSAL && j == qb) {  // mask on the diagonal tile (key > query)
+#pragma unroll
+          for (int c = 0; c < BKV; ++c)
+            if (c > r) v[c] = __float_as_uint(-INFINITY);
+        }
+        float mx8[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) mx8[e] = __uint_as_float(v[e]);
+#pragma unroll
+        for (int c = 8; c < BKV; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(v[c]));
+        const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+        const float m_new = fmaxf(m, mx * scale_log2);
+        const float alpha = ex2(m - m_new);
+        m = m_new;
+        mbar_wait(&p_empty[buf], ((g >> 1) & 1) ^ 1);
+        uint8_t *prow = sP + buf * kPBytes + r * 128;
+        float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int c0 = 0; c0 < BKV; c0 += 32) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int c = 0; c < 32; c += 2) {
+            const float p0 = ex2(fmaf(__uint_as_float(v[c0 + c]), scale_log2, -m_new));
+            const float p1 = ex2(fmaf(__uint_as_float(v[c0 + c + 1]), scale_log2, -m_new));
+            rs8[(c >> 1) & 7] += p0 + p1;
+            __nv_bfloat162 tb = __floats2bfloat162_rn(p0, p1);
+            pk[c >> 1] = *reinterpret_cast<uint32_t *>(&tb);
+          }
+          uint8_t *atom_row = prow + (c0 >> 6) * (BQ * 128);
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            const int chunk = ((c0 & 63) >> 3) + ch;
+            *reinterpret_cast<uint4 *>(atom_row + ((chunk ^ (r & 7)) << 4)) =
+                make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&s_empty[buf]);
+        fence_async_smem();
+        mbar_arrive(&p_full[buf]);
+        const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+        l = l * alpha + rs;
+        if (j > 0) add_o(g - 1, alpha_prev);
+        alpha_prev = alpha;
+      }
+      add_o(g - 1, alpha_prev);
+      const float inv = 1.f / l;
+      __nv_bfloat16 *orow = out + (int64_t)(row0 + qb * BQ + r) * d + h * DH;
+#pragma unroll
+      for (int c = 0; c < DH; c += 8) {
+        uint4 w;
+        uint32_t *wp = reinterpret_cast<uint32_t *>(&w);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          __nv_bfloat162 t = __floats2bfloat162_rn(o[c + 2 * e] * inv, o[c + 2 * e + 1] * inv);
+          wp[e] = *reinterpret_cast<uint32_t *>(&t);
+        }
+        *reinterpret_cast<uint4 *>(orow + c) = w;
+      }
+      lse[(int64_t)(row0 + qb * BQ + r) * H + h] = m + log2f(l);
+    }
   }
   __syncthreads();
   if (warp == 2) {
@@ -480,6 +740,271 @@ __global__ void __launch_bounds__(kThreads2, 1)
 }
 
 // ---------------------------------------------------------------------------
+// forward, persistent with two query tiles per item: the ping-pong structure
+// of fwd2_kernel (softmax warpgroups A and B share every K/V tile) on the
+// persistent item loop of fwdp_kernel.  An item is the query-block pair
+// (2p, 2p+1) of one (sample, head): under causal masking the two tiles sweep
+// 2p+1 and 2p+2 K/V tiles, so the pair stays balanced, and the item list is
+// ordered heaviest first, so the persistent CTAs finish together.  The causal
+// mask is a separate instantiation of the tile body (only the diagonal tile
+// pays for it).  Q is double-buffered per item.
+// ---------------------------------------------------------------------------
+constexpr size_t kSmem2P = 1024 + 4 * kTileBytes /*Q pair x2*/ + 4 * kTileBytes /*K, V x2*/ + 2 * kPBytes + 512;
+
+template <bool CAUSAL>
+__global__ void __launch_bounds__(kThreads2, 1)
+    fwd2p_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16 *__restrict__ out, float *__restrict__ lse,
+                 int S, int H, int BH, float scale_log2) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sQ = smem;                   // [2 items][2 tiles]
+  uint8_t *sK = sQ + 4 * kTileBytes;    // [2] stages
+  uint8_t *sV = sK + 2 * kTileBytes;    // [2] stages
+  uint8_t *sP = sV + 2 * kTileBytes;    // [2] tiles
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sP + 2 * kPBytes);
+  uint64_t *q_full = bar, *q_empty = bar + 2;        // [item stage]
+  uint64_t *kv_full = bar + 4, *kv_empty = bar + 6;  // [kv stage]
+  uint64_t *s_full = bar + 8, *s_empty = bar + 10;   // [tile]
+  uint64_t *p_full = bar + 12, *p_empty = bar + 14;  // [tile]
+  uint64_t *o_full = bar + 16, *o_empty = bar + 18;  // [tile]
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 20);
+
+  const int nq = S / BQ, np = nq / 2, n_items = np * BH;
+  const int d = H * DH;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr uint32_t C_S = 0, C_O = 2 * BKV;  // TMEM: S_A, S_B | O_A, O_B
+  auto item = [&](int i, int &bh, int &p) {
+    if (CAUSAL) {
+      p = np - 1 - i / BH;
+      bh = i % BH;
+    } else {
+      p = i % np;
+      bh = i / np;
+    }
+  };
+  auto nkv_of = [&](int qb) { return CAUSAL ? qb + 1 : nq; };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 128);
+      mbar_init(&p_full[i], 128);
+      mbar_init(&p_empty[i], 1);
+      mbar_init(&o_full[i], 1);
+      mbar_init(&o_empty[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int g = 0, it = 0;
+      for (int i = blockIdx.x; i < n_items; i += gridDim.x, ++it) {
+        int bh, p;
+        item(i, bh, p);
+        const int b = bh / H, h = bh % H, row0 = b * S;
+        const int qs = it & 1;
+        mbar_wait(&q_empty[qs], ((it >> 1) & 1) ^ 1);
+        mbar_expect_tx(&q_full[qs], 2 * kTileBytes);
+        tma_load_2d(sQ + (2 * qs) * kTileBytes, &tm, &q_full[qs], h * DH, row0 + (2 * p) * BQ);
+        tma_load_2d(sQ + (2 * qs + 1) * kTileBytes, &tm, &q_full[qs], h * DH, row0 + (2 * p + 1) * BQ);
+        const int nkv = nkv_of(2 * p + 1);
+        for (int j = 0; j < nkv; ++j, ++g) {
+          const int st = g & 1;
+          mbar_wait(&kv_empty[st], ((g >> 1) & 1) ^ 1);
+          mbar_expect_tx(&kv_full[st], 2 * kTileBytes);
+          tma_load_2d(sK + st * kTileBytes, &tm, &kv_full[st], d + h * DH, row0 + j * BKV);
+          tma_load_2d(sV + st * kTileBytes, &tm, &kv_full[st], 2 * d + h * DH, row0 + j * BKV);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = idesc_bf16_f32(BQ, BKV, 0, 0);
+      constexpr uint32_t idesc_o = idesc_bf16_f32(BQ, DH, 0, 1);
+      int g0 = 0, it = 0;
+      int cs[2] = {0, 0}, cp[2] = {0, 0};  // S issues / PV issues per tile
+      for (int i = blockIdx.x; i < n_items; i += gridDim.x, ++it) {
+        int bh, p;
+        item(i, bh, p);
+        const int nkv_a = nkv_of(2 * p), nkv_b = nkv_of(2 * p + 1);
+        const int qs = it & 1;
+        mbar_wait(&q_full[qs], (it >> 1) & 1);
+        auto issue_s = [&](int t, int j) {  // S_t(j) = Q_t K_j^T
+          const int gj = g0 + j, st = gj & 1;
+          if (t == 0) mbar_wait(&kv_full[st], (gj >> 1) & 1);
+          mbar_wait(&s_empty[t], (cs[t] & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t q_base = smem_u32(sQ + (2 * qs + t) * kTileBytes), k_base = smem_u32(sK + st * kTileBytes);
+#pragma unroll
+          for (int kk = 0; kk < DH / 16; ++kk)
+            mma_bf16(tmem + C_S + t * BKV, umma_desc_sw128(q_base + kk * 32, 16, 1024),
+                     umma_desc_sw128(k_base + kk * 32, 16, 1024), idesc_s, kk > 0);
+          mma_commit(&s_full[t]);
+          ++cs[t];
+        };
+        auto issue_pv = [&](int t, int j) {  // O_t(j) = P_t(j) V_j
+          const int st = (g0 + j) & 1;
+          mbar_wait(&p_full[t], cp[t] & 1);
+          mbar_wait(&o_empty[t], (cp[t] & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t p_base = smem_u32(sP + t * kPBytes), v_base = smem_u32(sV + st * kTileBytes);
+#pragma unroll
+          for (int kk = 0; kk < BKV / 16; ++kk)
+            mma_bf16(tmem + C_O + t * DH, umma_desc_sw128(p_base + (kk >> 2) * (BQ * 128) + (kk & 3) * 32, 16, 1024),
+                     umma_desc_sw128(v_base + kk * 2048, BKV * 128, 1024), idesc_o, kk > 0);
+          mma_commit(&o_full[t]);
+          mma_commit(&p_empty[t]);
+          ++cp[t];
+        };
+        issue_s(0, 0);
+        issue_s(1, 0);
+        for (int j = 0; j < nkv_b; ++j) {
+          if (j < nkv_a) {
+            issue_pv(0, j);
+            if (j + 1 < nkv_a) issue_s(0, j + 1);
+          }
+          issue_pv(1, j);
+          mma_commit(&kv_empty[(g0 + j) & 1]);
+          if (j + 1 < nkv_b) {
+            if (!(j + 1 < nkv_a)) mbar_wait(&kv_full[(g0 + j + 1) & 1], ((g0 + j + 1) >> 1) & 1);
+            issue_s(1, j + 1);
+          }
+        }
+        mma_commit(&q_empty[qs]);  // every Q K^T of this item issued: Q pair free once they retire
+        g0 += nkv_b;
+      }
+    }
+  } else if (warp >= 4) {
+    const int t = (warp - 4) >> 2;  // query tile: 0 = A (2p), 1 = B (2p+1)
+    const int q = warp & 3;
+    const int r = q * 32 + lane;
+    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
+    const uint32_t s_addr = tmem + lane_addr + C_S + t * BKV;
+    int n = 0;  // tiles this warpgroup has processed (buffer parities)
+    for (int i = blockIdx.x; i < n_items; i += gridDim.x) {
+      int bh, p;
+      item(i, bh, p);
+      const int b = bh / H, h = bh % H, row0 = b * S;
+      const int qb = 2 * p + t;
+      const int nkv = nkv_of(qb);
+      float o[DH];
+#pragma unroll
+      for (int c = 0; c < DH; ++c) o[c] = 0.f;
+      float m = -INFINITY, l = 0.f, alpha_prev = 1.f;
+      auto add_o = [&](int nn, float alpha) {
+        mbar_wait(&o_full[t], nn & 1);
+        tc_fence_after();
+        uint32_t v[DH];
+#pragma unroll
+        for (int c0 = 0; c0 < DH; c0 += 32)
+          tmem_ld_32x32b_x32(tmem + lane_addr + C_O + t * DH + c0, *reinterpret_cast<uint32_t(*)[32]>(v + c0));
+        tmem_ld_wait();
+        tc_fence_before();
+        mbar_arrive(&o_empty[t]);
+#pragma unroll
+        for (int c = 0; c < DH; ++c) o[c] = o[c] * alpha + __uint_as_float(v[c]);
+      };
+      // one K/V tile: row max (pass 1), exp / row sum / bf16 P (pass 2)
+      auto tile = [&](auto diag_tag) -> float {
+        constexpr bool DIAG = decltype(diag_tag)::value;
+        float mx = -INFINITY;
+#pragma unroll
+        for (int c0 = 0; c0 < BKV; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(s_addr + c0, v);
+          tmem_ld_wait();
+          float m8[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) m8[e] = -INFINITY;
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const float x = (DIAG && c0 + c > r) ? -INFINITY : __uint_as_float(v[c]);
+            m8[c & 7] = fmaxf(m8[c & 7], x);
+          }
+          mx = fmaxf(mx, fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                                fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))));
+        }
+        const float m_new = fmaxf(m, mx * scale_log2);
+        const float alpha = ex2(m - m_new);
+        m = m_new;
+        mbar_wait(&p_empty[t], (n & 1) ^ 1);
+        uint8_t *prow = sP + t * kPBytes + r * 128;
+        float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int c0 = 0; c0 < BKV; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(s_addr + c0, v);
+          tmem_ld_wait();
+          uint32_t pk[16];
+#pragma unroll
+          for (int c = 0; c < 32; c += 2) {
+            float p0 = ex2(fmaf(__uint_as_float(v[c]), scale_log2, -m_new));
+            float p1 = ex2(fmaf(__uint_as_float(v[c + 1]), scale_log2, -m_new));
+            if (DIAG && c0 + c > r) p0 = 0.f;
+            if (DIAG && c0 + c + 1 > r) p1 = 0.f;
+            rs8[(c >> 1) & 7] += p0 + p1;
+            __nv_bfloat162 tb = __floats2bfloat162_rn(p0, p1);
+            pk[c >> 1] = *reinterpret_cast<uint32_t *>(&tb);
+          }
+          uint8_t *atom_row = prow + (c0 >> 6) * (BQ * 128);
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            const int chunk = ((c0 & 63) >> 3) + ch;
+            *reinterpret_cast<uint4 *>(atom_row + ((chunk ^ (r & 7)) << 4)) =
+                make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&s_empty[t]);
+        fence_async_smem();
+        mbar_arrive(&p_full[t]);
+        const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+        l = l * alpha + rs;
+        return alpha;
+      };
+      for (int j = 0; j < nkv; ++j, ++n) {
+        mbar_wait(&s_full[t], n & 1);
+        tc_fence_after();
+        const float alpha = (CAUSAL && j == qb) ? tile(std::true_type{}) : tile(std::false_type{});
+        if (j > 0) add_o(n - 1, alpha_prev);
+        alpha_prev = alpha;
+      }
+      add_o(n - 1, alpha_prev);
+      const float inv = 1.f / l;
+      __nv_bfloat16 *orow = out + (int64_t)(row0 + qb * BQ + r) * d + h * DH;
+#pragma unroll
+      for (int c = 0; c < DH; c += 8) {
+        uint4 w;
+        uint32_t *wp = reinterpret_cast<uint32_t *>(&w);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          __nv_bfloat162 tb = __floats2bfloat162_rn(o[c + 2 * e] * inv, o[c + 2 * e + 1] * inv);
+          wp[e] = *reinterpret_cast<uint32_t *>(&tb);
+        }
+        *reinterpret_cast<uint4 *>(orow + c) = w;
+      }
+      lse[(int64_t)(row0 + qb * BQ + r) * H + h] = m + log2f(l);
+    }
+  }
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // forward, lean variant: two CTAs per SM hide each other's latencies.  P goes
 // to TMEM (bf16 pairs packed into S's own columns, FA4-style) and is read by
 // the PV MMA as its A operand, O accumulates in TMEM (rescaled in place by the
@@ -701,7 +1226,7 @@ constexpr size_t kSmemBwd = 1024 + 2 * kTileBytes /*K,V*/ + 4 * kTileBytes /*Q,d
                             2 * 2 * BQ * 4 /*lse,D x2*/ + 512;
 
 template <bool CAUSAL>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads2, 1)
     bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                const __grid_constant__ CUtensorMap tm_dq,
                const float *__restrict__ lse, const float *__restrict__ dvec, float *__restrict__ dq_acc,
@@ -745,11 +1270,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&q_empty[i], 1);
     }
     mbar_init(st_full, 1);
-    mbar_init(st_empty, 128);
-    mbar_init(p_full, 128);
+    mbar_init(st_empty, 256);
+    mbar_init(p_full, 256);
     mbar_init(p_empty, 1);
     mbar_init(dq_full, 1);
-    mbar_init(dq_empty, 128);
+    mbar_init(dq_empty, 256);
     mbar_init(acc_full, 1);
     fence_barrier_init();
   }
@@ -780,11 +1305,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(kv_full, 0);
       const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV);
       const uint32_t p_base = smem_u32(sP), ds_base = smem_u32(sdS);
-      for (int i = q_begin, n = 0; i < nq; ++i, ++n) {
+      const int count = nq - q_begin;
+      // S^T = K Q^T and dP^T = V dO^T of block n (TMEM C_ST / C_DP)
+      auto issue_st = [&](int n) {
         const int st = n & 1;
-        const uint32_t ph = n & 1;
         mbar_wait(&q_full[st], (n >> 1) & 1);
-        mbar_wait(st_empty, ph ^ 1);
+        mbar_wait(st_empty, (n & 1) ^ 1);
         tc_fence_after();
         const uint32_t q_base = smem_u32(sQ + st * kTileBytes), do_base = smem_u32(sdO + st * kTileBytes);
 #pragma unroll
@@ -795,8 +1321,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                    umma_desc_sw128(do_base + kk * 32, 16, 1024), id_kk, kk > 0);
         }
         mma_commit(st_full);
+      };
+      issue_st(0);
+      for (int n = 0; n < count; ++n) {
+        const int st = n & 1;
+        const uint32_t ph = n & 1;
+        // block n+1's S^T / dP^T go in as soon as the softmax warps have read
+        // block n's (st_empty), ahead of block n's gradient MMAs, so the next
+        // elementwise pass never waits for them
+        if (n + 1 < count) issue_st(n + 1);
+        const uint32_t q_base = smem_u32(sQ + st * kTileBytes), do_base = smem_u32(sdO + st * kTileBytes);
         mbar_wait(p_full, ph);
-        mbar_wait(dq_empty, ph ^ 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < BQ / 16; ++kk) {  // reduction over the 128 queries
@@ -806,6 +1341,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_bf16(tmem + C_DK, umma_desc_sw128(ds_base + a_off, 16, 1024),
                    umma_desc_sw128(q_base + kk * 2048, BQ * 128, 1024), id_kmn, (n > 0 || kk > 0) ? 1u : 0u);
         }
+        mbar_wait(dq_empty, ph ^ 1);  // the previous block's dQ has left TMEM
+        tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk)  // reduction over the 128 keys
           mma_bf16(tmem + C_DQ, umma_desc_sw128(ds_base + kk * 2048, BKV * 128, 1024),
@@ -817,127 +1354,133 @@ __global__ void __launch_bounds__(kThreads, 1)
       mma_commit(acc_full);
     }
   } else if (warp >= 4) {
+    // two softmax warpgroups on the same TMEM lanes (key rows): warpgroup wg
+    // owns queries [64 wg, 64 wg + 64) of every block, half of dQ's columns,
+    // and dV (wg 0) or dK (wg 1) at the end -- two warps per SM sub-partition
+    // hide each other's MUFU / TMEM / shared-memory latencies
+    const int wg = (warp - 4) >> 2;
     const int q4 = warp & 3;
     const int r = q4 * 32 + lane;  // key row (S^T, dP^T, dV, dK) / query row (dQ) == TMEM lane
     const uint32_t lane_addr = (uint32_t)(q4 * 32) << 16;
+    // lse (wg 0) and D (wg 1) of the query blocks (tiny, strided: plain
+    // loads), fetched one block ahead so their latency hides behind the
+    // previous block's work
+    const float *src = wg == 0 ? lse : dvec;
+    float *dst = wg == 0 ? sL : sD;
+    float x_next = src[(int64_t)(row0 + q_begin * BQ + r) * H + h];
+    // dQ of block nn (query block qblk): TMEM -> one TMA reduce-add of the whole
+    // 128 x 64 fp32 tile (in L2) instead of 8192 scalar atomics, staged in
+    // SW128 rows (conflict-free writes); each warpgroup drains 32 columns
+    auto dq_out = [&](int qblk, int nn) {
+      mbar_wait(dq_full, nn & 1);
+      tc_fence_after();
+      uint32_t q[32];
+      tmem_ld_32x32b_x32(tmem + lane_addr + C_DQ + wg * 32, q);
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(dq_empty);
+      if (wg == 0 && r == 0) bulk_wait_read0();  // the previous block's reduce has read the stage
+      asm volatile("bar.sync 2, 256;" ::: "memory");
+      uint8_t *chunk = sDQ + wg * (BQ * 128) + r * 128;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        *reinterpret_cast<float4 *>(chunk + ((j ^ (r & 7)) << 4)) =
+            make_float4(__uint_as_float(q[4 * j]) * scale, __uint_as_float(q[4 * j + 1]) * scale,
+                        __uint_as_float(q[4 * j + 2]) * scale, __uint_as_float(q[4 * j + 3]) * scale);
+      fence_async_smem();
+      asm volatile("bar.sync 2, 256;" ::: "memory");
+      if (wg == 0 && r == 0) {
+#pragma unroll
+        for (int c = 0; c < DH / 32; ++c)
+          tma_reduce_add_2d(&tm_dq, sDQ + c * (BQ * 128), h * DH + 32 * c, row0 + qblk * BQ);
+        bulk_commit();
+      }
+    };
+    const int hq = wg;
+    uint8_t *prow = sP + r * 128 + hq * (BKV * 128);
+    uint8_t *dsrow = sdS + r * 128 + hq * (BKV * 128);
     for (int i = q_begin, n = 0; i < nq; ++i, ++n) {
       const int st = n & 1;
       const uint32_t ph = n & 1;
-      // lse and D of this query block (tiny: read through L1, not TMA)
-      sL[st * BQ + r] = lse[(int64_t)(row0 + i * BQ + r) * H + h];
-      sD[st * BQ + r] = dvec[(int64_t)(row0 + i * BQ + r) * H + h];
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      dst[st * BQ + r] = x_next;
+      if (i + 1 < nq) x_next = src[(int64_t)(row0 + (i + 1) * BQ + r) * H + h];
+      asm volatile("bar.sync 1, 256;" ::: "memory");
       mbar_wait(st_full, ph);
       tc_fence_after();
       const bool diag = CAUSAL && i == kb;
       const float *Ls = sL + st * BQ;
       const float *Ds = sD + st * BQ;
-      uint8_t *prow = sP + r * 128;
-      uint8_t *dsrow = sdS + r * 128;
-      // two halves of 64 queries (one swizzle atom each) keep S and dP rows in registers
-#pragma unroll 1
-      for (int hq = 0; hq < 2; ++hq) {
-        uint32_t sv[64], dp[64];
+      // this warpgroup's 64 queries in two 32-column chunks; the first chunk is
+      // computed before waiting for the previous block's gradient MMAs to
+      // release P^T / dS^T, so that wait overlaps it
 #pragma unroll
-        for (int c0 = 0; c0 < 64; c0 += 32) {
-          tmem_ld_32x32b_x32(tmem + lane_addr + C_ST + hq * 64 + c0, *reinterpret_cast<uint32_t(*)[32]>(sv + c0));
-          tmem_ld_32x32b_x32(tmem + lane_addr + C_DP + hq * 64 + c0, *reinterpret_cast<uint32_t(*)[32]>(dp + c0));
-        }
+      for (int c0 = 0; c0 < 64; c0 += 32) {
+        uint32_t sv[32], dp[32];
+        tmem_ld_32x32b_x32(tmem + lane_addr + C_ST + hq * 64 + c0, sv);
+        tmem_ld_32x32b_x32(tmem + lane_addr + C_DP + hq * 64 + c0, dp);
         tmem_ld_wait();
-        if (hq == 1) {
+        if (c0 == 32) {
           tc_fence_before();
           mbar_arrive(st_empty);  // S^T / dP^T fully read: the next block's MMAs may overwrite
-        } else {
-          mbar_wait(p_empty, ph ^ 1);  // the previous block's MMAs have consumed P^T / dS^T
         }
-#pragma unroll
-        for (int c0 = 0; c0 < 64; c0 += 32) {
-          uint32_t pk[16], dk[16];
+        uint32_t pk[16], dk[16];
+        // the causal mask is a separate instantiation: only the diagonal block pays for it
+        auto elementwise = [&](auto diag_tag) {
+          constexpr bool DIAG = decltype(diag_tag)::value;
 #pragma unroll
           for (int c = 0; c < 32; c += 2) {
             const int qi = hq * 64 + c0 + c;
-            float p0 = ex2(fmaf(__uint_as_float(sv[c0 + c]), scale_log2, -Ls[qi]));
-            float p1 = ex2(fmaf(__uint_as_float(sv[c0 + c + 1]), scale_log2, -Ls[qi + 1]));
-            if (diag && qi < r) p0 = 0.f;  // query < key: masked
-            if (diag && qi + 1 < r) p1 = 0.f;
-            const float s0 = p0 * (__uint_as_float(dp[c0 + c]) - Ds[qi]);
-            const float s1 = p1 * (__uint_as_float(dp[c0 + c + 1]) - Ds[qi + 1]);
+            float p0 = ex2(fmaf(__uint_as_float(sv[c]), scale_log2, -Ls[qi]));
+            float p1 = ex2(fmaf(__uint_as_float(sv[c + 1]), scale_log2, -Ls[qi + 1]));
+            if (DIAG && qi < r) p0 = 0.f;  // query < key: masked
+            if (DIAG && qi + 1 < r) p1 = 0.f;
+            const float s0 = p0 * (__uint_as_float(dp[c]) - Ds[qi]);
+            const float s1 = p1 * (__uint_as_float(dp[c + 1]) - Ds[qi + 1]);
             __nv_bfloat162 tp = __floats2bfloat162_rn(p0, p1), td = __floats2bfloat162_rn(s0, s1);
             pk[c >> 1] = *reinterpret_cast<uint32_t *>(&tp);
             dk[c >> 1] = *reinterpret_cast<uint32_t *>(&td);
           }
-          const uint32_t atom = hq * (BKV * 128);
+        };
+        if (diag) elementwise(std::true_type{});
+        else elementwise(std::false_type{});
+        if (c0 == 0) mbar_wait(p_empty, ph ^ 1);  // the previous block's MMAs have consumed P^T / dS^T
 #pragma unroll
-          for (int ch = 0; ch < 4; ++ch) {
-            const int chunk = (c0 >> 3) + ch;
-            const uint32_t off = atom + ((chunk ^ (r & 7)) << 4);
-            *reinterpret_cast<uint4 *>(prow + off) = make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
-            *reinterpret_cast<uint4 *>(dsrow + off) =
-                make_uint4(dk[4 * ch], dk[4 * ch + 1], dk[4 * ch + 2], dk[4 * ch + 3]);
-          }
+        for (int ch = 0; ch < 4; ++ch) {
+          const uint32_t off = (((c0 >> 3) + ch) ^ (r & 7)) << 4;
+          *reinterpret_cast<uint4 *>(prow + off) = make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+          *reinterpret_cast<uint4 *>(dsrow + off) = make_uint4(dk[4 * ch], dk[4 * ch + 1], dk[4 * ch + 2], dk[4 * ch + 3]);
         }
       }
       fence_async_smem();
       mbar_arrive(p_full);
-      // dQ_i rows (TMEM lane = query) -> fp32 atomics
-      mbar_wait(dq_full, ph);
-      tc_fence_after();
-      uint32_t q[DH];
-#pragma unroll
-      for (int c0 = 0; c0 < DH; c0 += 32)
-        tmem_ld_32x32b_x32(tmem + lane_addr + C_DQ + c0, *reinterpret_cast<uint32_t(*)[32]>(q + c0));
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(dq_empty);
-      // dQ_i: one TMA reduce-add of the whole 128 x 64 fp32 tile (in L2) instead
-      // of 8192 scalar atomics -- staged in SW128 rows (conflict-free writes)
-      if (r == 0) bulk_wait_read0();  // the previous block's reduce has read the stage
-      asm volatile("bar.sync 2, 128;" ::: "memory");
-#pragma unroll
-      for (int c = 0; c < DH / 32; ++c) {
-        uint8_t *chunk = sDQ + c * (BQ * 128) + r * 128;
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          *reinterpret_cast<float4 *>(chunk + ((j ^ (r & 7)) << 4)) =
-              make_float4(__uint_as_float(q[32 * c + 4 * j]) * scale, __uint_as_float(q[32 * c + 4 * j + 1]) * scale,
-                          __uint_as_float(q[32 * c + 4 * j + 2]) * scale, __uint_as_float(q[32 * c + 4 * j + 3]) * scale);
-      }
-      fence_async_smem();
-      asm volatile("bar.sync 2, 128;" ::: "memory");
-      if (r == 0) {
-#pragma unroll
-        for (int c = 0; c < DH / 32; ++c) tma_reduce_add_2d(&tm_dq, sDQ + c * (BQ * 128), h * DH + 32 * c, row0 + i * BQ);
-        bulk_commit();
-      }
+      // the previous block's dQ is complete by now (its MMAs finished before P^T
+      // could be rewritten): drain it while this block's gradient MMAs run
+      if (n > 0) dq_out(i - 1, n - 1);
     }
-    if (r == 0) bulk_wait0();
-    // dV, dK of this key block
+    dq_out(nq - 1, nq - 1 - q_begin);
+    if (wg == 0 && r == 0) bulk_wait0();
+    // dV (warpgroup 0) or dK (warpgroup 1) of this key block
     mbar_wait(acc_full, 0);
     tc_fence_after();
-    uint32_t vv[DH], kk2[DH];
+    uint32_t acc[DH];
 #pragma unroll
-    for (int c0 = 0; c0 < DH; c0 += 32) {
-      tmem_ld_32x32b_x32(tmem + lane_addr + C_DV + c0, *reinterpret_cast<uint32_t(*)[32]>(vv + c0));
-      tmem_ld_32x32b_x32(tmem + lane_addr + C_DK + c0, *reinterpret_cast<uint32_t(*)[32]>(kk2 + c0));
-    }
+    for (int c0 = 0; c0 < DH; c0 += 32)
+      tmem_ld_32x32b_x32(tmem + lane_addr + (wg == 0 ? C_DV : C_DK) + c0, *reinterpret_cast<uint32_t(*)[32]>(acc + c0));
     tmem_ld_wait();
     const int64_t ld = 3 * (int64_t)d;
-    __nv_bfloat16 *dk_row = dqkv + (int64_t)(row0 + kb * BKV + r) * ld + d + h * DH;
-    __nv_bfloat16 *dv_row = dk_row + d;
+    __nv_bfloat16 *orow = dqkv + (int64_t)(row0 + kb * BKV + r) * ld + (wg == 0 ? 2 * d : d) + h * DH;
+    const float osc = wg == 0 ? 1.f : scale;
 #pragma unroll
     for (int c = 0; c < DH; c += 8) {
-      uint4 wk, wv;
-      uint32_t *pk = reinterpret_cast<uint32_t *>(&wk), *pv = reinterpret_cast<uint32_t *>(&wv);
+      uint4 w;
+      uint32_t *pw = reinterpret_cast<uint32_t *>(&w);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        __nv_bfloat162 a = __floats2bfloat162_rn(__uint_as_float(kk2[c + 2 * e]) * scale,
-                                                 __uint_as_float(kk2[c + 2 * e + 1]) * scale);
-        __nv_bfloat162 bvv = __floats2bfloat162_rn(__uint_as_float(vv[c + 2 * e]), __uint_as_float(vv[c + 2 * e + 1]));
-        pk[e] = *reinterpret_cast<uint32_t *>(&a);
-        pv[e] = *reinterpret_cast<uint32_t *>(&bvv);
+        __nv_bfloat162 a = __floats2bfloat162_rn(__uint_as_float(acc[c + 2 * e]) * osc,
+                                                 __uint_as_float(acc[c + 2 * e + 1]) * osc);
+        pw[e] = *reinterpret_cast<uint32_t *>(&a);
       }
-      *reinterpret_cast<uint4 *>(dk_row + c) = wk;
-      *reinterpret_cast<uint4 *>(dv_row + c) = wv;
+      *reinterpret_cast<uint4 *>(orow + c) = w;
     }
   }
   __syncthreads();
@@ -986,7 +1529,7 @@ int backward_main(const void *qkv, const void *dout, const float *lse, const flo
     attr[causal ? 1 : 0] = true;
   }
   const float scale = 1.f / sqrtf((float)DH);
-  k<<<dim3(S / BKV, B * H), kThreads, kSmemBwd, s>>>(tq, td, tdq, lse, dvec, dq_acc, static_cast<__nv_bfloat16 *>(dqkv), S,
+  k<<<dim3(S / BKV, B * H), kThreads2, kSmemBwd, s>>>(tq, td, tdq, lse, dvec, dq_acc, static_cast<__nv_bfloat16 *>(dqkv), S,
                                                       H, 1.4426950408889634f * scale, scale);
   count_launch();
   HM_CUDA(cudaGetLastError());
@@ -1011,13 +1554,16 @@ int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causa
     return fail(HM_ERR_DEVICE, "attention tensor map encode failed");
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
   ProfScope ps(KC_ATTN_FWD, s, 4.0 * B * (double)S * S * H * DH * (causal ? 0.5 : 1.0), (double)B * S * H * DH * 2 * 4);
-  static const bool two_tiles = !(getenv("HM_ATTN_FWD") && (getenv("HM_ATTN_FWD")[0] == '1' ||
-                                                             getenv("HM_ATTN_FWD")[0] == '3'));
+  // HM_ATTN_FWD: unset = persistent kernel over query-block pairs (S % 256 ==
+  // 0; causal from S = 1024), else the persistent single-tile kernel (causal)
+  // or one CTA per query block; 1 = one CTA per query block; 2 = two tiles per CTA (full
+  // attention); 3 = lean (P/O in TMEM); p = persistent single tile; q =
+  // persistent pairs
+  static const char *mode_env = getenv("HM_ATTN_FWD");
+  static const char mode = mode_env ? mode_env[0] : 'd';
+  const bool two_tiles = mode == '2';
   // two query tiles per CTA (ping-pong softmax warpgroups) for full attention:
-  // 1.31x at 8 x 512 x 16 heads.  Causal attention stays on one tile per CTA:
-  // pairing blocks either unbalances the CTAs (2p, 2p+1) or leaves the longer
-  // tile running alone for most of its K/V sweep (p, nq-1-p) -- both measured
-  // slower than the single-tile kernel's finer-grained 128-query CTAs.
+  // 1.31x at 8 x 512 x 16 heads.
   if (two_tiles && !causal && S % (2 * BQ) == 0) {
     static bool attr2[2] = {false, false};
     auto k2 = causal ? fwd2_kernel<true> : fwd2_kernel<false>;
@@ -1030,7 +1576,41 @@ int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causa
     HM_CUDA(cudaGetLastError());
     return HM_OK;
   }
-  static const bool lean = getenv("HM_ATTN_FWD") && getenv("HM_ATTN_FWD")[0] == '3';
+  // pairs win from S = 1024 causal (1771 vs 2073 ns per tile and SM, 25 heads);
+  // shorter causal sequences have too little work per pair
+  if ((mode == 'q' || (mode == 'd' && (!causal || S >= 1024))) && S % (2 * BQ) == 0) {  // persistent pairs
+    static bool attrq[2] = {false, false};
+    static int sms_q = 0;
+    if (!sms_q) HM_CUDA(cudaDeviceGetAttribute(&sms_q, cudaDevAttrMultiProcessorCount, 0));
+    auto kq = causal ? fwd2p_kernel<true> : fwd2p_kernel<false>;
+    if (!attrq[causal ? 1 : 0]) {
+      HM_CUDA(cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem2P));
+      attrq[causal ? 1 : 0] = true;
+    }
+    const int items = (S / (2 * BQ)) * B * H;
+    kq<<<dim3(items < sms_q ? items : sms_q), kThreads2, kSmem2P, s>>>(tm, static_cast<__nv_bfloat16 *>(o), lse, S, H,
+                                                                      B * H, scale_log2);
+    count_launch();
+    HM_CUDA(cudaGetLastError());
+    return HM_OK;
+  }
+  if (mode == 'p' || (mode == 'd' && causal)) {  // persistent, one CTA per SM
+    static bool attrp[2] = {false, false};
+    static int sms = 0;
+    if (!sms) HM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    auto kp = causal ? fwdp_kernel<true> : fwdp_kernel<false>;
+    if (!attrp[causal ? 1 : 0]) {
+      HM_CUDA(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemP));
+      attrp[causal ? 1 : 0] = true;
+    }
+    const int items = (S / BQ) * B * H;
+    kp<<<dim3(items < sms ? items : sms), kThreads, kSmemP, s>>>(tm, static_cast<__nv_bfloat16 *>(o), lse, S, H, B * H,
+                                                                  scale_log2);
+    count_launch();
+    HM_CUDA(cudaGetLastError());
+    return HM_OK;
+  }
+  static const bool lean = mode == '3';
   if (lean) {  // P / O in TMEM, two CTAs per SM (experimental)
     static bool attr3[2] = {false, false};
     auto k3 = causal ? fwd3_kernel<true> : fwd3_kernel<false>;

@@ -303,6 +303,24 @@ def test_attention_bwd_tcgen05_opt_in():
     assert r.returncode == 0, r.stderr[-2000:]
 
 
+@pytest.mark.parametrize("mode", ["1", "2", "3", "p", "q"])
+def test_attention_fwd_every_variant(mode):
+    """Every forward variant (HM_ATTN_FWD is read once per process, so each runs
+    in a subprocess) on shapes where the persistent kernel walks one item per
+    CTA, several items per CTA, and a ragged last round."""
+    import subprocess
+    import sys
+    here = __import__("os").path.dirname(__import__("os").path.abspath(__file__))
+    cases = [(2, 128, 4, True), (1, 512, 2, False), (2, 1024, 3, True), (3, 1024, 25, True), (2, 512, 40, False),
+             (1, 256, 25, True)]
+    code = (f"import torch, sys; sys.path.insert(0, {here!r}); sys.path.insert(0, {here + '/..'!r}); "
+            "import test_kernels_gpu as T; from paper_2202_01306_b200 import ops; "
+            f"[T.test_attention_fwd_tcgen05_matches(ops, *c) for c in {cases!r}]")
+    env = dict(__import__("os").environ, HM_ATTN_FWD=mode)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+
+
 def _conv_ref(x, w):
     import torch.nn.functional as F
     return F.conv2d(x.float().permute(0, 3, 1, 2), w.float().permute(0, 3, 1, 2), padding=1).permute(0, 2, 3, 1)

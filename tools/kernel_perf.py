@@ -155,6 +155,34 @@ def bench_attn():
                           "peak": tf_peak, "peak_kind": kind}), flush=True)
 
 
+def bench_attn_sweep():
+    """Forward time per 128x128 tile as the tiles per CTA grow (same total
+    tiles): separates per-CTA fixed cost from per-tile cost.  Graph-timed,
+    back-to-back launches (no flush), so launch latency is excluded."""
+    DH = 64
+    total_tiles = 2048 * 16
+    for causal in (False, True):
+        for S in (256, 512, 1024, 2048, 4096):
+            nq = S // 128
+            per_bh = nq * nq if not causal else nq * (nq + 1) // 2
+            BH = max(1, total_tiles // per_bh)
+            H = 16
+            B = max(1, BH // H)
+            d = H * DH
+            qkv = torch.randn(B * S, 3 * d, device="cuda").to(torch.bfloat16)
+            out = torch.empty(B * S, d, device="cuda", dtype=torch.bfloat16)
+            lse = torch.empty(B * S, H, device="cuda")
+            ms = time_graph(lambda: ops.attn_fwd(qkv, out, lse, batch=B, seq=S, heads=H, head_dim=DH, causal=causal),
+                            reps=10)
+            tiles = B * H * per_bh
+            fl = 4.0 * B * S * S * H * DH * (0.5 if causal else 1.0)
+            print(json.dumps({"kernel": "attn_fwd_sweep", "causal": causal, "S": S, "B": B, "H": H,
+                              "ctas": B * H * nq, "tiles": tiles, "ms": round(ms, 4),
+                              "ns_per_tile_per_sm": round(ms * 1e6 * 148 / tiles, 1),
+                              "tflops": round(fl / ms / 1e9, 1),
+                              "env": os.environ.get("HM_ATTN_FWD")}), flush=True)
+
+
 def bench_ln():
     _, hbm, kind = peaks()
     for rows, d in ((4096, 1600), (4096, 1024), (4096, 8192)):
@@ -201,6 +229,8 @@ if __name__ == "__main__":
     if what == "gemm_sweep":
         SWEEP = [(bn, cg, 0) for cg in (1, 2) for bn in (128, 192, 256) if not (bn == 192 and cg == 2)]
         what = "gemm"
+    if what == "attn_sweep":
+        bench_attn_sweep()
     if what in ("attn", "all"):
         bench_attn()
     if what in ("gemm", "all"):
