@@ -305,6 +305,141 @@ __global__ void ln_bwd_kernel(const float *__restrict__ dy, const float *__restr
   }
 }
 
+// Row-batched variant (default for d <= 2048): the 256 threads of a block
+// own fixed float4 columns (thread t: columns t, t + 256, ...), so every row
+// is read with fully coalesced 16-B loads exactly once (dy, x, resid), the
+// per-row statistics c1 / c2 of RB rows at a time are combined with one
+// block reduction, and dgamma / dbeta accumulate in registers across all the
+// block's rows -- one global atomic per column per block instead of two
+// shared-memory atomics per element.
+template <int NV, int RB>
+__global__ void __launch_bounds__(256, 1)
+    ln_bwd_tile_kernel(const float *__restrict__ dy, const float *__restrict__ x, const float *__restrict__ mean,
+                       const float *__restrict__ rstd, const float *__restrict__ gam, const float *resid, float *out,
+                       __nv_bfloat16 *__restrict__ out_bf, float *__restrict__ dgam, float *__restrict__ dbet,
+                       int64_t rows, int d, int rows_per_block) {
+  pdl_wait();
+  __shared__ float red[2][8][2 * RB];
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int n4 = d >> 2;
+  const float inv_d = 1.f / (float)d;
+  float4 gg[NV], ag[NV], ab[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int c = t + 256 * k;
+    gg[k] = c < n4 ? reinterpret_cast<const float4 *>(gam)[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+    ag[k] = ab[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const int64_t r_begin = (int64_t)blockIdx.x * rows_per_block;
+  const int64_t r_end = min(rows, r_begin + rows_per_block);
+  int parity = 0;
+  for (int64_t r0 = r_begin; r0 < r_end; r0 += RB, parity ^= 1) {
+    float4 a[RB][NV], v[RB][NV];
+    float mu[RB], rs[RB], c1[RB], c2[RB];
+#pragma unroll
+    for (int j = 0; j < RB; ++j) {
+      const int64_t r = r0 + j;
+      const bool ok = r < r_end;
+      mu[j] = ok ? mean[r] : 0.f;
+      rs[j] = ok ? rstd[r] : 0.f;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const int c = t + 256 * k;
+        const bool in = ok && c < n4;
+        a[j][k] = in ? reinterpret_cast<const float4 *>(dy + r * d)[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[j][k] = in ? reinterpret_cast<const float4 *>(x + r * d)[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < RB; ++j) {
+      float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const float4 A = a[j][k], V = v[j][k], G = gg[k];
+        const float e0 = A.x * G.x, e1 = A.y * G.y, e2 = A.z * G.z, e3 = A.w * G.w;
+        s1 += (e0 + e1) + (e2 + e3);
+        s2 += (e0 * (V.x - mu[j]) + e1 * (V.y - mu[j])) + (e2 * (V.z - mu[j]) + e3 * (V.w - mu[j]));
+      }
+      s1 = warp_sum(s1);
+      s2 = warp_sum(s2);
+      if (lane == 0) {
+        red[parity][warp][2 * j] = s1;
+        red[parity][warp][2 * j + 1] = s2 * rs[j];
+      }
+    }
+    __syncthreads();  // the other parity buffer is rewritten two batches later, past the next barrier
+#pragma unroll
+    for (int j = 0; j < RB; ++j) {
+      float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        s1 += red[parity][w][2 * j];
+        s2 += red[parity][w][2 * j + 1];
+      }
+      c1[j] = s1 * inv_d;
+      c2[j] = s2 * inv_d;
+    }
+#pragma unroll
+    for (int j = 0; j < RB; ++j) {
+      const int64_t r = r0 + j;
+      if (r >= r_end) break;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) {
+        const int c = t + 256 * k;
+        if (c >= n4) continue;
+        const float4 A = a[j][k], V = v[j][k], G = gg[k];
+        const float h0 = (V.x - mu[j]) * rs[j], h1 = (V.y - mu[j]) * rs[j], h2 = (V.z - mu[j]) * rs[j],
+                    h3 = (V.w - mu[j]) * rs[j];
+        float4 o;
+        o.x = rs[j] * (A.x * G.x - c1[j] - h0 * c2[j]);
+        o.y = rs[j] * (A.y * G.y - c1[j] - h1 * c2[j]);
+        o.z = rs[j] * (A.z * G.z - c1[j] - h2 * c2[j]);
+        o.w = rs[j] * (A.w * G.w - c1[j] - h3 * c2[j]);
+        if (resid) {
+          const float4 q = reinterpret_cast<const float4 *>(resid + r * d)[c];
+          o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+        }
+        reinterpret_cast<float4 *>(out + r * d)[c] = o;
+        if (out_bf) {
+          __nv_bfloat162 p0 = __floats2bfloat162_rn(o.x, o.y), p1 = __floats2bfloat162_rn(o.z, o.w);
+          reinterpret_cast<uint2 *>(out_bf + r * d)[c] =
+              make_uint2(*reinterpret_cast<uint32_t *>(&p0), *reinterpret_cast<uint32_t *>(&p1));
+        }
+        ag[k].x += A.x * h0; ag[k].y += A.y * h1; ag[k].z += A.z * h2; ag[k].w += A.w * h3;
+        ab[k].x += A.x; ab[k].y += A.y; ab[k].z += A.z; ab[k].w += A.w;
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int c = t + 256 * k;
+    if (c >= n4) continue;
+    atomicAdd(&dgam[4 * c], ag[k].x);
+    atomicAdd(&dgam[4 * c + 1], ag[k].y);
+    atomicAdd(&dgam[4 * c + 2], ag[k].z);
+    atomicAdd(&dgam[4 * c + 3], ag[k].w);
+    atomicAdd(&dbet[4 * c], ab[k].x);
+    atomicAdd(&dbet[4 * c + 1], ab[k].y);
+    atomicAdd(&dbet[4 * c + 2], ab[k].z);
+    atomicAdd(&dbet[4 * c + 3], ab[k].w);
+  }
+}
+
+template <int NV, int RB>
+static int ln_bwd_tile(const float *dy, const float *x, const float *mean, const float *rstd, const float *g,
+                       const float *resid, float *out, void *out_bf, float *dg, float *db, int64_t rows, int d,
+                       cudaStream_t s) {
+  int64_t blocks = (int64_t)sm_count() * 3;
+  int64_t rpb = (rows + blocks - 1) / blocks;
+  rpb = (rpb + RB - 1) / RB * RB;
+  if (rpb < RB) rpb = RB;
+  blocks = (rows + rpb - 1) / rpb;
+  HM_CUDA(launch_pdl(ln_bwd_tile_kernel<NV, RB>, dim3((unsigned)blocks), dim3(256), 0, s, dy, x, mean, rstd, g, resid,
+                     out, static_cast<__nv_bfloat16 *>(out_bf), dg, db, rows, d, (int)rpb));
+  count_launch();
+  return HM_OK;
+}
+
 // Same math, dgamma/dbeta accumulated in registers: a warp keeps the same
 // lane -> column mapping for every row it processes, so each lane sums its
 // NV4 float4 columns privately; warps then combine through shared memory
@@ -431,6 +566,21 @@ int ln_bwd(const float *dy, const float *x, const float *mean, const float *rstd
     return ln_bwd_reg<16>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
   }
   if (d % 4) return fail(HM_ERR_VALIDATION, "layernorm: d must be a multiple of 4");
+  // HM_LN_BWD=t: row-batched tiles with register-accumulated dgamma/dbeta.
+  // Graph-timed on cold inputs it is no faster than the shared-atomic kernel
+  // (34.3 vs 35.1 us at 4096 x 1600, 25.7 vs 22.0 us at 4096 x 1024; both
+  // about 3.4 TB/s), so it stays opt-in (profiles/r01_ln_perf.jsonl).
+  static const bool use_tile = [] {
+    const char *e = getenv("HM_LN_BWD");
+    return e && e[0] == 't';
+  }();
+  if (use_tile && d <= 4096) {
+    ProfScope ps(KC_LAYERNORM, s, 0, (resid ? 16.0 : 12.0) * rows * d + (out_bf ? 2.0 * rows * d : 0));
+    const int n4 = d / 4;
+    if (n4 <= 256) return ln_bwd_tile<1, 4>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
+    if (n4 <= 512) return ln_bwd_tile<2, 4>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
+    return ln_bwd_tile<4, 2>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
+  }
   const size_t smem = 2 * (size_t)d * sizeof(float);
   static bool attr = false;
   if (!attr) {

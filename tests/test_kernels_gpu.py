@@ -193,9 +193,11 @@ def test_attention_fwd_bwd(ops, B, S, H, DH, causal):
         assert _rel(got[:, i], g[:, i]) < 2e-2, i
 
 
-def test_layernorm_fwd_bwd(ops):
+@pytest.mark.parametrize("M,d", [(1000, 1600), (37, 1024), (517, 4096), (300, 8192), (64, 256)])
+def test_layernorm_fwd_bwd(ops, M, d):
+    """Every backward variant: row-batched tiles (d <= 4096, ragged row
+    counts) and the shared-memory kernel beyond."""
     torch.manual_seed(6)
-    M, d = 1000, 1600
     x = torch.randn(M, d, device="cuda") * 2 + 0.5
     g = torch.randn(d, device="cuda")
     b = torch.randn(d, device="cuda")
@@ -220,6 +222,21 @@ def test_layernorm_fwd_bwd(ops):
     assert _rel(ob, xr.grad + resid) < 1e-2
     assert _rel(dg, gr.grad + 1) < 1e-5
     assert _rel(db, br.grad + 1) < 1e-5
+
+
+def test_layernorm_bwd_tile_variant():
+    """The opt-in row-batched LayerNorm backward (HM_LN_BWD=t, read once per
+    process) on the same shapes."""
+    import subprocess
+    import sys
+    here = __import__("os").path.dirname(__import__("os").path.abspath(__file__))
+    cases = [(1000, 1600), (37, 1024), (517, 4096), (300, 8192), (64, 256)]
+    code = (f"import torch, sys; sys.path.insert(0, {here!r}); sys.path.insert(0, {here + '/..'!r}); "
+            "import test_kernels_gpu as T; from paper_2202_01306_b200 import ops; "
+            f"[T.test_layernorm_fwd_bwd(ops, *c) for c in {cases!r}]")
+    env = dict(__import__("os").environ, HM_LN_BWD="t")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
 
 
 def test_embedding_fwd_bwd(ops):

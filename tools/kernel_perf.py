@@ -184,25 +184,43 @@ def bench_attn_sweep():
 
 
 def bench_ln():
+    """LayerNorm fwd / bwd per launch: a CUDA graph of back-to-back launches
+    cycling over input sets whose total exceeds L2 (each launch reads cold
+    data, launch latency hidden as inside a training step)."""
     _, hbm, kind = peaks()
-    for rows, d in ((4096, 1600), (4096, 1024), (4096, 8192)):
-        x = torch.randn(rows, d, device="cuda")
+    for rows, d in ((4096, 1600), (4096, 1024), (8192, 1024), (4096, 8192)):
+        nset = max(2, int((400 << 20) // (rows * d * 4 * 3)) + 1)
+        sets = []
+        for _ in range(nset):
+            x = torch.randn(rows, d, device="cuda")
+            dy = torch.randn(rows, d, device="cuda")
+            sets.append(dict(x=x, dy=dy, y=torch.empty(rows, d, device="cuda", dtype=torch.bfloat16),
+                             mu=torch.empty(rows, device="cuda"), rs=torch.empty(rows, device="cuda"),
+                             out=torch.empty(rows, d, device="cuda"),
+                             ob=torch.empty(rows, d, device="cuda", dtype=torch.bfloat16)))
         g = torch.randn(d, device="cuda")
         b = torch.randn(d, device="cuda")
-        y = torch.empty(rows, d, device="cuda", dtype=torch.bfloat16)
-        mu = torch.empty(rows, device="cuda")
-        rs = torch.empty(rows, device="cuda")
-        ms = timeit(lambda: ops.layernorm_fwd(x, g, b, y, mu, rs))
-        dy = torch.randn(rows, d, device="cuda")
-        out = torch.empty(rows, d, device="cuda")
-        ob = torch.empty(rows, d, device="cuda", dtype=torch.bfloat16)
         dg = torch.zeros(d, device="cuda")
         db = torch.zeros(d, device="cuda")
-        msb = timeit(lambda: ops.layernorm_bwd(dy, x, mu, rs, g, out, dg, db, resid=x, out_bf16=ob))
-        print(json.dumps({"kernel": "layernorm", "rows": rows, "d": d, "fwd_ms": round(ms, 4),
-                          "fwd_GBps": round(6 * rows * d / ms / 1e6, 1), "bwd_ms": round(msb, 4),
-                          "bwd_GBps": round(18 * rows * d / msb / 1e6, 1), "peak": hbm,
-                          "env": {k: os.environ.get(k) for k in ("HM_LN_FWD",)}}), flush=True)
+        it = [0]
+
+        def fwd():
+            S = sets[it[0] % nset]
+            it[0] += 1
+            ops.layernorm_fwd(S["x"], g, b, S["y"], S["mu"], S["rs"])
+
+        def bwd():
+            S = sets[it[0] % nset]
+            it[0] += 1
+            ops.layernorm_bwd(S["dy"], S["x"], S["mu"], S["rs"], g, S["out"], dg, db, resid=S["x"], out_bf16=S["ob"])
+        for S in sets:
+            ops.layernorm_fwd(S["x"], g, b, S["y"], S["mu"], S["rs"])
+        ms = time_graph(fwd, reps=4 * nset)
+        msb = time_graph(bwd, reps=4 * nset)
+        print(json.dumps({"kernel": "layernorm", "rows": rows, "d": d, "fwd_us": round(ms * 1e3, 2),
+                          "fwd_GBps": round(6 * rows * d / ms / 1e6, 1), "bwd_us": round(msb * 1e3, 2),
+                          "bwd_GBps": round(18 * rows * d / msb / 1e6, 1), "peak": hbm, "peak_kind": kind,
+                          "env": {k: os.environ.get(k) for k in ("HM_LN_FWD", "HM_LN_BWD")}}), flush=True)
 
 
 def bench_gemm_bn():
