@@ -588,6 +588,9 @@ static int g_force_bn = env_int("HM_GEMM_BN"), g_force_cg = env_int("HM_GEMM_CG"
 // 128 x 192 single-CTA tiles (fit 1600-wide outputs in 9 column tiles)
 static const bool g_tile192 = getenv("HM_GEMM_192") ? atoi(getenv("HM_GEMM_192")) != 0 : true;
 static const double g_eff192 = getenv("HM_GEMM_EFF192") ? atof(getenv("HM_GEMM_EFF192")) : 0.70;
+// 256 x 192 pair tiles (K-major B only: each CTA stages 96 B rows, which an
+// MN-major 128-B swizzle atom of 64 columns cannot hold)
+static const double g_eff192p = getenv("HM_GEMM_EFF192P") ? atof(getenv("HM_GEMM_EFF192P")) : 0.80;
 
 static TileCfg pick_tile(int64_t M, int64_t N, int64_t K, int epi, bool allow192 = true, bool b_mn = false) {
   const int env_bn = g_force_bn, env_cg = g_force_cg, env_s = g_force_s;
@@ -599,9 +602,11 @@ static TileCfg pick_tile(int64_t M, int64_t N, int64_t K, int epi, bool allow192
     if (env_cg && cg != env_cg) continue;
     for (int bn : {128, 192, 256}) {
       if (env_bn && bn != env_bn) continue;
-      if (bn == 192 && (cg == 2 || !g_tile192 || !allow192)) continue;
+      if (bn == 192 && (!g_tile192 || !allow192 || (cg == 2 && b_mn))) continue;
       // pair tiles lose more when B is MN-major (dgrad / wgrad: 64-wide B chunks per k-block)
-      const double eff = bn == 128 ? 0.55 : bn == 192 ? g_eff192 : (cg == 1 ? 0.80 : (b_mn ? 0.86 : 0.93));
+      const double eff = bn == 128   ? 0.55
+                         : bn == 192 ? (cg == 1 ? g_eff192 : g_eff192p)
+                                     : (cg == 1 ? 0.80 : (b_mn ? 0.86 : 0.93));
       const double t_kb = bn / 256.0 / eff;
       const int64_t tiles = ((M + BM * cg - 1) / (BM * cg)) * ((N + bn - 1) / bn);
       const int64_t slots = sms / cg;
@@ -689,6 +694,7 @@ int run(const void *A, const void *B, void *D, int64_t M, int64_t N, int64_t K, 
     return fail(HM_ERR_VALIDATION, "gemm: aux must be 16B aligned with 16B pitch");
   TileCfg tc = pick_tile(M, N, K, epi, true, b_mn != 0);
   if (force_bn) tc.bn = force_bn;
+  if (tc.bn == 192 && tc.cg == 2 && b_mn) tc.cg = 1;  // forced pair: MN-major B cannot stage 96-row halves
   const int bn = tc.bn;
   Args a{};
   a.M = (int)M; a.N = (int)N; a.K = (int)K;
@@ -711,7 +717,11 @@ int run(const void *A, const void *B, void *D, int64_t M, int64_t N, int64_t K, 
   } else {
     tx = td;
   }
-  if (bn == 192) {  // single-CTA only (a pair would stage 96-row B halves)
+  if (bn == 192 && tc.cg == 2) {  // pair tiles: K-major B only
+    if (a_mn) return launch<192, 1, 0, 2>(ta, tb, td, tx, a, stream);
+    return launch<192, 0, 0, 2>(ta, tb, td, tx, a, stream);
+  }
+  if (bn == 192) {
     switch ((a_mn ? 2 : 0) | (b_mn ? 1 : 0)) {
       case 0: return launch<192, 0, 0, 1>(ta, tb, td, tx, a, stream);
       case 1: return launch<192, 0, 1, 1>(ta, tb, td, tx, a, stream);
@@ -884,9 +894,9 @@ extern "C" int hm_k_conv_wgrad(const void *dy, const void *x, float *dw, int32_t
 
 extern "C" int hm_k_gemm_set_tile(int32_t bn, int32_t cta_pair, int32_t splits) {
   if ((bn && bn != 128 && bn != 192 && bn != 256) || (cta_pair && cta_pair != 1 && cta_pair != 2) || splits < 0 ||
-      splits > 32 || (bn == 192 && cta_pair == 2))
+      splits > 32)
     return hm::fail(HM_ERR_VALIDATION,
-                    "gemm tile override: bn in {0,128,192,256} (192 single-CTA), cta_pair in {0,1,2}, splits in [0,32]");
+                    "gemm tile override: bn in {0,128,192,256}, cta_pair in {0,1,2}, splits in [0,32]");
   hm::gemm::g_force_bn = bn;
   hm::gemm::g_force_cg = cta_pair;
   hm::gemm::g_force_s = splits;

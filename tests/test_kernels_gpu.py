@@ -87,7 +87,7 @@ def test_gemm_epilogues(ops):
     assert _rel(dg, x.grad) < 1e-2
 
 
-@pytest.mark.parametrize("bn,cg", [(128, 1), (192, 1), (256, 1), (128, 2), (256, 2)])
+@pytest.mark.parametrize("bn,cg", [(128, 1), (192, 1), (256, 1), (128, 2), (192, 2), (256, 2)])
 def test_gemm_every_tile_config(ops, bn, cg):
     """Each forced tile configuration (128/256-wide tiles, single CTA or CTA
     pair with cta_group::2 MMAs) on every operand layout and epilogue, with M,

@@ -241,11 +241,13 @@ if __name__ == "__main__":
         bench_gemm_bn()
         sys.exit(0)
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if os.environ.get("HM_KP_GRAPH"):
+        GRAPH = True
     if what == "gemm_graph":
         GRAPH = True
         what = "gemm"
     if what == "gemm_sweep":
-        SWEEP = [(bn, cg, 0) for cg in (1, 2) for bn in (128, 192, 256) if not (bn == 192 and cg == 2)]
+        SWEEP = [(bn, cg, 0) for cg in (1, 2) for bn in (128, 192, 256)]
         what = "gemm"
     if what == "attn_sweep":
         bench_attn_sweep()
