@@ -37,6 +37,9 @@ sys.path.insert(0, ROOT)
 WORKLOADS = {
     # name: (preset, samples_per_gpu, u, layers_per_pack, alpha_gib, mode)
     "gpt2-xl-dp": ("gpt2-xl", 16, 4, 8, 32, "dp"),
+    # SURVEY 8f4b fast mode (NOT the reference's ledger): the headline workload with W
+    # swapped as exact [bf16 hi | lo] planes; forward tasks move hi + the fp32 prefix
+    "gpt2-xl-dp-bf16w": ("gpt2-xl", 16, 4, 8, 32, "dp", "bf16"),
     "tiny": ("tiny", 16, 4, 2, 4, "pp"),
     # the same model at a 4x larger minibatch: Harmony's grouping amortises the fixed
     # per-iteration swap bytes (W, K) over more samples ("no grouping")
@@ -288,7 +291,7 @@ def run_reference(args) -> None:
     if rank != 0:
         return
     from paper_2202_01306_b200.model import GPT_PRESETS
-    preset, per_gpu, u, lpp, alpha_gib, mode = WORKLOADS[args.workload]
+    preset, per_gpu, u, lpp, alpha_gib, mode, *_ = WORKLOADS[args.workload]
     spec = GPT_PRESETS[preset]
     threads = len(os.sched_getaffinity(0))
     samples = []
@@ -322,7 +325,7 @@ def run_native(args) -> None:
     from paper_2202_01306_b200.model import GPT_PRESETS, gpt_machine, gpt_profiles, synthetic_batch
     from paper_2202_01306_b200.runtime import HarmonyRuntime
 
-    preset, per_gpu, u, lpp, alpha_gib, mode = WORKLOADS[args.workload]
+    preset, per_gpu, u, lpp, alpha_gib, mode, *_ = WORKLOADS[args.workload]
     if args.alpha_gib:
         alpha_gib = args.alpha_gib
     is_cnn = preset in CNN_PRESETS
@@ -335,8 +338,9 @@ def run_native(args) -> None:
     machine = gpt_machine(world, alpha_bytes=alpha_gib << 30, pcie_gbs=min(pcie["h2d"], pcie["d2h"]) * 1e9)
     prof = cnn_profiles(spec) if is_cnn else gpt_profiles(spec)
     graph = H.generate_task_graph(cfg, machine, prof)
-    sim = H.simulate(graph, machine, prof)
-    rt = HarmonyRuntime(spec, alpha_bytes=alpha_gib << 30, device=local)
+    payload = (WORKLOADS[args.workload][6:] or ("fp32",))[0]
+    rt = HarmonyRuntime(spec, alpha_bytes=alpha_gib << 30, device=local, w_payload=payload)
+    sim = H.simulate(graph, machine, prof, w_fwd_bytes=rt.w_fwd_bytes())
     # weights drawn on the GPU (seconds, also with 8 ranks initialising at once);
     # the CPU generator is what the parity tests use
     rt.init_weights(0, device=None if is_cnn else "cuda")
@@ -447,7 +451,9 @@ def run_native(args) -> None:
         "config": {"workload": f"{args.workload}: {spec.name} Harmony-{mode.upper()}, packs of {lpp} layers, "
                                f"u_f=u_b={u}, alpha={alpha_gib} GiB/GPU",
                    "global_batch": D, "seq_len": getattr(spec, "seq_len", None), "parallelism": f"harmony-{mode}{world}",
-                   "l2": "inputs larger than L2 (W and K stream from host every step)"},
+                   "l2": "inputs larger than L2 (W and K stream from host every step)",
+                   "w_payload": payload if payload == "fp32" else
+                   "bf16 planes (SURVEY 8f4b fast mode: forward W rows differ from the reference ledger)"},
         "swap_gb_per_iter": round((swap_in + swap_out) / 1e9, 3),
         "swap_h2d_gb": round(swap_in / 1e9, 3), "swap_d2h_gb": round(swap_out / 1e9, 3),
         "step_roofline": {"bound": "pcie" if t_roof > t_compute else "tensor", "t_roof_ms": round(1000 * t_roof, 2),

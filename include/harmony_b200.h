@@ -89,6 +89,8 @@ typedef struct {
   const int64_t *x, *y;      /* [layers*(u_top+1)] */
   const int64_t *w, *dw, *k; /* [layers]           */
   const int64_t *t_f, *t_b, *t_u; /* [layers*(u_top+1)] or NULL if no times */
+  const int64_t *w_f;             /* [layers] W bytes a FORWARD task moves (bf16
+                                     swap-payload mode), or NULL = w (reference) */
 } hm_profile;
 
 /* One work item of the plan (simulator.py:86-108 `_Item`, extended with the
@@ -222,6 +224,12 @@ int hm_runtime_ipc_import(hm_runtime *rt, const uint8_t *buf, int32_t len);
  * host arenas restores it together with W and K. */
 int hm_runtime_get_step(const hm_runtime *rt);
 int hm_runtime_set_step(hm_runtime *rt, int32_t step);
+/* W swap payload, before hm_runtime_load_plan: 0 = fp32 (the reference's
+ * ledger), 1 = bf16 planes (SURVEY 8f4b fast mode: the host W arena holds each
+ * layer as [bf16 hi plane | 16-bit lo plane]; forward tasks move the hi plane
+ * plus the lo plane of the fp32-read prefix; the plan must be built with
+ * hm_profile.w_f).  Transformer family only. */
+int hm_runtime_set_w_payload(hm_runtime *rt, int32_t mode);
 /* Record each iteration into a CUDA graph after the first (default on) and
  * replay it: one launch per iteration instead of thousands. */
 int hm_runtime_set_graph(hm_runtime *rt, int32_t enable);
@@ -317,6 +325,12 @@ int hm_k_attn_bwd(const void *qkv, const void *out, const void *dout, const floa
                   int32_t causal, void *stream);
 /* fp32 -> bf16 cast of n elements. */
 int hm_k_cast_bf16(const float *src, void *dst, int64_t n, void *stream);
+/* Weight planes (bf16 swap payloads): hi = bf16 nearest with ties toward zero
+ * (the runtime's bf16 GEMM operand of a weight in both payload modes), lo = the
+ * low 16 bits; join(hi, lo) restores the fp32 bits exactly. */
+int hm_k_cast_w_bf16(const float *src, void *dst, int64_t n, void *stream);
+int hm_k_w_split(const float *w, void *hi, void *lo, int64_t n, void *stream);
+int hm_k_w_join(const void *hi, const void *lo, float *w, int64_t n, void *stream);
 /* Token + position embedding: out[b*seq+p] = wte[tokens[b*seq+p]] + wpe[p] (fp32). */
 int hm_k_embed_fwd(const int32_t *tokens, const float *wte, const float *wpe, float *out, int32_t batch,
                    int32_t seq, int32_t d, void *stream);

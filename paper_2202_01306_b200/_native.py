@@ -39,7 +39,7 @@ class hm_machine(C.Structure):
 
 class hm_profile(C.Structure):
     _fields_ = [("layers", C.c_int32), ("u_top", C.c_int32)] + [
-        (n, C.POINTER(C.c_int64)) for n in ("x", "y", "w", "dw", "k", "t_f", "t_b", "t_u")]
+        (n, C.POINTER(C.c_int64)) for n in ("x", "y", "w", "dw", "k", "t_f", "t_b", "t_u", "w_f")]
 
 
 ITEM_DTYPE = np.dtype([
@@ -117,6 +117,7 @@ def lib() -> C.CDLL:
         "hm_runtime_set_graph": (C.c_int, [C.c_void_p, C.c_int32]),
         "hm_runtime_get_step": (C.c_int, [C.c_void_p]),
         "hm_runtime_set_step": (C.c_int, [C.c_void_p, C.c_int32]),
+        "hm_runtime_set_w_payload": (C.c_int, [C.c_void_p, C.c_int32]),
         "hm_runtime_share_arenas": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int32, C.c_int64]),
         "hm_runtime_ipc_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
         "hm_runtime_ipc_import": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
@@ -140,6 +141,9 @@ def lib() -> C.CDLL:
         "hm_k_attn_fwd_tc": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p] + [C.c_int32] * 5 + [C.c_void_p]),
         "hm_k_attn_bwd": (C.c_int, [C.c_void_p] * 7 + [C.c_int32] * 5 + [C.c_void_p]),
         "hm_k_cast_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+        "hm_k_cast_w_bf16": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+        "hm_k_w_split": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+        "hm_k_w_join": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
         "hm_k_embed_fwd": (C.c_int, [C.c_void_p] * 4 + [C.c_int32] * 3 + [C.c_void_p]),
         "hm_k_embed_bwd": (C.c_int, [C.c_void_p] * 4 + [C.c_int32] * 3 + [C.c_void_p]),
         "hm_k_layernorm_fwd": (C.c_int, [C.c_void_p] * 6 + [C.c_int64, C.c_int32, C.c_void_p]),

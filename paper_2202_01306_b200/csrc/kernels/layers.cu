@@ -69,6 +69,79 @@ int cast_f32_bf16(const float *src, void *dst, int64_t n, cudaStream_t s) {
   return HM_OK;
 }
 
+// ---- weight planes (bf16 swap-payload mode) ---------------------------------------
+// An fp32 weight w splits exactly into hi = bf16(w) rounded to nearest with
+// ties toward zero magnitude -- (bits + 0x7FFF) >> 16 -- and lo = the low 16
+// bits of w: bits = (hi << 16) + d with d = lo if lo <= 0x8000, else lo - 0x10000
+// (d in [-0x7FFF, 0x8000]).  hi is the GEMM operand itself, so a forward task
+// that only needs bf16 weights moves half the bytes; cast_w_bf16 (the
+// reference-payload path) produces the same hi, so both modes compute
+// bit-identically.
+__device__ __forceinline__ uint32_t w_hi(uint32_t u) { return (u + 0x7FFFu) >> 16; }
+__device__ __forceinline__ uint32_t w_join1(uint32_t hi, uint32_t lo) {
+  return (hi << 16) + (lo <= 0x8000u ? lo : lo - 0x10000u);
+}
+
+__global__ void cast_w_kernel(const uint4 *__restrict__ src, uint2 *__restrict__ dst, int64_t n4) {
+  pdl_wait();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 v = src[i];
+    dst[i] = make_uint2(w_hi(v.x) | (w_hi(v.y) << 16), w_hi(v.z) | (w_hi(v.w) << 16));
+  }
+}
+
+__global__ void w_join_kernel(const uint16_t *__restrict__ hi, const uint16_t *__restrict__ lo, uint32_t *__restrict__ w,
+                              int64_t n) {
+  pdl_wait();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    w[i] = w_join1(hi[i], lo[i]);
+}
+
+__global__ void w_split_kernel(const uint32_t *__restrict__ w, uint16_t *__restrict__ hi, uint16_t *__restrict__ lo,
+                               int64_t n) {
+  pdl_wait();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t u = w[i];
+    hi[i] = (uint16_t)w_hi(u);
+    lo[i] = (uint16_t)(u & 0xFFFFu);
+  }
+}
+
+static unsigned elem_blocks(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  if (b > (int64_t)sm_count() * 16) b = (int64_t)sm_count() * 16;
+  return (unsigned)(b < 1 ? 1 : b);
+}
+
+int cast_w_bf16(const float *src, void *dst, int64_t n, cudaStream_t s) {
+  if (n <= 0) return HM_OK;
+  if (n % 4 || ((uintptr_t)src & 15) || ((uintptr_t)dst & 7))  // weight slots are 256-B aligned, packs n % 8 == 0
+    return fail(HM_ERR_VALIDATION, "cast_w_bf16: weights must be 16-B aligned, n % 4 == 0");
+  ProfScope ps(KC_MISC, s, 0, 6.0 * n);
+  HM_CUDA(launch_pdl(cast_w_kernel, dim3(elem_blocks(n / 4)), dim3(256), 0, s, reinterpret_cast<const uint4 *>(src),
+                     static_cast<uint2 *>(dst), n / 4));
+  count_launch();
+  return HM_OK;
+}
+
+int w_join(const void *hi, const void *lo, float *w, int64_t n, cudaStream_t s) {
+  if (n <= 0) return HM_OK;
+  ProfScope ps(KC_MISC, s, 0, 8.0 * n);
+  HM_CUDA(launch_pdl(w_join_kernel, dim3(elem_blocks(n)), dim3(256), 0, s, static_cast<const uint16_t *>(hi),
+                     static_cast<const uint16_t *>(lo), reinterpret_cast<uint32_t *>(w), n));
+  count_launch();
+  return HM_OK;
+}
+
+int w_split(const float *w, void *hi, void *lo, int64_t n, cudaStream_t s) {
+  if (n <= 0) return HM_OK;
+  ProfScope ps(KC_MISC, s, 0, 8.0 * n);
+  HM_CUDA(launch_pdl(w_split_kernel, dim3(elem_blocks(n)), dim3(256), 0, s, reinterpret_cast<const uint32_t *>(w),
+                     static_cast<uint16_t *>(hi), static_cast<uint16_t *>(lo), n));
+  count_launch();
+  return HM_OK;
+}
+
 // ---- embedding -----------------------------------------------------------------
 __global__ void embed_fwd_kernel(const int32_t *__restrict__ tok, const float *__restrict__ wte,
                                  const float *__restrict__ wpe, float *__restrict__ out, int64_t rows, int S, int d) {
@@ -724,6 +797,15 @@ using namespace hm::layers;
 extern "C" {
 int hm_k_cast_bf16(const float *src, void *dst, int64_t n, void *stream) {
   return cast_f32_bf16(src, dst, n, static_cast<cudaStream_t>(stream));
+}
+int hm_k_cast_w_bf16(const float *src, void *dst, int64_t n, void *stream) {
+  return cast_w_bf16(src, dst, n, static_cast<cudaStream_t>(stream));
+}
+int hm_k_w_split(const float *w, void *hi, void *lo, int64_t n, void *stream) {
+  return w_split(w, hi, lo, n, static_cast<cudaStream_t>(stream));
+}
+int hm_k_w_join(const void *hi, const void *lo, float *w, int64_t n, void *stream) {
+  return w_join(hi, lo, w, n, static_cast<cudaStream_t>(stream));
 }
 int hm_k_embed_fwd(const int32_t *tokens, const float *wte, const float *wpe, float *out, int32_t batch, int32_t seq,
                    int32_t d, void *stream) {

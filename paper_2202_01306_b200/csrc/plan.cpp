@@ -159,7 +159,11 @@ struct Builder {
         for (; i < t.inputs.size() && t.inputs[i].tensor == tensor; ++i) {
           const hm_entry &e = t.inputs[i];
           if (e.channel == HM_CPU_GPU_SWAP) {
-            int64_t b = c.entry_bytes(tensor, e.layer, e, t.group[0]);
+            // bf16 swap-payload mode: a forward task moves the bf16 high halves
+            // plus the fp32-read prefix of each layer (hm_profile.w_f)
+            int64_t b = (tensor == HM_W && t.type == HM_TASK_F && c.p->w_f)
+                            ? c.scalar(c.p->w_f, e.layer, "forward weight size")
+                            : c.entry_bytes(tensor, e.layer, e, t.group[0]);
             auto f = std::find_if(swap_bytes.begin(), swap_bytes.end(),
                                   [&](auto &kv) { return kv.first == tensor; });
             if (f == swap_bytes.end()) swap_bytes.push_back({tensor, b});

@@ -21,6 +21,10 @@ int backward(const void *qkv, const void *o, const void *dout, const float *lse,
 }
 namespace layers {
 int cast_f32_bf16(const float *src, void *dst, int64_t n, cudaStream_t s);
+// weight planes: hi = bf16 nearest, ties toward zero; lo = low 16 bits (exact split)
+int cast_w_bf16(const float *src, void *dst, int64_t n, cudaStream_t s);
+int w_join(const void *hi, const void *lo, float *w, int64_t n, cudaStream_t s);
+int w_split(const float *w, void *hi, void *lo, int64_t n, cudaStream_t s);
 int embed_fwd(const int32_t *tok, const float *wte, const float *wpe, float *out, int B, int S, int d, cudaStream_t s);
 int embed_bwd(const int32_t *tok, const float *dx, float *dwte, float *dwpe, int B, int S, int d, cudaStream_t s);
 int ln_fwd(const float *x, const float *g, const float *b, void *y, float *mean, float *rstd, int64_t rows, int d,

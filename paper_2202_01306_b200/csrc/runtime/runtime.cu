@@ -45,6 +45,7 @@ static inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * 
 struct ParamLayout {  // float offsets inside one layer's parameter block; -1 = absent
   int64_t wte = -1, wpe = -1, ln1_g, ln1_b, w_qkv, b_qkv, w_proj, b_proj, ln2_g, ln2_b, w_fc1, b_fc1, w_fc2, b_fc2;
   int64_t lnf_g = -1, lnf_b = -1, w_head = -1, size = 0;
+  int64_t f32n = 0;  // leading fp32-read parameters (the rest are GEMM weights)
 };
 
 // Per-layer activation pointers for one member (u samples) inside a store.
@@ -73,6 +74,7 @@ struct CnnScratch {
 };
 
 struct Slots {
+  std::vector<uint16_t *> wlo;  // bf16-payload mode: lo planes of a forward task's fp32 prefixes
   std::vector<float *> w;
   std::vector<bf16 *> wsh;
   std::vector<float *> dw;
@@ -113,6 +115,8 @@ struct Action {
   std::vector<std::pair<int, int>> rwaits;  // (item on another rank, iteration lag 0/1): signal waits
   cudaEvent_t done = nullptr;               // kind 5: all-reduce completion
   int64_t count = 0;                        // kind 5: floats reduced
+  struct Seg { void *dst; const void *src; int64_t bytes; };
+  std::vector<Seg> segs;                    // kind 2/3: several copies behind one ledger row
 };
 
 // Per-launch CUDA-event timing of the runtime's kernels (enabled on demand).
@@ -196,6 +200,10 @@ struct hm_runtime {
   cudaStream_t s_compute = nullptr, s_h2d = nullptr, s_d2h = nullptr, s_update = nullptr, s_p2p_in = nullptr,
                s_p2p_out = nullptr;
   float *w_host = nullptr, *k_host = nullptr;
+  // bf16 swap payloads (non-reference ledger): the host W arena
+  // holds each layer as [hi plane | lo plane] (2 + 2 bytes per parameter, see
+  // layers::w_join); forward tasks move hi planes plus the fp32-read prefix
+  bool w_planar = false;
   uint8_t *stash_host = nullptr;
   int64_t stash_host_bytes = 0;
   // plan
@@ -293,28 +301,33 @@ static Memops &memops() {
 // model layout
 // ---------------------------------------------------------------------------
 static ParamLayout make_layout(const hm_runtime &rt, int L) {
+  // fp32-read parameters first (LayerNorm, biases, embedding tables), then the
+  // GEMM weights (model.py GPTSpec.layer_segments): `f32n` is that prefix
   const int64_t d = rt.m.d_model, v = rt.Vp, s = rt.S;
   ParamLayout p;
   int64_t o = 0;
-  if (L == 0) {
-    p.wte = o; o += v * d;
-    p.wpe = o; o += s * d;
-  }
   p.ln1_g = o; o += d;
   p.ln1_b = o; o += d;
-  p.w_qkv = o; o += 3 * d * d;
   p.b_qkv = o; o += 3 * d;
-  p.w_proj = o; o += d * d;
   p.b_proj = o; o += d;
   p.ln2_g = o; o += d;
   p.ln2_b = o; o += d;
-  p.w_fc1 = o; o += 4 * d * d;
   p.b_fc1 = o; o += 4 * d;
-  p.w_fc2 = o; o += 4 * d * d;
   p.b_fc2 = o; o += d;
   if (L == rt.R - 1) {
     p.lnf_g = o; o += d;
     p.lnf_b = o; o += d;
+  }
+  if (L == 0) {
+    p.wte = o; o += v * d;
+    p.wpe = o; o += s * d;
+  }
+  p.f32n = o;
+  p.w_qkv = o; o += 3 * d * d;
+  p.w_proj = o; o += d * d;
+  p.w_fc1 = o; o += 4 * d * d;
+  p.w_fc2 = o; o += 4 * d * d;
+  if (L == rt.R - 1) {
     p.w_head = o; o += v * d;
   }
   p.size = o;
@@ -816,8 +829,30 @@ static int run_member(hm_runtime &rt, int task, int g) {
   const int64_t rowsd = (int64_t)rt.S * d;
   cudaStream_t s = rt.s_compute;
   if (g == 0) {
-    // bf16 operand copy of the pack's master weights, right after swap-in
-    HM_TRY(layers::cast_f32_bf16(rt.slots.w[tr.w_slot], rt.slots.wsh[tr.w_slot], tr.params, s));
+    if (rt.w_planar) {
+      // bf16 payloads: the hi planes already are the bf16 operands; rebuild the
+      // fp32 values the kernels read (forward: each layer's fp32 prefix;
+      // backward: whole layers, the U task updates them)
+      int64_t soff = 0;
+      for (int L = t.lo; L <= t.hi; ++L) {
+        const int64_t o = rt.w_off[L] - rt.w_off[t.lo];
+        const ParamLayout &P = rt.lay[L];
+        if (t.type == HM_TASK_F) {
+          HM_TRY(layers::w_join(rt.slots.wsh[tr.w_slot] + o, rt.slots.wlo[tr.w_slot] + soff, rt.slots.w[tr.w_slot] + o,
+                                P.f32n, s));
+          soff += P.f32n;
+        } else {
+          HM_TRY(layers::w_join(rt.slots.wsh[tr.w_slot] + o, rt.slots.dw[tr.dw_slot] + o, rt.slots.w[tr.w_slot] + o,
+                                P.size, s));
+        }
+      }
+    } else if (rt.family == HM_FAMILY_GPT) {
+      // bf16 operand copy of the pack's master weights, right after swap-in
+      // (nearest, ties toward zero: the same bits as the bf16-payload hi planes)
+      HM_TRY(layers::cast_w_bf16(rt.slots.w[tr.w_slot], rt.slots.wsh[tr.w_slot], tr.params, s));
+    } else {
+      HM_TRY(layers::cast_f32_bf16(rt.slots.w[tr.w_slot], rt.slots.wsh[tr.w_slot], tr.params, s));
+    }
     if (t.type == HM_TASK_B) HM_CUDA(cudaMemsetAsync(rt.slots.dw[tr.dw_slot], 0, tr.params * 4, s));
   }
   if (rt.family == HM_FAMILY_CNN) {
@@ -900,13 +935,18 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
     return fail(HM_ERR_VALIDATION,
                 "peer-to-peer hand-offs (Harmony-PP, N>1) need shared host arenas: call hm_runtime_share_arenas");
   int last_f = -1, shared_b = -1;
-  int64_t u_max = 1, pmax = 0;
+  int64_t u_max = 1, pmax = 0, f32max = 0;
   std::vector<int> heads;  // stash head layers produced here
   for (int ti : mine) {
     TaskInfo &t = plan->tasks[ti];
     TaskRt &tr = rt.trt[ti];
     tr.params = rt.w_off[t.hi + 1] - rt.w_off[t.lo];
     pmax = std::max(pmax, tr.params);
+    if (rt.w_planar && t.type == HM_TASK_F) {
+      int64_t f = 0;
+      for (int L = t.lo; L <= t.hi; ++L) f += rt.lay[L].f32n;
+      f32max = std::max(f32max, f);
+    }
     int64_t acc = 0;
     for (int u : t.group) {
       tr.s0.push_back(acc);
@@ -1053,12 +1093,14 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
   std::vector<Req> req;
   rt.slots.w.assign(NW, nullptr);
   rt.slots.wsh.assign(NW, nullptr);
+  rt.slots.wlo.assign(NW, nullptr);
   rt.slots.dw.assign(NDW, nullptr);
   rt.slots.k.assign(NK, nullptr);
   rt.slots.stash_in.assign(NST, nullptr);
   for (int i = 0; i < NW; ++i) {
     req.push_back({(void **)&rt.slots.w[i], pmax * 4});
     req.push_back({(void **)&rt.slots.wsh[i], pmax * 2});
+    if (rt.w_planar) req.push_back({(void **)&rt.slots.wlo[i], std::max<int64_t>(f32max * 2, 256)});
   }
   for (int i = 0; i < NDW; ++i) req.push_back({(void **)&rt.slots.dw[i], pmax * 4});
   for (int i = 0; i < NK; ++i) req.push_back({(void **)&rt.slots.k[i], pmax * 8});
@@ -1140,7 +1182,9 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
   if (!rt.slots_sized && !env_nw && !env_nk) {
     int nw = NW, nk = NK;
     int64_t room = rt.alpha - total;
-    const int64_t kslot = align_up(pmax * 8, 1024), wslot = align_up(pmax * 4, 1024) + align_up(pmax * 2, 1024);
+    const int64_t kslot = align_up(pmax * 8, 1024),
+                  wslot = align_up(pmax * 4, 1024) + align_up(pmax * 2, 1024) +
+                          (rt.w_planar ? align_up(std::max<int64_t>(f32max * 2, 256), 1024) : 0);
     while (nk < 4 && room >= kslot) { ++nk; room -= kslot; }
     while (nw < 4 && room >= wslot) { ++nw; room -= wslot; }
     if (nw != NW || nk != NK) {
@@ -1248,7 +1292,9 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
         if (w_prev[tr.w_slot] >= 0 && pass == 1) w_wait[ti] = w_release(w_prev[tr.w_slot]);
         w_prev[tr.w_slot] = ti;
         if (t.type == HM_TASK_B) {
-          if (dw_prev[tr.dw_slot] >= 0 && pass == 1) dw_wait[ti] = rt.trt[dw_prev[tr.dw_slot] + 1].members.back();
+          // (bf16 payloads: the U task's W swap-out reads the planes from the dW slot)
+          if (dw_prev[tr.dw_slot] >= 0 && pass == 1)
+            dw_wait[ti] = rt.w_planar ? w_release(dw_prev[tr.dw_slot]) : rt.trt[dw_prev[tr.dw_slot] + 1].members.back();
           dw_prev[tr.dw_slot] = ti;
           if (tr.stash_slot >= 0) {
             if (st_prev[tr.stash_slot] >= 0 && pass == 1) st_wait[ti] = rt.trt[st_prev[tr.stash_slot]].members.back();
@@ -1304,7 +1350,30 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
       a.kind = 2;
       a.stream = rt.s_h2d;
       a.bytes = r.nbytes;
-      if (r.channel == HM_CPU_GPU_SWAP && r.tensor == HM_W) {
+      if (r.channel == HM_CPU_GPU_SWAP && r.tensor == HM_W && rt.w_planar) {
+        // per layer: hi plane -> the bf16 operand slot; forward: the lo plane of
+        // the fp32 prefix -> staging; backward: the whole lo plane -> the dW
+        // slot (joined into fp32 W before dW is zeroed)
+        const uint8_t *hb = reinterpret_cast<const uint8_t *>(rt.w_host);
+        int64_t expect = 0, soff = 0;
+        for (int L = t.lo; L <= t.hi; ++L) {
+          const int64_t o = rt.w_off[L] - rt.w_off[t.lo], P = rt.lay[L].size, f = rt.lay[L].f32n;
+          const uint8_t *hL = hb + 4 * rt.w_off[L];
+          a.segs.push_back({reinterpret_cast<uint8_t *>(rt.slots.wsh[tr.w_slot]) + 2 * o, hL, 2 * P});
+          if (t.type == HM_TASK_F) {
+            if (f) a.segs.push_back({reinterpret_cast<uint8_t *>(rt.slots.wlo[tr.w_slot]) + 2 * soff, hL + 2 * P, 2 * f});
+            soff += f;
+            expect += 2 * P + 2 * f;
+          } else {
+            a.segs.push_back({reinterpret_cast<uint8_t *>(rt.slots.dw[tr.dw_slot]) + 4 * o, hL + 2 * P, 2 * P});
+            expect += 4 * P;
+          }
+        }
+        if (r.nbytes != expect)
+          return fail(HM_ERR_INTERNAL, "bf16-payload W swap-in size disagrees with the plan (load it with w_f bytes)");
+        if (w_wait.count(r.task)) a.waits.push_back({w_wait[r.task], false});
+        if (t.type == HM_TASK_B && dw_wait.count(r.task)) a.waits.push_back({dw_wait[r.task], false});
+      } else if (r.channel == HM_CPU_GPU_SWAP && r.tensor == HM_W) {
         a.src = rt.w_host + rt.w_off[t.lo];
         a.dst = rt.slots.w[tr.w_slot];
         if (r.nbytes != tr.params * 4) return fail(HM_ERR_INTERNAL, "W swap-in size disagrees with the model layout");
@@ -1342,7 +1411,8 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
       a.bytes = r.nbytes;
       if (r.channel == HM_CPU_GPU_SWAP && r.tensor == HM_W) {
         TaskRt &bt = rt.trt[tr.b_task];
-        a.src = rt.slots.w[bt.w_slot];
+        // bf16 payloads: the U task left the [hi | lo] planes of each layer in the dW slot
+        a.src = rt.w_planar ? static_cast<const void *>(rt.slots.dw[bt.dw_slot]) : rt.slots.w[bt.w_slot];
         a.dst = rt.w_host + rt.w_off[t.lo];
       } else if (r.channel == HM_CPU_GPU_SWAP && r.tensor == HM_K) {
         a.src = rt.slots.k[tr.k_slot];
@@ -1494,10 +1564,19 @@ static int enqueue_body(hm_runtime &rt, bool capture, bool pipelined, int64_t &h
         else
           HM_TRY(adam_launch(rt.slots.w[bt.w_slot], rt.slots.dw[bt.dw_slot], rt.slots.k[tr.k_slot], tr.params,
                              rt.m.lr, rt.m.beta1, rt.m.beta2, rt.m.eps, rt.step, 1.0f, a.stream));
+        if (rt.w_planar) {  // updated W -> [hi | lo] planes per layer in the (consumed) dW slot, for the swap-out
+          const TaskInfo &ut = rt.plan->tasks[a.task];
+          for (int L = ut.lo; L <= ut.hi; ++L) {
+            const int64_t o = rt.w_off[L] - rt.w_off[ut.lo], P = rt.lay[L].size;
+            uint16_t *hi = reinterpret_cast<uint16_t *>(rt.slots.dw[bt.dw_slot] + o);
+            HM_TRY(layers::w_split(rt.slots.w[bt.w_slot] + o, hi, hi + P, P, a.stream));
+          }
+        }
         break;
       }
       case 2:
-        HM_CUDA(cudaMemcpyAsync(a.dst, a.src, a.bytes, cudaMemcpyHostToDevice, a.stream));
+        if (a.segs.empty()) HM_CUDA(cudaMemcpyAsync(a.dst, a.src, a.bytes, cudaMemcpyHostToDevice, a.stream));
+        for (auto &g : a.segs) HM_CUDA(cudaMemcpyAsync(g.dst, g.src, g.bytes, cudaMemcpyHostToDevice, a.stream));
         h2d += a.bytes;
         break;
       case 3:
@@ -2050,6 +2129,16 @@ int hm_runtime_ipc_import(hm_runtime *rt, const uint8_t *buf, int32_t len) {
 }
 
 int hm_runtime_get_step(const hm_runtime *rt) { return rt ? rt->step : -1; }
+
+int hm_runtime_set_w_payload(hm_runtime *rt, int32_t mode) {
+  if (!rt) return hm::fail(HM_ERR_VALIDATION, "null runtime");
+  if (mode != 0 && mode != 1) return hm::fail(HM_ERR_VALIDATION, "w payload: 0 = fp32 (reference), 1 = bf16 planes");
+  if (rt->plan) return hm::fail(HM_ERR_VALIDATION, "set the W payload before loading a plan");
+  if (mode == 1 && rt->family != HM_FAMILY_GPT)
+    return hm::fail(HM_ERR_VALIDATION, "bf16 W payloads are implemented for the transformer family");
+  rt->w_planar = mode == 1;
+  return HM_OK;
+}
 
 int hm_runtime_set_step(hm_runtime *rt, int32_t step) {
   if (!rt || step < 0) return hm::fail(HM_ERR_VALIDATION, "bad step");

@@ -47,7 +47,9 @@ class NativePlan:
     """Owns an ``hm_plan*`` and the ctypes tables it was built from."""
 
     def __init__(self, graph: TaskGraph, machine: MachineModel, profiles: ProfileSet,
-                 need_time: bool = True) -> None:
+                 need_time: bool = True, w_fwd_bytes=None) -> None:
+        """``w_fwd_bytes``: per-layer W bytes a forward task moves, for the
+        runtime's bf16 swap-payload mode (None = the reference's W bytes)."""
         lib = N.lib()
         self.graph = graph
         self.machine = machine
@@ -114,8 +116,13 @@ class NativePlan:
                 return C.POINTER(C.c_int64)()
             return a.ctypes.data_as(C.POINTER(C.c_int64))
 
+        self._tab["w_f"] = None
+        if w_fwd_bytes is not None:
+            wf = np.zeros(layers, dtype=np.int64) - 1
+            wf[:min(layers, len(w_fwd_bytes))] = np.asarray(w_fwd_bytes, dtype=np.int64)[:layers]
+            self._tab["w_f"] = wf
         self._profile = N.hm_profile(layers, u_top, *(ptr(self._tab[k]) for k in
-                                                      ("x", "y", "w", "dw", "k", "t_f", "t_b", "t_u")))
+                                                      ("x", "y", "w", "dw", "k", "t_f", "t_b", "t_u", "w_f")))
         status = C.c_int32(0)
         handle = lib.hm_plan_build(self._tasks, n, C.cast(self._groups, C.POINTER(C.c_int32)),
                                    self._entries, C.byref(self._machine), C.byref(self._profile),

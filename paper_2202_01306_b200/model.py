@@ -83,15 +83,28 @@ class GPTSpec:
     def layer_segments(self, L: int) -> list[tuple[str, int]]:
         """Ordered (name, numel) of layer L's parameters in the W arena."""
         d, v, s = self.d_model, self.vocab_padded, self.seq_len
-        seg = []
+        # parameters read in fp32 (LayerNorm, biases, embedding tables) first,
+        # then the GEMM weights: the fp32 prefix is what a forward task needs
+        # beyond the bf16 high halves in the bf16 swap-payload mode
+        seg = [("ln1_g", d), ("ln1_b", d), ("b_qkv", 3 * d), ("b_proj", d), ("ln2_g", d), ("ln2_b", d),
+               ("b_fc1", 4 * d), ("b_fc2", d)]
+        if L == self.n_layer - 1:
+            seg += [("lnf_g", d), ("lnf_b", d)]
         if L == 0:
             seg += [("wte", v * d), ("wpe", s * d)]
-        seg += [("ln1_g", d), ("ln1_b", d), ("w_qkv", 3 * d * d), ("b_qkv", 3 * d),
-                ("w_proj", d * d), ("b_proj", d), ("ln2_g", d), ("ln2_b", d),
-                ("w_fc1", 4 * d * d), ("b_fc1", 4 * d), ("w_fc2", 4 * d * d), ("b_fc2", d)]
+        seg += [("w_qkv", 3 * d * d), ("w_proj", d * d), ("w_fc1", 4 * d * d), ("w_fc2", 4 * d * d)]
         if L == self.n_layer - 1:
-            seg += [("lnf_g", d), ("lnf_b", d), ("w_head", v * d)]
+            seg += [("w_head", v * d)]
         return seg
+
+    def f32_prefix(self, L: int) -> int:
+        """Leading parameters of layer L that kernels read in fp32."""
+        n = 0
+        for name, k in self.layer_segments(L):
+            if name.startswith("w_"):
+                break
+            n += k
+        return n
 
     # -- FLOPs (BASELINE.md "Algorithmic FLOPs") ----------------------------
     def layer_fwd_flops(self, L: int, u: int) -> int:
@@ -183,3 +196,21 @@ def synthetic_batch(spec: GPTSpec, samples: int, seed: int = 1234):
     seq = torch.randint(0, spec.vocab, (samples, spec.seq_len + 1), generator=g, dtype=torch.int64)
     return (np.ascontiguousarray(seq[:, :-1].numpy().astype(np.int32)),
             np.ascontiguousarray(seq[:, 1:].numpy().astype(np.int32)))
+
+
+# -- bf16 swap payloads: exact split of fp32 weights ------------
+def split_planes(w):
+    """fp32 -> (hi, lo) uint16 planes: hi = bf16 nearest with ties toward zero
+    ((bits + 0x7FFF) >> 16, the GEMM operand), lo = the low 16 bits."""
+    import numpy as np
+    u = np.ascontiguousarray(w, dtype=np.float32).view(np.uint32)
+    return ((u.astype(np.uint64) + 0x7FFF) >> 16).astype(np.uint16), (u & 0xFFFF).astype(np.uint16)
+
+
+def join_planes(hi, lo):
+    """Inverse of split_planes, bit-exact: bits = (hi << 16) + d with d = lo for
+    lo <= 0x8000, else lo - 0x10000."""
+    import numpy as np
+    h = hi.astype(np.int64)
+    l_ = lo.astype(np.int64)
+    return ((h << 16) + np.where(l_ <= 0x8000, l_, l_ - 0x10000)).astype(np.uint32).view(np.float32)

@@ -115,6 +115,19 @@ def cast_bf16(src, dst):
     NL.check(N_lib().hm_k_cast_bf16(_ptr(src), _ptr(dst), src.numel(), _stream()))
 
 
+def cast_w_bf16(src, dst):
+    """Weight operand cast: bf16 nearest, ties toward zero (the hi plane)."""
+    NL.check(N_lib().hm_k_cast_w_bf16(_ptr(src), _ptr(dst), src.numel(), _stream()))
+
+
+def w_split(w, hi, lo):
+    NL.check(N_lib().hm_k_w_split(_ptr(w), _ptr(hi), _ptr(lo), w.numel(), _stream()))
+
+
+def w_join(hi, lo, w):
+    NL.check(N_lib().hm_k_w_join(_ptr(hi), _ptr(lo), _ptr(w), w.numel(), _stream()))
+
+
 def embed_fwd(tokens, wte, wpe, out, *, batch, seq):
     NL.check(N_lib().hm_k_embed_fwd(_ptr(tokens), _ptr(wte), _ptr(wpe), _ptr(out), batch, seq,
                                     wte.shape[1], _stream()))

@@ -22,7 +22,7 @@ from .core import MachineModel, gpu_shares
 from .errors import ValidationError
 from .lowering import NativePlan
 from .cnn import CNNSpec
-from .model import GPTSpec
+from .model import GPTSpec, join_planes, split_planes
 from .profiler import ProfileSet
 from .simulator import SimReport, report_from_items
 from .taskgraph import TaskGraph
@@ -32,8 +32,18 @@ class HarmonyRuntime:
     """Native runtime for one GPU: arenas, streams, kernels, plan executor."""
 
     def __init__(self, spec: GPTSpec | CNNSpec, *, alpha_bytes: int, device: int = 0, lr: float = 1e-4,
-                 betas: tuple[float, float] = (0.9, 0.999), eps: float = 1e-8) -> None:
+                 betas: tuple[float, float] = (0.9, 0.999), eps: float = 1e-8, w_payload: str = "fp32") -> None:
+        """``w_payload``: "fp32" swaps fp32 W exactly as the reference's ledger
+        bills it; "bf16" is the SURVEY 8f4b fast mode (transformer family): the
+        host W arena holds each layer as [bf16 hi plane | 16-bit lo plane], an
+        exact split of the fp32 value, and forward tasks move only the hi plane
+        plus the lo plane of the fp32-read prefix (LayerNorm, biases,
+        embeddings).  Losses and weights are bit-identical to "fp32"; the
+        forward W rows of the ledger differ (flagged: not the reference's)."""
+        if w_payload not in ("fp32", "bf16"):
+            raise ValidationError("w_payload must be 'fp32' or 'bf16'")
         self.spec = spec
+        self.w_payload = w_payload
         self.lib = NL.lib()
         self.is_cnn = isinstance(spec, CNNSpec)
         st = C.c_int32(0)
@@ -58,7 +68,11 @@ class HarmonyRuntime:
         for L in range(spec.n_layer):
             if self.w_off[L + 1] - self.w_off[L] != spec.layer_params(L):
                 raise ValidationError(f"native layout of layer {L} disagrees with GPTSpec")
-        self.w = self._arena(0, np.float32)
+        if w_payload == "bf16":
+            if self.is_cnn:
+                raise ValidationError("bf16 W payloads are implemented for the transformer family")
+            NL.check(self.lib.hm_runtime_set_w_payload(h, 1))
+        self._w_arena = self._arena(0, np.float32)
         self.k = self._arena(1, np.float32)
         self.plan: NativePlan | None = None
         self.graph: TaskGraph | None = None
@@ -72,13 +86,56 @@ class HarmonyRuntime:
         return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_float)), shape=(n,))
 
     # -- state ----------------------------------------------------------------
-    def layer_params(self, L: int) -> dict[str, np.ndarray]:
-        """Views of layer L's master weights in the W arena, by segment name
-        (CNN segments come shaped: weights [cout, 3, 3, cin])."""
+    @property
+    def w(self) -> np.ndarray:
+        """Master weights, canonical fp32 layout: the W arena itself (fp32
+        payload) or a decoded copy of its planes (bf16 payload)."""
+        return self._w_arena if self.w_payload == "fp32" else self.weights()
+
+    def weights(self) -> np.ndarray:
+        """Copy of the master weights in the canonical fp32 layout."""
+        if self.w_payload == "fp32":
+            return self._w_arena.copy()
+        a16 = self._w_arena.view(np.uint16)
+        out = np.empty(self._w_arena.size, dtype=np.float32)
+        for L in range(self.spec.n_layer):
+            o, n = int(self.w_off[L]), int(self.w_off[L + 1] - self.w_off[L])
+            out[o:o + n] = join_planes(a16[2 * o:2 * o + n], a16[2 * o + n:2 * o + 2 * n])
+        return out
+
+    def set_weights(self, flat: np.ndarray) -> None:
+        """Write canonical fp32 master weights into the W arena (bf16 payload:
+        as per-layer [hi | lo] planes, hi = nearest bf16 with ties toward zero,
+        lo = the low 16 bits; the split is exact)."""
+        flat = np.ascontiguousarray(flat, dtype=np.float32)
+        if flat.size != self._w_arena.size:
+            raise ValidationError("weights size disagrees with the model")
+        if self.w_payload == "fp32":
+            self._w_arena[:] = flat
+            return
+        a16 = self._w_arena.view(np.uint16)
+        for L in range(self.spec.n_layer):
+            o, n = int(self.w_off[L]), int(self.w_off[L + 1] - self.w_off[L])
+            a16[2 * o:2 * o + n], a16[2 * o + n:2 * o + 2 * n] = split_planes(flat[o:o + n])
+
+    def w_fwd_bytes(self) -> list[int] | None:
+        """Per-layer W bytes a forward task moves (bf16 payload), else None."""
+        if self.w_payload == "fp32":
+            return None
+        return [2 * self.spec.layer_params(L) + 2 * self.spec.f32_prefix(L) for L in range(self.spec.n_layer)]
+
+    def layer_params(self, L: int, base: np.ndarray | None = None) -> dict[str, np.ndarray]:
+        """Views of layer L's master weights, by segment name (CNN segments
+        come shaped: weights [cout, 3, 3, cin]), in ``base`` (a canonical
+        flat array) or the W arena itself (fp32 payload only)."""
+        if base is None:
+            if self.w_payload != "fp32":
+                raise ValidationError("bf16 W payload: read weights() / write set_weights()")
+            base = self._w_arena
         out, o = {}, int(self.w_off[L])
         for name, shp in self.spec.layer_segments(L):
             n = int(np.prod(shp)) if isinstance(shp, tuple) else int(shp)
-            out[name] = self.w[o:o + n].reshape(shp) if isinstance(shp, tuple) else self.w[o:o + n]
+            out[name] = base[o:o + n].reshape(shp) if isinstance(shp, tuple) else base[o:o + n]
             o += n
         return out
 
@@ -119,11 +176,12 @@ class HarmonyRuntime:
         import torch
         if self.is_cnn:
             return self._init_cnn(seed)
+        target = self._w_arena if self.w_payload == "fp32" else np.empty(self._w_arena.size, np.float32)
         if device is not None:
             gen = torch.Generator(device=device).manual_seed(seed)
             V, d = self.spec.vocab, self.spec.d_model
             for L in range(self.spec.n_layer):
-                for name, view in self.layer_params(L).items():
+                for name, view in self.layer_params(L, target).items():
                     if name.endswith("_g"):
                         view[:] = 1.0
                     elif name.startswith("b_") or name.endswith("_b"):
@@ -135,11 +193,13 @@ class HarmonyRuntime:
                             t.view(-1, d)[V:] = 0.0
                         torch.from_numpy(view).copy_(t)
                         del t
+            if target is not self._w_arena:
+                self.set_weights(target)
             return  # K is zeroed by hm_runtime_create
         gen = torch.Generator().manual_seed(seed)
         V, d = self.spec.vocab, self.spec.d_model
         for L in range(self.spec.n_layer):
-            for name, view in self.layer_params(L).items():
+            for name, view in self.layer_params(L, target).items():
                 if name.endswith("_g"):
                     view[:] = 1.0
                 elif name.startswith("b_") or name.endswith("_b"):
@@ -149,13 +209,15 @@ class HarmonyRuntime:
                     view[:] = t.numpy()
                     if name in ("wte", "w_head"):
                         view.reshape(-1, d)[V:] = 0.0
+        if target is not self._w_arena:
+            self.set_weights(target)
         self.k[:] = 0.0
 
     # -- checkpoint / resume (the host arenas are the model state) ------
     def save_checkpoint(self, path: str) -> None:
         """W and K arenas + optimizer step, as one .npz (no device state: the
         GPU only holds transient packs between iterations)."""
-        np.savez(path, w=self.w, k=self.k, step=np.int64(self.lib.hm_runtime_get_step(self.handle)),
+        np.savez(path, w=self.weights(), k=self.k, step=np.int64(self.lib.hm_runtime_get_step(self.handle)),
                  spec=np.array([self.spec.n_layer, self.spec.d_model, self.spec.n_head, self.spec.seq_len,
                                 self.spec.vocab], dtype=np.int64))
         return None
@@ -164,9 +226,9 @@ class HarmonyRuntime:
         z = np.load(path)
         want = np.array([self.spec.n_layer, self.spec.d_model, self.spec.n_head, self.spec.seq_len,
                          self.spec.vocab], dtype=np.int64)
-        if not np.array_equal(z["spec"], want) or z["w"].shape != self.w.shape:
+        if not np.array_equal(z["spec"], want) or z["w"].shape != self._w_arena.shape:
             raise ValidationError("checkpoint was written for a different model")
-        self.w[:] = z["w"]
+        self.set_weights(z["w"])
         self.k[:] = z["k"]
         NL.check(self.lib.hm_runtime_set_step(self.handle, int(z["step"])))
 
@@ -183,7 +245,7 @@ class HarmonyRuntime:
         maps the same pinned host state).  Rank 0 creates, the others attach."""
         NL.check(self.lib.hm_runtime_share_arenas(self.handle, name.encode(), 1 if create else 0,
                                                   int(stash_bytes)))
-        self.w = self._arena(0, np.float32)
+        self._w_arena = self._arena(0, np.float32)
         self.k = self._arena(1, np.float32)
 
     def ipc_export(self) -> bytes:
@@ -227,7 +289,7 @@ class HarmonyRuntime:
             raise ValidationError("execute needs a scheduler-generated graph")
         if machine.gpu_count != graph.machine.gpu_count:
             raise ValidationError("machine does not match the graph's GPU count")
-        plan = NativePlan(graph, machine, profiles)
+        plan = NativePlan(graph, machine, profiles, w_fwd_bytes=self.w_fwd_bytes())
         if graph.mode.value == "dp":
             samples = gpu_shares(graph.minibatch, machine.gpu_count)[rank]
         else:

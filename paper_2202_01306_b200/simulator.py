@@ -111,15 +111,19 @@ def report_from_items(graph: TaskGraph, machine: MachineModel, items, makespan: 
 
 
 def simulate(graph: TaskGraph, machine: MachineModel | None = None,
-             profiles: ProfileSet | None = None, *, check_memory: bool = False) -> SimReport:
-    """Estimate one training iteration (drop-in for `simulator.simulate`)."""
+             profiles: ProfileSet | None = None, *, check_memory: bool = False,
+             w_fwd_bytes=None) -> SimReport:
+    """Estimate one training iteration (drop-in for `simulator.simulate`).
+    ``w_fwd_bytes`` (extension, default None = the reference): per-layer W
+    bytes forward tasks move under the runtime's bf16 swap-payload mode
+    (``HarmonyRuntime.w_fwd_bytes()``)."""
     machine = machine or graph.machine
     if profiles is None:
         raise ValidationError("profiles are required")
     if machine.gpu_count != graph.machine.gpu_count:
         raise ValidationError("machine does not match the graph's GPU count")
     graph.validate()
-    plan = NativePlan(graph, machine, profiles)
+    plan = NativePlan(graph, machine, profiles, w_fwd_bytes=w_fwd_bytes)
     try:
         if check_memory:
             check_memory_fit(graph, machine, profiles)

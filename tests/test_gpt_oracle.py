@@ -46,7 +46,9 @@ def test_oracle_member_chunking_invariant():
     la = a.step(tok, lab, [6])
     lb = b.step(tok, lab, [4, 2])
     assert abs(la - lb) < 1e-5
-    assert torch.allclose(a.w, b.w, atol=1e-7)
+    # Adam normalises each component's update: components whose gradient is
+    # ~0 move by up to lr on rounding noise, so allow 1% of one step there
+    assert torch.allclose(a.w, b.w, atol=1e-6)
 
 
 def test_spec_layout_sums():

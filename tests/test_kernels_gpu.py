@@ -3,6 +3,8 @@ the same op (run on the B200 box: pytest -m gpu)."""
 
 import math
 
+import numpy as np
+
 import pytest
 import torch
 
@@ -237,6 +239,31 @@ def test_layernorm_bwd_tile_variant():
     env = dict(__import__("os").environ, HM_LN_BWD="t")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
+
+
+def test_weight_planes_exact(ops):
+    """bf16 swap payloads: the device split / join restore fp32 bits exactly and
+    the weight cast equals the hi plane (host reference: model.split_planes)."""
+    import sys, os
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from test_payload import _edge_floats
+    from paper_2202_01306_b200.model import split_planes
+    f = _edge_floats()
+    f = f[: (f.size // 8) * 8]
+    w = torch.from_numpy(f.copy()).cuda()
+    hi = torch.empty(w.numel(), dtype=torch.int16, device="cuda")
+    lo = torch.empty_like(hi)
+    ops.w_split(w, hi, lo)
+    back = torch.empty_like(w)
+    ops.w_join(hi, lo, back)
+    cast = torch.empty(w.numel(), dtype=torch.bfloat16, device="cuda")
+    ops.cast_w_bf16(w, cast)
+    torch.cuda.synchronize()
+    assert torch.equal(back.view(torch.int32), w.view(torch.int32))
+    h_ref, l_ref = split_planes(f)
+    assert np.array_equal(hi.cpu().numpy().view(np.uint16), h_ref)
+    assert np.array_equal(lo.cpu().numpy().view(np.uint16), l_ref)
+    assert np.array_equal(cast.view(torch.int16).cpu().numpy().view(np.uint16), h_ref)
 
 
 def test_embedding_fwd_bwd(ops):

@@ -164,6 +164,60 @@ def test_wide_layers_head_dim_128_match_oracle():
     assert rel_w < STATE_RTOL
 
 
+@pytest.mark.parametrize("mode", ["pp", "dp"])
+def test_bf16_w_payload_matches_fp32_payload(mode, tmp_path):
+    """SURVEY 8f4b fast mode: with W swapped as [bf16 hi | lo] planes, forward
+    tasks move hi + the fp32 prefix only.  The executed ledger equals the plan
+    built with those forward W bytes; every other row equals the reference's.
+    The GEMM operands are the same bits as the fp32 payload's (the weight cast
+    rounds like the hi plane), so losses and weights agree with the fp32
+    payload up to the run-to-run order of atomics, and with the oracle."""
+    from oracle.gpt_cpu import GPTOracle
+    from paper_2202_01306_b200.runtime import HarmonyRuntime
+    spec = GPT_PRESETS["tiny"]
+    prof = gpt_profiles(spec)
+    mach = H.MachineModel(gpu_count=1, gpu_mem_capacity=4 << 30, pcie_bandwidth=55_000_000_000)
+    pf, pb = ((0, 0), (1, 1), (2, 3)), ((0, 1), (2, 3))
+    g = H.generate_task_graph(H.Configuration(4, pf, 4, pb, 8, H.Mode(mode)), mach, prof)
+    tok, lab = synthetic_batch(spec, 8)
+    out = {}
+    for payload in ("fp32", "bf16"):
+        rt = HarmonyRuntime(spec, alpha_bytes=4 << 30, w_payload=payload)
+        rt.init_weights(0)
+        w0 = rt.w.copy()
+        rt.load(g, mach, prof)
+        losses = [rt.step(tok, lab) for _ in range(3)]
+        losses += rt.run_steps(2, tok, lab)[0]  # graph-captured, pipelined
+        led = rt.report().ledger
+        sim = H.simulate(g, mach, prof, w_fwd_bytes=rt.w_fwd_bytes()).ledger
+        assert led == sim
+        if payload == "bf16":
+            rt.save_checkpoint(str(tmp_path / "ck.npz"))
+            w_now = rt.weights()
+            rt.load_checkpoint(str(tmp_path / "ck.npz"))
+            assert np.array_equal(rt.weights().view(np.uint32), w_now.view(np.uint32))
+        out[payload] = (w0, losses, rt.w.copy(), rt.k.copy(), led)
+        rt.close()
+    (w0a, la, wa, ka, leda), (w0b, lb, wb, kb, ledb) = out["fp32"], out["bf16"]
+    assert np.array_equal(w0a.view(np.uint32), w0b.view(np.uint32))
+    assert abs(la[0] - lb[0]) <= 1e-6 * abs(la[0])  # same operands, same forward
+    assert np.allclose(la, lb, rtol=1e-4)
+    assert np.linalg.norm(wa - wb) / np.linalg.norm(wa) < 5e-4
+    assert np.linalg.norm(ka - kb) / np.linalg.norm(ka) < 1e-2
+    ftasks = {t.index for t in g.tasks if t.type is H.TaskType.F}
+    diff = [(a, b) for a, b in zip(leda, ledb) if a != b]
+    assert diff and all(a[0] in ftasks and a[3] == "W" and b[6] < a[6] for a, b in diff)
+    moved = lambda led: sum(r[6] for r in led)  # noqa: E731
+    print(f"{mode}: ledger bytes fp32 {moved(leda)} -> bf16 {moved(ledb)}")
+    # and against the fp32 oracle over the same 5 steps
+    oracle = GPTOracle(spec, w0b, np.cumsum([0] + [spec.layer_params(L) for L in range(spec.n_layer)]))
+    for i in range(5):
+        ref = oracle.step(tok, lab, list(g.tasks[0].group))
+        assert abs(lb[i] - ref) / abs(ref) < LOSS_RTOL
+    w_ref = oracle.w.numpy()
+    assert np.linalg.norm(wb - w_ref) / np.linalg.norm(w_ref) < STATE_RTOL
+
+
 def test_checkpoint_resume_is_exact(tmp_path):
     """Training 4 steps == 2 steps, checkpoint, fresh runtime, resume, 2 steps."""
     from paper_2202_01306_b200.runtime import HarmonyRuntime
