@@ -48,6 +48,7 @@ WORKLOADS = {
     "bert-large-pp": ("bert-large", 64, 16, 6, 32, "pp"),
     # north-star target shape: W + Adam state (184 GB) > one GPU's HBM
     "gpt-15b-dp": ("gpt-15b", 24, 4, 3, 170, "dp"),
+    "gpt-15b-dp-bf16w": ("gpt-15b", 24, 4, 3, 170, "dp", "bf16"),  # 8f4b fast mode (not the reference ledger)
     # config c5: deep-CNN packs (128 residual blocks at 56x56 / 28x28, implicit-GEMM convs)
     "resnet-dp": ("resnet-bench", 64, 32, 16, 12, "dp"),
 }

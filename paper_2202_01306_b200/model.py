@@ -203,14 +203,27 @@ def split_planes(w):
     """fp32 -> (hi, lo) uint16 planes: hi = bf16 nearest with ties toward zero
     ((bits + 0x7FFF) >> 16, the GEMM operand), lo = the low 16 bits."""
     import numpy as np
-    u = np.ascontiguousarray(w, dtype=np.float32).view(np.uint32)
-    return ((u.astype(np.uint64) + 0x7FFF) >> 16).astype(np.uint16), (u & 0xFFFF).astype(np.uint16)
+    u = np.ascontiguousarray(w, dtype=np.float32).view(np.uint32).reshape(-1)
+    hi = np.empty(u.size, np.uint16)
+    lo = np.empty(u.size, np.uint16)
+    step = 1 << 24  # bounded temporaries (a 15 B-parameter arena leaves little host RAM)
+    for i in range(0, u.size, step):
+        c = u[i:i + step]
+        # uint32 wrap-around only for NaN bit patterns >= 0xFFFF8001
+        hi[i:i + step] = (c + np.uint32(0x7FFF)) >> np.uint32(16)
+        lo[i:i + step] = c & np.uint32(0xFFFF)
+    return hi, lo
 
 
 def join_planes(hi, lo):
     """Inverse of split_planes, bit-exact: bits = (hi << 16) + d with d = lo for
     lo <= 0x8000, else lo - 0x10000."""
     import numpy as np
-    h = hi.astype(np.int64)
-    l_ = lo.astype(np.int64)
-    return ((h << 16) + np.where(l_ <= 0x8000, l_, l_ - 0x10000)).astype(np.uint32).view(np.float32)
+    out = np.empty(hi.size, np.uint32)
+    step = 1 << 24
+    for i in range(0, hi.size, step):
+        h = hi[i:i + step].astype(np.uint32)
+        l_ = lo[i:i + step].astype(np.uint32)
+        # (h << 16) + d, d = lo or lo - 0x10000: modulo 2^32 the same as subtracting 0x10000 from h << 16
+        out[i:i + step] = (h << np.uint32(16)) + l_ - np.where(l_ > 0x8000, np.uint32(0x10000), np.uint32(0))
+    return out.view(np.float32)

@@ -113,16 +113,28 @@ class HarmonyRuntime:
         if self.w_payload == "fp32":
             self._w_arena[:] = flat
             return
-        a16 = self._w_arena.view(np.uint16)
         for L in range(self.spec.n_layer):
-            o, n = int(self.w_off[L]), int(self.w_off[L + 1] - self.w_off[L])
-            a16[2 * o:2 * o + n], a16[2 * o + n:2 * o + 2 * n] = split_planes(flat[o:o + n])
+            self._set_layer(L, flat[int(self.w_off[L]):int(self.w_off[L + 1])])
 
     def w_fwd_bytes(self) -> list[int] | None:
         """Per-layer W bytes a forward task moves (bf16 payload), else None."""
         if self.w_payload == "fp32":
             return None
         return [2 * self.spec.layer_params(L) + 2 * self.spec.f32_prefix(L) for L in range(self.spec.n_layer)]
+
+    def _segment_views(self, L: int, buf: np.ndarray) -> dict[str, np.ndarray]:
+        """Views of layer L's segments in a layer-sized canonical buffer."""
+        out, o = {}, 0
+        for name, shp in self.spec.layer_segments(L):
+            n = int(np.prod(shp)) if isinstance(shp, tuple) else int(shp)
+            out[name] = buf[o:o + n].reshape(shp) if isinstance(shp, tuple) else buf[o:o + n]
+            o += n
+        return out
+
+    def _set_layer(self, L: int, buf: np.ndarray) -> None:
+        o, n = int(self.w_off[L]), int(self.w_off[L + 1] - self.w_off[L])
+        a16 = self._w_arena.view(np.uint16)
+        a16[2 * o:2 * o + n], a16[2 * o + n:2 * o + 2 * n] = split_planes(buf)
 
     def layer_params(self, L: int, base: np.ndarray | None = None) -> dict[str, np.ndarray]:
         """Views of layer L's master weights, by segment name (CNN segments
@@ -176,42 +188,34 @@ class HarmonyRuntime:
         import torch
         if self.is_cnn:
             return self._init_cnn(seed)
-        target = self._w_arena if self.w_payload == "fp32" else np.empty(self._w_arena.size, np.float32)
-        if device is not None:
-            gen = torch.Generator(device=device).manual_seed(seed)
-            V, d = self.spec.vocab, self.spec.d_model
-            for L in range(self.spec.n_layer):
-                for name, view in self.layer_params(L, target).items():
-                    if name.endswith("_g"):
-                        view[:] = 1.0
-                    elif name.startswith("b_") or name.endswith("_b"):
-                        view[:] = 0.0
-                    else:
-                        t = torch.empty(view.size, dtype=torch.float32, device=device).normal_(0.0, 0.02,
-                                                                                             generator=gen)
-                        if name in ("wte", "w_head"):
-                            t.view(-1, d)[V:] = 0.0
-                        torch.from_numpy(view).copy_(t)
-                        del t
-            if target is not self._w_arena:
-                self.set_weights(target)
-            return  # K is zeroed by hm_runtime_create
-        gen = torch.Generator().manual_seed(seed)
         V, d = self.spec.vocab, self.spec.d_model
+        gen = torch.Generator(device=device).manual_seed(seed) if device is not None else \
+            torch.Generator().manual_seed(seed)
         for L in range(self.spec.n_layer):
-            for name, view in self.layer_params(L, target).items():
+            # one layer at a time: the W arena itself (fp32 payload) or a layer-sized
+            # canonical buffer split into the arena's planes (bf16 payload)
+            o, n = int(self.w_off[L]), int(self.w_off[L + 1] - self.w_off[L])
+            buf = self._w_arena[o:o + n] if self.w_payload == "fp32" else np.empty(n, np.float32)
+            for name, view in self._segment_views(L, buf).items():
                 if name.endswith("_g"):
                     view[:] = 1.0
                 elif name.startswith("b_") or name.endswith("_b"):
                     view[:] = 0.0
+                elif device is not None:
+                    t = torch.empty(view.size, dtype=torch.float32, device=device).normal_(0.0, 0.02, generator=gen)
+                    if name in ("wte", "w_head"):
+                        t.view(-1, d)[V:] = 0.0
+                    torch.from_numpy(view).copy_(t)
+                    del t
                 else:
                     t = torch.empty(view.size, dtype=torch.float32).normal_(0.0, 0.02, generator=gen)
                     view[:] = t.numpy()
                     if name in ("wte", "w_head"):
                         view.reshape(-1, d)[V:] = 0.0
-        if target is not self._w_arena:
-            self.set_weights(target)
-        self.k[:] = 0.0
+            if self.w_payload != "fp32":
+                self._set_layer(L, buf)
+        if device is None:
+            self.k[:] = 0.0  # (hm_runtime_create zeroes K; kept for re-initialisation)
 
     # -- checkpoint / resume (the host arenas are the model state) ------
     def save_checkpoint(self, path: str) -> None:
