@@ -13,7 +13,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="gpt2-xl-dp")
 ap.add_argument("--steps", type=int, default=8)
 a = ap.parse_args()
-preset, D, u, lpp, alpha_gib, mode = bench.WORKLOADS[a.workload]
+preset, D, u, lpp, alpha_gib, mode, *_ = bench.WORKLOADS[a.workload]
 spec = GPT_PRESETS[preset]
 R = spec.n_layer
 packs = tuple((i, min(i + lpp, R) - 1) for i in range(0, R, lpp))

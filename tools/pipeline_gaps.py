@@ -15,7 +15,7 @@ ap.add_argument("--workload", default="gpt2-xl-dp")
 ap.add_argument("--steps", type=int, default=4)
 ap.add_argument("--out", default="gpurun_out/pipeline.json")
 a = ap.parse_args()
-preset, a.d, a.u, a.lpp, a.alpha, mode = bench.WORKLOADS[a.workload]
+preset, a.d, a.u, a.lpp, a.alpha, mode, *_ = bench.WORKLOADS[a.workload]
 from paper_2202_01306_b200.cnn import CNN_PRESETS, cnn_profiles, synthetic_images  # noqa: E402
 is_cnn = preset in CNN_PRESETS
 spec = CNN_PRESETS[preset] if is_cnn else GPT_PRESETS[preset]
