@@ -311,6 +311,14 @@ def test_bias_grad_and_cast(ops):
     db2 = torch.zeros(1600, device="cuda")
     ops.bias_grad(dyf, db2)
     assert _rel(db2, dyf.sum(0)) < 1e-5
+    # ragged row blocks and the two-column fallback (n % 8 != 0, strided rows)
+    for rows, n, pad, dt in ((37, 1032, 8, torch.bfloat16), (1003, 18, 2, torch.float32), (517, 4800, 2, torch.float32),
+                             (77, 1600, 0, torch.float32)):
+        big = torch.randn(rows, n + pad, device="cuda").to(dt)
+        v = big[:, :n]
+        dbx = torch.zeros(n, device="cuda")
+        ops.bias_grad(v, dbx)
+        assert _rel(dbx, v.float().sum(0)) < 1e-5, (rows, n, dt)
     src = torch.randn(1_000_001, device="cuda")
     dst = torch.empty(1_000_001, device="cuda", dtype=torch.bfloat16)
     ops.cast_bf16(src, dst)
