@@ -745,45 +745,58 @@ int cross_entropy(const float *logits, const int32_t *labels, int64_t rows, int6
 }
 
 // ---- bias gradient: db[n] += sum_r dy[r, n] ------------------------------------------
-// Column sums of dy [rows, n] (leading dimension ld) into db.  Each thread owns
-// 8 consecutive columns (one 16-B load per row for bf16, two for fp32) and
-// walks a block of rows four at a time, so every warp issues 512-B (bf16) /
-// 1-KB (fp32) coalesced loads with four rows in flight; one atomic per column
-// per row block.
+// Column sums of dy [rows, n] (leading dimension ld) into db.  A block is cx
+// column threads x (256 / cx) row lanes (cx = 8, 16 or 32: narrow convolution
+// biases get more row lanes): each thread owns 8 consecutive columns (one 16-B
+// load per row for bf16, two for fp32) and every ry-th row of the block's row
+// range, four rows in flight; the row lanes meet in shared memory and each
+// block adds one partial per column (few atomics per address).
 template <typename T>
-__global__ void bias_grad_kernel(const T *__restrict__ dy, float *__restrict__ db, int64_t rows, int n, int64_t ld,
-                                 int rows_per_block) {
+__global__ void __launch_bounds__(256) bias_grad_kernel(const T *__restrict__ dy, float *__restrict__ db, int64_t rows,
+                                                        int n, int64_t ld, int rows_per_block, int cx) {
   pdl_wait();
-  const int col = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
-  if (col >= n) return;
+  __shared__ float part[256 * 8];
+  const int ry = 256 / cx;
+  const int tx = threadIdx.x % cx, ty = threadIdx.x / cx;
+  const int col = (blockIdx.x * cx + tx) * 8;
   const int64_t r0 = (int64_t)blockIdx.y * rows_per_block;
   const int64_t r1 = min(rows, r0 + rows_per_block);
   float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-  auto add_row = [&](int64_t r) {
-    if constexpr (sizeof(T) == 2) {
-      const uint4 v = *reinterpret_cast<const uint4 *>(dy + r * ld + col);
-      const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&v);
+  if (col < n) {
+    auto add_row = [&](int64_t r) {
+      if constexpr (sizeof(T) == 2) {
+        const uint4 v = *reinterpret_cast<const uint4 *>(dy + r * ld + col);
+        const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&v);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float2 f = __bfloat1622float2(h[k]);
-        a[2 * k] += f.x;
-        a[2 * k + 1] += f.y;
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = __bfloat1622float2(h[k]);
+          a[2 * k] += f.x;
+          a[2 * k + 1] += f.y;
+        }
+      } else {
+        const float4 v0 = *reinterpret_cast<const float4 *>(dy + r * ld + col);
+        const float4 v1 = *reinterpret_cast<const float4 *>(dy + r * ld + col + 4);
+        a[0] += v0.x; a[1] += v0.y; a[2] += v0.z; a[3] += v0.w;
+        a[4] += v1.x; a[5] += v1.y; a[6] += v1.z; a[7] += v1.w;
       }
-    } else {
-      const float4 v0 = *reinterpret_cast<const float4 *>(dy + r * ld + col);
-      const float4 v1 = *reinterpret_cast<const float4 *>(dy + r * ld + col + 4);
-      a[0] += v0.x; a[1] += v0.y; a[2] += v0.z; a[3] += v0.w;
-      a[4] += v1.x; a[5] += v1.y; a[6] += v1.z; a[7] += v1.w;
+    };
+    int64_t r = r0 + ty;
+    for (; r + 3 * ry < r1; r += 4 * ry) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) add_row(r + (int64_t)ry * k);
     }
-  };
-  int64_t r = r0;
-  for (; r + 4 <= r1; r += 4) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k) add_row(r + k);
+    for (; r < r1; r += ry) add_row(r);
   }
-  for (; r < r1; ++r) add_row(r);
 #pragma unroll
-  for (int k = 0; k < 8; ++k) atomicAdd(db + col + k, a[k]);
+  for (int k = 0; k < 8; ++k) part[ty * (cx * 8) + tx * 8 + k] = a[k];
+  __syncthreads();
+  const int c = threadIdx.x;  // the block's cx * 8 columns
+  const int gc = blockIdx.x * cx * 8 + c;
+  if (c < cx * 8 && gc < n) {
+    float t = 0.f;
+    for (int y = 0; y < ry; ++y) t += part[y * (cx * 8) + c];
+    atomicAdd(db + gc, t);
+  }
 }
 
 // (n % 8 != 0 or unaligned rows: two columns per thread)
@@ -816,20 +829,37 @@ int bias_grad(const void *dy, int is_bf16, float *db, int64_t rows, int n, int64
   ProfScope ps(KC_MISC, s, 0, (is_bf16 ? 2.0 : 4.0) * rows * n);
   const int esz = is_bf16 ? 2 : 4;
   const bool wide = n % 8 == 0 && (ld * esz) % 16 == 0 && ((uintptr_t)dy & 15) == 0;
-  const int per = wide ? 8 : 2;
-  const int threads = 128;
-  const int gx = (n / per + threads - 1) / threads;
-  int64_t gy = (sm_count() * 8 + gx - 1) / gx;
+  int gx, threads;
+  int64_t gy;
+  int cx = 32;
+  if (wide) {  // cx column threads (8 columns each) x 256 / cx row lanes per block, ~4 blocks per SM
+    while (cx > 8 && cx / 2 * 8 >= n) cx /= 2;
+    threads = 256;
+    gx = (n + cx * 8 - 1) / (cx * 8);
+    gy = ((int64_t)sm_count() * 4 + gx - 1) / gx;
+  } else {
+    threads = 128;
+    gx = (n / 2 + threads - 1) / threads;
+    gy = ((int64_t)sm_count() * 8 + gx - 1) / gx;
+  }
   int rpb = (int)((rows + gy - 1) / gy);
   if (rpb < 32) rpb = 32;
   gy = (rows + rpb - 1) / rpb;
   const dim3 grid(gx, (unsigned)gy);
   if (is_bf16) {
-    auto k = wide ? bias_grad_kernel<__nv_bfloat16> : bias_grad2_kernel<__nv_bfloat16>;
-    HM_CUDA(launch_pdl(k, grid, dim3(threads), 0, s, static_cast<const __nv_bfloat16 *>(dy), db, rows, n, ld, rpb));
+    if (wide)
+      HM_CUDA(launch_pdl(bias_grad_kernel<__nv_bfloat16>, grid, dim3(threads), 0, s,
+                         static_cast<const __nv_bfloat16 *>(dy), db, rows, n, ld, rpb, cx));
+    else
+      HM_CUDA(launch_pdl(bias_grad2_kernel<__nv_bfloat16>, grid, dim3(threads), 0, s,
+                         static_cast<const __nv_bfloat16 *>(dy), db, rows, n, ld, rpb));
   } else {
-    auto k = wide ? bias_grad_kernel<float> : bias_grad2_kernel<float>;
-    HM_CUDA(launch_pdl(k, grid, dim3(threads), 0, s, static_cast<const float *>(dy), db, rows, n, ld, rpb));
+    if (wide)
+      HM_CUDA(launch_pdl(bias_grad_kernel<float>, grid, dim3(threads), 0, s, static_cast<const float *>(dy), db, rows,
+                         n, ld, rpb, cx));
+    else
+      HM_CUDA(launch_pdl(bias_grad2_kernel<float>, grid, dim3(threads), 0, s, static_cast<const float *>(dy), db, rows,
+                         n, ld, rpb));
   }
   count_launch();
   HM_CUDA(cudaGetLastError());

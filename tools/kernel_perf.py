@@ -223,6 +223,25 @@ def bench_ln():
                           "env": {k: os.environ.get(k) for k in ("HM_LN_FWD", "HM_LN_BWD")}}), flush=True)
 
 
+def bench_bias():
+    """Bias-gradient column sums (graph-timed, input sets larger than L2)."""
+    _, hbm, kind = peaks()
+    for rows, n, dt in ((4096, 6400, torch.bfloat16), (4096, 1600, torch.float32), (4096, 4800, torch.bfloat16),
+                        (200704, 64, torch.bfloat16), (200704, 128, torch.bfloat16), (50176, 256, torch.bfloat16)):
+        esz = 2 if dt == torch.bfloat16 else 4
+        nset = max(2, int((400 << 20) // (rows * n * esz)) + 1)
+        sets = [torch.randn(rows, n, device="cuda").to(dt) for _ in range(nset)]
+        db = torch.zeros(n, device="cuda")
+        it = [0]
+
+        def fn():
+            ops.bias_grad(sets[it[0] % nset], db)
+            it[0] += 1
+        ms = time_graph(fn, reps=4 * nset)
+        print(json.dumps({"kernel": "bias_grad", "rows": rows, "n": n, "dtype": str(dt), "us": round(ms * 1e3, 2),
+                          "GBps": round(rows * n * esz / ms / 1e6, 1), "peak": hbm, "peak_kind": kind}), flush=True)
+
+
 def bench_gemm_bn():
     """Same shapes with the tile width forced (HM_GEMM_BN is read once per
     process, so each width runs in a subprocess)."""
@@ -249,6 +268,8 @@ if __name__ == "__main__":
     if what == "gemm_sweep":
         SWEEP = [(bn, cg, 0) for cg in (1, 2) for bn in (128, 192, 256)]
         what = "gemm"
+    if what == "bias":
+        bench_bias()
     if what == "attn_sweep":
         bench_attn_sweep()
     if what in ("attn", "all"):
