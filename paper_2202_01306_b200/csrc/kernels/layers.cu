@@ -378,6 +378,201 @@ __global__ void ln_bwd_kernel(const float *__restrict__ dy, const float *__restr
   }
 }
 
+// Default LayerNorm backward: one warp per row, WARPS warps per block.  Each
+// warp keeps PRIVATE dgamma/dbeta partials in shared memory (its lanes own
+// fixed float4 columns, so plain read-modify-writes, no atomics: shared-memory
+// float atomics compile to CAS spin loops on sm_100a), the block sums its warps'
+// partials once and adds them to global memory (one atomic per column per
+// block).  The second pass re-reads dy / x from L1 / L2.
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+    ln_bwd_warp_kernel(const float *__restrict__ dy, const float *__restrict__ x, const float *__restrict__ mean,
+                       const float *__restrict__ rstd, const float *__restrict__ gam, const float *resid, float *out,
+                       __nv_bfloat16 *__restrict__ out_bf, float *__restrict__ dgam, float *__restrict__ dbet,
+                       int64_t rows, int d, int rows_per_block) {
+  pdl_wait();
+  extern __shared__ float4 spart4[];  // [WARPS][2][d / 4]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n4 = d / 4;
+  float4 *pg = spart4 + (size_t)warp * 2 * n4;
+  float4 *pb = pg + n4;
+  for (int i = lane; i < n4; i += 32) pg[i] = pb[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 *g4 = reinterpret_cast<const float4 *>(gam);
+  const int64_t r_begin = (int64_t)blockIdx.x * rows_per_block;
+  const int64_t r_end = min(rows, r_begin + rows_per_block);
+  for (int64_t r = r_begin + warp; r < r_end; r += WARPS) {
+    const float4 *dyr = reinterpret_cast<const float4 *>(dy + r * d);
+    const float4 *xr = reinterpret_cast<const float4 *>(x + r * d);
+    const float mu = mean[r], rs = rstd[r];
+    float c1 = 0.f, c2 = 0.f;
+#pragma unroll 4
+    for (int i = lane; i < n4; i += 32) {
+      const float4 a = dyr[i], v = xr[i], gg = g4[i];
+      const float h0 = (v.x - mu) * rs, h1 = (v.y - mu) * rs, h2 = (v.z - mu) * rs, h3 = (v.w - mu) * rs;
+      const float e0 = a.x * gg.x, e1 = a.y * gg.y, e2 = a.z * gg.z, e3 = a.w * gg.w;
+      c1 += (e0 + e1) + (e2 + e3);
+      c2 += (e0 * h0 + e1 * h1) + (e2 * h2 + e3 * h3);
+      float4 q = pg[i];
+      q.x += a.x * h0; q.y += a.y * h1; q.z += a.z * h2; q.w += a.w * h3;
+      pg[i] = q;
+      float4 t = pb[i];
+      t.x += a.x; t.y += a.y; t.z += a.z; t.w += a.w;
+      pb[i] = t;
+    }
+    c1 = warp_sum(c1) / d;
+    c2 = warp_sum(c2) / d;
+    float4 *outr = reinterpret_cast<float4 *>(out + r * d);
+    const float4 *rr = resid ? reinterpret_cast<const float4 *>(resid + r * d) : nullptr;
+    uint2 *ob = out_bf ? reinterpret_cast<uint2 *>(out_bf + r * d) : nullptr;
+#pragma unroll 4
+    for (int i = lane; i < n4; i += 32) {
+      const float4 a = dyr[i], v = xr[i], gg = g4[i];
+      float4 o;
+      o.x = rs * (a.x * gg.x - c1 - (v.x - mu) * rs * c2);
+      o.y = rs * (a.y * gg.y - c1 - (v.y - mu) * rs * c2);
+      o.z = rs * (a.z * gg.z - c1 - (v.z - mu) * rs * c2);
+      o.w = rs * (a.w * gg.w - c1 - (v.w - mu) * rs * c2);
+      if (rr) {
+        const float4 q = rr[i];
+        o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+      }
+      outr[i] = o;
+      if (ob) {
+        __nv_bfloat162 p0 = __floats2bfloat162_rn(o.x, o.y), p1 = __floats2bfloat162_rn(o.z, o.w);
+        ob[i] = make_uint2(*reinterpret_cast<uint32_t *>(&p0), *reinterpret_cast<uint32_t *>(&p1));
+      }
+    }
+  }
+  __syncthreads();
+  const float *sp = reinterpret_cast<const float *>(spart4);
+  for (int c = threadIdx.x; c < d; c += WARPS * 32) {
+    float sg = 0.f, sb = 0.f;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) {
+      sg += sp[(size_t)w * 2 * d + c];
+      sb += sp[(size_t)w * 2 * d + d + c];
+    }
+    atomicAdd(&dgam[c], sg);
+    atomicAdd(&dbet[c], sb);
+  }
+}
+
+// Register-resident variant of ln_bwd_warp_kernel (d <= 1024): each lane loads
+// its NV4 float4 columns of dy and x once, all loads in flight together, and
+// computes dx from registers -- one HBM read of each row instead of a second
+// pass through L2.
+template <int NV4, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+    ln_bwd_rowreg_kernel(const float *__restrict__ dy, const float *__restrict__ x, const float *__restrict__ mean,
+                         const float *__restrict__ rstd, const float *__restrict__ gam, const float *resid, float *out,
+                         __nv_bfloat16 *__restrict__ out_bf, float *__restrict__ dgam, float *__restrict__ dbet,
+                         int64_t rows, int d, int rows_per_block) {
+  pdl_wait();
+  extern __shared__ float4 spart4[];  // [WARPS][2][d / 4]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n4 = d / 4;
+  float4 *pg = spart4 + (size_t)warp * 2 * n4;
+  float4 *pb = pg + n4;
+  for (int i = lane; i < n4; i += 32) pg[i] = pb[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 *g4 = reinterpret_cast<const float4 *>(gam);
+  const int64_t r_begin = (int64_t)blockIdx.x * rows_per_block;
+  const int64_t r_end = min(rows, r_begin + rows_per_block);
+  for (int64_t r = r_begin + warp; r < r_end; r += WARPS) {
+    const float4 *dyr = reinterpret_cast<const float4 *>(dy + r * d);
+    const float4 *xr = reinterpret_cast<const float4 *>(x + r * d);
+    float4 a[NV4], v[NV4];
+#pragma unroll
+    for (int k = 0; k < NV4; ++k) {
+      const int i = lane + 32 * k;
+      if (i < n4) {
+        a[k] = dyr[i];
+        v[k] = xr[i];
+      }
+    }
+    const float mu = mean[r], rs = rstd[r];
+    float c1 = 0.f, c2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV4; ++k) {
+      const int i = lane + 32 * k;
+      if (i < n4) {
+        const float4 gg = g4[i];
+        v[k].x = (v[k].x - mu) * rs; v[k].y = (v[k].y - mu) * rs;  // v := xhat
+        v[k].z = (v[k].z - mu) * rs; v[k].w = (v[k].w - mu) * rs;
+        const float e0 = a[k].x * gg.x, e1 = a[k].y * gg.y, e2 = a[k].z * gg.z, e3 = a[k].w * gg.w;
+        c1 += (e0 + e1) + (e2 + e3);
+        c2 += (e0 * v[k].x + e1 * v[k].y) + (e2 * v[k].z + e3 * v[k].w);
+        float4 q = pg[i];
+        q.x += a[k].x * v[k].x; q.y += a[k].y * v[k].y; q.z += a[k].z * v[k].z; q.w += a[k].w * v[k].w;
+        pg[i] = q;
+        float4 t = pb[i];
+        t.x += a[k].x; t.y += a[k].y; t.z += a[k].z; t.w += a[k].w;
+        pb[i] = t;
+      }
+    }
+    c1 = warp_sum(c1) / d;
+    c2 = warp_sum(c2) / d;
+    float4 *outr = reinterpret_cast<float4 *>(out + r * d);
+    const float4 *rr = resid ? reinterpret_cast<const float4 *>(resid + r * d) : nullptr;
+    uint2 *ob = out_bf ? reinterpret_cast<uint2 *>(out_bf + r * d) : nullptr;
+#pragma unroll
+    for (int k = 0; k < NV4; ++k) {
+      const int i = lane + 32 * k;
+      if (i < n4) {
+        const float4 gg = g4[i];
+        float4 o;
+        o.x = rs * (a[k].x * gg.x - c1 - v[k].x * c2);
+        o.y = rs * (a[k].y * gg.y - c1 - v[k].y * c2);
+        o.z = rs * (a[k].z * gg.z - c1 - v[k].z * c2);
+        o.w = rs * (a[k].w * gg.w - c1 - v[k].w * c2);
+        if (rr) {
+          const float4 q = rr[i];
+          o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+        }
+        outr[i] = o;
+        if (ob) {
+          __nv_bfloat162 p0 = __floats2bfloat162_rn(o.x, o.y), p1 = __floats2bfloat162_rn(o.z, o.w);
+          ob[i] = make_uint2(*reinterpret_cast<uint32_t *>(&p0), *reinterpret_cast<uint32_t *>(&p1));
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const float *sp = reinterpret_cast<const float *>(spart4);
+  for (int c = threadIdx.x; c < d; c += WARPS * 32) {
+    float sg = 0.f, sb = 0.f;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) {
+      sg += sp[(size_t)w * 2 * d + c];
+      sb += sp[(size_t)w * 2 * d + d + c];
+    }
+    atomicAdd(&dgam[c], sg);
+    atomicAdd(&dbet[c], sb);
+  }
+}
+
+template <int NV4>
+static int ln_bwd_rowreg(const float *dy, const float *x, const float *mean, const float *rstd, const float *g,
+                         const float *resid, float *out, void *out_bf, float *dg, float *db, int64_t rows, int d,
+                         cudaStream_t s) {
+  constexpr int kWarps = 4;
+  const size_t smem = (size_t)kWarps * 2 * d * sizeof(float);
+  static size_t attr_smem = 0;
+  if (smem > attr_smem) {
+    HM_CUDA(cudaFuncSetAttribute(ln_bwd_rowreg_kernel<NV4, kWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    attr_smem = smem;
+  }
+  const int per_sm = std::max<int>(1, std::min<int>(4, (int)((200 * 1024) / smem)));
+  int64_t blocks = (int64_t)sm_count() * per_sm;
+  int rpb = (int)((rows + blocks - 1) / blocks);
+  if (rpb < kWarps) rpb = kWarps;
+  blocks = (rows + rpb - 1) / rpb;
+  HM_CUDA(launch_pdl(ln_bwd_rowreg_kernel<NV4, kWarps>, dim3((unsigned)blocks), dim3(kWarps * 32), smem, s, dy, x,
+                     mean, rstd, g, resid, out, static_cast<__nv_bfloat16 *>(out_bf), dg, db, rows, d, rpb));
+  count_launch();
+  return HM_OK;
+}
+
 // Row-batched variant (default for d <= 2048): the 256 threads of a block
 // own fixed float4 columns (thread t: columns t, t + 256, ...), so every row
 // is read with fully coalesced 16-B loads exactly once (dy, x, resid), the
@@ -639,8 +834,46 @@ int ln_bwd(const float *dy, const float *x, const float *mean, const float *rstd
     return ln_bwd_reg<16>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
   }
   if (d % 4) return fail(HM_ERR_VALIDATION, "layernorm: d must be a multiple of 4");
+  static const bool use_smem_atomic = [] {
+    const char *e = getenv("HM_LN_BWD");
+    return e && e[0] == 'a';
+  }();
+  static const bool use_two_pass = [] {
+    const char *e = getenv("HM_LN_BWD");
+    return e && e[0] == 'w';
+  }();
+  // rows in registers up to d = 1024 (4096 x 1024: 17.9 vs 22.0 us for the
+  // shared-atomic kernel; 8192 x 1024: 28.3 vs 40.8 us); wider rows spill the
+  // register budget, so the two-pass kernel (dy / x re-read from L2) takes them
+  // (4096 x 1600: 31.8 vs 34.0 us registers, 35.1 us atomics) -- profiles/r01_ln_perf_v2.jsonl
+  if (!use_smem_atomic && !use_two_pass && d <= 1024) {
+    ProfScope ps(KC_LAYERNORM, s, 0, (resid ? 16.0 : 12.0) * rows * d + (out_bf ? 2.0 * rows * d : 0));
+    const int nv4 = (d / 4 + 31) / 32;
+    if (nv4 <= 2) return ln_bwd_rowreg<2>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
+    if (nv4 <= 4) return ln_bwd_rowreg<4>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
+    return ln_bwd_rowreg<8>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
+  }
+  if (!use_smem_atomic && (size_t)4 * 2 * d * sizeof(float) <= 160 * 1024) {  // 4 warps' private partials
+    constexpr int kWarps = 4;
+    const size_t smem = (size_t)kWarps * 2 * d * sizeof(float);
+    static size_t attr_smem = 0;
+    if (smem > attr_smem) {
+      HM_CUDA(cudaFuncSetAttribute(ln_bwd_warp_kernel<kWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr_smem = smem;
+    }
+    ProfScope ps(KC_LAYERNORM, s, 0, (resid ? 16.0 : 12.0) * rows * d + (out_bf ? 2.0 * rows * d : 0));
+    const int per_sm = std::max<int>(1, std::min<int>(8, (int)((200 * 1024) / smem)));
+    int64_t blocks = (int64_t)sm_count() * per_sm;
+    int rpb = (int)((rows + blocks - 1) / blocks);
+    if (rpb < kWarps) rpb = kWarps;
+    blocks = (rows + rpb - 1) / rpb;
+    HM_CUDA(launch_pdl(ln_bwd_warp_kernel<kWarps>, dim3((unsigned)blocks), dim3(kWarps * 32), smem, s, dy, x, mean,
+                       rstd, g, resid, out, static_cast<__nv_bfloat16 *>(out_bf), dg, db, rows, d, rpb));
+    count_launch();
+    return HM_OK;
+  }
   // HM_LN_BWD=t: row-batched tiles with register-accumulated dgamma/dbeta.
-  // Graph-timed on cold inputs it is no faster than the shared-atomic kernel
+  // Graph-timed on cold inputs it was no faster than the shared-atomic kernel
   // (34.3 vs 35.1 us at 4096 x 1600, 25.7 vs 22.0 us at 4096 x 1024; both
   // about 3.4 TB/s), so it stays opt-in (profiles/r01_ln_perf.jsonl).
   static const bool use_tile = [] {

@@ -226,9 +226,12 @@ def test_layernorm_fwd_bwd(ops, M, d):
     assert _rel(db, br.grad + 1) < 1e-5
 
 
-def test_layernorm_bwd_tile_variant():
-    """The opt-in row-batched LayerNorm backward (HM_LN_BWD=t, read once per
-    process) on the same shapes."""
+@pytest.mark.parametrize("variant", ["t", "a", "w", "reg"])
+def test_layernorm_bwd_variants(variant):
+    """Every LayerNorm backward variant (HM_LN_BWD is read once per process):
+    row-batched tiles (t), shared-memory atomics (a), two-pass warps with
+    private partials (w), register-accumulated (reg); the default picks
+    registers (d <= 1024) / two-pass (d <= 5120) / atomics."""
     import subprocess
     import sys
     here = __import__("os").path.dirname(__import__("os").path.abspath(__file__))
@@ -236,7 +239,7 @@ def test_layernorm_bwd_tile_variant():
     code = (f"import torch, sys; sys.path.insert(0, {here!r}); sys.path.insert(0, {here + '/..'!r}); "
             "import test_kernels_gpu as T; from paper_2202_01306_b200 import ops; "
             f"[T.test_layernorm_fwd_bwd(ops, *c) for c in {cases!r}]")
-    env = dict(__import__("os").environ, HM_LN_BWD="t")
+    env = dict(__import__("os").environ, HM_LN_BWD=variant)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
 
