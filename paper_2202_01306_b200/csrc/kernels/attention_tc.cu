@@ -1,6 +1,6 @@
-// attention_tc.cu -- flash-attention forward on the 5th-gen tensor cores.
+// attention_tc.cu -- flash attention (head_dim 64) on the 5th-gen tensor cores.
 //
-// One CTA per (sample, head, 128-query block), head_dim 64:
+// Forward, per 128-query tile (fwd_kernel: one CTA per tile):
 //   warp 0     TMA: Q once, then K_j / V_j tiles (128 keys) into a 2-stage ring
 //   warp 1     MMA issuer: S_j = Q K_j^T (128x128x64) into TMEM (2 buffers),
 //              O_j = P_j V_j (128x64x128) into TMEM (2 buffers); S_{j+1} is
@@ -10,6 +10,10 @@
 //              P_j (bf16) written to 128B-swizzled smem as the next MMA's A
 //              operand, O accumulated in registers one tile behind with the
 //              running rescale
+// The default forward kernels are persistent (one CTA per SM walking a work
+// list): fwd2p_kernel (query-block pairs, two ping-pong softmax warpgroups)
+// and fwdp_kernel (single tiles, short causal sequences).  Backward: bwd_kernel
+// (one CTA per 128-key block, two softmax warpgroups, dQ by TMA reduce-add).
 // Output o [tokens, d] bf16 and lse [tokens, H] (log2 domain) exactly as the
 // mma.sync kernel (attention.cu), which stays the fallback for head_dim 128
 // and for sequence lengths that are not a multiple of 128.
