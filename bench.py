@@ -140,11 +140,21 @@ def _barrier(world: int) -> None:
         dist.barrier()
 
 
-def _pcie_gbs():
+def _pcie_gbs(reps: int = 3):
     """Measured pinned GB/s of this GPU's link (1 GiB copies): H2D alone, D2H
     alone, and both directions at once on two streams ("bidir", the sum;
     46 + 46 = 92 GB/s on the B200 boxes vs 55.6 alone -- the swap engine runs
-    both directions concurrently for most of an iteration)."""
+    both directions concurrently for most of an iteration).  The best of
+    ``reps`` probes: a roofline denominator is the link's attainable rate, and
+    one probe has been seen reading half of it (a transient on the host)."""
+    best = {}
+    for _ in range(reps):
+        for k, v in _pcie_probe().items():
+            best[k] = max(best.get(k, 0.0), v)
+    return best
+
+
+def _pcie_probe():
     import torch
     n = 1 << 30
     h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
