@@ -908,31 +908,39 @@ int ln_bwd(const float *dy, const float *x, const float *mean, const float *rstd
 // ---- softmax cross-entropy over the (padded) vocabulary -----------------------------
 // logits fp32 [rows, ldl], valid columns [0, V); loss_sum += sum_r CE_r (double);
 // dlogits bf16 [rows, ldl] = (softmax - onehot) * scale, zero in the padding.
-__global__ void ce_kernel(const float *__restrict__ logits, const int32_t *__restrict__ labels, int64_t ldl, int V,
-                          __nv_bfloat16 *__restrict__ dlog, double *loss_sum, float scale) {
+// One block per row.  Pass 1: online (max, sum of exp) over float4 chunks,
+// one rescale per 4 logits.  Pass 2 (row re-read, mostly from L2): softmax
+// minus one-hot, scaled, written as bf16x4.  exp via exp2 of log2e-scaled
+// values.  ldl % 4 == 0 and 16-B aligned rows (the padded vocabulary).
+__device__ __forceinline__ void ce_merge(float &m, float &s, float mo, float so) {
+  const float mn = fmaxf(m, mo);
+  s = (m == -INFINITY ? 0.f : s * exp2f(m - mn)) + (mo == -INFINITY ? 0.f : so * exp2f(mo - mn));
+  m = mn;
+}
+
+__global__ void __launch_bounds__(512) ce_kernel(const float *__restrict__ logits, const int32_t *__restrict__ labels,
+                                                 int64_t ldl, int V, __nv_bfloat16 *__restrict__ dlog, double *loss_sum,
+                                                 float scale) {
   pdl_wait();
+  constexpr float kL2E = 1.4426950408889634f;
   const int64_t r = blockIdx.x;
   const float *row = logits + r * ldl;
+  const float4 *row4 = reinterpret_cast<const float4 *>(row);
   __shared__ float red_m[32], red_s[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  float m = -INFINITY, s = 0.f;
-  for (int i = threadIdx.x; i < V; i += blockDim.x) {
-    const float v = row[i];
-    if (v > m) {
-      s = s * __expf(m - v) + 1.f;
-      m = v;
-    } else {
-      s += __expf(v - m);
-    }
-  }
-  // combine (m, s) pairs: warp, then block
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    const float mo = __shfl_xor_sync(0xffffffff, m, o), so = __shfl_xor_sync(0xffffffff, s, o);
-    const float mn = fmaxf(m, mo);
-    s = (m == -INFINITY ? 0.f : s * __expf(m - mn)) + (mo == -INFINITY ? 0.f : so * __expf(mo - mn));
+  const int V4 = V >> 2;  // whole float4 chunks inside the vocabulary
+  float m = -INFINITY, s = 0.f;  // in log2 units: m = max(x * log2e)
+#pragma unroll 4
+  for (int i = threadIdx.x; i < V4; i += blockDim.x) {
+    const float4 v = row4[i];
+    const float a = v.x * kL2E, b = v.y * kL2E, c = v.z * kL2E, e = v.w * kL2E;
+    const float mn = fmaxf(fmaxf(m, fmaxf(a, b)), fmaxf(c, e));
+    s = (m == -INFINITY ? 0.f : s * exp2f(m - mn)) + ((exp2f(a - mn) + exp2f(b - mn)) + (exp2f(c - mn) + exp2f(e - mn)));
     m = mn;
   }
+  for (int i = 4 * V4 + threadIdx.x; i < V; i += blockDim.x) ce_merge(m, s, row[i] * kL2E, 1.f);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) ce_merge(m, s, __shfl_xor_sync(0xffffffff, m, o), __shfl_xor_sync(0xffffffff, s, o));
   if (lane == 0) {
     red_m[warp] = m;
     red_s[warp] = s;
@@ -942,12 +950,7 @@ __global__ void ce_kernel(const float *__restrict__ logits, const int32_t *__res
     m = lane < nw ? red_m[lane] : -INFINITY;
     s = lane < nw ? red_s[lane] : 0.f;
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const float mo = __shfl_xor_sync(0xffffffff, m, o), so = __shfl_xor_sync(0xffffffff, s, o);
-      const float mn = fmaxf(m, mo);
-      s = (m == -INFINITY ? 0.f : s * __expf(m - mn)) + (mo == -INFINITY ? 0.f : so * __expf(mo - mn));
-      m = mn;
-    }
+    for (int o = 16; o; o >>= 1) ce_merge(m, s, __shfl_xor_sync(0xffffffff, m, o), __shfl_xor_sync(0xffffffff, s, o));
     if (lane == 0) {
       red_m[0] = m;
       red_s[0] = s;
@@ -958,18 +961,29 @@ __global__ void ce_kernel(const float *__restrict__ logits, const int32_t *__res
   s = red_s[0];
   const int lab = labels[r];
   const float inv = 1.f / s;
-  __nv_bfloat16 *drow = dlog + r * ldl;
-  for (int i = threadIdx.x; i < ldl; i += blockDim.x) {
-    float gval = 0.f;
-    if (i < V) gval = (__expf(row[i] - m) * inv - (i == lab ? 1.f : 0.f)) * scale;
-    drow[i] = __float2bfloat16_rn(gval);
+  uint2 *drow = reinterpret_cast<uint2 *>(dlog + r * ldl);
+  const int L4 = (int)(ldl >> 2);
+#pragma unroll 4
+  for (int i = threadIdx.x; i < L4; i += blockDim.x) {
+    const float4 v = row4[i];
+    const int c0 = 4 * i;
+    float g[4] = {0.f, 0.f, 0.f, 0.f};
+    const float x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (c0 + k < V) g[k] = (exp2f(x[k] * kL2E - m) * inv - (c0 + k == lab ? 1.f : 0.f)) * scale;
+    __nv_bfloat162 p0 = __floats2bfloat162_rn(g[0], g[1]), p1 = __floats2bfloat162_rn(g[2], g[3]);
+    drow[i] = make_uint2(*reinterpret_cast<uint32_t *>(&p0), *reinterpret_cast<uint32_t *>(&p1));
   }
-  if (threadIdx.x == 0) atomicAdd(loss_sum, (double)(logf(s) + m - row[lab]));
+  // loss = ln(sum e^x) - x_label = (m + log2 s) ln 2 - x_label
+  if (threadIdx.x == 0) atomicAdd(loss_sum, (double)((m + log2f(s)) * 0.6931471805599453f - row[lab]));
 }
 
 int cross_entropy(const float *logits, const int32_t *labels, int64_t rows, int64_t ldl, int V, void *dlogits,
                   double *loss_sum, float scale, cudaStream_t s) {
   ProfScope ps(KC_XENT, s, 0, 6.0 * rows * ldl);
+  if ((ldl & 3) || ((uintptr_t)logits & 15) || ((uintptr_t)dlogits & 7))
+    return fail(HM_ERR_VALIDATION, "cross_entropy: rows must be 16-B aligned, ldl % 4 == 0");
   HM_CUDA(launch_pdl(ce_kernel, dim3((unsigned)rows), dim3(512), 0, s, logits, labels, ldl, V, static_cast<__nv_bfloat16 *>(dlogits), loss_sum,
                                             scale));
   count_launch();

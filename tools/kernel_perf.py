@@ -242,6 +242,26 @@ def bench_bias():
                           "GBps": round(rows * n * esz / ms / 1e6, 1), "peak": hbm, "peak_kind": kind}), flush=True)
 
 
+def bench_xent():
+    """LM-head cross-entropy (logits fp32 read twice, dlogits bf16 written),
+    graph-timed over logits sets larger than L2."""
+    _, hbm, kind = peaks()
+    for M, V, Vp in ((4096, 50257, 50304), (8192, 30522, 30592)):
+        nset = max(2, int((600 << 20) // (M * Vp * 4)) + 1)
+        sets = [torch.randn(M, Vp, device="cuda") for _ in range(nset)]
+        labels = torch.randint(0, V, (M,), device="cuda", dtype=torch.int32)
+        dl = torch.empty(M, Vp, device="cuda", dtype=torch.bfloat16)
+        loss = torch.zeros(1, device="cuda", dtype=torch.float64)
+        it = [0]
+
+        def fn():
+            ops.cross_entropy(sets[it[0] % nset], labels, V, dl, loss, 1.0)
+            it[0] += 1
+        ms = time_graph(fn, reps=2 * nset)
+        print(json.dumps({"kernel": "cross_entropy", "M": M, "V": V, "us": round(ms * 1e3, 1),
+                          "GBps_1read": round(M * Vp * 6 / ms / 1e6, 1), "peak": hbm, "peak_kind": kind}), flush=True)
+
+
 def bench_gemm_bn():
     """Same shapes with the tile width forced (HM_GEMM_BN is read once per
     process, so each width runs in a subprocess)."""
@@ -270,6 +290,8 @@ if __name__ == "__main__":
         what = "gemm"
     if what == "bias":
         bench_bias()
+    if what == "xent":
+        bench_xent()
     if what == "attn_sweep":
         bench_attn_sweep()
     if what in ("attn", "all"):
