@@ -17,6 +17,7 @@
 #include <string>
 
 #include "../runtime/common.hpp"
+#include "pdl.cuh"
 
 namespace hm {
 namespace attn_tc {
@@ -227,23 +228,35 @@ __global__ void __launch_bounds__(THREADS) fwd_kernel(const __nv_bfloat16 *__res
 }
 
 // D[token, h] = sum_c dO * O  (the softmax-backward row term)
+// D[token, head] = sum_k dO * O over the head's DH values: one thread per
+// (token, head) row of DH bf16 (DH * 2 bytes = DH / 8 16-B loads of each input,
+// all in flight); consecutive threads read consecutive rows (coalesced).
 template <int DH>
 __global__ void dvec_kernel(const __nv_bfloat16 *__restrict__ o, const __nv_bfloat16 *__restrict__ dout,
                             float *__restrict__ dvec, int64_t rows, int H) {
-  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+  pdl_wait();
+  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (w >= rows * H) return;
-  const __nv_bfloat16 *a = o + w * DH;  // [tokens, H*DH] contiguous -> (token, h) rows of DH
-  const __nv_bfloat16 *c = dout + w * DH;
-  float acc = 0.f;
-  for (int i = lane * 2; i < DH; i += 64) {
-    float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(a + i));
-    float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(c + i));
-    acc += x.x * y.x + x.y * y.y;
-  }
+  const uint4 *a = reinterpret_cast<const uint4 *>(o + w * DH);
+  const uint4 *c = reinterpret_cast<const uint4 *>(dout + w * DH);
+  uint4 va[DH / 8], vc[DH / 8];
 #pragma unroll
-  for (int off = 16; off; off >>= 1) acc += __shfl_xor_sync(0xffffffff, acc, off);
-  if (lane == 0) dvec[w] = acc;
+  for (int k = 0; k < DH / 8; ++k) {
+    va[k] = a[k];
+    vc[k] = c[k];
+  }
+  float acc = 0.f;
+#pragma unroll
+  for (int k = 0; k < DH / 8; ++k) {
+    const __nv_bfloat162 *x = reinterpret_cast<const __nv_bfloat162 *>(&va[k]);
+    const __nv_bfloat162 *y = reinterpret_cast<const __nv_bfloat162 *>(&vc[k]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 fx = __bfloat1622float2(x[j]), fy = __bfloat1622float2(y[j]);
+      acc = fmaf(fx.x, fy.x, fmaf(fx.y, fy.y, acc));
+    }
+  }
+  dvec[w] = acc;
 }
 
 template <int DH, bool CAUSAL>
@@ -421,14 +434,20 @@ __global__ void __launch_bounds__(THREADS) bwd_kernel(const __nv_bfloat16 *__res
   }
 }
 
+// dQ (fp32 accumulator [rows, d]) -> the Q third of dqkv [rows, 3d] as bf16,
+// four values per thread (float4 in, bf16x4 out); d % 4 == 0.
 __global__ void dq_convert(const float *__restrict__ dq_acc, __nv_bfloat16 *__restrict__ dqkv, int64_t rows, int d,
                            float scale) {
-  const int64_t n2 = rows * d / 2;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = 2 * i;
-    const int64_t r = e / d, c = e % d;
-    float2 v = *reinterpret_cast<const float2 *>(dq_acc + e);
-    *reinterpret_cast<__nv_bfloat162 *>(dqkv + r * 3 * (int64_t)d + c) = __floats2bfloat162_rn(v.x * scale, v.y * scale);
+  pdl_wait();
+  const uint32_t d4 = (uint32_t)(d / 4);
+  const int64_t n4 = rows * d4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / d4;
+    const int64_t c = 4 * (i - r * d4);
+    const float4 v = reinterpret_cast<const float4 *>(dq_acc)[i];
+    __nv_bfloat162 p0 = __floats2bfloat162_rn(v.x * scale, v.y * scale), p1 = __floats2bfloat162_rn(v.z * scale, v.w * scale);
+    *reinterpret_cast<uint2 *>(dqkv + r * 3 * (int64_t)d + c) =
+        make_uint2(*reinterpret_cast<uint32_t *>(&p0), *reinterpret_cast<uint32_t *>(&p1));
   }
 }
 
@@ -468,7 +487,7 @@ static int bwd_launch(const __nv_bfloat16 *qkv, const __nv_bfloat16 *o, const __
   ProfScope ps(KC_ATTN_BWD, s, 10.0 * B * (double)S * S * H * DH * (CAUSAL ? 0.5 : 1.0), (double)rows * d * 2 * 8);
   HM_CUDA(cudaMemsetAsync(dq_acc, 0, rows * d * sizeof(float), s));
   const int64_t warps = rows * H;
-  dvec_kernel<DH><<<(unsigned)((warps * 32 + 255) / 256), 256, 0, s>>>(o, dout, dvec, rows, H);
+  HM_CUDA(launch_pdl(dvec_kernel<DH>, dim3((unsigned)((warps + 127) / 128)), dim3(128), 0, s, o, dout, dvec, rows, H));
   const float scale = 1.f / sqrtf((float)DH);
   // The tcgen05 backward (attention_tc.cu: TMEM accumulators, dQ as one TMA
   // reduce-add per query block) is the default where it applies (head_dim 64,
@@ -481,11 +500,11 @@ static int bwd_launch(const __nv_bfloat16 *qkv, const __nv_bfloat16 *o, const __
   if (use_tc && attn_tc::supported(S, DH)) {
     // tcgen05 main kernel; it folds the softmax scale into dq_acc
     HM_TRY(attn_tc::backward_main(qkv, dout, lse, dvec, dq_acc, dqkv, B, S, H, CAUSAL ? 1 : 0, s));
-    dq_convert<<<1184, 256, 0, s>>>(dq_acc, dqkv, rows, d, 1.f);
+    HM_CUDA(launch_pdl(dq_convert, dim3(1184), dim3(256), 0, s, (const float *)dq_acc, dqkv, rows, d, 1.f));
   } else {
     k<<<dim3(S / BKV, B * H), THREADS, bwd_smem<DH>(), s>>>(qkv, dout, lse, dvec, dq_acc, dqkv, S, H,
                                                              1.4426950408889634f * scale, scale);
-    dq_convert<<<1184, 256, 0, s>>>(dq_acc, dqkv, rows, d, scale);
+    HM_CUDA(launch_pdl(dq_convert, dim3(1184), dim3(256), 0, s, (const float *)dq_acc, dqkv, rows, d, scale));
   }
   count_launch(3);
   HM_CUDA(cudaGetLastError());
