@@ -923,9 +923,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
       // row read from TMEM in CH-column pieces (CH / 32 loads in flight per wait)
       auto tile = [&](auto diag_tag) -> float {
         constexpr bool DIAG = decltype(diag_tag)::value;
-        // full attention: 64-column halves (1129 vs 1220 ns per tile at s = 1024);
-        // causal keeps 32-column quarters (the masked instantiation spills more)
-        constexpr int CH = CAUSAL ? 32 : 64;
+        // 64-column halves (1135 vs 1220 ns per tile at s = 1024, full attention);
+        // the masked diagonal tile reads 32-column quarters
+        constexpr int CH = DIAG ? 32 : 64;
         float mx = -INFINITY;
 #pragma unroll
         for (int c0 = 0; c0 < BKV; c0 += CH) {
@@ -985,12 +985,23 @@ __global__ void __launch_bounds__(kThreads2, 1)
         l = l * alpha + rs;
         return alpha;
       };
-      for (int j = 0; j < nkv; ++j, ++n) {
+      // unmasked tiles in the loop; under causal masking the diagonal tile
+      // (always the last, j = qb) runs after it with its own instantiation
+      const int nfull = CAUSAL ? nkv - 1 : nkv;
+      for (int j = 0; j < nfull; ++j, ++n) {
         mbar_wait(&s_full[t], n & 1);
         tc_fence_after();
-        const float alpha = (CAUSAL && j == qb) ? tile(std::true_type{}) : tile(std::false_type{});
+        const float alpha = tile(std::false_type{});
         if (j > 0) add_o(n - 1, alpha_prev);
         alpha_prev = alpha;
+      }
+      if (CAUSAL) {
+        mbar_wait(&s_full[t], n & 1);
+        tc_fence_after();
+        const float alpha = tile(std::true_type{});
+        if (nfull > 0) add_o(n - 1, alpha_prev);
+        alpha_prev = alpha;
+        ++n;
       }
       add_o(n - 1, alpha_prev);
       const float inv = 1.f / l;
