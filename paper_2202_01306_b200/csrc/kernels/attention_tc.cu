@@ -51,7 +51,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     fwd_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16 *__restrict__ out, float *__restrict__ lse, int S,
                int H, float scale_log2) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned base by pointer arithmetic on the __shared__ array, so the
+  // compiler keeps the shared address space (STS / LDS, not generic ST / LD)
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *sQ = smem;
   uint8_t *sK = sQ + kTileBytes;
   uint8_t *sV = sK + 2 * kTileBytes;
@@ -280,7 +282,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     fwdp_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16 *__restrict__ out, float *__restrict__ lse,
                 int S, int H, int BH, float scale_log2) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned base by pointer arithmetic on the __shared__ array, so the
+  // compiler keeps the shared address space (STS / LDS, not generic ST / LD)
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *sQ = smem;                  // [2] items
   uint8_t *sK = sQ + 2 * kTileBytes;   // [2] stages
   uint8_t *sV = sK + 2 * kTileBytes;   // [2] stages
@@ -526,7 +530,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
     fwd2_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16 *__restrict__ out, float *__restrict__ lse,
                 int S, int H, float scale_log2) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned base by pointer arithmetic on the __shared__ array, so the
+  // compiler keeps the shared address space (STS / LDS, not generic ST / LD)
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *sQ = smem;                   // [2] query tiles
   uint8_t *sK = sQ + 2 * kTileBytes;    // [2] stages
   uint8_t *sV = sK + 2 * kTileBytes;    // [2] stages
@@ -760,7 +766,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
     fwd2p_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16 *__restrict__ out, float *__restrict__ lse,
                  int S, int H, int BH, float scale_log2) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned base by pointer arithmetic on the __shared__ array, so the
+  // compiler keeps the shared address space (STS / LDS, not generic ST / LD)
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *sQ = smem;                   // [2 items][2 tiles]
   uint8_t *sK = sQ + 4 * kTileBytes;    // [2] stages
   uint8_t *sV = sK + 2 * kTileBytes;    // [2] stages
@@ -1041,7 +1049,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     fwd3_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16 *__restrict__ out, float *__restrict__ lse,
                 int S, int H, float scale_log2) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned base by pointer arithmetic on the __shared__ array, so the
+  // compiler keeps the shared address space (STS / LDS, not generic ST / LD)
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *sQ = smem;
   uint8_t *sK = sQ + kTileBytes;
   uint8_t *sV = sK + 2 * kTileBytes;
@@ -1255,7 +1265,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
                const float *__restrict__ lse, const float *__restrict__ dvec, float *__restrict__ dq_acc,
                __nv_bfloat16 *__restrict__ dqkv, int S, int H, float scale_log2, float scale) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned base by pointer arithmetic on the __shared__ array, so the
+  // compiler keeps the shared address space (STS / LDS, not generic ST / LD)
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *sK = smem;
   uint8_t *sV = sK + kTileBytes;
   uint8_t *sQ = sV + kTileBytes;          // [2] stages
@@ -1451,17 +1463,25 @@ __global__ void __launch_bounds__(kThreads2, 1)
         auto elementwise = [&](auto diag_tag) {
           constexpr bool DIAG = decltype(diag_tag)::value;
 #pragma unroll
-          for (int c = 0; c < 32; c += 2) {
+          for (int c = 0; c < 32; c += 4) {
             const int qi = hq * 64 + c0 + c;
-            float p0 = ex2(fmaf(__uint_as_float(sv[c]), scale_log2, -Ls[qi]));
-            float p1 = ex2(fmaf(__uint_as_float(sv[c + 1]), scale_log2, -Ls[qi + 1]));
-            if (DIAG && qi < r) p0 = 0.f;  // query < key: masked
-            if (DIAG && qi + 1 < r) p1 = 0.f;
-            const float s0 = p0 * (__uint_as_float(dp[c]) - Ds[qi]);
-            const float s1 = p1 * (__uint_as_float(dp[c + 1]) - Ds[qi + 1]);
-            __nv_bfloat162 tp = __floats2bfloat162_rn(p0, p1), td = __floats2bfloat162_rn(s0, s1);
-            pk[c >> 1] = *reinterpret_cast<uint32_t *>(&tp);
-            dk[c >> 1] = *reinterpret_cast<uint32_t *>(&td);
+            // lse / D of four queries per 16-B shared-memory load (broadcast)
+            const float4 L4 = *reinterpret_cast<const float4 *>(Ls + qi);
+            const float4 D4 = *reinterpret_cast<const float4 *>(Ds + qi);
+            const float lq[4] = {L4.x, L4.y, L4.z, L4.w}, dq4[4] = {D4.x, D4.y, D4.z, D4.w};
+            float p[4], g[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              p[k] = ex2(fmaf(__uint_as_float(sv[c + k]), scale_log2, -lq[k]));
+              if (DIAG && qi + k < r) p[k] = 0.f;  // query < key: masked
+              g[k] = p[k] * (__uint_as_float(dp[c + k]) - dq4[k]);
+            }
+            __nv_bfloat162 tp0 = __floats2bfloat162_rn(p[0], p[1]), tp1 = __floats2bfloat162_rn(p[2], p[3]);
+            __nv_bfloat162 td0 = __floats2bfloat162_rn(g[0], g[1]), td1 = __floats2bfloat162_rn(g[2], g[3]);
+            pk[c >> 1] = *reinterpret_cast<uint32_t *>(&tp0);
+            pk[(c >> 1) + 1] = *reinterpret_cast<uint32_t *>(&tp1);
+            dk[c >> 1] = *reinterpret_cast<uint32_t *>(&td0);
+            dk[(c >> 1) + 1] = *reinterpret_cast<uint32_t *>(&td1);
           }
         };
         if (diag) elementwise(std::true_type{});

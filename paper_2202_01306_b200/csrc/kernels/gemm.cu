@@ -237,7 +237,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   using C = Cfg<BN, CG>;
   constexpr int kTileM = BM * CG;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned base by pointer arithmetic on the __shared__ array, so the
+  // compiler keeps the shared address space (STS / LDS, not generic ST / LD)
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *sA = smem;
   uint8_t *sB = smem + C::kStages * C::kABytes;
   uint8_t *sEpi = sB + C::kStages * C::kBBytes;
