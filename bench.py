@@ -140,6 +140,69 @@ def _barrier(world: int) -> None:
         dist.barrier()
 
 
+def _pcie_rates(world: int, rank: int) -> tuple[dict, dict]:
+    """(isolated, concurrent) link rates of this rank's GPU.  Isolated: the
+    ranks probe one after another (the per-GPU PCIe bound).  Concurrent: all
+    ranks probe at once; the sum over ranks is the host root complex's
+    aggregate rate (the host-root bound)."""
+    iso = {}
+    for r in range(world):
+        _barrier(world)
+        if r == rank:
+            iso = _pcie_gbs()
+    _barrier(world)
+    conc = _pcie_gbs(reps=1) if world > 1 else dict(iso)
+    _barrier(world)
+    return iso, conc
+
+
+def _sum_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)
+    return float(t.item())
+
+
+def _nccl_busbw(world: int, nbytes: int = 256 << 20) -> float:
+    """Measured all-reduce bus bandwidth (GB/s): 2(N-1)/N x bytes / time."""
+    if world == 1:
+        return 0.0
+    import torch
+    import torch.distributed as dist
+    x = torch.ones(nbytes // 4, dtype=torch.float32, device="cuda")
+    for _ in range(3):
+        dist.all_reduce(x)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        dist.all_reduce(x)
+    e1.record()
+    torch.cuda.synchronize()
+    t = _max_over_ranks(e0.elapsed_time(e1) / 1e3 / 10, world)
+    return 2 * (world - 1) / world * nbytes / t / 1e9
+
+
+def _host_precheck(spec, world: int, mode: str, stash_bytes: int) -> str | None:
+    """Pinned host memory the job needs (per-rank W + K replicas under
+    Harmony-DP, one shared copy under PP) vs what the host has available."""
+    need = spec.total_params() * 12 * (world if mode == "dp" else 1) + stash_bytes
+    avail = 0
+    try:
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemAvailable:"):
+                avail = int(ln.split()[1]) * 1024
+    except OSError:
+        return None
+    if avail and need > 0.92 * avail:
+        return (f"needs {need / 2**30:.1f} GiB of pinned host memory (W + Adam state{' per DP rank' if mode == 'dp' else ''}"
+                f" + stash), the host has {avail / 2**30:.1f} GiB available")
+    return None
+
+
 def _pcie_gbs(reps: int = 3):
     """Measured pinned GB/s of this GPU's link (1 GiB copies): H2D alone, D2H
     alone, and both directions at once on two streams ("bidir", the sum;
@@ -262,63 +325,115 @@ def cnn_port_sample(spec, threads: int, seconds_cap: float = 30.0) -> dict:
                       f"(fwd + bwd + Adam), {reps} reps of {dt:.2f} s"}
 
 
-def cpu_port_sample(spec, threads: int, seconds_cap: float = 30.0) -> dict:
-    """Time the torch-CPU fp32 port (oracle/gpt_cpu.py) on a bounded sample:
-    one sample through a 2-layer model of the workload's shapes (embedding +
-    1 block + 1 block with LN_f/head), fwd + bwd + Adam, then scale by the
-    FLOP ratio to the full model's per-sample cost."""
+def cpu_port_iteration(spec, samples: int, threads: int, groups=None) -> dict:
+    """One REAL training iteration of the torch-CPU fp32 port (oracle/gpt_cpu.py)
+    on the full-depth model: ``samples`` sequences forward + backward through
+    every layer, then Adam over every parameter -- the same work the Harmony
+    schedule does in one iteration at D = ``samples`` (its F/B/U tasks
+    compute exactly full-batch backprop followed by a per-pack Adam).  Nothing
+    is extrapolated: the returned rate is samples / measured seconds."""
     import numpy as np
     import torch
     from oracle.gpt_cpu import GPTOracle
-    from paper_2202_01306_b200.model import GPTSpec, synthetic_batch
+    from paper_2202_01306_b200.model import synthetic_batch
     torch.set_num_threads(threads)
-    small = GPTSpec(2, spec.d_model, spec.n_head, spec.seq_len, spec.vocab, spec.causal, "cpu-sample")
-    n = small.total_params()
+    n = spec.total_params()
     g = torch.Generator().manual_seed(0)
-    w = (torch.randn(n, generator=g) * 0.02).numpy()
-    off = np.cumsum([0] + [small.layer_params(L) for L in range(small.n_layer)])
-    o = GPTOracle(small, w, off)
-    tok, lab = synthetic_batch(small, 1)
-    o.step(tok, lab, [1])  # warm
+    w = torch.empty(n, dtype=torch.float32).normal_(0.0, 0.02, generator=g).numpy()
+    off = np.cumsum([0] + [spec.layer_params(L) for L in range(spec.n_layer)])
+    o = GPTOracle(spec, w, off)
+    del w
+    tok, lab = synthetic_batch(spec, samples)
+    groups = groups or [1] * samples
     t0 = time.perf_counter()
-    reps = 0
-    while True:
-        o.step(tok, lab, [1])
-        reps += 1
-        if time.perf_counter() - t0 > min(seconds_cap, 10.0) or reps >= 5:
-            break
-    dt = (time.perf_counter() - t0) / reps
-    f_small = sum(small.layer_fwd_flops(L, 1) for L in range(2))
-    f_full = sum(spec.layer_fwd_flops(L, 1) for L in range(spec.n_layer))
-    per_sample = dt * f_full / f_small
-    return {"value": 1.0 / per_sample, "unit": "samples/s", "cores": threads, "kind": "port",
-            "sample": f"torch-CPU fp32 port (oracle/gpt_cpu.py), 1 sample x 2-layer {spec.name}-shaped model "
-                      f"(embedding, blocks, LN_f + head, Adam), {reps} reps of {dt:.2f} s, scaled by FLOPs "
-                      f"to {spec.n_layer} layers ({f_full / f_small:.1f}x)"}
+    loss = o.step(tok, lab, groups)
+    dt = time.perf_counter() - t0
+    del o
+    return {"value": samples / dt, "unit": "samples/s", "cores": threads, "kind": "port", "seconds": dt,
+            "loss": loss,
+            "sample": f"one measured iteration of the torch-CPU fp32 port (oracle/gpt_cpu.py) of the full "
+                      f"{spec.n_layer}-layer {spec.name}: {samples} sample(s) x {spec.seq_len} tokens forward + "
+                      f"backward (member loop {groups}) + Adam over all {n / 1e9:.2f} B parameters, "
+                      f"{dt:.1f} s on {threads} threads"}
+
+
+def planner_port_seconds(graph, machine, prof) -> dict:
+    """Single-core wall time of the reference's planner path restated in pure
+    Python (oracle/schedule.py: generate_task_graph -> _build_items -> _run,
+    taskgraph.py:211-400, simulator.py:150-375) for the workload's config."""
+    from oracle import schedule as S
+    cfg = graph.config
+    ocfg = {"u_f": cfg.u_f, "p_f": [list(p) for p in cfg.p_f], "u_b": cfg.u_b, "p_b": [list(p) for p in cfg.p_b],
+            "minibatch": cfg.minibatch, "mode": cfg.mode.value}
+    tab = prof.tables(prof.layer_count, max(cfg.minibatch, 1))
+    oprof = {k: tab[k] for k in ("x", "y", "w", "dw", "k", "tF", "tB", "tU")}
+    groups = {}
+    for i, grp in enumerate(machine.p2p_groups):
+        for x in grp:
+            groups[x] = i
+    omach = {"gpu_count": machine.gpu_count, "pcie": machine.pcie_bandwidth,
+             "root": machine.root_link_bandwidth, "p2p_group_of": [groups[i] for i in range(machine.gpu_count)],
+             "cpu_offload_update": machine.cpu_offload_update, "update_cpu_rate": machine.update_cpu_rate}
+    t0 = time.perf_counter()
+    tasks = S.task_graph(ocfg, machine.gpu_count)
+    items = S.ledger_items(tasks, omach, oprof)
+    makespan = S.run(items)
+    dt = time.perf_counter() - t0
+    return {"seconds": round(dt, 4), "tasks": len(tasks), "items": len(items), "makespan_ns": makespan,
+            "cores": 1, "what": "task graph + swap plan + event-driven estimate (pure-Python restatement of the "
+                                "reference planner, oracle/schedule.py), single core"}
 
 
 def run_reference(args) -> None:
+    """Reference arm: the reference has no training runtime, so
+    the path's CPU implementation is the torch-CPU fp32 port of one Harmony
+    iteration.  It runs ONE full-depth iteration at D = 4 (BASELINE.md's
+    recipe for c3) on all host threads -- minutes of CPU work, so the
+    driver's --steps / --warmup are not repeated: the line reports the steps
+    that actually ran (1, no warm-up)."""
     world, rank, _ = _dist()
     if rank != 0:
         return
-    from paper_2202_01306_b200.model import GPT_PRESETS
+    import torch
+    from paper_2202_01306_b200 import MachineModel  # noqa: F401
+    import paper_2202_01306_b200 as H
+    from paper_2202_01306_b200.model import GPT_PRESETS, gpt_machine, gpt_profiles
     preset, per_gpu, u, lpp, alpha_gib, mode, *_ = WORKLOADS[args.workload]
     spec = GPT_PRESETS[preset]
     threads = len(os.sched_getaffinity(0))
-    samples = []
-    for _ in range(max(1, args.steps)):
-        samples.append(cpu_port_sample(spec, threads, seconds_cap=20.0)["value"])
-    cb = cpu_port_sample(spec, threads, seconds_cap=20.0)
-    v = statistics.median(samples)
-    line = {"impl": "reference", "metric": "samples/s (Harmony layer-pack training, GPT-2 XL)", "value": v,
-            "unit": "samples/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000.0 * per_gpu * args.gpus / v, "higher_is_better": True, "scaling": "weak",
+    D = per_gpu * args.gpus
+    R = spec.n_layer
+    packs = tuple((i, min(i + lpp, R) - 1) for i in range(0, R, lpp))
+    machine = gpt_machine(args.gpus, alpha_bytes=alpha_gib << 30)
+    prof = gpt_profiles(spec)
+    graph = H.generate_task_graph(H.Configuration(u, packs, u, packs, D, H.Mode(mode)), machine, prof)
+    plan = planner_port_seconds(graph, machine, prof)
+    sample_d = min(4, D)
+    it = cpu_port_iteration(spec, sample_d, threads)
+    v = it["value"]
+    line = {"impl": "reference", "metric": "samples/s (Harmony layer-pack training, GPT-2 XL)"
+            if preset == "gpt2-xl" else f"samples/s (Harmony layer-pack training, {spec.name})", "value": v,
+            "unit": "samples/s", "n_gpus": args.gpus, "steps": 1, "warmup": 0,
+            "ms_per_step": 1000.0 * it["seconds"], "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.workload}: {spec.name} Harmony-{mode.upper()} per-GPU minibatch {per_gpu}",
-                       "global_batch": per_gpu * args.gpus, "seq_len": spec.seq_len},
-            "cpu_baseline": dict(cb, value=v),
+            "config": _config(args.workload, spec, mode, lpp, u, alpha_gib, D, args.gpus,
+                              (WORKLOADS[args.workload][6:] or ("fp32",))[0]),
+            "sample": f"iteration at D={sample_d} (of the workload's D={D}): the per-sample work is the same, "
+                      f"the per-iteration Adam is amortised over {sample_d} instead of {D} samples",
+            "requested": {"steps": args.steps, "warmup": args.warmup},
+            "cpu_baseline": {k: it[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "planner_port": plan, "torch_threads": torch.get_num_threads(),
             "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def _config(workload, spec, mode, lpp, u, alpha_gib, D, world, payload) -> dict:
+    return {"workload": f"{workload}: {spec.name} Harmony-{mode.upper()}, packs of {lpp} layers, "
+                        f"u_f=u_b={u}, alpha={alpha_gib} GiB/GPU",
+            "global_batch": D, "seq_len": getattr(spec, "seq_len", None), "parallelism": f"harmony-{mode}{world}",
+            "l2": "inputs larger than L2 (W and K stream from host every step)",
+            "w_payload": payload if payload == "fp32" else
+            "bf16 planes (SURVEY 8f4b fast mode: forward W rows differ from the reference ledger)"}
 
 
 def run_native(args) -> None:
@@ -345,22 +460,53 @@ def run_native(args) -> None:
     R = spec.n_layer
     packs = tuple((i, min(i + lpp, R) - 1) for i in range(0, R, lpp))
     cfg = H.Configuration(u, packs, u, packs, D, H.Mode(mode))
-    pcie = _pcie_gbs()
+    pcie, pcie_conc = _pcie_rates(world, rank)
     machine = gpt_machine(world, alpha_bytes=alpha_gib << 30, pcie_gbs=min(pcie["h2d"], pcie["d2h"]) * 1e9)
     prof = cnn_profiles(spec) if is_cnn else gpt_profiles(spec)
     graph = H.generate_task_graph(cfg, machine, prof)
+    skip = _host_precheck(spec, world, mode, HarmonyRuntime.stash_bytes_for(graph, prof))
+    if skip:
+        if rank == 0:
+            print(json.dumps({"metric": f"samples/s (Harmony layer-pack training, {spec.name})", "value": None,
+                              "unit": "samples/s", "n_gpus": world, "skipped": skip,
+                              "config": {"workload": args.workload}}), flush=True)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
     payload = (WORKLOADS[args.workload][6:] or ("fp32",))[0]
     rt = HarmonyRuntime(spec, alpha_bytes=alpha_gib << 30, device=local, w_payload=payload)
     sim = H.simulate(graph, machine, prof, w_fwd_bytes=rt.w_fwd_bytes())
     # weights drawn on the GPU (seconds, also with 8 ranks initialising at once);
     # the CPU generator is what the parity tests use
-    rt.init_weights(0, device=None if is_cnn else "cuda")
-    if world > 1:
+    pp_multi = mode == "pp" and world > 1
+    if pp_multi:
+        # Harmony-PP: one pinned host copy of W / K / stash shared by every rank
+        # (rank 0 creates and initialises it); activations move over NVLink
+        import torch.distributed as dist
+        name = [f"hm_bench_{os.getpid()}" if rank == 0 else None]
+        dist.broadcast_object_list(name, src=0)
+        stash = HarmonyRuntime.stash_bytes_for(graph, prof)
+        if rank == 0:
+            rt.share_arenas(name[0], True, stash)
+            rt.init_weights(0, device=None if is_cnn else "cuda")
+        dist.barrier()
+        if rank != 0:
+            rt.share_arenas(name[0], False, stash)
+    else:
+        rt.init_weights(0, device=None if is_cnn else "cuda")
+    if world > 1 and mode == "dp":
         import torch.distributed as dist
         obj = [HarmonyRuntime.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         rt.init_comm(obj[0], world, rank)
     rt.load(graph, machine, prof, rank=rank)
+    if pp_multi:
+        blobs = [None] * world
+        dist.all_gather_object(blobs, rt.ipc_export())
+        for b in blobs:
+            rt.ipc_import(b)
+        dist.barrier()
     lo, hi = rt.sample_range()
     if is_cnn:
         img_all, labc_all = synthetic_images(spec, D)
@@ -385,6 +531,12 @@ def run_native(args) -> None:
     launches = ops.launch_count() - launches0
     cnt = rt.counters()
     rep = rt.report()
+    ledgers = [rep.ledger]
+    if world > 1:  # the plan's ledger is the union of the ranks' executed rows
+        import torch.distributed as dist
+        ledgers = [None] * world
+        dist.all_gather_object(ledgers, rep.ledger)
+    ledger_ok = sorted(r for led in ledgers for r in led) == sorted(sim.ledger)
     # stream utilisation of the last timed iteration (measured CUDA events)
     busy = {"h2d": 0, "d2h": 0, "compute": 0, "update": 0}
     for e in rep.trace:
@@ -439,7 +591,18 @@ def run_native(args) -> None:
     t_h2d = swap_in / (pcie["h2d"] * 1e9)
     t_d2h = swap_out / (pcie["d2h"] * 1e9)
     t_bidir = (swap_in + swap_out) / (pcie["bidir"] * 1e9)  # the link's two directions share ~92 GB/s
-    t_roof = max(t_compute, t_h2d, t_d2h, t_bidir)
+    # multi-GPU terms: the host root complex (every rank's swaps
+    # at the aggregate concurrent rate), NCCL (ring volume at the measured bus
+    # bandwidth), NVLink peer hand-offs (none under Harmony-DP)
+    tot_in = sum(r[6] for r in sim.ledger if r[1] == 0 and r[4] in ("cpu_gpu_swap", "message_passing"))
+    tot_out = sum(r[6] for r in sim.ledger if r[1] == 2 and r[4] in ("cpu_gpu_swap", "message_passing"))
+    root_h2d = _sum_over_ranks(pcie_conc["h2d"], world)
+    root_d2h = _sum_over_ranks(pcie_conc["d2h"], world)
+    t_root = max(tot_in / (root_h2d * 1e9), tot_out / (root_d2h * 1e9)) if world > 1 else 0.0
+    busbw = _nccl_busbw(world)
+    t_nccl = cnt["nccl_bytes"] / (busbw * 1e9) if world > 1 and busbw else 0.0
+    p2p = sum(r[6] for r in sim.ledger if r[4] == "peer2peer")
+    t_roof = max(t_compute, _max_over_ranks(max(t_h2d, t_d2h, t_bidir), world), t_root, t_nccl)
     ms_step = 1000.0 * t_total / args.steps
     clk = clocks.summary()
     share = {k: round(v["ms"] / (prof_iter_ns / 1e6), 4) for k, v in kstats.items()}
@@ -459,15 +622,16 @@ def run_native(args) -> None:
         "data": ("synthetic (images N(0,1), 3 channels zero-padded to 64, labels U[0,classes) seed 1234; "
                  "He-normal weights seed 0)") if is_cnn else
                 "synthetic (tokens U[0,V) seed 1234; weights N(0,0.02) from a CUDA generator seeded 0)",
-        "config": {"workload": f"{args.workload}: {spec.name} Harmony-{mode.upper()}, packs of {lpp} layers, "
-                               f"u_f=u_b={u}, alpha={alpha_gib} GiB/GPU",
-                   "global_batch": D, "seq_len": getattr(spec, "seq_len", None), "parallelism": f"harmony-{mode}{world}",
-                   "l2": "inputs larger than L2 (W and K stream from host every step)",
-                   "w_payload": payload if payload == "fp32" else
-                   "bf16 planes (SURVEY 8f4b fast mode: forward W rows differ from the reference ledger)"},
+        "config": _config(args.workload, spec, mode, lpp, u, alpha_gib, D, world, payload),
         "swap_gb_per_iter": round((swap_in + swap_out) / 1e9, 3),
         "swap_h2d_gb": round(swap_in / 1e9, 3), "swap_d2h_gb": round(swap_out / 1e9, 3),
-        "step_roofline": {"bound": "pcie" if t_roof > t_compute else "tensor", "t_roof_ms": round(1000 * t_roof, 2),
+        "step_roofline": {"bound": ("tensor" if t_roof == t_compute else "host_root" if t_roof == t_root
+                                    else "nccl" if t_roof == t_nccl else "pcie"),
+                          "t_roof_ms": round(1000 * t_roof, 2),
+                          "t_root_ms": round(1000 * t_root, 2), "t_nccl_ms": round(1000 * t_nccl, 2),
+                          "t_nvlink_ms": 0.0, "p2p_bytes": p2p,
+                          "root_gbs": {"h2d": round(root_h2d, 2), "d2h": round(root_d2h, 2)} if world > 1 else None,
+                          "nccl_busbw_gbs": round(busbw, 1) if world > 1 else None,
                           "t_compute_ms": round(1000 * t_compute, 2), "t_h2d_ms": round(1000 * t_h2d, 2),
                           "t_d2h_ms": round(1000 * t_d2h, 2), "t_bidir_ms": round(1000 * t_bidir, 2),
                           "frac": round(1000 * t_roof / ms_step, 4),
@@ -495,14 +659,21 @@ def run_native(args) -> None:
                 "d2h_bytes_per_step": 8},
         "gpu_launches": int(launches),
         "clocks": clk,
-        "loss": [round(x, 5) for x in losses[-3:]],
-        "ledger_rows": len(rep.ledger), "ledger_equals_plan": rep.ledger == sim.ledger,
+        "loss": [round(_sum_over_ranks(x, world) if mode == "pp" else x, 5) for x in losses[-3:]],
+        "ledger_rows": sum(len(x) for x in ledgers), "ledger_equals_plan": ledger_ok,
+        "host_arena_numa_node": rt.lib.hm_runtime_numa_node(rt.handle),
         "device_bytes": cnt["device_bytes"],
         "nccl_allreduce_gb_per_iter": round(cnt["nccl_bytes"] / 1e9, 3),
     }
     if not args.no_cpu_baseline and rank == 0 and world == 1:
-        line["cpu_baseline"] = (cnn_port_sample if is_cnn else cpu_port_sample)(
-            spec, len(os.sched_getaffinity(0)), seconds_cap=20.0)
+        # bounded sample: one measured full-depth iteration at D = 1 (GPT), one
+        # sample through the whole chain (CNN)
+        threads = len(os.sched_getaffinity(0))
+        if is_cnn:
+            line["cpu_baseline"] = cnn_port_sample(spec, threads, seconds_cap=20.0)
+        else:
+            it = cpu_port_iteration(spec, 1, threads)
+            line["cpu_baseline"] = {k: it[k] for k in ("value", "unit", "cores", "kind", "sample")}
     if rank == 0:
         print(json.dumps(line), flush=True)
     rt.close()
@@ -523,6 +694,28 @@ def main() -> None:
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "native":
         args.warmup = 3
+    if args.impl == "native" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: relaunch under torchrun (the driver's own launch sets WORLD_SIZE)
+        import socket
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            sys.stderr.write(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) are visible\n")
+            sys.exit(2)
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        os.execv(sys.executable, [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                                  f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+                                  f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:])
+    if args.impl == "native" and int(os.environ.get("WORLD_SIZE", "1")) != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE')}\n")
+        sys.exit(2)
+    # communicator set-up lines (rank count, NVLS / P2P transports) on stderr
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     if args.impl == "reference":
         run_reference(args)
     else:

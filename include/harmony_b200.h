@@ -138,7 +138,12 @@ typedef struct {
   int32_t n_layer;    /* R: chain layers (embedding fused into 0, head into R-1) */
   int32_t d_model, n_head, seq_len, vocab, vocab_padded;
   int32_t causal;     /* 1 = GPT, 0 = BERT-style full attention             */
-  int32_t math_mode;  /* 0 = bf16 operands / fp32 accumulate               */
+  int32_t math_mode;  /* 0 = bf16 tensor-core operands, fp32 accumulate (throughput
+                       *     mode; tolerance stated separately);
+                       * 1 = fp32 operands (parity mode): every activation kept in
+                       *     fp32, GEMMs as three-plane bf16 split products on the
+                       *     same tcgen05 kernel (fp32-level accuracy), fp32 SIMT
+                       *     attention / LayerNorm forward / cross-entropy       */
   double lr, beta1, beta2, eps; /* double: 1-beta computed exactly as torch does */
 } hm_model;
 
@@ -209,6 +214,12 @@ int hm_runtime_debug_read(const hm_runtime *rt, int32_t which, int64_t offset, i
 int hm_nccl_unique_id(const char *nccl_path, uint8_t *out);
 int hm_runtime_init_comm(hm_runtime *rt, const char *nccl_path, const uint8_t *id, int32_t nranks,
                          int32_t rank);
+/* Harmony-DP with several processes on ONE GPU (tests; NCCL cannot put two
+ * ranks on one device): the per-pack gradient sum runs over CUDA IPC instead
+ * of NCCL -- every rank sums all ranks' gradient buffers in rank order (the
+ * same bits everywhere), ordered by device-side counters.  Call before
+ * load_plan; after it, every rank exports / imports its IPC blob as for PP. */
+int hm_runtime_init_ipc_reduce(hm_runtime *rt, int32_t nranks, int32_t rank);
 /* Harmony-PP across processes (one per GPU): W, K and stash arenas live in
  * one POSIX shared-memory segment registered as pinned memory in every rank
  * (rank 0 creates it, then the others attach).  Call before load_plan. */
@@ -223,6 +234,9 @@ int hm_runtime_ipc_import(hm_runtime *rt, const uint8_t *buf, int32_t len);
 /* Optimizer step counter (Adam bias correction); checkpoint / resume of the
  * host arenas restores it together with W and K. */
 int hm_runtime_get_step(const hm_runtime *rt);
+/* NUMA node the W / K host arenas were placed on (the GPU's, from sysfs;
+ * -1 = unknown, default policy). */
+int hm_runtime_numa_node(const hm_runtime *rt);
 int hm_runtime_set_step(hm_runtime *rt, int32_t step);
 /* W swap payload, before hm_runtime_load_plan: 0 = fp32 (the reference's
  * ledger), 1 = bf16 planes (SURVEY 8f4b fast mode: the host W arena holds each
@@ -353,6 +367,30 @@ int hm_k_cross_entropy(const float *logits, const int32_t *labels, int64_t rows,
 /* db[n] += sum_r dy[r, n] (dy bf16 if is_bf16 else fp32, row pitch ld). */
 int hm_k_bias_grad(const void *dy, int32_t is_bf16, float *db, int64_t rows, int32_t n, int64_t ld,
                    void *stream);
+
+/* ---- fp32-operand parity mode (math_mode 1; kernels/precise.cu) ----------- */
+/* C = A . B^T with fp32 operands: each split into three bf16 planes
+ * (x = x0 + x1 + x2) in scratch_a / scratch_b (>= 3 x the operand's
+ * elements, rounded up to 8, each), the six plane products with i + j <= 2
+ * summed in fp32 by the tcgen05 GEMM.  Arguments as hm_k_gemm (batch 1);
+ * the bf16 epilogues write fp32; RESID / GELU / DGELU go through acc
+ * (>= m x n fp32 elements) and an elementwise pass (exact tanh GELU). */
+int hm_k_gemm_precise(const float *a, const float *b, void *d, int64_t m, int64_t n, int64_t k,
+                      int64_t lda, int64_t ldb, int64_t ldd, int32_t a_major, int32_t b_major,
+                      int32_t epilogue, const float *bias, void *aux, int64_t ld_aux, void *scratch_a,
+                      int64_t scratch_a_elems, void *scratch_b, int64_t scratch_b_elems, float *acc,
+                      int64_t acc_elems, void *stream);
+/* fp32 attention (layouts as hm_k_attn_fwd; lse is the natural log here). */
+int hm_k_attn_fwd_f32(const float *qkv, float *out, float *lse, int32_t batch, int32_t seq, int32_t heads,
+                      int32_t head_dim, int32_t causal, void *stream);
+int hm_k_attn_bwd_f32(const float *qkv, const float *out, const float *dout, const float *lse, float *dvec,
+                      float *dqkv, int32_t batch, int32_t seq, int32_t heads, int32_t head_dim,
+                      int32_t causal, void *stream);
+/* LayerNorm forward with fp32 output; cross-entropy with fp32 dlogits. */
+int hm_k_layernorm_fwd_f32(const float *x, const float *g, const float *b, float *y, float *mean,
+                           float *rstd, int64_t rows, int32_t d, void *stream);
+int hm_k_cross_entropy_f32(const float *logits, const int32_t *labels, int64_t rows, int64_t ld,
+                           int32_t vocab, float *dlogits, double *loss_sum, float scale, void *stream);
 
 #ifdef __cplusplus
 }

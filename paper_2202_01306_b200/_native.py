@@ -121,6 +121,16 @@ def lib() -> C.CDLL:
         "hm_runtime_share_arenas": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int32, C.c_int64]),
         "hm_runtime_ipc_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
         "hm_runtime_ipc_import": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
+        "hm_runtime_init_ipc_reduce": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),
+        "hm_runtime_numa_node": (C.c_int, [C.c_void_p]),
+        "hm_k_gemm_precise": (C.c_int, [C.c_void_p] * 3 + [C.c_int64] * 6 + [C.c_int32] * 3
+                              + [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                 C.c_void_p, C.c_int64, C.c_void_p]),
+        "hm_k_attn_fwd_f32": (C.c_int, [C.c_void_p] * 3 + [C.c_int32] * 5 + [C.c_void_p]),
+        "hm_k_attn_bwd_f32": (C.c_int, [C.c_void_p] * 6 + [C.c_int32] * 5 + [C.c_void_p]),
+        "hm_k_layernorm_fwd_f32": (C.c_int, [C.c_void_p] * 6 + [C.c_int64, C.c_int32, C.c_void_p]),
+        "hm_k_cross_entropy_f32": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int32,
+                                             C.c_void_p, C.c_void_p, C.c_float, C.c_void_p]),
         "hm_runtime_set_profiling": (C.c_int, [C.c_void_p, C.c_int32]),
         "hm_runtime_kernel_stats": (C.c_int, [C.c_void_p, P(C.c_double), C.c_int32]),
         "hm_runtime_kernel_launches": (C.c_int, [C.c_void_p, P(C.c_double), C.c_int32]),

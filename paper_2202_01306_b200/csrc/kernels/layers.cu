@@ -1071,6 +1071,46 @@ __global__ void bias_grad2_kernel(const T *__restrict__ dy, float *__restrict__ 
   atomicAdd(db + col + 1, a1);
 }
 
+// ---- gradient sum over ranks (IPC test backend of the Harmony-DP all-reduce) ---------
+struct RankSrcs {
+  const float *p[8];
+};
+__global__ void sum_ranks_kernel(RankSrcs src, int n, float *__restrict__ out, int64_t count) {
+  pdl_wait();
+  const int64_t n4 = count / 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 acc = reinterpret_cast<const float4 *>(src.p[0])[i];
+    for (int r = 1; r < n; ++r) {
+      const float4 v = reinterpret_cast<const float4 *>(src.p[r])[i];
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    reinterpret_cast<float4 *>(out)[i] = acc;
+  }
+  for (int64_t i = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float acc = src.p[0][i];
+    for (int r = 1; r < n; ++r) acc += src.p[r][i];
+    out[i] = acc;
+  }
+}
+
+int sum_ranks(const float *const *src, int n, float *out, int64_t count, cudaStream_t s) {
+  if (n < 1 || n > 8) return fail(HM_ERR_VALIDATION, "sum_ranks: 1..8 sources");
+  RankSrcs rs{};
+  for (int r = 0; r < n; ++r) {
+    if ((uintptr_t)src[r] & 15) return fail(HM_ERR_VALIDATION, "sum_ranks: sources must be 16-B aligned");
+    rs.p[r] = src[r];
+  }
+  ProfScope ps(KC_MISC, s, 0, 4.0 * (n + 1) * count);
+  const unsigned grid = (unsigned)std::min<int64_t>((count / 4 + 255) / 256 + 1, (int64_t)sm_count() * 8);
+  HM_CUDA(launch_pdl(sum_ranks_kernel, dim3(grid), dim3(256), 0, s, rs, n, out, count));
+  count_launch();
+  return HM_OK;
+}
+
 int bias_grad(const void *dy, int is_bf16, float *db, int64_t rows, int n, int64_t ld, cudaStream_t s) {
   if (n % 2) return fail(HM_ERR_VALIDATION, "bias_grad: n must be even");
   ProfScope ps(KC_MISC, s, 0, (is_bf16 ? 2.0 : 4.0) * rows * n);

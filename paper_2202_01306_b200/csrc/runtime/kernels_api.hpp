@@ -34,7 +34,24 @@ int ln_bwd(const float *dy, const float *x, const float *mean, const float *rstd
 int cross_entropy(const float *logits, const int32_t *labels, int64_t rows, int64_t ldl, int V, void *dlogits,
                   double *loss_sum, float scale, cudaStream_t s);
 int bias_grad(const void *dy, int is_bf16, float *db, int64_t rows, int n, int64_t ld, cudaStream_t s);
+// out[i] = src[0][i] + src[1][i] + ... (n <= 8 sources, summed in that order)
+int sum_ranks(const float *const *src, int n, float *out, int64_t count, cudaStream_t s);
 }  // namespace layers
+// fp32-operand parity mode (kernels/precise.cu): three-plane bf16 split GEMMs,
+// fp32 SIMT attention / LayerNorm forward / cross-entropy
+namespace prec {
+int split3(const float *x, void *planes, int64_t n, int64_t plane, cudaStream_t s);
+int gemm(const float *A, const float *B, void *D, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb,
+         int64_t ldd, int a_mn, int b_mn, int epi, const float *bias, void *aux, int64_t ld_aux, cudaStream_t s,
+         void *sa, int64_t sa_elems, void *sb, int64_t sb_elems, float *c32, int64_t c32_elems);
+int ln_fwd(const float *x, const float *g, const float *b, float *y, float *mean, float *rstd, int64_t rows, int d,
+           cudaStream_t s);
+int cross_entropy(const float *logits, const int32_t *labels, int64_t rows, int64_t ldl, int V, float *dlogits,
+                  double *loss_sum, float scale, cudaStream_t s);
+int attn_forward(const float *qkv, float *o, float *lse, int B, int S, int H, int DH, int causal, cudaStream_t s);
+int attn_backward(const float *qkv, const float *o, const float *dout, const float *lse, float *dvec, float *dqkv,
+                  int B, int S, int H, int DH, int causal, cudaStream_t s);
+}  // namespace prec
 namespace gemm {
 int run_conv(int mode, const void *act, const void *wt, void *out, int n, int h, int w, int cin, int cout, int epi,
              const float *bias, const void *aux, cudaStream_t stream);

@@ -20,6 +20,7 @@
 #include <cuda_bf16.h>
 #include <fcntl.h>
 #include <sys/mman.h>
+#include <sys/syscall.h>
 #include <unistd.h>
 
 #include <algorithm>
@@ -200,10 +201,21 @@ struct hm_runtime {
   cudaStream_t s_compute = nullptr, s_h2d = nullptr, s_d2h = nullptr, s_update = nullptr, s_p2p_in = nullptr,
                s_p2p_out = nullptr;
   float *w_host = nullptr, *k_host = nullptr;
+  // W / K arenas: anonymous mappings bound (preferred) to the GPU's NUMA node,
+  // then pinned with cudaHostRegister (NUMA-local host state)
+  int64_t w_map_bytes = 0, k_map_bytes = 0;
+  int numa_node = -1;
   // bf16 swap payloads (non-reference ledger): the host W arena
   // holds each layer as [hi plane | lo plane] (2 + 2 bytes per parameter, see
   // layers::w_join); forward tasks move hi planes plus the fp32-read prefix
   bool w_planar = false;
+  // fp32-operand parity mode (hm_model.math_mode = 1, kernels/precise.cu):
+  // activations fp32, GEMMs as three-plane bf16 split products; scratch for
+  // the planes of the largest A / B operand and one M x N accumulator
+  bool precise = false;
+  void *psa = nullptr, *psb = nullptr;
+  float *pc32 = nullptr;
+  int64_t psa_n = 0, psb_n = 0, pc32_n = 0;
   uint8_t *stash_host = nullptr;
   int64_t stash_host_bytes = 0;
   // plan
@@ -249,6 +261,14 @@ struct hm_runtime {
   int nranks = 1;
   cudaStream_t s_comm = nullptr;
   std::vector<cudaEvent_t> ar_events;
+  // Harmony-DP gradient sum over CUDA IPC (several processes on one GPU, where
+  // NCCL cannot run): each rank sums every rank's pack gradient, read through
+  // the peers' pools, in rank order (identical bits on every rank); ordered by
+  // device-side counters.  The multi-GPU path is NCCL.
+  bool ipc_reduce = false;
+  float *ar_tmp = nullptr;
+  std::map<int, int64_t> dw_off;                   // my U task -> pool offset of its gradient (dW slot)
+  std::vector<std::map<int, int64_t>> peer_dw_off;  // per peer
   // Harmony-PP across processes
   bool p2p_mode = false;
   bool shared_arena = false, shared_owner = false;
@@ -334,17 +354,18 @@ static ParamLayout make_layout(const hm_runtime &rt, int L) {
   return p;
 }
 
-// per-sample bytes of each stored tensor, in store order
+// per-sample bytes of each stored tensor, in store order (the GEMM operands
+// are bf16, or fp32 in the parity mode)
 static std::vector<int64_t> act_sizes(const hm_runtime &rt, bool head) {
-  const int64_t S = rt.S, d = rt.m.d_model, H = rt.H;
+  const int64_t S = rt.S, d = rt.m.d_model, H = rt.H, ob = rt.precise ? 4 : 2;
   std::vector<int64_t> v = {S * d * 4, S * 4, S * 4, S * H * 4, S * d * 4, S * 4, S * 4,        // x mean1 rstd1 lse h1 mean2 rstd2
-                            S * d * 2, S * 3 * d * 2, S * d * 2, S * d * 2, S * 4 * d * 2, S * 4 * d * 2};  // ln1 qkv o ln2 hpre a
+                            S * d * ob, S * 3 * d * ob, S * d * ob, S * d * ob, S * 4 * d * ob, S * 4 * d * ob};  // ln1 qkv o ln2 hpre a
   if (head) {
     v.push_back(S * d * 4);           // yl
     v.push_back(S * 4);               // meanf
     v.push_back(S * 4);               // rstdf
-    v.push_back(S * d * 2);           // lnf
-    v.push_back(S * (int64_t)rt.Vp * 2);  // dlog
+    v.push_back(S * d * ob);          // lnf
+    v.push_back(S * (int64_t)rt.Vp * ob);  // dlog
   }
   return v;
 }
@@ -656,21 +677,45 @@ static LayerW layer_weights(hm_runtime &rt, const TaskRt &tr, int lo, int L, int
   return lw;
 }
 
+// GEMM on the compute stream: the bf16 tcgen05 kernel, or in the parity mode
+// the three-plane split product over fp32 operands (same arguments)
+static int G(hm_runtime &rt, const void *A, const void *B, void *D, int64_t M, int64_t N, int64_t K, int64_t lda,
+             int64_t ldb, int64_t ldd, int a_mn, int b_mn, int epi, const float *bias = nullptr, void *aux = nullptr,
+             int64_t ld_aux = 0) {
+  if (rt.precise)
+    return prec::gemm(static_cast<const float *>(A), static_cast<const float *>(B), D, M, N, K, lda, ldb, ldd, a_mn,
+                      b_mn, epi, bias, aux, ld_aux, rt.s_compute, rt.psa, rt.psa_n, rt.psb, rt.psb_n, rt.pc32,
+                      rt.pc32_n);
+  return gemm::run(A, B, D, M, N, K, lda, ldb, ldd, a_mn, b_mn, epi, bias, aux, ld_aux, rt.s_compute, 0);
+}
+// a GEMM weight operand: the bf16 shadow, or the fp32 master in the parity mode
+static const void *wop(const hm_runtime &rt, const LayerW &W, int64_t off) {
+  return rt.precise ? static_cast<const void *>(W.w + off) : static_cast<const void *>(W.wsh + off);
+}
+static int ln_fwd_any(hm_runtime &rt, const float *x, const float *g, const float *b, void *y, float *mean,
+                      float *rstd, int64_t rows, int d) {
+  if (rt.precise) return prec::ln_fwd(x, g, b, static_cast<float *>(y), mean, rstd, rows, d, rt.s_compute);
+  return layers::ln_fwd(x, g, b, y, mean, rstd, rows, d, rt.s_compute);
+}
+
 static int block_fwd(hm_runtime &rt, const Acts &A, const float *x, float *y, int u, const LayerW &W) {
   const int64_t M = (int64_t)u * rt.S, d = rt.m.d_model;
   cudaStream_t s = rt.s_compute;
   const ParamLayout &P = *W.p;
-  HM_TRY(layers::ln_fwd(x, W.w + P.ln1_g, W.w + P.ln1_b, A.ln1, A.mean1, A.rstd1, M, (int)d, s));
-  HM_TRY(gemm::run(A.ln1, W.wsh + P.w_qkv, A.qkv, M, 3 * d, d, d, d, 3 * d, 0, 0, HM_EPI_STORE_BF16, W.w + P.b_qkv,
-                   nullptr, 0, s, 0));
-  HM_TRY(attn::forward(A.qkv, A.o, A.lse, u, rt.S, rt.H, rt.DH, rt.m.causal, s));
-  HM_TRY(gemm::run(A.o, W.wsh + P.w_proj, A.h1, M, d, d, d, d, d, 0, 0, HM_EPI_RESID_F32, W.w + P.b_proj,
-                   const_cast<float *>(x), d, s, 0));
-  HM_TRY(layers::ln_fwd(A.h1, W.w + P.ln2_g, W.w + P.ln2_b, A.ln2, A.mean2, A.rstd2, M, (int)d, s));
-  HM_TRY(gemm::run(A.ln2, W.wsh + P.w_fc1, A.a, M, 4 * d, d, d, d, 4 * d, 0, 0, HM_EPI_GELU_BF16, W.w + P.b_fc1,
-                   A.hpre, 4 * d, s, 0));
-  HM_TRY(gemm::run(A.a, W.wsh + P.w_fc2, y, M, d, 4 * d, 4 * d, 4 * d, d, 0, 0, HM_EPI_RESID_F32, W.w + P.b_fc2,
-                   A.h1, d, s, 0));
+  HM_TRY(ln_fwd_any(rt, x, W.w + P.ln1_g, W.w + P.ln1_b, A.ln1, A.mean1, A.rstd1, M, (int)d));
+  HM_TRY(G(rt, A.ln1, wop(rt, W, P.w_qkv), A.qkv, M, 3 * d, d, d, d, 3 * d, 0, 0, HM_EPI_STORE_BF16, W.w + P.b_qkv));
+  if (rt.precise)
+    HM_TRY(prec::attn_forward(reinterpret_cast<const float *>(A.qkv), reinterpret_cast<float *>(A.o), A.lse, u, rt.S,
+                              rt.H, rt.DH, rt.m.causal, s));
+  else
+    HM_TRY(attn::forward(A.qkv, A.o, A.lse, u, rt.S, rt.H, rt.DH, rt.m.causal, s));
+  HM_TRY(G(rt, A.o, wop(rt, W, P.w_proj), A.h1, M, d, d, d, d, d, 0, 0, HM_EPI_RESID_F32, W.w + P.b_proj,
+           const_cast<float *>(x), d));
+  HM_TRY(ln_fwd_any(rt, A.h1, W.w + P.ln2_g, W.w + P.ln2_b, A.ln2, A.mean2, A.rstd2, M, (int)d));
+  HM_TRY(G(rt, A.ln2, wop(rt, W, P.w_fc1), A.a, M, 4 * d, d, d, d, 4 * d, 0, 0, HM_EPI_GELU_BF16, W.w + P.b_fc1,
+           A.hpre, 4 * d));
+  HM_TRY(G(rt, A.a, wop(rt, W, P.w_fc2), y, M, d, 4 * d, 4 * d, 4 * d, d, 0, 0, HM_EPI_RESID_F32, W.w + P.b_fc2, A.h1,
+           d));
   return HM_OK;
 }
 
@@ -679,13 +724,14 @@ static int head_fwd(hm_runtime &rt, const Acts &A, int u, int64_t s0, const Laye
   const int64_t M = (int64_t)u * rt.S, d = rt.m.d_model;
   cudaStream_t s = rt.s_compute;
   const ParamLayout &P = *W.p;
-  HM_TRY(layers::ln_fwd(A.yl, W.w + P.lnf_g, W.w + P.lnf_b, A.lnf, A.meanf, A.rstdf, M, (int)d, s));
-  HM_TRY(gemm::run(A.lnf, W.wsh + P.w_head, rt.T.logits, M, rt.Vp, d, d, d, rt.Vp, 0, 0, HM_EPI_STORE_F32, nullptr,
-                   nullptr, 0, s, 0));
-  HM_TRY(layers::cross_entropy(rt.T.logits, rt.labels + s0 * rt.S, M, rt.Vp, rt.V, A.dlog,
-                               rt.count_loss ? rt.loss_cur : rt.loss_sink,
-                               (float)(1.0 / (double)rt.global_tokens), s));
-  return HM_OK;
+  HM_TRY(ln_fwd_any(rt, A.yl, W.w + P.lnf_g, W.w + P.lnf_b, A.lnf, A.meanf, A.rstdf, M, (int)d));
+  HM_TRY(G(rt, A.lnf, wop(rt, W, P.w_head), rt.T.logits, M, rt.Vp, d, d, d, rt.Vp, 0, 0, HM_EPI_STORE_F32));
+  double *loss = rt.count_loss ? rt.loss_cur : rt.loss_sink;
+  const float scale = (float)(1.0 / (double)rt.global_tokens);
+  if (rt.precise)
+    return prec::cross_entropy(rt.T.logits, rt.labels + s0 * rt.S, M, rt.Vp, rt.V, reinterpret_cast<float *>(A.dlog),
+                               loss, scale, s);
+  return layers::cross_entropy(rt.T.logits, rt.labels + s0 * rt.S, M, rt.Vp, rt.V, A.dlog, loss, scale, s);
 }
 
 static int head_bwd(hm_runtime &rt, const Acts &A, int u, const LayerW &W) {
@@ -693,10 +739,8 @@ static int head_bwd(hm_runtime &rt, const Acts &A, int u, const LayerW &W) {
   cudaStream_t s = rt.s_compute;
   const ParamLayout &P = *W.p;
   Scratch &T = rt.T;
-  HM_TRY(gemm::run(A.dlog, W.wsh + P.w_head, T.dln, M, d, Vp, Vp, d, d, 0, 1, HM_EPI_STORE_F32, nullptr, nullptr, 0,
-                   s, 0));
-  HM_TRY(gemm::run(A.dlog, A.lnf, W.dw + P.w_head, Vp, d, M, Vp, d, d, 1, 1, HM_EPI_ACC_F32, nullptr, nullptr, 0, s,
-                   0));
+  HM_TRY(G(rt, A.dlog, wop(rt, W, P.w_head), T.dln, M, d, Vp, Vp, d, d, 0, 1, HM_EPI_STORE_F32));
+  HM_TRY(G(rt, A.dlog, A.lnf, W.dw + P.w_head, Vp, d, M, Vp, d, d, 1, 1, HM_EPI_ACC_F32));
   HM_TRY(layers::ln_bwd(T.dln, A.yl, A.meanf, A.rstdf, W.w + P.lnf_g, nullptr, T.dyh, nullptr, W.dw + P.lnf_g,
                         W.dw + P.lnf_b, M, (int)d, s));
   return HM_OK;
@@ -708,29 +752,34 @@ static int block_bwd(hm_runtime &rt, const Acts &A, const float *x, const float 
   cudaStream_t s = rt.s_compute;
   const ParamLayout &P = *W.p;
   Scratch &T = rt.T;
-  HM_TRY(layers::cast_f32_bf16(dy, T.dy_bf, M * d, s));
+  const int opbf = rt.precise ? 0 : 1;  // the dgrad outputs feeding bias gradients are bf16 operands
+  const void *dyop = dy;
+  if (!rt.precise) {
+    HM_TRY(layers::cast_f32_bf16(dy, T.dy_bf, M * d, s));
+    dyop = T.dy_bf;
+  }
   HM_TRY(layers::bias_grad(dy, 0, W.dw + P.b_fc2, M, (int)d, d, s));
-  HM_TRY(gemm::run(T.dy_bf, A.a, W.dw + P.w_fc2, d, 4 * d, M, d, 4 * d, 4 * d, 1, 1, HM_EPI_ACC_F32, nullptr,
-                   nullptr, 0, s, 0));
-  HM_TRY(gemm::run(T.dy_bf, W.wsh + P.w_fc2, T.dh, M, 4 * d, d, d, 4 * d, 4 * d, 0, 1, HM_EPI_DGELU_BF16, nullptr,
-                   A.hpre, 4 * d, s, 0));
-  HM_TRY(layers::bias_grad(T.dh, 1, W.dw + P.b_fc1, M, (int)(4 * d), 4 * d, s));
-  HM_TRY(gemm::run(T.dh, A.ln2, W.dw + P.w_fc1, 4 * d, d, M, 4 * d, d, d, 1, 1, HM_EPI_ACC_F32, nullptr, nullptr, 0,
-                   s, 0));
-  HM_TRY(gemm::run(T.dh, W.wsh + P.w_fc1, T.dln, M, d, 4 * d, 4 * d, d, d, 0, 1, HM_EPI_STORE_F32, nullptr, nullptr,
-                   0, s, 0));
-  HM_TRY(layers::ln_bwd(T.dln, A.h1, A.mean2, A.rstd2, W.w + P.ln2_g, dy, T.dh1, T.dh1_bf, W.dw + P.ln2_g,
-                        W.dw + P.ln2_b, M, (int)d, s));
+  HM_TRY(G(rt, dyop, A.a, W.dw + P.w_fc2, d, 4 * d, M, d, 4 * d, 4 * d, 1, 1, HM_EPI_ACC_F32));
+  HM_TRY(G(rt, dyop, wop(rt, W, P.w_fc2), T.dh, M, 4 * d, d, d, 4 * d, 4 * d, 0, 1, HM_EPI_DGELU_BF16, nullptr,
+           A.hpre, 4 * d));
+  HM_TRY(layers::bias_grad(T.dh, opbf, W.dw + P.b_fc1, M, (int)(4 * d), 4 * d, s));
+  HM_TRY(G(rt, T.dh, A.ln2, W.dw + P.w_fc1, 4 * d, d, M, 4 * d, d, d, 1, 1, HM_EPI_ACC_F32));
+  HM_TRY(G(rt, T.dh, wop(rt, W, P.w_fc1), T.dln, M, d, 4 * d, 4 * d, d, d, 0, 1, HM_EPI_STORE_F32));
+  HM_TRY(layers::ln_bwd(T.dln, A.h1, A.mean2, A.rstd2, W.w + P.ln2_g, dy, T.dh1, rt.precise ? nullptr : T.dh1_bf,
+                        W.dw + P.ln2_g, W.dw + P.ln2_b, M, (int)d, s));
   HM_TRY(layers::bias_grad(T.dh1, 0, W.dw + P.b_proj, M, (int)d, d, s));
-  HM_TRY(gemm::run(T.dh1_bf, A.o, W.dw + P.w_proj, d, d, M, d, d, d, 1, 1, HM_EPI_ACC_F32, nullptr, nullptr, 0, s, 0));
-  HM_TRY(gemm::run(T.dh1_bf, W.wsh + P.w_proj, T.dout, M, d, d, d, d, d, 0, 1, HM_EPI_STORE_BF16, nullptr, nullptr, 0,
-                   s, 0));
-  HM_TRY(attn::backward(A.qkv, A.o, T.dout, A.lse, T.dvec, T.dq, T.dqkv, u, rt.S, rt.H, rt.DH, rt.m.causal, s));
-  HM_TRY(layers::bias_grad(T.dqkv, 1, W.dw + P.b_qkv, M, (int)(3 * d), 3 * d, s));
-  HM_TRY(gemm::run(T.dqkv, A.ln1, W.dw + P.w_qkv, 3 * d, d, M, 3 * d, d, d, 1, 1, HM_EPI_ACC_F32, nullptr, nullptr, 0,
-                   s, 0));
-  HM_TRY(gemm::run(T.dqkv, W.wsh + P.w_qkv, T.dln, M, d, 3 * d, 3 * d, d, d, 0, 1, HM_EPI_STORE_F32, nullptr, nullptr,
-                   0, s, 0));
+  const void *dh1op = rt.precise ? static_cast<const void *>(T.dh1) : static_cast<const void *>(T.dh1_bf);
+  HM_TRY(G(rt, dh1op, A.o, W.dw + P.w_proj, d, d, M, d, d, d, 1, 1, HM_EPI_ACC_F32));
+  HM_TRY(G(rt, dh1op, wop(rt, W, P.w_proj), T.dout, M, d, d, d, d, d, 0, 1, HM_EPI_STORE_BF16));
+  if (rt.precise)
+    HM_TRY(prec::attn_backward(reinterpret_cast<const float *>(A.qkv), reinterpret_cast<const float *>(A.o),
+                               reinterpret_cast<const float *>(T.dout), A.lse, T.dvec,
+                               reinterpret_cast<float *>(T.dqkv), u, rt.S, rt.H, rt.DH, rt.m.causal, s));
+  else
+    HM_TRY(attn::backward(A.qkv, A.o, T.dout, A.lse, T.dvec, T.dq, T.dqkv, u, rt.S, rt.H, rt.DH, rt.m.causal, s));
+  HM_TRY(layers::bias_grad(T.dqkv, opbf, W.dw + P.b_qkv, M, (int)(3 * d), 3 * d, s));
+  HM_TRY(G(rt, T.dqkv, A.ln1, W.dw + P.w_qkv, 3 * d, d, M, 3 * d, d, d, 1, 1, HM_EPI_ACC_F32));
+  HM_TRY(G(rt, T.dqkv, wop(rt, W, P.w_qkv), T.dln, M, d, 3 * d, 3 * d, d, d, 0, 1, HM_EPI_STORE_F32));
   HM_TRY(layers::ln_bwd(T.dln, x, A.mean1, A.rstd1, W.w + P.ln1_g, T.dh1, dx, nullptr, W.dw + P.ln1_g,
                         W.dw + P.ln1_b, M, (int)d, s));
   return HM_OK;
@@ -846,6 +895,8 @@ static int run_member(hm_runtime &rt, int task, int g) {
                                 P.size, s));
         }
       }
+    } else if (rt.precise) {
+      // parity mode: the GEMMs split the fp32 master weights themselves
     } else if (rt.family == HM_FAMILY_GPT) {
       // bf16 operand copy of the pack's master weights, right after swap-in
       // (nearest, ties toward zero: the same bits as the bf16-payload hi planes)
@@ -1099,7 +1150,7 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
   rt.slots.stash_in.assign(NST, nullptr);
   for (int i = 0; i < NW; ++i) {
     req.push_back({(void **)&rt.slots.w[i], pmax * 4});
-    req.push_back({(void **)&rt.slots.wsh[i], pmax * 2});
+    req.push_back({(void **)&rt.slots.wsh[i], rt.precise ? 256 : pmax * 2});
     if (rt.w_planar) req.push_back({(void **)&rt.slots.wlo[i], std::max<int64_t>(f32max * 2, 256)});
   }
   for (int i = 0; i < NDW; ++i) req.push_back({(void **)&rt.slots.dw[i], pmax * 4});
@@ -1124,7 +1175,9 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
       out_bufs.push_back({ti, &tr.out_buf});
     }
   }
-  req.push_back({(void **)&rt.sig, (int64_t)plan->items.size() * 4 + 64});
+  // per-item completion counters, then (ready, read) counters per task for the IPC gradient sum
+  req.push_back({(void **)&rt.sig, (int64_t)(plan->items.size() + 2 * plan->tasks.size()) * 4 + 64});
+  if (rt.ipc_reduce) req.push_back({(void **)&rt.ar_tmp, pmax * 4});
   req.push_back({(void **)&rt.loss_sink, 256});
   req.push_back({(void **)&rt.shared_store, shared_bytes});
   req.push_back({(void **)&rt.work_store, work_bytes});
@@ -1152,11 +1205,20 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
     for (auto &kv : rt.relay_g) req.push_back({(void **)&kv.second, (int64_t)minibatch * bnd(rt, kv.first + 1)});
     req.push_back({(void **)&rt.CT.dpool, u_max * cmax * 4});
   } else {
+  const int64_t ob = rt.precise ? 4 : 2;  // GEMM operand bytes
   req.push_back({(void **)&T.dy_bf, rows_u * d * 2});
-  req.push_back({(void **)&T.dh, rows_u * 4 * d * 2});
+  req.push_back({(void **)&T.dh, rows_u * 4 * d * ob});
   req.push_back({(void **)&T.dh1_bf, rows_u * d * 2});
-  req.push_back({(void **)&T.dout, rows_u * d * 2});
-  req.push_back({(void **)&T.dqkv, rows_u * 3 * d * 2});
+  req.push_back({(void **)&T.dout, rows_u * d * ob});
+  req.push_back({(void **)&T.dqkv, rows_u * 3 * d * ob});
+  if (rt.precise) {  // split planes of the largest A / B operand; the fused-epilogue accumulator
+    rt.psa_n = 3 * (std::max(rows_u * 4 * d, rows_u * (int64_t)rt.Vp) + 8);
+    rt.psb_n = 3 * (std::max({(int64_t)rt.Vp * d, 4 * d * d, rows_u * 4 * d}) + 8);
+    rt.pc32_n = rows_u * 4 * d;
+    req.push_back({(void **)&rt.psa, rt.psa_n * 2});
+    req.push_back({(void **)&rt.psb, rt.psb_n * 2});
+    req.push_back({(void **)&rt.pc32, rt.pc32_n * 4});
+  }
   req.push_back({(void **)&T.dln, rows_u * d * 4});
   req.push_back({(void **)&T.dh1, rows_u * d * 4});
   req.push_back({(void **)&T.dvec, rows_u * rt.H * 4});
@@ -1183,7 +1245,7 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
     int nw = NW, nk = NK;
     int64_t room = rt.alpha - total;
     const int64_t kslot = align_up(pmax * 8, 1024),
-                  wslot = align_up(pmax * 4, 1024) + align_up(pmax * 2, 1024) +
+                  wslot = align_up(pmax * 4, 1024) + align_up(rt.precise ? 256 : pmax * 2, 1024) +
                           (rt.w_planar ? align_up(std::max<int64_t>(f32max * 2, 256), 1024) : 0);
     while (nk < 4 && room >= kslot) { ++nk; room -= kslot; }
     while (nw < 4 && room >= wslot) { ++nw; room -= wslot; }
@@ -1233,6 +1295,7 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
 
   // ---- actions ----------------------------------------------------------------
   rt.actions.clear();
+  rt.dw_off.clear();
   for (auto &e : rt.ar_events) cudaEventDestroy(e);
   rt.ar_events.clear();
   for (auto &e : rt.ev_start) cudaEventDestroy(e);
@@ -1321,7 +1384,7 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
     TaskRt &tr = rt.trt[r.task];
     if (r.is_compute) {
       if (t.type == HM_TASK_U) {
-        if (rt.comm) {  // (a 1-rank communicator still runs the collective: the N=1 test of this path)
+        if (rt.comm || rt.ipc_reduce) {  // (a 1-rank communicator still runs the collective: the N=1 test of this path)
           // sum the pack's gradient over the data-parallel ranks on the comm
           // stream; overlaps the next backward task on the compute stream
           Action ar;
@@ -1332,6 +1395,7 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
           ar.waits.push_back({bt.members.back(), false});
           ar.dst = rt.slots.dw[bt.dw_slot];
           ar.count = tr.params;
+          rt.dw_off[r.task] = reinterpret_cast<uint8_t *>(ar.dst) - rt.pool;
           cudaEvent_t e;
           HM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
           rt.ar_events.push_back(e);
@@ -1485,6 +1549,88 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
   return HM_OK;
 }
 
+// Drop the loaded plan and everything derived from it (actions, events,
+// captured graphs, peer mappings); the device pool is kept for reuse.
+static void unload_plan(hm_runtime &rt) {
+  cudaDeviceSynchronize();
+  for (auto &g : rt.graph_exec)
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+  rt.actions.clear();
+  rt.trt.clear();
+  for (auto &e : rt.ar_events) cudaEventDestroy(e);
+  rt.ar_events.clear();
+  for (auto *v : {&rt.ev_start, &rt.ev_end, &rt.ev_tstart, &rt.ev_tend})
+    for (auto &e : *v)
+      if (e) {
+        cudaEventDestroy(e);
+        e = nullptr;
+      }
+  rt.ev_start.clear();
+  rt.ev_end.clear();
+  rt.ev_tstart.clear();
+  rt.ev_tend.clear();
+  rt.ev_live.clear();
+  for (size_t i = 0; i < rt.peer_pool.size(); ++i)
+    if (rt.peer_pool[i] && (int)i != rt.rank) cudaIpcCloseMemHandle(rt.peer_pool[i]);
+  rt.peer_pool.clear();
+  rt.peer_out_off.clear();
+  rt.peer_sig_off.clear();
+  rt.peer_dw_off.clear();
+  rt.ledger.clear();
+  rt.trace.clear();
+  rt.iterations = 0;
+  rt.plan = nullptr;
+}
+
+// Harmony-DP gradient sum of one pack over CUDA IPC (hm_runtime_init_ipc_reduce):
+//   publish "my gradient is complete" (ready counter of the U task), wait for
+//   every peer's, sum all ranks' gradients in rank order into ar_tmp (reads
+//   the peers' dW slots through their mapped pools), publish "done reading",
+//   wait until every peer has read mine, then overwrite my dW with the sum.
+//   Everything is enqueued on the comm stream with device-side waits.
+static int ipc_grad_sum(hm_runtime &rt, const Action &a) {
+  if (!memops().wait || !memops().write) return fail(HM_ERR_DEVICE, "stream memory operations unavailable");
+  if (rt.nranks > 8) return fail(HM_ERR_VALIDATION, "IPC gradient sum: at most 8 ranks");
+  const int64_t base = (int64_t)rt.plan->items.size() + 2 * (int64_t)a.task;
+  auto counter = [&](int rank, int64_t idx) -> CUdeviceptr {
+    return reinterpret_cast<CUdeviceptr>(rt.peer_pool[rank] + rt.peer_sig_off[rank]) + 4 * (CUdeviceptr)idx;
+  };
+  const float *src[8] = {nullptr};
+  for (int p = 0; p < rt.nranks; ++p) {
+    if (p >= (int)rt.peer_pool.size() || !rt.peer_pool[p])
+      return fail(HM_ERR_VALIDATION, "IPC gradient sum: rank " + std::to_string(p) + " not imported");
+    if (p == rt.rank) {
+      src[p] = static_cast<const float *>(a.dst);
+      continue;
+    }
+    auto it = rt.peer_dw_off[p].find(a.task);
+    if (it == rt.peer_dw_off[p].end()) return fail(HM_ERR_INTERNAL, "peer exported no gradient buffer for this pack");
+    src[p] = reinterpret_cast<const float *>(rt.peer_pool[p] + it->second);
+  }
+  const cuuint32_t step = (cuuint32_t)rt.step;
+  auto publish = [&](int64_t idx) -> int {
+    if (memops().write(a.stream, counter(rt.rank, idx), step, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+      return fail(HM_ERR_DEVICE, "cuStreamWriteValue32 failed");
+    return HM_OK;
+  };
+  auto await_all = [&](int64_t idx) -> int {
+    for (int p = 0; p < rt.nranks; ++p)
+      if (p != rt.rank && memops().wait(a.stream, counter(p, idx), step, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+        return fail(HM_ERR_DEVICE, "cuStreamWaitValue32 failed");
+    return HM_OK;
+  };
+  HM_TRY(publish(base));
+  HM_TRY(await_all(base));
+  HM_TRY(layers::sum_ranks(src, rt.nranks, rt.ar_tmp, a.count, a.stream));
+  HM_TRY(publish(base + 1));
+  HM_TRY(await_all(base + 1));
+  HM_CUDA(cudaMemcpyAsync(a.dst, rt.ar_tmp, a.count * 4, cudaMemcpyDeviceToDevice, a.stream));
+  return HM_OK;
+}
+
 static int join_streams(hm_runtime &rt) {
   cudaStream_t others[] = {rt.s_h2d, rt.s_d2h, rt.s_update, rt.s_comm};
   for (size_t i = 0; i < 4; ++i) {
@@ -1543,8 +1689,12 @@ static int enqueue_body(hm_runtime &rt, bool capture, bool pipelined, int64_t &h
         return fail(HM_ERR_DEVICE, "cuStreamWaitValue32 failed");
     }
     if (a.kind == 5) {
-      ncclResult_t nr = nccl().all_reduce(a.dst, a.dst, (size_t)a.count, ncclFloat32, ncclSum, rt.comm, a.stream);
-      if (nr != ncclSuccess) return fail(HM_ERR_DEVICE, std::string("ncclAllReduce: ") + nccl().error_string(nr));
+      if (rt.ipc_reduce) {
+        HM_TRY(ipc_grad_sum(rt, a));
+      } else {
+        ncclResult_t nr = nccl().all_reduce(a.dst, a.dst, (size_t)a.count, ncclFloat32, ncclSum, rt.comm, a.stream);
+        if (nr != ncclSuccess) return fail(HM_ERR_DEVICE, std::string("ncclAllReduce: ") + nccl().error_string(nr));
+      }
       HM_CUDA(cudaEventRecord(a.done, a.stream));
       coll += 2 * (rt.nranks - 1) * a.count * 4 / rt.nranks;
       continue;
@@ -1629,7 +1779,7 @@ static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *l
   HM_CUDA(cudaMemcpyAsync(rt.labels, labels, lb, is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, sc));
   int64_t h2d = 0, d2h = 0, coll = 0;
   const int gi = rt.profiling ? 1 : 0;
-  const bool use_graph = rt.use_graph && !rt.p2p_mode && rt.iterations >= 1;
+  const bool use_graph = rt.use_graph && !rt.p2p_mode && !rt.ipc_reduce && rt.iterations >= 1;
   if (use_graph) {
     if (!rt.graph_exec[gi]) {
       // record the iteration once (with or without per-kernel timing events)
@@ -1794,6 +1944,51 @@ static int run_steps(hm_runtime &rt, int n, const int32_t *tokens, const int32_t
 }  // namespace hm
 
 namespace hm {
+// NUMA node of the GPU's PCIe function (sysfs), -1 if unknown
+static int gpu_numa_node(int device) {
+  char bus[64] = {0};
+  if (cudaDeviceGetPCIBusId(bus, sizeof bus, device) != cudaSuccess) return -1;
+  std::string b(bus);
+  for (auto &c : b) c = (char)tolower(c);
+  std::vector<std::string> names = {b};
+  const size_t colon = b.find(':');
+  if (colon == 8) names.push_back(b.substr(4));  // 8-digit PCI domain -> sysfs' 4 digits
+  for (auto &n : names) {
+    FILE *f = fopen(("/sys/bus/pci/devices/" + n + "/numa_node").c_str(), "r");
+    if (!f) continue;
+    int node = -1;
+    if (fscanf(f, "%d", &node) != 1) node = -1;
+    fclose(f);
+    return node;
+  }
+  return -1;
+}
+
+// Pinned host arena of `bytes`: an anonymous mapping with a preferred-node
+// memory policy (pages are faulted in by the pinning, on that node), huge
+// pages advised, registered with CUDA.  Zero-filled.
+static void *numa_pinned_alloc(int64_t bytes, int node) {
+  void *p = mmap(nullptr, (size_t)bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  if (p == MAP_FAILED) return nullptr;
+  madvise(p, (size_t)bytes, MADV_HUGEPAGE);
+  if (node >= 0 && node < 1024) {
+    unsigned long mask[16] = {0};
+    mask[node / 64] = 1UL << (node % 64);
+    const int kMpolPreferred = 1;
+    syscall(SYS_mbind, p, (unsigned long)bytes, kMpolPreferred, mask, 1024UL, 0U);  // best effort
+  }
+  if (cudaHostRegister(p, (size_t)bytes, cudaHostRegisterPortable) != cudaSuccess) {
+    munmap(p, (size_t)bytes);
+    return nullptr;
+  }
+  return p;
+}
+static void numa_pinned_free(void *p, int64_t bytes) {
+  if (!p) return;
+  cudaHostUnregister(p);
+  munmap(p, (size_t)bytes);
+}
+
 // streams, events and the pinned W / K arenas (shared by both model families)
 static hm_runtime *finish_create(std::unique_ptr<hm_runtime> rt, int32_t *status) {
   auto bad = [&](int code, const std::string &msg) -> hm_runtime * {
@@ -1813,10 +2008,17 @@ static hm_runtime *finish_create(std::unique_ptr<hm_runtime> rt, int32_t *status
       cudaHostAlloc(&rt->loss_host, 64 * sizeof(double), cudaHostAllocDefault) != cudaSuccess)
     return bad(HM_ERR_DEVICE, "pinned alloc");
   cudaEventCreate(&rt->ev_first);
-  if (cudaHostAlloc(&rt->w_host, rt->total_params * 4, cudaHostAllocDefault) != cudaSuccess ||
-      cudaHostAlloc(&rt->k_host, rt->total_params * 8, cudaHostAllocDefault) != cudaSuccess)
+  rt->numa_node = gpu_numa_node(rt->device);
+  rt->w_map_bytes = align_up(std::max<int64_t>(rt->total_params * 4, 4096), 1 << 21);
+  rt->k_map_bytes = align_up(std::max<int64_t>(rt->total_params * 8, 4096), 1 << 21);
+  rt->w_host = static_cast<float *>(numa_pinned_alloc(rt->w_map_bytes, rt->numa_node));
+  rt->k_host = static_cast<float *>(numa_pinned_alloc(rt->k_map_bytes, rt->numa_node));  // zero: Adam state at step 0
+  if (!rt->w_host || !rt->k_host) {
+    numa_pinned_free(rt->w_host, rt->w_map_bytes);
+    numa_pinned_free(rt->k_host, rt->k_map_bytes);
+    rt->w_host = rt->k_host = nullptr;
     return bad(HM_ERR_DEVICE, "pinned host arena allocation failed (" + std::to_string(rt->total_params * 12) + " B)");
-  std::memset(rt->k_host, 0, rt->total_params * 8);
+  }
   if (status) *status = HM_OK;
   return rt.release();
 }
@@ -1839,6 +2041,8 @@ hm_runtime *hm_runtime_create(int32_t device, const hm_model *model, int64_t alp
   if (dh != 64 && dh != 128) return bad(HM_ERR_VALIDATION, "head_dim must be 64 or 128");
   if (model->seq_len % 64 || model->d_model % 64) return bad(HM_ERR_VALIDATION, "seq_len and d_model must be multiples of 64");
   if (model->vocab_padded % 8 || model->vocab_padded < model->vocab) return bad(HM_ERR_VALIDATION, "bad padded vocab");
+  if (model->math_mode != 0 && model->math_mode != 1)
+    return bad(HM_ERR_VALIDATION, "math_mode: 0 = bf16 operands, 1 = fp32 operands (parity mode)");
   if (cudaSetDevice(device) != cudaSuccess) return bad(HM_ERR_DEVICE, "cudaSetDevice failed");
   auto rt = std::make_unique<hm_runtime>();
   rt->device = device;
@@ -1850,6 +2054,7 @@ hm_runtime *hm_runtime_create(int32_t device, const hm_model *model, int64_t alp
   rt->DH = dh;
   rt->V = model->vocab;
   rt->Vp = model->vocab_padded;
+  rt->precise = model->math_mode == 1;
   rt->w_off.assign(rt->R + 1, 0);
   for (int L = 0; L < rt->R; ++L) {
     rt->lay.push_back(hm::make_layout(*rt, L));
@@ -1943,9 +2148,9 @@ int hm_runtime_layer_offsets(const hm_runtime *rt, int64_t *w_off, int32_t cap) 
 int hm_runtime_load_plan(hm_runtime *rt, hm_plan *plan, int32_t rank, int32_t minibatch) {
   if (!rt || !plan) return hm::fail(HM_ERR_VALIDATION, "null argument");
   if (cudaSetDevice(rt->device) != cudaSuccess) return hm::fail(HM_ERR_DEVICE, "cudaSetDevice");
-  int64_t global = 0;
-  for (auto &t : plan->p->tasks) (void)t;
+  if (minibatch < 1) return hm::fail(HM_ERR_VALIDATION, "minibatch must be >= 1");
   // global tokens = minibatch of the whole job: sum over ranks' F groups of task 0 of each rank
+  int64_t global = 0;
   std::map<int, int64_t> per_rank;
   for (auto &t : plan->p->tasks)
     if (t.type == HM_TASK_F && (t.lo == 0)) {
@@ -1954,8 +2159,16 @@ int hm_runtime_load_plan(hm_runtime *rt, hm_plan *plan, int32_t rank, int32_t mi
       per_rank[t.dev_id] += s;
     }
   for (auto &kv : per_rank) global += kv.second;
+  // The previous plan's device state does not survive a (re)load: any failure
+  // below leaves the runtime with NO plan (run calls then fail with "no plan
+  // loaded"), never with a half-built one that points at freed buffers.  Peer
+  // pool mappings are dropped too: the pool is reallocated, so every rank
+  // must export / import again after loading.
+  hm::unload_plan(*rt);
   rt->global_tokens = global * hm::labels_per_sample(*rt);
-  return hm::load_plan(*rt, plan->p, rank, minibatch);
+  const int rc = hm::load_plan(*rt, plan->p, rank, minibatch);
+  if (rc != HM_OK) hm::unload_plan(*rt);
+  return rc;
 }
 
 int hm_runtime_run_iteration(hm_runtime *rt, const int32_t *tokens, const int32_t *labels, int32_t is_device,
@@ -2021,6 +2234,17 @@ int hm_runtime_init_comm(hm_runtime *rt, const char *nccl_path, const uint8_t *i
   return HM_OK;
 }
 
+int hm_runtime_init_ipc_reduce(hm_runtime *rt, int32_t nranks, int32_t rank) {
+  if (!rt) return hm::fail(HM_ERR_VALIDATION, "null runtime");
+  if (rt->comm) return hm::fail(HM_ERR_VALIDATION, "an NCCL communicator is already attached");
+  if (nranks < 1 || nranks > 8 || rank < 0 || rank >= nranks)
+    return hm::fail(HM_ERR_VALIDATION, "IPC gradient sum: 1 <= nranks <= 8, 0 <= rank < nranks");
+  if (rt->plan) return hm::fail(HM_ERR_VALIDATION, "call before hm_runtime_load_plan");
+  rt->ipc_reduce = true;
+  rt->nranks = nranks;
+  return HM_OK;
+}
+
 int hm_runtime_share_arenas(hm_runtime *rt, const char *shm_name, int32_t create, int64_t stash_bytes) {
   if (!rt || !shm_name || !*shm_name) return hm::fail(HM_ERR_VALIDATION, "shared arena needs a name");
   if (rt->shared_arena) return hm::fail(HM_ERR_VALIDATION, "arenas already shared");
@@ -2042,8 +2266,9 @@ int hm_runtime_share_arenas(hm_runtime *rt, const char *shm_name, int32_t create
     munmap(p, total);
     return hm::fail(HM_ERR_DEVICE, "cudaHostRegister of the shared arena failed");
   }
-  if (rt->w_host) cudaFreeHost(rt->w_host);
-  if (rt->k_host) cudaFreeHost(rt->k_host);
+  hm::numa_pinned_free(rt->w_host, rt->w_map_bytes);
+  hm::numa_pinned_free(rt->k_host, rt->k_map_bytes);
+  rt->w_host = rt->k_host = nullptr;
   if (rt->stash_host) cudaFreeHost(rt->stash_host);
   uint8_t *base = static_cast<uint8_t *>(p);
   rt->w_host = reinterpret_cast<float *>(base);
@@ -2079,56 +2304,95 @@ int hm_runtime_ipc_export(hm_runtime *rt, uint8_t *buf, int32_t cap) {
     put(&task, 4);
     put(&kv.second, 8);
   }
+  const int32_t m = (int32_t)rt->dw_off.size();  // gradient buffers read by the IPC gradient sum
+  put(&m, 4);
+  for (auto &kv : rt->dw_off) {
+    const int32_t task = kv.first;
+    put(&task, 4);
+    put(&kv.second, 8);
+  }
   if ((int32_t)out.size() > cap) return hm::fail(HM_ERR_VALIDATION, "ipc buffer too small");
   std::memcpy(buf, out.data(), out.size());
   return (int)out.size();
 }
 
 int hm_runtime_ipc_import(hm_runtime *rt, const uint8_t *buf, int32_t len) {
-  if (!rt || !buf || len < 8) return hm::fail(HM_ERR_VALIDATION, "bad ipc blob");
+  if (!rt || !buf || len < 0) return hm::fail(HM_ERR_VALIDATION, "bad ipc blob");
+  if (!rt->plan) return hm::fail(HM_ERR_VALIDATION, "load a plan before importing peers");
   size_t o = 0;
-  auto get = [&](void *p, size_t n) {
+  bool ok = true;
+  auto get = [&](void *p, size_t n) {  // bounds-checked read of the blob
+    if (!ok || o + n > (size_t)len) {
+      ok = false;
+      return;
+    }
     std::memcpy(p, buf + o, n);
     o += n;
   };
-  uint32_t magic;
-  int32_t peer, n;
+  uint32_t magic = 0;
+  int32_t peer = -1, n = -1;
   cudaIpcMemHandle_t h;
-  int64_t sig_off;
+  int64_t sig_off = -1;
   get(&magic, 4);
-  if (magic != 0x484d3250) return hm::fail(HM_ERR_VALIDATION, "bad ipc blob magic");
+  if (!ok || magic != 0x484d3250) return hm::fail(HM_ERR_VALIDATION, "bad ipc blob magic");
   get(&peer, 4);
   get(&h, sizeof(h));
   get(&sig_off, 8);
   get(&n, 4);
+  if (!ok) return hm::fail(HM_ERR_VALIDATION, "truncated ipc blob header");
   if (peer < 0 || peer > 4096) return hm::fail(HM_ERR_VALIDATION, "bad peer rank");
-  if ((int)rt->peer_pool.size() <= peer) {
-    rt->peer_pool.resize(peer + 1, nullptr);
-    rt->peer_out_off.resize(peer + 1);
-    rt->peer_sig_off.resize(peer + 1, 0);
-  }
-  rt->peer_out_off[peer].clear();
+  if (n < 0 || (size_t)n * 12 + 4 > (size_t)len - o) return hm::fail(HM_ERR_VALIDATION, "ipc blob length disagrees with its entry count");
+  std::map<int, int64_t> offs, dwo;
   for (int i = 0; i < n; ++i) {
     int32_t task;
     int64_t off;
     get(&task, 4);
     get(&off, 8);
-    rt->peer_out_off[peer][task] = off;
+    if (!ok || off < 0) return hm::fail(HM_ERR_VALIDATION, "bad ipc blob entry");
+    offs[task] = off;
   }
-  rt->peer_sig_off[peer] = sig_off;
+  int32_t m = -1;
+  get(&m, 4);
+  if (!ok || m < 0 || (size_t)m * 12 != (size_t)len - o) return hm::fail(HM_ERR_VALIDATION, "ipc blob length disagrees with its gradient entry count");
+  for (int i = 0; i < m; ++i) {
+    int32_t task;
+    int64_t off;
+    get(&task, 4);
+    get(&off, 8);
+    if (!ok || off < 0) return hm::fail(HM_ERR_VALIDATION, "bad ipc blob gradient entry");
+    dwo[task] = off;
+  }
+  if (sig_off < 0) return hm::fail(HM_ERR_VALIDATION, "bad ipc blob signal offset");
+  if ((int)rt->peer_pool.size() <= peer) {
+    rt->peer_pool.resize(peer + 1, nullptr);
+    rt->peer_out_off.resize(peer + 1);
+    rt->peer_sig_off.resize(peer + 1, 0);
+    rt->peer_dw_off.resize(peer + 1);
+  }
+  rt->peer_dw_off[peer] = std::move(dwo);
   if (peer == rt->rank) {
+    rt->peer_out_off[peer] = std::move(offs);
+    rt->peer_sig_off[peer] = sig_off;
     rt->peer_pool[peer] = rt->pool;
     return HM_OK;
   }
   if (cudaSetDevice(rt->device) != cudaSuccess) return hm::fail(HM_ERR_DEVICE, "cudaSetDevice");
+  if (rt->peer_pool[peer]) {  // re-import: close the previous mapping first
+    cudaIpcCloseMemHandle(rt->peer_pool[peer]);
+    rt->peer_pool[peer] = nullptr;
+  }
   void *p = nullptr;
   if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
     return hm::fail(HM_ERR_DEVICE, "cudaIpcOpenMemHandle failed for rank " + std::to_string(peer));
+  rt->peer_out_off[peer] = std::move(offs);
+  rt->peer_sig_off[peer] = sig_off;
   rt->peer_pool[peer] = static_cast<uint8_t *>(p);
   return HM_OK;
 }
 
 int hm_runtime_get_step(const hm_runtime *rt) { return rt ? rt->step : -1; }
+
+int hm_runtime_numa_node(const hm_runtime *rt) { return rt ? rt->numa_node : -1; }
 
 int hm_runtime_set_w_payload(hm_runtime *rt, int32_t mode) {
   if (!rt) return hm::fail(HM_ERR_VALIDATION, "null runtime");
@@ -2136,6 +2400,8 @@ int hm_runtime_set_w_payload(hm_runtime *rt, int32_t mode) {
   if (rt->plan) return hm::fail(HM_ERR_VALIDATION, "set the W payload before loading a plan");
   if (mode == 1 && rt->family != HM_FAMILY_GPT)
     return hm::fail(HM_ERR_VALIDATION, "bf16 W payloads are implemented for the transformer family");
+  if (mode == 1 && rt->precise)
+    return hm::fail(HM_ERR_VALIDATION, "bf16 W payloads feed bf16 GEMM operands: not with math_mode 1 (fp32 operands)");
   rt->w_planar = mode == 1;
   return HM_OK;
 }
@@ -2201,8 +2467,8 @@ void hm_runtime_free(hm_runtime *rt) {
     munmap(rt->shm_ptr, rt->shm_bytes);
     if (rt->shared_owner) shm_unlink(rt->shm_name.c_str());
   } else {
-    if (rt->w_host) cudaFreeHost(rt->w_host);
-    if (rt->k_host) cudaFreeHost(rt->k_host);
+    hm::numa_pinned_free(rt->w_host, rt->w_map_bytes);
+    hm::numa_pinned_free(rt->k_host, rt->k_map_bytes);
     if (rt->stash_host) cudaFreeHost(rt->stash_host);
   }
   cudaStream_t ss[] = {rt->s_compute, rt->s_h2d, rt->s_d2h, rt->s_update, rt->s_p2p_in, rt->s_p2p_out, rt->s_comm};

@@ -32,18 +32,31 @@ class HarmonyRuntime:
     """Native runtime for one GPU: arenas, streams, kernels, plan executor."""
 
     def __init__(self, spec: GPTSpec | CNNSpec, *, alpha_bytes: int, device: int = 0, lr: float = 1e-4,
-                 betas: tuple[float, float] = (0.9, 0.999), eps: float = 1e-8, w_payload: str = "fp32") -> None:
+                 betas: tuple[float, float] = (0.9, 0.999), eps: float = 1e-8, w_payload: str = "fp32",
+                 math: str = "bf16") -> None:
         """``w_payload``: "fp32" swaps fp32 W exactly as the reference's ledger
         bills it; "bf16" is the SURVEY 8f4b fast mode (transformer family): the
         host W arena holds each layer as [bf16 hi plane | 16-bit lo plane], an
         exact split of the fp32 value, and forward tasks move only the hi plane
         plus the lo plane of the fp32-read prefix (LayerNorm, biases,
         embeddings).  Losses and weights are bit-identical to "fp32"; the
-        forward W rows of the ledger differ (flagged: not the reference's)."""
+        forward W rows of the ledger differ (flagged: not the reference's).
+
+        ``math``: "bf16" = bf16 tensor-core operands with fp32 accumulation
+        (the throughput mode); "fp32" = the parity mode (transformer family):
+        fp32 activations, GEMMs as three-plane bf16 split products on the same
+        tcgen05 kernel, fp32 attention (DESIGN.md section 6 states both
+        modes' tolerances).  The swap plan and ledger are the same."""
         if w_payload not in ("fp32", "bf16"):
             raise ValidationError("w_payload must be 'fp32' or 'bf16'")
+        if math not in ("bf16", "fp32"):
+            raise ValidationError("math must be 'bf16' or 'fp32'")
+        if math == "fp32" and (isinstance(spec, CNNSpec) or w_payload == "bf16"):
+            raise ValidationError("math='fp32' is implemented for the transformer family with fp32 W payloads")
         self.spec = spec
         self.w_payload = w_payload
+        self.math = math
+        self.hparams = (float(lr), float(betas[0]), float(betas[1]), float(eps))
         self.lib = NL.lib()
         self.is_cnn = isinstance(spec, CNNSpec)
         st = C.c_int32(0)
@@ -55,7 +68,8 @@ class HarmonyRuntime:
             h = self.lib.hm_runtime_create_cnn(device, C.byref(m), int(alpha_bytes), C.byref(st))
         else:
             m = NL.hm_model(spec.n_layer, spec.d_model, spec.n_head, spec.seq_len, spec.vocab,
-                            spec.vocab_padded, 1 if spec.causal else 0, 0, lr, betas[0], betas[1], eps)
+                            spec.vocab_padded, 1 if spec.causal else 0, 1 if math == "fp32" else 0,
+                            lr, betas[0], betas[1], eps)
             self._model = m
             h = self.lib.hm_runtime_create(device, C.byref(m), int(alpha_bytes), C.byref(st))
         if not h:
@@ -78,6 +92,8 @@ class HarmonyRuntime:
         self.graph: TaskGraph | None = None
         self.rank = 0
         self.samples = 0
+        self.device = device
+        self._checked: tuple | None = None  # (ptr, version) of the last range-checked CUDA inputs
 
     def _arena(self, kind: int, dtype) -> np.ndarray:
         nbytes = C.c_int64(0)
@@ -218,20 +234,31 @@ class HarmonyRuntime:
             self.k[:] = 0.0  # (hm_runtime_create zeroes K; kept for re-initialisation)
 
     # -- checkpoint / resume (the host arenas are the model state) ------
+    def _fingerprint(self) -> np.ndarray:
+        """Model identity stored with a checkpoint: the family's shape fields
+        (CNN: every layer's (type, cin, cout, h, w, skip) and the classes)."""
+        sp = self.spec
+        if self.is_cnn:
+            rows = [list(lay) + [sk] for lay, sk in zip(sp.layers, sp.skips)]
+            return np.array([1, sp.n_layer, sp.classes] + [v for r in rows for v in r], dtype=np.int64)
+        return np.array([0, sp.n_layer, sp.d_model, sp.n_head, sp.seq_len, sp.vocab, int(sp.causal)],
+                        dtype=np.int64)
+
     def save_checkpoint(self, path: str) -> None:
-        """W and K arenas + optimizer step, as one .npz (no device state: the
-        GPU only holds transient packs between iterations)."""
+        """W and K arenas + optimizer step and hyperparameters, as one .npz (no
+        device state: the GPU only holds transient packs between iterations).
+        W is stored in the canonical fp32 layout whatever the payload mode."""
         np.savez(path, w=self.weights(), k=self.k, step=np.int64(self.lib.hm_runtime_get_step(self.handle)),
-                 spec=np.array([self.spec.n_layer, self.spec.d_model, self.spec.n_head, self.spec.seq_len,
-                                self.spec.vocab], dtype=np.int64))
+                 spec=self._fingerprint(), hparams=np.array(self.hparams, dtype=np.float64))
         return None
 
     def load_checkpoint(self, path: str) -> None:
         z = np.load(path)
-        want = np.array([self.spec.n_layer, self.spec.d_model, self.spec.n_head, self.spec.seq_len,
-                         self.spec.vocab], dtype=np.int64)
-        if not np.array_equal(z["spec"], want) or z["w"].shape != self._w_arena.shape:
+        if not np.array_equal(z["spec"], self._fingerprint()) or z["w"].shape != (int(self.w_off[-1]),):
             raise ValidationError("checkpoint was written for a different model")
+        if "hparams" in z and not np.array_equal(z["hparams"], np.array(self.hparams, dtype=np.float64)):
+            raise ValidationError(f"checkpoint optimizer hyperparameters {tuple(z['hparams'])} differ from this "
+                                  f"runtime's {self.hparams} (resume would not be exact)")
         self.set_weights(z["w"])
         self.k[:] = z["k"]
         NL.check(self.lib.hm_runtime_set_step(self.handle, int(z["step"])))
@@ -282,6 +309,12 @@ class HarmonyRuntime:
         NL.check(NL.lib().hm_nccl_unique_id(cls.nccl_path(), buf))
         return bytes(buf)
 
+    def init_ipc_reduce(self, nranks: int, rank: int) -> None:
+        """Harmony-DP with several processes on ONE GPU (tests): the per-pack
+        gradient sum runs over CUDA IPC instead of NCCL.  Call before load();
+        after it, exchange ipc_export() blobs and ipc_import() every rank's."""
+        NL.check(self.lib.hm_runtime_init_ipc_reduce(self.handle, nranks, rank))
+
     def init_comm(self, unique_id: bytes, nranks: int, rank: int) -> None:
         """Join the job's NCCL communicator (call before load())."""
         buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
@@ -298,9 +331,17 @@ class HarmonyRuntime:
             samples = gpu_shares(graph.minibatch, machine.gpu_count)[rank]
         else:
             samples = graph.minibatch
-        NL.check(self.lib.hm_runtime_load_plan(self.handle, plan.handle, rank, samples))
+        # the native side drops the previous plan first and keeps none on failure
+        old, self.plan, self.graph = self.plan, None, None
+        rc = self.lib.hm_runtime_load_plan(self.handle, plan.handle, rank, samples)
+        if old is not None:
+            old.close()
+        if rc != 0:
+            plan.close()
+            NL.check(rc)
         self.plan, self.graph, self.rank, self.samples = plan, graph, rank, samples
         self.machine = machine
+        self._checked = None
 
     def sample_range(self) -> tuple[int, int]:
         """Global sample indices this rank processes."""
@@ -309,6 +350,54 @@ class HarmonyRuntime:
             lo = sum(sh[:self.rank])
             return lo, lo + sh[self.rank]
         return 0, self.samples
+
+    def _gpt_inputs(self, tokens, labels):
+        """Validate one minibatch of token ids / labels (shared by step and
+        run_steps): both [samples, seq_len], ids in [0, vocab).  Host arrays
+        are cast to contiguous int32; CUDA tensors must already be contiguous
+        int32 on this runtime's device (an int64 tensor would be read as
+        interleaved int32 halves).  Returns (tokens, labels, is_device)."""
+        want = (self.samples, self.spec.seq_len)
+        V = self.spec.vocab
+        if hasattr(tokens, "is_cuda") or hasattr(labels, "is_cuda"):
+            import torch
+            if not (isinstance(tokens, torch.Tensor) and isinstance(labels, torch.Tensor)
+                    and tokens.is_cuda and labels.is_cuda):
+                raise ValidationError("tokens and labels must both be host arrays or both CUDA tensors")
+            for name, t in (("tokens", tokens), ("labels", labels)):
+                if t.dtype != torch.int32:
+                    raise ValidationError(f"{name} must be int32 (got {t.dtype})")
+                if tuple(t.shape) != want:
+                    raise ValidationError(f"{name} must be {list(want)} (got {list(t.shape)})")
+                if not t.is_contiguous():
+                    raise ValidationError(f"{name} must be contiguous")
+                if t.device.index != self.device:
+                    raise ValidationError(f"{name} is on cuda:{t.device.index}, the runtime on cuda:{self.device}")
+            # the runtime's streams are non-blocking: torch's pending work on
+            # the buffers must be finished before they are read
+            torch.cuda.current_stream(tokens.device).synchronize()
+            key = (tokens.data_ptr(), tokens._version, labels.data_ptr(), labels._version)
+            if key != self._checked:  # range check once per buffer version
+                lo = min(int(tokens.min()), int(labels.min()))
+                hi = max(int(tokens.max()), int(labels.max()))
+                if lo < 0 or hi >= V:
+                    raise ValidationError(f"token ids / labels must lie in [0, {V}) (got [{lo}, {hi}])")
+                self._checked = key
+            return tokens, labels, True
+        t = np.ascontiguousarray(tokens, dtype=np.int32)
+        lb = np.ascontiguousarray(labels, dtype=np.int32)
+        for name, a, src in (("tokens", t, tokens), ("labels", lb, labels)):
+            if a.shape != want:
+                raise ValidationError(f"{name} must be {list(want)} (got {list(a.shape)})")
+            if not np.array_equal(a, np.asarray(src)):
+                raise ValidationError(f"{name} do not fit int32")
+            if a.size and (int(a.min()) < 0 or int(a.max()) >= V):
+                raise ValidationError(f"{name} must lie in [0, {V}) (got [{int(a.min())}, {int(a.max())}])")
+        return t, lb, False
+
+    @staticmethod
+    def _ptr(x) -> int:
+        return x.data_ptr() if hasattr(x, "data_ptr") else x.ctypes.data
 
     def step(self, tokens, labels) -> float:
         """One training iteration on this rank's samples.  ``tokens`` /
@@ -321,21 +410,9 @@ class HarmonyRuntime:
             NL.check(self.lib.hm_runtime_run_iteration(self.handle, C.c_void_p(img.data_ptr()),
                                                        C.c_void_p(lab.data_ptr()), int(img.is_cuda), C.byref(loss)))
             return loss.value
-        if hasattr(tokens, "is_cuda") and tokens.is_cuda:
-            # the runtime's streams are non-blocking: torch's pending work on
-            # the token buffers must be finished before they are read
-            import torch
-            torch.cuda.current_stream(tokens.device).synchronize()
-            rc = self.lib.hm_runtime_run_iteration(self.handle, C.c_void_p(tokens.data_ptr()),
-                                                   C.c_void_p(labels.data_ptr()), 1, C.byref(loss))
-        else:
-            t = np.ascontiguousarray(tokens, dtype=np.int32)
-            lb = np.ascontiguousarray(labels, dtype=np.int32)
-            if t.shape != (self.samples, self.spec.seq_len):
-                raise ValidationError(f"tokens must be [{self.samples}, {self.spec.seq_len}]")
-            rc = self.lib.hm_runtime_run_iteration(self.handle, t.ctypes.data, lb.ctypes.data, 0,
-                                                   C.byref(loss))
-        NL.check(rc)
+        t, lb, dev = self._gpt_inputs(tokens, labels)
+        NL.check(self.lib.hm_runtime_run_iteration(self.handle, C.c_void_p(self._ptr(t)), C.c_void_p(self._ptr(lb)),
+                                                   int(dev), C.byref(loss)))
         return loss.value
 
     def _cnn_inputs(self, images, labels):
@@ -349,6 +426,8 @@ class HarmonyRuntime:
         labels = torch.as_tensor(labels, dtype=torch.int32, device=images.device)
         if tuple(labels.shape) != (self.samples,):
             raise ValidationError(f"labels must be [{self.samples}]")
+        if labels.numel() and (int(labels.min()) < 0 or int(labels.max()) >= self.spec.classes):
+            raise ValidationError(f"labels must lie in [0, {self.spec.classes})")
         images, labels = images.contiguous(), labels.contiguous()
         if images.is_cuda:
             torch.cuda.current_stream(images.device).synchronize()
@@ -367,17 +446,9 @@ class HarmonyRuntime:
                                                    C.c_void_p(lab.data_ptr()), int(img.is_cuda), losses,
                                                    C.byref(total)))
             return list(losses), total.value / 1e9
-        if hasattr(tokens, "is_cuda") and tokens.is_cuda:
-            import torch
-            torch.cuda.current_stream(tokens.device).synchronize()
-            rc = self.lib.hm_runtime_run_steps(self.handle, n, C.c_void_p(tokens.data_ptr()),
-                                               C.c_void_p(labels.data_ptr()), 1, losses, C.byref(total))
-        else:
-            t = np.ascontiguousarray(tokens, dtype=np.int32)
-            lb = np.ascontiguousarray(labels, dtype=np.int32)
-            rc = self.lib.hm_runtime_run_steps(self.handle, n, t.ctypes.data, lb.ctypes.data, 0, losses,
-                                               C.byref(total))
-        NL.check(rc)
+        t, lb, dev = self._gpt_inputs(tokens, labels)
+        NL.check(self.lib.hm_runtime_run_steps(self.handle, n, C.c_void_p(self._ptr(t)), C.c_void_p(self._ptr(lb)),
+                                               int(dev), losses, C.byref(total)))
         return list(losses), total.value / 1e9
 
     def counters(self) -> dict:

@@ -1,0 +1,143 @@
+"""Numerics parity of the runtime against the torch-CPU fp32 oracle, measured
+on what training changes: per layer, the weight update after K steps
+(w_K - w_0 vs the oracle's), and Adam's m and v (zero at step 0, so they are
+deltas already), plus the loss at every step.
+
+Two arithmetic modes:
+* ``math="fp32"`` -- the parity mode (fp32 activations; GEMMs as three-plane
+  bf16 split products, fp32-level accuracy; fp32 attention): the north star's
+  "within 1e-3 relative in fp32-accumulate mode" holds for the loss and for
+  every layer's weight / m / v deltas.
+* ``math="bf16"`` -- the throughput mode the bench runs (bf16 tensor-core
+  operands, fp32 accumulate, fp32 master state): loss within 1e-3; per-layer
+  deltas within the separately stated bf16 tolerances below (bf16 operand
+  rounding changes gradients by ~0.4% per element, and Adam's normalised
+  update turns that into sign noise where a gradient is near zero).
+
+Configs: c1 (tiny GPT-2, 10 steps) and the benchmarked c3 shape (GPT-2 XL
+layers: d=1600, 25 heads, seq 1024, V=50257) at 4 layers, D=4, PP and DP,
+3 steps.  The schedule ledger equals simulate's at every step."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2202_01306_b200 as H
+from paper_2202_01306_b200.model import GPT_PRESETS, GPTSpec, gpt_profiles, synthetic_batch
+
+pytestmark = pytest.mark.gpu
+
+# fp32-operand parity mode (north star: 1e-3 relative).  Measured on B200
+# (r2): loss <= 4e-6; per-layer dW 2.6e-5 (c1), 3.5e-4 (c3 shape), 6.1e-4
+# (d=8192); m, v <= 1.5e-4.
+FP32_TOL = {"loss": 1e-3, "dw": 1e-3, "m": 1e-3, "v": 1e-3}
+# bf16 throughput mode, stated separately.  Measured: loss 1.3e-5 (c1),
+# 2.7e-5 (c3 shape), 9.2e-4 (d=8192, lr 1e-5); per-layer dW 1.7e-2 (c1),
+# 5.0e-2 (c3 shape), 7.4e-2 (d=8192); m <= 1.9e-2, v <= 2.3e-2.
+BF16_TOL = {"loss": 1e-3, "dw": 1e-1, "m": 5e-2, "v": 5e-2}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+
+
+_oracle_cache = {}
+
+
+def _oracle_run(spec, cfg, steps, w0, w_off, lr):
+    """Oracle trajectory (losses, final w, m, v), cached per configuration so
+    both arithmetic modes compare against one CPU run."""
+    key = (spec, cfg, steps, lr)
+    if key not in _oracle_cache:
+        from oracle.gpt_cpu import GPTOracle
+        o = GPTOracle(spec, w0, w_off, lr=lr)
+        tok, lab = synthetic_batch(spec, cfg.minibatch)
+        groups = list(cfg_groups(cfg))
+        losses = [o.step(tok, lab, groups) for _ in range(steps)]
+        _oracle_cache[key] = (losses, o.w.numpy().copy(), o.m.numpy().copy(), o.v.numpy().copy())
+    return _oracle_cache[key]
+
+
+def cfg_groups(cfg):
+    return H.microbatch_groups(cfg.minibatch, cfg.u_f)
+
+
+def per_layer_rel(a, b, off, base=None):
+    """max over layers of ||(a - base) - (b - base)|| / ||b - base||."""
+    out = []
+    for L in range(len(off) - 1):
+        o0, o1 = int(off[L]), int(off[L + 1])
+        da = a[o0:o1] - (base[o0:o1] if base is not None else 0)
+        db = b[o0:o1] - (base[o0:o1] if base is not None else 0)
+        out.append(float(np.linalg.norm(da - db) / max(np.linalg.norm(db), 1e-30)))
+    return out
+
+
+def run_parity(spec, cfg, steps, math, alpha=16 << 30, lr=1e-4):
+    from paper_2202_01306_b200.runtime import HarmonyRuntime
+    prof = gpt_profiles(spec, u_max=64)
+    mach = H.MachineModel(gpu_count=1, gpu_mem_capacity=alpha, pcie_bandwidth=55_000_000_000)
+    g = H.generate_task_graph(cfg, mach, prof)
+    rt = HarmonyRuntime(spec, alpha_bytes=alpha, lr=lr, math=math)
+    rt.init_weights(0)
+    w0 = rt.w.copy()
+    rt.load(g, mach, prof)
+    tok, lab = synthetic_batch(spec, cfg.minibatch)
+    sim = H.simulate(g, mach, prof)
+    losses = []
+    for _ in range(steps):
+        losses.append(rt.step(tok, lab))
+        assert rt.report().ledger == sim.ledger
+    w, k = rt.w.copy(), rt.k.copy()
+    off = rt.w_off.copy()
+    rt.close()
+    ref_l, ref_w, ref_m, ref_v = _oracle_run(spec, cfg, steps, w0, off, lr)
+    res = {
+        "loss": max(abs(a - b) / abs(b) for a, b in zip(losses, ref_l)),
+        "dw": per_layer_rel(w, ref_w, off, w0),
+        "m": per_layer_rel(k[0::2], ref_m, off),
+        "v": per_layer_rel(k[1::2], ref_v, off),
+    }
+    print(f"{spec.name} {cfg.mode.value} math={math}: loss {res['loss']:.2e}  "
+          f"dW {max(res['dw']):.2e} {['%.1e' % x for x in res['dw']]}  "
+          f"m {max(res['m']):.2e}  v {max(res['v']):.2e}")
+    return res
+
+
+def check(res, tol):
+    assert res["loss"] < tol["loss"], res
+    for key in ("dw", "m", "v"):
+        assert max(res[key]) < tol[key], (key, res[key])
+
+
+@pytest.mark.parametrize("math", ["fp32", "bf16"])
+def test_c1_tiny_per_layer_deltas(math):
+    spec = GPT_PRESETS["tiny"]
+    packs = ((0, 1), (2, 3))
+    cfg = H.Configuration(4, packs, 4, packs, 16, H.Mode.PP)
+    check(run_parity(spec, cfg, 10, math), FP32_TOL if math == "fp32" else BF16_TOL)
+
+
+@pytest.mark.parametrize("math", ["fp32", "bf16"])
+@pytest.mark.parametrize("mode", ["pp", "dp"])
+def test_c3_gpt2xl_shape_per_layer_deltas(mode, math):
+    """The benchmarked config's layer shapes (GPT-2 XL: d=1600, 25 heads of
+    64, seq 1024, vocab 50257 padded to 50304 -- the 192-wide GEMM tiles, the
+    two-pass LayerNorm backward and the vocab-50304 head) at 4 layers, D=4 in
+    groups of 2, recompute from the stash; 3 steps."""
+    spec = GPTSpec(4, 1600, 25, 1024, 50257, True, "gpt2-xl-4l")
+    packs = ((0, 1), (2, 3))
+    cfg = H.Configuration(2, packs, 2, packs, 4, H.Mode(mode))
+    check(run_parity(spec, cfg, 3, math, alpha=40 << 30), FP32_TOL if math == "fp32" else BF16_TOL)
+
+
+@pytest.mark.parametrize("math", ["fp32", "bf16"])
+def test_wide_head_dim_128_per_layer_deltas(math):
+    """The c4 / gpt-15b layer shape (d=8192, 64 heads of 128) at 2 layers,
+    seq 256, vocab 1024 (lr 1e-5, see test_runtime_gpu)."""
+    spec = GPTSpec(2, 8192, 64, 256, 1024, causal=True, name="wide-2l")
+    packs = ((0, 0), (1, 1))
+    cfg = H.Configuration(1, packs, 1, packs, 2, H.Mode.PP)
+    check(run_parity(spec, cfg, 3, math, alpha=60 << 30, lr=1e-5), FP32_TOL if math == "fp32" else BF16_TOL)

@@ -2,7 +2,11 @@
 (CUDA IPC and stream memory operations work between processes on the same
 device).  Checks: the union of the ranks' executed ledgers equals the
 planner's ledger (including the peer2peer X / Y / dY rows), and loss and
-weights match the torch-CPU oracle -- for step-by-step and pipelined runs."""
+weights match the torch-CPU oracle -- for step-by-step and pipelined runs,
+at the tiny c1 shape and at the c4 (GPT-40B) layer shape at reduced depth
+(d=8192, 64 heads of 128, seq 256): loss within 1e-3 at every step, per-layer
+weight deltas / Adam moments within the stated tolerances
+(tests/test_parity_gpu.py)."""
 
 import os
 import socket
@@ -24,25 +28,39 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, shm, pipelined, q):
+SPECS = {
+    "tiny": dict(preset="tiny", lr=1e-4, alpha=4 << 30),
+    # the 40B config's layer (805 M parameters, 3.2 GB of fp32 W per layer)
+    "wide": dict(spec=(4, 8192, 64, 256, 1024), lr=1e-5, alpha=48 << 30),
+}
+
+
+def _spec(name):
+    from paper_2202_01306_b200.model import GPT_PRESETS, GPTSpec
+    c = SPECS[name]
+    return GPT_PRESETS[c["preset"]] if "preset" in c else GPTSpec(*c["spec"], causal=True, name="gpt-40b-layers")
+
+
+def _worker(rank, world, port, shm, pipelined, name, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_2202_01306_b200 as H
         from paper_2202_01306_b200.model import GPT_PRESETS, gpt_profiles, synthetic_batch
         from paper_2202_01306_b200.runtime import HarmonyRuntime
-        spec = GPT_PRESETS["tiny"]
+        spec = _spec(name)
+        lr, alpha = SPECS[name]["lr"], SPECS[name]["alpha"]
         prof = gpt_profiles(spec)
-        mach = H.MachineModel(gpu_count=world, gpu_mem_capacity=4 << 30, pcie_bandwidth=55_000_000_000)
+        mach = H.MachineModel(gpu_count=world, gpu_mem_capacity=alpha, pcie_bandwidth=55_000_000_000)
         pf = ((0, 0), (1, 1), (2, 3))
         pb = ((0, 1), (2, 3))
         g = H.generate_task_graph(H.Configuration(4, pf, 4, pb, 8, H.Mode.PP), mach, prof)
         torch.cuda.set_device(0)
-        rt = HarmonyRuntime(spec, alpha_bytes=4 << 30, device=0)
+        rt = HarmonyRuntime(spec, alpha_bytes=alpha, device=0, lr=lr)
         stash = HarmonyRuntime.stash_bytes_for(g, prof)
         if rank == 0:
             rt.share_arenas(shm, True, stash)
-            rt.init_weights(0)
+            rt.init_weights(0, device="cuda" if name != "tiny" else None)
         dist.barrier()
         if rank != 0:
             rt.share_arenas(shm, False, stash)
@@ -65,9 +83,13 @@ def _worker(rank, world, port, shm, pipelined, q):
         dist.barrier()
         rep = rt.report()
         out = {"rank": rank, "losses": losses, "ledger": rep.ledger, "p2p": rt.counters()["p2p_bytes"]}
-        if rank == 0:
-            out["w_final"] = rt.w.copy()
-            out["w0"] = w0
+        if rank == 0:  # weights travel as files (GBs at the 40B layer shape)
+            d = os.environ.get("TMPDIR", "/tmp")
+            out["w_final"] = os.path.join(d, f"{shm}_w_final.npy")
+            out["w0"] = os.path.join(d, f"{shm}_w0.npy")
+            np.save(out["w_final"], rt.w)
+            np.save(out["w0"], w0)
+            del w0
         gathered = [None] * world
         dist.all_gather_object(gathered, out)
         if rank == 0:
@@ -79,35 +101,41 @@ def _worker(rank, world, port, shm, pipelined, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("pipelined", [False, True])
-def test_pp_two_ranks_one_gpu(pipelined):
+@pytest.mark.parametrize("name,pipelined", [("tiny", False), ("tiny", True), ("wide", True)])
+def test_pp_two_ranks_one_gpu(name, pipelined):
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     shm = f"hm_pp_test_{os.getpid()}_{int(pipelined)}"
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, shm, pipelined, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, shm, pipelined, name, q)) for r in range(2)]
     for p in procs:
         p.start()
-    res = q.get(timeout=300)
+    res = q.get(timeout=900)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
     r0, r1 = sorted(res["ranks"], key=lambda x: x["rank"])
+    for key in ("w0", "w_final"):
+        path = r0[key]
+        r0[key] = np.load(path)
+        os.unlink(path)
     assert sorted(r0["ledger"] + r1["ledger"]) == res["sim_ledger"]
     assert any(row[4] == "peer2peer" for row in res["sim_ledger"])
     # oracle
     from oracle.gpt_cpu import GPTOracle
-    from paper_2202_01306_b200.model import GPT_PRESETS, synthetic_batch
-    spec = GPT_PRESETS["tiny"]
-    o = GPTOracle(spec, r0["w0"], res["w_off"])
+    from paper_2202_01306_b200.model import synthetic_batch
+    from test_parity_gpu import BF16_TOL, per_layer_rel
+    spec = _spec(name)
+    o = GPTOracle(spec, r0["w0"], res["w_off"], lr=SPECS[name]["lr"])
     tok, lab = synthetic_batch(spec, 8)
     ref = [o.step(tok, lab, [8]) for _ in range(3)]
     # the rank running the last forward task owns the loss; the other reports 0
     losses = [max(a, b) for a, b in zip(r0["losses"], r1["losses"])]
     assert min(min(r0["losses"]), min(r1["losses"])) == 0.0
     for a, b in zip(losses, ref):
-        assert abs(a - b) / b < 2e-3, (losses, ref)
-    rel = np.linalg.norm(r0["w_final"] - o.w.numpy()) / np.linalg.norm(o.w.numpy())
-    assert rel < 1e-3, rel
+        assert abs(a - b) / b < BF16_TOL["loss"], (losses, ref)
+    dw = per_layer_rel(r0["w_final"], o.w.numpy(), res["w_off"], r0["w0"])
+    print(f"PP N=2 {name}: loss {losses} vs {ref}; per-layer dW rel {['%.1e' % x for x in dw]}")
+    assert max(dw) < BF16_TOL["dw"], dw
