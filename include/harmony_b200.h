@@ -42,6 +42,8 @@ extern "C" {
 #define HM_ERR_MISSING_PROFILE (-5) /* MissingProfileError                   */
 #define HM_ERR_INTERNAL (-6)        /* invariant violation                   */
 #define HM_ERR_PROFILE_RANGE (-7)   /* ProfileRangeError                     */
+#define HM_ERR_LAYER_TOO_LARGE (-8) /* LayerTooLargeError (packing)          */
+#define HM_ERR_UNPACKABLE (-9)      /* UnpackableError (packing)             */
 
 /* ---- enums shared with the Python lowering (taskgraph.py:61-71, core.py:44-54) */
 enum hm_tensor { HM_X = 0, HM_Y = 1, HM_DX = 2, HM_DY = 3, HM_W = 4, HM_DW = 5, HM_K = 6, HM_SX = 7 };
@@ -114,6 +116,16 @@ typedef struct hm_plan hm_plan;
 hm_plan *hm_plan_build(const hm_task *tasks, int32_t n_tasks, const int32_t *groups,
                        const hm_entry *entries, const hm_machine *machine,
                        const hm_profile *profile, int32_t *status);
+/* Layer-pack decomposition of layers [0, count) (paper Algorithm 2;
+ * replaces packing.balanced_time_pack / greedy_maxpack_baseline,
+ * pkg/src/wrapsched/packing.py:67-186).  mode 0 = balanced time, 1 = greedy.
+ * time / mem: per-layer pass time (ns) and memory (bytes) at the microbatch;
+ * ckpt: per-layer bytes a FORWARD pack adds for its checkpointed input
+ * (x(first, u)), NULL for backward packs.  Out: the first layer of each pack
+ * (in/out *n_packs = capacity / count).  HM_ERR_LAYER_TOO_LARGE sets
+ * *bad_layer; HM_ERR_UNPACKABLE when no pack count fits alpha. */
+int hm_pack_layers(int32_t mode, int32_t count, const int64_t *time, const int64_t *mem, const int64_t *ckpt,
+                   int64_t alpha, int32_t *first_layer, int32_t *n_packs, int32_t *bad_layer);
 /* Run the FIFO event loop (simulator._run); returns status, fills start/end. */
 int hm_plan_simulate(hm_plan *plan, int64_t *makespan_ns);
 int32_t hm_plan_item_count(const hm_plan *plan);
@@ -258,6 +270,9 @@ int hm_runtime_kernel_stats(const hm_runtime *rt, double *out, int32_t cap);
  * to last CTA end on %globaltimer -- is recorded by GEMM launches only);
  * returns the number of launches (copies at most cap). */
 int hm_runtime_kernel_launches(const hm_runtime *rt, double *out, int32_t cap);
+/* GEMM calls of the last profiled iteration, 7 fields each {m, n, k, a_major,
+ * b_major, epilogue, has_bias}, in launch order; returns the count. */
+int hm_runtime_gemm_shapes(const hm_runtime *rt, int64_t *out, int32_t cap);
 void hm_runtime_free(hm_runtime *rt);
 
 /* ---- kernels, testable alone (raw device pointers, a cudaStream_t) -------- */
@@ -322,6 +337,11 @@ int hm_k_gemm_tile(int64_t m, int64_t n, int64_t k, int32_t epilogue, int32_t b_
 /* Force a tile configuration for every later GEMM of the process (0 = auto);
  * for tests and tuning (same as HM_GEMM_BN / HM_GEMM_CG / HM_GEMM_SPLITK). */
 int hm_k_gemm_set_tile(int32_t bn, int32_t cta_pair, int32_t splits);
+/* The GEMM's own per-launch time (us) for one shape {m, n, k, a_major,
+ * b_major, epilogue, has_bias}: a CUDA graph of `reps` back-to-back launches
+ * on rotating random operand sets (inputs not L2-resident), timed with CUDA
+ * events around whole graph replays. */
+int hm_k_gemm_replay(const int64_t *shape, int32_t reps, void *stream, double *us_per_launch);
 
 /* Fused attention over qkv [batch*seq, 3*heads*head_dim] bf16 (q|k|v thirds).
  * out [batch*seq, heads*head_dim] bf16; lse [batch*seq, heads] fp32 (log2).

@@ -90,6 +90,8 @@ def lib() -> C.CDLL:
         "hm_plan_edge_count": (C.c_int32, [C.c_void_p]),
         "hm_plan_edges": (C.c_int, [C.c_void_p, P(C.c_int32), P(C.c_int32), P(C.c_int32), C.c_int32]),
         "hm_plan_free": (None, [C.c_void_p]),
+        "hm_pack_layers": (C.c_int, [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                     C.c_void_p, C.c_void_p, C.c_void_p]),
         "hm_runtime_create": (C.c_void_p, [C.c_int32, P(hm_model), C.c_int64, P(C.c_int32)]),
         "hm_runtime_arena": (C.c_void_p, [C.c_void_p, C.c_int32, P(C.c_int64)]),
         "hm_runtime_layer_offsets": (C.c_int, [C.c_void_p, P(C.c_int64), C.c_int32]),
@@ -123,6 +125,8 @@ def lib() -> C.CDLL:
         "hm_runtime_ipc_import": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
         "hm_runtime_init_ipc_reduce": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),
         "hm_runtime_numa_node": (C.c_int, [C.c_void_p]),
+        "hm_runtime_gemm_shapes": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
+        "hm_k_gemm_replay": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
         "hm_k_gemm_precise": (C.c_int, [C.c_void_p] * 3 + [C.c_int64] * 6 + [C.c_int32] * 3
                               + [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
                                  C.c_void_p, C.c_int64, C.c_void_p]),

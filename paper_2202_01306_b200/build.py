@@ -60,7 +60,8 @@ def _compile(src: str, force: bool) -> tuple[str, str]:
     newest_dep = max([os.path.getmtime(src)] + [os.path.getmtime(h) for h in _headers()])
     if not force and os.path.exists(obj) and os.path.getmtime(obj) >= newest_dep:
         return obj, ""
-    flags = COMMON + (CUFLAGS if src.endswith(".cu") else ARCH + ["-x", "cu"])
+    # host planner code: no FMA contraction, so double arithmetic rounds like the reference's Python
+    flags = COMMON + (CUFLAGS if src.endswith(".cu") else ARCH + ["-x", "cu", "-Xcompiler", "-ffp-contract=off"])
     cmd = [nvcc()] + flags + ["-c", src, "-o", obj]
     p = subprocess.run(cmd, capture_output=True, text=True)
     if p.returncode != 0:

@@ -23,6 +23,7 @@
 #include <cstdlib>
 #include <mutex>
 #include <tuple>
+#include <vector>
 #include <map>
 
 #include "../runtime/common.hpp"
@@ -680,10 +681,16 @@ static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMa
   return HM_OK;
 }
 
+std::vector<int64_t> *&shape_log() {
+  static std::vector<int64_t> *log = nullptr;
+  return log;
+}
+
 int run(const void *A, const void *B, void *D, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb,
         int64_t ldd, int a_mn, int b_mn, int epi, const float *bias, void *aux, int64_t ld_aux,
         cudaStream_t stream, int force_bn) {
   if (M <= 0 || N <= 0 || K <= 0) return fail(HM_ERR_VALIDATION, "gemm: empty problem");
+  if (shape_log()) shape_log()->insert(shape_log()->end(), {M, N, K, a_mn, b_mn, epi, bias ? 1 : 0});
   if (epi < HM_EPI_STORE_BF16 || epi > HM_EPI_ADD_BF16) return fail(HM_ERR_VALIDATION, "gemm: unknown epilogue");
   if ((lda * 2) % 16 || (ldb * 2) % 16) return fail(HM_ERR_VALIDATION, "gemm: operand pitch must be 16B aligned");
   if (((uintptr_t)A | (uintptr_t)B) & 15) return fail(HM_ERR_VALIDATION, "gemm: operands must be 16B aligned");

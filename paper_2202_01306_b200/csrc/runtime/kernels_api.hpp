@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
 
 namespace hm {
 int adam_launch_dev(float *w, const float *g, float *k, int64_t n, double b1, double b2, double eps,
@@ -13,6 +14,8 @@ int adam_launch(float *w, const float *g, float *k, int64_t n, double lr, double
 namespace gemm {
 int run(const void *A, const void *B, void *D, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb, int64_t ldd,
         int a_mn, int b_mn, int epi, const float *bias, void *aux, int64_t ld_aux, cudaStream_t stream, int force_bn);
+// when set, every gemm::run call appends {M, N, K, a_mn, b_mn, epi, has_bias}
+std::vector<int64_t> *&shape_log();
 }
 namespace attn {
 int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int DH, int causal, cudaStream_t s);

@@ -181,6 +181,7 @@ struct hm_runtime {
   hm::RtProfiler prof;
   double kstats[hm::KC_COUNT][4] = {{0}};  // ms, flops, bytes, launches (accumulated)
   std::vector<double> klaunch;  // last profiled iteration: (class, flops, bytes, event ms, device-clock ms) per launch
+  std::vector<int64_t> gemm_shapes;  // GEMM calls of the last profiled enqueue, 7 fields each (gemm::shape_log)
   int device = 0;
   hm_model m{};
   int family = HM_FAMILY_GPT;          // GPT / BERT transformer chain or deep CNN
@@ -1788,9 +1789,14 @@ static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *l
         rt.prof.capture = true;
       }
       profiler() = rt.profiling ? &rt.prof : nullptr;
+      if (rt.profiling) {
+        rt.gemm_shapes.clear();
+        gemm::shape_log() = &rt.gemm_shapes;
+      }
       const int64_t l0 = launch_counter().load();
       HM_CUDA(cudaStreamBeginCapture(sc, cudaStreamCaptureModeRelaxed));
       int rc = enqueue_body(rt, true, false, h2d, d2h, coll);
+      gemm::shape_log() = nullptr;
       cudaGraph_t g = nullptr;
       cudaError_t ce = cudaStreamEndCapture(sc, &g);
       profiler() = nullptr;
@@ -1818,7 +1824,12 @@ static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *l
     rt.prof.reset();
     if (rt.profiling) HM_CUDA(rt.prof.clear_spans(sc));
     profiler() = rt.profiling ? &rt.prof : nullptr;
+    if (rt.profiling) {
+      rt.gemm_shapes.clear();
+      gemm::shape_log() = &rt.gemm_shapes;
+    }
     int rc = enqueue_body(rt, false, false, h2d, d2h, coll);
+    gemm::shape_log() = nullptr;
     profiler() = nullptr;
     HM_TRY(rc);
   }
@@ -2438,6 +2449,15 @@ int hm_runtime_kernel_launches(const hm_runtime *rt, double *out, int32_t cap) {
   if (out)
     for (int i = 0; i < n && i < cap; ++i)
       for (int j = 0; j < 5; ++j) out[5 * i + j] = rt->klaunch[5 * i + j];
+  return n;
+}
+
+int hm_runtime_gemm_shapes(const hm_runtime *rt, int64_t *out, int32_t cap) {
+  if (!rt) return hm::fail(HM_ERR_VALIDATION, "null runtime");
+  const int n = (int)(rt->gemm_shapes.size() / 7);
+  if (out)
+    for (int i = 0; i < n && i < cap; ++i)
+      for (int j = 0; j < 7; ++j) out[7 * i + j] = rt->gemm_shapes[7 * i + j];
   return n;
 }
 

@@ -90,6 +90,9 @@ HM_ERR_DEADLOCK = -3
 HM_ERR_DEVICE = -4
 HM_ERR_MISSING_PROFILE = -5
 HM_ERR_INTERNAL = -6
+HM_ERR_PROFILE_RANGE = -7
+HM_ERR_LAYER_TOO_LARGE = -8
+HM_ERR_UNPACKABLE = -9
 
 _STATUS = {
     HM_ERR_VALIDATION: ValidationError,
@@ -98,6 +101,9 @@ _STATUS = {
     HM_ERR_DEVICE: DeviceError,
     HM_ERR_MISSING_PROFILE: MissingProfileError,
     HM_ERR_INTERNAL: WrapschedError,
+    HM_ERR_PROFILE_RANGE: ProfileRangeError,
+    HM_ERR_LAYER_TOO_LARGE: LayerTooLargeError,
+    HM_ERR_UNPACKABLE: UnpackableError,
 }
 
 

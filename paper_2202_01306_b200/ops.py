@@ -161,3 +161,13 @@ def bias_grad(dy, db):
 
 def N_lib():
     return NL.lib()
+
+
+def gemm_replay_us(shape, reps: int = 32) -> float:
+    """The GEMM's own per-launch time (us) for one logged shape (m, n, k,
+    a_major, b_major, epilogue, has_bias): back-to-back launches in a CUDA
+    graph, CUDA-event timed, rotating operand sets (hm_k_gemm_replay)."""
+    arr = (C.c_int64 * 7)(*shape)
+    us = C.c_double(0.0)
+    NL.check(N_lib().hm_k_gemm_replay(arr, reps, _stream(), C.byref(us)))
+    return us.value

@@ -479,6 +479,20 @@ class HarmonyRuntime:
             self.lib.hm_runtime_kernel_launches(self.handle, out.ctypes.data_as(C.POINTER(C.c_double)), n)
         return out
 
+    def gemm_shapes(self) -> list[tuple]:
+        """Distinct GEMM calls of the last profiled iteration with their
+        counts: [((m, n, k, a_major, b_major, epilogue, has_bias), count)]."""
+        n = self.lib.hm_runtime_gemm_shapes(self.handle, None, 0)
+        if n <= 0:
+            return []
+        buf = np.zeros((n, 7), dtype=np.int64)
+        self.lib.hm_runtime_gemm_shapes(self.handle, buf.ctypes.data, n)
+        out: dict[tuple, int] = {}
+        for row in buf:
+            key = tuple(int(x) for x in row)
+            out[key] = out.get(key, 0) + 1
+        return list(out.items())
+
     def measured_items(self) -> np.ndarray:
         n1 = self.lib.hm_runtime_ledger_count(self.handle)
         n2 = self.lib.hm_runtime_trace_count(self.handle)
