@@ -348,8 +348,9 @@ int hm_k_gemm_replay(const int64_t *shape, int32_t reps, void *stream, double *u
  * head_dim 64 or 128; seq multiple of 64; causal 1 = GPT mask. */
 int hm_k_attn_fwd(const void *qkv, void *out, float *lse, int32_t batch, int32_t seq, int32_t heads,
                   int32_t head_dim, int32_t causal, void *stream);
-/* Same forward on tcgen05 tensor cores (head_dim 64, seq % 128 == 0); the
- * runtime uses it whenever the shape allows. */
+/* Same forward on tcgen05 tensor cores (head_dim 64 or 128, seq % 128 == 0);
+ * hm_k_attn_fwd / hm_k_attn_bwd and the runtime use it whenever the shape
+ * allows. */
 int hm_k_attn_fwd_tc(const void *qkv, void *out, float *lse, int32_t batch, int32_t seq, int32_t heads,
                      int32_t head_dim, int32_t causal, void *stream);
 /* Backward: writes dq|dk|dv into dqkv (same layout as qkv).  Scratch:

@@ -5,6 +5,7 @@ new `execute`), reading and writing the reference's JSON documents.
     python -m paper_2202_01306_b200 search   --machine m.json --profiles p.json --spec s.json --out-dir run/
     python -m paper_2202_01306_b200 execute  --preset gpt2-xl --machine m.json --config c.json --steps 3 --out r.json
     python -m paper_2202_01306_b200 profile  --preset gpt2-xl --out p.json
+    python -m paper_2202_01306_b200 gantt    --report measured.json [--compare estimate.json] --fmt svg --out g.svg
 
 Exit codes follow the reference (`cli.py:66-71`): 0 ok, 2 validation error,
 3 infeasible, 4 internal / device error.
@@ -58,7 +59,27 @@ def _execute(a) -> int:
     g = generate_task_graph(cfg, m, p)
     rep = execute(g, m, p, model=spec, batch=synthetic_batch(spec, cfg.minibatch), steps=a.steps)
     F.save_json(F.report_to_doc(rep), a.out)
+    if a.gantt:  # estimate and measurement of the same graph on one time axis
+        from .gantt import render_comparison
+        from .simulator import simulate
+        open(a.gantt, "w").write(render_comparison(simulate(g, m, p), rep, title=a.preset))
     print(f"measured iteration {rep.makespan_ns / 1e6:.3f} ms; {rep.caveats[-1]}")
+    return 0
+
+
+def _gantt(a) -> int:
+    from .gantt import render_comparison, render_gantt
+    rep = F.report_from_doc(F.load_json(a.report))
+    if a.compare:
+        if a.fmt != "svg":
+            raise ValidationError("--compare renders SVG only")
+        doc = render_comparison(F.report_from_doc(F.load_json(a.compare)), rep)
+    else:
+        doc = render_gantt(rep, a.fmt, width=a.width)
+    if a.out:
+        open(a.out, "w").write(doc)
+    else:
+        sys.stdout.write(doc)
     return 0
 
 
@@ -96,7 +117,15 @@ def build_parser() -> argparse.ArgumentParser:
     s.add_argument("--profiles")
     s.add_argument("--steps", type=int, default=1)
     s.add_argument("--out", required=True)
+    s.add_argument("--gantt", help="SVG of the estimated and the measured trace")
     s.set_defaults(fn=_execute)
+    s = sub.add_parser("gantt")
+    s.add_argument("--report", required=True, help="sim_report JSON (simulate or execute)")
+    s.add_argument("--compare", help="a second report drawn above it (e.g. the estimate)")
+    s.add_argument("--fmt", choices=("text", "svg"), default="text")
+    s.add_argument("--width", type=int, default=100)
+    s.add_argument("--out")
+    s.set_defaults(fn=_gantt)
     s = sub.add_parser("profile")
     s.add_argument("--preset", required=True)
     s.add_argument("--u", type=int, nargs="+", default=[1, 2, 4])

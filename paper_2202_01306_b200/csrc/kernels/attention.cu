@@ -26,6 +26,12 @@ int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causa
 int backward_main(const void *qkv, const void *dout, const float *lse, const float *dvec, float *dq_acc, void *dqkv,
                   int B, int S, int H, int causal, cudaStream_t s);
 }  // namespace attn_tc
+namespace attn_tc128 {  // head_dim 128 (attention_tc128.cu)
+bool supported(int S, int DH);
+int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causal, cudaStream_t s);
+int backward_main(const void *qkv, const void *dout, const float *lse, const float *dvec, float *dq_acc, void *dqkv,
+                  int B, int S, int H, int causal, cudaStream_t s);
+}  // namespace attn_tc128
 namespace attn {
 
 constexpr int BQ = 64, BKV = 64, THREADS = 128;
@@ -497,9 +503,10 @@ static int bwd_launch(const __nv_bfloat16 *qkv, const __nv_bfloat16 *o, const __
     const char *e = getenv("HM_ATTN_BWD");
     return !(e && std::string(e) == "mma");
   }();
-  if (use_tc && attn_tc::supported(S, DH)) {
+  if (use_tc && (attn_tc::supported(S, DH) || attn_tc128::supported(S, DH))) {
     // tcgen05 main kernel; it folds the softmax scale into dq_acc
-    HM_TRY(attn_tc::backward_main(qkv, dout, lse, dvec, dq_acc, dqkv, B, S, H, CAUSAL ? 1 : 0, s));
+    if (DH == 64) HM_TRY(attn_tc::backward_main(qkv, dout, lse, dvec, dq_acc, dqkv, B, S, H, CAUSAL ? 1 : 0, s));
+    else HM_TRY(attn_tc128::backward_main(qkv, dout, lse, dvec, dq_acc, dqkv, B, S, H, CAUSAL ? 1 : 0, s));
     HM_CUDA(launch_pdl(dq_convert, dim3(1184), dim3(256), 0, s, (const float *)dq_acc, dqkv, rows, d, 1.f));
   } else {
     k<<<dim3(S / BKV, B * H), THREADS, bwd_smem<DH>(), s>>>(qkv, dout, lse, dvec, dq_acc, dqkv, S, H,
@@ -518,6 +525,7 @@ int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int DH, i
     return e && std::string(e) == "mma";
   }();
   if (!force_mma && attn_tc::supported(S, DH)) return attn_tc::forward(qkv, o, lse, B, S, H, causal, s);
+  if (!force_mma && attn_tc128::supported(S, DH)) return attn_tc128::forward(qkv, o, lse, B, S, H, causal, s);
   auto q = static_cast<const __nv_bfloat16 *>(qkv);
   auto out = static_cast<__nv_bfloat16 *>(o);
   if (DH == 64) return causal ? fwd_launch<64, true>(q, out, lse, B, S, H, s) : fwd_launch<64, false>(q, out, lse, B, S, H, s);

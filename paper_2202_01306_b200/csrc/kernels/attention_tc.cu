@@ -15,8 +15,8 @@
 // and fwdp_kernel (single tiles, short causal sequences).  Backward: bwd_kernel
 // (one CTA per 128-key block, two softmax warpgroups, dQ by TMA reduce-add).
 // Output o [tokens, d] bf16 and lse [tokens, H] (log2 domain) exactly as the
-// mma.sync kernel (attention.cu), which stays the fallback for head_dim 128
-// and for sequence lengths that are not a multiple of 128.
+// mma.sync kernel (attention.cu), which stays the fallback for sequence
+// lengths that are not a multiple of 128 (head_dim 128: attention_tc128.cu).
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -1681,9 +1681,18 @@ int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causa
 }  // namespace attn_tc
 }  // namespace hm
 
+namespace hm {
+namespace attn_tc128 {
+bool supported(int S, int DH);
+int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causal, cudaStream_t s);
+}  // namespace attn_tc128
+}  // namespace hm
+
 extern "C" int hm_k_attn_fwd_tc(const void *qkv, void *out, float *lse, int32_t batch, int32_t seq, int32_t heads,
                                 int32_t head_dim, int32_t causal, void *stream) {
+  if (hm::attn_tc128::supported(seq, head_dim))
+    return hm::attn_tc128::forward(qkv, out, lse, batch, seq, heads, causal, static_cast<cudaStream_t>(stream));
   if (!hm::attn_tc::supported(seq, head_dim))
-    return hm::fail(HM_ERR_VALIDATION, "tcgen05 attention needs head_dim 64 and seq % 128 == 0");
+    return hm::fail(HM_ERR_VALIDATION, "tcgen05 attention needs head_dim 64 or 128 and seq % 128 == 0");
   return hm::attn_tc::forward(qkv, out, lse, batch, seq, heads, causal, static_cast<cudaStream_t>(stream));
 }

@@ -1517,18 +1517,24 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
     if (plan->items[item].rec.gpu == rank) a.xwaits.push_back(item);
     else a.rwaits.push_back({item, 1});
   };
+  // host W / K / stash regions: another rank's transfers touch the same bytes
+  // only when the arenas are one shared segment (Harmony-PP across processes);
+  // Harmony-DP ranks with their own replicas never wait on each other here
+  auto xdep_host = [&](Action &a, int item) {
+    if (plan->items[item].rec.gpu == rank || rt.shared_arena) xdep(a, item);
+  };
   for (auto &a : rt.actions) {
     if (a.item < 0) continue;
     const hm_item &r = plan->items[a.item].rec;
     if (a.kind == 2 && r.tensor == HM_W)  // host W region rewritten by last iteration's swap-out
       for (int o : w_out)
-        if (overlaps(plan->items[o].rec.task, r.task)) xdep(a, o);
+        if (overlaps(plan->items[o].rec.task, r.task)) xdep_host(a, o);
     if (a.kind == 2 && r.tensor == HM_K)
       for (int o : k_out)
-        if (overlaps(plan->items[o].rec.task, r.task)) xdep(a, o);
+        if (overlaps(plan->items[o].rec.task, r.task)) xdep_host(a, o);
     if (a.kind == 3 && r.tensor == HM_SX)  // host stash region still read by last iteration's stash-in
       for (int o : sx_in)
-        if (plan->items[o].rec.layer == r.layer) xdep(a, o);
+        if (plan->items[o].rec.layer == r.layer) xdep_host(a, o);
     if (a.kind == 0 && plan->tasks[r.task].type == HM_TASK_F)
       for (int L : rt.trt[r.task].stash_heads) {
         auto it = sx_out.find({L, r.member});
@@ -1540,6 +1546,8 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
     if (a.kind == 6)  // my receive buffer is read by last iteration's compute of this task
       xdep(a, rt.trt[r.task].members.back());
   }
+  rt.counters[7] = 0;  // cross-rank (device-counter) waits per iteration
+  for (auto &a : rt.actions) rt.counters[7] += (int64_t)a.rwaits.size();
   // W leaves before K: the next iteration's forward needs W first
   for (size_t i = 0; i + 1 < rt.actions.size(); ++i) {
     Action &x = rt.actions[i], &y = rt.actions[i + 1];

@@ -455,7 +455,8 @@ class HarmonyRuntime:
         out = (C.c_int64 * 8)()
         NL.check(self.lib.hm_runtime_counters(self.handle, out, 8))
         return {"kernels": out[0], "iteration_ns": out[1], "device_bytes": out[2],
-                "h2d_bytes": out[3], "d2h_bytes": out[4], "p2p_bytes": out[5], "nccl_bytes": out[6]}
+                "h2d_bytes": out[3], "d2h_bytes": out[4], "p2p_bytes": out[5], "nccl_bytes": out[6],
+                "rank_waits": out[7]}
 
     KERNEL_CLASSES = ("gemm", "attn_fwd", "attn_bwd", "layernorm", "xent", "adam", "other")
 

@@ -62,7 +62,8 @@ def _worker(rank, world, port, D, math, q):
         torch.cuda.synchronize()
         dist.barrier()
         out = {"rank": rank, "losses": losses, "ledger": rt.report().ledger, "w": rt.w.copy(), "k": rt.k.copy(),
-               "w0": w0, "w_off": rt.w_off.copy(), "nccl_bytes": rt.counters()["nccl_bytes"]}
+               "w0": w0, "w_off": rt.w_off.copy(), "nccl_bytes": rt.counters()["nccl_bytes"],
+               "rank_waits": rt.counters()["rank_waits"]}
         gathered = [None] * world
         dist.all_gather_object(gathered, out)
         if rank == 0:
@@ -90,6 +91,9 @@ def test_dp_two_ranks_one_gpu(D, math):
     r0, r1 = sorted(res["ranks"], key=lambda x: x["rank"])
     assert sorted(r0["ledger"] + r1["ledger"]) == sorted(res["sim_ledger"])
     assert r0["nccl_bytes"] > 0
+    # per-rank host replicas: no transfer waits on another rank's counters (the
+    # NCCL path imports no peer pools, so such a wait could never be satisfied)
+    assert r0["rank_waits"] == 0 and r1["rank_waits"] == 0
     # both replicas: the same summed gradient, the same Adam -> the same bits
     assert np.array_equal(r0["w"].view(np.uint32), r1["w"].view(np.uint32))
     assert np.array_equal(r0["k"].view(np.uint32), r1["k"].view(np.uint32))

@@ -172,7 +172,11 @@ def _attn_ref(qkv, B, S, H, DH, causal):
 
 
 @pytest.mark.parametrize("B,S,H,DH,causal", [(2, 128, 4, 64, True), (1, 512, 2, 64, False),
-                                             (2, 256, 3, 64, True), (1, 256, 2, 128, True)])
+                                             (2, 256, 3, 64, True), (1, 256, 2, 128, True),
+                                             # head_dim 128 (attention_tc128.cu): odd query-tile count,
+                                             # full attention, the >HBM GPT shape at 1024 tokens
+                                             (2, 384, 3, 128, True), (1, 512, 2, 128, False),
+                                             (1, 1024, 4, 128, True), (1, 128, 2, 128, False)])
 def test_attention_fwd_bwd(ops, B, S, H, DH, causal):
     torch.manual_seed(5)
     d = H * DH
@@ -330,11 +334,11 @@ def test_bias_grad_and_cast(ops):
     assert torch.equal(dst, src.to(torch.bfloat16))
 
 
-@pytest.mark.parametrize("B,S,H,causal", [(2, 128, 4, True), (1, 512, 2, False), (2, 1024, 3, True),
-                                          (1, 256, 25, True)])
-def test_attention_fwd_tcgen05_matches(ops, B, S, H, causal):
+@pytest.mark.parametrize("B,S,H,causal,DH", [(2, 128, 4, True, 64), (1, 512, 2, False, 64), (2, 1024, 3, True, 64),
+                                             (1, 256, 25, True, 64), (2, 1024, 3, True, 128),
+                                             (1, 640, 2, False, 128), (4, 1024, 64, True, 128)])
+def test_attention_fwd_tcgen05_matches(ops, B, S, H, causal, DH):
     torch.manual_seed(11)
-    DH = 64
     d = H * DH
     qkv = _bf(B * S, 3 * d)
     out = torch.empty(B * S, d, device="cuda", dtype=torch.bfloat16)
@@ -354,7 +358,8 @@ def test_attention_bwd_tcgen05_opt_in():
     code = (f"import torch, sys; sys.path.insert(0, {here!r}); sys.path.insert(0, {here + '/..'!r}); "
             "import test_kernels_gpu as T; "
             "from paper_2202_01306_b200 import ops; "
-            "T.test_attention_fwd_bwd(ops, 2, 256, 3, 64, True); T.test_attention_fwd_bwd(ops, 1, 512, 2, 64, False)")
+            "T.test_attention_fwd_bwd(ops, 2, 256, 3, 64, True); T.test_attention_fwd_bwd(ops, 1, 512, 2, 64, False); "
+            "T.test_attention_fwd_bwd(ops, 1, 256, 2, 128, True)")
     env = dict(__import__("os").environ, HM_ATTN_BWD="mma")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]

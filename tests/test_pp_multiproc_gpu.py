@@ -82,7 +82,8 @@ def _worker(rank, world, port, shm, pipelined, name, q):
         torch.cuda.synchronize()
         dist.barrier()
         rep = rt.report()
-        out = {"rank": rank, "losses": losses, "ledger": rep.ledger, "p2p": rt.counters()["p2p_bytes"]}
+        out = {"rank": rank, "losses": losses, "ledger": rep.ledger, "p2p": rt.counters()["p2p_bytes"],
+               "rank_waits": rt.counters()["rank_waits"]}
         if rank == 0:  # weights travel as files (GBs at the 40B layer shape)
             d = os.environ.get("TMPDIR", "/tmp")
             out["w_final"] = os.path.join(d, f"{shm}_w_final.npy")
@@ -117,6 +118,8 @@ def test_pp_two_ranks_one_gpu(name, pipelined):
         p.join(timeout=120)
         assert p.exitcode == 0
     r0, r1 = sorted(res["ranks"], key=lambda x: x["rank"])
+    # activations and the shared host arenas order the ranks through device counters
+    assert r0["rank_waits"] > 0 and r1["rank_waits"] > 0
     for key in ("w0", "w_final"):
         path = r0[key]
         r0[key] = np.load(path)

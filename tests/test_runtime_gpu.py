@@ -355,3 +355,34 @@ def test_dp_allreduce_path_with_one_rank_nccl():
     # gradients, split-K reduce-adds)
     assert np.allclose(l0, l1, rtol=1e-4)
     assert np.linalg.norm(w0 - w1) / np.linalg.norm(w0) < 5e-4
+
+
+def test_measured_trace_gantt(tmp_path):
+    """Real-trace Gantt: the executed iteration's CUDA-event
+    trace drawn under the estimate; same lanes, one rectangle per event."""
+    import xml.etree.ElementTree as ET
+    from paper_2202_01306_b200.gantt import render_comparison, render_gantt
+    from paper_2202_01306_b200.runtime import HarmonyRuntime
+    spec = GPT_PRESETS["tiny"]
+    prof = gpt_profiles(spec)
+    mach = H.MachineModel(gpu_count=1, gpu_mem_capacity=4 << 30, pcie_bandwidth=55_000_000_000)
+    packs = ((0, 1), (2, 3))
+    g = H.generate_task_graph(H.Configuration(4, packs, 4, packs, 16, H.Mode.PP), mach, prof)
+    rt = HarmonyRuntime(spec, alpha_bytes=4 << 30)
+    rt.init_weights(0)
+    rt.load(g, mach, prof)
+    tok, lab = synthetic_batch(spec, 16)
+    for _ in range(2):
+        rt.step(tok, lab)
+    rep = rt.report()
+    sim = H.simulate(g, mach, prof)
+    rt.close()
+    assert {(e.task, e.label) for e in rep.trace} == {(e.task, e.label) for e in sim.trace}
+    assert all(e.end_ns >= e.start_ns >= 0 for e in rep.trace)
+    svg = render_comparison(sim, rep, title="tiny c1")
+    root = ET.fromstring(svg)
+    n_rect = sum(1 for e in root.iter() if e.tag.endswith("rect"))
+    lanes = len({e.resource for e in sim.trace}) + len({e.resource for e in rep.trace})
+    assert n_rect == lanes + len(sim.trace) + len(rep.trace)
+    (tmp_path / "tiny_gantt.svg").write_text(svg)
+    print(render_gantt(rep, width=100))
