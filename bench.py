@@ -49,6 +49,12 @@ WORKLOADS = {
     # north-star target shape: W + Adam state (184 GB) > one GPU's HBM
     "gpt-15b-dp": ("gpt-15b", 24, 4, 3, 170, "dp"),
     "gpt-15b-dp-bf16w": ("gpt-15b", 24, 4, 3, 170, "dp", "bf16"),  # 8f4b fast mode (not the reference ledger)
+    # SURVEY 8f row-4 fast mode (NOT the reference ledger at N > 1): one shared host arena,
+    # gradients reduce-scattered, rank g updates / swaps shard g of each pack's K and W --
+    # per GPU 2|W| + 5|W|/N of PCIe instead of 7|W|, one host copy instead of N (so the
+    # >HBM model runs Harmony-DP past N = 1); identical to the replicated run at N = 1
+    "gpt2-xl-dp-shard": ("gpt2-xl", 16, 4, 8, 32, "dp", "fp32", "sharded"),
+    "gpt-15b-dp-shard": ("gpt-15b", 24, 4, 3, 170, "dp", "fp32", "sharded"),
     # config c4: GPT-style 40B (48 x d8192, 64 heads of 128; W + Adam = 474 GB of pinned host
     # state, one shared copy) as Harmony-PP: D = 8 per GPU (64 on 8 B200), packs of 2 layers;
     # skipped with a clear reason when the host cannot pin its state (the precheck)
@@ -190,10 +196,17 @@ def _nccl_busbw(world: int, nbytes: int = 256 << 20) -> float:
     return 2 * (world - 1) / world * nbytes / t / 1e9
 
 
-def _host_precheck(spec, world: int, mode: str, stash_bytes: int) -> str | None:
+def _dp_update(workload: str) -> str:
+    w = WORKLOADS[workload]
+    return w[7] if len(w) > 7 else "replicated"
+
+
+def _host_precheck(spec, world: int, mode: str, stash_bytes: int, dp_update: str = "replicated") -> str | None:
     """Pinned host memory the job needs (per-rank W + K replicas under
-    Harmony-DP, one shared copy under PP) vs what the host has available."""
-    need = spec.total_params() * 12 * (world if mode == "dp" else 1) + stash_bytes
+    Harmony-DP, one shared copy under PP and the sharded DP update) vs what
+    the host has available."""
+    replicas = world if mode == "dp" and dp_update == "replicated" else 1
+    need = spec.total_params() * 12 * replicas + stash_bytes * (world if mode == "dp" else 1)
     avail = 0
     try:
         for ln in open("/proc/meminfo"):
@@ -437,7 +450,9 @@ def _config(workload, spec, mode, lpp, u, alpha_gib, D, world, payload) -> dict:
             "global_batch": D, "seq_len": getattr(spec, "seq_len", None), "parallelism": f"harmony-{mode}{world}",
             "l2": "inputs larger than L2 (W and K stream from host every step)",
             "w_payload": payload if payload == "fp32" else
-            "bf16 planes (SURVEY 8f4b fast mode: forward W rows differ from the reference ledger)"}
+            "bf16 planes (SURVEY 8f4b fast mode: forward W rows differ from the reference ledger)",
+            "dp_update": _dp_update(workload) if _dp_update(workload) == "replicated" else
+            "sharded (SURVEY 8f row-4 fast mode: U rows carry one shard each at N > 1)"}
 
 
 def run_native(args) -> None:
@@ -468,7 +483,8 @@ def run_native(args) -> None:
     machine = gpt_machine(world, alpha_bytes=alpha_gib << 30, pcie_gbs=min(pcie["h2d"], pcie["d2h"]) * 1e9)
     prof = cnn_profiles(spec) if is_cnn else gpt_profiles(spec)
     graph = H.generate_task_graph(cfg, machine, prof)
-    skip = _host_precheck(spec, world, mode, HarmonyRuntime.stash_bytes_for(graph, prof))
+    dp_update = _dp_update(args.workload)
+    skip = _host_precheck(spec, world, mode, HarmonyRuntime.stash_bytes_for(graph, prof), dp_update)
     if skip:
         if rank == 0:
             print(json.dumps({"metric": f"samples/s (Harmony layer-pack training, {spec.name})", "value": None,
@@ -479,14 +495,15 @@ def run_native(args) -> None:
             dist.destroy_process_group()
         return
     payload = (WORKLOADS[args.workload][6:] or ("fp32",))[0]
-    rt = HarmonyRuntime(spec, alpha_bytes=alpha_gib << 30, device=local, w_payload=payload)
-    sim = H.simulate(graph, machine, prof, w_fwd_bytes=rt.w_fwd_bytes())
+    rt = HarmonyRuntime(spec, alpha_bytes=alpha_gib << 30, device=local, w_payload=payload, dp_update=dp_update)
+    sim = H.simulate(graph, machine, prof, w_fwd_bytes=rt.w_fwd_bytes(), dp_update=dp_update)
     # weights drawn on the GPU (seconds, also with 8 ranks initialising at once);
     # the CPU generator is what the parity tests use
     pp_multi = mode == "pp" and world > 1
-    if pp_multi:
-        # Harmony-PP: one pinned host copy of W / K / stash shared by every rank
-        # (rank 0 creates and initialises it); activations move over NVLink
+    shard_multi = mode == "dp" and dp_update == "sharded" and world > 1
+    if pp_multi or shard_multi:
+        # Harmony-PP / sharded DP: one pinned host copy of W / K (/ stash) shared
+        # by every rank (rank 0 creates and initialises it)
         import torch.distributed as dist
         name = [f"hm_bench_{os.getpid()}" if rank == 0 else None]
         dist.broadcast_object_list(name, src=0)
@@ -505,7 +522,7 @@ def run_native(args) -> None:
         dist.broadcast_object_list(obj, src=0)
         rt.init_comm(obj[0], world, rank)
     rt.load(graph, machine, prof, rank=rank)
-    if pp_multi:
+    if pp_multi or shard_multi:  # device counters (and PP activation buffers) of every peer
         blobs = [None] * world
         dist.all_gather_object(blobs, rt.ipc_export())
         for b in blobs:

@@ -81,6 +81,14 @@ typedef struct {
   int64_t p2p_bandwidth;       /* 0 = pcie_bandwidth (reference model)   */
   int64_t update_cpu_rate;
   const int32_t *p2p_group_of; /* [gpu_count] switch-group id per GPU    */
+  /* Harmony-DP fast mode (not the reference ledger): the U
+   * task on GPU g updates only shard g of its pack -- parameters
+   * [g*c, min(P, (g+1)*c)) with c = 64*ceil(P / (64 N)) -- so its K-in,
+   * K-out and W-out rows carry that shard (8, 8 and 4 bytes per parameter)
+   * and its update time scales by the shard's share.  The gradient is
+   * reduce-scattered instead of all-reduced; W and K live in ONE host arena
+   * all ranks share.  0 = the reference (every rank updates a replica). */
+  int32_t dp_sharded_update;
 } hm_machine;
 
 /* Integer profile tables, row-major [layer][u] with u = 0..u_top (u = 0 is

@@ -68,11 +68,12 @@ class GPTOracle:
         return x + a @ p["w_fc2"].t() + p["b_fc2"]
 
     def loss_sum(self, flat, tokens, labels):
-        """Summed token CE of one member (tokens/labels int64 [u, S])."""
+        """Summed token CE of one member (tokens/labels int64 [u, S]).
+        ``flat`` is the flat parameter vector or per-layer view dicts."""
         s = self.spec
         x = None
         for L in range(s.n_layer):
-            p = self._views(flat, L)
+            p = flat[L] if isinstance(flat, list) else self._views(flat, L)
             if L == 0:
                 x = p["wte"][tokens] + p["wpe"][None, :, :]
             x = self._block(p, x)
@@ -87,15 +88,29 @@ class GPTOracle:
         tokens = torch.as_tensor(tokens, dtype=torch.long)
         labels = torch.as_tensor(labels, dtype=torch.long)
         n_tok = tokens.numel()
-        flat = self.w.clone().requires_grad_(True)
+        # one autograd leaf per parameter segment (views of a copy of W): the
+        # backward of a slice of one flat leaf would materialise a zero tensor
+        # of the WHOLE model per segment (minutes per iteration at 1.5 B)
+        base = self.w.clone()
+        leaves = []
+        for L in range(self.spec.n_layer):
+            leaves.append({k: t.requires_grad_(True) for k, t in self._views(base, L).items()})
         total = 0.0
         s0 = 0
         for u in groups:
-            ls = self.loss_sum(flat, tokens[s0:s0 + u], labels[s0:s0 + u])
+            ls = self.loss_sum(leaves, tokens[s0:s0 + u], labels[s0:s0 + u])
             (ls / n_tok).backward()
             total += ls.item()
             s0 += u
-        g = flat.grad
+        g = torch.zeros_like(self.w)
+        for L in range(self.spec.n_layer):
+            o = self.off[L]
+            for name, n in _segments(self.spec, L):
+                t = leaves[L][name]
+                if t.grad is not None:
+                    g[o:o + n] = t.grad.reshape(-1)
+                o += n
+        del leaves, base
         self.t += 1
         # torch.optim.Adam (no weight decay), elementwise over every pack
         self.m.lerp_(g, 1 - self.b1)

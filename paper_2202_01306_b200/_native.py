@@ -34,7 +34,7 @@ class hm_machine(C.Structure):
     _fields_ = [("gpu_count", C.c_int32), ("cpu_offload_update", C.c_int32),
                 ("pcie_bandwidth", C.c_int64), ("root_link_bandwidth", C.c_int64),
                 ("p2p_bandwidth", C.c_int64), ("update_cpu_rate", C.c_int64),
-                ("p2p_group_of", C.POINTER(C.c_int32))]
+                ("p2p_group_of", C.POINTER(C.c_int32)), ("dp_sharded_update", C.c_int32)]
 
 
 class hm_profile(C.Structure):

@@ -11,6 +11,7 @@
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <string>
 #include <vector>
 
 #include "../runtime/common.hpp"
@@ -31,7 +32,7 @@ __global__ void fill_random_bf16(__nv_bfloat16 *p, int64_t n, uint32_t seed) {
   }
 }
 
-static int replay(const int64_t *shape, int reps, cudaStream_t s, double *us) {
+static int replay(const int64_t *shape, int reps, cudaStream_t caller, double *us) {
   const int64_t M = shape[0], N = shape[1], K = shape[2];
   const int a_mn = (int)shape[3], b_mn = (int)shape[4], epi = (int)shape[5], has_bias = (int)shape[6];
   if (M <= 0 || N <= 0 || K <= 0 || reps < 1) return fail(HM_ERR_VALIDATION, "gemm replay: bad shape");
@@ -42,6 +43,12 @@ static int replay(const int64_t *shape, int reps, cudaStream_t s, double *us) {
                         epi == HM_EPI_RESID_RELU_BF16 || epi == HM_EPI_DRELU_BF16 || epi == HM_EPI_ADD_BF16;
   const int64_t set_by = 2 * (a_el + b_el) + d_by + (need_aux ? aux_by : 0);
   const int sets = (int)std::max<int64_t>(1, std::min<int64_t>(8, (256LL << 20) / std::max<int64_t>(set_by, 1) + 1));
+  // a private non-blocking stream: the caller's may be the legacy default
+  // stream, which cannot be captured into a graph
+  (void)caller;
+  cudaStream_t s = nullptr;
+  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(HM_ERR_DEVICE, "gemm replay: stream create");
   std::vector<void *> bufs;
   auto alloc = [&](int64_t bytes) -> void * {
     void *p = nullptr;
@@ -52,6 +59,7 @@ static int replay(const int64_t *shape, int reps, cudaStream_t s, double *us) {
   auto cleanup = [&]() {
     cudaStreamSynchronize(s);
     for (void *p : bufs) cudaFree(p);
+    cudaStreamDestroy(s);
   };
   struct Set { void *a, *b, *d, *aux; };
   std::vector<Set> S(sets);
@@ -83,8 +91,9 @@ static int replay(const int64_t *shape, int reps, cudaStream_t s, double *us) {
   if (rc != HM_OK) return cleanup(), rc;
   cudaGraph_t g = nullptr;
   cudaGraphExec_t ge = nullptr;
-  if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
-    return cleanup(), fail(HM_ERR_DEVICE, "gemm replay: capture");
+  cudaStreamSynchronize(s);
+  cudaError_t be = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+  if (be != cudaSuccess) return cleanup(), fail(HM_ERR_DEVICE, std::string("gemm replay: capture: ") + cudaGetErrorString(be));
   const int64_t launches0 = launch_counter().load();
   for (int r = 0; r < reps && rc == HM_OK; ++r) rc = one(r);
   cudaError_t ce = cudaStreamEndCapture(s, &g);

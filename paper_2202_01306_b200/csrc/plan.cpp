@@ -65,6 +65,21 @@ struct Ctx {
     return s;
   }
   // simulator.py:133-147
+  // sharded Harmony-DP update: (shard params, pack params) of a U task, or {-1, -1}
+  std::pair<int64_t, int64_t> update_shard(const TaskInfo &t) const {
+    if (!m->dp_sharded_update || t.type != HM_TASK_U) return {-1, -1};
+    int64_t P = 0;
+    for (int32_t L = t.lo; L <= t.hi; ++L) {
+      const int64_t w = scalar(p->w, L, "weight size"), k = scalar(p->k, L, "optimizer-state size");
+      if (w % 4 || k != 2 * w)
+        throw Error{HM_ERR_VALIDATION, "sharded update needs fp32 weights and K = 2 W (Adam m, v) for layer " +
+                                           std::to_string(L)};
+      P += w / 4;
+    }
+    int64_t off, len;
+    dp_shard(P, N, t.dev_id, &off, &len);
+    return {len, P};
+  }
   int64_t compute_ns(const TaskInfo &t, int32_t u) const {
     if (t.type == HM_TASK_F) return pack_time(p->t_f, t.lo, t.hi, u, "time F");
     if (t.type == HM_TASK_B) {
@@ -78,6 +93,8 @@ struct Ctx {
     } else {
       for (int32_t L = t.lo; L <= t.hi; ++L) d += table(p->t_u, L, 1, "time U");
     }
+    const auto sh = update_shard(t);
+    if (sh.second > 0) d = d * sh.first / sh.second;  // the shard's share of the pack
     return d;
   }
   int32_t res(int32_t kind, int32_t gpu) const { return kind * N + gpu; }
@@ -241,6 +258,10 @@ struct Builder {
           task_inputs.push_back(it);
         }
       }
+      const auto shard = c.update_shard(t);  // sharded DP update: this GPU's K shard only
+      if (shard.second >= 0)
+        for (auto &kv : swap_bytes)
+          if (kv.first == HM_K) kv.second = 8 * shard.first;
       // task-level swap-ins sorted by tensor name (simulator.py:251-260)
       std::stable_sort(swap_bytes.begin(), swap_bytes.end(), [](auto &a, auto &b) {
         return std::strcmp(kTensorName[a.first], kTensorName[b.first]) < 0;
@@ -308,6 +329,11 @@ struct Builder {
           else f->second += b;
         }
       }
+      if (shard.second >= 0)
+        for (auto &kv : swap_out) {
+          if (kv.first == HM_K) kv.second = 8 * shard.first;
+          if (kv.first == HM_W) kv.second = 4 * shard.first;
+        }
       std::stable_sort(swap_out.begin(), swap_out.end(), [](auto &a, auto &b) {
         return std::strcmp(kTensorName[a.first], kTensorName[b.first]) < 0;
       });
@@ -331,6 +357,7 @@ Plan *build_plan(const hm_task *tasks, int32_t n_tasks, const int32_t *groups,
     throw Error{HM_ERR_VALIDATION, "bandwidths must be positive"};
   Plan *plan = new Plan();
   plan->gpu_count = machine->gpu_count;
+  plan->dp_sharded = machine->dp_sharded_update != 0;
   try {
     plan->tasks.resize(n_tasks);
     for (int32_t i = 0; i < n_tasks; ++i) {

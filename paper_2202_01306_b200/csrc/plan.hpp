@@ -7,6 +7,7 @@
 // order of the dependency DAG: the executor enqueues them in that order.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -34,8 +35,19 @@ struct TaskInfo {
   std::vector<hm_entry> inputs, outputs;
 };
 
+// Harmony-DP sharded update (hm_machine.dp_sharded_update): GPU g's shard of
+// a pack with `params` parameters, in parameters.  Shards are 64-parameter
+// aligned (256-B device / host offsets); trailing ranks may get none.
+inline int64_t dp_shard_chunk(int64_t params, int32_t n) { return (params + 64 * (int64_t)n - 1) / (64 * (int64_t)n) * 64; }
+inline void dp_shard(int64_t params, int32_t n, int32_t g, int64_t *off, int64_t *len) {
+  const int64_t c = dp_shard_chunk(params, n);
+  *off = std::min<int64_t>((int64_t)g * c, params);
+  *len = std::min<int64_t>(c, params - *off);
+}
+
 struct Plan {
   int32_t gpu_count = 1;
+  bool dp_sharded = false;  // built with hm_machine.dp_sharded_update
   std::vector<TaskInfo> tasks;
   std::vector<Item> items;
   std::vector<std::vector<int32_t>> member_computes;  // per task

@@ -2,7 +2,8 @@
 //
 // The library links no NCCL so it loads on hosts without one; Harmony-DP
 // opens the libnccl.so.2 torch already ships (path passed from Python) and
-// uses only the stable core API (unique id, comm init, all-reduce).
+// uses only the stable core API (unique id, comm init, all-reduce,
+// reduce-scatter).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -19,6 +20,8 @@ struct Nccl {
   ncclResult_t (*comm_init_rank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*all_reduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                              cudaStream_t) = nullptr;
+  ncclResult_t (*reduce_scatter)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                 cudaStream_t) = nullptr;
   ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
   const char *(*error_string)(ncclResult_t) = nullptr;
 
@@ -32,9 +35,10 @@ struct Nccl {
     get_unique_id = reinterpret_cast<decltype(get_unique_id)>(dlsym(handle, "ncclGetUniqueId"));
     comm_init_rank = reinterpret_cast<decltype(comm_init_rank)>(dlsym(handle, "ncclCommInitRank"));
     all_reduce = reinterpret_cast<decltype(all_reduce)>(dlsym(handle, "ncclAllReduce"));
+    reduce_scatter = reinterpret_cast<decltype(reduce_scatter)>(dlsym(handle, "ncclReduceScatter"));
     comm_destroy = reinterpret_cast<decltype(comm_destroy)>(dlsym(handle, "ncclCommDestroy"));
     error_string = reinterpret_cast<decltype(error_string)>(dlsym(handle, "ncclGetErrorString"));
-    if (!get_unique_id || !comm_init_rank || !all_reduce || !comm_destroy || !error_string) {
+    if (!get_unique_id || !comm_init_rank || !all_reduce || !reduce_scatter || !comm_destroy || !error_string) {
       err = "NCCL symbols missing";
       return false;
     }

@@ -90,6 +90,9 @@ struct TaskRt {
   bool from_shared = false;           // B task reading the shared store
   int64_t params = 0;                 // pack parameter count
   int b_task = -1;                    // U: its B task
+  // U under the sharded Harmony-DP update: this rank's shard of the pack
+  // (parameters [sh_off, sh_off + sh_len)) and the reduce-scatter chunk
+  int64_t sh_off = 0, sh_len = -1, sh_chunk = 0;
   std::vector<int> members;           // member compute item ids
   std::vector<int64_t> s0;            // member sample offsets
   std::set<int> stash_heads;          // F: layers whose input is stashed
@@ -116,6 +119,7 @@ struct Action {
   std::vector<std::pair<int, int>> rwaits;  // (item on another rank, iteration lag 0/1): signal waits
   cudaEvent_t done = nullptr;               // kind 5: all-reduce completion
   int64_t count = 0;                        // kind 5: floats reduced
+  int pack_lo = -1, pack_ord = -1;          // kind 5: the pack (first layer) and its rank among my U tasks
   struct Seg { void *dst; const void *src; int64_t bytes; };
   std::vector<Seg> segs;                    // kind 2/3: several copies behind one ledger row
 };
@@ -219,6 +223,10 @@ struct hm_runtime {
   int64_t psa_n = 0, psb_n = 0, pc32_n = 0;
   uint8_t *stash_host = nullptr;
   int64_t stash_host_bytes = 0;
+  // sharded Harmony-DP: each rank stashes its OWN samples, so its stash stays
+  // private even though W / K live in the shared arena
+  uint8_t *stash_priv = nullptr;
+  int64_t stash_priv_bytes = 0;
   // plan
   hm::Plan *plan = nullptr;
   int rank = 0;
@@ -268,7 +276,13 @@ struct hm_runtime {
   // device-side counters.  The multi-GPU path is NCCL.
   bool ipc_reduce = false;
   float *ar_tmp = nullptr;
-  std::map<int, int64_t> dw_off;                   // my U task -> pool offset of its gradient (dW slot)
+  // sharded Harmony-DP update (hm_machine.dp_sharded_update): gradients are
+  // reduce-scattered, rank g updates shard g of each pack in the ONE shared
+  // host arena; the next iteration's W swap-ins wait for every rank's W-out
+  bool dp_shard = false;
+  // the IPC gradient sum pairs the ranks' buffers by PACK (task indices differ
+  // between Harmony-DP ranks): first layer -> pool offset of its gradient
+  std::map<int, int64_t> dw_off;
   std::vector<std::map<int, int64_t>> peer_dw_off;  // per peer
   // Harmony-PP across processes
   bool p2p_mode = false;
@@ -986,14 +1000,33 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
   if (rt.p2p_mode && !rt.shared_arena)
     return fail(HM_ERR_VALIDATION,
                 "peer-to-peer hand-offs (Harmony-PP, N>1) need shared host arenas: call hm_runtime_share_arenas");
+  rt.dp_shard = plan->dp_sharded && plan->gpu_count > 1;  // (one rank: the shard is the whole pack)
+  if (rt.dp_shard) {
+    if (!rt.shared_arena)
+      return fail(HM_ERR_VALIDATION, "the sharded Harmony-DP update needs one host arena shared by all ranks "
+                                     "(hm_runtime_share_arenas)");
+    if (rt.w_planar) return fail(HM_ERR_VALIDATION, "the sharded update and bf16 swap payloads are exclusive");
+    if (!(rt.comm || rt.ipc_reduce) || rt.nranks != plan->gpu_count)
+      return fail(HM_ERR_VALIDATION, "the sharded update needs the job's gradient communicator over all " +
+                                         std::to_string(plan->gpu_count) + " ranks (init_comm / init_ipc_reduce "
+                                         "before load)");
+  }
   int last_f = -1, shared_b = -1;
   int64_t u_max = 1, pmax = 0, f32max = 0;
+  int64_t kmax = 0, dwmax = 0;  // K slot / dW slot parameters (the sharded update shrinks K, pads dW)
   std::vector<int> heads;  // stash head layers produced here
   for (int ti : mine) {
     TaskInfo &t = plan->tasks[ti];
     TaskRt &tr = rt.trt[ti];
     tr.params = rt.w_off[t.hi + 1] - rt.w_off[t.lo];
     pmax = std::max(pmax, tr.params);
+    kmax = std::max(kmax, tr.params);
+    dwmax = std::max(dwmax, tr.params);
+    if (t.type == HM_TASK_U && rt.dp_shard) {
+      dp_shard(tr.params, plan->gpu_count, rank, &tr.sh_off, &tr.sh_len);
+      tr.sh_chunk = dp_shard_chunk(tr.params, plan->gpu_count);
+      dwmax = std::max(dwmax, tr.sh_chunk * plan->gpu_count);  // reduce-scatter send buffer
+    }
     if (rt.w_planar && t.type == HM_TASK_F) {
       int64_t f = 0;
       for (int L = t.lo; L <= t.hi; ++L) f += rt.lay[L].f32n;
@@ -1154,8 +1187,13 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
     req.push_back({(void **)&rt.slots.wsh[i], rt.precise ? 256 : pmax * 2});
     if (rt.w_planar) req.push_back({(void **)&rt.slots.wlo[i], std::max<int64_t>(f32max * 2, 256)});
   }
-  for (int i = 0; i < NDW; ++i) req.push_back({(void **)&rt.slots.dw[i], pmax * 4});
-  for (int i = 0; i < NK; ++i) req.push_back({(void **)&rt.slots.k[i], pmax * 8});
+  if (rt.dp_shard) {  // K slots hold one shard
+    kmax = 0;
+    for (int ti : mine)
+      if (plan->tasks[ti].type == HM_TASK_U) kmax = std::max(kmax, rt.trt[ti].sh_chunk);
+  }
+  for (int i = 0; i < NDW; ++i) req.push_back({(void **)&rt.slots.dw[i], dwmax * 4});
+  for (int i = 0; i < NK; ++i) req.push_back({(void **)&rt.slots.k[i], std::max<int64_t>(kmax * 8, 256)});
   for (int i = 0; i < NST; ++i) req.push_back({(void **)&rt.slots.stash_in[i], std::max<int64_t>(stash_in_max, 256)});
   for (int i = 0; i < 2; ++i) {
     req.push_back({(void **)&rt.carry[i], carry_bytes});
@@ -1286,12 +1324,22 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
     rt.stash_host_off[kv.first] = sh;
     sh += align_up(kv.second, 4096);
   }
-  if (sh > rt.stash_host_bytes) {
+  uint8_t *stash_base = rt.stash_host;
+  if (rt.dp_shard) {
+    if (sh > rt.stash_priv_bytes) {
+      if (rt.stash_priv) cudaFreeHost(rt.stash_priv);
+      rt.stash_priv = nullptr;
+      HM_CUDA(cudaHostAlloc(&rt.stash_priv, std::max<int64_t>(sh, 4096), cudaHostAllocDefault));
+      rt.stash_priv_bytes = sh;
+    }
+    stash_base = rt.stash_priv;
+  } else if (sh > rt.stash_host_bytes) {
     if (rt.shared_arena) return fail(HM_ERR_VALIDATION, "shared stash arena too small: need " + std::to_string(sh));
     if (rt.stash_host) cudaFreeHost(rt.stash_host);
     rt.stash_host = nullptr;
     HM_CUDA(cudaHostAlloc(&rt.stash_host, std::max<int64_t>(sh, 4096), cudaHostAllocDefault));
     rt.stash_host_bytes = sh;
+    stash_base = rt.stash_host;
   }
 
   // ---- actions ----------------------------------------------------------------
@@ -1370,6 +1418,7 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
         k_prev[tr.k_slot] = ti;
       }
     }
+  int u_ord = 0;  // my U tasks in plan order (the same sequence on every DP rank)
   for (size_t i = 0; i < plan->items.size(); ++i) {
     const hm_item &r = plan->items[i].rec;
     if (r.gpu != rank) continue;
@@ -1395,8 +1444,10 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
           TaskRt &bt = rt.trt[tr.b_task];
           ar.waits.push_back({bt.members.back(), false});
           ar.dst = rt.slots.dw[bt.dw_slot];
-          ar.count = tr.params;
-          rt.dw_off[r.task] = reinterpret_cast<uint8_t *>(ar.dst) - rt.pool;
+          ar.count = rt.dp_shard ? tr.sh_chunk : tr.params;  // reduce-scatter: per-rank receive count
+          ar.pack_lo = t.lo;
+          ar.pack_ord = u_ord++;
+          rt.dw_off[t.lo] = reinterpret_cast<uint8_t *>(ar.dst) - rt.pool;
           cudaEvent_t e;
           HM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
           rt.ar_events.push_back(e);
@@ -1444,9 +1495,10 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
         if (r.nbytes != tr.params * 4) return fail(HM_ERR_INTERNAL, "W swap-in size disagrees with the model layout");
         if (w_wait.count(r.task)) a.waits.push_back({w_wait[r.task], false});
       } else if (r.channel == HM_CPU_GPU_SWAP && r.tensor == HM_K) {
-        a.src = rt.k_host + 2 * rt.w_off[t.lo];
+        const int64_t off = rt.dp_shard ? tr.sh_off : 0, len = rt.dp_shard ? tr.sh_len : tr.params;
+        a.src = rt.k_host + 2 * (rt.w_off[t.lo] + off);
         a.dst = rt.slots.k[tr.k_slot];
-        if (r.nbytes != tr.params * 8) return fail(HM_ERR_INTERNAL, "K swap-in size disagrees with the model layout");
+        if (r.nbytes != len * 8) return fail(HM_ERR_INTERNAL, "K swap-in size disagrees with the model layout");
         if (k_wait.count(r.task)) a.waits.push_back({k_wait[r.task], false});
       } else if (r.channel == HM_PEER2PEER) {
         // pull the producer's output over NVLink into this task's receive buffer
@@ -1463,7 +1515,7 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
         a.peer_off = off;
       } else if (r.channel == HM_MESSAGE_PASSING && r.tensor == HM_SX) {
         if (!rt.stash_host_off.count(r.layer)) return fail(HM_ERR_INTERNAL, "stash-in of an unknown head");
-        a.src = rt.stash_host + rt.stash_host_off[r.layer];
+        a.src = stash_base + rt.stash_host_off[r.layer];
         a.dst = rt.slots.stash_in[tr.stash_slot];
         if (r.nbytes != stash_bytes[r.layer]) return fail(HM_ERR_INTERNAL, "stash-in size disagrees with x(L)");
         if (st_wait.count(r.task)) a.waits.push_back({st_wait[r.task], false});
@@ -1477,16 +1529,20 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
       if (r.channel == HM_CPU_GPU_SWAP && r.tensor == HM_W) {
         TaskRt &bt = rt.trt[tr.b_task];
         // bf16 payloads: the U task left the [hi | lo] planes of each layer in the dW slot
-        a.src = rt.w_planar ? static_cast<const void *>(rt.slots.dw[bt.dw_slot]) : rt.slots.w[bt.w_slot];
-        a.dst = rt.w_host + rt.w_off[t.lo];
+        const int64_t off = rt.dp_shard ? tr.sh_off : 0, len = rt.dp_shard ? tr.sh_len : tr.params;
+        a.src = rt.w_planar ? static_cast<const void *>(rt.slots.dw[bt.dw_slot]) : rt.slots.w[bt.w_slot] + off;
+        a.dst = rt.w_host + rt.w_off[t.lo] + off;
+        if (!rt.w_planar && r.nbytes != len * 4) return fail(HM_ERR_INTERNAL, "W swap-out size disagrees with the model layout");
       } else if (r.channel == HM_CPU_GPU_SWAP && r.tensor == HM_K) {
+        const int64_t off = rt.dp_shard ? tr.sh_off : 0, len = rt.dp_shard ? tr.sh_len : tr.params;
         a.src = rt.slots.k[tr.k_slot];
-        a.dst = rt.k_host + 2 * rt.w_off[t.lo];
+        a.dst = rt.k_host + 2 * (rt.w_off[t.lo] + off);
+        if (r.nbytes != len * 8) return fail(HM_ERR_INTERNAL, "K swap-out size disagrees with the model layout");
       } else if (r.channel == HM_MESSAGE_PASSING && r.tensor == HM_SX) {
         const int64_t per = bnd(rt, r.layer);
         const int64_t boff = tr.s0[r.member] * per;
         a.src = rt.stash_dev.at(r.layer) + boff;
-        a.dst = rt.stash_host + rt.stash_host_off[r.layer] + boff;
+        a.dst = stash_base + rt.stash_host_off[r.layer] + boff;
         if (r.nbytes != (int64_t)t.group[r.member] * per) return fail(HM_ERR_INTERNAL, "stash-out size disagrees");
       } else {
         return fail(HM_ERR_VALIDATION, "unsupported output transfer in plan");
@@ -1523,6 +1579,10 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
   auto xdep_host = [&](Action &a, int item) {
     if (plan->items[item].rec.gpu == rank || rt.shared_arena) xdep(a, item);
   };
+  // sharded update: each rank's K shard and its stash are its own regions
+  auto xdep_k = [&](Action &a, int item) {
+    if (plan->items[item].rec.gpu == rank || !rt.dp_shard) xdep_host(a, item);
+  };
   for (auto &a : rt.actions) {
     if (a.item < 0) continue;
     const hm_item &r = plan->items[a.item].rec;
@@ -1531,10 +1591,10 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
         if (overlaps(plan->items[o].rec.task, r.task)) xdep_host(a, o);
     if (a.kind == 2 && r.tensor == HM_K)
       for (int o : k_out)
-        if (overlaps(plan->items[o].rec.task, r.task)) xdep_host(a, o);
+        if (overlaps(plan->items[o].rec.task, r.task)) xdep_k(a, o);
     if (a.kind == 3 && r.tensor == HM_SX)  // host stash region still read by last iteration's stash-in
       for (int o : sx_in)
-        if (plan->items[o].rec.layer == r.layer) xdep_host(a, o);
+        if (plan->items[o].rec.layer == r.layer) xdep_k(a, o);
     if (a.kind == 0 && plan->tasks[r.task].type == HM_TASK_F)
       for (int L : rt.trt[r.task].stash_heads) {
         auto it = sx_out.find({L, r.member});
@@ -1603,7 +1663,9 @@ static void unload_plan(hm_runtime &rt) {
 static int ipc_grad_sum(hm_runtime &rt, const Action &a) {
   if (!memops().wait || !memops().write) return fail(HM_ERR_DEVICE, "stream memory operations unavailable");
   if (rt.nranks > 8) return fail(HM_ERR_VALIDATION, "IPC gradient sum: at most 8 ranks");
-  const int64_t base = (int64_t)rt.plan->items.size() + 2 * (int64_t)a.task;
+  // (ready, read) counters of this pack: indexed by its rank among the U
+  // tasks, which is the same on every Harmony-DP rank
+  const int64_t base = (int64_t)rt.plan->items.size() + 2 * (int64_t)a.pack_ord;
   auto counter = [&](int rank, int64_t idx) -> CUdeviceptr {
     return reinterpret_cast<CUdeviceptr>(rt.peer_pool[rank] + rt.peer_sig_off[rank]) + 4 * (CUdeviceptr)idx;
   };
@@ -1615,7 +1677,7 @@ static int ipc_grad_sum(hm_runtime &rt, const Action &a) {
       src[p] = static_cast<const float *>(a.dst);
       continue;
     }
-    auto it = rt.peer_dw_off[p].find(a.task);
+    auto it = rt.peer_dw_off[p].find(a.pack_lo);
     if (it == rt.peer_dw_off[p].end()) return fail(HM_ERR_INTERNAL, "peer exported no gradient buffer for this pack");
     src[p] = reinterpret_cast<const float *>(rt.peer_pool[p] + it->second);
   }
@@ -1631,12 +1693,20 @@ static int ipc_grad_sum(hm_runtime &rt, const Action &a) {
         return fail(HM_ERR_DEVICE, "cuStreamWaitValue32 failed");
     return HM_OK;
   };
+  // sharded update: only this rank's shard of the sum is needed
+  int64_t off = 0, len = a.count;
+  if (rt.dp_shard) {
+    off = rt.trt[a.task].sh_off;
+    len = rt.trt[a.task].sh_len;
+    for (int p = 0; p < rt.nranks; ++p) src[p] += off;
+  }
   HM_TRY(publish(base));
   HM_TRY(await_all(base));
-  HM_TRY(layers::sum_ranks(src, rt.nranks, rt.ar_tmp, a.count, a.stream));
+  if (len > 0) HM_TRY(layers::sum_ranks(src, rt.nranks, rt.ar_tmp, len, a.stream));
   HM_TRY(publish(base + 1));
   HM_TRY(await_all(base + 1));
-  HM_CUDA(cudaMemcpyAsync(a.dst, rt.ar_tmp, a.count * 4, cudaMemcpyDeviceToDevice, a.stream));
+  if (len > 0)
+    HM_CUDA(cudaMemcpyAsync(static_cast<float *>(a.dst) + off, rt.ar_tmp, len * 4, cudaMemcpyDeviceToDevice, a.stream));
   return HM_OK;
 }
 
@@ -1700,12 +1770,17 @@ static int enqueue_body(hm_runtime &rt, bool capture, bool pipelined, int64_t &h
     if (a.kind == 5) {
       if (rt.ipc_reduce) {
         HM_TRY(ipc_grad_sum(rt, a));
+      } else if (rt.dp_shard) {  // in place: rank g receives the sum of chunk g
+        float *buf = static_cast<float *>(a.dst);
+        ncclResult_t nr = nccl().reduce_scatter(buf, buf + (int64_t)rt.rank * a.count, (size_t)a.count, ncclFloat32,
+                                                ncclSum, rt.comm, a.stream);
+        if (nr != ncclSuccess) return fail(HM_ERR_DEVICE, std::string("ncclReduceScatter: ") + nccl().error_string(nr));
       } else {
         ncclResult_t nr = nccl().all_reduce(a.dst, a.dst, (size_t)a.count, ncclFloat32, ncclSum, rt.comm, a.stream);
         if (nr != ncclSuccess) return fail(HM_ERR_DEVICE, std::string("ncclAllReduce: ") + nccl().error_string(nr));
       }
       HM_CUDA(cudaEventRecord(a.done, a.stream));
-      coll += 2 * (rt.nranks - 1) * a.count * 4 / rt.nranks;
+      coll += rt.dp_shard ? (rt.nranks - 1) * a.count * 4 : 2 * (rt.nranks - 1) * a.count * 4 / rt.nranks;
       continue;
     }
     HM_CUDA(cudaEventRecord(rt.ev_start[a.item], a.stream));
@@ -1717,7 +1792,12 @@ static int enqueue_body(hm_runtime &rt, bool capture, bool pipelined, int64_t &h
       case 1: {
         TaskRt &tr = rt.trt[a.task];
         TaskRt &bt = rt.trt[tr.b_task];
-        if (capture)  // step-dependent scalars read from device memory at replay
+        if (rt.dp_shard) {  // this rank's shard only (K slot holds just the shard)
+          if (tr.sh_len > 0)
+            HM_TRY(adam_launch(rt.slots.w[bt.w_slot] + tr.sh_off, rt.slots.dw[bt.dw_slot] + tr.sh_off,
+                               rt.slots.k[tr.k_slot], tr.sh_len, rt.m.lr, rt.m.beta1, rt.m.beta2, rt.m.eps, rt.step,
+                               1.0f, a.stream));
+        } else if (capture)  // step-dependent scalars read from device memory at replay
           HM_TRY(adam_launch_dev(rt.slots.w[bt.w_slot], rt.slots.dw[bt.dw_slot], rt.slots.k[tr.k_slot], tr.params,
                                  rt.m.beta1, rt.m.beta2, rt.m.eps, rt.adam_dev, 1.0f, a.stream));
         else
@@ -1756,7 +1836,9 @@ static int enqueue_body(hm_runtime &rt, bool capture, bool pipelined, int64_t &h
         return fail(HM_ERR_INTERNAL, "bad action");
     }
     HM_CUDA(cudaEventRecord(rt.ev_end[a.item], a.stream));
-    if (rt.p2p_mode) {  // publish completion of this item for the peers (value = iteration)
+    // publish completion of this item for the peers (value = iteration): every
+    // item under Harmony-PP, the W swap-outs under the sharded DP update
+    if (rt.p2p_mode || (rt.dp_shard && a.kind == 3 && rt.plan->items[a.item].rec.tensor == HM_W)) {
       if (!memops().write) return fail(HM_ERR_DEVICE, "cuStreamWriteValue32 unavailable");
       if (memops().write(a.stream, reinterpret_cast<CUdeviceptr>(rt.sig) + 4 * (CUdeviceptr)a.item,
                          (cuuint32_t)rt.step, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
@@ -1788,7 +1870,7 @@ static int run_iteration(hm_runtime &rt, const int32_t *tokens, const int32_t *l
   HM_CUDA(cudaMemcpyAsync(rt.labels, labels, lb, is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, sc));
   int64_t h2d = 0, d2h = 0, coll = 0;
   const int gi = rt.profiling ? 1 : 0;
-  const bool use_graph = rt.use_graph && !rt.p2p_mode && !rt.ipc_reduce && rt.iterations >= 1;
+  const bool use_graph = rt.use_graph && !rt.p2p_mode && !rt.ipc_reduce && !rt.dp_shard && rt.iterations >= 1;
   if (use_graph) {
     if (!rt.graph_exec[gi]) {
       // record the iteration once (with or without per-kernel timing events)
@@ -2499,6 +2581,7 @@ void hm_runtime_free(hm_runtime *rt) {
     hm::numa_pinned_free(rt->k_host, rt->k_map_bytes);
     if (rt->stash_host) cudaFreeHost(rt->stash_host);
   }
+  if (rt->stash_priv) cudaFreeHost(rt->stash_priv);
   cudaStream_t ss[] = {rt->s_compute, rt->s_h2d, rt->s_d2h, rt->s_update, rt->s_p2p_in, rt->s_p2p_out, rt->s_comm};
   for (auto s : ss) if (s) cudaStreamDestroy(s);
   delete rt;

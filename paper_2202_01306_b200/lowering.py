@@ -14,7 +14,7 @@ import numpy as np
 
 from . import _native as N
 from .core import MachineModel, TensorKind
-from .errors import MissingProfileError
+from .errors import MissingProfileError, ValidationError
 from .profiler import ProfileSet
 from .taskgraph import ChannelKind, TaskGraph, TaskType
 
@@ -47,9 +47,17 @@ class NativePlan:
     """Owns an ``hm_plan*`` and the ctypes tables it was built from."""
 
     def __init__(self, graph: TaskGraph, machine: MachineModel, profiles: ProfileSet,
-                 need_time: bool = True, w_fwd_bytes=None) -> None:
+                 need_time: bool = True, w_fwd_bytes=None, dp_update: str = "replicated") -> None:
         """``w_fwd_bytes``: per-layer W bytes a forward task moves, for the
-        runtime's bf16 swap-payload mode (None = the reference's W bytes)."""
+        runtime's bf16 swap-payload mode (None = the reference's W bytes).
+        ``dp_update``: "replicated" (the reference: every Harmony-DP rank
+        updates its own replica) or "sharded" (hm_machine.dp_sharded_update:
+        rank g updates shard g of each pack; fast mode, not the reference
+        ledger at N > 1)."""
+        if dp_update not in ("replicated", "sharded"):
+            raise ValidationError(f"dp_update must be 'replicated' or 'sharded' (got {dp_update!r})")
+        if dp_update == "sharded" and graph.mode.value != "dp":
+            raise ValidationError("the sharded update applies to Harmony-DP graphs only")
         lib = N.lib()
         self.graph = graph
         self.machine = machine
@@ -97,7 +105,8 @@ class NativePlan:
         self._machine = N.hm_machine(machine.gpu_count, 1 if machine.cpu_offload_update else 0,
                                      machine.pcie_bandwidth, machine.root_link_bandwidth,
                                      machine.p2p_bandwidth, machine.update_cpu_rate,
-                                     C.cast(self._group_of, C.POINTER(C.c_int32)))
+                                     C.cast(self._group_of, C.POINTER(C.c_int32)),
+                                     1 if dp_update == "sharded" else 0)
         layers = max(layers_needed, 1)
         tab = profiles.tables(layers, u_top, need_time=need_time)
         self._tab = {}

@@ -33,7 +33,7 @@ class HarmonyRuntime:
 
     def __init__(self, spec: GPTSpec | CNNSpec, *, alpha_bytes: int, device: int = 0, lr: float = 1e-4,
                  betas: tuple[float, float] = (0.9, 0.999), eps: float = 1e-8, w_payload: str = "fp32",
-                 math: str = "bf16") -> None:
+                 math: str = "bf16", dp_update: str = "replicated") -> None:
         """``w_payload``: "fp32" swaps fp32 W exactly as the reference's ledger
         bills it; "bf16" is the SURVEY 8f4b fast mode (transformer family): the
         host W arena holds each layer as [bf16 hi plane | 16-bit lo plane], an
@@ -46,7 +46,22 @@ class HarmonyRuntime:
         (the throughput mode); "fp32" = the parity mode (transformer family):
         fp32 activations, GEMMs as three-plane bf16 split products on the same
         tcgen05 kernel, fp32 attention (DESIGN.md section 6 states both
-        modes' tolerances).  The swap plan and ledger are the same."""
+        modes' tolerances).  The swap plan and ledger are the same.
+
+        ``dp_update`` (Harmony-DP only): "replicated" is the reference -- every
+        rank keeps its own host replica of W and K and updates every pack;
+        "sharded" is the SURVEY 8f row-4 fast mode -- one host arena shared by
+        all ranks (``share_arenas``), gradients reduce-scattered, rank g
+        updates, swaps in and swaps out only shard g of each pack's K and W
+        (hm_machine.dp_sharded_update states the split).  Per GPU that moves
+        2|W| + 5|W|/N instead of 7|W| (Adam fp32) and holds one host copy
+        instead of N; the U rows of the ledger differ from the reference at
+        N > 1 (flagged; ``simulate(..., dp_update="sharded")`` prices it)."""
+        if dp_update not in ("replicated", "sharded"):
+            raise ValidationError("dp_update must be 'replicated' or 'sharded'")
+        if dp_update == "sharded" and w_payload != "fp32":
+            raise ValidationError("the sharded update and bf16 W payloads are exclusive")
+        self.dp_update = dp_update
         if w_payload not in ("fp32", "bf16"):
             raise ValidationError("w_payload must be 'fp32' or 'bf16'")
         if math not in ("bf16", "fp32"):
@@ -326,7 +341,10 @@ class HarmonyRuntime:
             raise ValidationError("execute needs a scheduler-generated graph")
         if machine.gpu_count != graph.machine.gpu_count:
             raise ValidationError("machine does not match the graph's GPU count")
-        plan = NativePlan(graph, machine, profiles, w_fwd_bytes=self.w_fwd_bytes())
+        dp_update = self.dp_update if graph.mode.value == "dp" else "replicated"
+        if self.dp_update == "sharded" and graph.mode.value != "dp":
+            raise ValidationError("dp_update='sharded' applies to Harmony-DP graphs")
+        plan = NativePlan(graph, machine, profiles, w_fwd_bytes=self.w_fwd_bytes(), dp_update=dp_update)
         if graph.mode.value == "dp":
             samples = gpu_shares(graph.minibatch, machine.gpu_count)[rank]
         else:

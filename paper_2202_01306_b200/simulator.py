@@ -112,18 +112,20 @@ def report_from_items(graph: TaskGraph, machine: MachineModel, items, makespan: 
 
 def simulate(graph: TaskGraph, machine: MachineModel | None = None,
              profiles: ProfileSet | None = None, *, check_memory: bool = False,
-             w_fwd_bytes=None) -> SimReport:
+             w_fwd_bytes=None, dp_update: str = "replicated") -> SimReport:
     """Estimate one training iteration (drop-in for `simulator.simulate`).
     ``w_fwd_bytes`` (extension, default None = the reference): per-layer W
     bytes forward tasks move under the runtime's bf16 swap-payload mode
-    (``HarmonyRuntime.w_fwd_bytes()``)."""
+    (``HarmonyRuntime.w_fwd_bytes()``).  ``dp_update`` (extension, default
+    the reference): "sharded" prices the Harmony-DP sharded update (rank g's
+    U task moves / updates only shard g of the pack's K and W)."""
     machine = machine or graph.machine
     if profiles is None:
         raise ValidationError("profiles are required")
     if machine.gpu_count != graph.machine.gpu_count:
         raise ValidationError("machine does not match the graph's GPU count")
     graph.validate()
-    plan = NativePlan(graph, machine, profiles, w_fwd_bytes=w_fwd_bytes)
+    plan = NativePlan(graph, machine, profiles, w_fwd_bytes=w_fwd_bytes, dp_update=dp_update)
     try:
         if check_memory:
             check_memory_fit(graph, machine, profiles)

@@ -32,7 +32,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, D, math, q):
+def _worker(rank, world, port, D, math, q, update="replicated", shm=""):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -45,8 +45,17 @@ def _worker(rank, world, port, D, math, q):
         packs = ((0, 1), (2, 3))
         g = H.generate_task_graph(H.Configuration(2, packs, 2, packs, D, H.Mode.DP), mach, prof)
         torch.cuda.set_device(0)
-        rt = HarmonyRuntime(spec, alpha_bytes=4 << 30, device=0, math=math)
-        rt.init_weights(0)  # same seed on every rank: identical replicas
+        rt = HarmonyRuntime(spec, alpha_bytes=4 << 30, device=0, math=math, dp_update=update)
+        if update == "sharded":  # one host arena for all ranks (rank 0 creates and initialises it)
+            stash = HarmonyRuntime.stash_bytes_for(g, prof)
+            if rank == 0:
+                rt.share_arenas(shm, True, stash)
+                rt.init_weights(0)
+            dist.barrier()
+            if rank != 0:
+                rt.share_arenas(shm, False, stash)
+        else:
+            rt.init_weights(0)  # same seed on every rank: identical replicas
         w0 = rt.w.copy()
         rt.init_ipc_reduce(world, rank)
         rt.load(g, mach, prof, rank=rank)
@@ -67,21 +76,28 @@ def _worker(rank, world, port, D, math, q):
         gathered = [None] * world
         dist.all_gather_object(gathered, out)
         if rank == 0:
-            q.put({"ranks": gathered, "sim_ledger": H.simulate(g, mach, prof).ledger})
+            q.put({"ranks": gathered, "sim_ledger": H.simulate(g, mach, prof, dp_update=update).ledger,
+                   "ref_ledger": H.simulate(g, mach, prof).ledger})
         dist.barrier()
         rt.close()
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("D,math", [(8, "bf16"), (7, "bf16"), (8, "fp32")])
-def test_dp_two_ranks_one_gpu(D, math):
+@pytest.mark.parametrize("D,math,update", [(8, "bf16", "replicated"), (7, "bf16", "replicated"),
+                                           (8, "fp32", "replicated"), (8, "fp32", "sharded"),
+                                           (7, "bf16", "sharded")])
+def test_dp_two_ranks_one_gpu(D, math, update):
+    """Replicated (the reference) and sharded (SURVEY 8f row 4 fast mode:
+    reduce-scattered gradients, rank g updates shard g of each pack in one
+    shared host arena) Harmony-DP."""
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, D, math, q)) for r in range(2)]
+    shm = f"hm_dp_test_{os.getpid()}_{D}_{math}"
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, D, math, q, update, shm)) for r in range(2)]
     for p in procs:
         p.start()
     res = q.get(timeout=300)
@@ -91,9 +107,21 @@ def test_dp_two_ranks_one_gpu(D, math):
     r0, r1 = sorted(res["ranks"], key=lambda x: x["rank"])
     assert sorted(r0["ledger"] + r1["ledger"]) == sorted(res["sim_ledger"])
     assert r0["nccl_bytes"] > 0
-    # per-rank host replicas: no transfer waits on another rank's counters (the
-    # NCCL path imports no peer pools, so such a wait could never be satisfied)
-    assert r0["rank_waits"] == 0 and r1["rank_waits"] == 0
+    if update == "replicated":
+        # per-rank host replicas: no transfer waits on another rank's counters
+        # (the NCCL path imports no peer pools, so such a wait could never be met)
+        assert r0["rank_waits"] == 0 and r1["rank_waits"] == 0
+    else:
+        # shared arena: W swap-ins wait for every rank's shard W-out of the last
+        # iteration; K and W-out rows carry one shard each, so the union of the
+        # ranks' ledgers moves |K| and |W| once per pack instead of once per rank
+        assert r0["rank_waits"] > 0 and r1["rank_waits"] > 0
+        def vol(led, tensor, stage):
+            return sum(r[6] for r in led if r[3] == tensor and r[1] == stage)
+        union = r0["ledger"] + r1["ledger"]
+        for tensor, stage in (("K", 0), ("K", 2), ("W", 2)):
+            assert 2 * vol(union, tensor, stage) == vol(res["ref_ledger"], tensor, stage)
+        assert vol(union, "W", 0) == vol(res["ref_ledger"], "W", 0)
     # both replicas: the same summed gradient, the same Adam -> the same bits
     assert np.array_equal(r0["w"].view(np.uint32), r1["w"].view(np.uint32))
     assert np.array_equal(r0["k"].view(np.uint32), r1["k"].view(np.uint32))

@@ -146,3 +146,63 @@ def test_errors_are_reference_classes():
         H.Configuration(1, ((0, 1),), 1, ((0, 0), (1, 1)), 2, H.Mode.PP).validate()
     with pytest.raises(H.ValidationError):
         H.MachineModel(gpu_count=0, gpu_mem_capacity=1, pcie_bandwidth=1)
+
+
+# ---- sharded Harmony-DP update (SURVEY 8f row 4 fast mode) -------------------
+def _dp_graph(n, D=16, u=2):
+    import paper_2202_01306_b200 as H
+    from paper_2202_01306_b200.model import GPT_PRESETS, gpt_profiles
+    spec = GPT_PRESETS["tiny"]
+    prof = gpt_profiles(spec)
+    m = H.MachineModel(gpu_count=n, gpu_mem_capacity=4 << 30, pcie_bandwidth=55_000_000_000)
+    packs = ((0, 1), (2, 3))
+    g = H.generate_task_graph(H.Configuration(u, packs, u, packs, D, H.Mode.DP), m, prof)
+    return H, spec, prof, m, g
+
+
+def _vol(ledger, tensor, stage, gpu=None):
+    return sum(r[6] for r in ledger if r[3] == tensor and r[1] == stage and (gpu is None or r[7] == gpu))
+
+
+def test_sharded_update_is_the_reference_at_one_gpu():
+    H, spec, prof, m, g = _dp_graph(1)
+    a = H.simulate(g, m, prof)
+    b = H.simulate(g, m, prof, dp_update="sharded")
+    assert a.ledger == b.ledger and a.makespan_ns == b.makespan_ns
+
+
+@pytest.mark.parametrize("n", [2, 3, 4, 8])
+def test_sharded_update_moves_each_shard_once(n):
+    H, spec, prof, m, g = _dp_graph(n, D=2 * n)
+    ref = H.simulate(g, m, prof)
+    sh = H.simulate(g, m, prof, dp_update="sharded")
+    # K in / out and W out: |K| and |W| once per pack over all ranks (N copies in the reference)
+    for tensor, stage in (("K", 0), ("K", 2), ("W", 2)):
+        assert n * _vol(sh.ledger, tensor, stage) == _vol(ref.ledger, tensor, stage)
+    # the forward / backward W swap-ins are unchanged
+    assert _vol(sh.ledger, "W", 0) == _vol(ref.ledger, "W", 0)
+    # every other row is identical
+    keep = lambda led: sorted(r for r in led if not (r[3] in ("K", "W") and (r[3] == "K" or r[1] == 2)))  # noqa: E731
+    assert keep(sh.ledger) == keep(ref.ledger)
+    # rank g's rows are its 64-parameter-aligned shard of each pack
+    P = [sum(spec.layer_params(L) for L in range(lo, hi + 1)) for lo, hi in ((0, 1), (2, 3))]
+    c = [-(-p // (64 * n)) * 64 for p in P]
+    for gpu in range(n):
+        want = sum(max(0, min(ci, p - gpu * ci)) for p, ci in zip(P, c))
+        assert _vol(sh.ledger, "W", 2, gpu) == 4 * want
+        assert _vol(sh.ledger, "K", 0, gpu) == 8 * want
+    assert sh.makespan_ns < ref.makespan_ns
+
+
+def test_sharded_update_rejects_pp():
+    import paper_2202_01306_b200 as H
+    from paper_2202_01306_b200.errors import ValidationError
+    from paper_2202_01306_b200.model import GPT_PRESETS, gpt_profiles
+    prof = gpt_profiles(GPT_PRESETS["tiny"])
+    m = H.MachineModel(gpu_count=2, gpu_mem_capacity=4 << 30, pcie_bandwidth=55_000_000_000)
+    packs = ((0, 1), (2, 3))
+    g = H.generate_task_graph(H.Configuration(4, packs, 4, packs, 16, H.Mode.PP), m, prof)
+    with pytest.raises(ValidationError):
+        H.simulate(g, m, prof, dp_update="sharded")
+    with pytest.raises(ValidationError):
+        H.simulate(g, m, prof, dp_update="zero")
