@@ -31,14 +31,17 @@ class CNNOracle:
         self.lr, self.b1, self.b2, self.eps = lr, betas[0], betas[1], eps
         self.t = 0
 
-    def _views(self, flat, L):
+    def _raw(self, flat, L):
         out, o = {}, self.off[L]
         for name, shp in self.spec.layer_segments(L):
             n = int(np.prod(shp))
-            t = flat[o:o + n].view(*shp)
-            out[name] = t.permute(0, 3, 1, 2) if len(shp) == 4 else t  # [cout, cin, 3, 3]
+            out[name] = flat[o:o + n].view(*shp)
             o += n
         return out
+
+    def _views(self, flat, L):
+        raw = flat[L] if isinstance(flat, list) else self._raw(flat, L)
+        return {k: t.permute(0, 3, 1, 2) if t.dim() == 4 else t for k, t in raw.items()}  # [cout, cin, 3, 3]
 
     def loss_sum(self, flat, images, labels):
         """Summed cross-entropy of one member: images [u, h, w, c] fp32 NHWC."""
@@ -68,14 +71,26 @@ class CNNOracle:
         images = torch.as_tensor(images).float()
         labels = torch.as_tensor(labels, dtype=torch.long)
         n = labels.numel()
-        flat = self.w.clone().requires_grad_(True)
+        # one autograd leaf per parameter segment (a slice of one flat leaf
+        # would materialise a whole-model zero tensor per segment in backward)
+        base = self.w.clone()
+        leaves = [{k: t.requires_grad_(True) for k, t in self._raw(base, L).items()}
+                  for L in range(len(self.spec.layers))]
         total, s0 = 0.0, 0
         for u in groups:
-            ls = self.loss_sum(flat, images[s0:s0 + u], labels[s0:s0 + u])
+            ls = self.loss_sum(leaves, images[s0:s0 + u], labels[s0:s0 + u])
             (ls / n).backward()
             total += ls.item()
             s0 += u
-        g = flat.grad
+        g = torch.zeros_like(self.w)
+        for L, lv in enumerate(leaves):
+            o = self.off[L]
+            for name, shp in self.spec.layer_segments(L):
+                k = int(np.prod(shp))
+                if lv[name].grad is not None:
+                    g[o:o + k] = lv[name].grad.reshape(-1)
+                o += k
+        del leaves, base
         self.t += 1
         self.m.lerp_(g, 1 - self.b1)
         self.v.mul_(self.b2).addcmul_(g, g, value=1 - self.b2)
