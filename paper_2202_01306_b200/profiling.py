@@ -102,3 +102,49 @@ def profile_gpt(spec: GPTSpec | CNNSpec, u_values=None, u_max: int = 8, stride: 
 
 
 profile_model = profile_gpt  # either family (GPTSpec or CNNSpec)
+
+
+def runtime_mem_oracle(spec: GPTSpec | CNNSpec, packs, alpha_bytes: int, *, minibatch_per_u: int = 1,
+                       device: int = 0, mode: Mode = Mode.DP):
+    """The paper's OOM probe (`PAPER.md:385-394`) on the real runtime: a
+    callable u -> bool that loads the plan of ``packs`` at microbatch u
+    (minibatch = u * ``minibatch_per_u``) into a runtime capped at
+    ``alpha_bytes`` and reports whether it fits.  The runtime sizes every
+    device buffer of the plan (W / dW / K slots, activation stores, scratch,
+    receive buffers) and cudaMallocs them as ONE pool: a plan that does not fit
+    raises CapacityViolationError (or the allocation fails) -- exactly the
+    failure the reference's ``slow_start_max_u`` expects from its oracle
+    (`profiler.py:196-223`).  The returned callable records the pool bytes of
+    every fitting u in ``.device_bytes`` (the measured memory model) and is
+    closed with ``.close()``."""
+    from .errors import CapacityViolationError, DeviceError
+    from .runtime import HarmonyRuntime
+    rt = HarmonyRuntime(spec, alpha_bytes=alpha_bytes, device=device)
+    mach = MachineModel(gpu_count=1, gpu_mem_capacity=alpha_bytes, pcie_bandwidth=55_000_000_000)
+
+    def fits(u: int) -> bool:
+        D = u * minibatch_per_u
+        prof = shape_profiles(spec, u_max=max(64, u))
+        g = generate_task_graph(Configuration(u, packs, u, packs, D, mode), mach, prof)
+        try:
+            rt.load(g, mach, prof)
+        except (CapacityViolationError, DeviceError):
+            return False
+        fits.device_bytes[u] = rt.counters()["device_bytes"]
+        return True
+
+    fits.device_bytes = {}
+    fits.close = rt.close
+    return fits
+
+
+def probe_max_microbatch(spec: GPTSpec | CNNSpec, packs, alpha_bytes: int, u_cap: int = 256, **kw) -> tuple[int, dict]:
+    """Largest microbatch the runtime can execute ``packs`` with under
+    ``alpha_bytes``: the reference's slow-start search driven by the runtime's
+    own admission (``runtime_mem_oracle``).  Returns (u, {u: device bytes})."""
+    from .profiler import slow_start_max_u
+    oracle = runtime_mem_oracle(spec, packs, alpha_bytes, **kw)
+    try:
+        return slow_start_max_u(oracle, u_cap), dict(oracle.device_bytes)
+    finally:
+        oracle.close()

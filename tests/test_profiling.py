@@ -30,3 +30,44 @@ def test_samples_from_synthetic_trace_and_fit():
         assert prof.time_ns("U", L, 1) == 500 + L
         assert prof.w_bytes(L) == 4 * spec.layer_params(L)
         assert prof.x_bytes(L, 2) == gpt_profiles(spec).x_bytes(L, 2)
+
+
+def test_slow_start_with_a_monotone_oracle_matches_scan():
+    """The probe the runtime oracle plugs into (reference `profiler.py:196-223`)."""
+    from paper_2202_01306_b200.profiler import slow_start_max_u
+    for limit in (1, 2, 3, 7, 8, 9, 31, 64, 100):
+        calls = []
+
+        def fits(u, limit=limit):
+            calls.append(u)
+            return u <= limit
+        assert slow_start_max_u(fits, 64) == min(limit, 64)
+
+
+def test_runtime_oom_probe_gpu():
+    """The OOM oracle is the runtime itself: every u the slow-start search
+    accepts loads under alpha, u + 1 does not, and the answer equals a brute
+    scan; the measured pool bytes grow with u (the measured memory model)."""
+    import pytest
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2202_01306_b200.model import GPT_PRESETS
+    from paper_2202_01306_b200.profiling import probe_max_microbatch, runtime_mem_oracle
+    spec = GPT_PRESETS["tiny"]
+    packs = ((0, 1), (2, 3))
+    big = runtime_mem_oracle(spec, packs, 64 << 30)
+    assert big(4) and big(16) and big(17)
+    by = big.device_bytes
+    big.close()
+    assert by[17] > by[16] > by[4]
+    alpha = (by[4] + by[16]) // 2  # the answer lies strictly between 4 and 16
+    u, seen = probe_max_microbatch(spec, packs, alpha, u_cap=64)
+    assert 4 <= u < 16
+    scan = runtime_mem_oracle(spec, packs, alpha)
+    assert [scan(v) for v in range(1, 20)] == [v <= u for v in range(1, 20)]
+    scan.close()
+    assert all(b <= alpha for b in seen.values())
+
+
+test_runtime_oom_probe_gpu = __import__("pytest").mark.gpu(test_runtime_oom_probe_gpu)
