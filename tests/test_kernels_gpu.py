@@ -373,8 +373,8 @@ def test_attention_fwd_every_variant(mode):
     import subprocess
     import sys
     here = __import__("os").path.dirname(__import__("os").path.abspath(__file__))
-    cases = [(2, 128, 4, True), (1, 512, 2, False), (2, 1024, 3, True), (3, 1024, 25, True), (2, 512, 40, False),
-             (1, 256, 25, True)]
+    cases = [(2, 128, 4, True, 64), (1, 512, 2, False, 64), (2, 1024, 3, True, 64), (3, 1024, 25, True, 64),
+             (2, 512, 40, False, 64), (1, 256, 25, True, 64)]
     code = (f"import torch, sys; sys.path.insert(0, {here!r}); sys.path.insert(0, {here + '/..'!r}); "
             "import test_kernels_gpu as T; from paper_2202_01306_b200 import ops; "
             f"[T.test_attention_fwd_tcgen05_matches(ops, *c) for c in {cases!r}]")

@@ -4,7 +4,7 @@ device).  Checks: the union of the ranks' executed ledgers equals the
 planner's ledger (including the peer2peer X / Y / dY rows), and loss and
 weights match the torch-CPU oracle -- for step-by-step and pipelined runs,
 at the tiny c1 shape and at the c4 (GPT-40B) layer shape at reduced depth
-(d=8192, 64 heads of 128, seq 256): loss within 1e-3 at every step, per-layer
+(d=8192, 64 heads of 128, seq 128, 2 steps): loss within 1e-3 at every step, per-layer
 weight deltas / Adam moments within the stated tolerances
 (tests/test_parity_gpu.py)."""
 
@@ -31,7 +31,7 @@ def _port():
 SPECS = {
     "tiny": dict(preset="tiny", lr=1e-4, alpha=4 << 30),
     # the 40B config's layer (805 M parameters, 3.2 GB of fp32 W per layer)
-    "wide": dict(spec=(4, 8192, 64, 256, 1024), lr=1e-5, alpha=48 << 30),
+    "wide": dict(spec=(4, 8192, 64, 128, 1024), lr=1e-5, alpha=48 << 30, steps=2),
 }
 
 
@@ -72,7 +72,7 @@ def _worker(rank, world, port, shm, pipelined, name, q):
             rt.ipc_import(b)
         dist.barrier()
         tok, lab = synthetic_batch(spec, 8)
-        steps = 3
+        steps = SPECS[name].get("steps", 3)
         if pipelined:
             losses, _ = rt.run_steps(steps, tok, lab)
         else:
@@ -133,7 +133,7 @@ def test_pp_two_ranks_one_gpu(name, pipelined):
     spec = _spec(name)
     o = GPTOracle(spec, r0["w0"], res["w_off"], lr=SPECS[name]["lr"])
     tok, lab = synthetic_batch(spec, 8)
-    ref = [o.step(tok, lab, [8]) for _ in range(3)]
+    ref = [o.step(tok, lab, [8]) for _ in range(SPECS[name].get("steps", 3))]
     # the rank running the last forward task owns the loss; the other reports 0
     losses = [max(a, b) for a, b in zip(r0["losses"], r1["losses"])]
     assert min(min(r0["losses"]), min(r1["losses"])) == 0.0
