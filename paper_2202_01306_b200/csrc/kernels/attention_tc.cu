@@ -27,6 +27,11 @@
 #include "sm100.cuh"
 
 namespace hm {
+namespace attn_tc128 {  // attention_tc128.cu
+bool supported(int S, int DH);
+int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causal, cudaStream_t s);
+int forward64(const void *qkv, void *o, float *lse, int B, int S, int H, int causal, cudaStream_t s);
+}  // namespace attn_tc128
 namespace attn_tc {
 
 using namespace sm100;
@@ -1604,6 +1609,9 @@ int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causa
   // persistent pairs
   static const char *mode_env = getenv("HM_ATTN_FWD");
   static const char mode = mode_env ? mode_env[0] : 'd';
+  // t = query-tile pairs with P and O resident in TMEM (attention_tc128.cu's
+  // dataflow at head_dim 64)
+  if (mode == 't') return attn_tc128::forward64(qkv, o, lse, B, S, H, causal, s);
   const bool two_tiles = mode == '2';
   // two query tiles per CTA (ping-pong softmax warpgroups) for full attention:
   // 1.31x at 8 x 512 x 16 heads.
@@ -1681,12 +1689,6 @@ int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causa
 }  // namespace attn_tc
 }  // namespace hm
 
-namespace hm {
-namespace attn_tc128 {
-bool supported(int S, int DH);
-int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causal, cudaStream_t s);
-}  // namespace attn_tc128
-}  // namespace hm
 
 extern "C" int hm_k_attn_fwd_tc(const void *qkv, void *out, float *lse, int32_t batch, int32_t seq, int32_t heads,
                                 int32_t head_dim, int32_t causal, void *stream) {

@@ -58,7 +58,9 @@ constexpr uint32_t kDqStage = SUBQ * DH * 4;  // dQ of one sub-block, fp32 row-m
 constexpr int kThreads = 384;              // TMA, MMA, TMEM-alloc, idle, 2 x 4 softmax warps
 constexpr float kRescaleLog2 = 8.f;        // lazy-rescale threshold (log2 units)
 
-constexpr size_t kFwdSmem = 1024 + 2 * kTile /*Q x2 tiles*/ + 2 * kTile /*K x2*/ + 2 * kTile /*V x2*/ + 256;
+template <int HD>
+constexpr size_t fwd_smem() { return 1024 + 6 * (size_t)HD * 256 /*Q x2 tiles, K x2, V x2*/ + 256; }
+constexpr size_t kFwdSmem = fwd_smem<128>();
 constexpr size_t kBwdSmem = 1024 + 2 * kTile /*K, V*/ + 4 * kSubTile /*Q, dO x2*/ + 2 * kPT /*P^T, dS^T*/ +
                             kDqStage + 2 * 2 * SUBQ * 4 /*lse, D x2*/ + 512;
 static_assert(kFwdSmem <= 232448 && kBwdSmem <= 232448, "shared memory");
@@ -71,18 +73,22 @@ __device__ __forceinline__ float ex2(float x) {
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // ---------------------------------------------------------------------------
-// forward
+// forward (HD = 128; HD = 64 is the same dataflow with one SW128 atom per
+// tile and O in 64 TMEM columns -- selectable for head_dim 64 with
+// HM_ATTN_FWD=t, see attention_tc.cu)
 // ---------------------------------------------------------------------------
-template <bool CAUSAL>
+template <int HD, bool CAUSAL>
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16 *__restrict__ out, float *__restrict__ lse,
                int S, int H, float scale_log2) {
   extern __shared__ uint8_t smem_raw[];
+  constexpr uint32_t TILE = HD * 256;  // 128 rows x HD head dims bf16 (HD / 64 SW128 atoms)
+  constexpr int DH = HD;
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *sQ = smem;              // [2 tiles]
-  uint8_t *sK = sQ + 2 * kTile;    // [2 stages]
-  uint8_t *sV = sK + 2 * kTile;    // [2 stages]
-  uint64_t *bar = reinterpret_cast<uint64_t *>(sV + 2 * kTile);
+  uint8_t *sK = sQ + 2 * TILE;    // [2 stages]
+  uint8_t *sV = sK + 2 * TILE;    // [2 stages]
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sV + 2 * TILE);
   uint64_t *q_full = bar;
   uint64_t *kv_full = bar + 1, *kv_empty = bar + 3;
   uint64_t *s_full = bar + 5, *p_full = bar + 7, *o_full = bar + 9;
@@ -121,17 +127,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(q_full, (has1 ? 2 : 1) * kTile);
+      mbar_expect_tx(q_full, (has1 ? 2 : 1) * TILE);
       for (int t = 0; t < (has1 ? 2 : 1); ++t)
-        for (int a = 0; a < 2; ++a)
-          tma_load_2d(sQ + t * kTile + a * kAtom, &tm, q_full, h * DH + 64 * a, row0 + (qb0 + t) * BQ);
+        for (int a = 0; a < DH / 64; ++a)
+          tma_load_2d(sQ + t * TILE + a * kAtom, &tm, q_full, h * DH + 64 * a, row0 + (qb0 + t) * BQ);
       for (int j = 0; j < nkv_all; ++j) {
         const int st = j & 1;
         mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[st], 2 * kTile);
-        for (int a = 0; a < 2; ++a) {
-          tma_load_2d(sK + st * kTile + a * kAtom, &tm, &kv_full[st], d + h * DH + 64 * a, row0 + j * BKV);
-          tma_load_2d(sV + st * kTile + a * kAtom, &tm, &kv_full[st], 2 * d + h * DH + 64 * a, row0 + j * BKV);
+        mbar_expect_tx(&kv_full[st], 2 * TILE);
+        for (int a = 0; a < DH / 64; ++a) {
+          tma_load_2d(sK + st * TILE + a * kAtom, &tm, &kv_full[st], d + h * DH + 64 * a, row0 + j * BKV);
+          tma_load_2d(sV + st * TILE + a * kAtom, &tm, &kv_full[st], 2 * d + h * DH + 64 * a, row0 + j * BKV);
         }
       }
     }
@@ -143,7 +149,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(q_full, 0);
       auto issue_s = [&](int t, int j) {
         tc_fence_after();
-        const uint32_t q_base = smem_u32(sQ + t * kTile), k_base = smem_u32(sK + (j & 1) * kTile);
+        const uint32_t q_base = smem_u32(sQ + t * TILE), k_base = smem_u32(sK + (j & 1) * TILE);
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
           const uint32_t off = (kk >> 2) * kAtom + (kk & 3) * 32;
@@ -155,7 +161,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto issue_o = [&](int t, int j) {
         mbar_wait(&p_full[t], j & 1);  // P_t(j) packed and O_t rescaled
         tc_fence_after();
-        const uint32_t v_base = smem_u32(sV + (j & 1) * kTile);
+        const uint32_t v_base = smem_u32(sV + (j & 1) * TILE);
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk)
           mma_bf16_ts(tmem + t * 256 + C_O, tmem + t * 256 + C_S + kk * 8,
@@ -592,23 +598,33 @@ static int make_map(CUtensorMap *tm, const void *base, int64_t inner, int64_t ro
 
 bool supported(int S, int DHx) { return DHx == DH && S % BQ == 0; }
 
-int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causal, cudaStream_t s) {
-  const int d = H * DH;
+template <int HD>
+static int forward_hd(const void *qkv, void *o, float *lse, int B, int S, int H, int causal, cudaStream_t s) {
+  const int d = H * HD;
   CUtensorMap tm;
   HM_TRY(make_map(&tm, qkv, 3 * (int64_t)d, (int64_t)B * S, 3 * (int64_t)d * 2, 128));
-  const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
-  ProfScope ps(KC_ATTN_FWD, s, 4.0 * B * (double)S * S * H * DH * (causal ? 0.5 : 1.0), (double)B * S * H * DH * 2 * 4);
+  const float scale_log2 = 1.4426950408889634f / sqrtf((float)HD);
+  ProfScope ps(KC_ATTN_FWD, s, 4.0 * B * (double)S * S * H * HD * (causal ? 0.5 : 1.0), (double)B * S * H * HD * 2 * 4);
   static bool attr[2] = {false, false};
-  auto k = causal ? fwd_kernel<true> : fwd_kernel<false>;
+  auto k = causal ? fwd_kernel<HD, true> : fwd_kernel<HD, false>;
   if (!attr[causal ? 1 : 0]) {
-    HM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFwdSmem));
+    HM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fwd_smem<HD>()));
     attr[causal ? 1 : 0] = true;
   }
   const int npair = (S / BQ + 1) / 2;
-  k<<<dim3(npair, B * H), kThreads, kFwdSmem, s>>>(tm, static_cast<__nv_bfloat16 *>(o), lse, S, H, scale_log2);
+  k<<<dim3(npair, B * H), kThreads, fwd_smem<HD>(), s>>>(tm, static_cast<__nv_bfloat16 *>(o), lse, S, H, scale_log2);
   count_launch();
   HM_CUDA(cudaGetLastError());
   return HM_OK;
+}
+
+int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causal, cudaStream_t s) {
+  return forward_hd<128>(qkv, o, lse, B, S, H, causal, s);
+}
+
+// head_dim 64 through the same kernel (attention_tc.cu dispatches it on HM_ATTN_FWD=t)
+int forward64(const void *qkv, void *o, float *lse, int B, int S, int H, int causal, cudaStream_t s) {
+  return forward_hd<64>(qkv, o, lse, B, S, H, causal, s);
 }
 
 // dq_acc must be zeroed by the caller; it receives scale * dS K (fp32)
