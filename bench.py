@@ -41,6 +41,8 @@ WORKLOADS = {
     # swapped as exact [bf16 hi | lo] planes; forward tasks move hi + the fp32 prefix
     "gpt2-xl-dp-bf16w": ("gpt2-xl", 16, 4, 8, 32, "dp", "bf16"),
     "tiny": ("tiny", 16, 4, 2, 4, "pp"),
+    "tiny-dp": ("tiny", 16, 4, 2, 4, "dp"),
+    "tiny-dp-shard": ("tiny", 16, 4, 2, 4, "dp", "fp32", "sharded"),
     # the same model at a 4x larger minibatch: Harmony's grouping amortises the fixed
     # per-iteration swap bytes (W, K) over more samples ("no grouping")
     "gpt2-xl-dp-d64": ("gpt2-xl", 64, 8, 4, 64, "dp"),
@@ -131,7 +133,21 @@ def _dist():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if SHARE_GPU:  # test mode: every rank on cuda:0
+        local = 0
     return world, rank, local
+
+
+# HM_BENCH_SHARE_GPU=1 (test mode, never a bench number): N ranks share ONE GPU,
+# the control plane runs on gloo and the per-pack gradient sum on the runtime's
+# CUDA-IPC backend (NCCL cannot place two ranks on one device).  It exercises
+# the multi-rank bench path -- launch, barriers, max over ranks, the ledger
+# union, shared arenas, device-counter ordering -- on a one-GPU box.
+SHARE_GPU = os.environ.get("HM_BENCH_SHARE_GPU") == "1"
+
+
+def _coll_device() -> str:
+    return "cpu" if SHARE_GPU else "cuda"
 
 
 def _max_over_ranks(x: float, world: int) -> float:
@@ -139,7 +155,7 @@ def _max_over_ranks(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=_coll_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -171,14 +187,14 @@ def _sum_over_ranks(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device=_coll_device())
     dist.all_reduce(t)
     return float(t.item())
 
 
 def _nccl_busbw(world: int, nbytes: int = 256 << 20) -> float:
     """Measured all-reduce bus bandwidth (GB/s): 2(N-1)/N x bytes / time."""
-    if world == 1:
+    if world == 1 or SHARE_GPU:
         return 0.0
     import torch
     import torch.distributed as dist
@@ -463,7 +479,10 @@ def run_native(args) -> None:
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if SHARE_GPU:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2202_01306_b200 as H
     from paper_2202_01306_b200 import ops
     from paper_2202_01306_b200.cnn import CNN_PRESETS, cnn_profiles, synthetic_images
@@ -518,11 +537,14 @@ def run_native(args) -> None:
         rt.init_weights(0, device=None if is_cnn else "cuda")
     if world > 1 and mode == "dp":
         import torch.distributed as dist
-        obj = [HarmonyRuntime.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        rt.init_comm(obj[0], world, rank)
+        if SHARE_GPU:
+            rt.init_ipc_reduce(world, rank)
+        else:
+            obj = [HarmonyRuntime.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            rt.init_comm(obj[0], world, rank)
     rt.load(graph, machine, prof, rank=rank)
-    if pp_multi or shard_multi:  # device counters (and PP activation buffers) of every peer
+    if pp_multi or shard_multi or (SHARE_GPU and world > 1):  # device counters (PP: activation buffers) of every peer
         blobs = [None] * world
         dist.all_gather_object(blobs, rt.ipc_export())
         for b in blobs:
@@ -742,7 +764,7 @@ def main() -> None:
         import socket
         import torch
         have = torch.cuda.device_count()
-        if have < args.gpus:
+        if have < args.gpus and not SHARE_GPU:
             sys.stderr.write(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) are visible\n")
             sys.exit(2)
         sk = socket.socket()
