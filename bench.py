@@ -63,6 +63,11 @@ WORKLOADS = {
     "gpt-40b-pp": ("gpt-40b", 8, 4, 2, 160, "pp"),
     # config c5: deep-CNN packs (128 residual blocks at 56x56 / 28x28, implicit-GEMM convs)
     "resnet-dp": ("resnet-bench", 64, 32, 16, 12, "dp"),
+    # config c5 at its named depth: ResNet-1026 (517 chain layers: 511
+    # residual blocks, 0.80 B parameters) and VGG-416 at 224x224 (stem to 56x56), 1000
+    # classes, packs of 32 layers -- the deep-chain swap stress
+    "resnet-1026-dp": ("resnet-1026", 32, 16, 32, 40, "dp"),
+    "vgg-416-dp": ("vgg-416", 32, 16, 32, 40, "dp"),
 }
 
 

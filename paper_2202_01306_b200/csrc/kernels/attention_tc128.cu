@@ -95,8 +95,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 11);
 
   const int nq = S / BQ, npair = (nq + 1) >> 1;
-  const int pr = CAUSAL ? npair - 1 - (int)blockIdx.x : (int)blockIdx.x;  // heaviest first
-  const int bh = blockIdx.y, b = bh / H, h = bh % H;
+  // blockIdx.x (fastest in launch order) walks the heads, blockIdx.y the
+  // pairs: every head's heaviest causal pair launches before any lighter one
+  const int pr = CAUSAL ? npair - 1 - (int)blockIdx.y : (int)blockIdx.y;
+  const int bh = blockIdx.x, b = bh / H, h = bh % H;
   const int d = H * DH;
   const int qb0 = 2 * pr;
   const bool has1 = qb0 + 1 < nq;
@@ -326,8 +328,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 14);
 
   const int nq = S / SUBQ;
-  const int kb = blockIdx.x;
-  const int bh = blockIdx.y, b = bh / H, h = bh % H;
+  const int kb = blockIdx.y;  // heads fastest: the heavy causal key blocks (small kb) launch first
+  const int bh = blockIdx.x, b = bh / H, h = bh % H;
   const int d = H * DH;
   const int q_begin = CAUSAL ? kb * (BKV / SUBQ) : 0;
   const int count = nq - q_begin;
@@ -612,7 +614,7 @@ static int forward_hd(const void *qkv, void *o, float *lse, int B, int S, int H,
     attr[causal ? 1 : 0] = true;
   }
   const int npair = (S / BQ + 1) / 2;
-  k<<<dim3(npair, B * H), kThreads, fwd_smem<HD>(), s>>>(tm, static_cast<__nv_bfloat16 *>(o), lse, S, H, scale_log2);
+  k<<<dim3(B * H, npair), kThreads, fwd_smem<HD>(), s>>>(tm, static_cast<__nv_bfloat16 *>(o), lse, S, H, scale_log2);
   count_launch();
   HM_CUDA(cudaGetLastError());
   return HM_OK;
@@ -653,7 +655,7 @@ int backward_main(const void *qkv, const void *dout, const float *lse, const flo
     attr[causal ? 1 : 0] = true;
   }
   const float scale = 1.f / sqrtf((float)DH);
-  k<<<dim3(S / BKV, B * H), kThreads, kBwdSmem, s>>>(tkv, tq, tdo, tdq, lse, dvec, static_cast<__nv_bfloat16 *>(dqkv),
+  k<<<dim3(B * H, S / BKV), kThreads, kBwdSmem, s>>>(tkv, tq, tdo, tdq, lse, dvec, static_cast<__nv_bfloat16 *>(dqkv),
                                                      S, H, 1.4426950408889634f * scale, scale);
   count_launch();
   HM_CUDA(cudaGetLastError());

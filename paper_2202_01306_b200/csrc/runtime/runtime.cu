@@ -1304,6 +1304,7 @@ static int load_plan(hm_runtime &rt, Plan *plan, int rank, int minibatch) {
   }
   HM_CUDA(cudaMalloc(&rt.pool, total));
   rt.pool_bytes = total;
+  rt.counters[2] = total;  // device bytes of the loaded plan (readable before any iteration)
   int64_t off = 0;
   for (auto &r : req) {
     *r.ptr = rt.pool + off;

@@ -91,3 +91,26 @@ def oracle_inputs(case):
 def native_lib():
     from paper_2202_01306_b200 import _native
     return _native.lib()
+
+
+def collect_or_fail(q, procs, timeout: float):
+    """Wait for the rank processes' result on ``q``; fail at once (with the
+    exit codes) if a rank dies first instead of waiting out the timeout."""
+    import queue as _queue
+    import time as _time
+    t_end = _time.monotonic() + timeout
+    while True:
+        try:
+            return q.get(timeout=2.0)
+        except _queue.Empty:
+            dead = [(i, p.exitcode) for i, p in enumerate(procs) if p.exitcode is not None and p.exitcode != 0]
+            if dead:
+                for p in procs:
+                    if p.is_alive():
+                        p.kill()
+                raise AssertionError(f"rank process(es) died before reporting: {dead}")
+            if _time.monotonic() > t_end:
+                for p in procs:
+                    if p.is_alive():
+                        p.kill()
+                raise AssertionError(f"no result from the ranks within {timeout} s")

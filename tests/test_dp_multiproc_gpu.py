@@ -20,6 +20,7 @@ import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
+from conftest import collect_or_fail
 
 pytestmark = pytest.mark.gpu
 
@@ -100,7 +101,7 @@ def test_dp_two_ranks_one_gpu(D, math, update):
     procs = [ctx.Process(target=_worker, args=(r, 2, port, D, math, q, update, shm)) for r in range(2)]
     for p in procs:
         p.start()
-    res = q.get(timeout=300)
+    res = collect_or_fail(q, procs, 300)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0

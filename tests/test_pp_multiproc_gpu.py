@@ -16,6 +16,7 @@ import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
+from conftest import collect_or_fail
 
 pytestmark = pytest.mark.gpu
 
@@ -113,7 +114,7 @@ def test_pp_two_ranks_one_gpu(name, pipelined):
     procs = [ctx.Process(target=_worker, args=(r, 2, port, shm, pipelined, name, q)) for r in range(2)]
     for p in procs:
         p.start()
-    res = q.get(timeout=900)
+    res = collect_or_fail(q, procs, 900)
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
