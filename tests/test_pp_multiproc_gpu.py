@@ -32,7 +32,7 @@ def _port():
 SPECS = {
     "tiny": dict(preset="tiny", lr=1e-4, alpha=4 << 30),
     # the 40B config's layer (805 M parameters, 3.2 GB of fp32 W per layer)
-    "wide": dict(spec=(4, 8192, 64, 128, 1024), lr=1e-5, alpha=48 << 30, steps=2),
+    "wide": dict(spec=(4, 8192, 64, 128, 1024), lr=1e-5, alpha=70 << 30, steps=2),
 }
 
 
