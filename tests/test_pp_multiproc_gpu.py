@@ -32,7 +32,9 @@ def _port():
 SPECS = {
     "tiny": dict(preset="tiny", lr=1e-4, alpha=4 << 30),
     # the 40B config's layer (805 M parameters, 3.2 GB of fp32 W per layer)
-    "wide": dict(spec=(4, 8192, 64, 128, 1024), lr=1e-5, alpha=70 << 30, steps=2),
+    # (fp32-operand parity mode: per-layer updates within 1e-3; in the bf16 mode Adam's
+    # first steps turn operand rounding into sign flips of near-zero gradients)
+    "wide": dict(spec=(4, 8192, 64, 128, 1024), lr=1e-5, alpha=70 << 30, steps=2, math="fp32"),
 }
 
 
@@ -57,7 +59,7 @@ def _worker(rank, world, port, shm, pipelined, name, q):
         pb = ((0, 1), (2, 3))
         g = H.generate_task_graph(H.Configuration(4, pf, 4, pb, 8, H.Mode.PP), mach, prof)
         torch.cuda.set_device(0)
-        rt = HarmonyRuntime(spec, alpha_bytes=alpha, device=0, lr=lr)
+        rt = HarmonyRuntime(spec, alpha_bytes=alpha, device=0, lr=lr, math=SPECS[name].get("math", "bf16"))
         stash = HarmonyRuntime.stash_bytes_for(g, prof)
         if rank == 0:
             rt.share_arenas(shm, True, stash)
@@ -130,7 +132,7 @@ def test_pp_two_ranks_one_gpu(name, pipelined):
     # oracle
     from oracle.gpt_cpu import GPTOracle
     from paper_2202_01306_b200.model import synthetic_batch
-    from test_parity_gpu import BF16_TOL, per_layer_rel
+    from test_parity_gpu import BF16_TOL, FP32_TOL, per_layer_rel
     spec = _spec(name)
     o = GPTOracle(spec, r0["w0"], res["w_off"], lr=SPECS[name]["lr"])
     tok, lab = synthetic_batch(spec, 8)
@@ -138,8 +140,9 @@ def test_pp_two_ranks_one_gpu(name, pipelined):
     # the rank running the last forward task owns the loss; the other reports 0
     losses = [max(a, b) for a, b in zip(r0["losses"], r1["losses"])]
     assert min(min(r0["losses"]), min(r1["losses"])) == 0.0
+    tol = FP32_TOL if SPECS[name].get("math") == "fp32" else BF16_TOL
     for a, b in zip(losses, ref):
-        assert abs(a - b) / b < BF16_TOL["loss"], (losses, ref)
+        assert abs(a - b) / b < tol["loss"], (losses, ref)
     dw = per_layer_rel(r0["w_final"], o.w.numpy(), res["w_off"], r0["w0"])
     print(f"PP N=2 {name}: loss {losses} vs {ref}; per-layer dW rel {['%.1e' % x for x in dw]}")
-    assert max(dw) < BF16_TOL["dw"], dw
+    assert max(dw) < tol["dw"], dw
