@@ -27,6 +27,9 @@
 #include "sm100.cuh"
 
 namespace hm {
+namespace attn_fwd64 {  // attention_fwd64.cu
+int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causal, cudaStream_t s);
+}  // namespace attn_fwd64
 namespace attn_tc128 {  // attention_tc128.cu
 bool supported(int S, int DH);
 int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causal, cudaStream_t s);
@@ -1612,6 +1615,8 @@ int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causa
   // t = query-tile pairs with P and O resident in TMEM (attention_tc128.cu's
   // dataflow at head_dim 64)
   if (mode == 't') return attn_tc128::forward64(qkv, o, lse, B, S, H, causal, s);
+  // f = rotating S buffers in TMEM, whole-row softmax in registers (attention_fwd64.cu)
+  if (mode == 'f') return attn_fwd64::forward(qkv, o, lse, B, S, H, causal, s);
   const bool two_tiles = mode == '2';
   // two query tiles per CTA (ping-pong softmax warpgroups) for full attention:
   // 1.31x at 8 x 512 x 16 heads.
