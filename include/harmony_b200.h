@@ -339,11 +339,14 @@ int hm_k_add_bf16(const void *a, const void *b, void *out, int64_t n, void *stre
 /* Tile configuration the GEMM picks for an (m, n, k, epilogue, B major) problem:
  * bn = output tile width (128 | 192 | 256; 192 single-CTA only), cta_pair = 1 (128-row tile on one SM) or
  * 2 (256-row tile on a CTA pair, tcgen05.mma.cta_group::2), splits = split-K
- * factor (ACC_F32 only; partial sums meet in a TMA reduce-add). */
+ * factor (ACC_F32 only; partial sums meet in a TMA reduce-add), 0 = stream-K
+ * (ACC_F32 only: each persistent CTA pair runs an equal share of the
+ * tiles x k-blocks sequence, tiles cut between CTAs summed by the same reduce-add). */
 int hm_k_gemm_tile(int64_t m, int64_t n, int64_t k, int32_t epilogue, int32_t b_major, int32_t *bn,
                    int32_t *cta_pair, int32_t *splits);
-/* Force a tile configuration for every later GEMM of the process (0 = auto);
- * for tests and tuning (same as HM_GEMM_BN / HM_GEMM_CG / HM_GEMM_SPLITK). */
+/* Force a tile configuration for every later GEMM of the process (0 = auto;
+ * splits = -1 forces stream-K for ACC_F32); for tests and tuning (same as
+ * HM_GEMM_BN / HM_GEMM_CG / HM_GEMM_SPLITK). */
 int hm_k_gemm_set_tile(int32_t bn, int32_t cta_pair, int32_t splits);
 /* The GEMM's own per-launch time (us) for one shape {m, n, k, a_major,
  * b_major, epilogue, has_bias}: a CUDA graph of `reps` back-to-back launches

@@ -6,7 +6,7 @@
 // One CTA per pair of 128-query tiles (heaviest causal pairs first):
 //   warp 0      TMA: both Q tiles once, then K_j / V_j into a 3-stage ring
 //   warp 1      TMEM allocation, MMA issuer
-//   warps 2-5   softmax of tile 0, warps 6-9 of tile 1 (one thread per
+//   warps 4-7   softmax of tile 0, warps 8-11 of tile 1 (one thread per
 //               query row; warp w reads TMEM lanes 32 (w % 4) .. + 31)
 // TMEM (512 columns): three rotating 128-column S buffers + O_0, O_1 (64
 // columns each).  S buffers are handed out in the order the S tiles are
@@ -18,9 +18,10 @@
 // throughput.
 //
 // Softmax per tile: the whole S row (128 fp32) is read with four
-// tcgen05.ld.x32 and one wait (10 warps: up to 200 registers per thread),
-// masked on the causal
-// diagonal, reduced with 3-input max, exponentiated with packed f32x2 FMA /
+// tcgen05.ld.x32 and one wait, masked on the causal
+// diagonal (the softmax warpgroups raise their register budget to 216 with
+// setmaxnreg, the TMA / MMA warpgroup drops to 72: three warps share each
+// SMSP's 16K registers), reduced with 3-input max, exponentiated with packed f32x2 FMA /
 // add (half the FP32 issue slots) and ex2.approx, and written back as bf16
 // pairs into the S buffer's own columns, where the PV MMA reads it as its A
 // operand straight from TMEM.  O stays in TMEM; it is rescaled in place only
@@ -45,7 +46,7 @@ constexpr int DH = 64, BQ = 128, BKV = 128;
 constexpr int kStages = 3;               // K / V ring
 constexpr int kSBuf = 3;                 // rotating S / P buffers in TMEM
 constexpr uint32_t kTile = BQ * DH * 2;  // 128 rows x 128 B: one SW128 atom column, 16 KB
-constexpr int kThreads = 320;  // 10 warps: <= 204 registers per thread
+constexpr int kThreads = 384;
 constexpr float kRescaleLog2 = 8.f;      // lazy-rescale threshold (log2 units)
 constexpr uint32_t C_O = kSBuf * BKV;    // O_t at columns [384 + 64 t, 448 + 64 t)
 constexpr size_t kSmem = 1024 + 2 * kTile /*Q pair*/ + 2 * kStages * kTile /*K, V*/ + 256;
@@ -84,6 +85,14 @@ __device__ __forceinline__ float2 mul2(float2 a, float2 b) {
       : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
   return d;
 }
+template <int N>
+__device__ __forceinline__ void reg_alloc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <int N>
+__device__ __forceinline__ void reg_dealloc() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
 __device__ __forceinline__ uint32_t bf16x2(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
@@ -91,7 +100,7 @@ __device__ __forceinline__ uint32_t bf16x2(float lo, float hi) {
 }
 
 template <bool CAUSAL>
-__global__ void __maxnreg__(200)
+__global__ void __launch_bounds__(kThreads, 1)
     fwd_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16 *__restrict__ out, float *__restrict__ lse,
                int S, int H, float scale_log2) {
   extern __shared__ uint8_t smem_raw[];
@@ -142,7 +151,8 @@ __global__ void __maxnreg__(200)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp < 2) {
+  if (warp < 4) {
+    reg_dealloc<72>();  // 3 x 168 per SMSP at launch = 72 + 2 x 216
     if (warp == 0 && lane == 0) {
       mbar_expect_tx(q_full, (has1 ? 2 : 1) * kTile);
       tma_load_2d(sQ, &tm, q_full, h * DH, row0 + qb0 * BQ);
@@ -200,7 +210,8 @@ __global__ void __maxnreg__(200)
       }
     }
   } else {
-    const int t = (warp - 2) >> 2;
+    reg_alloc<216>();
+    const int t = (warp >> 2) - 1;
     const int nkv = t == 0 ? nkv0 : nkv1;
     if (nkv > 0) {
       const int q4 = warp & 3;

@@ -43,6 +43,9 @@ constexpr int kThreads = 128 + 32 * kEpiWarps;
 struct Args {
   int32_t M, N, K, num_m, num_n, num_k;
   int32_t splits;  // split-K factor (ACC_F32 only: partial sums meet in the TMA reduce-add)
+  int32_t streamk;  // 1: stream-K (ACC_F32 only): every CTA (pair) takes an equal run of the
+                    // tiles x k-blocks sequence; a tile cut between two runs is summed by
+                    // the reduce-add like a split
   // implicit-GEMM 3x3 convolution (MODE 1-3): image H x W of the im2col
   // operand, its 64-channel blocks, and (dgrad) the output-channel blocks
   int32_t cv_h, cv_w, cv_cb, cv_cbo;
@@ -69,11 +72,43 @@ struct Cfg {
   static constexpr size_t kSmem = 1024 + (size_t)kStages * (kABytes + kBBytes) + kEpiWarps * 4096 + 256;
 };
 
-// k-block range of split `sp` of `n` over num_k k-blocks
-__device__ __forceinline__ void split_range(int sp, int n, int num_k, int &lo, int &hi) {
-  lo = (int)((int64_t)sp * num_k / n);
-  hi = (int)((int64_t)(sp + 1) * num_k / n);
-}
+// The work units a persistent CTA (pair) `slot` of `nslots` visits, in order:
+// (tile, k-block range).  Classic: units (tile, split) round robin.  Stream-K:
+// the contiguous run [slot * T / nslots, (slot + 1) * T / nslots) of the
+// T = tiles x num_k k-block sequence, cut at tile boundaries.
+struct UnitIter {
+  int64_t g, g_end;  // stream-K cursor / end, or classic unit index / unit count
+  int step;
+  __device__ UnitIter(const Args &a, int slot, int nslots) {
+    const int64_t tiles = (int64_t)a.num_m * a.num_n;
+    if (a.streamk) {
+      const int64_t T = tiles * a.num_k;
+      g = slot * T / nslots;
+      g_end = (slot + 1) * T / nslots;
+      step = 0;
+    } else {
+      g = slot;
+      g_end = tiles * a.splits;
+      step = nslots;
+    }
+  }
+  __device__ bool next(const Args &a, int &tile, int &kb0, int &kb1) {
+    if (g >= g_end) return false;
+    if (a.streamk) {
+      tile = (int)(g / a.num_k);
+      kb0 = (int)(g - (int64_t)tile * a.num_k);
+      kb1 = (int)min((int64_t)a.num_k, kb0 + (g_end - g));
+      g += kb1 - kb0;
+    } else {
+      tile = (int)(g / a.splits);
+      const int sp = (int)(g - (int64_t)tile * a.splits);
+      kb0 = (int)((int64_t)sp * a.num_k / a.splits);
+      kb1 = (int)((int64_t)(sp + 1) * a.num_k / a.splits);
+      g += step;
+    }
+    return true;
+  }
+};
 
 // grouped raster: kGroupM row-tiles sweep the column tiles together (L2 reuse of B)
 __device__ __forceinline__ void tile_coord(int t, int num_m, int num_n, int &mb, int &nb) {
@@ -284,9 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  const int nsplit = args.splits;
-  const int ntiles = args.num_m * args.num_n * nsplit;  // work units: (tile, k-split)
-  const int unit0 = blockIdx.x / CG, unit_step = gridDim.x / CG;
+  const int slot = blockIdx.x / CG, nslots = gridDim.x / CG;  // persistent CTA (pair) index
 
   if (warp == 0) {
     if (lane == 0) {
@@ -297,10 +330,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (args.span) atomicMax(&args.span[0], ~globaltimer());
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = unit0; t < ntiles; t += unit_step) {
-        int mb, nb, kb0, kb1;
-        tile_coord(t / nsplit, args.num_m, args.num_n, mb, nb);
-        split_range(t % nsplit, nsplit, args.num_k, kb0, kb1);
+      UnitIter it(args, slot, nslots);
+      int tile, kb0, kb1;
+      while (it.next(args, tile, kb0, kb1)) {
+        int mb, nb;
+        tile_coord(tile, args.num_m, args.num_n, mb, nb);
         const int m0 = mb * kTileM + (int)rank * BM;           // this CTA's A rows
         const int n0 = nb * BN + (int)rank * C::kBRows;        // this CTA's B rows
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -375,14 +409,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int local = 0;
-      for (int t = unit0; t < ntiles; t += unit_step, ++local) {
+      UnitIter it(args, slot, nslots);
+      int tile, kb0, kb1;
+      for (; it.next(args, tile, kb0, kb1); ++local) {
         const int acc = local & 1;
         const uint32_t use = (uint32_t)(local >> 1);
         mbar_wait(&tempty[acc], (use & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        int kb0, kb1;
-        split_range(t % nsplit, nsplit, args.num_k, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -431,9 +465,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const CUtensorMap *tsrc = &tmX;
     griddep_wait();  // epilogue reads / writes global memory of the previous kernel's outputs
     int local = 0;
-    for (int t = unit0; t < ntiles; t += unit_step, ++local) {
+    UnitIter it(args, slot, nslots);
+    int tile, kb0_, kb1_;
+    for (; it.next(args, tile, kb0_, kb1_); ++local) {
       int mb, nb;
-      tile_coord(t / nsplit, args.num_m, args.num_n, mb, nb);
+      tile_coord(tile, args.num_m, args.num_n, mb, nb);
       const int acc = local & 1;
       const uint32_t use = (uint32_t)(local >> 1);
       const int row0 = mb * kTileM + (int)rank * BM + q * 32;
@@ -567,7 +603,7 @@ static int make_map(CUtensorMap *out, const void *ptr, uint64_t d0, uint64_t d1,
 static int num_sms();
 
 struct TileCfg {
-  int bn, cg, splits;
+  int bn, cg, splits, streamk;
 };
 
 static int env_int(const char *name) {
@@ -588,6 +624,9 @@ static int env_int(const char *name) {
 // HM_GEMM_SPLITK force a choice.
 static int g_force_bn = env_int("HM_GEMM_BN"), g_force_cg = env_int("HM_GEMM_CG"),
            g_force_s = env_int("HM_GEMM_SPLITK");
+// stream-K for ACC_F32: unset = by the cost model, 0 = never, 1 = always
+// (HM_GEMM_SPLITK / hm_k_gemm_set_tile splits = -1 also force it)
+static const int g_streamk = getenv("HM_GEMM_STREAMK") ? atoi(getenv("HM_GEMM_STREAMK")) : -1;
 // 128 x 192 single-CTA tiles (fit 1600-wide outputs in 9 column tiles)
 static const bool g_tile192 = getenv("HM_GEMM_192") ? atoi(getenv("HM_GEMM_192")) != 0 : true;
 static const double g_eff192 = getenv("HM_GEMM_EFF192") ? atof(getenv("HM_GEMM_EFF192")) : 0.70;
@@ -596,10 +635,12 @@ static const double g_eff192 = getenv("HM_GEMM_EFF192") ? atof(getenv("HM_GEMM_E
 static const double g_eff192p = getenv("HM_GEMM_EFF192P") ? atof(getenv("HM_GEMM_EFF192P")) : 0.80;
 
 static TileCfg pick_tile(int64_t M, int64_t N, int64_t K, int epi, bool allow192 = true, bool b_mn = false) {
-  const int env_bn = g_force_bn, env_cg = g_force_cg, env_s = g_force_s;
+  const int env_bn = g_force_bn, env_cg = g_force_cg, env_s = g_force_s > 0 ? g_force_s : 0;
+  const bool acc = epi == HM_EPI_ACC_F32;
+  const bool force_sk = acc && (g_force_s == -1 || g_streamk == 1), allow_sk = acc && !env_s && g_streamk != 0;
   const int64_t sms = num_sms();
   const int64_t num_k = (K + BK - 1) / BK;
-  TileCfg best{256, 1, 1};
+  TileCfg best{256, 1, 1, 0};
   double best_t = 1e300;
   for (int cg = 1; cg <= 2; ++cg) {
     if (env_cg && cg != env_cg) continue;
@@ -613,14 +654,25 @@ static TileCfg pick_tile(int64_t M, int64_t N, int64_t K, int epi, bool allow192
       const double t_kb = bn / 256.0 / eff;
       const int64_t tiles = ((M + BM * cg - 1) / (BM * cg)) * ((N + bn - 1) / bn);
       const int64_t slots = sms / cg;
-      for (int s = 1; s <= (epi == HM_EPI_ACC_F32 ? 32 : 1); ++s) {
+      for (int s = 1; s <= (acc ? 32 : 1); ++s) {
         if (env_s && s != env_s) continue;
         if (s > 1 && num_k / s < 8) break;
         const double waves = (double)((tiles * s + slots - 1) / slots);
         const double t = waves * ((double)num_k / s + 4.0) * t_kb * (s > 1 ? 1.03 : 1.0);
-        if (t < best_t) {
+        if (t < best_t && !force_sk) {
           best_t = t;
-          best = TileCfg{bn, cg, s};
+          best = TileCfg{bn, cg, s, 0};
+        }
+      }
+      // stream-K (reduce-add epilogue only): every slot runs ceil(tiles x num_k / slots)
+      // k-blocks, paying the fill / epilogue tail once per tile segment it touches
+      if (allow_sk || force_sk) {
+        const int64_t per = (tiles * num_k + slots - 1) / slots;
+        const int64_t segs = std::min<int64_t>(tiles, (per + num_k - 1) / num_k + 1);
+        const double t = ((double)per + 4.0 * (double)segs) * t_kb * 1.02;
+        if (t < best_t || (force_sk && !best.streamk)) {
+          best_t = t;
+          best = TileCfg{bn, cg, 1, 1};
         }
       }
     }
@@ -650,7 +702,7 @@ static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMa
     if (e != cudaSuccess) return fail(HM_ERR_DEVICE, std::string("gemm smem attr: ") + cudaGetErrorString(e));
     attr = true;
   }
-  const int units = a.num_m * a.num_n * a.splits;
+  const int units = a.streamk ? a.num_m * a.num_n * a.num_k : a.num_m * a.num_n * a.splits;
   const int grid = CG * std::min(units, num_sms() / CG);
   const bool f32 = a.epi == HM_EPI_STORE_F32 || a.epi == HM_EPI_ACC_F32 || a.epi == HM_EPI_RESID_F32;
   const double io = (double)a.M * a.N * (f32 ? 4 : 2) * (a.epi == HM_EPI_ACC_F32 || a.epi >= HM_EPI_RESID_F32 ? 2 : 1);
@@ -711,6 +763,7 @@ int run(const void *A, const void *B, void *D, int64_t M, int64_t N, int64_t K, 
   a.num_n = (int)((N + bn - 1) / bn);
   a.num_k = (int)((K + BK - 1) / BK);
   a.splits = tc.splits;
+  a.streamk = tc.streamk;
   a.d = D; a.ldd = ldd; a.bias = bias; a.aux = aux; a.ld_aux = ld_aux; a.epi = epi;
   CUtensorMap ta, tb, td, tx;
   int rc = a_mn ? make_map(&ta, A, M, K, lda * 2, 64) : make_map(&ta, A, K, M, lda * 2, BM);
@@ -855,6 +908,7 @@ int run_conv(int mode, const void *act, const void *wt, void *out, int n, int h,
   a.num_n = (int)((N + tc.bn - 1) / tc.bn);
   a.num_k = (int)((K + BK - 1) / BK);
   a.splits = tc.splits;
+  a.streamk = tc.streamk;
   a.d = out; a.ldd = N; a.bias = bias; a.aux = const_cast<void *>(aux); a.ld_aux = N; a.epi = epi;
   a.cv_h = h; a.cv_w = w; a.cv_cb = (mode == 2 ? cout : cin) / 64; a.cv_cbo = cout / 64;
   const bool f32out = mode == 3;
@@ -902,10 +956,10 @@ extern "C" int hm_k_conv_wgrad(const void *dy, const void *x, float *dw, int32_t
 }
 
 extern "C" int hm_k_gemm_set_tile(int32_t bn, int32_t cta_pair, int32_t splits) {
-  if ((bn && bn != 128 && bn != 192 && bn != 256) || (cta_pair && cta_pair != 1 && cta_pair != 2) || splits < 0 ||
+  if ((bn && bn != 128 && bn != 192 && bn != 256) || (cta_pair && cta_pair != 1 && cta_pair != 2) || splits < -1 ||
       splits > 32)
     return hm::fail(HM_ERR_VALIDATION,
-                    "gemm tile override: bn in {0,128,192,256}, cta_pair in {0,1,2}, splits in [0,32]");
+                    "gemm tile override: bn in {0,128,192,256}, cta_pair in {0,1,2}, splits in [-1,32] (-1 = stream-K)");
   hm::gemm::g_force_bn = bn;
   hm::gemm::g_force_cg = cta_pair;
   hm::gemm::g_force_s = splits;
@@ -917,7 +971,7 @@ extern "C" int hm_k_gemm_tile(int64_t m, int64_t n, int64_t k, int32_t epilogue,
   const hm::gemm::TileCfg t = hm::gemm::pick_tile(m, n, k, epilogue, true, b_major != 0);
   *bn = t.bn;
   *cta_pair = t.cg;
-  *splits = t.splits;
+  *splits = t.streamk ? 0 : t.splits;
   return HM_OK;
 }
 
