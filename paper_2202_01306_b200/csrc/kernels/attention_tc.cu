@@ -1,19 +1,19 @@
-// attention_tc.cu -- flash attention (head_dim 64) on the 5th-gen tensor cores.
+// attention_tc.cu -- flash attention (head_dim 64) on the 5th-gen tensor cores:
+// the backward, and the persistent query-block-pair forward (HM_ATTN_FWD=q;
+// the default forward is attention_fwd64.cu).
 //
-// Forward, per 128-query tile (fwd_kernel: one CTA per tile):
-//   warp 0     TMA: Q once, then K_j / V_j tiles (128 keys) into a 2-stage ring
-//   warp 1     MMA issuer: S_j = Q K_j^T (128x128x64) into TMEM (2 buffers),
-//              O_j = P_j V_j (128x64x128) into TMEM (2 buffers); S_{j+1} is
-//              issued before waiting for P_j so QK^T overlaps the softmax
-//   warps 4-7  softmax / epilogue, one thread per query row (TMEM lane):
-//              tcgen05.ld the S row, online max / exp2 / sum in registers,
-//              P_j (bf16) written to 128B-swizzled smem as the next MMA's A
-//              operand, O accumulated in registers one tile behind with the
-//              running rescale
-// The default forward kernels are persistent (one CTA per SM walking a work
-// list): fwd2p_kernel (query-block pairs, two ping-pong softmax warpgroups)
-// and fwdp_kernel (single tiles, short causal sequences).  Backward: bwd_kernel
-// (one CTA per 128-key block, two softmax warpgroups, dQ by TMA reduce-add).
+// fwd2p_kernel (one CTA per SM walking a list of query-block pairs):
+//   warp 0      TMA: the pair's Q tiles (double-buffered per item), then
+//               K_j / V_j tiles (128 keys) into a 2-stage ring
+//   warp 1      MMA issuer: S = Q K_j^T (128x128x64) into TMEM per tile,
+//               O = P V_j (128x64x128) into TMEM per tile
+//   warps 4-11  two softmax warpgroups (one per query tile), one thread per
+//               query row (TMEM lane): the S row from TMEM, online max /
+//               exp2 / sum in registers, P (bf16) into 128B-swizzled smem as
+//               the PV MMA's A operand, O accumulated in registers one tile
+//               behind with the running rescale
+// Backward: bwd_kernel (one CTA per 128-key block, two softmax warpgroups, dQ
+// by TMA reduce-add).
 // Output o [tokens, d] bf16 and lse [tokens, H] (log2 domain) exactly as the
 // mma.sync kernel (attention.cu), which stays the fallback for sequence
 // lengths that are not a multiple of 128 (head_dim 128: attention_tc128.cu).
@@ -40,10 +40,9 @@ namespace attn_tc {
 using namespace sm100;
 
 constexpr int BQ = 128, BKV = 128, DH = 64;
-constexpr int kThreads = 256;
+constexpr int kThreads2 = 384;  // TMA, MMA, TMEM-alloc, idle, 2 x 4 softmax / elementwise warps
 constexpr uint32_t kTileBytes = BKV * DH * 2;  // 16 KB: 128 rows x 128 B
 constexpr uint32_t kPBytes = BQ * BKV * 2;     // 32 KB: two 64-key swizzle atoms
-constexpr size_t kSmem = 1024 + kTileBytes /*Q*/ + 2 * kTileBytes /*K*/ + 2 * kTileBytes /*V*/ + 2 * kPBytes + 512;
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -54,713 +53,10 @@ __device__ __forceinline__ float ex2(float x) {
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 
-template <bool CAUSAL>
-__global__ void __launch_bounds__(kThreads, 1)
-    fwd_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16 *__restrict__ out, float *__restrict__ lse, int S,
-               int H, float scale_log2) {
-  extern __shared__ uint8_t smem_raw[];
-  // 1024-B aligned base by pointer arithmetic on the __shared__ array, so the
-  // compiler keeps the shared address space (STS / LDS, not generic ST / LD)
-  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t *sQ = smem;
-  uint8_t *sK = sQ + kTileBytes;
-  uint8_t *sV = sK + 2 * kTileBytes;
-  uint8_t *sP = sV + 2 * kTileBytes;
-  uint64_t *bar = reinterpret_cast<uint64_t *>(sP + 2 * kPBytes);
-  uint64_t *q_full = bar;
-  uint64_t *kv_full = bar + 1, *kv_empty = bar + 3;
-  uint64_t *s_full = bar + 5, *s_empty = bar + 7;
-  uint64_t *p_full = bar + 9, *p_empty = bar + 11;
-  uint64_t *o_full = bar + 13, *o_empty = bar + 15;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 17);
-
-  const int nq = S / BQ;
-  const int qb = CAUSAL ? nq - 1 - (int)blockIdx.x : (int)blockIdx.x;
-  const int bh = blockIdx.y, b = bh / H, h = bh % H;
-  const int d = H * DH;
-  const int nkv = CAUSAL ? qb + 1 : S / BKV;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tm);
-    mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
-      mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 128);
-      mbar_init(&p_full[i], 128);
-      mbar_init(&p_empty[i], 1);
-      mbar_init(&o_full[i], 1);
-      mbar_init(&o_empty[i], 128);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc<512>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const int row0 = b * S;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      mbar_expect_tx(q_full, kTileBytes);
-      tma_load_2d(sQ, &tm, q_full, h * DH, row0 + qb * BQ);
-      for (int j = 0; j < nkv; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[st], 2 * kTileBytes);
-        tma_load_2d(sK + st * kTileBytes, &tm, &kv_full[st], d + h * DH, row0 + j * BKV);
-        tma_load_2d(sV + st * kTileBytes, &tm, &kv_full[st], 2 * d + h * DH, row0 + j * BKV);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc_s = idesc_bf16_f32(BQ, BKV, 0, 0);  // Q K-major, K K-major
-      constexpr uint32_t idesc_o = idesc_bf16_f32(BQ, DH, 0, 1);   // P K-major, V MN-major
-      mbar_wait(q_full, 0);
-      const uint32_t q_base = smem_u32(sQ);
-      auto issue_s = [&](int j) {
-        const int st = j & 1, buf = j & 1;
-        mbar_wait(&kv_full[st], (j >> 1) & 1);
-        mbar_wait(&s_empty[buf], ((j >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t k_base = smem_u32(sK + st * kTileBytes);
-#pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk)
-          mma_bf16(tmem + buf * BKV, umma_desc_sw128(q_base + kk * 32, 16, 1024),
-                   umma_desc_sw128(k_base + kk * 32, 16, 1024), idesc_s, kk > 0);
-        mma_commit(&s_full[buf]);
-      };
-      issue_s(0);
-      for (int j = 0; j < nkv; ++j) {
-        if (j + 1 < nkv) issue_s(j + 1);
-        const int st = j & 1, buf = j & 1;
-        mbar_wait(&p_full[buf], (j >> 1) & 1);
-        mbar_wait(&o_empty[buf], ((j >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t p_base = smem_u32(sP + buf * kPBytes);
-        const uint32_t v_base = smem_u32(sV + st * kTileBytes);
-#pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk)
-          mma_bf16(tmem + 2 * BKV + buf * DH,
-                   umma_desc_sw128(p_base + (kk >> 2) * (BQ * 128) + (kk & 3) * 32, 16, 1024),
-                   umma_desc_sw128(v_base + kk * 2048, BKV * 128, 1024), idesc_o, kk > 0);
-        mma_commit(&o_full[buf]);
-        mma_commit(&kv_empty[st]);
-        mma_commit(&p_empty[buf]);
-      }
-    }
-  } else if (warp >= 4) {
-    const int q = warp & 3;
-    const int r = q * 32 + lane;  // query row inside the block == TMEM lane
-    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    float o[DH];
-#pragma unroll
-    for (int c = 0; c < DH; ++c) o[c] = 0.f;
-    float m = -INFINITY, l = 0.f, alpha_prev = 1.f;
-    auto add_o = [&](int j, float alpha) {
-      const int buf = j & 1;
-      mbar_wait(&o_full[buf], (j >> 1) & 1);
-      tc_fence_after();
-      uint32_t v[DH];
-#pragma unroll
-      for (int c0 = 0; c0 < DH; c0 += 32)
-        tmem_ld_32x32b_x32(tmem + lane_addr + 2 * BKV + buf * DH + c0, *reinterpret_cast<uint32_t(*)[32]>(v + c0));
-      tmem_ld_wait();
-#pragma unroll
-      for (int c = 0; c < DH; ++c) o[c] = o[c] * alpha + __uint_as_float(v[c]);
-      tc_fence_before();
-      mbar_arrive(&o_empty[buf]);
-    };
-    for (int j = 0; j < nkv; ++j) {
-      const int buf = j & 1;
-      mbar_wait(&s_full[buf], (j >> 1) & 1);
-      tc_fence_after();
-      const uint32_t s_addr = tmem + lane_addr + buf * BKV;
-      const bool diag = CAUSAL && j == qb;
-      // the whole S row in registers: four TMEM loads in flight, one wait
-      uint32_t v[BKV];
-#pragma unroll
-      for (int c0 = 0; c0 < BKV; c0 += 32)
-        tmem_ld_32x32b_x32(s_addr + c0, *reinterpret_cast<uint32_t(*)[32]>(v + c0));
-      tmem_ld_wait();
-      if (diag) {  // causal mask on the diagonal tile (key > query)
-#pragma unroll
-        for (int c = 0; c < BKV; ++c)
-          if (c > r) v[c] = __float_as_uint(-INFINITY);
-      }
-      // row max with 8 independent chains (one warp per SM sub-partition: no
-      // other warp hides the FMNMX latency)
-      float mx8[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) mx8[e] = __uint_as_float(v[e]);
-#pragma unroll
-      for (int c = 8; c < BKV; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(v[c]));
-      const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-      const float m_new = fmaxf(m, mx * scale_log2);
-      const float alpha = ex2(m - m_new);
-      m = m_new;
-      // P_j goes to smem buffer `buf`: wait until the MMA of P_{j-2} has consumed it
-      mbar_wait(&p_empty[buf], ((j >> 1) & 1) ^ 1);
-      uint8_t *prow = sP + buf * kPBytes + r * 128;
-      float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int c0 = 0; c0 < BKV; c0 += 32) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int c = 0; c < 32; c += 2) {
-          const float p0 = ex2(fmaf(__uint_as_float(v[c0 + c]), scale_log2, -m_new));
-          const float p1 = ex2(fmaf(__uint_as_float(v[c0 + c + 1]), scale_log2, -m_new));
-          rs8[(c >> 1) & 7] += p0 + p1;
-          __nv_bfloat162 t = __floats2bfloat162_rn(p0, p1);
-          pk[c >> 1] = *reinterpret_cast<uint32_t *>(&t);
-        }
-        // 32 keys = four 16-byte chunks of the 64-key swizzle atom (c0 / 64)
-        uint8_t *atom_row = prow + (c0 >> 6) * (BQ * 128);
-#pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
-          const int chunk = ((c0 & 63) >> 3) + ch;
-          *reinterpret_cast<uint4 *>(atom_row + ((chunk ^ (r & 7)) << 4)) =
-              make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(&s_empty[buf]);
-      fence_async_smem();  // generic-proxy P writes -> visible to the MMA (async proxy)
-      mbar_arrive(&p_full[buf]);
-      const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
-      l = l * alpha + rs;
-      if (j > 0) add_o(j - 1, alpha_prev);
-      alpha_prev = alpha;
-    }
-    add_o(nkv - 1, alpha_prev);
-    // o is at the scale of the last tile's max; l too
-    const float inv = 1.f / l;
-    __nv_bfloat16 *orow = out + (int64_t)(row0 + qb * BQ + r) * d + h * DH;
-#pragma unroll
-    for (int c = 0; c < DH; c += 8) {
-      uint4 w;
-      uint32_t *wp = reinterpret_cast<uint32_t *>(&w);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        __nv_bfloat162 t = __floats2bfloat162_rn(o[c + 2 * e] * inv, o[c + 2 * e + 1] * inv);
-        wp[e] = *reinterpret_cast<uint32_t *>(&t);
-      }
-      *reinterpret_cast<uint4 *>(orow + c) = w;
-    }
-    lse[(int64_t)(row0 + qb * BQ + r) * H + h] = m + log2f(l);
-  }
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc<512>(tmem);
-  }
-}
-
 // ---------------------------------------------------------------------------
-// forward, persistent: one CTA per SM walks a list of (sample-head, query
-// block) work items, heaviest first for causal attention.  Same warp roles
-// and per-tile dataflow as fwd_kernel, but the TMEM allocation, barrier set-up
-// and pipeline fill are paid once per SM instead of once per 128 queries: the
-// TMA warp loads the next item's Q (double-buffered) and first K/V tiles, and
-// the MMA warp issues its first Q K^T, while the softmax warps are still on
-// the previous item's last tile and epilogue.  All ring / buffer parities
-// follow one running tile counter across items.
-// ---------------------------------------------------------------------------
-constexpr size_t kSmemP = 1024 + 2 * kTileBytes /*Q x2*/ + 2 * kTileBytes /*K*/ + 2 * kTileBytes /*V*/ + 2 * kPBytes + 512;
-
-struct FwdItems {
-  int nq, bh_count, n_items;
-  __device__ __forceinline__ void item(int i, bool causal, int &bh, int &qb) const {
-    if (causal) {  // heaviest (longest K/V sweep) first
-      qb = nq - 1 - i / bh_count;
-      bh = i % bh_count;
-    } else {
-      qb = i % nq;
-      bh = i / nq;
-    }
-  }
-};
-
-template <bool CAUSAL>
-__global__ void __launch_bounds__(kThreads, 1)
-    fwdp_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16 *__restrict__ out, float *__restrict__ lse,
-                int S, int H, int BH, float scale_log2) {
-  extern __shared__ uint8_t smem_raw[];
-  // 1024-B aligned base by pointer arithmetic on the __shared__ array, so the
-  // compiler keeps the shared address space (STS / LDS, not generic ST / LD)
-  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t *sQ = smem;                  // [2] items
-  uint8_t *sK = sQ + 2 * kTileBytes;   // [2] stages
-  uint8_t *sV = sK + 2 * kTileBytes;   // [2] stages
-  uint8_t *sP = sV + 2 * kTileBytes;   // [2] tiles
-  uint64_t *bar = reinterpret_cast<uint64_t *>(sP + 2 * kPBytes);
-  uint64_t *q_full = bar, *q_empty = bar + 2;
-  uint64_t *kv_full = bar + 4, *kv_empty = bar + 6;
-  uint64_t *s_full = bar + 8, *s_empty = bar + 10;
-  uint64_t *p_full = bar + 12, *p_empty = bar + 14;
-  uint64_t *o_full = bar + 16, *o_empty = bar + 18;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 20);
-
-  const FwdItems W{S / BQ, BH, (S / BQ) * BH};
-  const int d = H * DH;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  auto nkv_of = [&](int qb) { return CAUSAL ? qb + 1 : S / BKV; };
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tm);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&q_full[i], 1);
-      mbar_init(&q_empty[i], 1);
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
-      mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 128);
-      mbar_init(&p_full[i], 128);
-      mbar_init(&p_empty[i], 1);
-      mbar_init(&o_full[i], 1);
-      mbar_init(&o_empty[i], 128);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc<512>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      int g = 0, it = 0;
-      for (int i = blockIdx.x; i < W.n_items; i += gridDim.x, ++it) {
-        int bh, qb;
-        W.item(i, CAUSAL, bh, qb);
-        const int b = bh / H, h = bh % H, row0 = b * S;
-        const int qs = it & 1;
-        mbar_wait(&q_empty[qs], ((it >> 1) & 1) ^ 1);
-        mbar_expect_tx(&q_full[qs], kTileBytes);
-        tma_load_2d(sQ + qs * kTileBytes, &tm, &q_full[qs], h * DH, row0 + qb * BQ);
-        const int nkv = nkv_of(qb);
-        for (int j = 0; j < nkv; ++j, ++g) {
-          const int st = g & 1;
-          mbar_wait(&kv_empty[st], ((g >> 1) & 1) ^ 1);
-          mbar_expect_tx(&kv_full[st], 2 * kTileBytes);
-          tma_load_2d(sK + st * kTileBytes, &tm, &kv_full[st], d + h * DH, row0 + j * BKV);
-          tma_load_2d(sV + st * kTileBytes, &tm, &kv_full[st], 2 * d + h * DH, row0 + j * BKV);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc_s = idesc_bf16_f32(BQ, BKV, 0, 0);  // Q K-major, K K-major
-      constexpr uint32_t idesc_o = idesc_bf16_f32(BQ, DH, 0, 1);   // P K-major, V MN-major
-      // flattened (item, tile) sequence; S of tile g+1 is issued before PV of tile g
-      int it_s = 0, j_s = 0, i_s = blockIdx.x, nkv_s = 0;  // cursor of the next S to issue
-      if (i_s < W.n_items) {
-        int bh, qb;
-        W.item(i_s, CAUSAL, bh, qb);
-        nkv_s = nkv_of(qb);
-      }
-      int g_s = 0;
-      auto issue_next_s = [&]() -> bool {
-        if (i_s >= W.n_items) return false;
-        const int qs = it_s & 1;
-        if (j_s == 0) mbar_wait(&q_full[qs], (it_s >> 1) & 1);
-        const int st = g_s & 1, buf = g_s & 1;
-        mbar_wait(&kv_full[st], (g_s >> 1) & 1);
-        mbar_wait(&s_empty[buf], ((g_s >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t q_base = smem_u32(sQ + qs * kTileBytes), k_base = smem_u32(sK + st * kTileBytes);
-#pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk)
-          mma_bf16(tmem + buf * BKV, umma_desc_sw128(q_base + kk * 32, 16, 1024),
-                   umma_desc_sw128(k_base + kk * 32, 16, 1024), idesc_s, kk > 0);
-        mma_commit(&s_full[buf]);
-        ++g_s;
-        if (++j_s == nkv_s) {  // last Q K^T of this item: Q buffer free once it retires
-          mma_commit(&q_empty[qs]);
-          j_s = 0;
-          ++it_s;
-          i_s += gridDim.x;
-          if (i_s < W.n_items) {
-            int bh, qb;
-            W.item(i_s, CAUSAL, bh, qb);
-            nkv_s = nkv_of(qb);
-          }
-        }
-        return true;
-      };
-      issue_next_s();
-      for (int g = 0; g < g_s; ++g) {
-        issue_next_s();
-        const int st = g & 1, buf = g & 1;
-        mbar_wait(&p_full[buf], (g >> 1) & 1);
-        mbar_wait(&o_empty[buf], ((g >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t p_base = smem_u32(sP + buf * kPBytes);
-        const uint32_t v_base = smem_u32(sV + st * kTileBytes);
-#pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk)
-          mma_bf16(tmem + 2 * BKV + buf * DH,
-                   umma_desc_sw128(p_base + (kk >> 2) * (BQ * 128) + (kk & 3) * 32, 16, 1024),
-                   umma_desc_sw128(v_base + kk * 2048, BKV * 128, 1024), idesc_o, kk > 0);
-        mma_commit(&o_full[buf]);
-        mma_commit(&kv_empty[st]);
-        mma_commit(&p_empty[buf]);
-      }
-    }
-  } else if (warp >= 4) {
-    const int q = warp & 3;
-    const int r = q * 32 + lane;  // query row inside the block == TMEM lane
-    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    int g = 0;
-    for (int i = blockIdx.x; i < W.n_items; i += gridDim.x) {
-      int bh, qb;
-      W.item(i, CAUSAL, bh, qb);
-      const int b = bh / H, h = bh % H, row0 = b * S;
-      const int nkv = nkv_of(qb);
-      float o[DH];
-#pragma unroll
-      for (int c = 0; c < DH; ++c) o[c] = 0.f;
-      float m = -INFINITY, l = 0.f, alpha_prev = 1.f;
-      auto add_o = [&](int gg, float alpha) {
-        const int buf = gg & 1;
-        mbar_wait(&o_full[buf], (gg >> 1) & 1);
-        tc_fence_after();
-        uint32_t v[DH];
-#pragma unroll
-        for (int c0 = 0; c0 < DH; c0 += 32)
-          tmem_ld_32x32b_x32(tmem + lane_addr + 2 * BKV + buf * DH + c0, *reinterpret_cast<uint32_t(*)[32]>(v + c0));
-        tmem_ld_wait();
-        tc_fence_before();
-        mbar_arrive(&o_empty[buf]);
-#pragma unroll
-        for (int c = 0; c < DH; ++c) o[c] = o[c] * alpha + __uint_as_float(v[c]);
-      };
-      for (int j = 0; j < nkv; ++j, ++g) {
-        const int buf = g & 1;
-        mbar_wait(&s_full[buf], (g >> 1) & 1);
-        tc_fence_after();
-        const uint32_t s_addr = tmem + lane_addr + buf * BKV;
-        uint32_t v[BKV];
-#pragma unroll
-        for (int c0 = 0; c0 < BKV; c0 += 32)
-          tmem_ld_32x32b_x32(s_addr + c0, *reinterpret_cast<uint32_t(*)[32]>(v + c0));
-        tmem_ld_wait();
-        if (CAUSAL && j == qb) {  // mask on the diagonal tile (key > query)
-#pragma unroll
-          for (int c = 0; c < BKV; ++c)
-            if (c > r) v[c] = __float_as_uint(-INFINITY);
-        }
-        float mx8[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) mx8[e] = __uint_as_float(v[e]);
-#pragma unroll
-        for (int c = 8; c < BKV; ++c) mx8[c & 7] = fmaxf(mx8[c & 7], __uint_as_float(v[c]));
-        const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-        const float m_new = fmaxf(m, mx * scale_log2);
-        const float alpha = ex2(m - m_new);
-        m = m_new;
-        mbar_wait(&p_empty[buf], ((g >> 1) & 1) ^ 1);
-        uint8_t *prow = sP + buf * kPBytes + r * 128;
-        float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int c0 = 0; c0 < BKV; c0 += 32) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int c = 0; c < 32; c += 2) {
-            const float p0 = ex2(fmaf(__uint_as_float(v[c0 + c]), scale_log2, -m_new));
-            const float p1 = ex2(fmaf(__uint_as_float(v[c0 + c + 1]), scale_log2, -m_new));
-            rs8[(c >> 1) & 7] += p0 + p1;
-            __nv_bfloat162 tb = __floats2bfloat162_rn(p0, p1);
-            pk[c >> 1] = *reinterpret_cast<uint32_t *>(&tb);
-          }
-          uint8_t *atom_row = prow + (c0 >> 6) * (BQ * 128);
-#pragma unroll
-          for (int ch = 0; ch < 4; ++ch) {
-            const int chunk = ((c0 & 63) >> 3) + ch;
-            *reinterpret_cast<uint4 *>(atom_row + ((chunk ^ (r & 7)) << 4)) =
-                make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
-          }
-        }
-        tc_fence_before();
-        mbar_arrive(&s_empty[buf]);
-        fence_async_smem();
-        mbar_arrive(&p_full[buf]);
-        const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
-        l = l * alpha + rs;
-        if (j > 0) add_o(g - 1, alpha_prev);
-        alpha_prev = alpha;
-      }
-      add_o(g - 1, alpha_prev);
-      const float inv = 1.f / l;
-      __nv_bfloat16 *orow = out + (int64_t)(row0 + qb * BQ + r) * d + h * DH;
-#pragma unroll
-      for (int c = 0; c < DH; c += 8) {
-        uint4 w;
-        uint32_t *wp = reinterpret_cast<uint32_t *>(&w);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          __nv_bfloat162 t = __floats2bfloat162_rn(o[c + 2 * e] * inv, o[c + 2 * e + 1] * inv);
-          wp[e] = *reinterpret_cast<uint32_t *>(&t);
-        }
-        *reinterpret_cast<uint4 *>(orow + c) = w;
-      }
-      lse[(int64_t)(row0 + qb * BQ + r) * H + h] = m + log2f(l);
-    }
-  }
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc<512>(tmem);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// forward, two query tiles per CTA (256 queries): two softmax warpgroups (A =
-// warps 4-7, B = warps 8-11; causal: query blocks p and nq-1-p, so every CTA
-// does the same work; full attention: 2p and 2p+1) share every K/V tile,
-// and the MMA thread interleaves them -- S_A(j+1) is issued while softmax B
-// works on S_B(j) and vice versa -- so the exp / pack work of one tile hides
-// the MMA and TMEM latencies of the other.  The S row is read from TMEM twice
-// (max pass, exp pass) in 32-column chunks to keep the thread under 168
-// registers (12 warps per CTA).
-// ---------------------------------------------------------------------------
-constexpr int kThreads2 = 384;
-constexpr size_t kSmem2 = 1024 + 2 * kTileBytes /*Q_A, Q_B*/ + 4 * kTileBytes /*K, V x2*/ + 2 * kPBytes /*P_A, P_B*/ + 512;
-
-template <bool CAUSAL>
-__global__ void __launch_bounds__(kThreads2, 1)
-    fwd2_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16 *__restrict__ out, float *__restrict__ lse,
-                int S, int H, float scale_log2) {
-  extern __shared__ uint8_t smem_raw[];
-  // 1024-B aligned base by pointer arithmetic on the __shared__ array, so the
-  // compiler keeps the shared address space (STS / LDS, not generic ST / LD)
-  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t *sQ = smem;                   // [2] query tiles
-  uint8_t *sK = sQ + 2 * kTileBytes;    // [2] stages
-  uint8_t *sV = sK + 2 * kTileBytes;    // [2] stages
-  uint8_t *sP = sV + 2 * kTileBytes;    // [2] tiles
-  uint64_t *bar = reinterpret_cast<uint64_t *>(sP + 2 * kPBytes);
-  uint64_t *q_full = bar;
-  uint64_t *kv_full = bar + 1, *kv_empty = bar + 3;
-  uint64_t *s_full = bar + 5, *s_empty = bar + 7;   // [tile]
-  uint64_t *p_full = bar + 9, *p_empty = bar + 11;  // [tile]
-  uint64_t *o_full = bar + 13, *o_empty = bar + 15; // [tile]
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 17);
-
-  const int nq = S / BQ;
-  const int pr = (int)blockIdx.x;
-  // causal: pair query block p with nq-1-p, so every CTA walks nq+1 KV tiles
-  // (balanced); full attention: consecutive blocks
-  const int qb_a = CAUSAL ? pr : 2 * pr, qb_b = CAUSAL ? nq - 1 - pr : 2 * pr + 1;
-  const int bh = blockIdx.y, b = bh / H, h = bh % H;
-  const int d = H * DH;
-  // KV tiles each query tile needs (nkv_b >= nkv_a)
-  const int nkv_a = CAUSAL ? qb_a + 1 : S / BKV, nkv_b = CAUSAL ? qb_b + 1 : S / BKV;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr uint32_t C_S = 0, C_O = 2 * BKV;  // TMEM: S_A, S_B | O_A, O_B
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tm);
-    mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
-      mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 128);
-      mbar_init(&p_full[i], 128);
-      mbar_init(&p_empty[i], 1);
-      mbar_init(&o_full[i], 1);
-      mbar_init(&o_empty[i], 128);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc<512>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const int row0 = b * S;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      mbar_expect_tx(q_full, 2 * kTileBytes);
-      tma_load_2d(sQ, &tm, q_full, h * DH, row0 + qb_a * BQ);
-      tma_load_2d(sQ + kTileBytes, &tm, q_full, h * DH, row0 + qb_b * BQ);
-      for (int j = 0; j < nkv_b; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[st], 2 * kTileBytes);
-        tma_load_2d(sK + st * kTileBytes, &tm, &kv_full[st], d + h * DH, row0 + j * BKV);
-        tma_load_2d(sV + st * kTileBytes, &tm, &kv_full[st], 2 * d + h * DH, row0 + j * BKV);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc_s = idesc_bf16_f32(BQ, BKV, 0, 0);
-      constexpr uint32_t idesc_o = idesc_bf16_f32(BQ, DH, 0, 1);
-      mbar_wait(q_full, 0);
-      auto issue_s = [&](int t, int j) {  // S_t(j) = Q_t K_j^T
-        const int st = j & 1;
-        if (t == 0) mbar_wait(&kv_full[st], (j >> 1) & 1);
-        mbar_wait(&s_empty[t], (j & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t q_base = smem_u32(sQ + t * kTileBytes), k_base = smem_u32(sK + st * kTileBytes);
-#pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk)
-          mma_bf16(tmem + C_S + t * BKV, umma_desc_sw128(q_base + kk * 32, 16, 1024),
-                   umma_desc_sw128(k_base + kk * 32, 16, 1024), idesc_s, kk > 0);
-        mma_commit(&s_full[t]);
-      };
-      auto issue_pv = [&](int t, int j) {  // O_t(j) = P_t(j) V_j
-        const int st = j & 1;
-        mbar_wait(&p_full[t], j & 1);
-        mbar_wait(&o_empty[t], (j & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t p_base = smem_u32(sP + t * kPBytes), v_base = smem_u32(sV + st * kTileBytes);
-#pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk)
-          mma_bf16(tmem + C_O + t * DH, umma_desc_sw128(p_base + (kk >> 2) * (BQ * 128) + (kk & 3) * 32, 16, 1024),
-                   umma_desc_sw128(v_base + kk * 2048, BKV * 128, 1024), idesc_o, kk > 0);
-        mma_commit(&o_full[t]);
-        mma_commit(&p_empty[t]);
-      };
-      if (nkv_a > 0) issue_s(0, 0);
-      else mbar_wait(&kv_full[0], 0);
-      issue_s(1, 0);
-      for (int j = 0; j < nkv_b; ++j) {
-        if (j < nkv_a) {
-          issue_pv(0, j);
-          if (j + 1 < nkv_a) issue_s(0, j + 1);
-        }
-        issue_pv(1, j);
-        mma_commit(&kv_empty[j & 1]);  // both tiles are done with K_j / V_j once these MMAs retire
-        if (j + 1 < nkv_b) {
-          if (!(j + 1 < nkv_a)) mbar_wait(&kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
-          issue_s(1, j + 1);
-        }
-      }
-    }
-  } else if (warp >= 4) {
-    const int t = (warp - 4) >> 2;  // query tile: 0 = A, 1 = B
-    const int qb = t == 0 ? qb_a : qb_b;
-    const int nkv = t == 0 ? nkv_a : nkv_b;
-    const int q = warp & 3;
-    const int r = q * 32 + lane;
-    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    const uint32_t s_addr = tmem + lane_addr + C_S + t * BKV;
-    float o[DH];
-#pragma unroll
-    for (int c = 0; c < DH; ++c) o[c] = 0.f;
-    float m = -INFINITY, l = 0.f, alpha_prev = 1.f;
-    auto add_o = [&](int j, float alpha) {
-      mbar_wait(&o_full[t], j & 1);
-      tc_fence_after();
-      uint32_t v[DH];
-#pragma unroll
-      for (int c0 = 0; c0 < DH; c0 += 32)
-        tmem_ld_32x32b_x32(tmem + lane_addr + C_O + t * DH + c0, *reinterpret_cast<uint32_t(*)[32]>(v + c0));
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(&o_empty[t]);
-#pragma unroll
-      for (int c = 0; c < DH; ++c) o[c] = o[c] * alpha + __uint_as_float(v[c]);
-    };
-    for (int j = 0; j < nkv; ++j) {
-      mbar_wait(&s_full[t], j & 1);
-      tc_fence_after();
-      const bool diag = CAUSAL && j == qb;
-      // pass 1: row max over four 32-column chunks
-      float mx = -INFINITY;
-#pragma unroll
-      for (int c0 = 0; c0 < BKV; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(s_addr + c0, v);
-        tmem_ld_wait();
-        float m8[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) m8[e] = -INFINITY;
-#pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const float x = (diag && c0 + c > r) ? -INFINITY : __uint_as_float(v[c]);
-          m8[c & 7] = fmaxf(m8[c & 7], x);
-        }
-        mx = fmaxf(mx, fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
-                              fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7]))));
-      }
-      const float m_new = fmaxf(m, mx * scale_log2);
-      const float alpha = ex2(m - m_new);
-      m = m_new;
-      // P_t(j) goes to smem: wait until PV_t(j-1) has consumed the previous P
-      mbar_wait(&p_empty[t], (j & 1) ^ 1);
-      uint8_t *prow = sP + t * kPBytes + r * 128;
-      float rs8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      // pass 2: exp, row sum, bf16 pack into the 128B-swizzled A operand
-#pragma unroll
-      for (int c0 = 0; c0 < BKV; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(s_addr + c0, v);
-        tmem_ld_wait();
-        uint32_t pk[16];
-#pragma unroll
-        for (int c = 0; c < 32; c += 2) {
-          float p0 = ex2(fmaf(__uint_as_float(v[c]), scale_log2, -m_new));
-          float p1 = ex2(fmaf(__uint_as_float(v[c + 1]), scale_log2, -m_new));
-          if (diag && c0 + c > r) p0 = 0.f;
-          if (diag && c0 + c + 1 > r) p1 = 0.f;
-          rs8[(c >> 1) & 7] += p0 + p1;
-          __nv_bfloat162 tb = __floats2bfloat162_rn(p0, p1);
-          pk[c >> 1] = *reinterpret_cast<uint32_t *>(&tb);
-        }
-        uint8_t *atom_row = prow + (c0 >> 6) * (BQ * 128);
-#pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
-          const int chunk = ((c0 & 63) >> 3) + ch;
-          *reinterpret_cast<uint4 *>(atom_row + ((chunk ^ (r & 7)) << 4)) =
-              make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
-        }
-      }
-      tc_fence_before();
-      mbar_arrive(&s_empty[t]);
-      fence_async_smem();
-      mbar_arrive(&p_full[t]);
-      const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
-      l = l * alpha + rs;
-      if (j > 0) add_o(j - 1, alpha_prev);
-      alpha_prev = alpha;
-    }
-    add_o(nkv - 1, alpha_prev);
-    const float inv = 1.f / l;
-    __nv_bfloat16 *orow = out + (int64_t)(row0 + qb * BQ + r) * d + h * DH;
-#pragma unroll
-    for (int c = 0; c < DH; c += 8) {
-      uint4 w;
-      uint32_t *wp = reinterpret_cast<uint32_t *>(&w);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        __nv_bfloat162 tb = __floats2bfloat162_rn(o[c + 2 * e] * inv, o[c + 2 * e + 1] * inv);
-        wp[e] = *reinterpret_cast<uint32_t *>(&tb);
-      }
-      *reinterpret_cast<uint4 *>(orow + c) = w;
-    }
-    lse[(int64_t)(row0 + qb * BQ + r) * H + h] = m + log2f(l);
-  }
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc<512>(tmem);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// forward, persistent with two query tiles per item: the ping-pong structure
-// of fwd2_kernel (softmax warpgroups A and B share every K/V tile) on the
-// persistent item loop of fwdp_kernel.  An item is the query-block pair
+// forward, persistent with two query tiles per item: softmax warpgroups A and
+// B share every K/V tile, and the MMA thread interleaves them (S_A(j+1) is
+// issued while softmax B works on S_B(j) and vice versa).  An item is the query-block pair
 // (2p, 2p+1) of one (sample, head): under causal masking the two tiles sweep
 // 2p+1 and 2p+2 K/V tiles, so the pair stays balanced, and the item list is
 // ordered heaviest first, so the persistent CTAs finish together.  The causal
@@ -1040,198 +336,6 @@ __global__ void __launch_bounds__(kThreads2, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// forward, lean variant: two CTAs per SM hide each other's latencies.  P goes
-// to TMEM (bf16 pairs packed into S's own columns, FA4-style) and is read by
-// the PV MMA as its A operand, O accumulates in TMEM (rescaled in place by the
-// softmax threads when the row max moves), so a CTA needs 80 KB of shared
-// memory, 256 TMEM columns and <= 128 registers per thread.
-// ---------------------------------------------------------------------------
-constexpr size_t kSmem3 = 1024 + kTileBytes /*Q*/ + 4 * kTileBytes /*K, V x2*/ + 256;
-
-template <bool CAUSAL>
-__global__ void __launch_bounds__(kThreads, 2)
-    fwd3_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16 *__restrict__ out, float *__restrict__ lse,
-                int S, int H, float scale_log2) {
-  extern __shared__ uint8_t smem_raw[];
-  // 1024-B aligned base by pointer arithmetic on the __shared__ array, so the
-  // compiler keeps the shared address space (STS / LDS, not generic ST / LD)
-  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t *sQ = smem;
-  uint8_t *sK = sQ + kTileBytes;
-  uint8_t *sV = sK + 2 * kTileBytes;
-  uint64_t *bar = reinterpret_cast<uint64_t *>(sV + 2 * kTileBytes);
-  uint64_t *q_full = bar;
-  uint64_t *kv_full = bar + 1, *kv_empty = bar + 3;
-  uint64_t *s_full = bar + 5, *p_full = bar + 6, *o_full = bar + 7;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 8);
-
-  const int nq = S / BQ;
-  const int qb = CAUSAL ? nq - 1 - (int)blockIdx.x : (int)blockIdx.x;
-  const int bh = blockIdx.y, b = bh / H, h = bh % H;
-  const int d = H * DH;
-  const int nkv = CAUSAL ? qb + 1 : S / BKV;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr uint32_t C_S = 0, C_O = BKV;  // S (fp32, 128 cols; P bf16 pairs in its first 64) | O (64 cols)
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tm);
-    mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
-    }
-    mbar_init(s_full, 1);
-    mbar_init(p_full, 128);
-    mbar_init(o_full, 1);
-    fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc<256>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const int row0 = b * S;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      mbar_expect_tx(q_full, kTileBytes);
-      tma_load_2d(sQ, &tm, q_full, h * DH, row0 + qb * BQ);
-      for (int j = 0; j < nkv; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[st], 2 * kTileBytes);
-        tma_load_2d(sK + st * kTileBytes, &tm, &kv_full[st], d + h * DH, row0 + j * BKV);
-        tma_load_2d(sV + st * kTileBytes, &tm, &kv_full[st], 2 * d + h * DH, row0 + j * BKV);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc_s = idesc_bf16_f32(BQ, BKV, 0, 0);
-      constexpr uint32_t idesc_o = idesc_bf16_f32(BQ, DH, 0, 1);
-      mbar_wait(q_full, 0);
-      const uint32_t q_base = smem_u32(sQ);
-      for (int j = 0; j < nkv; ++j) {
-        const int st = j & 1;
-        mbar_wait(&kv_full[st], (j >> 1) & 1);
-        if (j > 0) mbar_wait(p_full, (j - 1) & 1);  // PV_{j-1} is issued before S_j overwrites its P
-        tc_fence_after();
-        const uint32_t k_base = smem_u32(sK + st * kTileBytes);
-#pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk)
-          mma_bf16(tmem + C_S, umma_desc_sw128(q_base + kk * 32, 16, 1024),
-                   umma_desc_sw128(k_base + kk * 32, 16, 1024), idesc_s, kk > 0);
-        mma_commit(s_full);
-        // O += P_j V_j once the softmax has packed P_j and rescaled O
-        mbar_wait(p_full, j & 1);
-        tc_fence_after();
-        const uint32_t v_base = smem_u32(sV + st * kTileBytes);
-#pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk)
-          mma_bf16_ts(tmem + C_O, tmem + C_S + kk * 8, umma_desc_sw128(v_base + kk * 2048, BKV * 128, 1024), idesc_o,
-                      (j > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(o_full);
-        mma_commit(&kv_empty[st]);
-      }
-    }
-  } else if (warp >= 4) {
-    const int q = warp & 3;
-    const int r = q * 32 + lane;
-    const uint32_t lane_addr = (uint32_t)(q * 32) << 16;
-    const uint32_t s_addr = tmem + lane_addr + C_S, o_addr = tmem + lane_addr + C_O;
-    float m = -INFINITY, l = 0.f;
-    for (int j = 0; j < nkv; ++j) {
-      mbar_wait(s_full, j & 1);
-      tc_fence_after();
-      const bool diag = CAUSAL && j == qb;
-      float mx = -INFINITY;
-#pragma unroll
-      for (int c0 = 0; c0 < BKV; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(s_addr + c0, v);
-        tmem_ld_wait();
-        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-        for (int c = 0; c < 32; ++c) {
-          const float x = (diag && c0 + c > r) ? -INFINITY : __uint_as_float(v[c]);
-          m4[c & 3] = fmaxf(m4[c & 3], x);
-        }
-        mx = fmaxf(mx, fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])));
-      }
-      const float m_new = fmaxf(m, mx * scale_log2);
-      const float alpha = ex2(m - m_new);
-      m = m_new;
-      if (j > 0) {  // O_{j-1} complete: rescale it in place before PV_j accumulates
-        mbar_wait(o_full, (j - 1) & 1);
-        tc_fence_after();
-        if (__any_sync(0xffffffffu, alpha != 1.f)) {  // warp-uniform: tcgen05.ld / st are .sync.aligned
-#pragma unroll
-          for (int c0 = 0; c0 < DH; c0 += 32) {
-            uint32_t ov[32];
-            tmem_ld_32x32b_x32(o_addr + c0, ov);
-            tmem_ld_wait();
-#pragma unroll
-            for (int c = 0; c < 32; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * alpha);
-            tmem_st_32x32b_x32(o_addr + c0, ov);
-          }
-        }
-      }
-      float rs4[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-      for (int c0 = 0; c0 < BKV; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(s_addr + c0, v);
-        tmem_ld_wait();
-        uint32_t pk[16];
-#pragma unroll
-        for (int c = 0; c < 32; c += 2) {
-          float p0 = ex2(fmaf(__uint_as_float(v[c]), scale_log2, -m_new));
-          float p1 = ex2(fmaf(__uint_as_float(v[c + 1]), scale_log2, -m_new));
-          if (diag && c0 + c > r) p0 = 0.f;
-          if (diag && c0 + c + 1 > r) p1 = 0.f;
-          rs4[(c >> 1) & 3] += p0 + p1;
-          __nv_bfloat162 tb = __floats2bfloat162_rn(p0, p1);
-          pk[c >> 1] = *reinterpret_cast<uint32_t *>(&tb);
-        }
-        // keys c0..c0+31 -> P columns c0/2..c0/2+15 (S columns already read)
-        tmem_st_32x32b_x16(s_addr + (c0 >> 1), pk);
-      }
-      tmem_st_wait();
-      l = l * alpha + ((rs4[0] + rs4[1]) + (rs4[2] + rs4[3]));
-      tc_fence_before();
-      mbar_arrive(p_full);
-    }
-    mbar_wait(o_full, (nkv - 1) & 1);
-    tc_fence_after();
-    const float inv = 1.f / l;
-    __nv_bfloat16 *orow = out + (int64_t)(row0 + qb * BQ + r) * d + h * DH;
-#pragma unroll
-    for (int c0 = 0; c0 < DH; c0 += 32) {
-      uint32_t ov[32];
-      tmem_ld_32x32b_x32(o_addr + c0, ov);
-      tmem_ld_wait();
-#pragma unroll
-      for (int c = 0; c < 32; c += 8) {
-        uint4 w;
-        uint32_t *wp = reinterpret_cast<uint32_t *>(&w);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          __nv_bfloat162 tb = __floats2bfloat162_rn(__uint_as_float(ov[c + 2 * e]) * inv,
-                                                    __uint_as_float(ov[c + 2 * e + 1]) * inv);
-          wp[e] = *reinterpret_cast<uint32_t *>(&tb);
-        }
-        *reinterpret_cast<uint4 *>(orow + c0 + c) = w;
-      }
-    }
-    lse[(int64_t)(row0 + qb * BQ + r) * H + h] = m + log2f(l);
-  }
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc<256>(tmem);
   }
 }
 
@@ -1591,6 +695,13 @@ int backward_main(const void *qkv, const void *dout, const float *lse, const flo
 bool supported(int S, int DHx) { return DHx == DH && S % BQ == 0; }
 
 int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causal, cudaStream_t s) {
+  // HM_ATTN_FWD: unset = attention_fwd64.cu (rotating S buffers in TMEM, whole-row
+  // softmax in registers); q = the persistent query-block-pair kernel below (the
+  // round-1 default, S % 256 == 0); t = attention_tc128.cu's dataflow at head_dim 64
+  static const char *mode_env = getenv("HM_ATTN_FWD");
+  static const char mode = mode_env ? mode_env[0] : 'd';
+  if (mode == 't') return attn_tc128::forward64(qkv, o, lse, B, S, H, causal, s);
+  if (mode != 'q' || S % (2 * BQ) != 0) return attn_fwd64::forward(qkv, o, lse, B, S, H, causal, s);
   EncodeFn fn = encode_fn();
   if (!fn) return fail(HM_ERR_DEVICE, "cuTensorMapEncodeTiled unavailable");
   const int d = H * DH;
@@ -1605,87 +716,17 @@ int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causa
     return fail(HM_ERR_DEVICE, "attention tensor map encode failed");
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
   ProfScope ps(KC_ATTN_FWD, s, 4.0 * B * (double)S * S * H * DH * (causal ? 0.5 : 1.0), (double)B * S * H * DH * 2 * 4);
-  // HM_ATTN_FWD: unset = persistent kernel over query-block pairs (S % 256 ==
-  // 0; causal from S = 1024), else the persistent single-tile kernel (causal)
-  // or one CTA per query block; 1 = one CTA per query block; 2 = two tiles per CTA (full
-  // attention); 3 = lean (P/O in TMEM); p = persistent single tile; q =
-  // persistent pairs
-  static const char *mode_env = getenv("HM_ATTN_FWD");
-  static const char mode = mode_env ? mode_env[0] : 'd';
-  // t = query-tile pairs with P and O resident in TMEM (attention_tc128.cu's
-  // dataflow at head_dim 64)
-  if (mode == 't') return attn_tc128::forward64(qkv, o, lse, B, S, H, causal, s);
-  // f = rotating S buffers in TMEM, whole-row softmax in registers (attention_fwd64.cu)
-  if (mode == 'f') return attn_fwd64::forward(qkv, o, lse, B, S, H, causal, s);
-  const bool two_tiles = mode == '2';
-  // two query tiles per CTA (ping-pong softmax warpgroups) for full attention:
-  // 1.31x at 8 x 512 x 16 heads.
-  if (two_tiles && !causal && S % (2 * BQ) == 0) {
-    static bool attr2[2] = {false, false};
-    auto k2 = causal ? fwd2_kernel<true> : fwd2_kernel<false>;
-    if (!attr2[causal ? 1 : 0]) {
-      HM_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem2));
-      attr2[causal ? 1 : 0] = true;
-    }
-    k2<<<dim3(S / (2 * BQ), B * H), kThreads2, kSmem2, s>>>(tm, static_cast<__nv_bfloat16 *>(o), lse, S, H, scale_log2);
-    count_launch();
-    HM_CUDA(cudaGetLastError());
-    return HM_OK;
+  static bool attrq[2] = {false, false};
+  static int sms_q = 0;
+  if (!sms_q) HM_CUDA(cudaDeviceGetAttribute(&sms_q, cudaDevAttrMultiProcessorCount, 0));
+  auto kq = causal ? fwd2p_kernel<true> : fwd2p_kernel<false>;
+  if (!attrq[causal ? 1 : 0]) {
+    HM_CUDA(cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem2P));
+    attrq[causal ? 1 : 0] = true;
   }
-  // pairs win from S = 1024 causal (1771 vs 2073 ns per tile and SM, 25 heads);
-  // shorter causal sequences have too little work per pair
-  if ((mode == 'q' || (mode == 'd' && (!causal || S >= 1024))) && S % (2 * BQ) == 0) {  // persistent pairs
-    static bool attrq[2] = {false, false};
-    static int sms_q = 0;
-    if (!sms_q) HM_CUDA(cudaDeviceGetAttribute(&sms_q, cudaDevAttrMultiProcessorCount, 0));
-    auto kq = causal ? fwd2p_kernel<true> : fwd2p_kernel<false>;
-    if (!attrq[causal ? 1 : 0]) {
-      HM_CUDA(cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem2P));
-      attrq[causal ? 1 : 0] = true;
-    }
-    const int items = (S / (2 * BQ)) * B * H;
-    kq<<<dim3(items < sms_q ? items : sms_q), kThreads2, kSmem2P, s>>>(tm, static_cast<__nv_bfloat16 *>(o), lse, S, H,
-                                                                      B * H, scale_log2);
-    count_launch();
-    HM_CUDA(cudaGetLastError());
-    return HM_OK;
-  }
-  if (mode == 'p' || (mode == 'd' && causal)) {  // persistent, one CTA per SM
-    static bool attrp[2] = {false, false};
-    static int sms = 0;
-    if (!sms) HM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-    auto kp = causal ? fwdp_kernel<true> : fwdp_kernel<false>;
-    if (!attrp[causal ? 1 : 0]) {
-      HM_CUDA(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemP));
-      attrp[causal ? 1 : 0] = true;
-    }
-    const int items = (S / BQ) * B * H;
-    kp<<<dim3(items < sms ? items : sms), kThreads, kSmemP, s>>>(tm, static_cast<__nv_bfloat16 *>(o), lse, S, H, B * H,
-                                                                  scale_log2);
-    count_launch();
-    HM_CUDA(cudaGetLastError());
-    return HM_OK;
-  }
-  static const bool lean = mode == '3';
-  if (lean) {  // P / O in TMEM, two CTAs per SM (experimental)
-    static bool attr3[2] = {false, false};
-    auto k3 = causal ? fwd3_kernel<true> : fwd3_kernel<false>;
-    if (!attr3[causal ? 1 : 0]) {
-      HM_CUDA(cudaFuncSetAttribute(k3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem3));
-      attr3[causal ? 1 : 0] = true;
-    }
-    k3<<<dim3(S / BQ, B * H), kThreads, kSmem3, s>>>(tm, static_cast<__nv_bfloat16 *>(o), lse, S, H, scale_log2);
-    count_launch();
-    HM_CUDA(cudaGetLastError());
-    return HM_OK;
-  }
-  static bool attr[2] = {false, false};
-  auto k = causal ? fwd_kernel<true> : fwd_kernel<false>;
-  if (!attr[causal ? 1 : 0]) {
-    HM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
-    attr[causal ? 1 : 0] = true;
-  }
-  k<<<dim3(S / BQ, B * H), kThreads, kSmem, s>>>(tm, static_cast<__nv_bfloat16 *>(o), lse, S, H, scale_log2);
+  const int items = (S / (2 * BQ)) * B * H;
+  kq<<<dim3(items < sms_q ? items : sms_q), kThreads2, kSmem2P, s>>>(tm, static_cast<__nv_bfloat16 *>(o), lse, S, H,
+                                                                    B * H, scale_log2);
   count_launch();
   HM_CUDA(cudaGetLastError());
   return HM_OK;

@@ -624,9 +624,12 @@ static int env_int(const char *name) {
 // HM_GEMM_SPLITK force a choice.
 static int g_force_bn = env_int("HM_GEMM_BN"), g_force_cg = env_int("HM_GEMM_CG"),
            g_force_s = env_int("HM_GEMM_SPLITK");
-// stream-K for ACC_F32: unset = by the cost model, 0 = never, 1 = always
-// (HM_GEMM_SPLITK / hm_k_gemm_set_tile splits = -1 also force it)
-static const int g_streamk = getenv("HM_GEMM_STREAMK") ? atoi(getenv("HM_GEMM_STREAMK")) : -1;
+// stream-K for ACC_F32: 1 = always, -1 = when the cost model prefers it, unset / 0 =
+// never (hm_k_gemm_set_tile splits = -1 also forces it).  Off by default: on the
+// GPT-2 XL weight-gradient shapes it measured 2-9% slower than the split-K units
+// the model picks (profiles/r02_gemm_streamk_ab.jsonl): every CTA pair touches 3-4
+// tile segments, each paying a pipeline fill and a full-tile reduce-add epilogue.
+static const int g_streamk = getenv("HM_GEMM_STREAMK") ? atoi(getenv("HM_GEMM_STREAMK")) : 0;
 // 128 x 192 single-CTA tiles (fit 1600-wide outputs in 9 column tiles)
 static const bool g_tile192 = getenv("HM_GEMM_192") ? atoi(getenv("HM_GEMM_192")) != 0 : true;
 static const double g_eff192 = getenv("HM_GEMM_EFF192") ? atof(getenv("HM_GEMM_EFF192")) : 0.70;

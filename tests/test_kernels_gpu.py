@@ -365,7 +365,7 @@ def test_attention_bwd_tcgen05_opt_in():
     assert r.returncode == 0, r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("mode", ["1", "2", "3", "p", "q", "t", "f"])
+@pytest.mark.parametrize("mode", ["q", "t", "d"])
 def test_attention_fwd_every_variant(mode):
     """Every forward variant (HM_ATTN_FWD is read once per process, so each runs
     in a subprocess) on shapes where the persistent kernel walks one item per
