@@ -358,24 +358,36 @@ static EncodeFn encode_fn() {
 
 
 // ---------------------------------------------------------------------------
-// backward: one CTA per (sample, head, 128-key block), looping over the query
-// blocks that attend to it (FA2 dataflow on tcgen05):
+// backward (FA2 dataflow on tcgen05), persistent: one CTA per SM walks a list
+// of (sample-head, 128-key block) items, looping over the query blocks that
+// attend to each key block:
 //   S^T  = K Q^T        dP^T = V dO^T          (TMEM, 128 keys x 128 queries)
 //   P^T  = exp2(S^T * c - lse)   dS^T = P^T * (dP^T - D)   (bf16 -> smem)
 //   dV  += P^T dO       dK  += dS^T Q          (TMEM accumulators)
-//   dQ_i = dS K  -> fp32 atomics into dq_acc (scaled), converted by dq_convert
+//   dQ_i = dS K  -> one TMA reduce-add per block into dq_acc (scaled fp32),
+//                   converted by dq_convert
+// Causal items are listed heaviest first (key block 0 sees every query
+// block) and dealt to the CTAs in a snake order (round r: CTA c takes item
+// r G + c for even r, r G + G - 1 - c for odd r), so the CTAs finish
+// together; TMEM allocation and barrier set-up are paid once per SM.  Every
+// ring / buffer parity follows one running block counter across items; the
+// next item's first S^T / dP^T only waits for its own K / V, and its first
+// dV / dK MMAs for the previous item's accumulators to have been drained.
 // ---------------------------------------------------------------------------
 constexpr uint32_t kDqStage = BQ * DH * 4;  // 32 KB: dQ tile (fp32) staged for the TMA reduce-add
 constexpr size_t kSmemBwd = 1024 + 2 * kTileBytes /*K,V*/ + 4 * kTileBytes /*Q,dO x2*/ + 2 * kPBytes /*P^T,dS^T*/ +
                             kDqStage +
                             2 * 2 * BQ * 4 /*lse,D x2*/ + 512;
 
+// the r-th item of CTA c of G (snake order over a heaviest-first list)
+__device__ __forceinline__ int bwd_item(int r, int c, int G) { return r * G + ((r & 1) ? G - 1 - c : c); }
+
 template <bool CAUSAL>
 __global__ void __launch_bounds__(kThreads2, 1)
     bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                const __grid_constant__ CUtensorMap tm_dq,
                const float *__restrict__ lse, const float *__restrict__ dvec, float *__restrict__ dq_acc,
-               __nv_bfloat16 *__restrict__ dqkv, int S, int H, float scale_log2, float scale) {
+               __nv_bfloat16 *__restrict__ dqkv, int S, int H, int BH, float scale_log2, float scale) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned base by pointer arithmetic on the __shared__ array, so the
   // compiler keeps the shared address space (STS / LDS, not generic ST / LD)
@@ -390,20 +402,30 @@ __global__ void __launch_bounds__(kThreads2, 1)
   float *sL = reinterpret_cast<float *>(sDQ + kDqStage);  // [2][128] lse
   float *sD = sL + 2 * BQ;                               // [2][128] D
   uint64_t *bar = reinterpret_cast<uint64_t *>(sD + 2 * BQ);
-  uint64_t *kv_full = bar;
-  uint64_t *q_full = bar + 1, *q_empty = bar + 3;
-  uint64_t *st_full = bar + 5, *st_empty = bar + 6;
-  uint64_t *p_full = bar + 7, *p_empty = bar + 8;
-  uint64_t *dq_full = bar + 9, *dq_empty = bar + 10, *acc_full = bar + 11;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 12);
+  uint64_t *kv_full = bar, *kv_empty = bar + 1;
+  uint64_t *q_full = bar + 2, *q_empty = bar + 4;
+  uint64_t *st_full = bar + 6, *st_empty = bar + 7;
+  uint64_t *p_full = bar + 8, *p_empty = bar + 9;
+  uint64_t *dq_full = bar + 10, *dq_empty = bar + 11;
+  uint64_t *acc_full = bar + 12, *acc_empty = bar + 13;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 14);
 
-  const int nq = S / BQ;
-  const int kb = blockIdx.x;
-  const int bh = blockIdx.y, b = bh / H, h = bh % H;
+  const int nq = S / BQ, nkb = S / BKV, n_items = nkb * BH;
+  const int G = gridDim.x, c = blockIdx.x;
   const int d = H * DH;
-  const int q_begin = CAUSAL ? kb : 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row0 = b * S;
+  auto decode = [&](int i, int &kb, int &b, int &h) {
+    int bh;
+    if (CAUSAL) {  // key block 0 first: it sees every query block
+      kb = i / BH;
+      bh = i % BH;
+    } else {
+      kb = i % nkb;
+      bh = i / nkb;
+    }
+    b = bh / H;
+    h = bh % H;
+  };
   // TMEM columns
   constexpr uint32_t C_ST = 0, C_DP = 128, C_DV = 256, C_DK = 320, C_DQ = 384;
 
@@ -412,6 +434,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     tma_prefetch(&tm_do);
     tma_prefetch(&tm_dq);
     mbar_init(kv_full, 1);
+    mbar_init(kv_empty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
@@ -423,6 +446,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     mbar_init(dq_full, 1);
     mbar_init(dq_empty, 256);
     mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 256);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -433,15 +457,22 @@ __global__ void __launch_bounds__(kThreads2, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(kv_full, 2 * kTileBytes);
-      tma_load_2d(sK, &tm_qkv, kv_full, d + h * DH, row0 + kb * BKV);
-      tma_load_2d(sV, &tm_qkv, kv_full, 2 * d + h * DH, row0 + kb * BKV);
-      for (int i = q_begin, n = 0; i < nq; ++i, ++n) {
-        const int st = n & 1;
-        mbar_wait(&q_empty[st], ((n >> 1) & 1) ^ 1);
-        mbar_expect_tx(&q_full[st], 2 * kTileBytes);
-        tma_load_2d(sQ + st * kTileBytes, &tm_qkv, &q_full[st], h * DH, row0 + i * BQ);
-        tma_load_2d(sdO + st * kTileBytes, &tm_do, &q_full[st], h * DH, row0 + i * BQ);
+      int n = 0;  // running query-block counter (Q / dO stage parities)
+      for (int r = 0, i; (i = bwd_item(r, c, G)) < n_items; ++r) {
+        int kb, b, h;
+        decode(i, kb, b, h);
+        const int row0 = b * S;
+        mbar_wait(kv_empty, (r & 1) ^ 1);  // every MMA of the previous item has read K / V
+        mbar_expect_tx(kv_full, 2 * kTileBytes);
+        tma_load_2d(sK, &tm_qkv, kv_full, d + h * DH, row0 + kb * BKV);
+        tma_load_2d(sV, &tm_qkv, kv_full, 2 * d + h * DH, row0 + kb * BKV);
+        for (int qi = CAUSAL ? kb : 0; qi < nq; ++qi, ++n) {
+          const int st = n & 1;
+          mbar_wait(&q_empty[st], ((n >> 1) & 1) ^ 1);
+          mbar_expect_tx(&q_full[st], 2 * kTileBytes);
+          tma_load_2d(sQ + st * kTileBytes, &tm_qkv, &q_full[st], h * DH, row0 + qi * BQ);
+          tma_load_2d(sdO + st * kTileBytes, &tm_do, &q_full[st], h * DH, row0 + qi * BQ);
+        }
       }
     }
   } else if (warp == 1) {
@@ -449,11 +480,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
       constexpr uint32_t id_kk = idesc_bf16_f32(128, 128, 0, 0);   // S^T, dP^T: K-major x K-major
       constexpr uint32_t id_kmn = idesc_bf16_f32(128, DH, 0, 1);   // dV, dK: A K-major, B MN-major
       constexpr uint32_t id_mnmn = idesc_bf16_f32(128, DH, 1, 1);  // dQ: A MN-major (dS), B MN-major (K)
-      mbar_wait(kv_full, 0);
       const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV);
       const uint32_t p_base = smem_u32(sP), ds_base = smem_u32(sdS);
-      const int count = nq - q_begin;
-      // S^T = K Q^T and dP^T = V dO^T of block n (TMEM C_ST / C_DP)
+      // S^T = K Q^T and dP^T = V dO^T of running block n (TMEM C_ST / C_DP)
       auto issue_st = [&](int n) {
         const int st = n & 1;
         mbar_wait(&q_full[st], (n >> 1) & 1);
@@ -469,56 +498,65 @@ __global__ void __launch_bounds__(kThreads2, 1)
         }
         mma_commit(st_full);
       };
-      issue_st(0);
-      for (int n = 0; n < count; ++n) {
-        const int st = n & 1;
-        const uint32_t ph = n & 1;
-        // block n+1's S^T / dP^T go in as soon as the softmax warps have read
-        // block n's (st_empty), ahead of block n's gradient MMAs, so the next
-        // elementwise pass never waits for them
-        if (n + 1 < count) issue_st(n + 1);
-        const uint32_t q_base = smem_u32(sQ + st * kTileBytes), do_base = smem_u32(sdO + st * kTileBytes);
-        mbar_wait(p_full, ph);
-        tc_fence_after();
+      int n = 0;
+      for (int r = 0, i; (i = bwd_item(r, c, G)) < n_items; ++r) {
+        int kb, b, h;
+        decode(i, kb, b, h);
+        const int count = nq - (CAUSAL ? kb : 0);
+        mbar_wait(kv_full, r & 1);
+        issue_st(n);
+        for (int blk = 0; blk < count; ++blk, ++n) {
+          const int st = n & 1;
+          const uint32_t ph = n & 1;
+          // block n+1's S^T / dP^T go in as soon as the softmax warps have read
+          // block n's (st_empty), ahead of block n's gradient MMAs, so the next
+          // elementwise pass never waits for them
+          if (blk + 1 < count) issue_st(n + 1);
+          const uint32_t q_base = smem_u32(sQ + st * kTileBytes), do_base = smem_u32(sdO + st * kTileBytes);
+          mbar_wait(p_full, ph);
+          if (blk == 0) mbar_wait(acc_empty, (r & 1) ^ 1);  // the previous item's dV / dK drained
+          tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < BQ / 16; ++kk) {  // reduction over the 128 queries
-          const uint32_t a_off = (kk >> 2) * (BKV * 128) + (kk & 3) * 32;
-          mma_bf16(tmem + C_DV, umma_desc_sw128(p_base + a_off, 16, 1024),
-                   umma_desc_sw128(do_base + kk * 2048, BQ * 128, 1024), id_kmn, (n > 0 || kk > 0) ? 1u : 0u);
-          mma_bf16(tmem + C_DK, umma_desc_sw128(ds_base + a_off, 16, 1024),
-                   umma_desc_sw128(q_base + kk * 2048, BQ * 128, 1024), id_kmn, (n > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < BQ / 16; ++kk) {  // reduction over the 128 queries
+            const uint32_t a_off = (kk >> 2) * (BKV * 128) + (kk & 3) * 32;
+            mma_bf16(tmem + C_DV, umma_desc_sw128(p_base + a_off, 16, 1024),
+                     umma_desc_sw128(do_base + kk * 2048, BQ * 128, 1024), id_kmn, (blk > 0 || kk > 0) ? 1u : 0u);
+            mma_bf16(tmem + C_DK, umma_desc_sw128(ds_base + a_off, 16, 1024),
+                     umma_desc_sw128(q_base + kk * 2048, BQ * 128, 1024), id_kmn, (blk > 0 || kk > 0) ? 1u : 0u);
+          }
+          mbar_wait(dq_empty, ph ^ 1);  // the previous block's dQ has left TMEM
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < BKV / 16; ++kk)  // reduction over the 128 keys
+            mma_bf16(tmem + C_DQ, umma_desc_sw128(ds_base + kk * 2048, BKV * 128, 1024),
+                     umma_desc_sw128(k_base + kk * 2048, BKV * 128, 1024), id_mnmn, kk > 0);
+          mma_commit(dq_full);
+          mma_commit(&q_empty[st]);
+          mma_commit(p_empty);
         }
-        mbar_wait(dq_empty, ph ^ 1);  // the previous block's dQ has left TMEM
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk)  // reduction over the 128 keys
-          mma_bf16(tmem + C_DQ, umma_desc_sw128(ds_base + kk * 2048, BKV * 128, 1024),
-                   umma_desc_sw128(k_base + kk * 2048, BKV * 128, 1024), id_mnmn, kk > 0);
-        mma_commit(dq_full);
-        mma_commit(&q_empty[st]);
-        mma_commit(p_empty);
+        mma_commit(acc_full);
+        mma_commit(kv_empty);
       }
-      mma_commit(acc_full);
     }
   } else if (warp >= 4) {
     // two softmax warpgroups on the same TMEM lanes (key rows): warpgroup wg
     // owns queries [64 wg, 64 wg + 64) of every block, half of dQ's columns,
-    // and dV (wg 0) or dK (wg 1) at the end -- two warps per SM sub-partition
-    // hide each other's MUFU / TMEM / shared-memory latencies
+    // and dV (wg 0) or dK (wg 1) at the end of an item -- two warps per SM
+    // sub-partition hide each other's MUFU / TMEM / shared-memory latencies
     const int wg = (warp - 4) >> 2;
     const int q4 = warp & 3;
-    const int r = q4 * 32 + lane;  // key row (S^T, dP^T, dV, dK) / query row (dQ) == TMEM lane
+    const int rr = q4 * 32 + lane;  // key row (S^T, dP^T, dV, dK) / query row (dQ) == TMEM lane
     const uint32_t lane_addr = (uint32_t)(q4 * 32) << 16;
     // lse (wg 0) and D (wg 1) of the query blocks (tiny, strided: plain
     // loads), fetched one block ahead so their latency hides behind the
     // previous block's work
     const float *src = wg == 0 ? lse : dvec;
     float *dst = wg == 0 ? sL : sD;
-    float x_next = src[(int64_t)(row0 + q_begin * BQ + r) * H + h];
-    // dQ of block nn (query block qblk): TMEM -> one TMA reduce-add of the whole
-    // 128 x 64 fp32 tile (in L2) instead of 8192 scalar atomics, staged in
-    // SW128 rows (conflict-free writes); each warpgroup drains 32 columns
-    auto dq_out = [&](int qblk, int nn) {
+    // dQ of running block nn (query block qblk of the item at row0 / head h):
+    // TMEM -> one TMA reduce-add of the whole 128 x 64 fp32 tile (in L2)
+    // instead of 8192 scalar atomics, staged in SW128 rows (conflict-free
+    // writes); each warpgroup drains 32 columns
+    auto dq_out = [&](int qrow, int hh, int nn) {
       mbar_wait(dq_full, nn & 1);
       tc_fence_after();
       uint32_t q[32];
@@ -526,117 +564,131 @@ __global__ void __launch_bounds__(kThreads2, 1)
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(dq_empty);
-      if (wg == 0 && r == 0) bulk_wait_read0();  // the previous block's reduce has read the stage
+      if (wg == 0 && rr == 0) bulk_wait_read0();  // the previous block's reduce has read the stage
       asm volatile("bar.sync 2, 256;" ::: "memory");
-      uint8_t *chunk = sDQ + wg * (BQ * 128) + r * 128;
+      uint8_t *chunk = sDQ + wg * (BQ * 128) + rr * 128;
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        *reinterpret_cast<float4 *>(chunk + ((j ^ (r & 7)) << 4)) =
+        *reinterpret_cast<float4 *>(chunk + ((j ^ (rr & 7)) << 4)) =
             make_float4(__uint_as_float(q[4 * j]) * scale, __uint_as_float(q[4 * j + 1]) * scale,
                         __uint_as_float(q[4 * j + 2]) * scale, __uint_as_float(q[4 * j + 3]) * scale);
       fence_async_smem();
       asm volatile("bar.sync 2, 256;" ::: "memory");
-      if (wg == 0 && r == 0) {
+      if (wg == 0 && rr == 0) {
 #pragma unroll
-        for (int c = 0; c < DH / 32; ++c)
-          tma_reduce_add_2d(&tm_dq, sDQ + c * (BQ * 128), h * DH + 32 * c, row0 + qblk * BQ);
+        for (int cc = 0; cc < DH / 32; ++cc)
+          tma_reduce_add_2d(&tm_dq, sDQ + cc * (BQ * 128), hh * DH + 32 * cc, qrow);
         bulk_commit();
       }
     };
     const int hq = wg;
-    uint8_t *prow = sP + r * 128 + hq * (BKV * 128);
-    uint8_t *dsrow = sdS + r * 128 + hq * (BKV * 128);
-    for (int i = q_begin, n = 0; i < nq; ++i, ++n) {
-      const int st = n & 1;
-      const uint32_t ph = n & 1;
-      dst[st * BQ + r] = x_next;
-      if (i + 1 < nq) x_next = src[(int64_t)(row0 + (i + 1) * BQ + r) * H + h];
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      mbar_wait(st_full, ph);
-      tc_fence_after();
-      const bool diag = CAUSAL && i == kb;
-      const float *Ls = sL + st * BQ;
-      const float *Ds = sD + st * BQ;
-      // this warpgroup's 64 queries in two 32-column chunks; the first chunk is
-      // computed before waiting for the previous block's gradient MMAs to
-      // release P^T / dS^T, so that wait overlaps it
+    uint8_t *prow = sP + rr * 128 + hq * (BKV * 128);
+    uint8_t *dsrow = sdS + rr * 128 + hq * (BKV * 128);
+    int n = 0;
+    int prev_qrow = 0, prev_h = 0;  // the block whose dQ is drained next
+    for (int r = 0, it; (it = bwd_item(r, c, G)) < n_items; ++r) {
+      int kb, b, h;
+      decode(it, kb, b, h);
+      const int row0 = b * S;
+      const int q_begin = CAUSAL ? kb : 0;
+      float x_next = src[(int64_t)(row0 + q_begin * BQ + rr) * H + h];
+      for (int i = q_begin; i < nq; ++i, ++n) {
+        const int st = n & 1;
+        const uint32_t ph = n & 1;
+        dst[st * BQ + rr] = x_next;
+        if (i + 1 < nq) x_next = src[(int64_t)(row0 + (i + 1) * BQ + rr) * H + h];
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        mbar_wait(st_full, ph);
+        tc_fence_after();
+        const bool diag = CAUSAL && i == kb;
+        const float *Ls = sL + st * BQ;
+        const float *Ds = sD + st * BQ;
+        // this warpgroup's 64 queries in two 32-column chunks; the first chunk is
+        // computed before waiting for the previous block's gradient MMAs to
+        // release P^T / dS^T, so that wait overlaps it
 #pragma unroll
-      for (int c0 = 0; c0 < 64; c0 += 32) {
-        uint32_t sv[32], dp[32];
-        tmem_ld_32x32b_x32(tmem + lane_addr + C_ST + hq * 64 + c0, sv);
-        tmem_ld_32x32b_x32(tmem + lane_addr + C_DP + hq * 64 + c0, dp);
-        tmem_ld_wait();
-        if (c0 == 32) {
-          tc_fence_before();
-          mbar_arrive(st_empty);  // S^T / dP^T fully read: the next block's MMAs may overwrite
-        }
-        uint32_t pk[16], dk[16];
-        // the causal mask is a separate instantiation: only the diagonal block pays for it
-        auto elementwise = [&](auto diag_tag) {
-          constexpr bool DIAG = decltype(diag_tag)::value;
-#pragma unroll
-          for (int c = 0; c < 32; c += 4) {
-            const int qi = hq * 64 + c0 + c;
-            // lse / D of four queries per 16-B shared-memory load (broadcast)
-            const float4 L4 = *reinterpret_cast<const float4 *>(Ls + qi);
-            const float4 D4 = *reinterpret_cast<const float4 *>(Ds + qi);
-            const float lq[4] = {L4.x, L4.y, L4.z, L4.w}, dq4[4] = {D4.x, D4.y, D4.z, D4.w};
-            float p[4], g[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              p[k] = ex2(fmaf(__uint_as_float(sv[c + k]), scale_log2, -lq[k]));
-              if (DIAG && qi + k < r) p[k] = 0.f;  // query < key: masked
-              g[k] = p[k] * (__uint_as_float(dp[c + k]) - dq4[k]);
-            }
-            __nv_bfloat162 tp0 = __floats2bfloat162_rn(p[0], p[1]), tp1 = __floats2bfloat162_rn(p[2], p[3]);
-            __nv_bfloat162 td0 = __floats2bfloat162_rn(g[0], g[1]), td1 = __floats2bfloat162_rn(g[2], g[3]);
-            pk[c >> 1] = *reinterpret_cast<uint32_t *>(&tp0);
-            pk[(c >> 1) + 1] = *reinterpret_cast<uint32_t *>(&tp1);
-            dk[c >> 1] = *reinterpret_cast<uint32_t *>(&td0);
-            dk[(c >> 1) + 1] = *reinterpret_cast<uint32_t *>(&td1);
+        for (int c0 = 0; c0 < 64; c0 += 32) {
+          uint32_t sv[32], dp[32];
+          tmem_ld_32x32b_x32(tmem + lane_addr + C_ST + hq * 64 + c0, sv);
+          tmem_ld_32x32b_x32(tmem + lane_addr + C_DP + hq * 64 + c0, dp);
+          tmem_ld_wait();
+          if (c0 == 32) {
+            tc_fence_before();
+            mbar_arrive(st_empty);  // S^T / dP^T fully read: the next block's MMAs may overwrite
           }
-        };
-        if (diag) elementwise(std::true_type{});
-        else elementwise(std::false_type{});
-        if (c0 == 0) mbar_wait(p_empty, ph ^ 1);  // the previous block's MMAs have consumed P^T / dS^T
+          uint32_t pk[16], dk[16];
+          // the causal mask is a separate instantiation: only the diagonal block pays for it
+          auto elementwise = [&](auto diag_tag) {
+            constexpr bool DIAG = decltype(diag_tag)::value;
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
-          const uint32_t off = (((c0 >> 3) + ch) ^ (r & 7)) << 4;
-          *reinterpret_cast<uint4 *>(prow + off) = make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
-          *reinterpret_cast<uint4 *>(dsrow + off) = make_uint4(dk[4 * ch], dk[4 * ch + 1], dk[4 * ch + 2], dk[4 * ch + 3]);
+            for (int cq = 0; cq < 32; cq += 4) {
+              const int qi = hq * 64 + c0 + cq;
+              // lse / D of four queries per 16-B shared-memory load (broadcast)
+              const float4 L4 = *reinterpret_cast<const float4 *>(Ls + qi);
+              const float4 D4 = *reinterpret_cast<const float4 *>(Ds + qi);
+              const float lq[4] = {L4.x, L4.y, L4.z, L4.w}, dq4[4] = {D4.x, D4.y, D4.z, D4.w};
+              float p[4], g[4];
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                p[k] = ex2(fmaf(__uint_as_float(sv[cq + k]), scale_log2, -lq[k]));
+                if (DIAG && qi + k < rr) p[k] = 0.f;  // query < key: masked
+                g[k] = p[k] * (__uint_as_float(dp[cq + k]) - dq4[k]);
+              }
+              __nv_bfloat162 tp0 = __floats2bfloat162_rn(p[0], p[1]), tp1 = __floats2bfloat162_rn(p[2], p[3]);
+              __nv_bfloat162 td0 = __floats2bfloat162_rn(g[0], g[1]), td1 = __floats2bfloat162_rn(g[2], g[3]);
+              pk[cq >> 1] = *reinterpret_cast<uint32_t *>(&tp0);
+              pk[(cq >> 1) + 1] = *reinterpret_cast<uint32_t *>(&tp1);
+              dk[cq >> 1] = *reinterpret_cast<uint32_t *>(&td0);
+              dk[(cq >> 1) + 1] = *reinterpret_cast<uint32_t *>(&td1);
+            }
+          };
+          if (diag) elementwise(std::true_type{});
+          else elementwise(std::false_type{});
+          if (c0 == 0) mbar_wait(p_empty, ph ^ 1);  // the previous block's MMAs have consumed P^T / dS^T
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch) {
+            const uint32_t off = (((c0 >> 3) + ch) ^ (rr & 7)) << 4;
+            *reinterpret_cast<uint4 *>(prow + off) = make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+            *reinterpret_cast<uint4 *>(dsrow + off) = make_uint4(dk[4 * ch], dk[4 * ch + 1], dk[4 * ch + 2], dk[4 * ch + 3]);
+          }
         }
+        fence_async_smem();
+        mbar_arrive(p_full);
+        // the previous block's dQ is complete by now (its MMAs finished before P^T
+        // could be rewritten): drain it while this block's gradient MMAs run
+        if (n > 0) dq_out(prev_qrow, prev_h, n - 1);
+        prev_qrow = row0 + i * BQ;
+        prev_h = h;
       }
-      fence_async_smem();
-      mbar_arrive(p_full);
-      // the previous block's dQ is complete by now (its MMAs finished before P^T
-      // could be rewritten): drain it while this block's gradient MMAs run
-      if (n > 0) dq_out(i - 1, n - 1);
-    }
-    dq_out(nq - 1, nq - 1 - q_begin);
-    if (wg == 0 && r == 0) bulk_wait0();
-    // dV (warpgroup 0) or dK (warpgroup 1) of this key block
-    mbar_wait(acc_full, 0);
-    tc_fence_after();
-    uint32_t acc[DH];
+      // dV (warpgroup 0) or dK (warpgroup 1) of this key block
+      mbar_wait(acc_full, r & 1);
+      tc_fence_after();
+      uint32_t acc[DH];
 #pragma unroll
-    for (int c0 = 0; c0 < DH; c0 += 32)
-      tmem_ld_32x32b_x32(tmem + lane_addr + (wg == 0 ? C_DV : C_DK) + c0, *reinterpret_cast<uint32_t(*)[32]>(acc + c0));
-    tmem_ld_wait();
-    const int64_t ld = 3 * (int64_t)d;
-    __nv_bfloat16 *orow = dqkv + (int64_t)(row0 + kb * BKV + r) * ld + (wg == 0 ? 2 * d : d) + h * DH;
-    const float osc = wg == 0 ? 1.f : scale;
+      for (int c0 = 0; c0 < DH; c0 += 32)
+        tmem_ld_32x32b_x32(tmem + lane_addr + (wg == 0 ? C_DV : C_DK) + c0,
+                           *reinterpret_cast<uint32_t(*)[32]>(acc + c0));
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(acc_empty);  // the next item's first dV / dK MMAs may overwrite
+      const int64_t ld = 3 * (int64_t)d;
+      __nv_bfloat16 *orow = dqkv + (int64_t)(row0 + kb * BKV + rr) * ld + (wg == 0 ? 2 * d : d) + h * DH;
+      const float osc = wg == 0 ? 1.f : scale;
 #pragma unroll
-    for (int c = 0; c < DH; c += 8) {
-      uint4 w;
-      uint32_t *pw = reinterpret_cast<uint32_t *>(&w);
+      for (int cc = 0; cc < DH; cc += 8) {
+        uint4 w;
+        uint32_t *pw = reinterpret_cast<uint32_t *>(&w);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        __nv_bfloat162 a = __floats2bfloat162_rn(__uint_as_float(acc[c + 2 * e]) * osc,
-                                                 __uint_as_float(acc[c + 2 * e + 1]) * osc);
-        pw[e] = *reinterpret_cast<uint32_t *>(&a);
+        for (int e = 0; e < 4; ++e) {
+          __nv_bfloat162 a2 = __floats2bfloat162_rn(__uint_as_float(acc[cc + 2 * e]) * osc,
+                                                    __uint_as_float(acc[cc + 2 * e + 1]) * osc);
+          pw[e] = *reinterpret_cast<uint32_t *>(&a2);
+        }
+        *reinterpret_cast<uint4 *>(orow + cc) = w;
       }
-      *reinterpret_cast<uint4 *>(orow + c) = w;
     }
+    if (n > 0) dq_out(prev_qrow, prev_h, n - 1);
+    if (wg == 0 && rr == 0) bulk_wait0();
   }
   __syncthreads();
   if (warp == 2) {
@@ -684,8 +736,12 @@ int backward_main(const void *qkv, const void *dout, const float *lse, const flo
     attr[causal ? 1 : 0] = true;
   }
   const float scale = 1.f / sqrtf((float)DH);
-  k<<<dim3(S / BKV, B * H), kThreads2, kSmemBwd, s>>>(tq, td, tdq, lse, dvec, dq_acc, static_cast<__nv_bfloat16 *>(dqkv), S,
-                                                      H, 1.4426950408889634f * scale, scale);
+  static int sms = 0;
+  if (!sms) HM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const int items = (S / BKV) * B * H;
+  k<<<dim3(items < sms ? items : sms), kThreads2, kSmemBwd, s>>>(tq, td, tdq, lse, dvec, dq_acc,
+                                                                 static_cast<__nv_bfloat16 *>(dqkv), S, H, B * H,
+                                                                 1.4426950408889634f * scale, scale);
   count_launch();
   HM_CUDA(cudaGetLastError());
   return HM_OK;
