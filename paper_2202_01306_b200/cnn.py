@@ -212,9 +212,10 @@ CNN_PRESETS = {
     "resnet-fine-tiny": cnn_chain("resnet-fine-tiny", 16, [64, 128], [2, 2], 10, "fine"),
     # BASELINE config c5 shapes at 224^2 / 1000 classes (stem, two stem downs to
     # 56^2, stages at 56/28/14/7): ResNet-1026 = 1 + 2 + 2 x 510 + 3 = 1026
-    # convolutions + classifier; VGG-416 = 1 + 2 + 409 + 4 = 416 convolutions
+    # convolutions + classifier; VGG-416 = 1 + 2 + 410 + 3 = 416 convolutions
+    # (four stages: a fifth would pool the 7^2 maps)
     "resnet-1026": cnn_chain("resnet-1026", 224, [64, 128, 256, 512], [128, 128, 128, 126], 1000, "res", 2),
-    "vgg-416": cnn_chain("vgg-416", 224, [64, 128, 256, 512, 512], [82, 82, 82, 82, 81], 1000, "vgg", 2),
+    "vgg-416": cnn_chain("vgg-416", 224, [64, 128, 256, 512], [103, 103, 103, 101], 1000, "vgg", 2),
     # one-GPU bench workload: ResNet-style, 56x56, 128 blocks
     "resnet-bench": cnn_chain("resnet-bench", 56, [128, 256], [64, 62], 1000, "res"),
 }

@@ -20,6 +20,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <cstdio>
 #include <mutex>
 #include <type_traits>
 
@@ -387,7 +388,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
     bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                const __grid_constant__ CUtensorMap tm_dq,
                const float *__restrict__ lse, const float *__restrict__ dvec, float *__restrict__ dq_acc,
-               __nv_bfloat16 *__restrict__ dqkv, int S, int H, int BH, float scale_log2, float scale) {
+               __nv_bfloat16 *__restrict__ dqkv, int S, int H, int BH, float scale_log2, float scale,
+               unsigned long long *trace) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned base by pointer arithmetic on the __shared__ array, so the
   // compiler keeps the shared address space (STS / LDS, not generic ST / LD)
@@ -428,6 +430,11 @@ __global__ void __launch_bounds__(kThreads2, 1)
   };
   // TMEM columns
   constexpr uint32_t C_ST = 0, C_DP = 128, C_DV = 256, C_DK = 320, C_DQ = 384;
+  // diagnostics (HM_ATTN_TRACE=1): clock64 at the phase boundaries of CTA 0's
+  // first 64 blocks, trace[event * 64 + block]
+  auto mark = [&](int ev, int nn) {
+    if (trace && c == 0 && nn < 64) trace[ev * 64 + nn] = clock64();
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm_qkv);
@@ -497,6 +504,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
                    umma_desc_sw128(do_base + kk * 32, 16, 1024), id_kk, kk > 0);
         }
         mma_commit(st_full);
+        mark(0, n);
       };
       int n = 0;
       for (int r = 0, i; (i = bwd_item(r, c, G)) < n_items; ++r) {
@@ -514,6 +522,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
           if (blk + 1 < count) issue_st(n + 1);
           const uint32_t q_base = smem_u32(sQ + st * kTileBytes), do_base = smem_u32(sdO + st * kTileBytes);
           mbar_wait(p_full, ph);
+          mark(1, n);
           if (blk == 0) mbar_wait(acc_empty, (r & 1) ^ 1);  // the previous item's dV / dK drained
           tc_fence_after();
 #pragma unroll
@@ -533,6 +542,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
           mma_commit(dq_full);
           mma_commit(&q_empty[st]);
           mma_commit(p_empty);
+          mark(2, n);
         }
         mma_commit(acc_full);
         mma_commit(kv_empty);
@@ -599,6 +609,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
         if (i + 1 < nq) x_next = src[(int64_t)(row0 + (i + 1) * BQ + rr) * H + h];
         asm volatile("bar.sync 1, 256;" ::: "memory");
         mbar_wait(st_full, ph);
+        if (wg == 0 && rr == 0) mark(3, n);
         tc_fence_after();
         const bool diag = CAUSAL && i == kb;
         const float *Ls = sL + st * BQ;
@@ -644,7 +655,10 @@ __global__ void __launch_bounds__(kThreads2, 1)
           };
           if (diag) elementwise(std::true_type{});
           else elementwise(std::false_type{});
-          if (c0 == 0) mbar_wait(p_empty, ph ^ 1);  // the previous block's MMAs have consumed P^T / dS^T
+          if (c0 == 0) {
+            mbar_wait(p_empty, ph ^ 1);  // the previous block's MMAs have consumed P^T / dS^T
+            if (wg == 0 && rr == 0) mark(4, n);
+          }
 #pragma unroll
           for (int ch = 0; ch < 4; ++ch) {
             const uint32_t off = (((c0 >> 3) + ch) ^ (rr & 7)) << 4;
@@ -654,9 +668,11 @@ __global__ void __launch_bounds__(kThreads2, 1)
         }
         fence_async_smem();
         mbar_arrive(p_full);
+        if (rr == 0) mark(wg == 0 ? 5 : 7, n);
         // the previous block's dQ is complete by now (its MMAs finished before P^T
         // could be rewritten): drain it while this block's gradient MMAs run
         if (n > 0) dq_out(prev_qrow, prev_h, n - 1);
+        if (wg == 0 && rr == 0) mark(6, n);
         prev_qrow = row0 + i * BQ;
         prev_h = h;
       }
@@ -739,9 +755,29 @@ int backward_main(const void *qkv, const void *dout, const float *lse, const flo
   static int sms = 0;
   if (!sms) HM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   const int items = (S / BKV) * B * H;
+  // HM_ATTN_TRACE=1 (diagnostics): CTA 0's phase timestamps, printed to stderr
+  static const bool tracing = getenv("HM_ATTN_TRACE") && getenv("HM_ATTN_TRACE")[0] == '1';
+  static unsigned long long *tbuf = nullptr;
+  if (tracing && !tbuf) {
+    HM_CUDA(cudaMalloc(&tbuf, 8 * 64 * sizeof(unsigned long long)));
+    HM_CUDA(cudaMemset(tbuf, 0, 8 * 64 * sizeof(unsigned long long)));
+  }
   k<<<dim3(items < sms ? items : sms), kThreads2, kSmemBwd, s>>>(tq, td, tdq, lse, dvec, dq_acc,
                                                                  static_cast<__nv_bfloat16 *>(dqkv), S, H, B * H,
-                                                                 1.4426950408889634f * scale, scale);
+                                                                 1.4426950408889634f * scale, scale,
+                                                                 tracing ? tbuf : nullptr);
+  if (tracing) {
+    unsigned long long h[8 * 64];
+    HM_CUDA(cudaStreamSynchronize(s));
+    HM_CUDA(cudaMemcpy(h, tbuf, sizeof h, cudaMemcpyDeviceToHost));
+    fprintf(stderr, "{\"attn_bwd_trace\": [");
+    for (int e = 0; e < 8; ++e) {
+      fprintf(stderr, "%s[", e ? ", " : "");
+      for (int n = 0; n < 64; ++n) fprintf(stderr, "%s%llu", n ? ", " : "", h[e * 64 + n] ? h[e * 64 + n] - h[0] : 0ULL);
+      fprintf(stderr, "]");
+    }
+    fprintf(stderr, "]}\n");
+  }
   count_launch();
   HM_CUDA(cudaGetLastError());
   return HM_OK;

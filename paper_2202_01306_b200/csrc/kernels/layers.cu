@@ -573,6 +573,154 @@ static int ln_bwd_rowreg(const float *dy, const float *x, const float *mean, con
   return HM_OK;
 }
 
+// Register-resident rows wider than one warp can hold (d > 1024): a row is
+// split over WPR warps (lane l of warp w of the row group owns float4 columns
+// 32 w + l, + 32 WPR, ...), so dy and x are read from HBM exactly once with
+// all loads in flight; the row statistics c1 / c2 combine across the group's
+// warps through shared memory under a named barrier, and dgamma / dbeta
+// accumulate in registers over every row the group visits (fixed columns per
+// lane), folded per block in shared memory and added to global memory once
+// per column per block.
+template <int NV4, int WARPS, int WPR>
+__global__ void __launch_bounds__(WARPS * 32)
+    ln_bwd_wide_kernel(const float *__restrict__ dy, const float *__restrict__ x, const float *__restrict__ mean,
+                       const float *__restrict__ rstd, const float *__restrict__ gam, const float *resid, float *out,
+                       __nv_bfloat16 *__restrict__ out_bf, float *__restrict__ dgam, float *__restrict__ dbet,
+                       int64_t rows, int d, int rows_per_block) {
+  constexpr int G = WARPS / WPR;  // row groups per block
+  pdl_wait();
+  extern __shared__ float sred[];  // [2][G][WPR][2] row statistics, then [G][2][d] dgamma / dbeta partials
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = warp / WPR, wi = warp % WPR;
+  const int n4 = d / 4;
+  const float4 *g4 = reinterpret_cast<const float4 *>(gam);
+  float4 gg[NV4], accg[NV4], accb[NV4];
+#pragma unroll
+  for (int k = 0; k < NV4; ++k) {
+    const int i = wi * 32 + lane + 32 * WPR * k;
+    gg[k] = i < n4 ? g4[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    accg[k] = accb[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const int64_t r_begin = (int64_t)blockIdx.x * rows_per_block;
+  const int64_t r_end = min(rows, r_begin + rows_per_block);
+  int par = 0;
+  for (int64_t r = r_begin + grp; r < r_end; r += G, par ^= 1) {
+    const float4 *dyr = reinterpret_cast<const float4 *>(dy + r * d);
+    const float4 *xr = reinterpret_cast<const float4 *>(x + r * d);
+    float4 a[NV4], v[NV4];
+#pragma unroll
+    for (int k = 0; k < NV4; ++k) {
+      const int i = wi * 32 + lane + 32 * WPR * k;
+      if (i < n4) {
+        a[k] = dyr[i];
+        v[k] = xr[i];
+      } else {
+        a[k] = v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    const float mu = mean[r], rs = rstd[r];
+    float c1 = 0.f, c2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV4; ++k) {
+      v[k].x = (v[k].x - mu) * rs; v[k].y = (v[k].y - mu) * rs;  // v := xhat (0 past the row end: a = 0 there)
+      v[k].z = (v[k].z - mu) * rs; v[k].w = (v[k].w - mu) * rs;
+      const float e0 = a[k].x * gg[k].x, e1 = a[k].y * gg[k].y, e2 = a[k].z * gg[k].z, e3 = a[k].w * gg[k].w;
+      c1 += (e0 + e1) + (e2 + e3);
+      c2 += (e0 * v[k].x + e1 * v[k].y) + (e2 * v[k].z + e3 * v[k].w);
+      accg[k].x += a[k].x * v[k].x; accg[k].y += a[k].y * v[k].y;
+      accg[k].z += a[k].z * v[k].z; accg[k].w += a[k].w * v[k].w;
+      accb[k].x += a[k].x; accb[k].y += a[k].y; accb[k].z += a[k].z; accb[k].w += a[k].w;
+    }
+    c1 = warp_sum(c1);
+    c2 = warp_sum(c2);
+    float *red = sred + ((par * G + grp) * WPR) * 2;
+    if (lane == 0) {
+      red[2 * wi] = c1;
+      red[2 * wi + 1] = c2;
+    }
+    // the row group's warps only (double-buffered by row parity: the next row's
+    // writes go to the other buffer, the one after waits behind this barrier)
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(WPR * 32) : "memory");
+    c1 = 0.f;
+    c2 = 0.f;
+#pragma unroll
+    for (int w = 0; w < WPR; ++w) {
+      c1 += red[2 * w];
+      c2 += red[2 * w + 1];
+    }
+    c1 /= d;
+    c2 /= d;
+    float4 *outr = reinterpret_cast<float4 *>(out + r * d);
+    const float4 *rr = resid ? reinterpret_cast<const float4 *>(resid + r * d) : nullptr;
+    uint2 *ob = out_bf ? reinterpret_cast<uint2 *>(out_bf + r * d) : nullptr;
+#pragma unroll
+    for (int k = 0; k < NV4; ++k) {
+      const int i = wi * 32 + lane + 32 * WPR * k;
+      if (i < n4) {
+        float4 o;
+        o.x = rs * (a[k].x * gg[k].x - c1 - v[k].x * c2);
+        o.y = rs * (a[k].y * gg[k].y - c1 - v[k].y * c2);
+        o.z = rs * (a[k].z * gg[k].z - c1 - v[k].z * c2);
+        o.w = rs * (a[k].w * gg[k].w - c1 - v[k].w * c2);
+        if (rr) {
+          const float4 q = rr[i];
+          o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+        }
+        outr[i] = o;
+        if (ob) {
+          __nv_bfloat162 p0 = __floats2bfloat162_rn(o.x, o.y), p1 = __floats2bfloat162_rn(o.z, o.w);
+          ob[i] = make_uint2(*reinterpret_cast<uint32_t *>(&p0), *reinterpret_cast<uint32_t *>(&p1));
+        }
+      }
+    }
+  }
+  __syncthreads();
+  float4 *part = reinterpret_cast<float4 *>(sred + 4 * G * WPR);  // [G][2][n4] float4
+#pragma unroll
+  for (int k = 0; k < NV4; ++k) {
+    const int i = wi * 32 + lane + 32 * WPR * k;
+    if (i < n4) {
+      part[(size_t)(grp * 2) * n4 + i] = accg[k];
+      part[(size_t)(grp * 2 + 1) * n4 + i] = accb[k];
+    }
+  }
+  __syncthreads();
+  const float *pf = reinterpret_cast<const float *>(part);
+  for (int c = threadIdx.x; c < d; c += WARPS * 32) {
+    float sg = 0.f, sb = 0.f;
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+      sg += pf[(size_t)(q * 2) * d + c];
+      sb += pf[(size_t)(q * 2 + 1) * d + c];
+    }
+    atomicAdd(&dgam[c], sg);
+    atomicAdd(&dbet[c], sb);
+  }
+}
+
+template <int NV4, int WARPS, int WPR>
+static int ln_bwd_wide(const float *dy, const float *x, const float *mean, const float *rstd, const float *g,
+                       const float *resid, float *out, void *out_bf, float *dg, float *db, int64_t rows, int d,
+                       cudaStream_t s) {
+  constexpr int G = WARPS / WPR;
+  const size_t smem = (size_t)4 * G * WPR * sizeof(float) + (size_t)G * 2 * d * sizeof(float) + 16;
+  static size_t attr_smem = 0;
+  if (smem > attr_smem) {
+    HM_CUDA(cudaFuncSetAttribute(ln_bwd_wide_kernel<NV4, WARPS, WPR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    attr_smem = smem;
+  }
+  const int per_sm = std::max<int>(1, std::min<int>(4, (int)((200 * 1024) / smem)));
+  int64_t blocks = (int64_t)sm_count() * per_sm;
+  int rpb = (int)((rows + blocks - 1) / blocks);
+  if (rpb < G) rpb = G;
+  blocks = (rows + rpb - 1) / rpb;
+  HM_CUDA(launch_pdl(ln_bwd_wide_kernel<NV4, WARPS, WPR>, dim3((unsigned)blocks), dim3(WARPS * 32), smem, s, dy, x,
+                     mean, rstd, g, resid, out, static_cast<__nv_bfloat16 *>(out_bf), dg, db, rows, d, rpb));
+  count_launch();
+  return HM_OK;
+}
+
 // Row-batched variant (default for d <= 2048): the 256 threads of a block
 // own fixed float4 columns (thread t: columns t, t + 256, ...), so every row
 // is read with fully coalesced 16-B loads exactly once (dy, x, resid), the
@@ -852,6 +1000,23 @@ int ln_bwd(const float *dy, const float *x, const float *mean, const float *rstd
     if (nv4 <= 2) return ln_bwd_rowreg<2>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
     if (nv4 <= 4) return ln_bwd_rowreg<4>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
     return ln_bwd_rowreg<8>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
+  }
+  // wider rows (d > 1024) split over 2 (d <= 2048) or 8 (d <= 8192) warps, still
+  // register-resident: one HBM read of dy / x
+  static const bool use_wide = [] {
+    const char *e = getenv("HM_LN_BWD");
+    return !(e && e[0] == 'w');
+  }();
+  if (use_wide && !use_smem_atomic && d % 4 == 0 && d <= 8192) {
+    ProfScope ps(KC_LAYERNORM, s, 0, (resid ? 16.0 : 12.0) * rows * d + (out_bf ? 2.0 * rows * d : 0));
+    const int n4 = d / 4;
+    if (d <= 2048) {
+      if (n4 <= 64 * 4) return ln_bwd_wide<4, 8, 2>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
+      if (n4 <= 64 * 7) return ln_bwd_wide<7, 8, 2>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
+      return ln_bwd_wide<8, 8, 2>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
+    }
+    if (n4 <= 256 * 4) return ln_bwd_wide<4, 8, 8>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
+    return ln_bwd_wide<8, 8, 8>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
   }
   if (!use_smem_atomic && (size_t)4 * 2 * d * sizeof(float) <= 160 * 1024) {  // 4 warps' private partials
     constexpr int kWarps = 4;

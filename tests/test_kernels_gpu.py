@@ -199,10 +199,12 @@ def test_attention_fwd_bwd(ops, B, S, H, DH, causal):
         assert _rel(got[:, i], g[:, i]) < 2e-2, i
 
 
-@pytest.mark.parametrize("M,d", [(1000, 1600), (37, 1024), (517, 4096), (300, 8192), (64, 256)])
+@pytest.mark.parametrize("M,d", [(1000, 1600), (37, 1024), (517, 4096), (300, 8192), (64, 256), (77, 1028),
+                                 (33, 2048), (45, 5124)])
 def test_layernorm_fwd_bwd(ops, M, d):
-    """Every backward variant: row-batched tiles (d <= 4096, ragged row
-    counts) and the shared-memory kernel beyond."""
+    """The default backward: rows in registers (one warp per row up to d = 1024,
+    rows split over 2 / 8 warps up to 2048 / 8192), ragged row counts and
+    column tails."""
     torch.manual_seed(6)
     x = torch.randn(M, d, device="cuda") * 2 + 0.5
     g = torch.randn(d, device="cuda")
@@ -234,12 +236,12 @@ def test_layernorm_fwd_bwd(ops, M, d):
 def test_layernorm_bwd_variants(variant):
     """Every LayerNorm backward variant (HM_LN_BWD is read once per process):
     row-batched tiles (t), shared-memory atomics (a), two-pass warps with
-    private partials (w), register-accumulated (reg); the default picks
-    registers (d <= 1024) / two-pass (d <= 5120) / atomics."""
+    private partials (w), register-accumulated (reg); the default keeps rows in
+    registers (one warp per row up to d = 1024, 2 / 8 warps per row up to 8192)."""
     import subprocess
     import sys
     here = __import__("os").path.dirname(__import__("os").path.abspath(__file__))
-    cases = [(1000, 1600), (37, 1024), (517, 4096), (300, 8192), (64, 256)]
+    cases = [(1000, 1600), (37, 1024), (517, 4096), (300, 8192), (64, 256), (77, 1028)]
     code = (f"import torch, sys; sys.path.insert(0, {here!r}); sys.path.insert(0, {here + '/..'!r}); "
             "import test_kernels_gpu as T; from paper_2202_01306_b200 import ops; "
             f"[T.test_layernorm_fwd_bwd(ops, *c) for c in {cases!r}]")
