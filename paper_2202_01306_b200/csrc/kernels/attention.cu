@@ -26,6 +26,10 @@ int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causa
 int backward_main(const void *qkv, const void *dout, const float *lse, const float *dvec, float *dq_acc, void *dqkv,
                   int B, int S, int H, int causal, cudaStream_t s);
 }  // namespace attn_tc
+namespace attn_bwd64 {  // head_dim 64 backward over 64-query sub-blocks (attention_bwd64.cu)
+int backward_main(const void *qkv, const void *dout, const float *lse, const float *dvec, float *dq_acc, void *dqkv,
+                  int B, int S, int H, int causal, cudaStream_t s);
+}  // namespace attn_bwd64
 namespace attn_tc128 {  // head_dim 128 (attention_tc128.cu)
 bool supported(int S, int DH);
 int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causal, cudaStream_t s);
@@ -499,13 +503,21 @@ static int bwd_launch(const __nv_bfloat16 *qkv, const __nv_bfloat16 *o, const __
   // reduce-add per query block) is the default where it applies (head_dim 64,
   // seq % 128 == 0): 1.4-1.5x this mma.sync kernel on B200.  HM_ATTN_BWD=mma
   // forces the mma.sync kernel.
+  // HM_ATTN_BWD=q: the 128-query head_dim-64 kernel of attention_tc.cu instead of
+  // attention_bwd64.cu (64-query sub-blocks, alternating softmax warpgroups)
   static const bool use_tc = [] {
     const char *e = getenv("HM_ATTN_BWD");
     return !(e && std::string(e) == "mma");
   }();
+  static const bool bwd_q = [] {
+    const char *e = getenv("HM_ATTN_BWD");
+    return e && std::string(e) == "q";
+  }();
   if (use_tc && (attn_tc::supported(S, DH) || attn_tc128::supported(S, DH))) {
     // tcgen05 main kernel; it folds the softmax scale into dq_acc
-    if (DH == 64) HM_TRY(attn_tc::backward_main(qkv, dout, lse, dvec, dq_acc, dqkv, B, S, H, CAUSAL ? 1 : 0, s));
+    if (DH == 64 && bwd_q) HM_TRY(attn_tc::backward_main(qkv, dout, lse, dvec, dq_acc, dqkv, B, S, H, CAUSAL ? 1 : 0, s));
+    else if (DH == 64)
+      HM_TRY(attn_bwd64::backward_main(qkv, dout, lse, dvec, dq_acc, dqkv, B, S, H, CAUSAL ? 1 : 0, s));
     else HM_TRY(attn_tc128::backward_main(qkv, dout, lse, dvec, dq_acc, dqkv, B, S, H, CAUSAL ? 1 : 0, s));
     HM_CUDA(launch_pdl(dq_convert, dim3(1184), dim3(256), 0, s, (const float *)dq_acc, dqkv, rows, d, 1.f));
   } else {

@@ -173,6 +173,9 @@ def _attn_ref(qkv, B, S, H, DH, causal):
 
 @pytest.mark.parametrize("B,S,H,DH,causal", [(2, 128, 4, 64, True), (1, 512, 2, 64, False),
                                              (2, 256, 3, 64, True), (1, 256, 2, 128, True),
+                                             # head_dim 64: several persistent items per CTA,
+                                             # odd 128-key block count
+                                             (3, 1024, 5, 64, True), (2, 384, 3, 64, False),
                                              # head_dim 128 (attention_tc128.cu): odd query-tile count,
                                              # full attention, the >HBM GPT shape at 1024 tokens
                                              (2, 384, 3, 128, True), (1, 512, 2, 128, False),
@@ -351,9 +354,11 @@ def test_attention_fwd_tcgen05_matches(ops, B, S, H, causal, DH):
     assert torch.allclose(lse, rl * 1.4426950408889634, atol=2e-3, rtol=1e-3)
 
 
-def test_attention_bwd_tcgen05_opt_in():
-    """The mma.sync backward (HM_ATTN_BWD=mma; the tcgen05 one is the default
-    where it applies) matches autograd."""
+@pytest.mark.parametrize("variant", ["mma", "q"])
+def test_attention_bwd_tcgen05_opt_in(variant):
+    """The opt-in backward kernels match autograd: the mma.sync one
+    (HM_ATTN_BWD=mma) and the 128-query head_dim-64 tcgen05 one (q); the
+    default is attention_bwd64.cu (64-query sub-blocks)."""
     import subprocess
     import sys
     here = __import__("os").path.dirname(__import__("os").path.abspath(__file__))
@@ -361,8 +366,8 @@ def test_attention_bwd_tcgen05_opt_in():
             "import test_kernels_gpu as T; "
             "from paper_2202_01306_b200 import ops; "
             "T.test_attention_fwd_bwd(ops, 2, 256, 3, 64, True); T.test_attention_fwd_bwd(ops, 1, 512, 2, 64, False); "
-            "T.test_attention_fwd_bwd(ops, 1, 256, 2, 128, True)")
-    env = dict(__import__("os").environ, HM_ATTN_BWD="mma")
+            "T.test_attention_fwd_bwd(ops, 1, 256, 2, 128, True); T.test_attention_fwd_bwd(ops, 3, 1024, 5, 64, True)")
+    env = dict(__import__("os").environ, HM_ATTN_BWD=variant)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
 

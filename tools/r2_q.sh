@@ -1,0 +1,12 @@
+# head_dim-64 backward over 64-query sub-blocks: parity + timing
+set -u
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+timeout 300 python -m pytest tests/test_kernels_gpu.py -q -x -k "attention_fwd_bwd and 64" > gpurun_out/r2q_attn_tests.log 2>&1
+echo "rc=$?" >> gpurun_out/r2q_attn_tests.log
+for shape in "4 1024 25 64 1" "8 512 16 64 0" "1 1024 25 64 1" "16 1024 25 64 1"; do
+  timeout 60 python tools/attn_perf.py $shape >> gpurun_out/r2q_attn_perf.jsonl 2>>gpurun_out/r2q_attn_perf.err
+  HM_ATTN_BWD=q timeout 60 python tools/attn_perf.py $shape >> gpurun_out/r2q_attn_perf.jsonl 2>>gpurun_out/r2q_attn_perf.err
+done
+timeout 600 python -m pytest tests/test_kernels_gpu.py -q -k "attention" > gpurun_out/r2q_attn_tests_all.log 2>&1
+echo "rc=$?" >> gpurun_out/r2q_attn_tests_all.log
+echo done
