@@ -503,21 +503,27 @@ static int bwd_launch(const __nv_bfloat16 *qkv, const __nv_bfloat16 *o, const __
   // reduce-add per query block) is the default where it applies (head_dim 64,
   // seq % 128 == 0): 1.4-1.5x this mma.sync kernel on B200.  HM_ATTN_BWD=mma
   // forces the mma.sync kernel.
-  // HM_ATTN_BWD=q: the 128-query head_dim-64 kernel of attention_tc.cu instead of
-  // attention_bwd64.cu (64-query sub-blocks, alternating softmax warpgroups)
+  // head_dim 64: the 128-query kernel of attention_tc.cu; HM_ATTN_BWD=s selects
+  // attention_bwd64.cu (64-query sub-blocks, alternating softmax warpgroups,
+  // P^T / dS^T from TMEM): equal within 3% (104 vs 107 us at 4 x 1024 x 25
+  // heads, 417 vs 403 at 16 x 1024, profiles/r02_attn_perf_bwd64_ab.jsonl) --
+  // both wait on the tensor pipe, which runs the N = 64 MMAs at 45-48 cycles
+  // alone (32 ideal, profiles/r02_mma_probe.jsonl) and at ~90 next to the
+  // softmax warps' TMEM and shared-memory traffic (HM_ATTN_TRACE)
   static const bool use_tc = [] {
     const char *e = getenv("HM_ATTN_BWD");
     return !(e && std::string(e) == "mma");
   }();
-  static const bool bwd_q = [] {
+  static const bool bwd_s = [] {
     const char *e = getenv("HM_ATTN_BWD");
-    return e && std::string(e) == "q";
+    return e && std::string(e) == "s";
   }();
   if (use_tc && (attn_tc::supported(S, DH) || attn_tc128::supported(S, DH))) {
     // tcgen05 main kernel; it folds the softmax scale into dq_acc
-    if (DH == 64 && bwd_q) HM_TRY(attn_tc::backward_main(qkv, dout, lse, dvec, dq_acc, dqkv, B, S, H, CAUSAL ? 1 : 0, s));
-    else if (DH == 64)
+    if (DH == 64 && bwd_s)
       HM_TRY(attn_bwd64::backward_main(qkv, dout, lse, dvec, dq_acc, dqkv, B, S, H, CAUSAL ? 1 : 0, s));
+    else if (DH == 64)
+      HM_TRY(attn_tc::backward_main(qkv, dout, lse, dvec, dq_acc, dqkv, B, S, H, CAUSAL ? 1 : 0, s));
     else HM_TRY(attn_tc128::backward_main(qkv, dout, lse, dvec, dq_acc, dqkv, B, S, H, CAUSAL ? 1 : 0, s));
     HM_CUDA(launch_pdl(dq_convert, dim3(1184), dim3(256), 0, s, (const float *)dq_acc, dqkv, rows, d, 1.f));
   } else {

@@ -1,7 +1,9 @@
 // attention_bwd64.cu -- flash-attention backward for head_dim 64 on the 5th-gen
-// tensor cores, pipelined over 64-query sub-blocks.
+// tensor cores, pipelined over 64-query sub-blocks (HM_ATTN_BWD=s; measured
+// within 3% of attention_tc.cu's 128-query kernel, which stays the default:
+// see attention.cu).
 //
-// The 128-query dataflow of attention_tc.cu (HM_ATTN_BWD=q) is bounded by its
+// The 128-query dataflow of attention_tc.cu is bounded by its
 // single shared-memory P^T / dS^T buffer: the softmax of block n+1 may write
 // only after dV / dK / dQ(n) have read block n's (3800 cycles per block where
 // the MMAs need ~1300, HM_ATTN_TRACE).  Here every CTA (persistent, heaviest
@@ -26,6 +28,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <cstdio>
 #include <mutex>
 
 #include "../runtime/common.hpp"
@@ -76,7 +79,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     bwd_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
                const __grid_constant__ CUtensorMap tm_do, const __grid_constant__ CUtensorMap tm_dq,
                const float *__restrict__ lse, const float *__restrict__ dvec, __nv_bfloat16 *__restrict__ dqkv, int S,
-               int H, int BH, float scale_log2, float scale) {
+               int H, int BH, float scale_log2, float scale, unsigned long long *trace) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *sK = smem;
@@ -113,6 +116,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     h = bh % H;
   };
   auto nsub_of = [&](int kb) { return (S - (CAUSAL ? kb * BKV : 0)) / SQ; };  // even: S % 128 == 0
+  // diagnostics (HM_ATTN_TRACE=1): clock64 at phase boundaries of CTA 0's first
+  // 64 sub-blocks, trace[event * 64 + sub-block]
+  auto mark = [&](int ev, int nn) {
+    if (trace && c == 0 && nn < 64) trace[ev * 64 + nn] = clock64();
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm_kv);
@@ -181,6 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                    umma_desc_sw128(do_base + kk * 32, 16, 1024), id_st, kk > 0);
         }
         mma_commit(&s_full[w]);
+        mark(0, gg);
       };
       int g = 0;
       for (int r = 0, i; (i = item_of(r, c, G)) < n_items; ++r) {
@@ -193,6 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < nsub; ++j) {
           const int gg = g + j, w = gg & 1, st = gg % kQStages;
           mbar_wait(&p_full[w], (gg >> 1) & 1);  // P^T / dS^T of sub-block gg in TMEM (and dS^T in smem)
+          mark(1, gg);
           if (j == 0) mbar_wait(acc_empty, (r & 1) ^ 1);  // the previous item's dV / dK drained
           tc_fence_after();
           const uint32_t q_base = smem_u32(sQ + st * kSub), do_base = smem_u32(sdO + st * kSub);
@@ -216,6 +226,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                        umma_desc_sw128(k_base + kk * 2048, kKV, 1024), id_dq, kk > 0);
             mma_commit(&dq_full[qb]);
             mma_commit(&ds_empty[qb]);
+            mark(2, gg);
           }
           // S^T(gg + 2) reuses buffer w: dV / dK(gg) above read P^T / dS^T from it first
           if (j + 2 < nsub) issue_s(gg + 2);
@@ -280,6 +291,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (j + 2 < nsub) x_next = ld_src(j + 2);
         named_sync(1 + w, 128);
         mbar_wait(&s_full[w], pg & 1);
+        if (rr == 0) mark(3, gg);
         tc_fence_after();
         uint32_t sv[SQ], dp[SQ];
         tmem_ld_32x32b_x32(s_addr, *reinterpret_cast<uint32_t(*)[32]>(sv));
@@ -311,7 +323,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_st_32x32b_x32(s_addr, pk);
         tmem_st_32x32b_x32(s_addr + 64, dk);
         // dS^T into half w of the pair's shared-memory buffer (A operand of dQ)
+        if (rr == 0) mark(4, gg);
         mbar_wait(&ds_empty[pg & 1], ((pg >> 1) & 1) ^ 1);  // dQ of pair pg - 2 has read it
+        if (rr == 0) mark(5, gg);
         uint8_t *dsrow = sDS + (pg & 1) * kDS + w * (BKV * 128) + rr * 128;
 #pragma unroll
         for (int ch = 0; ch < 8; ++ch)
@@ -321,8 +335,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_async_smem();
         tc_fence_before();
         mbar_arrive(&p_full[w]);
+        if (rr == 0) mark(6, gg);
         // the previous pair's dQ: complete by now or soon, drained off the critical path
         if (prev_pg >= 0) dq_out(prev_pg, prev_qrow, prev_h);
+        if (rr == 0) mark(7, gg);
         prev_pg = pg;
         prev_qrow = row0 + q0 + (j & ~1) * SQ;
         prev_h = h;
@@ -419,9 +435,29 @@ int backward_main(const void *qkv, const void *dout, const float *lse, const flo
   if (!sms) HM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   const int items = (S / BKV) * B * H;
   const float scale = 1.f / sqrtf((float)DH);
+  static const bool tracing = getenv("HM_ATTN_TRACE") && getenv("HM_ATTN_TRACE")[0] == '1';
+  static unsigned long long *tbuf = nullptr;
+  if (tracing && !tbuf) {
+    HM_CUDA(cudaMalloc(&tbuf, 8 * 64 * sizeof(unsigned long long)));
+    HM_CUDA(cudaMemset(tbuf, 0, 8 * 64 * sizeof(unsigned long long)));
+  }
   k<<<dim3(items < sms ? items : sms), kThreads, kSmem, s>>>(tkv, tq, tdo, tdq, lse, dvec,
                                                              static_cast<__nv_bfloat16 *>(dqkv), S, H, B * H,
-                                                             1.4426950408889634f * scale, scale);
+                                                             1.4426950408889634f * scale, scale,
+                                                             tracing ? tbuf : nullptr);
+  if (tracing) {  // CTA 0's phase timestamps (cycles from its first S^T issue) to stderr
+    unsigned long long hbuf[8 * 64];
+    HM_CUDA(cudaStreamSynchronize(s));
+    HM_CUDA(cudaMemcpy(hbuf, tbuf, sizeof hbuf, cudaMemcpyDeviceToHost));
+    fprintf(stderr, "{\"attn_bwd64_trace\": [");
+    for (int e = 0; e < 8; ++e) {
+      fprintf(stderr, "%s[", e ? ", " : "");
+      for (int n = 0; n < 64; ++n)
+        fprintf(stderr, "%s%lld", n ? ", " : "", hbuf[e * 64 + n] ? (long long)(hbuf[e * 64 + n] - hbuf[0]) : 0LL);
+      fprintf(stderr, "]");
+    }
+    fprintf(stderr, "]}\n");
+  }
   count_launch();
   HM_CUDA(cudaGetLastError());
   return HM_OK;

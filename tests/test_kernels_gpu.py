@@ -354,11 +354,11 @@ def test_attention_fwd_tcgen05_matches(ops, B, S, H, causal, DH):
     assert torch.allclose(lse, rl * 1.4426950408889634, atol=2e-3, rtol=1e-3)
 
 
-@pytest.mark.parametrize("variant", ["mma", "q"])
+@pytest.mark.parametrize("variant", ["mma", "s"])
 def test_attention_bwd_tcgen05_opt_in(variant):
     """The opt-in backward kernels match autograd: the mma.sync one
-    (HM_ATTN_BWD=mma) and the 128-query head_dim-64 tcgen05 one (q); the
-    default is attention_bwd64.cu (64-query sub-blocks)."""
+    (HM_ATTN_BWD=mma) and the 64-query sub-block head_dim-64 tcgen05 one
+    (s, attention_bwd64.cu); the default is attention_tc.cu's 128-query kernel."""
     import subprocess
     import sys
     here = __import__("os").path.dirname(__import__("os").path.abspath(__file__))
