@@ -14,9 +14,11 @@ Two arithmetic modes:
   rounding changes gradients by ~0.4% per element, and Adam's normalised
   update turns that into sign noise where a gradient is near zero).
 
-Configs: c1 (tiny GPT-2, 10 steps) and the benchmarked c3 shape (GPT-2 XL
+Configs: c1 (tiny GPT-2, 10 steps), the benchmarked c3 shape (GPT-2 XL
 layers: d=1600, 25 heads, seq 1024, V=50257) at 4 layers, D=4, PP and DP,
-3 steps.  The schedule ledger equals simulate's at every step."""
+3 steps, c2 at its benched grouping (BERT-Large layers, D=64 as u=16
+microbatches, 6 layers, 2 steps) and the c4 layer shape (d=8192, head_dim
+128).  The schedule ledger equals simulate's at every step."""
 
 import numpy as np
 import pytest
@@ -131,6 +133,17 @@ def test_c3_gpt2xl_shape_per_layer_deltas(mode, math):
     packs = ((0, 1), (2, 3))
     cfg = H.Configuration(2, packs, 2, packs, 4, H.Mode(mode))
     check(run_parity(spec, cfg, 3, math, alpha=40 << 30), FP32_TOL if math == "fp32" else BF16_TOL)
+
+
+@pytest.mark.parametrize("math", ["fp32", "bf16"])
+def test_c2_bert_large_benched_grouping(math):
+    """Config c2 at the benched grouping (bench.py bert-large-pp: D = 64 in
+    microbatches of u = 16, full attention at seq 512, vocab 30522): BERT-Large
+    layers at 6 layers in two packs of 3, 2 steps."""
+    spec = GPTSpec(6, 1024, 16, 512, 30522, False, "bert-large-6l")
+    packs = ((0, 2), (3, 5))
+    cfg = H.Configuration(16, packs, 16, packs, 64, H.Mode.PP)
+    check(run_parity(spec, cfg, 2, math, alpha=40 << 30), FP32_TOL if math == "fp32" else BF16_TOL)
 
 
 @pytest.mark.parametrize("math", ["fp32", "bf16"])
