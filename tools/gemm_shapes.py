@@ -3,7 +3,7 @@ timed by graph replay (ops.gemm_replay_us, L2-rotating operand sets).  One
 JSON line per shape; the tile configuration follows the process's env
 switches (HM_GEMM_STREAMK, HM_GEMM_BN, ...).
 
-    python tools/gemm_shapes.py [tag]"""
+    python tools/gemm_shapes.py [tag] [shape index]"""
 import json
 import os
 import sys
@@ -26,9 +26,12 @@ EPI_NAME = {v: k for k, v in ops.EPI.items()}
 def main() -> None:
     import torch
     tag = sys.argv[1] if len(sys.argv) > 1 else ""
+    only = int(sys.argv[2]) if len(sys.argv) > 2 else None
     torch.cuda.init()
     tot_f = tot_us = 0.0
-    for shp, count in SHAPES:
+    for idx, (shp, count) in enumerate(SHAPES):
+        if only is not None and idx != only:
+            continue
         us = ops.gemm_replay_us(shp, reps=32)
         fl = 2.0 * shp[0] * shp[1] * shp[2]
         tot_f += fl * count
