@@ -3,11 +3,16 @@
 // head_dim-64 shape hits first: the MUFU exp2 rate (16384 ex2 per 128 x 128
 // tile against 512 cycles of MMA) and the softmax's wait on the tensor pipe.
 //
-// One CTA per pair of 128-query tiles (heaviest causal pairs first):
-//   warp 0      TMA: both Q tiles once, then K_j / V_j into a 3-stage ring
-//   warp 1      TMEM allocation, MMA issuer
+// Persistent: one CTA per SM walks (sample-head, query-tile pair) items,
+// causal pairs heaviest first, dealt in snake order; every ring / buffer
+// parity follows running counters across items, the next item's Q pair is
+// double-buffered, and its first S MMAs are issued while the current item's
+// last tiles are still in the softmax (16 x 1024 x 25 heads: 114.6 vs 138.6 us
+// for one CTA per pair).
+//   warp 0      TMA: Q pairs, then K_j / V_j into a 3-stage ring
+//   warp 1      MMA issuer
 //   warps 4-7   softmax of tile 0, warps 8-11 of tile 1 (one thread per
-//               query row; warp w reads TMEM lanes 32 (w % 4) .. + 31)
+//               query row = TMEM lane)
 // TMEM (512 columns): three rotating 128-column S buffers + O_0, O_1 (64
 // columns each).  S buffers are handed out in the order the S tiles are
 // computed (S_0(0), S_1(0), S_0(1), S_1(1), ...), so S for the next step of
@@ -49,7 +54,7 @@ constexpr uint32_t kTile = BQ * DH * 2;  // 128 rows x 128 B: one SW128 atom col
 constexpr int kThreads = 384;
 constexpr float kRescaleLog2 = 8.f;      // lazy-rescale threshold (log2 units)
 constexpr uint32_t C_O = kSBuf * BKV;    // O_t at columns [384 + 64 t, 448 + 64 t)
-constexpr size_t kSmem = 1024 + 2 * kTile /*Q pair*/ + 2 * kStages * kTile /*K, V*/ + 256;
+constexpr size_t kSmem = 1024 + 4 * kTile /*Q pair x 2 items*/ + 2 * kStages * kTile /*K, V*/ + 256;
 static_assert(C_O + 2 * DH == 512, "TMEM budget");
 
 __device__ __forceinline__ float ex2(float x) {
@@ -99,50 +104,99 @@ __device__ __forceinline__ uint32_t bf16x2(float lo, float hi) {
   return r;
 }
 
+// the r-th item of CTA c of G (snake order over a heaviest-first list)
+__device__ __forceinline__ int item_of(int r, int c, int G) { return r * G + ((r & 1) ? G - 1 - c : c); }
+
+// One item = the query-tile pair (2 pr, 2 pr + 1) of one (sample, head), and
+// the global bases of its running counters.  Positions n = 0 .. npos - 1
+// order its S / PV MMAs: S_0(0), S_1(0), S_0(1), S_1(1), ... then the longer
+// tile alone.
+struct Item {
+  bool valid;
+  int r, b, h, pr, nkv0, nkv1, mn, tlast, npos;
+  int kvb, pb, g0, g1;  // first global K/V block, position, tile-0 and tile-1 step
+  __device__ void at(int n, int &t, int &j) const {
+    if (n < 2 * mn) {
+      t = n & 1;
+      j = n >> 1;
+    } else {
+      t = tlast;
+      j = mn + (n - 2 * mn);
+    }
+  }
+};
+
+template <bool CAUSAL>
+__device__ __forceinline__ Item make_item(int r, int c, int G, int S, int H, int BH, int kvb, int pb, int g0, int g1) {
+  Item it;
+  const int nq = S / BQ, npair = (nq + 1) >> 1, n_items = npair * BH;
+  const int i = item_of(r, c, G);
+  it.valid = i < n_items;
+  it.r = r;
+  int bh;
+  if (CAUSAL) {  // heaviest pairs first
+    it.pr = npair - 1 - i / BH;
+    bh = i % BH;
+  } else {
+    it.pr = i % npair;
+    bh = i / npair;
+  }
+  it.b = bh / H;
+  it.h = bh % H;
+  const int qb0 = 2 * it.pr;
+  const bool has1 = qb0 + 1 < nq;
+  it.nkv0 = CAUSAL ? qb0 + 1 : S / BKV;
+  it.nkv1 = has1 ? (CAUSAL ? qb0 + 2 : S / BKV) : 0;
+  it.mn = it.nkv0 < it.nkv1 ? it.nkv0 : it.nkv1;
+  it.tlast = it.nkv1 >= it.nkv0 ? 1 : 0;
+  it.npos = it.nkv0 + it.nkv1;
+  it.kvb = kvb;
+  it.pb = pb;
+  it.g0 = g0;
+  it.g1 = g1;
+  return it;
+}
+
 template <bool CAUSAL>
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16 *__restrict__ out, float *__restrict__ lse,
-               int S, int H, float scale_log2) {
+               int S, int H, int BH, float scale_log2) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t *sQ = smem;                  // [2 tiles]
-  uint8_t *sK = sQ + 2 * kTile;        // [kStages]
+  uint8_t *sQ = smem;                  // [2 items][2 tiles]
+  uint8_t *sK = sQ + 4 * kTile;        // [kStages]
   uint8_t *sV = sK + kStages * kTile;  // [kStages]
   uint64_t *bar = reinterpret_cast<uint64_t *>(sV + kStages * kTile);
-  uint64_t *q_full = bar;
-  uint64_t *kv_full = bar + 1, *kv_empty = bar + 1 + kStages;
-  uint64_t *s_full = bar + 1 + 2 * kStages;       // [kSBuf]
-  uint64_t *p_full = s_full + kSBuf;              // [tile]
-  uint64_t *o_full = p_full + 2;                  // [tile]
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(o_full + 2);
+  uint64_t *q_full = bar, *q_empty = bar + 2;                   // [item parity]
+  uint64_t *kv_full = bar + 4, *kv_empty = kv_full + kStages;  // [stage]
+  uint64_t *s_full = kv_empty + kStages;                       // [S buffer]
+  uint64_t *p_full = s_full + kSBuf;                           // [tile][step parity]
+  uint64_t *o_full = p_full + 4;                               // [tile]: every PV_t
+  uint64_t *o_done = o_full + 2;                               // [tile]: the item's last PV_t
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(o_done + 2);
 
-  const int nq = S / BQ, npair = (nq + 1) >> 1;
-  // blockIdx.x (fastest in launch order) walks the heads, blockIdx.y the
-  // pairs: every head's heaviest causal pair launches before any lighter one
-  const int pr = CAUSAL ? npair - 1 - (int)blockIdx.y : (int)blockIdx.y;
-  const int bh = blockIdx.x, b = bh / H, h = bh % H;
+  const int G = gridDim.x, c = blockIdx.x;
   const int d = H * DH;
-  const int qb0 = 2 * pr;
-  const bool has1 = qb0 + 1 < nq;
-  const int nkv0 = CAUSAL ? qb0 + 1 : S / BKV;
-  const int nkv1 = has1 ? (CAUSAL ? qb0 + 2 : S / BKV) : 0;
-  const int mn = nkv0 < nkv1 ? nkv0 : nkv1, nall = nkv0 > nkv1 ? nkv0 : nkv1, npos = nkv0 + nkv1;
-  const int tlast = nkv1 >= nkv0 ? 1 : 0;  // the tile that runs alone past step mn
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row0 = b * S;
+  auto next_item = [&](const Item &it) {
+    return make_item<CAUSAL>(it.r + 1, c, G, S, H, BH, it.kvb + (it.nkv0 > it.nkv1 ? it.nkv0 : it.nkv1),
+                             it.pb + it.npos, it.g0 + it.nkv0, it.g1 + it.nkv1);
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm);
-    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+      mbar_init(&o_full[i], 1);
+      mbar_init(&o_done[i], 1);
+    }
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
     }
     for (int i = 0; i < kSBuf; ++i) mbar_init(&s_full[i], 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&p_full[i], 128);
-      mbar_init(&o_full[i], 1);
-    }
+    for (int i = 0; i < 4; ++i) mbar_init(&p_full[i], 128);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -154,75 +208,89 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp < 4) {
     reg_dealloc<72>();  // 3 x 168 per SMSP at launch = 72 + 2 x 216
     if (warp == 0 && lane == 0) {
-      mbar_expect_tx(q_full, (has1 ? 2 : 1) * kTile);
-      tma_load_2d(sQ, &tm, q_full, h * DH, row0 + qb0 * BQ);
-      if (has1) tma_load_2d(sQ + kTile, &tm, q_full, h * DH, row0 + (qb0 + 1) * BQ);
-      for (int j = 0; j < nall; ++j) {
-        const int st = j % kStages;
-        mbar_wait(&kv_empty[st], ((j / kStages) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[st], 2 * kTile);
-        tma_load_2d(sK + st * kTile, &tm, &kv_full[st], d + h * DH, row0 + j * BKV);
-        tma_load_2d(sV + st * kTile, &tm, &kv_full[st], 2 * d + h * DH, row0 + j * BKV);
+      for (Item it = make_item<CAUSAL>(0, c, G, S, H, BH, 0, 0, 0, 0); it.valid; it = next_item(it)) {
+        const int row0 = it.b * S, qp = it.r & 1;
+        mbar_wait(&q_empty[qp], ((it.r >> 1) & 1) ^ 1);
+        mbar_expect_tx(&q_full[qp], (it.nkv1 > 0 ? 2 : 1) * kTile);
+        tma_load_2d(sQ + (2 * qp) * kTile, &tm, &q_full[qp], it.h * DH, row0 + 2 * it.pr * BQ);
+        if (it.nkv1 > 0)
+          tma_load_2d(sQ + (2 * qp + 1) * kTile, &tm, &q_full[qp], it.h * DH, row0 + (2 * it.pr + 1) * BQ);
+        const int nall = it.nkv0 > it.nkv1 ? it.nkv0 : it.nkv1;
+        for (int j = 0; j < nall; ++j) {
+          const int kb = it.kvb + j, st = kb % kStages;
+          mbar_wait(&kv_empty[st], ((kb / kStages) & 1) ^ 1);
+          mbar_expect_tx(&kv_full[st], 2 * kTile);
+          tma_load_2d(sK + st * kTile, &tm, &kv_full[st], d + it.h * DH, row0 + j * BKV);
+          tma_load_2d(sV + st * kTile, &tm, &kv_full[st], 2 * d + it.h * DH, row0 + j * BKV);
+        }
       }
     } else if (warp == 1 && lane == 0) {
       constexpr uint32_t idesc_s = idesc_bf16_f32(BQ, BKV, 0, 0);  // Q K-major, K K-major
       constexpr uint32_t idesc_o = idesc_bf16_f32(BQ, DH, 0, 1);   // P (TMEM), V MN-major
-      // position n of the S / PV sequence -> (tile, step)
-      auto at = [&](int n, int &t, int &j) {
-        if (n < 2 * mn) {
-          t = n & 1;
-          j = n >> 1;
-        } else {
-          t = tlast;
-          j = mn + (n - 2 * mn);
+      // S cursor: runs up to kSBuf positions ahead of the PVs, across items
+      Item sit = make_item<CAUSAL>(0, c, G, S, H, BH, 0, 0, 0, 0);
+      int s_loc = 0;
+      auto issue_next_s = [&]() {
+        while (sit.valid && s_loc >= sit.npos) {
+          sit = next_item(sit);
+          s_loc = 0;
         }
-      };
-      mbar_wait(q_full, 0);
-      auto issue_s = [&](int n) {
+        if (!sit.valid) return;
+        const int qp = sit.r & 1;
+        if (s_loc == 0) mbar_wait(&q_full[qp], (sit.r >> 1) & 1);
         int t, j;
-        at(n, t, j);
-        const int st = j % kStages;
-        mbar_wait(&kv_full[st], (j / kStages) & 1);
+        sit.at(s_loc, t, j);
+        const int kb = sit.kvb + j, st = kb % kStages, P = sit.pb + s_loc;
+        mbar_wait(&kv_full[st], (kb / kStages) & 1);
         tc_fence_after();
-        const uint32_t q_base = smem_u32(sQ + t * kTile), k_base = smem_u32(sK + st * kTile);
+        const uint32_t q_base = smem_u32(sQ + (2 * qp + t) * kTile), k_base = smem_u32(sK + st * kTile);
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk)
-          mma_bf16(tmem + (n % kSBuf) * BKV, umma_desc_sw128(q_base + kk * 32, 16, 1024),
+          mma_bf16(tmem + (P % kSBuf) * BKV, umma_desc_sw128(q_base + kk * 32, 16, 1024),
                    umma_desc_sw128(k_base + kk * 32, 16, 1024), idesc_s, kk > 0);
-        mma_commit(&s_full[n % kSBuf]);
+        mma_commit(&s_full[P % kSBuf]);
+        if (s_loc == sit.npos - 1) mma_commit(&q_empty[qp]);  // the item's last Q K^T: its Q pair is free
+        ++s_loc;
       };
-      for (int n = 0; n < kSBuf && n < npos; ++n) issue_s(n);
-      for (int n = 0; n < npos; ++n) {
-        int t, j;
-        at(n, t, j);
-        mbar_wait(&p_full[t], j & 1);  // P_t(j) written into S buffer n % 3 (and O_t rescaled)
-        tc_fence_after();
-        const uint32_t v_base = smem_u32(sV + (j % kStages) * kTile);
-        const uint32_t p_tm = tmem + (n % kSBuf) * BKV;
+      for (int k = 0; k < kSBuf; ++k) issue_next_s();
+      for (Item it = make_item<CAUSAL>(0, c, G, S, H, BH, 0, 0, 0, 0); it.valid; it = next_item(it)) {
+        for (int n = 0; n < it.npos; ++n) {
+          int t, j;
+          it.at(n, t, j);
+          const int gs = (t == 0 ? it.g0 : it.g1) + j, P = it.pb + n, kb = it.kvb + j;
+          mbar_wait(&p_full[2 * t + (gs & 1)], (gs >> 1) & 1);  // P_t(j) in S buffer P % 3 (and O_t rescaled)
+          tc_fence_after();
+          const uint32_t v_base = smem_u32(sV + (kb % kStages) * kTile);
+          const uint32_t p_tm = tmem + (P % kSBuf) * BKV;
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk)
-          mma_bf16_ts(tmem + C_O + t * DH, p_tm + kk * 8, umma_desc_sw128(v_base + kk * 2048, kTile, 1024), idesc_o,
-                      (j > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(&o_full[t]);
-        if (t == 1 || j >= mn) mma_commit(&kv_empty[j % kStages]);  // last use of K_j / V_j
-        // S(n + 3) overwrites P(n) in TMEM: issued after PV(n), which reads it first
-        if (n + kSBuf < npos) issue_s(n + kSBuf);
+          for (int kk = 0; kk < BKV / 16; ++kk)
+            mma_bf16_ts(tmem + C_O + t * DH, p_tm + kk * 8, umma_desc_sw128(v_base + kk * 2048, kTile, 1024), idesc_o,
+                        (j > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(&o_full[t]);
+          if (j == (t == 0 ? it.nkv0 : it.nkv1) - 1) mma_commit(&o_done[t]);  // O_t of this item final
+          if (t == 1 || j >= it.mn) mma_commit(&kv_empty[kb % kStages]);  // last use of K_j / V_j
+          // S(P + 3) overwrites P(P) in TMEM: issued after PV(P), which reads it first
+          issue_next_s();
+        }
       }
     }
   } else {
     reg_alloc<216>();
     const int t = (warp >> 2) - 1;
-    const int nkv = t == 0 ? nkv0 : nkv1;
-    if (nkv > 0) {
-      const int q4 = warp & 3;
-      const int r = q4 * 32 + lane;  // query row inside the tile == TMEM lane
-      const int qb = qb0 + t;
-      const uint32_t lane_addr = (uint32_t)(q4 * 32) << 16;
-      const uint32_t o_addr = tmem + lane_addr + C_O + t * DH;
-      const float2 sc2 = make_float2(scale_log2, scale_log2);
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;  // query row inside the tile == TMEM lane
+    const uint32_t lane_addr = (uint32_t)(q4 * 32) << 16;
+    const uint32_t o_addr = tmem + lane_addr + C_O + t * DH;
+    const float2 sc2 = make_float2(scale_log2, scale_log2);
+    int done = 0;  // items this tile has finished (o_done parity)
+    for (Item it = make_item<CAUSAL>(0, c, G, S, H, BH, 0, 0, 0, 0); it.valid; it = next_item(it)) {
+      const int nkv = t == 0 ? it.nkv0 : it.nkv1;
+      if (nkv == 0) continue;
+      const int qb = 2 * it.pr + t, row0 = it.b * S, g_base = t == 0 ? it.g0 : it.g1;
       float m = -INFINITY, l = 0.f;  // m: the max the exponents are taken against (log2 domain)
       for (int j = 0; j < nkv; ++j) {
-        const int n = j < mn ? 2 * j + t : 2 * mn + (j - mn);
+        const int n = it.pb + (j < it.mn ? 2 * j + t : 2 * it.mn + (j - it.mn));  // global position
+        const int gs = g_base + j;                                                // global step of this tile
         const int buf = n % kSBuf;
         const uint32_t s_addr = tmem + lane_addr + buf * BKV;
         mbar_wait(&s_full[buf], (n / kSBuf) & 1);
@@ -234,17 +302,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld_wait();
         if (CAUSAL && j == qb) {  // diagonal tile: keys after the query are masked
 #pragma unroll
-          for (int c = 0; c < BKV; ++c)
-            if (c > r) v[c] = 0xff800000u;  // -inf
+          for (int cc = 0; cc < BKV; ++cc)
+            if (cc > r) v[cc] = 0xff800000u;  // -inf
         }
         float mx[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) mx[e] = fmaxf(__uint_as_float(v[e]), __uint_as_float(v[4 + e]));
 #pragma unroll
-        for (int c = 8; c < BKV; c += 8) {
+        for (int cc = 8; cc < BKV; cc += 8) {
 #pragma unroll
           for (int e = 0; e < 4; ++e)
-            mx[e] = fmaxf(mx[e], fmaxf(__uint_as_float(v[c + e]), __uint_as_float(v[c + 4 + e])));
+            mx[e] = fmaxf(mx[e], fmaxf(__uint_as_float(v[cc + e]), __uint_as_float(v[cc + 4 + e])));
         }
         const float m_row = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * scale_log2;
         float alpha = 1.f;
@@ -253,8 +321,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           m = m_row;
         }
         if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {  // warp-uniform: tcgen05.ld / st are .sync.aligned
-          // PV_t(j - 2) is complete (S(n) was issued after it); wait for PV_t(j - 1)
-          mbar_wait(&o_full[t], (j - 1) & 1);
+          // PV_t(gs - 2) is complete (S of this step was issued after it); wait for PV_t(gs - 1)
+          mbar_wait(&o_full[t], (gs - 1) & 1);
           tc_fence_after();
           const float2 a2 = make_float2(alpha, alpha);
 #pragma unroll
@@ -263,10 +331,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_ld_32x32b_x32(o_addr + c0, ov);
             tmem_ld_wait();
 #pragma unroll
-            for (int c = 0; c < 32; c += 2) {
-              const float2 o2 = mul2(make_float2(__uint_as_float(ov[c]), __uint_as_float(ov[c + 1])), a2);
-              ov[c] = __float_as_uint(o2.x);
-              ov[c + 1] = __float_as_uint(o2.y);
+            for (int cc = 0; cc < 32; cc += 2) {
+              const float2 o2 = mul2(make_float2(__uint_as_float(ov[cc]), __uint_as_float(ov[cc + 1])), a2);
+              ov[cc] = __float_as_uint(o2.x);
+              ov[cc + 1] = __float_as_uint(o2.y);
             }
             tmem_st_32x32b_x32(o_addr + c0, ov);
           }
@@ -277,11 +345,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c0 = 0; c0 < BKV; c0 += 32) {
           uint32_t pk[16];
 #pragma unroll
-          for (int c = 0; c < 32; c += 2) {
-            const float2 x = fma2(make_float2(__uint_as_float(v[c0 + c]), __uint_as_float(v[c0 + c + 1])), sc2, nm2);
+          for (int cc = 0; cc < 32; cc += 2) {
+            const float2 x = fma2(make_float2(__uint_as_float(v[c0 + cc]), __uint_as_float(v[c0 + cc + 1])), sc2, nm2);
             const float2 p = make_float2(ex2(x.x), ex2(x.y));
-            rs[(c >> 1) & 1] = add2(rs[(c >> 1) & 1], p);
-            pk[c >> 1] = bf16x2(p.x, p.y);
+            rs[(cc >> 1) & 1] = add2(rs[(cc >> 1) & 1], p);
+            pk[cc >> 1] = bf16x2(p.x, p.y);
           }
           // keys c0..c0+31 -> P columns c0/2..c0/2+15 (every S column already read)
           tmem_st_32x32b_x16(s_addr + (c0 >> 1), pk);
@@ -289,28 +357,33 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_st_wait();
         l = l * alpha + ((rs[0].x + rs[0].y) + (rs[1].x + rs[1].y));
         tc_fence_before();
-        mbar_arrive(&p_full[t]);
+        mbar_arrive(&p_full[2 * t + (gs & 1)]);
       }
-      mbar_wait(&o_full[t], (nkv - 1) & 1);
+      // epilogue: O / l and lse once the item's last PV_t has completed (a
+      // dedicated barrier: o_full's parity can lag by two phases here); the next
+      // item's first PV_t overwrites O only after this thread's next P
+      mbar_wait(&o_done[t], done & 1);
+      ++done;
       tc_fence_after();
       const float inv = 1.f / l;
-      __nv_bfloat16 *orow = out + (int64_t)(row0 + qb * BQ + r) * d + h * DH;
+      __nv_bfloat16 *orow = out + (int64_t)(row0 + qb * BQ + r) * d + it.h * DH;
 #pragma unroll
       for (int c0 = 0; c0 < DH; c0 += 32) {
         uint32_t ov[32];
         tmem_ld_32x32b_x32(o_addr + c0, ov);
         tmem_ld_wait();
 #pragma unroll
-        for (int c = 0; c < 32; c += 8) {
+        for (int cc = 0; cc < 32; cc += 8) {
           uint4 w;
-          w.x = bf16x2(__uint_as_float(ov[c]) * inv, __uint_as_float(ov[c + 1]) * inv);
-          w.y = bf16x2(__uint_as_float(ov[c + 2]) * inv, __uint_as_float(ov[c + 3]) * inv);
-          w.z = bf16x2(__uint_as_float(ov[c + 4]) * inv, __uint_as_float(ov[c + 5]) * inv);
-          w.w = bf16x2(__uint_as_float(ov[c + 6]) * inv, __uint_as_float(ov[c + 7]) * inv);
-          *reinterpret_cast<uint4 *>(orow + c0 + c) = w;
+          w.x = bf16x2(__uint_as_float(ov[cc]) * inv, __uint_as_float(ov[cc + 1]) * inv);
+          w.y = bf16x2(__uint_as_float(ov[cc + 2]) * inv, __uint_as_float(ov[cc + 3]) * inv);
+          w.z = bf16x2(__uint_as_float(ov[cc + 4]) * inv, __uint_as_float(ov[cc + 5]) * inv);
+          w.w = bf16x2(__uint_as_float(ov[cc + 6]) * inv, __uint_as_float(ov[cc + 7]) * inv);
+          *reinterpret_cast<uint4 *>(orow + c0 + cc) = w;
         }
       }
-      lse[(int64_t)(row0 + qb * BQ + r) * H + h] = m + log2f(l);
+      lse[(int64_t)(row0 + qb * BQ + r) * H + it.h] = m + log2f(l);
+      tc_fence_before();
     }
   }
   tc_fence_before();
@@ -365,7 +438,11 @@ int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causa
     attr[causal ? 1 : 0] = true;
   }
   const int npair = (S / BQ + 1) / 2;
-  k<<<dim3(B * H, npair), kThreads, kSmem, s>>>(tm, static_cast<__nv_bfloat16 *>(o), lse, S, H, scale_log2);
+  static int sms = 0;
+  if (!sms) HM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const int items = npair * B * H;
+  k<<<dim3(items < sms ? items : sms), kThreads, kSmem, s>>>(tm, static_cast<__nv_bfloat16 *>(o), lse, S, H, B * H,
+                                                             scale_log2);
   count_launch();
   HM_CUDA(cudaGetLastError());
   return HM_OK;
