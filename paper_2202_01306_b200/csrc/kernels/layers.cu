@@ -677,15 +677,19 @@ __global__ void __launch_bounds__(WARPS * 32)
   for (int64_t r = r_begin + grp; r < r_end; r += G, par ^= 1) {
     const float4 *dyr = reinterpret_cast<const float4 *>(dy + r * d);
     const float4 *xr = reinterpret_cast<const float4 *>(x + r * d);
-    float4 a[NV4], v[NV4];
+    const float4 *rr = resid ? reinterpret_cast<const float4 *>(resid + r * d) : nullptr;
+    // dy, x and the residual all in flight before the first use (the residual
+    // would otherwise be a second dependent HBM round trip after the barrier)
+    float4 a[NV4], v[NV4], q[NV4];
 #pragma unroll
     for (int k = 0; k < NV4; ++k) {
       const int i = wi * 32 + lane + 32 * WPR * k;
       if (i < n4) {
         a[k] = dyr[i];
         v[k] = xr[i];
+        q[k] = rr ? rr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
       } else {
-        a[k] = v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        a[k] = v[k] = q[k] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
     const float mu = mean[r], rs = rstd[r];
@@ -721,21 +725,16 @@ __global__ void __launch_bounds__(WARPS * 32)
     c1 /= d;
     c2 /= d;
     float4 *outr = reinterpret_cast<float4 *>(out + r * d);
-    const float4 *rr = resid ? reinterpret_cast<const float4 *>(resid + r * d) : nullptr;
     uint2 *ob = out_bf ? reinterpret_cast<uint2 *>(out_bf + r * d) : nullptr;
 #pragma unroll
     for (int k = 0; k < NV4; ++k) {
       const int i = wi * 32 + lane + 32 * WPR * k;
       if (i < n4) {
         float4 o;
-        o.x = rs * (a[k].x * gg[k].x - c1 - v[k].x * c2);
-        o.y = rs * (a[k].y * gg[k].y - c1 - v[k].y * c2);
-        o.z = rs * (a[k].z * gg[k].z - c1 - v[k].z * c2);
-        o.w = rs * (a[k].w * gg[k].w - c1 - v[k].w * c2);
-        if (rr) {
-          const float4 q = rr[i];
-          o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
-        }
+        o.x = rs * (a[k].x * gg[k].x - c1 - v[k].x * c2) + q[k].x;
+        o.y = rs * (a[k].y * gg[k].y - c1 - v[k].y * c2) + q[k].y;
+        o.z = rs * (a[k].z * gg[k].z - c1 - v[k].z * c2) + q[k].z;
+        o.w = rs * (a[k].w * gg[k].w - c1 - v[k].w * c2) + q[k].w;
         outr[i] = o;
         if (ob) {
           __nv_bfloat162 p0 = __floats2bfloat162_rn(o.x, o.y), p1 = __floats2bfloat162_rn(o.z, o.w);
