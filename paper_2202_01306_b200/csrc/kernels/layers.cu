@@ -284,6 +284,65 @@ __global__ void __launch_bounds__(256) ln_fwd_reg_kernel(const float *__restrict
   }
 }
 
+// Rows of 1024 < d <= 2048 (GPT-2 XL's 1600): two warps per row, four rows per
+// 256-thread block, half the row's float4 per lane (the one-warp kernel holds
+// 13 float4 per lane at d = 1600 and keeps fewer rows in flight); mean and
+// variance combine across the pair under a named barrier.
+template <int NV4>
+__global__ void __launch_bounds__(256) ln_fwd_pair_kernel(const float *__restrict__ x, const float *__restrict__ gam,
+                                                          const float *__restrict__ bet, __nv_bfloat16 *__restrict__ y,
+                                                          float *__restrict__ mean, float *__restrict__ rstd,
+                                                          int64_t rows, int d, float eps) {
+  pdl_wait();
+  __shared__ float red[2][4][2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, grp = warp >> 1, wi = warp & 1;
+  const int64_t r = (int64_t)blockIdx.x * 4 + grp;
+  if (r >= rows) return;  // both warps of the row leave together
+  const float4 *xr = reinterpret_cast<const float4 *>(x + r * d);
+  const int n4 = d / 4;
+  float4 v[NV4];
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV4; ++k) {
+    const int i = wi * 32 + lane + 64 * k;
+    v[k] = i < n4 ? xr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+#pragma unroll
+  for (int k = 0; k < NV4; ++k) s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+  s = warp_sum(s);
+  if (lane == 0) red[0][grp][wi] = s;
+  asm volatile("bar.sync %0, 64;" ::"r"(1 + grp) : "memory");
+  const float mu = (red[0][grp][0] + red[0][grp][1]) / d;
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV4; ++k)
+    if (wi * 32 + lane + 64 * k < n4) {
+      const float a = v[k].x - mu, b = v[k].y - mu, c = v[k].z - mu, e = v[k].w - mu;
+      q += (a * a + b * b) + (c * c + e * e);
+    }
+  q = warp_sum(q);
+  if (lane == 0) red[1][grp][wi] = q;
+  asm volatile("bar.sync %0, 64;" ::"r"(1 + grp) : "memory");
+  const float rs = rsqrtf((red[1][grp][0] + red[1][grp][1]) / d + eps);
+  uint2 *yr = reinterpret_cast<uint2 *>(y + r * d);
+  const float4 *g4 = reinterpret_cast<const float4 *>(gam);
+  const float4 *b4 = reinterpret_cast<const float4 *>(bet);
+#pragma unroll
+  for (int k = 0; k < NV4; ++k) {
+    const int i = wi * 32 + lane + 64 * k;
+    if (i < n4) {
+      const float4 gg = __ldg(g4 + i), bb = __ldg(b4 + i);
+      __nv_bfloat162 a = __floats2bfloat162_rn((v[k].x - mu) * rs * gg.x + bb.x, (v[k].y - mu) * rs * gg.y + bb.y);
+      __nv_bfloat162 c = __floats2bfloat162_rn((v[k].z - mu) * rs * gg.z + bb.z, (v[k].w - mu) * rs * gg.w + bb.w);
+      yr[i] = make_uint2(*reinterpret_cast<uint32_t *>(&a), *reinterpret_cast<uint32_t *>(&c));
+    }
+  }
+  if (lane == 0 && wi == 0) {
+    mean[r] = mu;
+    rstd[r] = rs;
+  }
+}
+
 // Wide rows (d > 2048, e.g. 8192): one 256-thread block per row, the row in
 // registers (NV4 float4 per thread, all loads in flight), mean and variance by
 // two block reductions -- one HBM read of x instead of three L2 passes.
@@ -357,6 +416,14 @@ int ln_fwd(const float *x, const float *g, const float *b, void *y, float *mean,
     auto yy = static_cast<__nv_bfloat16 *>(y);
     const int nv4 = (d / 4 + 31) / 32;
     cudaError_t e = cudaErrorInvalidValue;
+    if (d > 1024 && d <= 2048) {  // two warps per row (4096 x 1600: see profiles/r02_ln_perf*)
+      const dim3 grid2((unsigned)((rows + 3) / 4));
+      const int p4 = (d / 4 + 63) / 64;
+      HM_CUDA(launch_pdl(p4 <= 7 ? ln_fwd_pair_kernel<7> : ln_fwd_pair_kernel<8>, grid2, block, 0, s, x, g, b, yy, mean,
+                         rstd, rows, d, 1e-5f));
+      count_launch();
+      return HM_OK;
+    }
     if (nv4 <= 4) e = launch_pdl(ln_fwd_reg_kernel<4>, grid, block, 0, s, x, g, b, yy, mean, rstd, rows, d, 1e-5f);
     else if (nv4 <= 8) e = launch_pdl(ln_fwd_reg_kernel<8>, grid, block, 0, s, x, g, b, yy, mean, rstd, rows, d, 1e-5f);
     else if (nv4 <= 13) e = launch_pdl(ln_fwd_reg_kernel<13>, grid, block, 0, s, x, g, b, yy, mean, rstd, rows, d, 1e-5f);
