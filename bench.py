@@ -312,10 +312,12 @@ def _gemm_groups(launches, top=8):
 
 
 def _ncu_traffic() -> dict:
-    """DRAM traffic of the dominant kernel from the committed `ncu --set full`
-    capture (profiles/r01_gemm_ncu_summary.json, made by tools/ncu_summary.py)."""
-    p = os.path.join(ROOT, "profiles", "r01_gemm_ncu_summary.json")
-    if not os.path.exists(p):
+    """DRAM traffic of the dominant kernel from the newest committed `ncu --set
+    full` capture of in-step GEMM launches (profiles/r0N_gemm_ncu_summary.json,
+    made by tools/ncu_summary.py)."""
+    cands = [os.path.join(ROOT, "profiles", f"r0{n}_gemm_ncu_summary.json") for n in (2, 1)]
+    p = next((c for c in cands if os.path.exists(c)), None)
+    if p is None:
         return {}
     d = json.load(open(p))
     return {"traffic": d["dram_bytes_per_launch_mean"],
