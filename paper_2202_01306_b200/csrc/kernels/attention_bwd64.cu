@@ -431,8 +431,7 @@ int backward_main(const void *qkv, const void *dout, const float *lse, const flo
     HM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
     attr[causal ? 1 : 0] = true;
   }
-  static int sms = 0;
-  if (!sms) HM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const int sms = current_sm_count();
   const int items = (S / BKV) * B * H;
   const float scale = 1.f / sqrtf((float)DH);
   static const bool tracing = getenv("HM_ATTN_TRACE") && getenv("HM_ATTN_TRACE")[0] == '1';

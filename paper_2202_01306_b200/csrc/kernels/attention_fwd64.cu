@@ -438,8 +438,7 @@ int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causa
     attr[causal ? 1 : 0] = true;
   }
   const int npair = (S / BQ + 1) / 2;
-  static int sms = 0;
-  if (!sms) HM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const int sms = current_sm_count();
   const int items = npair * B * H;
   k<<<dim3(items < sms ? items : sms), kThreads, kSmem, s>>>(tm, static_cast<__nv_bfloat16 *>(o), lse, S, H, B * H,
                                                              scale_log2);

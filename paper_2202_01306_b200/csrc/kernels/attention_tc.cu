@@ -757,8 +757,7 @@ int backward_main(const void *qkv, const void *dout, const float *lse, const flo
     attr[causal ? 1 : 0] = true;
   }
   const float scale = 1.f / sqrtf((float)DH);
-  static int sms = 0;
-  if (!sms) HM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const int sms = current_sm_count();
   const int items = (S / BKV) * B * H;
   // HM_ATTN_TRACE=1 (diagnostics): CTA 0's phase timestamps, printed to stderr
   static const bool tracing = getenv("HM_ATTN_TRACE") && getenv("HM_ATTN_TRACE")[0] == '1';
@@ -814,8 +813,7 @@ int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causa
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
   ProfScope ps(KC_ATTN_FWD, s, 4.0 * B * (double)S * S * H * DH * (causal ? 0.5 : 1.0), (double)B * S * H * DH * 2 * 4);
   static bool attrq[2] = {false, false};
-  static int sms_q = 0;
-  if (!sms_q) HM_CUDA(cudaDeviceGetAttribute(&sms_q, cudaDevAttrMultiProcessorCount, 0));
+  const int sms_q = current_sm_count();
   auto kq = causal ? fwd2p_kernel<true> : fwd2p_kernel<false>;
   if (!attrq[causal ? 1 : 0]) {
     HM_CUDA(cudaFuncSetAttribute(kq, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem2P));

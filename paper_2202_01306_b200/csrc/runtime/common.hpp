@@ -22,6 +22,14 @@ inline int fail(int code, const std::string &msg) {
 // delta over its timed region as "gpu_launches".
 std::atomic<int64_t> &launch_counter();
 inline void count_launch(int64_t n = 1) { launch_counter().fetch_add(n, std::memory_order_relaxed); }
+// SMs of the calling thread's current device (persistent kernels size their grid with it)
+inline int current_sm_count() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      n <= 0)
+    n = 148;
+  return n;
+}
 
 // Optional per-launch timing hook (set by the runtime while profiling).
 enum KernelClass { KC_GEMM = 0, KC_ATTN_FWD, KC_ATTN_BWD, KC_LAYERNORM, KC_XENT, KC_ADAM, KC_MISC, KC_COUNT };
