@@ -173,9 +173,11 @@ def _attn_ref(qkv, B, S, H, DH, causal):
 
 @pytest.mark.parametrize("B,S,H,DH,causal", [(2, 128, 4, 64, True), (1, 512, 2, 64, False),
                                              (2, 256, 3, 64, True), (1, 256, 2, 128, True),
-                                             # head_dim 64: several persistent items per CTA,
-                                             # odd 128-key block count
+                                             # head_dim 64: odd 128-key block count; more
+                                             # (sample-head, tile pair) / key-block items than
+                                             # SMs, so persistent CTAs walk several items
                                              (3, 1024, 5, 64, True), (2, 384, 3, 64, False),
+                                             (8, 1024, 25, 64, True), (4, 512, 40, 64, False),
                                              # head_dim 128 (attention_tc128.cu): odd query-tile count,
                                              # full attention, the >HBM GPT shape at 1024 tokens
                                              (2, 384, 3, 128, True), (1, 512, 2, 128, False),
