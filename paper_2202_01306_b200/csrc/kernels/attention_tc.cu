@@ -376,7 +376,7 @@ static EncodeFn encode_fn() {
 // dV / dK MMAs for the previous item's accumulators to have been drained.
 // ---------------------------------------------------------------------------
 constexpr uint32_t kDqStage = BQ * DH * 4;  // 32 KB: dQ tile (fp32) staged for the TMA reduce-add
-constexpr size_t kSmemBwd = 1024 + 2 * kTileBytes /*K,V*/ + 4 * kTileBytes /*Q,dO x2*/ + 2 * kPBytes /*P^T,dS^T*/ +
+constexpr size_t kSmemBwd = 1024 + 2 * kTileBytes /*K,V*/ + 4 * kTileBytes /*Q,dO x2*/ + 2 * kPBytes /*dS^T x2*/ +
                             kDqStage +
                             2 * 2 * BQ * 4 /*lse,D x2*/ + 512;
 
@@ -398,19 +398,19 @@ __global__ void __launch_bounds__(kThreads2, 1)
   uint8_t *sV = sK + kTileBytes;
   uint8_t *sQ = sV + kTileBytes;          // [2] stages
   uint8_t *sdO = sQ + 2 * kTileBytes;     // [2] stages
-  uint8_t *sP = sdO + 2 * kTileBytes;     // P^T  [128 keys x 128 queries]
-  uint8_t *sdS = sP + kPBytes;            // dS^T
-  uint8_t *sDQ = sdS + kPBytes;           // dQ stage: 2 x [128 rows x 32 fp32] SW128 chunks
+  uint8_t *sdS = sdO + 2 * kTileBytes;    // dS^T [2 blocks][128 keys x 128 queries] (P^T lives in TMEM)
+  uint8_t *sDQ = sdS + 2 * kPBytes;       // dQ stage: 2 x [128 rows x 32 fp32] SW128 chunks
   float *sL = reinterpret_cast<float *>(sDQ + kDqStage);  // [2][128] lse
   float *sD = sL + 2 * BQ;                               // [2][128] D
   uint64_t *bar = reinterpret_cast<uint64_t *>(sD + 2 * BQ);
   uint64_t *kv_full = bar, *kv_empty = bar + 1;
   uint64_t *q_full = bar + 2, *q_empty = bar + 4;
   uint64_t *st_full = bar + 6, *st_empty = bar + 7;
-  uint64_t *p_full = bar + 8, *p_empty = bar + 9;
+  uint64_t *p_full = bar + 8, *pt_free = bar + 9;  // P^T (TMEM) + dS^T (smem) written / P^T read by dV
   uint64_t *dq_full = bar + 10, *dq_empty = bar + 11;
   uint64_t *acc_full = bar + 12, *acc_empty = bar + 13;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 14);
+  uint64_t *ds_empty = bar + 14;                  // [dS^T buffer]: read by dK / dQ
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 16);
 
   const int nq = S / BQ, nkb = S / BKV, n_items = nkb * BH;
   const int G = gridDim.x, c = blockIdx.x;
@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     h = bh % H;
   };
   // TMEM columns
-  constexpr uint32_t C_ST = 0, C_DP = 128, C_DV = 256, C_DK = 320, C_DQ = 384;
+  constexpr uint32_t C_ST = 0, C_DP = 128, C_DV = 256, C_DK = 320, C_DQ = 384, C_PT = 448;
   // diagnostics (HM_ATTN_TRACE=1): clock64 at the phase boundaries of CTA 0's
   // first 64 blocks, trace[event * 64 + block]
   auto mark = [&](int ev, int nn) {
@@ -449,7 +449,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
     mbar_init(st_full, 1);
     mbar_init(st_empty, 256);
     mbar_init(p_full, 256);
-    mbar_init(p_empty, 1);
+    mbar_init(pt_free, 1);
+    mbar_init(&ds_empty[0], 1);
+    mbar_init(&ds_empty[1], 1);
     mbar_init(dq_full, 1);
     mbar_init(dq_empty, 256);
     mbar_init(acc_full, 1);
@@ -488,7 +490,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
       constexpr uint32_t id_kmn = idesc_bf16_f32(128, DH, 0, 1);   // dV, dK: A K-major, B MN-major
       constexpr uint32_t id_mnmn = idesc_bf16_f32(128, DH, 1, 1);  // dQ: A MN-major (dS), B MN-major (K)
       const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV);
-      const uint32_t p_base = smem_u32(sP), ds_base = smem_u32(sdS);
+      const uint32_t ds_buf0 = smem_u32(sdS);
       // S^T = K Q^T and dP^T = V dO^T of running block n (TMEM C_ST / C_DP)
       auto issue_st = [&](int n) {
         const int st = n & 1;
@@ -519,22 +521,29 @@ __global__ void __launch_bounds__(kThreads2, 1)
           // block n+1's S^T / dP^T go in as soon as the softmax warps have read
           // block n's (st_empty), ahead of block n's gradient MMAs, so the next
           // elementwise pass never waits for them.  (Issuing them after dV /
-          // dK(n) instead measured 4450 vs 3800 cycles per block, HM_ATTN_TRACE:
-          // the next softmax then starts only after dV / dK.)  What bounds a
-          // block is the single P^T / dS^T buffer in shared memory: softmax n+1
-          // writes only after dV / dK / dQ(n) have read it; double-buffering it
-          // needs 264 KB.
+          // dK(n) instead measured 4450 vs 3800 cycles per block, HM_ATTN_TRACE.)
+          // P^T lives in TMEM (the dV MMA's A operand) and dS^T is double-
+          // buffered in shared memory, so softmax n+1 waits only for dV(n).
+          // What bounds a block is shared-memory bandwidth: the SS MMAs read
+          // ~160 KB per block (128 B / clock feeds a 128x64x16 SS MMA exactly,
+          // so these N = 64 MMAs run at 48 cycles alone), plus the TMA, dS^T
+          // and dQ-stage traffic: ~2300 of the ~3800 cycles per block, and the
+          // trace shows the MMAs at ~120 cycles each (profiles/r02_attn_bwd_trace_pt_tmem.log).
           if (blk + 1 < count) issue_st(n + 1);
           const uint32_t q_base = smem_u32(sQ + st * kTileBytes), do_base = smem_u32(sdO + st * kTileBytes);
           mbar_wait(p_full, ph);
           mark(1, n);
           if (blk == 0) mbar_wait(acc_empty, (r & 1) ^ 1);  // the previous item's dV / dK drained
           tc_fence_after();
+          const uint32_t ds_base = ds_buf0 + (n & 1) * kPBytes;
 #pragma unroll
-          for (int kk = 0; kk < BQ / 16; ++kk) {  // reduction over the 128 queries
+          for (int kk = 0; kk < BQ / 16; ++kk)  // dV += P^T dO, P^T from TMEM (16 queries = 8 columns)
+            mma_bf16_ts(tmem + C_DV, tmem + C_PT + kk * 8, umma_desc_sw128(do_base + kk * 2048, BQ * 128, 1024),
+                        id_kmn, (blk > 0 || kk > 0) ? 1u : 0u);
+          mma_commit(pt_free);  // P^T read: the next block's softmax may overwrite it
+#pragma unroll
+          for (int kk = 0; kk < BQ / 16; ++kk) {  // dK += dS^T Q, reduction over the 128 queries
             const uint32_t a_off = (kk >> 2) * (BKV * 128) + (kk & 3) * 32;
-            mma_bf16(tmem + C_DV, umma_desc_sw128(p_base + a_off, 16, 1024),
-                     umma_desc_sw128(do_base + kk * 2048, BQ * 128, 1024), id_kmn, (blk > 0 || kk > 0) ? 1u : 0u);
             mma_bf16(tmem + C_DK, umma_desc_sw128(ds_base + a_off, 16, 1024),
                      umma_desc_sw128(q_base + kk * 2048, BQ * 128, 1024), id_kmn, (blk > 0 || kk > 0) ? 1u : 0u);
           }
@@ -546,7 +555,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
                      umma_desc_sw128(k_base + kk * 2048, BKV * 128, 1024), id_mnmn, kk > 0);
           mma_commit(dq_full);
           mma_commit(&q_empty[st]);
-          mma_commit(p_empty);
+          mma_commit(&ds_empty[n & 1]);
           mark(2, n);
         }
         mma_commit(acc_full);
@@ -597,8 +606,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
       }
     };
     const int hq = wg;
-    uint8_t *prow = sP + rr * 128 + hq * (BKV * 128);
-    uint8_t *dsrow = sdS + rr * 128 + hq * (BKV * 128);
+    uint8_t *dsrow0 = sdS + rr * 128 + hq * (BKV * 128);  // + (block & 1) * kPBytes
+    const uint32_t pt_addr = tmem + lane_addr + C_PT + hq * 32;  // this warpgroup's P^T columns
     int n = 0;
     int prev_qrow = 0, prev_h = 0;  // the block whose dQ is drained next
     for (int r = 0, it; (it = bwd_item(r, c, G)) < n_items; ++r) {
@@ -620,8 +629,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
         const float *Ls = sL + st * BQ;
         const float *Ds = sD + st * BQ;
         // this warpgroup's 64 queries in two 32-column chunks; the first chunk is
-        // computed before waiting for the previous block's gradient MMAs to
-        // release P^T / dS^T, so that wait overlaps it
+        // computed before waiting for dV(n - 1) to release P^T (TMEM) and dK / dQ
+        // (n - 2) the dS^T buffer, so those waits overlap it
+        uint8_t *dsrow = dsrow0 + (n & 1) * kPBytes;
 #pragma unroll
         for (int c0 = 0; c0 < 64; c0 += 32) {
           uint32_t sv[32], dp[32];
@@ -661,21 +671,25 @@ __global__ void __launch_bounds__(kThreads2, 1)
           if (diag) elementwise(std::true_type{});
           else elementwise(std::false_type{});
           if (c0 == 0) {
-            mbar_wait(p_empty, ph ^ 1);  // the previous block's MMAs have consumed P^T / dS^T
+            mbar_wait(&ds_empty[n & 1], ((n >> 1) & 1) ^ 1);  // dK / dQ(n - 2) have read this dS^T buffer
+            mbar_wait(pt_free, ph ^ 1);                       // dV(n - 1) has read P^T
+            tc_fence_after();
             if (wg == 0 && rr == 0) mark(4, n);
           }
+          tmem_st_32x32b_x16(pt_addr + (c0 >> 1), pk);  // queries c0..c0+31 -> 16 bf16-pair columns
 #pragma unroll
           for (int ch = 0; ch < 4; ++ch) {
             const uint32_t off = (((c0 >> 3) + ch) ^ (rr & 7)) << 4;
-            *reinterpret_cast<uint4 *>(prow + off) = make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
             *reinterpret_cast<uint4 *>(dsrow + off) = make_uint4(dk[4 * ch], dk[4 * ch + 1], dk[4 * ch + 2], dk[4 * ch + 3]);
           }
         }
+        tmem_st_wait();
         fence_async_smem();
+        tc_fence_before();
         mbar_arrive(p_full);
         if (rr == 0) mark(wg == 0 ? 5 : 7, n);
-        // the previous block's dQ is complete by now (its MMAs finished before P^T
-        // could be rewritten): drain it while this block's gradient MMAs run
+        // the previous block's dQ: drained while this block's gradient MMAs run
+        // (dQ(n) cannot start before this drain releases the TMEM columns)
         if (n > 0) dq_out(prev_qrow, prev_h, n - 1);
         if (wg == 0 && rr == 0) mark(6, n);
         prev_qrow = row0 + i * BQ;
