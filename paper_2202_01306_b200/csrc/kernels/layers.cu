@@ -857,266 +857,8 @@ static int ln_bwd_wide(const float *dy, const float *x, const float *mean, const
   return HM_OK;
 }
 
-// Row-batched variant (default for d <= 2048): the 256 threads of a block
-// own fixed float4 columns (thread t: columns t, t + 256, ...), so every row
-// is read with fully coalesced 16-B loads exactly once (dy, x, resid), the
-// per-row statistics c1 / c2 of RB rows at a time are combined with one
-// block reduction, and dgamma / dbeta accumulate in registers across all the
-// block's rows -- one global atomic per column per block instead of two
-// shared-memory atomics per element.
-template <int NV, int RB>
-__global__ void __launch_bounds__(256, 1)
-    ln_bwd_tile_kernel(const float *__restrict__ dy, const float *__restrict__ x, const float *__restrict__ mean,
-                       const float *__restrict__ rstd, const float *__restrict__ gam, const float *resid, float *out,
-                       __nv_bfloat16 *__restrict__ out_bf, float *__restrict__ dgam, float *__restrict__ dbet,
-                       int64_t rows, int d, int rows_per_block) {
-  pdl_wait();
-  __shared__ float red[2][8][2 * RB];
-  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-  const int n4 = d >> 2;
-  const float inv_d = 1.f / (float)d;
-  float4 gg[NV], ag[NV], ab[NV];
-#pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    const int c = t + 256 * k;
-    gg[k] = c < n4 ? reinterpret_cast<const float4 *>(gam)[c] : make_float4(0.f, 0.f, 0.f, 0.f);
-    ag[k] = ab[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  const int64_t r_begin = (int64_t)blockIdx.x * rows_per_block;
-  const int64_t r_end = min(rows, r_begin + rows_per_block);
-  int parity = 0;
-  for (int64_t r0 = r_begin; r0 < r_end; r0 += RB, parity ^= 1) {
-    float4 a[RB][NV], v[RB][NV];
-    float mu[RB], rs[RB], c1[RB], c2[RB];
-#pragma unroll
-    for (int j = 0; j < RB; ++j) {
-      const int64_t r = r0 + j;
-      const bool ok = r < r_end;
-      mu[j] = ok ? mean[r] : 0.f;
-      rs[j] = ok ? rstd[r] : 0.f;
-#pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        const int c = t + 256 * k;
-        const bool in = ok && c < n4;
-        a[j][k] = in ? reinterpret_cast<const float4 *>(dy + r * d)[c] : make_float4(0.f, 0.f, 0.f, 0.f);
-        v[j][k] = in ? reinterpret_cast<const float4 *>(x + r * d)[c] : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < RB; ++j) {
-      float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        const float4 A = a[j][k], V = v[j][k], G = gg[k];
-        const float e0 = A.x * G.x, e1 = A.y * G.y, e2 = A.z * G.z, e3 = A.w * G.w;
-        s1 += (e0 + e1) + (e2 + e3);
-        s2 += (e0 * (V.x - mu[j]) + e1 * (V.y - mu[j])) + (e2 * (V.z - mu[j]) + e3 * (V.w - mu[j]));
-      }
-      s1 = warp_sum(s1);
-      s2 = warp_sum(s2);
-      if (lane == 0) {
-        red[parity][warp][2 * j] = s1;
-        red[parity][warp][2 * j + 1] = s2 * rs[j];
-      }
-    }
-    __syncthreads();  // the other parity buffer is rewritten two batches later, past the next barrier
-#pragma unroll
-    for (int j = 0; j < RB; ++j) {
-      float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-      for (int w = 0; w < 8; ++w) {
-        s1 += red[parity][w][2 * j];
-        s2 += red[parity][w][2 * j + 1];
-      }
-      c1[j] = s1 * inv_d;
-      c2[j] = s2 * inv_d;
-    }
-#pragma unroll
-    for (int j = 0; j < RB; ++j) {
-      const int64_t r = r0 + j;
-      if (r >= r_end) break;
-#pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        const int c = t + 256 * k;
-        if (c >= n4) continue;
-        const float4 A = a[j][k], V = v[j][k], G = gg[k];
-        const float h0 = (V.x - mu[j]) * rs[j], h1 = (V.y - mu[j]) * rs[j], h2 = (V.z - mu[j]) * rs[j],
-                    h3 = (V.w - mu[j]) * rs[j];
-        float4 o;
-        o.x = rs[j] * (A.x * G.x - c1[j] - h0 * c2[j]);
-        o.y = rs[j] * (A.y * G.y - c1[j] - h1 * c2[j]);
-        o.z = rs[j] * (A.z * G.z - c1[j] - h2 * c2[j]);
-        o.w = rs[j] * (A.w * G.w - c1[j] - h3 * c2[j]);
-        if (resid) {
-          const float4 q = reinterpret_cast<const float4 *>(resid + r * d)[c];
-          o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
-        }
-        reinterpret_cast<float4 *>(out + r * d)[c] = o;
-        if (out_bf) {
-          __nv_bfloat162 p0 = __floats2bfloat162_rn(o.x, o.y), p1 = __floats2bfloat162_rn(o.z, o.w);
-          reinterpret_cast<uint2 *>(out_bf + r * d)[c] =
-              make_uint2(*reinterpret_cast<uint32_t *>(&p0), *reinterpret_cast<uint32_t *>(&p1));
-        }
-        ag[k].x += A.x * h0; ag[k].y += A.y * h1; ag[k].z += A.z * h2; ag[k].w += A.w * h3;
-        ab[k].x += A.x; ab[k].y += A.y; ab[k].z += A.z; ab[k].w += A.w;
-      }
-    }
-  }
-#pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    const int c = t + 256 * k;
-    if (c >= n4) continue;
-    atomicAdd(&dgam[4 * c], ag[k].x);
-    atomicAdd(&dgam[4 * c + 1], ag[k].y);
-    atomicAdd(&dgam[4 * c + 2], ag[k].z);
-    atomicAdd(&dgam[4 * c + 3], ag[k].w);
-    atomicAdd(&dbet[4 * c], ab[k].x);
-    atomicAdd(&dbet[4 * c + 1], ab[k].y);
-    atomicAdd(&dbet[4 * c + 2], ab[k].z);
-    atomicAdd(&dbet[4 * c + 3], ab[k].w);
-  }
-}
-
-template <int NV, int RB>
-static int ln_bwd_tile(const float *dy, const float *x, const float *mean, const float *rstd, const float *g,
-                       const float *resid, float *out, void *out_bf, float *dg, float *db, int64_t rows, int d,
-                       cudaStream_t s) {
-  int64_t blocks = (int64_t)sm_count() * 3;
-  int64_t rpb = (rows + blocks - 1) / blocks;
-  rpb = (rpb + RB - 1) / RB * RB;
-  if (rpb < RB) rpb = RB;
-  blocks = (rows + rpb - 1) / rpb;
-  HM_CUDA(launch_pdl(ln_bwd_tile_kernel<NV, RB>, dim3((unsigned)blocks), dim3(256), 0, s, dy, x, mean, rstd, g, resid,
-                     out, static_cast<__nv_bfloat16 *>(out_bf), dg, db, rows, d, (int)rpb));
-  count_launch();
-  return HM_OK;
-}
-
-// Same math, dgamma/dbeta accumulated in registers: a warp keeps the same
-// lane -> column mapping for every row it processes, so each lane sums its
-// NV4 float4 columns privately; warps then combine through shared memory
-// and one atomic per column per block.  Used for d <= 2048.
-template <int NV4>
-__global__ void __launch_bounds__(256) ln_bwd_reg_kernel(const float *__restrict__ dy, const float *__restrict__ x,
-                                                         const float *__restrict__ mean, const float *__restrict__ rstd,
-                                                         const float *__restrict__ gam, const float *resid, float *out,
-                                                         __nv_bfloat16 *__restrict__ out_bf, float *__restrict__ dgam,
-                                                         float *__restrict__ dbet, int64_t rows, int d, int rows_per_block) {
-  extern __shared__ float spart[];  // [nwarps][2][d]
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const int n4 = d / 4;
-  float4 ag[NV4], ab[NV4];
-#pragma unroll
-  for (int k = 0; k < NV4; ++k) ag[k] = ab[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-  const float4 *g4 = reinterpret_cast<const float4 *>(gam);
-  const int64_t r_begin = (int64_t)blockIdx.x * rows_per_block;
-  const int64_t r_end = min(rows, r_begin + rows_per_block);
-  for (int64_t r = r_begin + warp; r < r_end; r += nw) {
-    const float4 *dyr = reinterpret_cast<const float4 *>(dy + r * d);
-    const float4 *xr = reinterpret_cast<const float4 *>(x + r * d);
-    const float mu = mean[r], rs = rstd[r];
-    float c1 = 0.f, c2 = 0.f;
-#pragma unroll
-    for (int k = 0; k < NV4; ++k) {
-      const int i = lane + 32 * k;
-      if (i < n4) {
-        const float4 a = dyr[i], v = xr[i], gg = g4[i];
-        const float4 hh = make_float4((v.x - mu) * rs, (v.y - mu) * rs, (v.z - mu) * rs, (v.w - mu) * rs);
-        c1 += a.x * gg.x + a.y * gg.y + a.z * gg.z + a.w * gg.w;
-        c2 += a.x * gg.x * hh.x + a.y * gg.y * hh.y + a.z * gg.z * hh.z + a.w * gg.w * hh.w;
-        ag[k].x += a.x * hh.x; ag[k].y += a.y * hh.y; ag[k].z += a.z * hh.z; ag[k].w += a.w * hh.w;
-        ab[k].x += a.x; ab[k].y += a.y; ab[k].z += a.z; ab[k].w += a.w;
-      }
-    }
-    c1 = warp_sum(c1) / d;
-    c2 = warp_sum(c2) / d;
-    float4 *outr = reinterpret_cast<float4 *>(out + r * d);
-    const float4 *rr = resid ? reinterpret_cast<const float4 *>(resid + r * d) : nullptr;
-    uint2 *ob = out_bf ? reinterpret_cast<uint2 *>(out_bf + r * d) : nullptr;
-#pragma unroll
-    for (int k = 0; k < NV4; ++k) {
-      const int i = lane + 32 * k;
-      if (i < n4) {  // second pass re-reads the row (L1/L2 resident)
-        const float4 a = dyr[i], v = xr[i], gg = g4[i];
-        const float4 hh = make_float4((v.x - mu) * rs, (v.y - mu) * rs, (v.z - mu) * rs, (v.w - mu) * rs);
-        float4 o;
-        o.x = rs * (a.x * gg.x - c1 - hh.x * c2);
-        o.y = rs * (a.y * gg.y - c1 - hh.y * c2);
-        o.z = rs * (a.z * gg.z - c1 - hh.z * c2);
-        o.w = rs * (a.w * gg.w - c1 - hh.w * c2);
-        if (rr) {
-          const float4 q = rr[i];
-          o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
-        }
-        outr[i] = o;
-        if (ob) {
-          __nv_bfloat162 p0 = __floats2bfloat162_rn(o.x, o.y), p1 = __floats2bfloat162_rn(o.z, o.w);
-          ob[i] = make_uint2(*reinterpret_cast<uint32_t *>(&p0), *reinterpret_cast<uint32_t *>(&p1));
-        }
-      }
-    }
-  }
-  float4 *mine = reinterpret_cast<float4 *>(spart + (size_t)warp * 2 * d);
-#pragma unroll
-  for (int k = 0; k < NV4; ++k) {
-    const int i = lane + 32 * k;
-    if (i < n4) {
-      mine[i] = ag[k];
-      mine[n4 + i] = ab[k];
-    }
-  }
-  __syncthreads();
-  for (int c = threadIdx.x; c < d; c += blockDim.x) {
-    float sg = 0.f, sb = 0.f;
-    for (int w = 0; w < nw; ++w) {
-      sg += spart[(size_t)w * 2 * d + c];
-      sb += spart[(size_t)w * 2 * d + d + c];
-    }
-    atomicAdd(&dgam[c], sg);
-    atomicAdd(&dbet[c], sb);
-  }
-}
-
-template <int NV4>
-static int ln_bwd_reg(const float *dy, const float *x, const float *mean, const float *rstd, const float *g,
-                      const float *resid, float *out, void *out_bf, float *dg, float *db, int64_t rows, int d,
-                      cudaStream_t s) {
-  const int nw = 8;
-  const size_t smem = (size_t)nw * 2 * d * sizeof(float);
-  static bool attr = false;
-  if (!attr) {
-    HM_CUDA(cudaFuncSetAttribute(ln_bwd_reg_kernel<NV4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    attr = true;
-  }
-  int64_t blocks = sm_count() * 2;
-  int rpb = (int)((rows + blocks - 1) / blocks);
-  if (rpb < 8) rpb = 8;
-  blocks = (rows + rpb - 1) / rpb;
-  ln_bwd_reg_kernel<NV4><<<(unsigned)blocks, nw * 32, smem, s>>>(dy, x, mean, rstd, g, resid, out,
-                                                               static_cast<__nv_bfloat16 *>(out_bf), dg, db, rows, d, rpb);
-  count_launch();
-  HM_CUDA(cudaGetLastError());
-  return HM_OK;
-}
-
 int ln_bwd(const float *dy, const float *x, const float *mean, const float *rstd, const float *g, const float *resid,
            float *out, void *out_bf, float *dg, float *db, int64_t rows, int d, cudaStream_t s) {
-  // The register-accumulated variant (ln_bwd_reg_kernel) measured slower on
-  // B200 (70 us vs 38 us at 4096 x 1600: one 8-warp block per SM is too little
-  // memory parallelism); it stays behind HM_LN_BWD=reg for tuning.
-  static const bool use_reg = [] {
-    const char *e = getenv("HM_LN_BWD");
-    return e && e[0] == 'r';
-  }();
-  if (use_reg && d % 4 == 0 && d <= 2048) {
-    ProfScope ps(KC_LAYERNORM, s, 0, (resid ? 16.0 : 12.0) * rows * d + (out_bf ? 2.0 * rows * d : 0));
-    const int nv4 = (d / 4 + 31) / 32;
-    if (nv4 <= 2) return ln_bwd_reg<2>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
-    if (nv4 <= 4) return ln_bwd_reg<4>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
-    if (nv4 <= 8) return ln_bwd_reg<8>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
-    if (nv4 <= 13) return ln_bwd_reg<13>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
-    return ln_bwd_reg<16>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
-  }
   if (d % 4) return fail(HM_ERR_VALIDATION, "layernorm: d must be a multiple of 4");
   static const bool use_smem_atomic = [] {
     const char *e = getenv("HM_LN_BWD");
@@ -1126,10 +868,11 @@ int ln_bwd(const float *dy, const float *x, const float *mean, const float *rstd
     const char *e = getenv("HM_LN_BWD");
     return e && e[0] == 'w';
   }();
-  // rows in registers up to d = 1024 (4096 x 1024: 17.9 vs 22.0 us for the
-  // shared-atomic kernel; 8192 x 1024: 28.3 vs 40.8 us); wider rows spill the
-  // register budget, so the two-pass kernel (dy / x re-read from L2) takes them
-  // (4096 x 1600: 31.8 vs 34.0 us registers, 35.1 us atomics) -- profiles/r01_ln_perf_v2.jsonl
+  // Rows in registers: one warp per row up to d = 1024 (4096 x 1024: 17.9 vs 22.0
+  // us for the shared-atomic kernel), 2 / 8 warps per row up to d = 8192 (4096 x
+  // 1600: 26.0 vs 31.9 us for the two-pass kernel; 4096 x 8192: 98 vs 183 us,
+  // profiles/r02_ln_perf*.jsonl).  HM_LN_BWD=w forces the two-pass kernel (dy / x
+  // re-read from L2), a the shared-atomic one (also the fallback above d = 8192).
   if (!use_smem_atomic && !use_two_pass && d <= 1024) {
     ProfScope ps(KC_LAYERNORM, s, 0, (resid ? 16.0 : 12.0) * rows * d + (out_bf ? 2.0 * rows * d : 0));
     const int nv4 = (d / 4 + 31) / 32;
@@ -1172,21 +915,6 @@ int ln_bwd(const float *dy, const float *x, const float *mean, const float *rstd
                        rstd, g, resid, out, static_cast<__nv_bfloat16 *>(out_bf), dg, db, rows, d, rpb));
     count_launch();
     return HM_OK;
-  }
-  // HM_LN_BWD=t: row-batched tiles with register-accumulated dgamma/dbeta.
-  // Graph-timed on cold inputs it was no faster than the shared-atomic kernel
-  // (34.3 vs 35.1 us at 4096 x 1600, 25.7 vs 22.0 us at 4096 x 1024; both
-  // about 3.4 TB/s), so it stays opt-in (profiles/r01_ln_perf.jsonl).
-  static const bool use_tile = [] {
-    const char *e = getenv("HM_LN_BWD");
-    return e && e[0] == 't';
-  }();
-  if (use_tile && d <= 4096) {
-    ProfScope ps(KC_LAYERNORM, s, 0, (resid ? 16.0 : 12.0) * rows * d + (out_bf ? 2.0 * rows * d : 0));
-    const int n4 = d / 4;
-    if (n4 <= 256) return ln_bwd_tile<1, 4>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
-    if (n4 <= 512) return ln_bwd_tile<2, 4>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
-    return ln_bwd_tile<4, 2>(dy, x, mean, rstd, g, resid, out, out_bf, dg, db, rows, d, s);
   }
   const size_t smem = 2 * (size_t)d * sizeof(float);
   static bool attr = false;
