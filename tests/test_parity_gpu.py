@@ -16,8 +16,8 @@ Two arithmetic modes:
 
 Configs: c1 (tiny GPT-2, 10 steps), the benchmarked c3 shape (GPT-2 XL
 layers: d=1600, 25 heads, seq 1024, V=50257) at 4 layers, D=4, PP and DP,
-3 steps, c2 at its benched grouping (BERT-Large layers, D=64 as u=16
-microbatches, 6 layers, 2 steps) and the c4 layer shape (d=8192, head_dim
+3 steps, c2 exactly as benched (BERT-Large, 24 layers, D=64 as u=16
+microbatches, packs of 6, 2 steps) and the c4 layer shape (d=8192, head_dim
 128).  The schedule ledger equals simulate's at every step."""
 
 import numpy as np
@@ -137,13 +137,15 @@ def test_c3_gpt2xl_shape_per_layer_deltas(mode, math):
 
 @pytest.mark.parametrize("math", ["fp32", "bf16"])
 def test_c2_bert_large_benched_grouping(math):
-    """Config c2 at the benched grouping (bench.py bert-large-pp: D = 64 in
-    microbatches of u = 16, full attention at seq 512, vocab 30522): BERT-Large
-    layers at 6 layers in two packs of 3, 2 steps."""
-    spec = GPTSpec(6, 1024, 16, 512, 30522, False, "bert-large-6l")
-    packs = ((0, 2), (3, 5))
+    """Config c2 exactly as benched (bench.py bert-large-pp): BERT-Large at full
+    depth (24 layers, d = 1024, 16 heads, seq 512, vocab 30522, full attention),
+    D = 64 in microbatches of u = 16, packs of 6 layers, 2 steps.  Measured:
+    fp32 mode loss 6e-8, per-layer dW <= 5.3e-4; bf16 mode loss 5e-6, dW <= 7.9e-2
+    (profiles/r02_parity_c2_full_depth.log)."""
+    spec = GPT_PRESETS["bert-large"]
+    packs = tuple((i, i + 5) for i in range(0, 24, 6))
     cfg = H.Configuration(16, packs, 16, packs, 64, H.Mode.PP)
-    check(run_parity(spec, cfg, 2, math, alpha=40 << 30), FP32_TOL if math == "fp32" else BF16_TOL)
+    check(run_parity(spec, cfg, 2, math, alpha=60 << 30), FP32_TOL if math == "fp32" else BF16_TOL)
 
 
 @pytest.mark.parametrize("math", ["fp32", "bf16"])
