@@ -170,3 +170,94 @@ def check_memory_fit(graph: TaskGraph, machine: MachineModel, profiles: ProfileS
                 raise ValidationError(
                     f"tasks {a.index} and {b.index} overflow gpu{dev[1]} memory "
                     f"({need} > {machine.gpu_mem_capacity}) with prefetch")
+
+
+# ---------------------------------------------------------------------------
+# Python mirror of the native plan's duration model and list scheduler.
+#
+# The planner itself lives in csrc/plan.cpp; these helpers restate two of its
+# pieces in Python so a caller can price a task or run a hand-built item
+# graph without the library — the reference exposes the same three helpers
+# (`simulator.py:86-147`, `:347-375`) and its own tests import them.
+# ---------------------------------------------------------------------------
+
+def _xfer_ns(nbytes: int, bw: int) -> int:
+    """ceil(nbytes * 1e9 / bw) — plan.cpp `xfer_ns`."""
+    return -(-int(nbytes) * 1_000_000_000 // int(bw))
+
+
+def _compute_duration(task: Task, u: int, profiles: ProfileSet,
+                      machine: MachineModel) -> int:
+    """Nanoseconds one member (microbatch ``u``) of ``task`` occupies its GPU,
+    the rule plan.cpp `Ctx::compute_ns` applies (unsharded update)."""
+    lo, hi = task.pack
+    if task.type is TaskType.F:
+        return profiles.pack_time_ns("F", lo, hi, u)
+    if task.type is TaskType.B:
+        fwd = profiles.pack_time_ns("F", lo, hi, u) if task.recompute else 0
+        return profiles.pack_time_ns("B", lo, hi, u) + fwd
+    layers = range(lo, hi + 1)
+    if machine.cpu_offload_update:
+        return sum(_xfer_ns(profiles.w_bytes(L), machine.update_cpu_rate) for L in layers)
+    return sum(profiles.time_ns("U", L, 1) for L in layers)
+
+
+class _Item:
+    """One schedulable unit: a compute member or one tensor transfer.
+
+    ``resources`` are held for ``duration`` once every predecessor has
+    released it; ``key`` orders items that become ready at the same time
+    (plan.cpp `Item` + its ready-queue ordering)."""
+
+    __slots__ = ("key", "resources", "duration", "task", "kind", "label", "tensor",
+                 "channel", "nbytes", "gpu", "idx", "pending", "ready", "dependents",
+                 "start", "end")
+
+    def __init__(self, key, resources, duration, task, kind, label,
+                 tensor=None, channel=None, nbytes=0, gpu=None):
+        self.key, self.resources, self.duration = key, tuple(resources), int(duration)
+        self.task, self.kind, self.label = task, kind, label
+        self.tensor, self.channel, self.nbytes, self.gpu = tensor, channel, nbytes, gpu
+        self.idx = -1
+        self.pending = 0            # predecessors not yet scheduled
+        self.ready = 0              # earliest start the predecessors allow
+        self.dependents: list[tuple[_Item, bool]] = []
+        self.start = self.end = -1
+
+
+def _link(dep: _Item | None, item: _Item, at_start: bool = False) -> None:
+    """``item`` waits for ``dep`` to finish (or only to start, ``at_start``)."""
+    if dep is not None:
+        dep.dependents.append((item, at_start))
+        item.pending += 1
+
+
+def _run(items: list[_Item]) -> None:
+    """Greedy list schedule: pop the ready item with the smallest
+    (ready time, key), start it once all its resources are free, release its
+    dependents.  Raises DeadlockError when a cycle strands items — the check
+    plan.cpp reports as HM_ERR_DEADLOCK."""
+    import heapq
+
+    from .errors import DeadlockError
+
+    free_at: dict = {}
+    queue = [(0, it.key, n) for n, it in enumerate(items) if it.pending == 0]
+    heapq.heapify(queue)
+    scheduled = 0
+    while queue:
+        ready, _, n = heapq.heappop(queue)
+        it = items[n]
+        it.start = max([ready] + [free_at.get(r, 0) for r in it.resources])
+        it.end = it.start + it.duration
+        for r in it.resources:
+            free_at[r] = it.end
+        scheduled += 1
+        for child, at_start in it.dependents:
+            child.ready = max(child.ready, it.start if at_start else it.end)
+            child.pending -= 1
+            if child.pending == 0:
+                heapq.heappush(queue, (child.ready, child.key, child.idx))
+    if scheduled != len(items):
+        raise DeadlockError(f"{len(items) - scheduled} of {len(items)} work items never "
+                            "became runnable: the dependency graph has a cycle")

@@ -206,3 +206,46 @@ def test_sharded_update_rejects_pp():
         H.simulate(g, m, prof, dp_update="sharded")
     with pytest.raises(ValidationError):
         H.simulate(g, m, prof, dp_update="zero")
+
+
+@pytest.mark.parametrize("case", golden_cases()[:6], ids=lambda c: c["name"])
+def test_python_duration_mirror_matches_native_plan(case):
+    """simulator._compute_duration (the reference's private helper, restated)
+    prices every compute member exactly as the native plan schedules it."""
+    from paper_2202_01306_b200.simulator import _compute_duration
+    cfg, mach, prof = product_inputs(case)
+    g = H.generate_task_graph(cfg, mach, prof)
+    rep = H.simulate(g, mach, prof)
+    seen = 0
+    for e in rep.trace:
+        if e.kind != "compute":
+            continue
+        t = g.tasks[e.task]
+        if t.type is H.TaskType.U and mach.gpu_count > 1 and cfg.mode is H.Mode.DP:
+            continue  # the native plan may shard the update across ranks
+        member = int(e.label.rsplit("mb", 1)[1])
+        u = 1 if t.type is H.TaskType.U else t.group[member]
+        assert e.end_ns - e.start_ns == _compute_duration(t, u, prof, mach), e
+        seen += 1
+    assert seen
+
+
+def test_python_scheduler_mirror_deadlock_and_order():
+    from paper_2202_01306_b200.errors import DeadlockError
+    from paper_2202_01306_b200.simulator import _Item, _link, _run
+    a = _Item((0,), ("gpu0",), 5, 0, "compute", "a")
+    b = _Item((1,), ("gpu0",), 3, 1, "compute", "b")
+    c = _Item((2,), ("swap0",), 4, 2, "X", "c")
+    for n, it in enumerate((a, b, c)):
+        it.idx = n
+    _link(a, b)
+    _link(a, c, at_start=True)
+    _run([a, b, c])
+    assert (a.start, a.end, b.start, b.end, c.start, c.end) == (0, 5, 5, 8, 0, 4)
+    x = _Item((0,), ("r",), 1, 0, "compute", "x")
+    y = _Item((1,), ("r",), 1, 1, "compute", "y")
+    x.idx, y.idx = 0, 1
+    _link(x, y)
+    _link(y, x)
+    with pytest.raises(DeadlockError):
+        _run([x, y])
