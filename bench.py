@@ -667,6 +667,23 @@ def run_native(args) -> None:
     busbw = _nccl_busbw(world)
     t_nccl = cnt["nccl_bytes"] / (busbw * 1e9) if world > 1 and busbw else 0.0
     p2p = sum(r[6] for r in sim.ledger if r[4] == "peer2peer")
+    # phase-serialised link bound: the forward packs' transfers (W in, stash
+    # out) and the backward + update packs' (W / stash / K in, W / K out) run
+    # in two windows -- the next iteration's forward waits on this one's
+    # updates -- so each window is bounded by its own direction mix
+    t_phase = 0.0
+    for is_f in (True, False):
+        ph_in = ph_out = 0
+        for r in sim.ledger:
+            if r[4] in ("cpu_gpu_swap", "message_passing") and r[7] == rank and \
+                    (graph.tasks[r[0]].type is H.TaskType.F) == is_f:
+                if r[1] == 0:
+                    ph_in += r[6]
+                elif r[1] == 2:
+                    ph_out += r[6]
+        t_phase += max(ph_in / (pcie["h2d"] * 1e9), ph_out / (pcie["d2h"] * 1e9),
+                       (ph_in + ph_out) / (pcie["bidir"] * 1e9))
+    t_phase = _max_over_ranks(t_phase, world)
     t_roof = max(t_compute, _max_over_ranks(max(t_h2d, t_d2h, t_bidir), world), t_root, t_nccl)
     ms_step = 1000.0 * t_total / args.steps
     clk = clocks.summary()
@@ -700,6 +717,11 @@ def run_native(args) -> None:
                           "t_compute_ms": round(1000 * t_compute, 2), "t_h2d_ms": round(1000 * t_h2d, 2),
                           "t_d2h_ms": round(1000 * t_d2h, 2), "t_bidir_ms": round(1000 * t_bidir, 2),
                           "frac": round(1000 * t_roof / ms_step, 4),
+                          "t_phase_ms": round(1000 * t_phase, 2),
+                          "frac_phase": round(1000 * max(t_phase, t_compute) / ms_step, 4),
+                          "phase_how": "sum over the forward and the backward + update windows of each window's "
+                                       "own max(H2D / h2d, D2H / d2h, (H2D + D2H) / bidir) from the ledger "
+                                       "(explanatory; frac above is the whole-step bound)",
                           "pcie_gbs": {k: round(v, 2) for k, v in pcie.items()},
                           "tensor_peak_tflops": pk["bf16"], "peak": pk["kind"]},
         "roofline": {"bound": "tensor", "achieved": round(roof_tflops, 1), "peak": pk["bf16"],

@@ -37,7 +37,11 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #include "../runtime/common.hpp"
 #include "sm100.cuh"
@@ -160,8 +164,13 @@ __device__ __forceinline__ Item make_item(int r, int c, int G, int S, int H, int
 template <bool CAUSAL>
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16 *__restrict__ out, float *__restrict__ lse,
-               int S, int H, int BH, float scale_log2) {
+               int S, int H, int BH, float scale_log2, unsigned long long *trace) {
   extern __shared__ uint8_t smem_raw[];
+  // diagnostics (HM_ATTN_TRACE=1): globaltimer per CTA -- [0] entry, [1] setup
+  // done, [4 + 4 k + 2 t] tile t's first S of item k, [+1] its epilogue done,
+  // [62] exit, [2] / [61] clock64 at setup / exit
+  unsigned long long *tr = trace ? trace + 64 * blockIdx.x : nullptr;
+  if (tr && threadIdx.x == 0) tr[0] = globaltimer();
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *sQ = smem;                  // [2 items][2 tiles]
   uint8_t *sK = sQ + 4 * kTile;        // [kStages]
@@ -204,6 +213,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (tr && threadIdx.x == 0) {
+    tr[1] = globaltimer();
+    tr[2] = clock64();
+  }
 
   if (warp < 4) {
     reg_dealloc<72>();  // 3 x 168 per SMSP at launch = 72 + 2 x 216
@@ -283,6 +296,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t o_addr = tmem + lane_addr + C_O + t * DH;
     const float2 sc2 = make_float2(scale_log2, scale_log2);
     int done = 0;  // items this tile has finished (o_done parity)
+    const bool rec = tr && q4 == 0 && lane == 0;
     for (Item it = make_item<CAUSAL>(0, c, G, S, H, BH, 0, 0, 0, 0); it.valid; it = next_item(it)) {
       const int nkv = t == 0 ? it.nkv0 : it.nkv1;
       if (nkv == 0) continue;
@@ -295,6 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t s_addr = tmem + lane_addr + buf * BKV;
         mbar_wait(&s_full[buf], (n / kSBuf) & 1);
         tc_fence_after();
+        if (rec && j == 0 && it.r < 14) tr[4 + 4 * it.r + 2 * t] = globaltimer();
         uint32_t v[BKV];
 #pragma unroll
         for (int q = 0; q < BKV / 32; ++q)
@@ -383,11 +398,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       lse[(int64_t)(row0 + qb * BQ + r) * H + it.h] = m + log2f(l);
+      if (rec && it.r < 14) tr[5 + 4 * it.r + 2 * t] = globaltimer();
       tc_fence_before();
     }
   }
   tc_fence_before();
   __syncthreads();
+  if (tr && threadIdx.x == 0) {
+    tr[61] = clock64();
+    tr[62] = globaltimer();
+  }
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
@@ -440,8 +460,29 @@ int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causa
   const int npair = (S / BQ + 1) / 2;
   const int sms = current_sm_count();
   const int items = npair * B * H;
-  k<<<dim3(items < sms ? items : sms), kThreads, kSmem, s>>>(tm, static_cast<__nv_bfloat16 *>(o), lse, S, H, B * H,
-                                                             scale_log2);
+  const int grid = items < sms ? items : sms;
+  static const bool tracing = getenv("HM_ATTN_TRACE") && getenv("HM_ATTN_TRACE")[0] == '1';
+  static unsigned long long *tbuf = nullptr;
+  if (tracing && !tbuf) HM_CUDA(cudaMalloc(&tbuf, 64 * 1024 * sizeof(unsigned long long)));
+  if (tracing) HM_CUDA(cudaMemsetAsync(tbuf, 0, 64 * grid * sizeof(unsigned long long), s));
+  k<<<dim3(grid), kThreads, kSmem, s>>>(tm, static_cast<__nv_bfloat16 *>(o), lse, S, H, B * H, scale_log2,
+                                        tracing ? tbuf : nullptr);
+  if (tracing) {  // one JSON line per launch: every CTA's timestamps, ns after the earliest entry
+    std::vector<unsigned long long> h(64 * grid);
+    HM_CUDA(cudaStreamSynchronize(s));
+    HM_CUDA(cudaMemcpy(h.data(), tbuf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    unsigned long long t0 = ~0ULL;
+    for (int c = 0; c < grid; ++c) t0 = std::min(t0, h[64 * c]);
+    fprintf(stderr, "{\"attn_fwd64_trace\": {\"B\": %d, \"S\": %d, \"H\": %d, \"cta\": [", B, S, H);
+    for (int c = 0; c < grid; ++c) {
+      fprintf(stderr, "%s[", c ? ", " : "");
+      for (int n = 0; n < 64; ++n)
+        fprintf(stderr, "%s%lld", n ? ", " : "",
+                n == 2 || n == 61 ? (long long)h[64 * c + n] : h[64 * c + n] ? (long long)(h[64 * c + n] - t0) : -1LL);
+      fprintf(stderr, "]");
+    }
+    fprintf(stderr, "]}}\n");
+  }
   count_launch();
   HM_CUDA(cudaGetLastError());
   return HM_OK;
