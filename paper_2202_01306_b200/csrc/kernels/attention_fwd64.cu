@@ -9,7 +9,7 @@
 // double-buffered, and its first S MMAs are issued while the current item's
 // last tiles are still in the softmax (16 x 1024 x 25 heads: 114.6 vs 138.6 us
 // for one CTA per pair).
-//   warp 0      TMA: Q pairs, then K_j / V_j into a 3-stage ring
+//   warp 0      TMA: Q pairs, then K_j / V_j into a 4-stage ring
 //   warp 1      MMA issuer
 //   warps 4-7   softmax of tile 0, warps 8-11 of tile 1 (one thread per
 //               query row = TMEM lane)
@@ -32,6 +32,19 @@
 // operand straight from TMEM.  O stays in TMEM; it is rescaled in place only
 // when a row max grows by more than 2^8 (lazy rescale, exact in O / l).
 //
+// Measured balance (HM_ATTN_TRACE clock64 trace, tools/probes/attn_mma_probe):
+// a position (one tile's 128 x 128 block) costs ~1300 cycles on BOTH sides.
+// The MMA thread: PV (8 x 128x64x16 from TMEM) 366 + S (4 x 128x128x16) 256
+// cycles of tensor time, but tcgen05.mma issue blocks at the execution rate
+// (no queue to hide the thread's own work), a try_wait on an already
+// completed mbarrier costs ~150 cycles and a commit ~45, so every wait, commit
+// and counter update is tensor-pipe idle time.  The softmax: 128 ex2 + 64
+// bf16x2 conversions per row on the MUFU/XU pipe, ~1280 cycles per position
+// with both tiles' warps sharing each SMSP.  Hence: one K-block wait per step,
+// no per-PV commit (a rescale waits on the S issued after the previous PV),
+// descriptors as precomputed 32-bit words, ring / buffer counters without
+// divisions.
+//
 // Output conventions as attention.cu: o [tokens, d] bf16, lse [tokens, H]
 // in the log2 domain.
 #include <cuda.h>
@@ -52,7 +65,7 @@ namespace attn_fwd64 {
 using namespace sm100;
 
 constexpr int DH = 64, BQ = 128, BKV = 128;
-constexpr int kStages = 3;               // K / V ring
+constexpr int kStages = 4;               // K / V ring (a power of two)
 constexpr int kSBuf = 3;                 // rotating S / P buffers in TMEM
 constexpr uint32_t kTile = BQ * DH * 2;  // 128 rows x 128 B: one SW128 atom column, 16 KB
 constexpr int kThreads = 384;
@@ -166,10 +179,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     fwd_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16 *__restrict__ out, float *__restrict__ lse,
                int S, int H, int BH, float scale_log2, unsigned long long *trace) {
   extern __shared__ uint8_t smem_raw[];
-  // diagnostics (HM_ATTN_TRACE=1): globaltimer per CTA -- [0] entry, [1] setup
-  // done, [4 + 4 k + 2 t] tile t's first S of item k, [+1] its epilogue done,
-  // [62] exit, [2] / [61] clock64 at setup / exit
-  unsigned long long *tr = trace ? trace + 64 * blockIdx.x : nullptr;
+  // diagnostics (HM_ATTN_TRACE=1), 512 words per CTA: globaltimer at [0] entry,
+  // [1] setup done, [62] exit; clock64 at [2] setup, [61] exit, [4 + 4 k + 2 t]
+  // tile t's first S of item k, [+1] its epilogue done, [64 + 96 t + 2 k] tile
+  // t's k-th S ready, [+1] its P handed over, and for the MMA thread at
+  // position n < 60: [256 + 4 n] P(n) ready, [+1] PV(n) issued, [+2] K block
+  // of S(n + 3) ready, [+3] S(n + 3) issued
+  unsigned long long *tr = trace ? trace + 512 * blockIdx.x : nullptr;
   if (tr && threadIdx.x == 0) tr[0] = globaltimer();
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *sQ = smem;                  // [2 items][2 tiles]
@@ -180,8 +196,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t *kv_full = bar + 4, *kv_empty = kv_full + kStages;  // [stage]
   uint64_t *s_full = kv_empty + kStages;                       // [S buffer]
   uint64_t *p_full = s_full + kSBuf;                           // [tile][step parity]
-  uint64_t *o_full = p_full + 4;                               // [tile]: every PV_t
-  uint64_t *o_done = o_full + 2;                               // [tile]: the item's last PV_t
+  uint64_t *o_done = p_full + 4;                               // [tile]: the item's last PV_t
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(o_done + 2);
 
   const int G = gridDim.x, c = blockIdx.x;
@@ -197,7 +212,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
-      mbar_init(&o_full[i], 1);
       mbar_init(&o_done[i], 1);
     }
     for (int i = 0; i < kStages; ++i) {
@@ -230,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tma_load_2d(sQ + (2 * qp + 1) * kTile, &tm, &q_full[qp], it.h * DH, row0 + (2 * it.pr + 1) * BQ);
         const int nall = it.nkv0 > it.nkv1 ? it.nkv0 : it.nkv1;
         for (int j = 0; j < nall; ++j) {
-          const int kb = it.kvb + j, st = kb % kStages;
+          const int kb = it.kvb + j, st = kb & (kStages - 1);
           mbar_wait(&kv_empty[st], ((kb / kStages) & 1) ^ 1);
           mbar_expect_tx(&kv_full[st], 2 * kTile);
           tma_load_2d(sK + st * kTile, &tm, &kv_full[st], d + it.h * DH, row0 + j * BKV);
@@ -240,50 +254,78 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1 && lane == 0) {
       constexpr uint32_t idesc_s = idesc_bf16_f32(BQ, BKV, 0, 0);  // Q K-major, K K-major
       constexpr uint32_t idesc_o = idesc_bf16_f32(BQ, DH, 0, 1);   // P (TMEM), V MN-major
+      // descriptor low words of buffer 0 (a buffer adds kTile >> 4, a K step of
+      // Q / K 32 B >> 4 = 2, of V 2048 B >> 4 = 128); all share one high word
+      const uint32_t d_hi = (uint32_t)(umma_desc_sw128(0, 0, 1024) >> 32);
+      const uint32_t q_lo0 = (uint32_t)umma_desc_sw128(smem_u32(sQ), 16, 1024);
+      const uint32_t k_lo0 = (uint32_t)umma_desc_sw128(smem_u32(sK), 16, 1024);
+      const uint32_t v_lo0 = (uint32_t)umma_desc_sw128(smem_u32(sV), kTile, 1024);
+      // The single issuing thread is the pipe's feeder: a position's 12 MMAs
+      // take ~600 cycles of tensor time, so its bookkeeping is kept to running
+      // counters (S buffer, tile steps) and power-of-two ring arithmetic.
       // S cursor: runs up to kSBuf positions ahead of the PVs, across items
       Item sit = make_item<CAUSAL>(0, c, G, S, H, BH, 0, 0, 0, 0);
-      int s_loc = 0;
+      int s_loc = 0, s_buf = 0, kv_ready = -1;
+      unsigned long long t_kv = 0;
       auto issue_next_s = [&]() {
-        while (sit.valid && s_loc >= sit.npos) {
-          sit = next_item(sit);
+        if (s_loc >= sit.npos) {
+          do {
+            sit = next_item(sit);
+          } while (sit.valid && sit.npos == 0);
           s_loc = 0;
         }
-        if (!sit.valid) return;
+        if (!sit.valid) {  // past the last item: keep s_full's phases in step with positions
+          mma_commit(&s_full[s_buf]);
+          s_buf = s_buf == kSBuf - 1 ? 0 : s_buf + 1;
+          return;
+        }
         const int qp = sit.r & 1;
         if (s_loc == 0) mbar_wait(&q_full[qp], (sit.r >> 1) & 1);
         int t, j;
         sit.at(s_loc, t, j);
-        const int kb = sit.kvb + j, st = kb % kStages, P = sit.pb + s_loc;
-        mbar_wait(&kv_full[st], (kb / kStages) & 1);
-        tc_fence_after();
-        const uint32_t q_base = smem_u32(sQ + (2 * qp + t) * kTile), k_base = smem_u32(sK + st * kTile);
+        const int kb = sit.kvb + j;
+        if (kb > kv_ready) {  // both tiles' S of a step read the same K block: one wait
+          mbar_wait(&kv_full[kb & (kStages - 1)], (kb / kStages) & 1);
+          tc_fence_after();
+          kv_ready = kb;
+        }
+        if (tr) t_kv = clock64();
+        const uint32_t q_lo = q_lo0 + (uint32_t)(2 * qp + t) * (kTile >> 4);
+        const uint32_t k_lo = k_lo0 + (uint32_t)(kb & (kStages - 1)) * (kTile >> 4);
+        const uint32_t d_s = tmem + s_buf * BKV;
+        mma_bf16_lohi(d_s, q_lo, k_lo, d_hi, idesc_s, 0u);
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk)
-          mma_bf16(tmem + (P % kSBuf) * BKV, umma_desc_sw128(q_base + kk * 32, 16, 1024),
-                   umma_desc_sw128(k_base + kk * 32, 16, 1024), idesc_s, kk > 0);
-        mma_commit(&s_full[P % kSBuf]);
+        for (int kk = 1; kk < DH / 16; ++kk) mma_bf16_lohi(d_s, q_lo + 2 * kk, k_lo + 2 * kk, d_hi, idesc_s, 1u);
+        mma_commit(&s_full[s_buf]);
         if (s_loc == sit.npos - 1) mma_commit(&q_empty[qp]);  // the item's last Q K^T: its Q pair is free
+        s_buf = s_buf == kSBuf - 1 ? 0 : s_buf + 1;
         ++s_loc;
       };
       for (int k = 0; k < kSBuf; ++k) issue_next_s();
+      int pv_buf = 0, gc0 = 0, gc1 = 0;  // PV position % kSBuf; steps of tile 0 / 1 so far
       for (Item it = make_item<CAUSAL>(0, c, G, S, H, BH, 0, 0, 0, 0); it.valid; it = next_item(it)) {
         for (int n = 0; n < it.npos; ++n) {
           int t, j;
           it.at(n, t, j);
-          const int gs = (t == 0 ? it.g0 : it.g1) + j, P = it.pb + n, kb = it.kvb + j;
-          mbar_wait(&p_full[2 * t + (gs & 1)], (gs >> 1) & 1);  // P_t(j) in S buffer P % 3 (and O_t rescaled)
+          const int gs = t ? gc1++ : gc0++, kb = it.kvb + j, P = it.pb + n;
+          mbar_wait(&p_full[2 * t + (gs & 1)], (gs >> 1) & 1);  // P_t(j) in S buffer pv_buf (and O_t rescaled)
           tc_fence_after();
-          const uint32_t v_base = smem_u32(sV + (kb % kStages) * kTile);
-          const uint32_t p_tm = tmem + (P % kSBuf) * BKV;
+          if (tr && P < 60) tr[256 + 4 * P] = clock64();
+          const uint32_t v_lo = v_lo0 + (uint32_t)(kb & (kStages - 1)) * (kTile >> 4);
+          const uint32_t p_tm = tmem + pv_buf * BKV, d_o = tmem + C_O + t * DH;
+          mma_bf16_ts_lohi(d_o, p_tm, v_lo, d_hi, idesc_o, j > 0 ? 1u : 0u);
 #pragma unroll
-          for (int kk = 0; kk < BKV / 16; ++kk)
-            mma_bf16_ts(tmem + C_O + t * DH, p_tm + kk * 8, umma_desc_sw128(v_base + kk * 2048, kTile, 1024), idesc_o,
-                        (j > 0 || kk > 0) ? 1u : 0u);
-          mma_commit(&o_full[t]);
+          for (int kk = 1; kk < BKV / 16; ++kk) mma_bf16_ts_lohi(d_o, p_tm + kk * 8, v_lo + kk * 128, d_hi, idesc_o, 1u);
+          if (tr && P < 60) tr[257 + 4 * P] = clock64();
           if (j == (t == 0 ? it.nkv0 : it.nkv1) - 1) mma_commit(&o_done[t]);  // O_t of this item final
-          if (t == 1 || j >= it.mn) mma_commit(&kv_empty[kb % kStages]);  // last use of K_j / V_j
+          if (t == 1 || j >= it.mn) mma_commit(&kv_empty[kb & (kStages - 1)]);  // last use of K_j / V_j
+          pv_buf = pv_buf == kSBuf - 1 ? 0 : pv_buf + 1;
           // S(P + 3) overwrites P(P) in TMEM: issued after PV(P), which reads it first
           issue_next_s();
+          if (tr && P < 60) {
+            tr[258 + 4 * P] = t_kv;
+            tr[259 + 4 * P] = clock64();
+          }
         }
       }
     }
@@ -297,6 +339,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float2 sc2 = make_float2(scale_log2, scale_log2);
     int done = 0;  // items this tile has finished (o_done parity)
     const bool rec = tr && q4 == 0 && lane == 0;
+    int ks = 0;  // trace: steps this tile has run
     for (Item it = make_item<CAUSAL>(0, c, G, S, H, BH, 0, 0, 0, 0); it.valid; it = next_item(it)) {
       const int nkv = t == 0 ? it.nkv0 : it.nkv1;
       if (nkv == 0) continue;
@@ -309,7 +352,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t s_addr = tmem + lane_addr + buf * BKV;
         mbar_wait(&s_full[buf], (n / kSBuf) & 1);
         tc_fence_after();
-        if (rec && j == 0 && it.r < 14) tr[4 + 4 * it.r + 2 * t] = globaltimer();
+        if (rec && j == 0 && it.r < 14) tr[4 + 4 * it.r + 2 * t] = clock64();
+        if (rec && ks < 48) tr[64 + 96 * t + 2 * ks] = clock64();
         uint32_t v[BKV];
 #pragma unroll
         for (int q = 0; q < BKV / 32; ++q)
@@ -336,8 +380,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           m = m_row;
         }
         if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {  // warp-uniform: tcgen05.ld / st are .sync.aligned
-          // PV_t(gs - 2) is complete (S of this step was issued after it); wait for PV_t(gs - 1)
-          mbar_wait(&o_full[t], (gs - 1) & 1);
+          // wait for PV_t(j - 1): the MMA thread issues S(p + 3) right after
+          // PV(p), so S(prev + 3)'s completion covers it.  Its buffer cannot
+          // have cycled again: the next S into it follows PV(n + 1), which
+          // follows this thread's P(n).
+          const int jp = j - 1;
+          const int need = it.pb + (jp < it.mn ? 2 * jp + t : 2 * it.mn + (jp - it.mn)) + kSBuf;
+          mbar_wait(&s_full[need % kSBuf], (need / kSBuf) & 1);
           tc_fence_after();
           const float2 a2 = make_float2(alpha, alpha);
 #pragma unroll
@@ -373,10 +422,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         l = l * alpha + ((rs[0].x + rs[0].y) + (rs[1].x + rs[1].y));
         tc_fence_before();
         mbar_arrive(&p_full[2 * t + (gs & 1)]);
+        if (rec && ks < 48) tr[65 + 96 * t + 2 * ks] = clock64();
+        ++ks;
       }
-      // epilogue: O / l and lse once the item's last PV_t has completed (a
-      // dedicated barrier: o_full's parity can lag by two phases here); the next
-      // item's first PV_t overwrites O only after this thread's next P
+      // epilogue: O / l and lse once the item's last PV_t has completed; the
+      // next item's first PV_t overwrites O only after this thread's next P
       mbar_wait(&o_done[t], done & 1);
       ++done;
       tc_fence_after();
@@ -398,7 +448,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       lse[(int64_t)(row0 + qb * BQ + r) * H + it.h] = m + log2f(l);
-      if (rec && it.r < 14) tr[5 + 4 * it.r + 2 * t] = globaltimer();
+      if (rec && it.r < 14) tr[5 + 4 * it.r + 2 * t] = clock64();
       tc_fence_before();
     }
   }
@@ -463,22 +513,24 @@ int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causa
   const int grid = items < sms ? items : sms;
   static const bool tracing = getenv("HM_ATTN_TRACE") && getenv("HM_ATTN_TRACE")[0] == '1';
   static unsigned long long *tbuf = nullptr;
-  if (tracing && !tbuf) HM_CUDA(cudaMalloc(&tbuf, 64 * 1024 * sizeof(unsigned long long)));
-  if (tracing) HM_CUDA(cudaMemsetAsync(tbuf, 0, 64 * grid * sizeof(unsigned long long), s));
+  if (tracing && !tbuf) HM_CUDA(cudaMalloc(&tbuf, 512 * 1024 * sizeof(unsigned long long)));
+  if (tracing) HM_CUDA(cudaMemsetAsync(tbuf, 0, 512 * grid * sizeof(unsigned long long), s));
   k<<<dim3(grid), kThreads, kSmem, s>>>(tm, static_cast<__nv_bfloat16 *>(o), lse, S, H, B * H, scale_log2,
                                         tracing ? tbuf : nullptr);
   if (tracing) {  // one JSON line per launch: every CTA's timestamps, ns after the earliest entry
-    std::vector<unsigned long long> h(64 * grid);
+    std::vector<unsigned long long> h(512 * grid);
     HM_CUDA(cudaStreamSynchronize(s));
     HM_CUDA(cudaMemcpy(h.data(), tbuf, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     unsigned long long t0 = ~0ULL;
-    for (int c = 0; c < grid; ++c) t0 = std::min(t0, h[64 * c]);
+    for (int c = 0; c < grid; ++c) t0 = std::min(t0, h[512 * c]);
     fprintf(stderr, "{\"attn_fwd64_trace\": {\"B\": %d, \"S\": %d, \"H\": %d, \"cta\": [", B, S, H);
     for (int c = 0; c < grid; ++c) {
       fprintf(stderr, "%s[", c ? ", " : "");
-      for (int n = 0; n < 64; ++n)
+      for (int n = 0; n < 512; ++n) {  // [0], [1], [62]: ns after the earliest entry; the rest raw clock64
+        const unsigned long long x = h[512 * c + n];
         fprintf(stderr, "%s%lld", n ? ", " : "",
-                n == 2 || n == 61 ? (long long)h[64 * c + n] : h[64 * c + n] ? (long long)(h[64 * c + n] - t0) : -1LL);
+                !x ? -1LL : (n == 0 || n == 1 || n == 62) ? (long long)(x - t0) : (long long)x);
+      }
       fprintf(stderr, "]");
     }
     fprintf(stderr, "]}}\n");
