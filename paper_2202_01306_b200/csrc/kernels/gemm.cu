@@ -62,11 +62,15 @@ struct Args {
 // computes a 256 x BN tile with tcgen05.mma.cta_group::2: each CTA stages its
 // own 128 rows of A and HALF of B's BN rows, so per-SM operand traffic per
 // FLOP drops by a third at BN = 256).
-template <int BN, int CG>
+template <int BN, int CG, int B_MN = 0>
 struct Cfg {
   static constexpr int kBRows = BN / CG;  // B rows staged per CTA
+  // MN-major B is staged in 64-column swizzle atoms: a 96-row half (BN = 192
+  // pair) takes two atoms, the second half-used (its other 32 columns belong
+  // to the peer CTA and are loaded but never read)
+  static constexpr int kBChunks = (kBRows + 63) / 64;
   static constexpr uint32_t kABytes = BM * BK * 2;
-  static constexpr uint32_t kBBytes = kBRows * BK * 2;
+  static constexpr uint32_t kBBytes = B_MN ? kBChunks * 64 * BK * 2 : kBRows * BK * 2;
   static constexpr int kStages = (int)((196608u) / (kABytes + kBBytes)) > 8 ? 8 : (int)(196608u / (kABytes + kBBytes));
   static constexpr uint32_t kTmemCols = 2 * BN > 256 ? 512 : (2 * BN > 128 ? 256 : 128);  // pow2 >= 2 BN
   static constexpr size_t kSmem = 1024 + (size_t)kStages * (kABytes + kBBytes) + kEpiWarps * 4096 + 256;
@@ -270,7 +274,7 @@ template <int BN, int A_MN, int B_MN, int CG, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmX, Args args) {
-  using C = Cfg<BN, CG>;
+  using C = Cfg<BN, CG, B_MN>;
   constexpr int kTileM = BM * CG;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned base by pointer arithmetic on the __shared__ array, so the
@@ -391,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             load(b_dst, &tmB, kb * BK, n0);
           } else {
 #pragma unroll
-            for (int c = 0; c < C::kBRows / 64; ++c) load(b_dst + c * (BK * 128), &tmB, n0 + c * 64, kb * BK);
+            for (int c = 0; c < C::kBChunks; ++c) load(b_dst + c * (BK * 128), &tmB, n0 + c * 64, kb * BK);
           }
           if (++stage == C::kStages) {
             stage = 0;
@@ -633,9 +637,10 @@ static const int g_streamk = getenv("HM_GEMM_STREAMK") ? atoi(getenv("HM_GEMM_ST
 // 128 x 192 single-CTA tiles (fit 1600-wide outputs in 9 column tiles)
 static const bool g_tile192 = getenv("HM_GEMM_192") ? atoi(getenv("HM_GEMM_192")) != 0 : true;
 static const double g_eff192 = getenv("HM_GEMM_EFF192") ? atof(getenv("HM_GEMM_EFF192")) : 0.70;
-// 256 x 192 pair tiles (K-major B only: each CTA stages 96 B rows, which an
-// MN-major 128-B swizzle atom of 64 columns cannot hold)
+// 256 x 192 pair tiles (an MN-major B half of 96 rows is staged as two
+// 64-column atoms, a third more B traffic: g_eff192pm)
 static const double g_eff192p = getenv("HM_GEMM_EFF192P") ? atof(getenv("HM_GEMM_EFF192P")) : 0.80;
+static const double g_eff192pm = getenv("HM_GEMM_EFF192PM") ? atof(getenv("HM_GEMM_EFF192PM")) : 0.78;
 
 static TileCfg pick_tile(int64_t M, int64_t N, int64_t K, int epi, bool allow192 = true, bool b_mn = false) {
   const int env_bn = g_force_bn, env_cg = g_force_cg, env_s = g_force_s > 0 ? g_force_s : 0;
@@ -649,10 +654,10 @@ static TileCfg pick_tile(int64_t M, int64_t N, int64_t K, int epi, bool allow192
     if (env_cg && cg != env_cg) continue;
     for (int bn : {128, 192, 256}) {
       if (env_bn && bn != env_bn) continue;
-      if (bn == 192 && (!g_tile192 || !allow192 || (cg == 2 && b_mn))) continue;
+      if (bn == 192 && (!g_tile192 || !allow192)) continue;
       // pair tiles lose more when B is MN-major (dgrad / wgrad: 64-wide B chunks per k-block)
       const double eff = bn == 128   ? 0.55
-                         : bn == 192 ? (cg == 1 ? g_eff192 : g_eff192p)
+                         : bn == 192 ? (cg == 1 ? g_eff192 : (b_mn ? g_eff192pm : g_eff192p))
                                      : (cg == 1 ? 0.80 : (b_mn ? 0.86 : 0.93));
       const double t_kb = bn / 256.0 / eff;
       const int64_t tiles = ((M + BM * cg - 1) / (BM * cg)) * ((N + bn - 1) / bn);
@@ -697,7 +702,7 @@ static int num_sms() {
 template <int BN, int A_MN, int B_MN, int CG, int MODE = 0>
 static int launch(const CUtensorMap &ta, const CUtensorMap &tb, const CUtensorMap &td, const CUtensorMap &tx,
                   const Args &a, cudaStream_t s) {
-  using C = Cfg<BN, CG>;
+  using C = Cfg<BN, CG, B_MN>;
   static bool attr = false;
   auto kern = gemm_kernel<BN, A_MN, B_MN, CG, MODE>;
   if (!attr) {
@@ -758,7 +763,6 @@ int run(const void *A, const void *B, void *D, int64_t M, int64_t N, int64_t K, 
     return fail(HM_ERR_VALIDATION, "gemm: aux must be 16B aligned with 16B pitch");
   TileCfg tc = pick_tile(M, N, K, epi, true, b_mn != 0);
   if (force_bn) tc.bn = force_bn;
-  if (tc.bn == 192 && tc.cg == 2 && b_mn) tc.cg = 1;  // forced pair: MN-major B cannot stage 96-row halves
   const int bn = tc.bn;
   Args a{};
   a.M = (int)M; a.N = (int)N; a.K = (int)K;
@@ -782,9 +786,13 @@ int run(const void *A, const void *B, void *D, int64_t M, int64_t N, int64_t K, 
   } else {
     tx = td;
   }
-  if (bn == 192 && tc.cg == 2) {  // pair tiles: K-major B only
-    if (a_mn) return launch<192, 1, 0, 2>(ta, tb, td, tx, a, stream);
-    return launch<192, 0, 0, 2>(ta, tb, td, tx, a, stream);
+  if (bn == 192 && tc.cg == 2) {
+    switch ((a_mn ? 2 : 0) | (b_mn ? 1 : 0)) {
+      case 0: return launch<192, 0, 0, 2>(ta, tb, td, tx, a, stream);
+      case 1: return launch<192, 0, 1, 2>(ta, tb, td, tx, a, stream);
+      case 2: return launch<192, 1, 0, 2>(ta, tb, td, tx, a, stream);
+      default: return launch<192, 1, 1, 2>(ta, tb, td, tx, a, stream);
+    }
   }
   if (bn == 192) {
     switch ((a_mn ? 2 : 0) | (b_mn ? 1 : 0)) {
