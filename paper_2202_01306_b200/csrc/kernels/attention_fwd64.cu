@@ -235,20 +235,32 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp < 4) {
     reg_dealloc<72>();  // 3 x 168 per SMSP at launch = 72 + 2 x 216
     if (warp == 0 && lane == 0) {
-      for (Item it = make_item<CAUSAL>(0, c, G, S, H, BH, 0, 0, 0, 0); it.valid; it = next_item(it)) {
-        const int row0 = it.b * S, qp = it.r & 1;
-        mbar_wait(&q_empty[qp], ((it.r >> 1) & 1) ^ 1);
-        mbar_expect_tx(&q_full[qp], (it.nkv1 > 0 ? 2 : 1) * kTile);
-        tma_load_2d(sQ + (2 * qp) * kTile, &tm, &q_full[qp], it.h * DH, row0 + 2 * it.pr * BQ);
-        if (it.nkv1 > 0)
-          tma_load_2d(sQ + (2 * qp + 1) * kTile, &tm, &q_full[qp], it.h * DH, row0 + (2 * it.pr + 1) * BQ);
+      auto load_q = [&](const Item &q) {
+        const int qp = q.r & 1, row0 = q.b * S;
+        mbar_wait(&q_empty[qp], ((q.r >> 1) & 1) ^ 1);
+        mbar_expect_tx(&q_full[qp], (q.nkv1 > 0 ? 2 : 1) * kTile);
+        tma_load_2d(sQ + (2 * qp) * kTile, &tm, &q_full[qp], q.h * DH, row0 + 2 * q.pr * BQ);
+        if (q.nkv1 > 0) tma_load_2d(sQ + (2 * qp + 1) * kTile, &tm, &q_full[qp], q.h * DH, row0 + (2 * q.pr + 1) * BQ);
+      };
+      Item it = make_item<CAUSAL>(0, c, G, S, H, BH, 0, 0, 0, 0);
+      if (it.valid) load_q(it);
+      for (; it.valid; it = next_item(it)) {
+        const int row0 = it.b * S;
         const int nall = it.nkv0 > it.nkv1 ? it.nkv0 : it.nkv1;
+        // the next item's Q pair goes out while this item's K / V still stream
+        // (a whole ring ahead of its first S), once the ring guarantees the
+        // item before this one has issued its last S (which frees that buffer)
+        const int j_q = nall - 1 < kStages ? nall - 1 : kStages;
         for (int j = 0; j < nall; ++j) {
           const int kb = it.kvb + j, st = kb & (kStages - 1);
           mbar_wait(&kv_empty[st], ((kb / kStages) & 1) ^ 1);
           mbar_expect_tx(&kv_full[st], 2 * kTile);
           tma_load_2d(sK + st * kTile, &tm, &kv_full[st], d + it.h * DH, row0 + j * BKV);
           tma_load_2d(sV + st * kTile, &tm, &kv_full[st], 2 * d + it.h * DH, row0 + j * BKV);
+          if (j == j_q) {
+            const Item nx = next_item(it);
+            if (nx.valid) load_q(nx);
+          }
         }
       }
     } else if (warp == 1 && lane == 0) {

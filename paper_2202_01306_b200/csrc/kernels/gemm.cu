@@ -642,9 +642,18 @@ static const double g_eff192 = getenv("HM_GEMM_EFF192") ? atof(getenv("HM_GEMM_E
 static const double g_eff192p = getenv("HM_GEMM_EFF192P") ? atof(getenv("HM_GEMM_EFF192P")) : 0.80;
 static const double g_eff192pm = getenv("HM_GEMM_EFF192PM") ? atof(getenv("HM_GEMM_EFF192PM")) : 0.78;
 
+int &max_kblocks_per_split() {
+  static int v = 0;
+  return v;
+}
+
 static TileCfg pick_tile(int64_t M, int64_t N, int64_t K, int epi, bool allow192 = true, bool b_mn = false) {
   const int env_bn = g_force_bn, env_cg = g_force_cg, env_s = g_force_s > 0 ? g_force_s : 0;
   const bool acc = epi == HM_EPI_ACC_F32;
+  // accuracy cap (fp32-operand mode): the tensor core's fp32 accumulation over a
+  // long K chain loses ~1e-5 relative at K = 6400 vs ~2e-6 in three splits
+  // summed by the reduce-add (profiles/r02_gemm_split_accuracy.jsonl)
+  const int64_t kcap = acc ? max_kblocks_per_split() : 0;
   const bool force_sk = acc && (g_force_s == -1 || g_streamk == 1), allow_sk = acc && !env_s && g_streamk != 0;
   const int64_t sms = num_sms();
   const int64_t num_k = (K + BK - 1) / BK;
@@ -662,9 +671,12 @@ static TileCfg pick_tile(int64_t M, int64_t N, int64_t K, int epi, bool allow192
       const double t_kb = bn / 256.0 / eff;
       const int64_t tiles = ((M + BM * cg - 1) / (BM * cg)) * ((N + bn - 1) / bn);
       const int64_t slots = sms / cg;
+      const int64_t num_k_tot = (K + BK - 1) / BK;
+      const int s_min = kcap > 0 ? (int)std::min<int64_t>(32, (num_k_tot + kcap - 1) / kcap) : 1;
       for (int s = 1; s <= (acc ? 32 : 1); ++s) {
         if (env_s && s != env_s) continue;
-        if (s > 1 && num_k / s < 8) break;
+        if (s < s_min && !env_s) continue;
+        if (s > 1 && num_k / s < 8 && s > s_min) break;
         const double waves = (double)((tiles * s + slots - 1) / slots);
         const double t = waves * ((double)num_k / s + 4.0) * t_kb * (s > 1 ? 1.03 : 1.0);
         if (t < best_t && !force_sk) {

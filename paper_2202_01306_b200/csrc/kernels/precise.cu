@@ -117,6 +117,15 @@ int gemm(const float *A, const float *B, void *D, int64_t M, int64_t N, int64_t 
   const int64_t ldt = fused ? N : ldd;
   const bf16 *a = static_cast<const bf16 *>(sa), *b = static_cast<const bf16 *>(sb);
   static const int order[6][2] = {{2, 0}, {0, 2}, {1, 1}, {1, 0}, {0, 1}, {0, 0}};  // smallest terms first
+  // the accumulating passes (all but the smallest, first term) sum K in
+  // chunks of at most 16 k-blocks (1024) in TMEM, the chunks in fp32 by the
+  // reduce-add: the tensor core's long-chain accumulation error, not the bf16
+  // planes, bounds this mode's accuracy otherwise
+  struct KCap {
+    int prev;
+    KCap() : prev(gemm::max_kblocks_per_split()) { gemm::max_kblocks_per_split() = 16; }
+    ~KCap() { gemm::max_kblocks_per_split() = prev; }
+  } kcap;
   for (int t = 0; t < 6; ++t) {
     const int i = order[t][0], j = order[t][1];
     const bool first = t == 0 && epi != HM_EPI_ACC_F32;

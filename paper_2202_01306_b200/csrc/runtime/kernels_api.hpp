@@ -16,6 +16,9 @@ int run(const void *A, const void *B, void *D, int64_t M, int64_t N, int64_t K, 
         int a_mn, int b_mn, int epi, const float *bias, void *aux, int64_t ld_aux, cudaStream_t stream, int force_bn);
 // when set, every gemm::run call appends {M, N, K, a_mn, b_mn, epi, has_bias}
 std::vector<int64_t> *&shape_log();
+// > 0: accumulating (ACC_F32) GEMMs split K so that no split sums more than
+// this many 64-deep k-blocks in TMEM (the fp32-operand mode's accuracy knob)
+int &max_kblocks_per_split();
 }
 namespace attn {
 int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int DH, int causal, cudaStream_t s);
