@@ -269,17 +269,23 @@ def _pcie_probe():
     e0.record()
     s1.wait_event(e0)
     s2.wait_event(e0)
+    eh, ed = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(s1):
         for _ in range(4):
             d.copy_(h, non_blocking=True)
+        eh.record(s1)
     with torch.cuda.stream(s2):
         for _ in range(4):
             h2.copy_(d2, non_blocking=True)
+        ed.record(s2)
     torch.cuda.current_stream().wait_stream(s1)
     torch.cuda.current_stream().wait_stream(s2)
     e1.record()
     torch.cuda.synchronize()
-    out["bidir"] = 8 * n / (e0.elapsed_time(e1) / 1e3) / 1e9
+    # each direction's rate over its own span (both start together): the sum is
+    # the two-direction capacity even when one direction finishes first (the
+    # total over the longer span would count the other's idle tail against it)
+    out["bidir"] = 4 * n / (e0.elapsed_time(eh) / 1e3) / 1e9 + 4 * n / (e0.elapsed_time(ed) / 1e3) / 1e9
     del h2, d2
     for name, fn in (("h2d", lambda: d.copy_(h, non_blocking=True)), ("d2h", lambda: h.copy_(d, non_blocking=True))):
         fn()
