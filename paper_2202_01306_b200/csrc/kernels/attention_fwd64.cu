@@ -10,7 +10,7 @@
 // last tiles are still in the softmax (16 x 1024 x 25 heads: 114.6 vs 138.6 us
 // for one CTA per pair).
 //   warp 0      TMA: Q pairs, then K_j / V_j into a 4-stage ring
-//   warp 1      MMA issuer
+//   warp 1      PV MMA issuer, warp 2 S MMA issuer
 //   warps 4-7   softmax of tile 0, warps 8-11 of tile 1 (one thread per
 //               query row = TMEM lane)
 // TMEM (512 columns): three rotating 128-column S buffers + O_0, O_1 (64
@@ -182,9 +182,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // diagnostics (HM_ATTN_TRACE=1), 512 words per CTA: globaltimer at [0] entry,
   // [1] setup done, [62] exit; clock64 at [2] setup, [61] exit, [4 + 4 k + 2 t]
   // tile t's first S of item k, [+1] its epilogue done, [64 + 96 t + 2 k] tile
-  // t's k-th S ready, [+1] its P handed over, and for the MMA thread at
-  // position n < 60: [256 + 4 n] P(n) ready, [+1] PV(n) issued, [+2] K block
-  // of S(n + 3) ready, [+3] S(n + 3) issued
+  // t's k-th S ready, [+1] its P handed over, and for the issuing threads at
+  // position n < 60: [256 + 4 n] P(n) ready, [+1] PV(n) issued, [+2] S(n)'s
+  // inputs ready, [+3] S(n) issued
   unsigned long long *tr = trace ? trace + 512 * blockIdx.x : nullptr;
   if (tr && threadIdx.x == 0) tr[0] = globaltimer();
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -197,7 +197,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t *s_full = kv_empty + kStages;                       // [S buffer]
   uint64_t *p_full = s_full + kSBuf;                           // [tile][step parity]
   uint64_t *o_done = p_full + 4;                               // [tile]: the item's last PV_t
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(o_done + 2);
+  uint64_t *pv_done = o_done + 2;                              // [S buffer]: PV read its P
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(pv_done + kSBuf);
 
   const int G = gridDim.x, c = blockIdx.x;
   const int d = H * DH;
@@ -218,7 +219,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
     }
-    for (int i = 0; i < kSBuf; ++i) mbar_init(&s_full[i], 1);
+    for (int i = 0; i < kSBuf; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&pv_done[i], 1);
+    }
     for (int i = 0; i < 4; ++i) mbar_init(&p_full[i], 128);
     fence_barrier_init();
   }
@@ -263,80 +267,89 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-    } else if (warp == 1 && lane == 0) {
+    } else if ((warp == 1 || warp == 2) && lane == 0) {
+      // Two issuing threads on two SM sub-partitions: warp 1 issues the PVs,
+      // warp 2 the S MMAs.  tcgen05.mma issue blocks at the execution rate and
+      // every mbarrier round trip costs ~150 cycles while the SS MMAs saturate
+      // shared memory, so one thread doing both left the tensor pipe idle for
+      // its waits and commits (~1300 cycles per 622 of MMAs); two threads wait
+      // while the other issues.  S(m) overwrites the P that PV(m - 3) reads, and
+      // MMAs of different threads are not ordered: the S thread waits for PV(m
+      // - 3) to COMPLETE (pv_done), which also lets a softmax rescale wait on
+      // S(prev + 3) for PV(prev).
       constexpr uint32_t idesc_s = idesc_bf16_f32(BQ, BKV, 0, 0);  // Q K-major, K K-major
       constexpr uint32_t idesc_o = idesc_bf16_f32(BQ, DH, 0, 1);   // P (TMEM), V MN-major
       // descriptor low words of buffer 0 (a buffer adds kTile >> 4, a K step of
       // Q / K 32 B >> 4 = 2, of V 2048 B >> 4 = 128); all share one high word
       const uint32_t d_hi = (uint32_t)(umma_desc_sw128(0, 0, 1024) >> 32);
-      const uint32_t q_lo0 = (uint32_t)umma_desc_sw128(smem_u32(sQ), 16, 1024);
-      const uint32_t k_lo0 = (uint32_t)umma_desc_sw128(smem_u32(sK), 16, 1024);
-      const uint32_t v_lo0 = (uint32_t)umma_desc_sw128(smem_u32(sV), kTile, 1024);
-      // The single issuing thread is the pipe's feeder: a position's 12 MMAs
-      // take ~600 cycles of tensor time, so its bookkeeping is kept to running
-      // counters (S buffer, tile steps) and power-of-two ring arithmetic.
-      // S cursor: runs up to kSBuf positions ahead of the PVs, across items
-      Item sit = make_item<CAUSAL>(0, c, G, S, H, BH, 0, 0, 0, 0);
-      int s_loc = 0, s_buf = 0, kv_ready = -1;
-      unsigned long long t_kv = 0;
-      auto issue_next_s = [&]() {
-        if (s_loc >= sit.npos) {
-          do {
-            sit = next_item(sit);
-          } while (sit.valid && sit.npos == 0);
-          s_loc = 0;
-        }
-        if (!sit.valid) {  // past the last item: keep s_full's phases in step with positions
-          mma_commit(&s_full[s_buf]);
-          s_buf = s_buf == kSBuf - 1 ? 0 : s_buf + 1;
-          return;
-        }
-        const int qp = sit.r & 1;
-        if (s_loc == 0) mbar_wait(&q_full[qp], (sit.r >> 1) & 1);
-        int t, j;
-        sit.at(s_loc, t, j);
-        const int kb = sit.kvb + j;
-        if (kb > kv_ready) {  // both tiles' S of a step read the same K block: one wait
-          mbar_wait(&kv_full[kb & (kStages - 1)], (kb / kStages) & 1);
-          tc_fence_after();
-          kv_ready = kb;
-        }
-        if (tr) t_kv = clock64();
-        const uint32_t q_lo = q_lo0 + (uint32_t)(2 * qp + t) * (kTile >> 4);
-        const uint32_t k_lo = k_lo0 + (uint32_t)(kb & (kStages - 1)) * (kTile >> 4);
-        const uint32_t d_s = tmem + s_buf * BKV;
-        mma_bf16_lohi(d_s, q_lo, k_lo, d_hi, idesc_s, 0u);
-#pragma unroll
-        for (int kk = 1; kk < DH / 16; ++kk) mma_bf16_lohi(d_s, q_lo + 2 * kk, k_lo + 2 * kk, d_hi, idesc_s, 1u);
-        mma_commit(&s_full[s_buf]);
-        if (s_loc == sit.npos - 1) mma_commit(&q_empty[qp]);  // the item's last Q K^T: its Q pair is free
-        s_buf = s_buf == kSBuf - 1 ? 0 : s_buf + 1;
-        ++s_loc;
-      };
-      for (int k = 0; k < kSBuf; ++k) issue_next_s();
-      int pv_buf = 0, gc0 = 0, gc1 = 0;  // PV position % kSBuf; steps of tile 0 / 1 so far
-      for (Item it = make_item<CAUSAL>(0, c, G, S, H, BH, 0, 0, 0, 0); it.valid; it = next_item(it)) {
-        for (int n = 0; n < it.npos; ++n) {
+      if (warp == 2) {
+        const uint32_t q_lo0 = (uint32_t)umma_desc_sw128(smem_u32(sQ), 16, 1024);
+        const uint32_t k_lo0 = (uint32_t)umma_desc_sw128(smem_u32(sK), 16, 1024);
+        Item sit = make_item<CAUSAL>(0, c, G, S, H, BH, 0, 0, 0, 0);
+        int s_loc = 0, s_buf = 0, kv_ready = -1, tail = 0;
+        for (int m = 0;; ++m) {
+          if (s_loc >= sit.npos) {
+            do {
+              sit = next_item(sit);
+            } while (sit.valid && sit.npos == 0);
+            s_loc = 0;
+          }
+          if (m >= kSBuf) {  // PV(m - 3) has read this buffer's P
+            mbar_wait(&pv_done[s_buf], ((m - kSBuf) / kSBuf) & 1);
+            tc_fence_after();
+          }
+          if (!sit.valid) {  // past the last item: kSBuf empty commits keep s_full's
+            mma_commit(&s_full[s_buf]);  // phases in step with the positions a rescale names
+            s_buf = s_buf == kSBuf - 1 ? 0 : s_buf + 1;
+            if (++tail == kSBuf) break;
+            continue;
+          }
+          const int qp = sit.r & 1;
+          if (s_loc == 0) mbar_wait(&q_full[qp], (sit.r >> 1) & 1);
           int t, j;
-          it.at(n, t, j);
-          const int gs = t ? gc1++ : gc0++, kb = it.kvb + j, P = it.pb + n;
-          mbar_wait(&p_full[2 * t + (gs & 1)], (gs >> 1) & 1);  // P_t(j) in S buffer pv_buf (and O_t rescaled)
+          sit.at(s_loc, t, j);
+          const int kb = sit.kvb + j;
+          if (kb > kv_ready) {  // both tiles' S of a step read the same K block: one wait
+            mbar_wait(&kv_full[kb & (kStages - 1)], (kb / kStages) & 1);
+            kv_ready = kb;
+          }
           tc_fence_after();
-          if (tr && P < 60) tr[256 + 4 * P] = clock64();
-          const uint32_t v_lo = v_lo0 + (uint32_t)(kb & (kStages - 1)) * (kTile >> 4);
-          const uint32_t p_tm = tmem + pv_buf * BKV, d_o = tmem + C_O + t * DH;
-          mma_bf16_ts_lohi(d_o, p_tm, v_lo, d_hi, idesc_o, j > 0 ? 1u : 0u);
+          if (tr && m < 60) tr[258 + 4 * m] = clock64();
+          const uint32_t q_lo = q_lo0 + (uint32_t)(2 * qp + t) * (kTile >> 4);
+          const uint32_t k_lo = k_lo0 + (uint32_t)(kb & (kStages - 1)) * (kTile >> 4);
+          const uint32_t d_s = tmem + s_buf * BKV;
+          mma_bf16_lohi(d_s, q_lo, k_lo, d_hi, idesc_s, 0u);
 #pragma unroll
-          for (int kk = 1; kk < BKV / 16; ++kk) mma_bf16_ts_lohi(d_o, p_tm + kk * 8, v_lo + kk * 128, d_hi, idesc_o, 1u);
-          if (tr && P < 60) tr[257 + 4 * P] = clock64();
-          if (j == (t == 0 ? it.nkv0 : it.nkv1) - 1) mma_commit(&o_done[t]);  // O_t of this item final
-          if (t == 1 || j >= it.mn) mma_commit(&kv_empty[kb & (kStages - 1)]);  // last use of K_j / V_j
-          pv_buf = pv_buf == kSBuf - 1 ? 0 : pv_buf + 1;
-          // S(P + 3) overwrites P(P) in TMEM: issued after PV(P), which reads it first
-          issue_next_s();
-          if (tr && P < 60) {
-            tr[258 + 4 * P] = t_kv;
-            tr[259 + 4 * P] = clock64();
+          for (int kk = 1; kk < DH / 16; ++kk) mma_bf16_lohi(d_s, q_lo + 2 * kk, k_lo + 2 * kk, d_hi, idesc_s, 1u);
+          mma_commit(&s_full[s_buf]);
+          if (s_loc == sit.npos - 1) mma_commit(&q_empty[qp]);  // the item's last Q K^T: its Q pair is free
+          if (tr && m < 60) tr[259 + 4 * m] = clock64();
+          s_buf = s_buf == kSBuf - 1 ? 0 : s_buf + 1;
+          ++s_loc;
+        }
+      } else {
+        const uint32_t v_lo0 = (uint32_t)umma_desc_sw128(smem_u32(sV), kTile, 1024);
+        int pv_buf = 0, gc0 = 0, gc1 = 0;  // PV position % kSBuf; steps of tile 0 / 1 so far
+        for (Item it = make_item<CAUSAL>(0, c, G, S, H, BH, 0, 0, 0, 0); it.valid; it = next_item(it)) {
+          for (int n = 0; n < it.npos; ++n) {
+            int t, j;
+            it.at(n, t, j);
+            const int gs = t ? gc1++ : gc0++, kb = it.kvb + j, P = it.pb + n;
+            mbar_wait(&p_full[2 * t + (gs & 1)], (gs >> 1) & 1);  // P_t(j) in S buffer pv_buf (and O_t rescaled)
+            tc_fence_after();
+            if (tr && P < 60) tr[256 + 4 * P] = clock64();
+            const uint32_t v_lo = v_lo0 + (uint32_t)(kb & (kStages - 1)) * (kTile >> 4);
+            const uint32_t p_tm = tmem + pv_buf * BKV, d_o = tmem + C_O + t * DH;
+            mma_bf16_ts_lohi(d_o, p_tm, v_lo, d_hi, idesc_o, j > 0 ? 1u : 0u);
+#pragma unroll
+            for (int kk = 1; kk < BKV / 16; ++kk) mma_bf16_ts_lohi(d_o, p_tm + kk * 8, v_lo + kk * 128, d_hi, idesc_o, 1u);
+            if (tr && P < 60) tr[257 + 4 * P] = clock64();
+            mma_commit(&pv_done[pv_buf]);
+            if (j == (t == 0 ? it.nkv0 : it.nkv1) - 1) mma_commit(&o_done[t]);  // O_t of this item final
+            // last use of K_j / V_j: the S MMAs that read K_j completed before
+            // their softmax handed over the P this PV reads
+            if (t == 1 || j >= it.mn) mma_commit(&kv_empty[kb & (kStages - 1)]);
+            pv_buf = pv_buf == kSBuf - 1 ? 0 : pv_buf + 1;
           }
         }
       }
@@ -392,10 +405,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           m = m_row;
         }
         if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {  // warp-uniform: tcgen05.ld / st are .sync.aligned
-          // wait for PV_t(j - 1): the MMA thread issues S(p + 3) right after
-          // PV(p), so S(prev + 3)'s completion covers it.  Its buffer cannot
-          // have cycled again: the next S into it follows PV(n + 1), which
-          // follows this thread's P(n).
+          // wait for PV_t(j - 1): S(prev + 3) is issued only once PV(prev) has
+          // completed, so its completion covers it.  Its buffer cannot have
+          // cycled again: the next S into it follows PV(n + 1), which follows
+          // this thread's P(n).
           const int jp = j - 1;
           const int need = it.pb + (jp < it.mn ? 2 * jp + t : 2 * it.mn + (jp - it.mn)) + kSBuf;
           mbar_wait(&s_full[need % kSBuf], (need / kSBuf) & 1);

@@ -404,12 +404,13 @@ __global__ void __launch_bounds__(kThreads2, 1)
   float *sD = sL + 2 * BQ;                               // [2][128] D
   uint64_t *bar = reinterpret_cast<uint64_t *>(sD + 2 * BQ);
   uint64_t *kv_full = bar, *kv_empty = bar + 1;
+  // q_empty[b]: block n's gradient MMAs retired (n & 1 == b) -- frees its Q / dO
+  // stage and dS^T buffer and publishes dQ(n)
   uint64_t *q_full = bar + 2, *q_empty = bar + 4;
   uint64_t *st_full = bar + 6, *st_empty = bar + 7;
   uint64_t *p_full = bar + 8, *pt_free = bar + 9;  // P^T (TMEM) + dS^T (smem) written / P^T read by dV
-  uint64_t *dq_full = bar + 10, *dq_empty = bar + 11;
+  uint64_t *dq_empty = bar + 11;
   uint64_t *acc_full = bar + 12, *acc_empty = bar + 13;
-  uint64_t *ds_empty = bar + 14;                  // [dS^T buffer]: read by dK / dQ
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 16);
 
   const int nq = S / BQ, nkb = S / BKV, n_items = nkb * BH;
@@ -450,9 +451,6 @@ __global__ void __launch_bounds__(kThreads2, 1)
     mbar_init(st_empty, 256);
     mbar_init(p_full, 256);
     mbar_init(pt_free, 1);
-    mbar_init(&ds_empty[0], 1);
-    mbar_init(&ds_empty[1], 1);
-    mbar_init(dq_full, 1);
     mbar_init(dq_empty, 256);
     mbar_init(acc_full, 1);
     mbar_init(acc_empty, 256);
@@ -553,9 +551,11 @@ __global__ void __launch_bounds__(kThreads2, 1)
           for (int kk = 0; kk < BKV / 16; ++kk)  // reduction over the 128 keys
             mma_bf16(tmem + C_DQ, umma_desc_sw128(ds_base + kk * 2048, BKV * 128, 1024),
                      umma_desc_sw128(k_base + kk * 2048, BKV * 128, 1024), id_mnmn, kk > 0);
-          mma_commit(dq_full);
+          // one commit frees block n's Q / dO stage (producer), its dS^T buffer
+          // (softmax, block n + 2) and publishes dQ(n) (softmax): every commit
+          // and wait of the single issuing thread idles the tensor pipe (~45 /
+          // ~150 cycles, see attention_fwd64.cu)
           mma_commit(&q_empty[st]);
-          mma_commit(&ds_empty[n & 1]);
           mark(2, n);
         }
         mma_commit(acc_full);
@@ -581,7 +581,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     // instead of 8192 scalar atomics, staged in SW128 rows (conflict-free
     // writes); each warpgroup drains 32 columns
     auto dq_out = [&](int qrow, int hh, int nn) {
-      mbar_wait(dq_full, nn & 1);
+      mbar_wait(&q_empty[nn & 1], (nn >> 1) & 1);  // block nn's gradient MMAs (dQ included) retired
       tc_fence_after();
       uint32_t q[32];
       tmem_ld_32x32b_x32(tmem + lane_addr + C_DQ + wg * 32, q);
@@ -671,7 +671,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
           if (diag) elementwise(std::true_type{});
           else elementwise(std::false_type{});
           if (c0 == 0) {
-            mbar_wait(&ds_empty[n & 1], ((n >> 1) & 1) ^ 1);  // dK / dQ(n - 2) have read this dS^T buffer
+            mbar_wait(&q_empty[n & 1], ((n >> 1) & 1) ^ 1);  // dK / dQ(n - 2) have read this dS^T buffer
             mbar_wait(pt_free, ph ^ 1);                       // dV(n - 1) has read P^T
             tc_fence_after();
             if (wg == 0 && rr == 0) mark(4, n);
