@@ -33,17 +33,16 @@
 // when a row max grows by more than 2^8 (lazy rescale, exact in O / l).
 //
 // Measured balance (HM_ATTN_TRACE clock64 trace, tools/probes/attn_mma_probe):
-// a position (one tile's 128 x 128 block) costs ~1300 cycles on BOTH sides.
-// The MMA thread: PV (8 x 128x64x16 from TMEM) 366 + S (4 x 128x128x16) 256
-// cycles of tensor time, but tcgen05.mma issue blocks at the execution rate
-// (no queue to hide the thread's own work), a try_wait on an already
-// completed mbarrier costs ~150 cycles and a commit ~45, so every wait, commit
-// and counter update is tensor-pipe idle time.  The softmax: 128 ex2 + 64
-// bf16x2 conversions per row on the MUFU/XU pipe, ~1280 cycles per position
-// with both tiles' warps sharing each SMSP.  Hence: one K-block wait per step,
-// no per-PV commit (a rescale waits on the S issued after the previous PV),
-// descriptors as precomputed 32-bit words, ring / buffer counters without
-// divisions.
+// a position (one tile's 128 x 128 block) holds 542 cycles of MMAs (PV 8 x
+// 128x64x16 from TMEM: 366; S 4 x 128x128x16: 256), but tcgen05.mma issue
+// blocks at the execution rate, a try_wait on an already completed mbarrier
+// costs ~150 cycles while the SS MMAs saturate shared memory and a commit
+// ~45, so one issuing thread left the pipe idle for its own waits (~1300
+// cycles per position).  Hence two issuing threads (PV / S) on two SM
+// sub-partitions, descriptors as precomputed 32-bit words, one K-block wait
+// per step and counters without divisions.  The softmax then bounds it: 128
+// ex2 + 64 bf16x2 conversions per row on the XU pipe with both tiles' warps on
+// each SMSP; one exponent pair in eight goes to the FMA pipe (ex2_poly2).
 //
 // Output conventions as attention.cu: o [tokens, d] bf16, lse [tokens, H]
 // in the log2 domain.
@@ -106,6 +105,23 @@ __device__ __forceinline__ float2 mul2(float2 a, float2 b) {
       : "=f"(d.x), "=f"(d.y)
       : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
   return d;
+}
+// 2^x for a pair of x <= 0 on the FMA / ALU pipes instead of the XU (MUFU)
+// pipe the softmax is bound by: x = j + f with j = rint(x) by magic-number
+// rounding and f in [-0.5, 0.5]; 2^f from a degree-3 polynomial (relative
+// error 7.5e-5, a fortieth of bf16's rounding step); j added into the
+// exponent field.  x is clamped at -120 (masked keys: 2^-120, not 0).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -120.f);
+  x.y = fmaxf(x.y, -120.f);
+  const float2 y = add2(x, make_float2(12582912.f, 12582912.f));  // 1.5 * 2^23: rint(x) in the low bits
+  const float2 j = add2(y, make_float2(-12582912.f, -12582912.f));
+  const float2 f = fma2(j, make_float2(-1.f, -1.f), x);
+  float2 q = fma2(make_float2(0.05517165f, 0.05517165f), f, make_float2(0.24261093f, 0.24261093f));
+  q = fma2(q, f, make_float2(0.69326096f, 0.69326096f));
+  q = fma2(q, f, make_float2(0.99992808f, 0.99992808f));
+  return make_float2(__uint_as_float(__float_as_uint(q.x) + (__float_as_uint(y.x) << 23)),
+                     __uint_as_float(__float_as_uint(q.y) + (__float_as_uint(y.y) << 23)));
 }
 template <int N>
 __device__ __forceinline__ void reg_alloc() {
@@ -174,7 +190,7 @@ __device__ __forceinline__ Item make_item(int r, int c, int G, int S, int H, int
   return it;
 }
 
-template <bool CAUSAL>
+template <bool CAUSAL, int EMU>
 __global__ void __launch_bounds__(kThreads, 1)
     fwd_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16 *__restrict__ out, float *__restrict__ lse,
                int S, int H, int BH, float scale_log2, unsigned long long *trace) {
@@ -436,7 +452,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int cc = 0; cc < 32; cc += 2) {
             const float2 x = fma2(make_float2(__uint_as_float(v[c0 + cc]), __uint_as_float(v[c0 + cc + 1])), sc2, nm2);
-            const float2 p = make_float2(ex2(x.x), ex2(x.y));
+            // EMU > 0: one exponent pair in EMU on the FMA pipe (the XU pipe bounds the softmax)
+            const float2 p = (EMU > 0 && (cc >> 1) % (EMU > 0 ? EMU : 1) == (EMU > 0 ? EMU : 1) - 1)
+                                 ? ex2_poly2(x)
+                                 : make_float2(ex2(x.x), ex2(x.y));
             rs[(cc >> 1) & 1] = add2(rs[(cc >> 1) & 1], p);
             pk[cc >> 1] = bf16x2(p.x, p.y);
           }
@@ -527,7 +546,11 @@ int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causa
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
   ProfScope ps(KC_ATTN_FWD, s, 4.0 * B * (double)S * S * H * DH * (causal ? 0.5 : 1.0), (double)B * S * H * DH * 2 * 4);
   static bool attr[2] = {false, false};
-  auto k = causal ? fwd_kernel<true> : fwd_kernel<false>;
+  // one exponent pair in eight on the FMA pipe (HM_ATTN_EMU=0: all on the XU
+  // pipe): 4 x 1024 x 25 causal 36.3 -> 35.4 us, 8 x 512 x 16 22.8 -> 21.8;
+  // one in four measured the same, one in two slower (profiles/r02_attn_emu_ab.jsonl)
+  static const bool emu = !(getenv("HM_ATTN_EMU") && atoi(getenv("HM_ATTN_EMU")) == 0);
+  auto k = causal ? (emu ? fwd_kernel<true, 8> : fwd_kernel<true, 0>) : (emu ? fwd_kernel<false, 8> : fwd_kernel<false, 0>);
   if (!attr[causal ? 1 : 0]) {
     HM_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem));
     attr[causal ? 1 : 0] = true;
