@@ -482,7 +482,13 @@ __global__ void __launch_bounds__(kThreads2, 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 || warp == 2) {
+    // Two issuing threads on two SM sub-partitions: warp 2 issues S^T / dP^T,
+    // warp 1 the gradient MMAs (dV, dK, dQ).  tcgen05.mma issue blocks at the
+    // execution rate and each mbarrier round trip costs ~150 cycles, so one
+    // thread issuing everything idled the pipe through its own waits.  The two
+    // streams touch disjoint TMEM / shared memory except through the softmax
+    // (st_full -> softmax -> p_full), which orders them.
     if (lane == 0) {
       constexpr uint32_t id_kk = idesc_bf16_f32(128, 128, 0, 0);   // S^T, dP^T: K-major x K-major
       constexpr uint32_t id_kmn = idesc_bf16_f32(128, DH, 0, 1);   // dV, dK: A K-major, B MN-major
@@ -507,59 +513,67 @@ __global__ void __launch_bounds__(kThreads2, 1)
         mark(0, n);
       };
       int n = 0;
-      for (int r = 0, i; (i = bwd_item(r, c, G)) < n_items; ++r) {
-        int kb, b, h;
-        decode(i, kb, b, h);
-        const int count = nq - (CAUSAL ? kb : 0);
-        mbar_wait(kv_full, r & 1);
-        issue_st(n);
-        for (int blk = 0; blk < count; ++blk, ++n) {
-          const int st = n & 1;
-          const uint32_t ph = n & 1;
+      if (warp == 2) {
+        for (int r = 0, i; (i = bwd_item(r, c, G)) < n_items; ++r) {
+          int kb, b, h;
+          decode(i, kb, b, h);
+          const int count = nq - (CAUSAL ? kb : 0);
+          mbar_wait(kv_full, r & 1);
           // block n+1's S^T / dP^T go in as soon as the softmax warps have read
-          // block n's (st_empty), ahead of block n's gradient MMAs, so the next
-          // elementwise pass never waits for them.  (Issuing them after dV /
-          // dK(n) instead measured 4450 vs 3800 cycles per block, HM_ATTN_TRACE.)
-          // P^T lives in TMEM (the dV MMA's A operand) and dS^T is double-
-          // buffered in shared memory, so softmax n+1 waits only for dV(n).
-          // What bounds a block is shared-memory bandwidth: the SS MMAs read
-          // ~160 KB per block (128 B / clock feeds a 128x64x16 SS MMA exactly,
-          // so these N = 64 MMAs run at 48 cycles alone), plus the TMA, dS^T
-          // and dQ-stage traffic: ~2300 of the ~3800 cycles per block, and the
-          // trace shows the MMAs at ~120 cycles each (profiles/r02_attn_bwd_trace_pt_tmem.log).
-          if (blk + 1 < count) issue_st(n + 1);
-          const uint32_t q_base = smem_u32(sQ + st * kTileBytes), do_base = smem_u32(sdO + st * kTileBytes);
-          mbar_wait(p_full, ph);
-          mark(1, n);
-          if (blk == 0) mbar_wait(acc_empty, (r & 1) ^ 1);  // the previous item's dV / dK drained
-          tc_fence_after();
-          const uint32_t ds_base = ds_buf0 + (n & 1) * kPBytes;
-#pragma unroll
-          for (int kk = 0; kk < BQ / 16; ++kk)  // dV += P^T dO, P^T from TMEM (16 queries = 8 columns)
-            mma_bf16_ts(tmem + C_DV, tmem + C_PT + kk * 8, umma_desc_sw128(do_base + kk * 2048, BQ * 128, 1024),
-                        id_kmn, (blk > 0 || kk > 0) ? 1u : 0u);
-          mma_commit(pt_free);  // P^T read: the next block's softmax may overwrite it
-#pragma unroll
-          for (int kk = 0; kk < BQ / 16; ++kk) {  // dK += dS^T Q, reduction over the 128 queries
-            const uint32_t a_off = (kk >> 2) * (BKV * 128) + (kk & 3) * 32;
-            mma_bf16(tmem + C_DK, umma_desc_sw128(ds_base + a_off, 16, 1024),
-                     umma_desc_sw128(q_base + kk * 2048, BQ * 128, 1024), id_kmn, (blk > 0 || kk > 0) ? 1u : 0u);
-          }
-          mbar_wait(dq_empty, ph ^ 1);  // the previous block's dQ has left TMEM
-          tc_fence_after();
-#pragma unroll
-          for (int kk = 0; kk < BKV / 16; ++kk)  // reduction over the 128 keys
-            mma_bf16(tmem + C_DQ, umma_desc_sw128(ds_base + kk * 2048, BKV * 128, 1024),
-                     umma_desc_sw128(k_base + kk * 2048, BKV * 128, 1024), id_mnmn, kk > 0);
-          // one commit frees block n's Q / dO stage (producer), its dS^T buffer
-          // (softmax, block n + 2) and publishes dQ(n) (softmax): every commit
-          // and wait of the single issuing thread idles the tensor pipe (~45 /
-          // ~150 cycles, see attention_fwd64.cu)
-          mma_commit(&q_empty[st]);
-          mark(2, n);
+          // block n's (st_empty, inside issue_st), while block n's gradient MMAs
+          // are still queued from the other thread
+          for (int blk = 0; blk < count; ++blk, ++n) issue_st(n);
         }
-        mma_commit(acc_full);
-        mma_commit(kv_empty);
+      } else {
+        for (int r = 0, i; (i = bwd_item(r, c, G)) < n_items; ++r) {
+          int kb, b, h;
+          decode(i, kb, b, h);
+          const int count = nq - (CAUSAL ? kb : 0);
+          mbar_wait(kv_full, r & 1);  // dQ reads K
+          for (int blk = 0; blk < count; ++blk, ++n) {
+            const int st = n & 1;
+            const uint32_t ph = n & 1;
+            // P^T lives in TMEM (the dV MMA's A operand) and dS^T is double-
+            // buffered in shared memory, so softmax n+1 waits only for dV(n).
+            // What bounds a block is shared-memory bandwidth: the SS MMAs read
+            // ~160 KB per block (128 B / clock feeds a 128x64x16 SS MMA exactly,
+            // so these N = 64 MMAs run at 48 cycles alone), plus the TMA, dS^T
+            // and dQ-stage traffic: ~2300 of the ~3800 cycles per block, and the
+            // trace shows the MMAs at ~120 cycles each (profiles/r02_attn_bwd_trace_pt_tmem.log).
+            const uint32_t q_base = smem_u32(sQ + st * kTileBytes), do_base = smem_u32(sdO + st * kTileBytes);
+            mbar_wait(p_full, ph);
+            mark(1, n);
+            if (blk == 0) mbar_wait(acc_empty, (r & 1) ^ 1);  // the previous item's dV / dK drained
+            tc_fence_after();
+            const uint32_t ds_base = ds_buf0 + (n & 1) * kPBytes;
+#pragma unroll
+            for (int kk = 0; kk < BQ / 16; ++kk)  // dV += P^T dO, P^T from TMEM (16 queries = 8 columns)
+              mma_bf16_ts(tmem + C_DV, tmem + C_PT + kk * 8, umma_desc_sw128(do_base + kk * 2048, BQ * 128, 1024),
+                          id_kmn, (blk > 0 || kk > 0) ? 1u : 0u);
+            mma_commit(pt_free);  // P^T read: the next block's softmax may overwrite it
+#pragma unroll
+            for (int kk = 0; kk < BQ / 16; ++kk) {  // dK += dS^T Q, reduction over the 128 queries
+              const uint32_t a_off = (kk >> 2) * (BKV * 128) + (kk & 3) * 32;
+              mma_bf16(tmem + C_DK, umma_desc_sw128(ds_base + a_off, 16, 1024),
+                       umma_desc_sw128(q_base + kk * 2048, BQ * 128, 1024), id_kmn, (blk > 0 || kk > 0) ? 1u : 0u);
+            }
+            mbar_wait(dq_empty, ph ^ 1);  // the previous block's dQ has left TMEM
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < BKV / 16; ++kk)  // reduction over the 128 keys
+              mma_bf16(tmem + C_DQ, umma_desc_sw128(ds_base + kk * 2048, BKV * 128, 1024),
+                       umma_desc_sw128(k_base + kk * 2048, BKV * 128, 1024), id_mnmn, kk > 0);
+            // one commit frees block n's Q / dO stage (producer; S^T / dP^T(n),
+            // the other thread's readers of Q / dO, completed before p_full(n)),
+            // its dS^T buffer (softmax, block n + 2) and publishes dQ(n)
+            // (softmax): every commit and wait idles the issuing thread (~45 /
+            // ~150 cycles, see attention_fwd64.cu)
+            mma_commit(&q_empty[st]);
+            mark(2, n);
+          }
+          mma_commit(acc_full);
+          mma_commit(kv_empty);
+        }
       }
     }
   } else if (warp >= 4) {
