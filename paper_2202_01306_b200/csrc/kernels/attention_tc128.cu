@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t *q_full = bar + 1, *q_empty = bar + 3;
   uint64_t *st_full = bar + 5, *st_empty = bar + 6;
   uint64_t *p_full = bar + 7, *p_empty = bar + 8;
-  uint64_t *dq_full = bar + 9, *dq_empty = bar + 11, *acc_full = bar + 13;
+  uint64_t *dq_empty = bar + 11, *acc_full = bar + 13;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 14);
 
   const int nq = S / SUBQ;
@@ -346,7 +346,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
-      mbar_init(&dq_full[i], 1);
       mbar_init(&dq_empty[i], 256);
     }
     mbar_init(st_full, 1);
@@ -379,7 +378,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 || warp == 2) {
+    // two issuing threads (see attention_fwd64.cu / attention_tc.cu): warp 2
+    // issues S^T / dP^T, warp 1 the gradient MMAs; the softmax orders them
     if (lane == 0) {
       constexpr uint32_t id_st = idesc_bf16_f32(BKV, SUBQ, 0, 0);  // S^T, dP^T: K-major x K-major
       constexpr uint32_t id_acc = idesc_bf16_f32(BKV, DH, 0, 1);   // dV, dK: A K-major, B MN-major
@@ -404,34 +405,37 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mma_commit(st_full);
       };
-      issue_st(0);
-      for (int n = 0; n < count; ++n) {
-        const int st = n & 1;
-        const uint32_t ph = n & 1;
-        if (n + 1 < count) issue_st(n + 1);
-        const uint32_t q_base = smem_u32(sQ + st * kSubTile), do_base = smem_u32(sdO + st * kSubTile);
-        mbar_wait(p_full, ph);
-        tc_fence_after();
+      if (warp == 2) {
+        for (int n = 0; n < count; ++n) issue_st(n);
+      } else {
+        for (int n = 0; n < count; ++n) {
+          const int st = n & 1;
+          const uint32_t ph = n & 1;
+          const uint32_t q_base = smem_u32(sQ + st * kSubTile), do_base = smem_u32(sdO + st * kSubTile);
+          mbar_wait(p_full, ph);
+          tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < SUBQ / 16; ++kk) {  // reduction over the 64 queries
-          const uint32_t acc = (n > 0 || kk > 0) ? 1u : 0u;
-          mma_bf16(tmem + C_DV, umma_desc_sw128(p_base + kk * 32, 16, 1024),
-                   umma_desc_sw128(do_base + kk * 2048, kSubAtom, 1024), id_acc, acc);
-          mma_bf16(tmem + C_DK, umma_desc_sw128(ds_base + kk * 32, 16, 1024),
-                   umma_desc_sw128(q_base + kk * 2048, kSubAtom, 1024), id_acc, acc);
+          for (int kk = 0; kk < SUBQ / 16; ++kk) {  // reduction over the 64 queries
+            const uint32_t acc = (n > 0 || kk > 0) ? 1u : 0u;
+            mma_bf16(tmem + C_DV, umma_desc_sw128(p_base + kk * 32, 16, 1024),
+                     umma_desc_sw128(do_base + kk * 2048, kSubAtom, 1024), id_acc, acc);
+            mma_bf16(tmem + C_DK, umma_desc_sw128(ds_base + kk * 32, 16, 1024),
+                     umma_desc_sw128(q_base + kk * 2048, kSubAtom, 1024), id_acc, acc);
+          }
+          const int qb = n & 1;
+          mbar_wait(&dq_empty[qb], ((n >> 1) & 1) ^ 1);  // dQ^T of sub-block n-2 has left this buffer
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < BKV / 16; ++kk)  // reduction over the 128 keys
+            mma_bf16(tmem + C_DQ + qb * SUBQ, umma_desc_sw128(k_base + kk * 2048, kAtom, 1024),
+                     umma_desc_sw128(ds_base + kk * 2048, kPT, 1024), id_dq, kk > 0);
+          // one commit publishes dQ^T(n) and frees sub-block n's Q / dO stage
+          // (S^T / dP^T(n), the other thread's readers, completed before p_full(n))
+          mma_commit(&q_empty[st]);
+          mma_commit(p_empty);
         }
-        const int qb = n & 1;
-        mbar_wait(&dq_empty[qb], ((n >> 1) & 1) ^ 1);  // dQ^T of sub-block n-2 has left this buffer
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk)  // reduction over the 128 keys
-          mma_bf16(tmem + C_DQ + qb * SUBQ, umma_desc_sw128(k_base + kk * 2048, kAtom, 1024),
-                   umma_desc_sw128(ds_base + kk * 2048, kPT, 1024), id_dq, kk > 0);
-        mma_commit(&dq_full[qb]);
-        mma_commit(&q_empty[st]);
-        mma_commit(p_empty);
+        mma_commit(acc_full);
       }
-      mma_commit(acc_full);
     }
   } else if (warp >= 4) {
     // two warpgroups on the same TMEM lanes: warpgroup wg owns queries
@@ -448,7 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // reduce-add of the 64 x 128 fp32 tile
     auto dq_out = [&](int qblk, int nn) {
       const int qb = nn & 1;
-      mbar_wait(&dq_full[qb], (nn >> 1) & 1);
+      mbar_wait(&q_empty[qb], (nn >> 1) & 1);  // sub-block nn's gradient MMAs (dQ^T included) retired
       tc_fence_after();
       uint32_t q[32];
       tmem_ld_32x32b_x32(tmem + lane_addr + C_DQ + qb * SUBQ + wg * 32, q);
