@@ -376,7 +376,10 @@ static EncodeFn encode_fn() {
 // dV / dK MMAs for the previous item's accumulators to have been drained.
 // ---------------------------------------------------------------------------
 constexpr uint32_t kDqStage = BQ * DH * 4;  // 32 KB: dQ tile (fp32) staged for the TMA reduce-add
-constexpr size_t kSmemBwd = 1024 + 2 * kTileBytes /*K,V*/ + 4 * kTileBytes /*Q,dO x2*/ + 2 * kPBytes /*dS^T x2*/ +
+// no alignment slack: the dynamic shared-memory base of a kernel without static
+// shared memory is 1024-B aligned on sm_100 (tools/probes/smem_base_probe.cu;
+// the kernel traps if not), and K / V x2 + Q / dO x2 + dS^T x2 fill 227 KB
+constexpr size_t kSmemBwd = 4 * kTileBytes /*K,V x2*/ + 4 * kTileBytes /*Q,dO x2*/ + 2 * kPBytes /*dS^T x2*/ +
                             kDqStage +
                             2 * 2 * BQ * 4 /*lse,D x2*/ + 512;
 
@@ -386,24 +389,25 @@ __device__ __forceinline__ int bwd_item(int r, int c, int G) { return r * G + ((
 template <bool CAUSAL>
 __global__ void __launch_bounds__(kThreads2, 1)
     bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-               const __grid_constant__ CUtensorMap tm_dq,
+               const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ CUtensorMap tm_dkv,
                const float *__restrict__ lse, const float *__restrict__ dvec, float *__restrict__ dq_acc,
                __nv_bfloat16 *__restrict__ dqkv, int S, int H, int BH, float scale_log2, float scale,
                unsigned long long *trace) {
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned base by pointer arithmetic on the __shared__ array, so the
   // compiler keeps the shared address space (STS / LDS, not generic ST / LD)
-  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t *sK = smem;
-  uint8_t *sV = sK + kTileBytes;
-  uint8_t *sQ = sV + kTileBytes;          // [2] stages
+  if (smem_u32(smem_raw) & 1023u) __trap();  // kSmemBwd has no alignment slack (see there)
+  uint8_t *smem = smem_raw;
+  uint8_t *sK = smem;                     // [2] items
+  uint8_t *sV = sK + 2 * kTileBytes;      // [2] items
+  uint8_t *sQ = sV + 2 * kTileBytes;      // [2] stages
   uint8_t *sdO = sQ + 2 * kTileBytes;     // [2] stages
   uint8_t *sdS = sdO + 2 * kTileBytes;    // dS^T [2 blocks][128 keys x 128 queries] (P^T lives in TMEM)
   uint8_t *sDQ = sdS + 2 * kPBytes;       // dQ stage: 2 x [128 rows x 32 fp32] SW128 chunks
   float *sL = reinterpret_cast<float *>(sDQ + kDqStage);  // [2][128] lse
   float *sD = sL + 2 * BQ;                               // [2][128] D
   uint64_t *bar = reinterpret_cast<uint64_t *>(sD + 2 * BQ);
-  uint64_t *kv_full = bar, *kv_empty = bar + 1;
+  uint64_t *kv_full = bar + 14, *kv_empty = bar + 16;  // [item parity]: K / V double-buffered across items
   // q_empty[b]: block n's gradient MMAs retired (n & 1 == b) -- frees its Q / dO
   // stage and dS^T buffer and publishes dQ(n)
   uint64_t *q_full = bar + 2, *q_empty = bar + 4;
@@ -411,7 +415,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
   uint64_t *p_full = bar + 8, *pt_free = bar + 9;  // P^T (TMEM) + dS^T (smem) written / P^T read by dV
   uint64_t *dq_empty = bar + 11;
   uint64_t *acc_full = bar + 12, *acc_empty = bar + 13;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 16);
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bar + 18);
 
   const int nq = S / BQ, nkb = S / BKV, n_items = nkb * BH;
   const int G = gridDim.x, c = blockIdx.x;
@@ -441,8 +445,11 @@ __global__ void __launch_bounds__(kThreads2, 1)
     tma_prefetch(&tm_qkv);
     tma_prefetch(&tm_do);
     tma_prefetch(&tm_dq);
-    mbar_init(kv_full, 1);
-    mbar_init(kv_empty, 1);
+    tma_prefetch(&tm_dkv);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+    }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&q_full[i], 1);
       mbar_init(&q_empty[i], 1);
@@ -469,10 +476,14 @@ __global__ void __launch_bounds__(kThreads2, 1)
         int kb, b, h;
         decode(i, kb, b, h);
         const int row0 = b * S;
-        mbar_wait(kv_empty, (r & 1) ^ 1);  // every MMA of the previous item has read K / V
-        mbar_expect_tx(kv_full, 2 * kTileBytes);
-        tma_load_2d(sK, &tm_qkv, kv_full, d + h * DH, row0 + kb * BKV);
-        tma_load_2d(sV, &tm_qkv, kv_full, 2 * d + h * DH, row0 + kb * BKV);
+        // K / V of item r in buffer r & 1: loaded while item r - 1 still runs,
+        // so the next item's first S^T / dP^T and elementwise pass overlap the
+        // current item's last gradient MMAs
+        const int ks = r & 1;
+        mbar_wait(&kv_empty[ks], ((r >> 1) & 1) ^ 1);  // every MMA of item r - 2 has read this buffer
+        mbar_expect_tx(&kv_full[ks], 2 * kTileBytes);
+        tma_load_2d(sK + ks * kTileBytes, &tm_qkv, &kv_full[ks], d + h * DH, row0 + kb * BKV);
+        tma_load_2d(sV + ks * kTileBytes, &tm_qkv, &kv_full[ks], 2 * d + h * DH, row0 + kb * BKV);
         for (int qi = CAUSAL ? kb : 0; qi < nq; ++qi, ++n) {
           const int st = n & 1;
           mbar_wait(&q_empty[st], ((n >> 1) & 1) ^ 1);
@@ -493,7 +504,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
       constexpr uint32_t id_kk = idesc_bf16_f32(128, 128, 0, 0);   // S^T, dP^T: K-major x K-major
       constexpr uint32_t id_kmn = idesc_bf16_f32(128, DH, 0, 1);   // dV, dK: A K-major, B MN-major
       constexpr uint32_t id_mnmn = idesc_bf16_f32(128, DH, 1, 1);  // dQ: A MN-major (dS), B MN-major (K)
-      const uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV);
+      uint32_t k_base = smem_u32(sK), v_base = smem_u32(sV);  // this item's K / V buffer
       const uint32_t ds_buf0 = smem_u32(sdS);
       // S^T = K Q^T and dP^T = V dO^T of running block n (TMEM C_ST / C_DP)
       auto issue_st = [&](int n) {
@@ -518,7 +529,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
           int kb, b, h;
           decode(i, kb, b, h);
           const int count = nq - (CAUSAL ? kb : 0);
-          mbar_wait(kv_full, r & 1);
+          mbar_wait(&kv_full[r & 1], (r >> 1) & 1);
+          k_base = smem_u32(sK + (r & 1) * kTileBytes);
+          v_base = smem_u32(sV + (r & 1) * kTileBytes);
           // block n+1's S^T / dP^T go in as soon as the softmax warps have read
           // block n's (st_empty, inside issue_st), while block n's gradient MMAs
           // are still queued from the other thread
@@ -529,7 +542,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
           int kb, b, h;
           decode(i, kb, b, h);
           const int count = nq - (CAUSAL ? kb : 0);
-          mbar_wait(kv_full, r & 1);  // dQ reads K
+          mbar_wait(&kv_full[r & 1], (r >> 1) & 1);  // dQ reads K
+          k_base = smem_u32(sK + (r & 1) * kTileBytes);
           for (int blk = 0; blk < count; ++blk, ++n) {
             const int st = n & 1;
             const uint32_t ph = n & 1;
@@ -541,11 +555,11 @@ __global__ void __launch_bounds__(kThreads2, 1)
             // and dQ-stage traffic: ~2300 of the ~3800 cycles per block, and the
             // trace shows the MMAs at ~120 cycles each (profiles/r02_attn_bwd_trace_pt_tmem.log).
             const uint32_t q_base = smem_u32(sQ + st * kTileBytes), do_base = smem_u32(sdO + st * kTileBytes);
+            const uint32_t ds_base = ds_buf0 + (n & 1) * kPBytes;
             mbar_wait(p_full, ph);
             mark(1, n);
             if (blk == 0) mbar_wait(acc_empty, (r & 1) ^ 1);  // the previous item's dV / dK drained
             tc_fence_after();
-            const uint32_t ds_base = ds_buf0 + (n & 1) * kPBytes;
 #pragma unroll
             for (int kk = 0; kk < BQ / 16; ++kk)  // dV += P^T dO, P^T from TMEM (16 queries = 8 columns)
               mma_bf16_ts(tmem + C_DV, tmem + C_PT + kk * 8, umma_desc_sw128(do_base + kk * 2048, BQ * 128, 1024),
@@ -572,7 +586,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
             mark(2, n);
           }
           mma_commit(acc_full);
-          mma_commit(kv_empty);
+          mma_commit(&kv_empty[r & 1]);
         }
       }
     }
@@ -624,6 +638,49 @@ __global__ void __launch_bounds__(kThreads2, 1)
     const uint32_t pt_addr = tmem + lane_addr + C_PT + hq * 32;  // this warpgroup's P^T columns
     int n = 0;
     int prev_qrow = 0, prev_h = 0;  // the block whose dQ is drained next
+    int pend_r = -1, pend_row = 0, pend_h = 0;  // the item whose dV / dK are still in TMEM
+    // dV (warpgroup 0) or dK (warpgroup 1) of item pend_r: TMEM -> registers,
+    // release the accumulators, then bf16 rows to global
+    auto drain_acc = [&]() {
+      if (pend_r < 0) return;
+      mbar_wait(acc_full, pend_r & 1);
+      tc_fence_after();
+      uint32_t acc[DH];
+#pragma unroll
+      for (int c0 = 0; c0 < DH; c0 += 32)
+        tmem_ld_32x32b_x32(tmem + lane_addr + (wg == 0 ? C_DV : C_DK) + c0,
+                           *reinterpret_cast<uint32_t(*)[32]>(acc + c0));
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(acc_empty);  // the next item's first dV / dK MMAs may overwrite
+      // this warpgroup's 128 x 64 bf16 tile, staged in SW128 rows in its half of
+      // the dQ stage, leaves as one TMA store: dqkv rows are 3d apart, and 16-B
+      // stores from every thread cost ~3000 cycles of LSU time per item
+      if (wg == 0 && rr == 0) bulk_wait_read0();  // the last dQ reduce-add has read the stage
+      asm volatile("bar.sync 2, 256;" ::: "memory");
+      uint8_t *trow = sDQ + wg * (BQ * 128) + rr * 128;
+      const float osc = wg == 0 ? 1.f : scale;
+#pragma unroll
+      for (int j = 0; j < DH / 8; ++j) {
+        uint4 w;
+        uint32_t *pw = reinterpret_cast<uint32_t *>(&w);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          __nv_bfloat162 a2 = __floats2bfloat162_rn(__uint_as_float(acc[8 * j + 2 * e]) * osc,
+                                                    __uint_as_float(acc[8 * j + 2 * e + 1]) * osc);
+          pw[e] = *reinterpret_cast<uint32_t *>(&a2);
+        }
+        *reinterpret_cast<uint4 *>(trow + ((j ^ (rr & 7)) << 4)) = w;
+      }
+      fence_async_smem();
+      asm volatile("bar.sync 2, 256;" ::: "memory");
+      if (wg == 0 && rr == 0) {
+        tma_store_2d(&tm_dkv, sDQ, 2 * d + pend_h * DH, pend_row);         // dV
+        tma_store_2d(&tm_dkv, sDQ + BQ * 128, d + pend_h * DH, pend_row);  // dK
+        bulk_commit();
+      }
+      pend_r = -1;
+    };
     for (int r = 0, it; (it = bwd_item(r, c, G)) < n_items; ++r) {
       int kb, b, h;
       decode(it, kb, b, h);
@@ -702,6 +759,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
         tc_fence_before();
         mbar_arrive(p_full);
         if (rr == 0) mark(wg == 0 ? 5 : 7, n);
+        drain_acc();  // the previous item's dV / dK (first block of an item only)
         // the previous block's dQ: drained while this block's gradient MMAs run
         // (dQ(n) cannot start before this drain releases the TMEM columns)
         if (n > 0) dq_out(prev_qrow, prev_h, n - 1);
@@ -709,33 +767,14 @@ __global__ void __launch_bounds__(kThreads2, 1)
         prev_qrow = row0 + i * BQ;
         prev_h = h;
       }
-      // dV (warpgroup 0) or dK (warpgroup 1) of this key block
-      mbar_wait(acc_full, r & 1);
-      tc_fence_after();
-      uint32_t acc[DH];
-#pragma unroll
-      for (int c0 = 0; c0 < DH; c0 += 32)
-        tmem_ld_32x32b_x32(tmem + lane_addr + (wg == 0 ? C_DV : C_DK) + c0,
-                           *reinterpret_cast<uint32_t(*)[32]>(acc + c0));
-      tmem_ld_wait();
-      tc_fence_before();
-      mbar_arrive(acc_empty);  // the next item's first dV / dK MMAs may overwrite
-      const int64_t ld = 3 * (int64_t)d;
-      __nv_bfloat16 *orow = dqkv + (int64_t)(row0 + kb * BKV + rr) * ld + (wg == 0 ? 2 * d : d) + h * DH;
-      const float osc = wg == 0 ? 1.f : scale;
-#pragma unroll
-      for (int cc = 0; cc < DH; cc += 8) {
-        uint4 w;
-        uint32_t *pw = reinterpret_cast<uint32_t *>(&w);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          __nv_bfloat162 a2 = __floats2bfloat162_rn(__uint_as_float(acc[cc + 2 * e]) * osc,
-                                                    __uint_as_float(acc[cc + 2 * e + 1]) * osc);
-          pw[e] = *reinterpret_cast<uint32_t *>(&a2);
-        }
-        *reinterpret_cast<uint4 *>(orow + cc) = w;
-      }
+      // this item's dV / dK are drained after the next item's first block has
+      // been handed to the MMAs (below), so that block's elementwise pass
+      // overlaps this item's last gradient MMAs
+      pend_r = r;
+      pend_row = row0 + kb * BKV;
+      pend_h = h;
     }
+    drain_acc();
     if (n > 0) dq_out(prev_qrow, prev_h, n - 1);
     if (wg == 0 && rr == 0) bulk_wait0();
   }
@@ -766,6 +805,8 @@ int backward_main(const void *qkv, const void *dout, const float *lse, const flo
   CUtensorMap tq, td;
   HM_TRY(make_map(&tq, qkv, 3 * (int64_t)d, (int64_t)B * S, 3 * (int64_t)d * 2));
   HM_TRY(make_map(&td, dout, d, (int64_t)B * S, (int64_t)d * 2));
+  CUtensorMap tdkv;  // dqkv [B*S, 3d] bf16, {64, 128} boxes: dK / dV tiles leave by TMA store
+  HM_TRY(make_map(&tdkv, dqkv, 3 * (int64_t)d, (int64_t)B * S, 3 * (int64_t)d * 2));
   CUtensorMap tdq;  // dq_acc [B*S, d] fp32, {32, 128} boxes in SW128 (the reduce-add target)
   {
     EncodeFn fn = encode_fn();
@@ -794,7 +835,7 @@ int backward_main(const void *qkv, const void *dout, const float *lse, const flo
     HM_CUDA(cudaMalloc(&tbuf, 8 * 64 * sizeof(unsigned long long)));
     HM_CUDA(cudaMemset(tbuf, 0, 8 * 64 * sizeof(unsigned long long)));
   }
-  k<<<dim3(items < sms ? items : sms), kThreads2, kSmemBwd, s>>>(tq, td, tdq, lse, dvec, dq_acc,
+  k<<<dim3(items < sms ? items : sms), kThreads2, kSmemBwd, s>>>(tq, td, tdq, tdkv, lse, dvec, dq_acc,
                                                                  static_cast<__nv_bfloat16 *>(dqkv), S, H, B * H,
                                                                  1.4426950408889634f * scale, scale,
                                                                  tracing ? tbuf : nullptr);
