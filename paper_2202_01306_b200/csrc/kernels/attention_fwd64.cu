@@ -70,7 +70,7 @@ constexpr uint32_t kTile = BQ * DH * 2;  // 128 rows x 128 B: one SW128 atom col
 constexpr int kThreads = 384;
 constexpr float kRescaleLog2 = 8.f;      // lazy-rescale threshold (log2 units)
 constexpr uint32_t C_O = kSBuf * BKV;    // O_t at columns [384 + 64 t, 448 + 64 t)
-constexpr size_t kSmem = 1024 + 4 * kTile /*Q pair x 2 items*/ + 2 * kStages * kTile /*K, V*/ + 256;
+constexpr size_t kSmem = 1024 + 4 * kTile /*Q pair x 2 items*/ + 2 * kStages * kTile /*K, V*/ + 2 * kTile /*O staging*/ + 256;
 static_assert(C_O + 2 * DH == 512, "TMEM budget");
 
 __device__ __forceinline__ float ex2(float x) {
@@ -123,6 +123,8 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   return make_float2(__uint_as_float(__float_as_uint(q.x) + (__float_as_uint(y.x) << 23)),
                      __uint_as_float(__float_as_uint(q.y) + (__float_as_uint(y.y) << 23)));
 }
+// generic-proxy shared-memory writes -> visible to the TMA (async proxy)
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void reg_alloc() {
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
@@ -192,7 +194,7 @@ __device__ __forceinline__ Item make_item(int r, int c, int G, int S, int H, int
 
 template <bool CAUSAL, int EMU>
 __global__ void __launch_bounds__(kThreads, 1)
-    fwd_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16 *__restrict__ out, float *__restrict__ lse,
+    fwd_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo, float *__restrict__ lse,
                int S, int H, int BH, float scale_log2, unsigned long long *trace) {
   extern __shared__ uint8_t smem_raw[];
   // diagnostics (HM_ATTN_TRACE=1), 512 words per CTA: globaltimer at [0] entry,
@@ -207,7 +209,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t *sQ = smem;                  // [2 items][2 tiles]
   uint8_t *sK = sQ + 4 * kTile;        // [kStages]
   uint8_t *sV = sK + kStages * kTile;  // [kStages]
-  uint64_t *bar = reinterpret_cast<uint64_t *>(sV + kStages * kTile);
+  uint8_t *sO = sV + kStages * kTile;  // [tile]: the item's O, SW128 rows, for one TMA store
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sO + 2 * kTile);
   uint64_t *q_full = bar, *q_empty = bar + 2;                   // [item parity]
   uint64_t *kv_full = bar + 4, *kv_empty = kv_full + kStages;  // [stage]
   uint64_t *s_full = kv_empty + kStages;                       // [S buffer]
@@ -475,7 +478,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       ++done;
       tc_fence_after();
       const float inv = 1.f / l;
-      __nv_bfloat16 *orow = out + (int64_t)(row0 + qb * BQ + r) * d + it.h * DH;
+      // O leaves as one TMA store per tile from SW128 staging (query rows are d
+      // apart in `out`: 16-B stores from every thread throttle the LSU)
+      const bool leader = q4 == 0 && lane == 0;
+      if (leader) bulk_wait_read0();  // this tile's previous store has read the staging
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + t) : "memory");
+      uint8_t *srow = sO + t * kTile + r * 128;
 #pragma unroll
       for (int c0 = 0; c0 < DH; c0 += 32) {
         uint32_t ov[32];
@@ -488,13 +496,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           w.y = bf16x2(__uint_as_float(ov[cc + 2]) * inv, __uint_as_float(ov[cc + 3]) * inv);
           w.z = bf16x2(__uint_as_float(ov[cc + 4]) * inv, __uint_as_float(ov[cc + 5]) * inv);
           w.w = bf16x2(__uint_as_float(ov[cc + 6]) * inv, __uint_as_float(ov[cc + 7]) * inv);
-          *reinterpret_cast<uint4 *>(orow + c0 + cc) = w;
+          *reinterpret_cast<uint4 *>(srow + ((((c0 + cc) >> 3) ^ (r & 7)) << 4)) = w;
         }
+      }
+      fence_async_smem();
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + t) : "memory");
+      if (leader) {
+        tma_store_2d(&tmo, sO + t * kTile, it.h * DH, row0 + qb * BQ);
+        bulk_commit();
       }
       lse[(int64_t)(row0 + qb * BQ + r) * H + it.h] = m + log2f(l);
       if (rec && it.r < 14) tr[5 + 4 * it.r + 2 * t] = clock64();
       tc_fence_before();
     }
+    if (q4 == 0 && lane == 0) bulk_wait0();  // the last O store has left shared memory
   }
   tc_fence_before();
   __syncthreads();
@@ -543,6 +558,15 @@ int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causa
          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return fail(HM_ERR_DEVICE, "attention (head_dim 64) tensor map encode failed");
+  CUtensorMap tmo;  // out [B*S, d] bf16, {64, 128} boxes, 128-B swizzle (TMA-stored O tiles)
+  {
+    cuuint64_t odims[2] = {(cuuint64_t)d, (cuuint64_t)B * S};
+    cuuint64_t ostrides[1] = {(cuuint64_t)d * 2};
+    if (fn(&tmo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, o, odims, ostrides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return fail(HM_ERR_DEVICE, "attention (head_dim 64) output tensor map encode failed");
+  }
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
   ProfScope ps(KC_ATTN_FWD, s, 4.0 * B * (double)S * S * H * DH * (causal ? 0.5 : 1.0), (double)B * S * H * DH * 2 * 4);
   static bool attr[2] = {false, false};
@@ -563,7 +587,7 @@ int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causa
   static unsigned long long *tbuf = nullptr;
   if (tracing && !tbuf) HM_CUDA(cudaMalloc(&tbuf, 512 * 1024 * sizeof(unsigned long long)));
   if (tracing) HM_CUDA(cudaMemsetAsync(tbuf, 0, 512 * grid * sizeof(unsigned long long), s));
-  k<<<dim3(grid), kThreads, kSmem, s>>>(tm, static_cast<__nv_bfloat16 *>(o), lse, S, H, B * H, scale_log2,
+  k<<<dim3(grid), kThreads, kSmem, s>>>(tm, tmo, lse, S, H, B * H, scale_log2,
                                         tracing ? tbuf : nullptr);
   if (tracing) {  // one JSON line per launch: every CTA's timestamps, ns after the earliest entry
     std::vector<unsigned long long> h(512 * grid);

@@ -4,5 +4,4 @@ timeout 600 python -m pytest tests/test_kernels_gpu.py -q -x -k "attn or attenti
 timeout 120 python tools/attn_perf.py 4 1024 25 64 1 50 > gpurun_out/tr_perf.jsonl 2>&1
 timeout 120 python tools/attn_perf.py 16 1024 25 64 1 20 >> gpurun_out/tr_perf.jsonl 2>&1
 timeout 120 python tools/attn_perf.py 8 512 16 64 0 20 >> gpurun_out/tr_perf.jsonl 2>&1
-HM_ATTN_TRACE=1 timeout 120 python tools/attn_perf.py 4 1024 25 64 1 2 > /dev/null 2> gpurun_out/tr_fwd64.log
 echo done
