@@ -629,7 +629,10 @@ def run_native(args) -> None:
     # launches), weighted by how often the iteration launches it
     gemm_replay = []
     for shp, count in gemm_shapes:
-        us = ops.gemm_replay_us(shp, reps=32)
+        # best of three replays: right after the pipelined run a replay has read
+        # up to 45% slow on the MN-major-B shapes of one box (the same shapes
+        # replayed standalone, tools/gemm_shapes.py, did not)
+        us = min(ops.gemm_replay_us(shp, reps=32) for _ in range(3))
         gemm_replay.append({"m": shp[0], "n": shp[1], "k": shp[2], "a_mn": shp[3], "b_mn": shp[4], "epi": shp[5],
                             "count": count, "us": round(us, 2),
                             "tflops": round(2.0 * shp[0] * shp[1] * shp[2] / (us * 1e-6) / 1e12, 1)})
@@ -741,8 +744,8 @@ def run_native(args) -> None:
                              "classifier GEMM)") if is_cnn else
                             "algorithmic 2MNK per launch / the kernel's own per-launch time: each GEMM shape of one "
                             "iteration (logged while profiling it) replayed as a CUDA graph of 32 back-to-back launches "
-                            "on rotating operand sets, CUDA events around whole graph replays, weighted by the "
-                            "iteration's launch counts (gemm_replay)",
+                            "on rotating operand sets, CUDA events around whole graph replays (best of three), "
+                            "weighted by the iteration's launch counts (gemm_replay)",
                      "peak_kind": "sustained (MEASURED_PEAKS bf16_tflops_sustained)",
                      "achieved_event_pairs": round(gemm_tflops, 1),
                      "event_pairs_how": "per-launch CUDA event pairs (graph event nodes) around every kernel of one "
