@@ -56,6 +56,7 @@
 #include <vector>
 
 #include "../runtime/common.hpp"
+#include "pdl.cuh"
 #include "sm100.cuh"
 
 namespace hm {
@@ -250,6 +251,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // programmatic dependent launch: the set-up above overlapped the previous
+  // kernel's tail; nothing global is read or written before it has completed
+  griddep_wait();
   if (tr && threadIdx.x == 0) {
     tr[1] = globaltimer();
     tr[2] = clock64();
@@ -587,8 +591,8 @@ int forward(const void *qkv, void *o, float *lse, int B, int S, int H, int causa
   static unsigned long long *tbuf = nullptr;
   if (tracing && !tbuf) HM_CUDA(cudaMalloc(&tbuf, 512 * 1024 * sizeof(unsigned long long)));
   if (tracing) HM_CUDA(cudaMemsetAsync(tbuf, 0, 512 * grid * sizeof(unsigned long long), s));
-  k<<<dim3(grid), kThreads, kSmem, s>>>(tm, tmo, lse, S, H, B * H, scale_log2,
-                                        tracing ? tbuf : nullptr);
+  HM_CUDA(launch_pdl(k, dim3(grid), dim3(kThreads), kSmem, s, tm, tmo, lse, S, H, B * H, scale_log2,
+                     tracing ? tbuf : nullptr));
   if (tracing) {  // one JSON line per launch: every CTA's timestamps, ns after the earliest entry
     std::vector<unsigned long long> h(512 * grid);
     HM_CUDA(cudaStreamSynchronize(s));

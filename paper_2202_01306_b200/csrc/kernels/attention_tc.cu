@@ -25,6 +25,7 @@
 #include <type_traits>
 
 #include "../runtime/common.hpp"
+#include "pdl.cuh"
 #include "sm100.cuh"
 
 namespace hm {
@@ -468,6 +469,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // programmatic dependent launch: the set-up above overlapped the previous
+  // kernel's tail (dvec); nothing global is read or written before it completed
+  griddep_wait();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -835,10 +839,9 @@ int backward_main(const void *qkv, const void *dout, const float *lse, const flo
     HM_CUDA(cudaMalloc(&tbuf, 8 * 64 * sizeof(unsigned long long)));
     HM_CUDA(cudaMemset(tbuf, 0, 8 * 64 * sizeof(unsigned long long)));
   }
-  k<<<dim3(items < sms ? items : sms), kThreads2, kSmemBwd, s>>>(tq, td, tdq, tdkv, lse, dvec, dq_acc,
-                                                                 static_cast<__nv_bfloat16 *>(dqkv), S, H, B * H,
-                                                                 1.4426950408889634f * scale, scale,
-                                                                 tracing ? tbuf : nullptr);
+  HM_CUDA(launch_pdl(k, dim3(items < sms ? items : sms), dim3(kThreads2), kSmemBwd, s, tq, td, tdq, tdkv, lse, dvec,
+                     dq_acc, static_cast<__nv_bfloat16 *>(dqkv), S, H, B * H, 1.4426950408889634f * scale, scale,
+                     tracing ? tbuf : nullptr));
   if (tracing) {
     unsigned long long h[8 * 64];
     HM_CUDA(cudaStreamSynchronize(s));

@@ -4,4 +4,5 @@ timeout 600 python -m pytest tests/test_kernels_gpu.py -q -x -k "attn or attenti
 timeout 120 python tools/attn_perf.py 4 1024 25 64 1 50 > gpurun_out/tr_perf.jsonl 2>&1
 timeout 120 python tools/attn_perf.py 16 1024 25 64 1 20 >> gpurun_out/tr_perf.jsonl 2>&1
 timeout 120 python tools/attn_perf.py 8 512 16 64 0 20 >> gpurun_out/tr_perf.jsonl 2>&1
+timeout 900 python bench.py --workload gpt2-xl-dp-d64 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/tr_d64.json 2> gpurun_out/tr_d64.err
 echo done
