@@ -41,6 +41,7 @@
 #include <type_traits>
 
 #include "../runtime/common.hpp"
+#include "pdl.cuh"
 #include "sm100.cuh"
 
 namespace hm {
@@ -126,6 +127,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  griddep_wait();  // programmatic dependent launch: set-up above overlapped the previous kernel
 
   if (warp == 0) {
     if (lane == 0) {
@@ -360,6 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  griddep_wait();  // programmatic dependent launch: set-up above overlapped the previous kernel
 
   if (warp == 0) {
     if (lane == 0) {
@@ -618,7 +621,8 @@ static int forward_hd(const void *qkv, void *o, float *lse, int B, int S, int H,
     attr[causal ? 1 : 0] = true;
   }
   const int npair = (S / BQ + 1) / 2;
-  k<<<dim3(B * H, npair), kThreads, fwd_smem<HD>(), s>>>(tm, static_cast<__nv_bfloat16 *>(o), lse, S, H, scale_log2);
+  HM_CUDA(launch_pdl(k, dim3(B * H, npair), dim3(kThreads), fwd_smem<HD>(), s, tm, static_cast<__nv_bfloat16 *>(o), lse,
+                     S, H, scale_log2));
   count_launch();
   HM_CUDA(cudaGetLastError());
   return HM_OK;
@@ -659,8 +663,8 @@ int backward_main(const void *qkv, const void *dout, const float *lse, const flo
     attr[causal ? 1 : 0] = true;
   }
   const float scale = 1.f / sqrtf((float)DH);
-  k<<<dim3(B * H, S / BKV), kThreads, kBwdSmem, s>>>(tkv, tq, tdo, tdq, lse, dvec, static_cast<__nv_bfloat16 *>(dqkv),
-                                                     S, H, 1.4426950408889634f * scale, scale);
+  HM_CUDA(launch_pdl(k, dim3(B * H, S / BKV), dim3(kThreads), kBwdSmem, s, tkv, tq, tdo, tdq, lse, dvec,
+                     static_cast<__nv_bfloat16 *>(dqkv), S, H, 1.4426950408889634f * scale, scale));
   count_launch();
   HM_CUDA(cudaGetLastError());
   return HM_OK;
