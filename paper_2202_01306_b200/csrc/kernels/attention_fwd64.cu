@@ -43,6 +43,9 @@
 // per step and counters without divisions.  The softmax then bounds it: 128
 // ex2 + 64 bf16x2 conversions per row on the XU pipe with both tiles' warps on
 // each SMSP; one exponent pair in eight goes to the FMA pipe (ex2_poly2).
+// O leaves each tile as one TMA store from SW128 staging, and the kernel is
+// launched with programmatic dependent launch (set-up overlaps the previous
+// kernel's tail).
 //
 // Output conventions as attention.cu: o [tokens, d] bf16, lse [tokens, H]
 // in the log2 domain.
