@@ -242,31 +242,36 @@ __global__ void __launch_bounds__(THREADS) fwd_kernel(const __nv_bfloat16 *__res
 // (token, head) row of DH bf16 (DH * 2 bytes = DH / 8 16-B loads of each input,
 // all in flight); consecutive threads read consecutive rows (coalesced).
 template <int DH>
+// D = rowsum(dO * O) per (token, head), and the dQ accumulator of that (token,
+// head) zeroed in the same pass (it receives reduce-adds next).  DH / 8
+// threads per (token, head), one 16-B load of O and of dO each: a warp reads
+// 32 x 16 B contiguous (one thread per (token, head) touched a 128-B stride).
 __global__ void dvec_kernel(const __nv_bfloat16 *__restrict__ o, const __nv_bfloat16 *__restrict__ dout,
-                            float *__restrict__ dvec, int64_t rows, int H) {
+                            float *__restrict__ dvec, float *__restrict__ dq_acc, int64_t rows, int H) {
   pdl_wait();
-  const int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (w >= rows * H) return;
-  const uint4 *a = reinterpret_cast<const uint4 *>(o + w * DH);
-  const uint4 *c = reinterpret_cast<const uint4 *>(dout + w * DH);
-  uint4 va[DH / 8], vc[DH / 8];
-#pragma unroll
-  for (int k = 0; k < DH / 8; ++k) {
-    va[k] = a[k];
-    vc[k] = c[k];
-  }
+  constexpr int TPR = DH / 8;  // threads per (token, head)
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t w = t / TPR;
+  const int part = (int)(t % TPR);
+  const bool live = w < rows * H;
   float acc = 0.f;
-#pragma unroll
-  for (int k = 0; k < DH / 8; ++k) {
-    const __nv_bfloat162 *x = reinterpret_cast<const __nv_bfloat162 *>(&va[k]);
-    const __nv_bfloat162 *y = reinterpret_cast<const __nv_bfloat162 *>(&vc[k]);
+  if (live) {
+    const uint4 va = reinterpret_cast<const uint4 *>(o + w * DH)[part];
+    const uint4 vc = reinterpret_cast<const uint4 *>(dout + w * DH)[part];
+    const __nv_bfloat162 *x = reinterpret_cast<const __nv_bfloat162 *>(&va);
+    const __nv_bfloat162 *y = reinterpret_cast<const __nv_bfloat162 *>(&vc);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const float2 fx = __bfloat1622float2(x[j]), fy = __bfloat1622float2(y[j]);
       acc = fmaf(fx.x, fy.x, fmaf(fx.y, fy.y, acc));
     }
+    float4 *z = reinterpret_cast<float4 *>(dq_acc + w * DH) + 2 * part;
+    z[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    z[1] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  dvec[w] = acc;
+#pragma unroll
+  for (int m = TPR / 2; m > 0; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+  if (live && part == 0) dvec[w] = acc;
 }
 
 template <int DH, bool CAUSAL>
@@ -495,9 +500,9 @@ static int bwd_launch(const __nv_bfloat16 *qkv, const __nv_bfloat16 *o, const __
   const int64_t rows = (int64_t)B * S;
   const int d = H * DH;
   ProfScope ps(KC_ATTN_BWD, s, 10.0 * B * (double)S * S * H * DH * (CAUSAL ? 0.5 : 1.0), (double)rows * d * 2 * 8);
-  HM_CUDA(cudaMemsetAsync(dq_acc, 0, rows * d * sizeof(float), s));
-  const int64_t warps = rows * H;
-  HM_CUDA(launch_pdl(dvec_kernel<DH>, dim3((unsigned)((warps + 127) / 128)), dim3(128), 0, s, o, dout, dvec, rows, H));
+  const int64_t threads = rows * H * (DH / 8);
+  HM_CUDA(launch_pdl(dvec_kernel<DH>, dim3((unsigned)((threads + 255) / 256)), dim3(256), 0, s, o, dout, dvec, dq_acc,
+                     rows, H));
   const float scale = 1.f / sqrtf((float)DH);
   // The tcgen05 backward (attention_tc.cu: TMEM accumulators, dQ as one TMA
   // reduce-add per query block) is the default where it applies (head_dim 64,
