@@ -155,4 +155,9 @@ def test_wide_head_dim_128_per_layer_deltas(math):
     spec = GPTSpec(2, 8192, 64, 256, 1024, causal=True, name="wide-2l")
     packs = ((0, 0), (1, 1))
     cfg = H.Configuration(1, packs, 1, packs, 2, H.Mode.PP)
-    check(run_parity(spec, cfg, 3, math, alpha=60 << 30, lr=1e-5), FP32_TOL if math == "fp32" else BF16_TOL)
+    # bf16 operands at this shape: the loss falls from 8.6 to 1.3 in three steps
+    # and two fp32 summation orders of the same bf16 products in the attention
+    # backward's D pre-pass measured 5.6e-4 and 1.04e-3 on it, so the bf16 mode's
+    # loss bound here is 2e-3 (the fp32-operand mode keeps 1e-3 and measures 1e-6)
+    tol = FP32_TOL if math == "fp32" else dict(BF16_TOL, loss=2e-3)
+    check(run_parity(spec, cfg, 3, math, alpha=60 << 30, lr=1e-5), tol)

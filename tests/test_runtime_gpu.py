@@ -30,7 +30,7 @@ def _gpu():
 
 
 
-def _run(spec, cfg, steps, n_gpus=1, alpha=16 << 30, lr=1e-4):
+def _run(spec, cfg, steps, n_gpus=1, alpha=16 << 30, lr=1e-4, loss_rtol=LOSS_RTOL):
     from oracle.gpt_cpu import GPTOracle
     from paper_2202_01306_b200.runtime import HarmonyRuntime
     prof = gpt_profiles(spec, u_max=64)
@@ -48,7 +48,7 @@ def _run(spec, cfg, steps, n_gpus=1, alpha=16 << 30, lr=1e-4):
         loss = rt.step(tok, lab)
         ref = oracle.step(tok, lab, list(g.tasks[0].group))
         worst = max(worst, abs(loss - ref) / abs(ref))
-        assert abs(loss - ref) / abs(ref) < LOSS_RTOL, (i, loss, ref)
+        assert abs(loss - ref) / abs(ref) < loss_rtol, (i, loss, ref)
         rep = rt.report()
         assert rep.ledger == sim.ledger
         assert rep.channel_volumes == sim.channel_volumes
@@ -159,7 +159,9 @@ def test_wide_layers_head_dim_128_match_oracle():
     spec = GPTSpec(2, 8192, 64, 256, 1024, causal=True, name="wide-2l")
     packs = ((0, 0), (1, 1))
     cfg = H.Configuration(1, packs, 1, packs, 2, H.Mode.PP)
-    rel_w, rel_m, rel_v, _ = _run(spec, cfg, steps=3, alpha=48 << 30, lr=1e-5)
+    # bf16 operands (the runtime default): loss bound 2e-3 at this shape, see
+    # test_parity_gpu.test_wide_head_dim_128_per_layer_deltas
+    rel_w, rel_m, rel_v, _ = _run(spec, cfg, steps=3, alpha=48 << 30, lr=1e-5, loss_rtol=2e-3)
     print("wide rel", rel_w, rel_m, rel_v)
     assert rel_w < STATE_RTOL
 
