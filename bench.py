@@ -241,6 +241,28 @@ def _host_precheck(spec, world: int, mode: str, stash_bytes: int, dp_update: str
     return None
 
 
+def phase_bound_s(graph, ledger, pcie: dict, rank: int = 0) -> float:
+    """Phase-serialised link bound (seconds) of one iteration on `rank`: the
+    forward packs' transfers (W in, stash out) and the backward + update packs'
+    (W / stash / K in, W / K out) run in two windows -- the next iteration's
+    forward waits on this one's updates -- so each window is bounded by its own
+    direction mix: max(H2D / h2d, D2H / d2h, (H2D + D2H) / bidir), summed."""
+    from paper_2202_01306_b200 import TaskType
+    total = 0.0
+    for is_f in (True, False):
+        ph_in = ph_out = 0
+        for r in ledger:
+            if r[4] in ("cpu_gpu_swap", "message_passing") and r[7] == rank and \
+                    (graph.tasks[r[0]].type is TaskType.F) == is_f:
+                if r[1] == 0:
+                    ph_in += r[6]
+                elif r[1] == 2:
+                    ph_out += r[6]
+        total += max(ph_in / (pcie["h2d"] * 1e9), ph_out / (pcie["d2h"] * 1e9),
+                     (ph_in + ph_out) / (pcie["bidir"] * 1e9))
+    return total
+
+
 def _pcie_gbs(reps: int = 3):
     """Measured pinned GB/s of this GPU's link (1 GiB copies): H2D alone, D2H
     alone, and both directions at once on two streams ("bidir", the sum;
@@ -676,22 +698,7 @@ def run_native(args) -> None:
     busbw = _nccl_busbw(world)
     t_nccl = cnt["nccl_bytes"] / (busbw * 1e9) if world > 1 and busbw else 0.0
     p2p = sum(r[6] for r in sim.ledger if r[4] == "peer2peer")
-    # phase-serialised link bound: the forward packs' transfers (W in, stash
-    # out) and the backward + update packs' (W / stash / K in, W / K out) run
-    # in two windows -- the next iteration's forward waits on this one's
-    # updates -- so each window is bounded by its own direction mix
-    t_phase = 0.0
-    for is_f in (True, False):
-        ph_in = ph_out = 0
-        for r in sim.ledger:
-            if r[4] in ("cpu_gpu_swap", "message_passing") and r[7] == rank and \
-                    (graph.tasks[r[0]].type is H.TaskType.F) == is_f:
-                if r[1] == 0:
-                    ph_in += r[6]
-                elif r[1] == 2:
-                    ph_out += r[6]
-        t_phase += max(ph_in / (pcie["h2d"] * 1e9), ph_out / (pcie["d2h"] * 1e9),
-                       (ph_in + ph_out) / (pcie["bidir"] * 1e9))
+    t_phase = phase_bound_s(graph, sim.ledger, pcie, rank)
     t_phase = _max_over_ranks(t_phase, world)
     t_roof = max(t_compute, _max_over_ranks(max(t_h2d, t_d2h, t_bidir), world), t_root, t_nccl)
     ms_step = 1000.0 * t_total / args.steps
