@@ -80,7 +80,7 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 // ---------------------------------------------------------------------------
 template <int HD, bool CAUSAL>
 __global__ void __launch_bounds__(kThreads, 1)
-    fwd_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16 *__restrict__ out, float *__restrict__ lse,
+    fwd_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo, float *__restrict__ lse,
                int S, int H, float scale_log2) {
   extern __shared__ uint8_t smem_raw[];
   constexpr uint32_t TILE = HD * 256;  // 128 rows x HD head dims bf16 (HD / 64 SW128 atoms)
@@ -271,7 +271,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&o_full[t], (nkv - 1) & 1);
       tc_fence_after();
       const float inv = 1.f / l;
-      __nv_bfloat16 *orow = out + (int64_t)(row0 + qb * BQ + r) * d + h * DH;
+      // O leaves as TMA stores (one per 64 head dims) from this tile's Q
+      // buffer, free once its last PV has completed (every S MMA of the tile
+      // was issued before it): rows are d apart in `out`, and 16-B stores from
+      // every thread throttle the LSU
+      uint8_t *srow = sQ + t * TILE + r * 128;
 #pragma unroll
       for (int c0 = 0; c0 < DH; c0 += 32) {
         uint32_t ov[32];
@@ -287,8 +291,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                       __uint_as_float(ov[c + 2 * e + 1]) * inv);
             wp[e] = *reinterpret_cast<uint32_t *>(&tb);
           }
-          *reinterpret_cast<uint4 *>(orow + c0 + c) = w;
+          const int col = c0 + c;
+          *reinterpret_cast<uint4 *>(srow + (col >> 6) * kAtom + ((((col & 63) >> 3) ^ (r & 7)) << 4)) = w;
         }
+      }
+      fence_async_smem();
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + t) : "memory");
+      if (q4 == 0 && lane == 0) {
+#pragma unroll
+        for (int a = 0; a < DH / 64; ++a) tma_store_2d(&tmo, sQ + t * TILE + a * kAtom, h * DH + 64 * a, row0 + qb * BQ);
+        bulk_commit();
+        bulk_wait0();  // shared memory is released when the CTA exits
       }
       lse[(int64_t)(row0 + qb * BQ + r) * H + h] = m + log2f(l);
     }
@@ -612,6 +625,8 @@ static int forward_hd(const void *qkv, void *o, float *lse, int B, int S, int H,
   const int d = H * HD;
   CUtensorMap tm;
   HM_TRY(make_map(&tm, qkv, 3 * (int64_t)d, (int64_t)B * S, 3 * (int64_t)d * 2, 128));
+  CUtensorMap tmo;  // out [B*S, d] bf16, {64, 128} SW128 boxes (TMA-stored O)
+  HM_TRY(make_map(&tmo, o, d, (int64_t)B * S, (int64_t)d * 2, 128));
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)HD);
   ProfScope ps(KC_ATTN_FWD, s, 4.0 * B * (double)S * S * H * HD * (causal ? 0.5 : 1.0), (double)B * S * H * HD * 2 * 4);
   static bool attr[2] = {false, false};
@@ -621,8 +636,7 @@ static int forward_hd(const void *qkv, void *o, float *lse, int B, int S, int H,
     attr[causal ? 1 : 0] = true;
   }
   const int npair = (S / BQ + 1) / 2;
-  HM_CUDA(launch_pdl(k, dim3(B * H, npair), dim3(kThreads), fwd_smem<HD>(), s, tm, static_cast<__nv_bfloat16 *>(o), lse,
-                     S, H, scale_log2));
+  HM_CUDA(launch_pdl(k, dim3(B * H, npair), dim3(kThreads), fwd_smem<HD>(), s, tm, tmo, lse, S, H, scale_log2));
   count_launch();
   HM_CUDA(cudaGetLastError());
   return HM_OK;
