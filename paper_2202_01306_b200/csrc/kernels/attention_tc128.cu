@@ -321,8 +321,8 @@ template <bool CAUSAL>
 __global__ void __launch_bounds__(kThreads, 1)
     bwd_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
                const __grid_constant__ CUtensorMap tm_do, const __grid_constant__ CUtensorMap tm_dq,
-               const float *__restrict__ lse, const float *__restrict__ dvec, __nv_bfloat16 *__restrict__ dqkv, int S,
-               int H, float scale_log2, float scale) {
+               const __grid_constant__ CUtensorMap tm_dkv, const float *__restrict__ lse,
+               const float *__restrict__ dvec, int S, int H, float scale_log2, float scale) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *sK = smem;
@@ -551,10 +551,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (wg == 0 && r == 0) bulk_wait0();
     mbar_wait(acc_full, 0);
     tc_fence_after();
-    const int64_t ld = 3 * (int64_t)d;
-    __nv_bfloat16 *orow = dqkv + (int64_t)(row0 + kb * BKV + r) * ld + (wg == 0 ? 2 * d : d) + h * DH;
+    // dV (warpgroup 0) / dK (warpgroup 1) staged in SW128 atoms in the (spent)
+    // V / K buffers and stored by TMA: rows are 3d apart in dqkv, and 16-B
+    // stores from every thread throttle the LSU at the end of every CTA
     const float osc = wg == 0 ? 1.f : scale;
     const uint32_t acc_addr = tmem + lane_addr + (wg == 0 ? C_DV : C_DK);
+    uint8_t *stage = wg == 0 ? sV : sK;
+    uint8_t *srow = stage + r * 128;
 #pragma unroll
     for (int c0 = 0; c0 < DH; c0 += 32) {
       uint32_t acc[32];
@@ -570,8 +573,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                    __uint_as_float(acc[c + 2 * e + 1]) * osc);
           pw[e] = *reinterpret_cast<uint32_t *>(&a);
         }
-        *reinterpret_cast<uint4 *>(orow + c0 + c) = w;
+        const int col = c0 + c;
+        *reinterpret_cast<uint4 *>(srow + (col >> 6) * kAtom + ((((col & 63) >> 3) ^ (r & 7)) << 4)) = w;
       }
+    }
+    fence_async_smem();
+    asm volatile("bar.sync %0, 128;" ::"r"(3 + wg) : "memory");
+    if (r == 0) {
+#pragma unroll
+      for (int a = 0; a < DH / 64; ++a)
+        tma_store_2d(&tm_dkv, stage + a * kAtom, (wg == 0 ? 2 * d : d) + h * DH + 64 * a, row0 + kb * BKV);
+      bulk_commit();
+      bulk_wait0();  // shared memory is released when the CTA exits
     }
   }
   tc_fence_before();
@@ -659,6 +672,8 @@ int backward_main(const void *qkv, const void *dout, const float *lse, const flo
   HM_TRY(make_map(&tkv, qkv, 3 * (int64_t)d, (int64_t)B * S, 3 * (int64_t)d * 2, BKV));
   HM_TRY(make_map(&tq, qkv, 3 * (int64_t)d, (int64_t)B * S, 3 * (int64_t)d * 2, SUBQ));
   HM_TRY(make_map(&tdo, dout, d, (int64_t)B * S, (int64_t)d * 2, SUBQ));
+  CUtensorMap tdkv;  // dqkv [B*S, 3d] bf16, {64, 128} SW128 boxes: TMA-stored dK / dV
+  HM_TRY(make_map(&tdkv, dqkv, 3 * (int64_t)d, (int64_t)B * S, 3 * (int64_t)d * 2, BKV));
   {  // dq_acc [B*S, d] fp32, {128, 64} boxes, no swizzle (row-major smem stage)
     EncodeFn fn = encode_fn();
     cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)B * S};
@@ -677,8 +692,8 @@ int backward_main(const void *qkv, const void *dout, const float *lse, const flo
     attr[causal ? 1 : 0] = true;
   }
   const float scale = 1.f / sqrtf((float)DH);
-  HM_CUDA(launch_pdl(k, dim3(B * H, S / BKV), dim3(kThreads), kBwdSmem, s, tkv, tq, tdo, tdq, lse, dvec,
-                     static_cast<__nv_bfloat16 *>(dqkv), S, H, 1.4426950408889634f * scale, scale));
+  HM_CUDA(launch_pdl(k, dim3(B * H, S / BKV), dim3(kThreads), kBwdSmem, s, tkv, tq, tdo, tdq, tdkv, lse, dvec, S, H,
+                     1.4426950408889634f * scale, scale));
   count_launch();
   HM_CUDA(cudaGetLastError());
   return HM_OK;
